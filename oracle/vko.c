@@ -1,0 +1,818 @@
+/*
+ * vko.c — CPU ORACLE drivers.  TEST INFRASTRUCTURE ONLY (see vko.h): only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load it.  It shares no code with the CUDA path.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off (no fast-math, no FTZ) -shared.
+ */
+#define _GNU_SOURCE
+#include "vko.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+/* ------------------------------------------------------------------ */
+/* O1: fp32 instantiation                                              */
+#define REAL float
+#define PIN float
+#define SFX _f32
+#define L(x) x##f
+#define SQRT sqrtf
+#define CEIL ceilf
+#define FLOOR floorf
+#define FMIN fminf
+#define FMAX fmaxf
+#define FMA fmaf
+#define EXPR expf
+#define VKO_IS_F32 1
+#include "vko_generic.inc"
+#undef REAL
+#undef PIN
+#undef SFX
+#undef L
+#undef SQRT
+#undef CEIL
+#undef FLOOR
+#undef FMIN
+#undef FMAX
+#undef FMA
+#undef EXPR
+#undef VKO_IS_F32
+
+/* ------------------------------------------------------------------ */
+/* O2: fp64 instantiation                                              */
+#define REAL double
+#define PIN double
+#define SFX _f64
+#define L(x) x
+#define SQRT sqrt
+#define CEIL ceil
+#define FLOOR floor
+#define FMIN fmin
+#define FMAX fmax
+#define FMA fma
+#define EXPR exp
+#define VKO_IS_F32 0
+#include "vko_generic.inc"
+#undef REAL
+#undef PIN
+#undef SFX
+#undef L
+#undef SQRT
+#undef CEIL
+#undef FLOOR
+#undef FMIN
+#undef FMAX
+#undef FMA
+#undef EXPR
+#undef VKO_IS_F32
+
+/* ------------------------------------------------------------------ */
+/* plain pthread parallel-for over [0, n) with dynamic chunks           */
+typedef void (*range_fn)(void* ctx, int64_t begin, int64_t end, int tid);
+typedef struct {
+    range_fn fn;
+    void* ctx;
+    int64_t n, chunk;
+    int64_t next;
+    pthread_mutex_t mu;
+    int tid;
+} pfor_t;
+
+static int resolve_threads(int nthreads) {
+    if (nthreads > 0) return nthreads;
+    long c = sysconf(_SC_NPROCESSORS_ONLN);
+    return c > 0 ? (int)c : 1;
+}
+
+typedef struct { pfor_t* p; int tid; } pfor_arg;
+
+static void* pfor_worker(void* argp) {
+    pfor_arg* a = (pfor_arg*)argp;
+    pfor_t* p = a->p;
+    for (;;) {
+        pthread_mutex_lock(&p->mu);
+        int64_t b = p->next;
+        p->next += p->chunk;
+        pthread_mutex_unlock(&p->mu);
+        if (b >= p->n) break;
+        int64_t e = b + p->chunk < p->n ? b + p->chunk : p->n;
+        p->fn(p->ctx, b, e, a->tid);
+    }
+    return NULL;
+}
+
+static void parallel_for(int64_t n, int64_t chunk, int nthreads, range_fn fn, void* ctx) {
+    if (n <= 0) return;
+    nthreads = resolve_threads(nthreads);
+    if (chunk < 1) chunk = 1;
+    pfor_t p = {fn, ctx, n, chunk, 0, PTHREAD_MUTEX_INITIALIZER, 0};
+    if (nthreads == 1 || n <= chunk) {
+        fn(ctx, 0, n, 0);
+        return;
+    }
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
+    pfor_arg* args = (pfor_arg*)malloc(sizeof(pfor_arg) * nthreads);
+    for (int i = 0; i < nthreads; i++) {
+        args[i].p = &p;
+        args[i].tid = i;
+        pthread_create(&th[i], NULL, pfor_worker, &args[i]);
+    }
+    for (int i = 0; i < nthreads; i++) pthread_join(th[i], NULL);
+    free(th);
+    free(args);
+}
+
+/* ------------------------------------------------------------------ */
+/* projection drivers                                                  */
+typedef struct {
+    const vko_config* cfg;
+    const vko_camera* cam;
+    const float *means, *ls, *q, *o, *sh;
+    proj_t_f32* P;
+} projctx_f32;
+
+static void proj_range_f32(void* vp, int64_t b, int64_t e, int tid) {
+    (void)tid;
+    projctx_f32* c = (projctx_f32*)vp;
+    const int64_t S = c->cfg->sh_coeffs * 3;
+    for (int64_t i = b; i < e; i++)
+        project_one_f32(c->cfg, c->cam, c->means + 3 * i, c->ls + 3 * i, c->q + 4 * i, c->o[i],
+                        c->sh + S * i, &c->P[i]);
+}
+
+static proj_t_f32* project_all_f32(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                                   const float* means, const float* ls, const float* q,
+                                   const float* o, const float* sh, int nthreads) {
+    proj_t_f32* P = (proj_t_f32*)malloc(sizeof(proj_t_f32) * (n > 0 ? n : 1));
+    projctx_f32 c = {cfg, cam, means, ls, q, o, sh, P};
+    parallel_for(n, 4096, nthreads, proj_range_f32, &c);
+    return P;
+}
+
+static proj_t_f64* project_all_f64(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                                   const double* means, const double* ls, const double* q,
+                                   const double* o, const double* sh) {
+    proj_t_f64* P = (proj_t_f64*)malloc(sizeof(proj_t_f64) * (n > 0 ? n : 1));
+    const int64_t S = cfg->sh_coeffs * 3;
+    for (int64_t i = 0; i < n; i++)
+        project_one_f64(cfg, cam, means + 3 * i, ls + 3 * i, q + 4 * i, o[i], sh + S * i, &P[i]);
+    return P;
+}
+
+#define WRITE_PROJ(P, i)                                                        \
+    do {                                                                        \
+        means2d[2 * (i)] = P.u; means2d[2 * (i) + 1] = P.v;                      \
+        conics[3 * (i)] = P.a; conics[3 * (i) + 1] = P.b; conics[3 * (i) + 2] = P.c; \
+        depths[i] = P.depth;                                                    \
+        int vis_ = (P.flags & VKO_F_VISIBLE) != 0;                              \
+        radii[2 * (i)] = vis_ ? P.rx : 0; radii[2 * (i) + 1] = vis_ ? P.ry : 0; \
+        tiles_touched[i] = vis_ ? P.tiles : 0;                                  \
+        colors[3 * (i)] = P.color[0]; colors[3 * (i) + 1] = P.color[1];          \
+        colors[3 * (i) + 2] = P.color[2];                                       \
+        opacities[i] = P.rho;                                                   \
+        if (cov2d) { cov2d[3 * (i)] = P.A; cov2d[3 * (i) + 1] = P.B; cov2d[3 * (i) + 2] = P.C; } \
+        if (flags) flags[i] = P.flags;                                          \
+    } while (0)
+
+void vko_project_fwd_f32(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                         const float* means, const float* log_scales, const float* quats,
+                         const float* opacity_logits, const float* sh, float* means2d,
+                         float* conics, float* depths, int32_t* radii, int32_t* tiles_touched,
+                         float* colors, float* opacities, float* cov2d, int32_t* flags,
+                         int nthreads) {
+    proj_t_f32* P = project_all_f32(cfg, cam, n, means, log_scales, quats, opacity_logits, sh, nthreads);
+    for (int64_t i = 0; i < n; i++) WRITE_PROJ(P[i], i);
+    free(P);
+}
+
+void vko_project_fwd_f64(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                         const double* means, const double* log_scales, const double* quats,
+                         const double* opacity_logits, const double* sh, double* means2d,
+                         double* conics, double* depths, int32_t* radii, int32_t* tiles_touched,
+                         double* colors, double* opacities, double* cov2d, int32_t* flags) {
+    proj_t_f64* P = project_all_f64(cfg, cam, n, means, log_scales, quats, opacity_logits, sh);
+    for (int64_t i = 0; i < n; i++) WRITE_PROJ(P[i], i);
+    free(P);
+}
+
+/* ------------------------------------------------------------------ */
+/* binning                                    */
+
+/* exclusive prefix sum, sequential loop */
+int64_t vko_scan_offsets(int64_t n, const int32_t* tiles_touched, uint32_t* offsets) {
+    int64_t acc = 0;
+    for (int64_t i = 0; i < n; i++) {
+        offsets[i] = (uint32_t)acc;
+        acc += tiles_touched[i];
+    }
+    return acc;
+}
+
+/* key = (tile << 32) | f32bits(depth), val = i, slots offsets[i]+k, rows
+ * outer, columns inner. The rect is recomputed from mean2d and radii
+ * exactly as in projection step 11. */
+void vko_gen_keys(const vko_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
+                  const float* depths, const int32_t* tiles_touched, const uint32_t* offsets,
+                  uint64_t* keys, uint32_t* vals) {
+    const int TX = (cam->width + 15) / 16, TY = (cam->height + 15) / 16;
+    for (int64_t i = 0; i < n; i++) {
+        if (tiles_touched[i] <= 0) continue;
+        float u = means2d[2 * i], v = means2d[2 * i + 1];
+        float rx = (float)radii[2 * i], ry = (float)radii[2 * i + 1];
+        int x0 = (int)fminf(fmaxf(floorf((u - rx) * 0.0625f), 0.0f), (float)TX);
+        int x1 = (int)fminf(fmaxf(ceilf((u + rx) * 0.0625f), 0.0f), (float)TX);
+        int y0 = (int)fminf(fmaxf(floorf((v - ry) * 0.0625f), 0.0f), (float)TY);
+        int y1 = (int)fminf(fmaxf(ceilf((v + ry) * 0.0625f), 0.0f), (float)TY);
+        uint32_t dbits;
+        memcpy(&dbits, &depths[i], 4);
+        int64_t slot = offsets[i];
+        for (int ty = y0; ty < y1; ty++)
+            for (int tx = x0; tx < x1; tx++) {
+                uint64_t tile = (uint64_t)(ty * TX + tx);
+                keys[slot] = (tile << 32) | (uint64_t)dbits;
+                vals[slot] = (uint32_t)i;
+                slot++;
+            }
+    }
+}
+
+typedef struct { uint64_t key; uint32_t val; uint32_t pos; } kv_t;
+
+static int kv_cmp(const void* pa, const void* pb) {
+    const kv_t* a = (const kv_t*)pa;
+    const kv_t* b = (const kv_t*)pb;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    return a->pos < b->pos ? -1 : (a->pos > b->pos ? 1 : 0); /* stability */
+}
+
+/* stable ascending sort by u64 key: library comparison sort on (key, slot) */
+void vko_sort_pairs(int64_t m, uint64_t* keys, uint32_t* vals) {
+    if (m <= 0) return;
+    kv_t* t = (kv_t*)malloc(sizeof(kv_t) * m);
+    for (int64_t i = 0; i < m; i++) { t[i].key = keys[i]; t[i].val = vals[i]; t[i].pos = (uint32_t)i; }
+    qsort(t, (size_t)m, sizeof(kv_t), kv_cmp);
+    for (int64_t i = 0; i < m; i++) { keys[i] = t[i].key; vals[i] = t[i].val; }
+    free(t);
+}
+
+/* CSR tile ranges: tile_offsets[t] = #{entries with tile < t} */
+void vko_tile_ranges(int64_t m, const uint64_t* keys, int32_t n_tiles, uint32_t* tile_offsets) {
+    int64_t j = 0;
+    for (int32_t t = 0; t <= n_tiles; t++) {
+        while (j < m && (int64_t)(keys[j] >> 32) < t) j++;
+        tile_offsets[t] = (uint32_t)j;
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* untiled render driver, generic over precision          */
+
+typedef struct { float depth; int32_t id; } dk_t;
+typedef struct { double depth; int32_t id; } dk64_t;
+
+static int dk_cmp(const void* pa, const void* pb) {
+    const dk_t* a = (const dk_t*)pa;
+    const dk_t* b = (const dk_t*)pb;
+    if (a->depth != b->depth) return a->depth < b->depth ? -1 : 1;
+    return a->id < b->id ? -1 : (a->id > b->id ? 1 : 0);
+}
+static int dk64_cmp(const void* pa, const void* pb) {
+    const dk64_t* a = (const dk64_t*)pa;
+    const dk64_t* b = (const dk64_t*)pb;
+    if (a->depth != b->depth) return a->depth < b->depth ? -1 : 1;
+    return a->id < b->id ? -1 : (a->id > b->id ? 1 : 0);
+}
+
+/* The oracle's OWN conservative pixel box for a candidate: the ellipse
+ * sigma <= k'' of its fp32 conic, k'' = ln(255 rho)*1.01 + 0.01, plus 2 px.
+ * It only accelerates candidate gathering; correctness of the bound is
+ * checked against the brute-force O3 in tests. */
+typedef struct { int32_t x0, x1, y0, y1; } pbox_t; /* inclusive pixel bounds, x0 > x1 = empty */
+
+static pbox_t oracle_box(double u, double v, double a, double b, double c, double rho, int W, int H, int brute) {
+    pbox_t r = {0, W - 1, 0, H - 1};
+    if (brute) return r;
+    if (!(rho >= 1.0 / 255.0)) { r.x0 = 1; r.x1 = 0; return r; }
+    double k = log(255.0 * rho) * 1.01 + 0.01;
+    double det = a * c - b * b;
+    if (!(det > 0) || !(a > 0) || !(c > 0)) return r; /* degenerate: whole image */
+    double hx = sqrt(2.0 * k * c / det) + 2.0, hy = sqrt(2.0 * k * a / det) + 2.0;
+    double fx0 = floor(u - hx), fx1 = ceil(u + hx), fy0 = floor(v - hy), fy1 = ceil(v + hy);
+    if (fx1 < 0 || fy1 < 0 || fx0 > W - 1 || fy0 > H - 1) { r.x0 = 1; r.x1 = 0; return r; }
+    r.x0 = fx0 < 0 ? 0 : (int32_t)fx0;
+    r.x1 = fx1 > W - 1 ? W - 1 : (int32_t)fx1;
+    r.y0 = fy0 < 0 ? 0 : (int32_t)fy0;
+    r.y1 = fy1 > H - 1 ? H - 1 : (int32_t)fy1;
+    return r;
+}
+
+#define BAND 16
+
+#define DEFINE_RENDER(SFXN, REALT, PROJT, ENTRYT, COMPOSITE, BACKWARD, ISF32)                  \
+    typedef struct {                                                                          \
+        const vko_config* cfg;                                                                \
+        const vko_camera* cam;                                                                \
+        const PROJT* P;                                                                       \
+        int64_t ncand;                                                                        \
+        const int32_t* cand; /* global ids in (depth,id) order */                             \
+        const pbox_t* box;   /* per candidate */                                              \
+        const REALT* dL;     /* [H,W,3] or NULL */                                            \
+        const uint8_t* row_mask;                                                              \
+        int brute;                                                                            \
+        REALT* image; float* T_final_f; double* T_final_d; int32_t* last_id; uint8_t* fragile; \
+        uint64_t* dhash;                                                                      \
+        int32_t** band_cand; int64_t* band_n; double** band_g; double** band_m;               \
+        int want_mass;                                                                        \
+        int64_t* st_viol; int64_t* st_eval; int64_t* st_comp; int64_t* st_frag; int64_t* st_rows; \
+        pthread_mutex_t* mu;                                                                  \
+    } rctx##SFXN;                                                                             \
+                                                                                              \
+    static void band_range##SFXN(void* vp, int64_t bb, int64_t be, int tid) {                 \
+        (void)tid;                                                                            \
+        rctx##SFXN* c = (rctx##SFXN*)vp;                                                      \
+        const int W = c->cam->width, H = c->cam->height;                                     \
+        for (int64_t band = bb; band < be; band++) {                                          \
+            int ys = (int)band * BAND, ye = ys + BAND < H ? ys + BAND : H;                     \
+            int any = 0;                                                                      \
+            for (int y = ys; y < ye; y++) any |= !c->row_mask || c->row_mask[y];              \
+            c->band_n[band] = 0;                                                              \
+            c->band_cand[band] = NULL; c->band_g[band] = NULL; c->band_m[band] = NULL;        \
+            if (!any) continue;                                                               \
+            /* candidates of this band, in global (depth,id) order */                         \
+            int64_t nb = 0;                                                                   \
+            for (int64_t i = 0; i < c->ncand; i++)                                            \
+                if (c->box[i].x0 <= c->box[i].x1 && c->box[i].y0 < ye && c->box[i].y1 >= ys) nb++; \
+            int32_t* bc = (int32_t*)malloc(sizeof(int32_t) * (nb > 0 ? nb : 1));              \
+            int32_t* bci = (int32_t*)malloc(sizeof(int32_t) * (nb > 0 ? nb : 1));             \
+            nb = 0;                                                                           \
+            for (int64_t i = 0; i < c->ncand; i++)                                            \
+                if (c->box[i].x0 <= c->box[i].x1 && c->box[i].y0 < ye && c->box[i].y1 >= ys) { \
+                    bc[nb] = c->cand[i]; bci[nb] = (int32_t)i; nb++;                          \
+                }                                                                             \
+            double* bg_ = NULL; double* bm_ = NULL;                                           \
+            if (c->dL) {                                                                      \
+                bg_ = (double*)calloc((size_t)(nb > 0 ? nb : 1) * 9, sizeof(double));         \
+                if (c->want_mass) bm_ = (double*)calloc((size_t)(nb > 0 ? nb : 1) * 9, sizeof(double)); \
+            }                                                                                 \
+            int64_t* cnt = (int64_t*)malloc(sizeof(int64_t) * (W + 1));                       \
+            int64_t cap = 0; int32_t* lists = NULL;                                           \
+            ENTRYT* ent = NULL; int64_t entcap = 0;                                           \
+            int64_t viol = 0, ev = 0, comp = 0, frag = 0, rows = 0;                           \
+            for (int y = ys; y < ye; y++) {                                                   \
+                if (c->row_mask && !c->row_mask[y]) continue;                                 \
+                rows++;                                                                       \
+                const int ty = y / 16;                                                        \
+                memset(cnt, 0, sizeof(int64_t) * (W + 1));                                    \
+                for (int64_t j = 0; j < nb; j++) {                                            \
+                    const pbox_t* bx = &c->box[bci[j]];                                       \
+                    if (bx->y0 > y || bx->y1 < y) continue;                                   \
+                    const PROJT* g = &c->P[bc[j]];                                            \
+                    for (int x = bx->x0; x <= bx->x1; x++) {                                  \
+                        if (c->cfg->footprint == VKO_FOOTPRINT_3SIGMA) {                      \
+                            int tx = x / 16;                                                  \
+                            if (!(g->flags & VKO_F_VISIBLE) || tx < g->x0 || tx >= g->x1 ||   \
+                                ty < g->y0 || ty >= g->y1) continue;                          \
+                        }                                                                     \
+                        cnt[x + 1]++;                                                         \
+                    }                                                                         \
+                }                                                                             \
+                for (int x = 0; x < W; x++) cnt[x + 1] += cnt[x];                             \
+                if (cnt[W] > cap) { cap = cnt[W]; lists = (int32_t*)realloc(lists, sizeof(int32_t) * cap); } \
+                int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * W);                        \
+                for (int x = 0; x < W; x++) fill[x] = cnt[x];                                 \
+                for (int64_t j = 0; j < nb; j++) {                                            \
+                    const pbox_t* bx = &c->box[bci[j]];                                       \
+                    if (bx->y0 > y || bx->y1 < y) continue;                                   \
+                    const PROJT* g = &c->P[bc[j]];                                            \
+                    for (int x = bx->x0; x <= bx->x1; x++) {                                  \
+                        if (c->cfg->footprint == VKO_FOOTPRINT_3SIGMA) {                      \
+                            int tx = x / 16;                                                  \
+                            if (!(g->flags & VKO_F_VISIBLE) || tx < g->x0 || tx >= g->x1 ||   \
+                                ty < g->y0 || ty >= g->y1) continue;                          \
+                        }                                                                     \
+                        lists[fill[x]++] = (int32_t)j;                                        \
+                    }                                                                         \
+                }                                                                             \
+                free(fill);                                                                   \
+                for (int x = 0; x < W; x++) {                                                 \
+                    int64_t len = cnt[x + 1] - cnt[x];                                        \
+                    if (len > entcap) { entcap = len; ent = (ENTRYT*)realloc(ent, sizeof(ENTRYT) * entcap); } \
+                    REALT out[3]; REALT Tf; int64_t last; int fr = 0; uint64_t hh = 0;         \
+                    const REALT px = (REALT)x + (REALT)0.5, py = (REALT)y + (REALT)0.5;       \
+                    int nent = COMPOSITE(c->P, bc, lists + cnt[x], len, px, py, out, &Tf, &last, ent, \
+                                         ISF32 ? &fr : NULL, &hh, &ev);                       \
+                    comp += nent;                                                             \
+                    const int64_t pix = (int64_t)y * W + x;                                   \
+                    for (int ch = 0; ch < 3; ch++)                                            \
+                        c->image[3 * pix + ch] = out[ch] + Tf * (REALT)c->cfg->bg[ch];        \
+                    if (c->T_final_f) c->T_final_f[pix] = (float)Tf;                          \
+                    if (c->T_final_d) c->T_final_d[pix] = (double)Tf;                         \
+                    if (c->last_id) c->last_id[pix] = last >= 0 ? bc[lists[cnt[x] + last]] : -1; \
+                    if (c->fragile) c->fragile[pix] = (uint8_t)fr;                            \
+                    if (c->dhash) c->dhash[pix] = hh;                                         \
+                    frag += fr;                                                               \
+                    /* footprint violation: composited outside the tile rect */               \
+                    const int tx = x / 16;                                                    \
+                    for (int e = 0; e < nent; e++) {                                          \
+                        const PROJT* g = &c->P[bc[ent[e].idx]];                               \
+                        if (!(g->flags & VKO_F_VISIBLE) || tx < g->x0 || tx >= g->x1 || ty < g->y0 || \
+                            ty >= g->y1) viol++;                                              \
+                    }                                                                         \
+                    if (c->dL) {                                                              \
+                        double wv[3] = {(double)c->dL[3 * pix], (double)c->dL[3 * pix + 1],   \
+                                        (double)c->dL[3 * pix + 2]};                          \
+                        double bgd[3] = {(double)c->cfg->bg[0], (double)c->cfg->bg[1], (double)c->cfg->bg[2]}; \
+                        BACKWARD(c->P, bc, ent, nent, px, py, wv, bgd, bg_, bm_);             \
+                    }                                                                         \
+                }                                                                             \
+            }                                                                                 \
+            free(cnt); free(lists); free(ent); free(bci);                                     \
+            c->band_cand[band] = bc; c->band_n[band] = nb; c->band_g[band] = bg_; c->band_m[band] = bm_; \
+            pthread_mutex_lock(c->mu);                                                        \
+            *c->st_viol += viol; *c->st_eval += ev; *c->st_comp += comp; *c->st_frag += frag; \
+            *c->st_rows += rows;                                                              \
+            pthread_mutex_unlock(c->mu);                                                      \
+        }                                                                                     \
+    }
+
+DEFINE_RENDER(_f32, float, proj_t_f32, entry_t_f32, composite_f32, backward_pixel_f32, 1)
+DEFINE_RENDER(_f64, double, proj_t_f64, entry_t_f64, composite_f64, backward_pixel_f64, 0)
+
+/* common tail: reduce per-band gradient partials in band order (deterministic) */
+static void reduce_bands(int64_t nbands, int32_t** band_cand, int64_t* band_n, double** band_g,
+                         double** band_m, int64_t n, double* dmeans2d, double* dconics,
+                         double* dcolors, double* dopacities, double* mass) {
+    if (dmeans2d) memset(dmeans2d, 0, sizeof(double) * 2 * n);
+    if (dconics) memset(dconics, 0, sizeof(double) * 3 * n);
+    if (dcolors) memset(dcolors, 0, sizeof(double) * 3 * n);
+    if (dopacities) memset(dopacities, 0, sizeof(double) * n);
+    if (mass) memset(mass, 0, sizeof(double) * 9 * n);
+    for (int64_t b = 0; b < nbands; b++) {
+        if (band_g[b]) {
+            for (int64_t j = 0; j < band_n[b]; j++) {
+                const int64_t g = band_cand[b][j];
+                const double* v = band_g[b] + 9 * j;
+                if (dmeans2d) { dmeans2d[2 * g] += v[0]; dmeans2d[2 * g + 1] += v[1]; }
+                if (dconics) { dconics[3 * g] += v[2]; dconics[3 * g + 1] += v[3]; dconics[3 * g + 2] += v[4]; }
+                if (dcolors) { dcolors[3 * g] += v[5]; dcolors[3 * g + 1] += v[6]; dcolors[3 * g + 2] += v[7]; }
+                if (dopacities) dopacities[g] += v[8];
+                if (mass && band_m[b])
+                    for (int k = 0; k < 9; k++) mass[9 * g + k] += band_m[b][9 * j + k];
+            }
+        }
+        free(band_cand[b]); free(band_g[b]); free(band_m[b]);
+    }
+}
+
+int vko_render_f32(const vko_config* cfg, const vko_camera* cam, int64_t n, const float* means,
+                   const float* log_scales, const float* quats, const float* opacity_logits,
+                   const float* sh, const float* dL_dimage, const uint8_t* row_mask, int brute,
+                   float* image, float* T_final, int32_t* last_id, uint8_t* fragile,
+                   int64_t* stats, double* dmeans2d, double* dconics, double* dcolors,
+                   double* dopacities, double* mass, int nthreads) {
+    const int W = cam->width, H = cam->height;
+    proj_t_f32* P = project_all_f32(cfg, cam, n, means, log_scales, quats, opacity_logits, sh, nthreads);
+    /* candidates: every projectable Gaussian, in ascending (f32 depth, id) */
+    int64_t nc = 0;
+    for (int64_t i = 0; i < n; i++) nc += (P[i].flags & VKO_F_PROJECTABLE) != 0;
+    dk_t* dk = (dk_t*)malloc(sizeof(dk_t) * (nc > 0 ? nc : 1));
+    nc = 0;
+    for (int64_t i = 0; i < n; i++)
+        if (P[i].flags & VKO_F_PROJECTABLE) { dk[nc].depth = P[i].depth; dk[nc].id = (int32_t)i; nc++; }
+    qsort(dk, (size_t)nc, sizeof(dk_t), dk_cmp);
+    int32_t* cand = (int32_t*)malloc(sizeof(int32_t) * (nc > 0 ? nc : 1));
+    pbox_t* box = (pbox_t*)malloc(sizeof(pbox_t) * (nc > 0 ? nc : 1));
+    for (int64_t i = 0; i < nc; i++) {
+        const proj_t_f32* g = &P[dk[i].id];
+        cand[i] = dk[i].id;
+        box[i] = oracle_box(g->u, g->v, g->a, g->b, g->c, g->rho, W, H, brute);
+    }
+    free(dk);
+    const int64_t nbands = (H + BAND - 1) / BAND;
+    int32_t** band_cand = (int32_t**)calloc(nbands > 0 ? nbands : 1, sizeof(int32_t*));
+    int64_t* band_n = (int64_t*)calloc(nbands > 0 ? nbands : 1, sizeof(int64_t));
+    double** band_g = (double**)calloc(nbands > 0 ? nbands : 1, sizeof(double*));
+    double** band_m = (double**)calloc(nbands > 0 ? nbands : 1, sizeof(double*));
+    int64_t viol = 0, ev = 0, comp = 0, frag = 0, rows = 0;
+    pthread_mutex_t mu = PTHREAD_MUTEX_INITIALIZER;
+    /* unrendered rows keep background / T=1 / -1 */
+    for (int64_t p = 0; p < (int64_t)W * H; p++) {
+        for (int ch = 0; ch < 3; ch++) image[3 * p + ch] = cfg->bg[ch];
+        if (T_final) T_final[p] = 1.0f;
+        if (last_id) last_id[p] = -1;
+        if (fragile) fragile[p] = 0;
+    }
+    rctx_f32 c = {cfg, cam, P, nc, cand, box, dL_dimage, row_mask, brute, image, T_final, NULL,
+                  last_id, fragile, NULL, band_cand, band_n, band_g, band_m, mass != NULL,
+                  &viol, &ev, &comp, &frag, &rows, &mu};
+    parallel_for(nbands, 1, nthreads, band_range_f32, &c);
+    reduce_bands(nbands, band_cand, band_n, band_g, band_m, n, dL_dimage ? dmeans2d : NULL,
+                 dL_dimage ? dconics : NULL, dL_dimage ? dcolors : NULL,
+                 dL_dimage ? dopacities : NULL, dL_dimage ? mass : NULL);
+    if (stats) {
+        stats[0] = viol; stats[1] = ev; stats[2] = comp; stats[3] = frag; stats[4] = nc; stats[5] = rows;
+        stats[6] = 0; stats[7] = 0;
+    }
+    free(band_cand); free(band_n); free(band_g); free(band_m);
+    free(cand); free(box); free(P);
+    return 0;
+}
+
+int vko_render_f64(const vko_config* cfg, const vko_camera* cam, int64_t n, const double* means,
+                   const double* log_scales, const double* quats, const double* opacity_logits,
+                   const double* sh, const double* dL_dimage, double* image,
+                   uint64_t* decision_hash, int32_t* proj_flags, double* dmeans2d,
+                   double* dconics, double* dcolors, double* dopacities) {
+    const int W = cam->width, H = cam->height;
+    proj_t_f64* P = project_all_f64(cfg, cam, n, means, log_scales, quats, opacity_logits, sh);
+    int64_t nc = 0;
+    for (int64_t i = 0; i < n; i++) {
+        if (proj_flags) proj_flags[i] = P[i].flags;
+        nc += (P[i].flags & VKO_F_PROJECTABLE) != 0;
+    }
+    dk64_t* dk = (dk64_t*)malloc(sizeof(dk64_t) * (nc > 0 ? nc : 1));
+    nc = 0;
+    for (int64_t i = 0; i < n; i++)
+        if (P[i].flags & VKO_F_PROJECTABLE) { dk[nc].depth = P[i].depth; dk[nc].id = (int32_t)i; nc++; }
+    qsort(dk, (size_t)nc, sizeof(dk64_t), dk64_cmp);
+    int32_t* cand = (int32_t*)malloc(sizeof(int32_t) * (nc > 0 ? nc : 1));
+    pbox_t* box = (pbox_t*)malloc(sizeof(pbox_t) * (nc > 0 ? nc : 1));
+    for (int64_t i = 0; i < nc; i++) {
+        cand[i] = dk[i].id;
+        box[i] = oracle_box(0, 0, 0, 0, 0, 1, W, H, 1); /* fp64 FD path: brute force */
+    }
+    free(dk);
+    const int64_t nbands = (H + BAND - 1) / BAND;
+    int32_t** band_cand = (int32_t**)calloc(nbands > 0 ? nbands : 1, sizeof(int32_t*));
+    int64_t* band_n = (int64_t*)calloc(nbands > 0 ? nbands : 1, sizeof(int64_t));
+    double** band_g = (double**)calloc(nbands > 0 ? nbands : 1, sizeof(double*));
+    double** band_m = (double**)calloc(nbands > 0 ? nbands : 1, sizeof(double*));
+    int64_t viol = 0, ev = 0, comp = 0, frag = 0, rows = 0;
+    pthread_mutex_t mu = PTHREAD_MUTEX_INITIALIZER;
+    rctx_f64 c = {cfg, cam, P, nc, cand, box, dL_dimage, NULL, 1, image, NULL, NULL, NULL, NULL,
+                  decision_hash, band_cand, band_n, band_g, band_m, 0,
+                  &viol, &ev, &comp, &frag, &rows, &mu};
+    parallel_for(nbands, 1, 1, band_range_f64, &c);
+    reduce_bands(nbands, band_cand, band_n, band_g, band_m, n, dL_dimage ? dmeans2d : NULL,
+                 dL_dimage ? dconics : NULL, dL_dimage ? dcolors : NULL,
+                 dL_dimage ? dopacities : NULL, NULL);
+    free(band_cand); free(band_n); free(band_g); free(band_m);
+    free(cand); free(box); free(P);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* projection backward, fp64                             */
+
+static const double C0d = 0.28209479177387814, C1d = 0.4886025119029199;
+static const double C2d[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                              -1.0925484305920792, 0.5462742152960396};
+static const double C3d[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                              0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+                              -0.5900435899266435};
+
+/* gradient of each basis function w.r.t. the (unit) direction (x,y,z) */
+static void sh_basis_grad(double x, double y, double z, int K, double Y[16], double dY[16][3]) {
+    memset(dY, 0, sizeof(double) * 48);
+    Y[0] = C0d;
+    if (K > 1) {
+        Y[1] = -C1d * y; dY[1][1] = -C1d;
+        Y[2] = C1d * z;  dY[2][2] = C1d;
+        Y[3] = -C1d * x; dY[3][0] = -C1d;
+    }
+    if (K > 4) {
+        double xx = x * x, yy = y * y, zz = z * z;
+        Y[4] = C2d[0] * x * y; dY[4][0] = C2d[0] * y; dY[4][1] = C2d[0] * x;
+        Y[5] = C2d[1] * y * z; dY[5][1] = C2d[1] * z; dY[5][2] = C2d[1] * y;
+        Y[6] = C2d[2] * (2 * zz - xx - yy);
+        dY[6][0] = -2 * C2d[2] * x; dY[6][1] = -2 * C2d[2] * y; dY[6][2] = 4 * C2d[2] * z;
+        Y[7] = C2d[3] * x * z; dY[7][0] = C2d[3] * z; dY[7][2] = C2d[3] * x;
+        Y[8] = C2d[4] * (xx - yy); dY[8][0] = 2 * C2d[4] * x; dY[8][1] = -2 * C2d[4] * y;
+    }
+    if (K > 9) {
+        double xx = x * x, yy = y * y, zz = z * z;
+        Y[9] = C3d[0] * y * (3 * xx - yy);
+        dY[9][0] = 6 * C3d[0] * x * y; dY[9][1] = C3d[0] * (3 * xx - 3 * yy);
+        Y[10] = C3d[1] * x * y * z;
+        dY[10][0] = C3d[1] * y * z; dY[10][1] = C3d[1] * x * z; dY[10][2] = C3d[1] * x * y;
+        Y[11] = C3d[2] * y * (4 * zz - xx - yy);
+        dY[11][0] = -2 * C3d[2] * x * y; dY[11][1] = C3d[2] * (4 * zz - xx - 3 * yy);
+        dY[11][2] = 8 * C3d[2] * y * z;
+        Y[12] = C3d[3] * z * (2 * zz - 3 * xx - 3 * yy);
+        dY[12][0] = -6 * C3d[3] * x * z; dY[12][1] = -6 * C3d[3] * y * z;
+        dY[12][2] = C3d[3] * (6 * zz - 3 * xx - 3 * yy);
+        Y[13] = C3d[4] * x * (4 * zz - xx - yy);
+        dY[13][0] = C3d[4] * (4 * zz - 3 * xx - yy); dY[13][1] = -2 * C3d[4] * x * y;
+        dY[13][2] = 8 * C3d[4] * x * z;
+        Y[14] = C3d[5] * z * (xx - yy);
+        dY[14][0] = 2 * C3d[5] * x * z; dY[14][1] = -2 * C3d[5] * y * z; dY[14][2] = C3d[5] * (xx - yy);
+        Y[15] = C3d[6] * x * (xx - 3 * yy);
+        dY[15][0] = C3d[6] * (3 * xx - 3 * yy); dY[15][1] = -6 * C3d[6] * x * y;
+    }
+}
+
+/* one Gaussian; decisions (cull, FOV clamp, colour clamp) from `flags` */
+static void proj_bwd_one(const vko_config* cfg, const vko_camera* cam, int32_t flags,
+                         const double mu[3], const double ls[3], const double q[4], double o,
+                         const double* sh, const double dm2[2], const double dcon[3],
+                         const double dcol[3], double drho, double dmu[3], double dls[3],
+                         double dq[4], double* dlogit, double* dsh) {
+    double R[9], ct[3];
+    for (int i = 0; i < 9; i++) R[i] = cam->R[i];
+    for (int i = 0; i < 3; i++) ct[i] = cam->t[i];
+    const double fx = cam->fx, fy = cam->fy, cx = cam->cx, cy = cam->cy;
+    const double W = cam->width, H = cam->height;
+    const int K = (cfg->sh_degree + 1) * (cfg->sh_degree + 1);
+    double t[3];
+    for (int j = 0; j < 3; j++) t[j] = R[3 * j] * mu[0] + R[3 * j + 1] * mu[1] + R[3 * j + 2] * mu[2] + ct[j];
+    const double tx = t[0], ty = t[1], tz = t[2];
+    double qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    double w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
+    double Rq[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                    2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                    2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    double s[3] = {exp(ls[0]), exp(ls[1]), exp(ls[2])};
+    double M[9], Mc[9];
+    for (int j = 0; j < 3; j++)
+        for (int k = 0; k < 3; k++) M[3 * j + k] = Rq[3 * j + k] * s[k];
+    for (int j = 0; j < 3; j++)
+        for (int k = 0; k < 3; k++)
+            Mc[3 * j + k] = R[3 * j] * M[k] + R[3 * j + 1] * M[3 + k] + R[3 * j + 2] * M[6 + k];
+    /* FOV clamp, branch from the fp32 decision */
+    double Lx = 0, Ly = 0;
+    int clx = 0, cly = 0;
+    if (cfg->fov_clamp) {
+        double lxp = (W - cx) / fx + 0.3 * (0.5 * W / fx), lxn = cx / fx + 0.3 * (0.5 * W / fx);
+        double lyp = (H - cy) / fy + 0.3 * (0.5 * H / fy), lyn = cy / fy + 0.3 * (0.5 * H / fy);
+        if (flags & VKO_F_FOVX_HI) { clx = 1; Lx = lxp; }
+        else if (flags & VKO_F_FOVX_LO) { clx = 1; Lx = -lxn; }
+        if (flags & VKO_F_FOVY_HI) { cly = 1; Ly = lyp; }
+        else if (flags & VKO_F_FOVY_LO) { cly = 1; Ly = -lyn; }
+    }
+    const double txc = clx ? tz * Lx : tx, tyc = cly ? tz * Ly : ty;
+    const double J00 = fx / tz, J02 = -fx * txc / (tz * tz), J11 = fy / tz, J12 = -fy * tyc / (tz * tz);
+    double K0[3], K1[3];
+    for (int k = 0; k < 3; k++) {
+        K0[k] = J00 * Mc[k] + J02 * Mc[6 + k];
+        K1[k] = J11 * Mc[3 + k] + J12 * Mc[6 + k];
+    }
+    const double A = K0[0] * K0[0] + K0[1] * K0[1] + K0[2] * K0[2] + 0.3;
+    const double B = K0[0] * K1[0] + K0[1] * K1[1] + K0[2] * K1[2];
+    const double C = K1[0] * K1[0] + K1[1] * K1[1] + K1[2] * K1[2] + 0.3;
+    const double det = A * C - B * B, det2 = det * det;
+    /* opacity: d logit = d rho * rho (1 - rho) */
+    const double rho = 1.0 / (1.0 + exp(-o));
+    *dlogit = drho * rho * (1 - rho);
+    /* colour: masked by the forward clamp; dsh = Y dcolour; direction term */
+    double cp[3];
+    for (int k = 0; k < 3; k++) cp[k] = -(R[k] * ct[0] + R[3 + k] * ct[1] + R[6 + k] * ct[2]);
+    double d[3] = {mu[0] - cp[0], mu[1] - cp[1], mu[2] - cp[2]};
+    double dl = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    double dh[3] = {d[0] / dl, d[1] / dl, d[2] / dl};
+    double Y[16], dY[16][3];
+    sh_basis_grad(dh[0], dh[1], dh[2], K, Y, dY);
+    double dce[3];
+    for (int ch = 0; ch < 3; ch++) dce[ch] = (flags & (VKO_F_CLAMP_R << ch)) ? 0.0 : dcol[ch];
+    double ddh[3] = {0, 0, 0};
+    for (int l = 0; l < K; l++)
+        for (int ch = 0; ch < 3; ch++) {
+            dsh[3 * l + ch] = Y[l] * dce[ch];
+            for (int k = 0; k < 3; k++) ddh[k] += dce[ch] * sh[3 * l + ch] * dY[l][k];
+        }
+    double proj = dh[0] * ddh[0] + dh[1] * ddh[1] + dh[2] * ddh[2];
+    for (int k = 0; k < 3; k++) dmu[k] = (ddh[k] - dh[k] * proj) / dl;
+    /* conic (a,b,c) = (C,-B,A)/det  ->  (A,B,C) */
+    const double da = dcon[0], db = dcon[1], dc = dcon[2];
+    const double dA = da * (-C * C / det2) + db * (B * C / det2) + dc * (1 / det - A * C / det2);
+    const double dB = da * (2 * B * C / det2) + db * (-1 / det - 2 * B * B / det2) + dc * (2 * A * B / det2);
+    const double dC = da * (1 / det - A * C / det2) + db * (A * B / det2) + dc * (-A * A / det2);
+    /* Sigma' = K K^T + 0.3 I :  dK = 2 G2 K */
+    double dK0[3], dK1[3];
+    for (int k = 0; k < 3; k++) {
+        dK0[k] = 2 * dA * K0[k] + dB * K1[k];
+        dK1[k] = dB * K0[k] + 2 * dC * K1[k];
+    }
+    /* K = J Mc */
+    double dJ00 = 0, dJ02 = 0, dJ11 = 0, dJ12 = 0;
+    for (int k = 0; k < 3; k++) {
+        dJ00 += dK0[k] * Mc[k];
+        dJ02 += dK0[k] * Mc[6 + k];
+        dJ11 += dK1[k] * Mc[3 + k];
+        dJ12 += dK1[k] * Mc[6 + k];
+    }
+    double dMc[9];
+    for (int k = 0; k < 3; k++) {
+        dMc[k] = J00 * dK0[k];
+        dMc[3 + k] = J11 * dK1[k];
+        dMc[6 + k] = J02 * dK0[k] + J12 * dK1[k];
+    }
+    /* Mc = R M */
+    double dM[9];
+    for (int j = 0; j < 3; j++)
+        for (int k = 0; k < 3; k++)
+            dM[3 * j + k] = R[j] * dMc[k] + R[3 + j] * dMc[3 + k] + R[6 + j] * dMc[6 + k];
+    /* M = Rq diag(s) */
+    double D[9];
+    for (int k = 0; k < 3; k++) {
+        double ds = 0;
+        for (int j = 0; j < 3; j++) {
+            ds += dM[3 * j + k] * Rq[3 * j + k];
+            D[3 * j + k] = dM[3 * j + k] * s[k];
+        }
+        dls[k] = ds * s[k];
+    }
+    double dqh[4];
+    dqh[0] = 2 * (-z * D[1] + y * D[2] + z * D[3] - x * D[5] - y * D[6] + x * D[7]);
+    dqh[1] = 2 * (y * D[1] + z * D[2] + y * D[3] - 2 * x * D[4] - w * D[5] + z * D[6] + w * D[7] - 2 * x * D[8]);
+    dqh[2] = 2 * (-2 * y * D[0] + x * D[1] + w * D[2] + x * D[3] + z * D[5] - w * D[6] + z * D[7] - 2 * y * D[8]);
+    dqh[3] = 2 * (-2 * z * D[0] - w * D[1] + x * D[2] + w * D[3] - 2 * z * D[4] + y * D[5] + x * D[6] + y * D[7]);
+    const double qd = w * dqh[0] + x * dqh[1] + y * dqh[2] + z * dqh[3];
+    const double qh[4] = {w, x, y, z};
+    for (int k = 0; k < 4; k++) dq[k] = (dqh[k] - qh[k] * qd) / qn;
+    /* t: from mean2d and from J */
+    double dt[3] = {0, 0, 0};
+    const double tz2 = tz * tz, tz3 = tz2 * tz;
+    dt[0] += fx / tz * dm2[0];
+    dt[1] += fy / tz * dm2[1];
+    dt[2] += -fx * tx / tz2 * dm2[0] - fy * ty / tz2 * dm2[1];
+    dt[2] += -fx / tz2 * dJ00 - fy / tz2 * dJ11;
+    if (!clx) { dt[0] += -fx / tz2 * dJ02; dt[2] += 2 * fx * tx / tz3 * dJ02; }
+    else { dt[2] += fx * Lx / tz2 * dJ02; }
+    if (!cly) { dt[1] += -fy / tz2 * dJ12; dt[2] += 2 * fy * ty / tz3 * dJ12; }
+    else { dt[2] += fy * Ly / tz2 * dJ12; }
+    /* t = R mu + t_cam */
+    for (int k = 0; k < 3; k++) dmu[k] += R[k] * dt[0] + R[3 + k] * dt[1] + R[6 + k] * dt[2];
+}
+
+typedef struct {
+    const vko_config* cfg;
+    const vko_camera* cam;
+    const float *means, *ls, *q, *o, *sh;
+    const double *dm2, *dcon, *dcol, *dop;
+    double *dmeans, *dls, *dq, *dol, *dsh;
+} pbctx;
+
+static void pbwd_range(void* vp, int64_t b, int64_t e, int tid) {
+    (void)tid;
+    pbctx* c = (pbctx*)vp;
+    const int64_t S = c->cfg->sh_coeffs * 3;
+    double* shd = (double*)malloc(sizeof(double) * S);
+    for (int64_t i = b; i < e; i++) {
+        memset(c->dmeans + 3 * i, 0, 3 * sizeof(double));
+        memset(c->dls + 3 * i, 0, 3 * sizeof(double));
+        memset(c->dq + 4 * i, 0, 4 * sizeof(double));
+        c->dol[i] = 0;
+        memset(c->dsh + S * i, 0, S * sizeof(double));
+        proj_t_f32 P;
+        project_one_f32(c->cfg, c->cam, c->means + 3 * i, c->ls + 3 * i, c->q + 4 * i, c->o[i],
+                        c->sh + S * i, &P);
+        if (!(P.flags & VKO_F_VISIBLE)) continue; /* never rasterised: no gradient */
+        double mu[3], ls[3], q[4];
+        for (int k = 0; k < 3; k++) { mu[k] = c->means[3 * i + k]; ls[k] = c->ls[3 * i + k]; }
+        for (int k = 0; k < 4; k++) q[k] = c->q[4 * i + k];
+        for (int k = 0; k < S; k++) shd[k] = c->sh[S * i + k];
+        proj_bwd_one(c->cfg, c->cam, P.flags, mu, ls, q, c->o[i], shd, c->dm2 + 2 * i,
+                     c->dcon + 3 * i, c->dcol + 3 * i, c->dop[i], c->dmeans + 3 * i,
+                     c->dls + 3 * i, c->dq + 4 * i, &c->dol[i], c->dsh + S * i);
+    }
+    free(shd);
+}
+
+void vko_project_bwd(const vko_config* cfg, const vko_camera* cam, int64_t n, const float* means,
+                     const float* log_scales, const float* quats, const float* opacity_logits,
+                     const float* sh, const double* dmeans2d, const double* dconics,
+                     const double* dcolors, const double* dopacities, double* dmeans,
+                     double* dlog_scales, double* dquats, double* dopacity_logits, double* dsh,
+                     int nthreads) {
+    pbctx c = {cfg, cam, means, log_scales, quats, opacity_logits, sh, dmeans2d, dconics, dcolors,
+               dopacities, dmeans, dlog_scales, dquats, dopacity_logits, dsh};
+    parallel_for(n, 4096, nthreads, pbwd_range, &c);
+}
+
+void vko_project_bwd_f64(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                         const double* means, const double* log_scales, const double* quats,
+                         const double* opacity_logits, const double* sh, const double* dmeans2d,
+                         const double* dconics, const double* dcolors, const double* dopacities,
+                         double* dmeans, double* dlog_scales, double* dquats,
+                         double* dopacity_logits, double* dsh) {
+    const int64_t S = cfg->sh_coeffs * 3;
+    for (int64_t i = 0; i < n; i++) {
+        memset(dmeans + 3 * i, 0, 3 * sizeof(double));
+        memset(dlog_scales + 3 * i, 0, 3 * sizeof(double));
+        memset(dquats + 4 * i, 0, 4 * sizeof(double));
+        dopacity_logits[i] = 0;
+        memset(dsh + S * i, 0, S * sizeof(double));
+        proj_t_f64 P;
+        project_one_f64(cfg, cam, means + 3 * i, log_scales + 3 * i, quats + 4 * i,
+                        opacity_logits[i], sh + S * i, &P);
+        if (!(P.flags & VKO_F_PROJECTABLE)) continue;
+        proj_bwd_one(cfg, cam, P.flags, means + 3 * i, log_scales + 3 * i, quats + 4 * i,
+                     opacity_logits[i], sh + S * i, dmeans2d + 2 * i, dconics + 3 * i,
+                     dcolors + 3 * i, dopacities[i], dmeans + 3 * i, dlog_scales + 3 * i,
+                     dquats + 4 * i, &dopacity_logits[i], dsh + S * i);
+    }
+}

@@ -1,0 +1,148 @@
+/*
+ * vko.h — CPU ORACLE for the VkSplat hot path.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load, call or execute anything under oracle/.  The product
+ * path (paper_2605_00219_b200/) never links or imports it, and the two share no
+ * code, headers, constants or helpers.
+ *
+ * What it computes (citations: P:n = /root/reference/PAPER.md line n,
+ * S:n = /root/reference/SPEC.md line n, SURVEY §8c = /root/repo/SURVEY.md):
+ *   - projection forward  ("Projection Forward")
+ *   - index offsets       ("Index Offset";       S:124-132; §8c.3)
+ *   - key generation      ("Generate Keys";      S:133-141; §8c.3)
+ *   - stable sort         ("Sorting";            S:142-150; §8c.3)
+ *   - tile ranges         ("Tile Ranges";        S:151-159; §8c.3)
+ *   - compositing fwd     ("Rasterization Forward"; §8c.1, §8c.4)
+ *     UNTILED: every pixel walks all candidates in global (depth, id) order.
+ *   - compositing bwd     ("Rasterization Backward"; §8c.5)
+ *   - projection bwd      ("Proj Bwd + Optimizer", projection part; §8c.6)
+ *
+ * Precision: O1 = fp32 forward with the operation order pinned in DESIGN.md §4
+ * (the kernel's precision, because fp32 values decide integers: footprints,
+ * tile rects, keys, skip/stop decisions).  O2 = the same formulas in fp64, and
+ * every backward accumulates in fp64.  O3 = brute force (no bounding box).
+ *
+ * Parity pins: see tests/test_oracle_*.py.  "VkSplat's actual kernel
+ * behaviour" is parity unpinned: the paper publishes timings only.
+ */
+#ifndef VKO_H
+#define VKO_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    float R[9];      /* world->camera rotation, row-major; OpenCV axes (x right, y down, z fwd) */
+    float t[3];      /* p_cam = R p_world + t */
+    float fx, fy, cx, cy;
+    int32_t width, height;
+} vko_camera;
+
+typedef struct {
+    int32_t sh_degree;   /* 0..3, active degree; K = (D+1)^2 coefficients used */
+    int32_t sh_coeffs;   /* stored coefficients per Gaussian (row stride / 3), >= K */
+    float near_plane;    /* 0.01 */
+    float bg[3];         /* background colour (north_star: empty scene gives bg) */
+    int32_t fov_clamp;   /* 1: gsplat/3DGS 1.3x tan-FOV clamp inside J */
+    int32_t footprint;   /* 0 = exact alpha-support bbox (default), 1 = 3-sigma square */
+} vko_config;
+
+enum { VKO_FOOTPRINT_SUPPORT = 0, VKO_FOOTPRINT_3SIGMA = 1 };
+
+/* per-Gaussian flag bits written by the projection */
+enum {
+    VKO_F_PROJECTABLE = 1 << 0, /* passed near / quaternion / det / finiteness / (support: rho) culls */
+    VKO_F_VISIBLE = 1 << 1,     /* tiles_touched > 0 */
+    VKO_F_CLAMP_R = 1 << 2,     /* colour channel clamped at 0 (raw <= 0) */
+    VKO_F_CLAMP_G = 1 << 3,
+    VKO_F_CLAMP_B = 1 << 4,
+    VKO_F_FOVX_HI = 1 << 5,     /* tx/tz > lim_x+ : clamped at the upper x limit */
+    VKO_F_FOVX_LO = 1 << 6,
+    VKO_F_FOVY_HI = 1 << 7,
+    VKO_F_FOVY_LO = 1 << 8
+};
+
+/* O1 projection (fp32, pinned order).  Outputs of non-visible rows: radii=0,
+ * tiles=0, other fields are still written (garbage allowed, compared only on
+ * visible rows).  cov2d [n,3] = (A,B,C) incl. +0.3 (nullable). */
+void vko_project_fwd_f32(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                         const float* means, const float* log_scales, const float* quats,
+                         const float* opacity_logits, const float* sh,
+                         float* means2d, float* conics, float* depths, int32_t* radii,
+                         int32_t* tiles_touched, float* colors, float* opacities,
+                         float* cov2d, int32_t* flags, int nthreads);
+
+/* O2 projection (fp64) of the same formulas; same layout, double outputs. */
+void vko_project_fwd_f64(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                         const double* means, const double* log_scales, const double* quats,
+                         const double* opacity_logits, const double* sh,
+                         double* means2d, double* conics, double* depths, int32_t* radii,
+                         int32_t* tiles_touched, double* colors, double* opacities,
+                         double* cov2d, int32_t* flags);
+
+/* Binning (integer, exact). */
+int64_t vko_scan_offsets(int64_t n, const int32_t* tiles_touched, uint32_t* offsets);
+void vko_gen_keys(const vko_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
+                  const float* depths, const int32_t* tiles_touched, const uint32_t* offsets,
+                  uint64_t* keys, uint32_t* vals);
+void vko_sort_pairs(int64_t m, uint64_t* keys, uint32_t* vals);
+void vko_tile_ranges(int64_t m, const uint64_t* keys, int32_t n_tiles, uint32_t* tile_offsets);
+
+/* Forward + (optional) backward compositing, untiled.
+ * Runs its own O1 projection from the parameters.
+ *   dL_dimage [H,W,3] nullable -> no backward.
+ *   row_mask [H] nullable -> all rows; else only rows with row_mask[y]!=0 are rendered
+ *   brute != 0 -> O3: every candidate is tested at every pixel (no bbox).
+ * Outputs: image [H,W,3], T_final [H,W], last_id [H,W] (-1 = none),
+ *          fragile [H,W] (1 = a decision lies within the fast-exp window, §8c.9),
+ *          stats [8]: 0 footprint violations, 1 evaluations, 2 composited,
+ *                     3 fragile pixels, 4 candidates, 5 rows rendered
+ * Backward outputs (fp64, overwritten): dmeans2d [n,2], dconics [n,3],
+ *   dcolors [n,3], dopacities [n]; mass [n,9] nullable = sum |terms|.        */
+int vko_render_f32(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                   const float* means, const float* log_scales, const float* quats,
+                   const float* opacity_logits, const float* sh,
+                   const float* dL_dimage, const uint8_t* row_mask, int brute,
+                   float* image, float* T_final, int32_t* last_id, uint8_t* fragile,
+                   int64_t* stats, double* dmeans2d, double* dconics, double* dcolors,
+                   double* dopacities, double* mass, int nthreads);
+
+/* fp64 forward render for finite differences (O2): image [H,W,3] double,
+ * decision hash per pixel [H,W] (uint64; folds skip/clamp/stop decisions) and
+ * projection flags [n].  If dL_dimage != NULL also returns the fp64 backward
+ * (exact gradient of this fp64 forward) in the d* outputs. */
+int vko_render_f64(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                   const double* means, const double* log_scales, const double* quats,
+                   const double* opacity_logits, const double* sh,
+                   const double* dL_dimage, double* image, uint64_t* decision_hash,
+                   int32_t* proj_flags, double* dmeans2d, double* dconics, double* dcolors,
+                   double* dopacities);
+
+/* Projection backward (O2, fp64).  Discrete decisions (cull,
+ * FOV clamp, colour clamp) come from the O1 fp32 projection of the same
+ * parameters.  Gradients are OVERWRITTEN (not accumulated). */
+void vko_project_bwd(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                     const float* means, const float* log_scales, const float* quats,
+                     const float* opacity_logits, const float* sh,
+                     const double* dmeans2d, const double* dconics, const double* dcolors,
+                     const double* dopacities,
+                     double* dmeans, double* dlog_scales, double* dquats,
+                     double* dopacity_logits, double* dsh, int nthreads);
+
+/* fp64-parameter variant (for FD on double parameters); decisions from the
+ * fp64 projection. */
+void vko_project_bwd_f64(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                         const double* means, const double* log_scales, const double* quats,
+                         const double* opacity_logits, const double* sh,
+                         const double* dmeans2d, const double* dconics, const double* dcolors,
+                         const double* dopacities,
+                         double* dmeans, double* dlog_scales, double* dquats,
+                         double* dopacity_logits, double* dsh);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark of the VkSplat hot path on B200 (BASELINE.json metric:
+"fwd+bwd rasterize iters/sec @5.8M Gaussians 1237x822; sort Gkeys/s; HBM GB/s").
+
+A step = one full pass of the hot path per rank: projection forward, index offsets + keys + radix
+sort + tile ranges, raster forward, raster backward, projection backward (SURVEY §8(a) rows
+a1-a8) for one view of the synthetic bicycle-shaped scene, plus (N > 1) the allreduce of the
+per-Gaussian gradient buffer (row a9).  Views are sharded across ranks (rank r renders ring views
+r, r+N, ...), so per-GPU work is fixed as N grows ("weak" scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config bicycle]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the reference arm of
+this tier) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd rasterize iters/sec @5.8M Gaussians 1237x822; sort Gkeys/s; HBM GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="bicycle")
+    ap.add_argument("--views-per-rank", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows-every", type=int, default=8, help="oracle raster sample: every k-th tile row")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm_gbs=float(d["hbm_gbs"]), sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)), src="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, src="fallback")
+
+
+# ----------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"], samples=0)
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                    reasons=reasons, samples=len(rows))
+
+
+# ----------------------------------------------------------------------------------- algorithmic work
+def algorithmic_bytes(n, vis, m, px, passes, K=16):
+    """Per-view algorithmic HBM bytes of the HBM-bound stages."""
+    sh = 12 * K
+    return dict(
+        project_fwd=12 * n + 28 * (n - vis) + (12 + 16 + 4 + sh) * vis + 12 * n + 40 * vis,
+        scan=8 * n,
+        keys=20 * vis + 12 * m,
+        sort=8 * m + 24 * passes * m,
+        project_bwd=8 * n + vis * ((40 + sh) + 36 + 2 * (40 + sh)),
+    )
+
+
+def raster_flops(e_fwd, c_fwd, e_bwd, c_bwd):
+    """Algorithmic fp32 operations: forward 10 per evaluated pair + 9 per composited
+    one; backward 10 per evaluated pair + 44 per composited one (the 9 gradient terms)."""
+    return dict(raster_fwd=10 * e_fwd + 9 * c_fwd, raster_bwd=10 * e_bwd + 44 * c_bwd)
+
+
+# ----------------------------------------------------------------------------------- ours
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_00219_b200 as P
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = synth.CONFIGS[args.config]
+    cfg = synth.default_render_config(3)
+    scene = synth.make_scene(c.n, c.kind, c.seed)
+    cams = synth.ring_cameras(c.width, c.height, c.kind, 8)
+    params = P.GaussianParams.from_host(scene)
+    del scene
+    n = params.n
+    vpr = args.views_per_rank
+    my_views = [(rank + world * j) % 8 for j in range(8)]
+    dLs = {v: torch.from_numpy(synth.upstream_grad(c.height, c.width, c.seed + 1000 + v)).cuda()
+           for v in set(my_views)}
+    rend = P.ViewRenderer(n, c.width, c.height)
+    for v in set(my_views):  # size the key capacity once (untimed)
+        rend.forward(cfg, cams[v], params)
+    rend._alloc_capacity(int(rend.capacity * 1.1))
+    stream = torch.cuda.current_stream()
+    stages = ["project_fwd", "bin_sort", "raster_fwd", "raster_bwd", "project_bwd", "allreduce"]
+
+    def step(s, ev=None):
+        for j in range(vpr):
+            v = my_views[(s * vpr + j) % len(my_views)]
+            cam = cams[v]
+            if ev is not None: ev[0].record(stream)
+            P.vks_project_fwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
+                              params.sh, rend.means2d, rend.conics, rend.depths, rend.radii, rend.tiles,
+                              rend.colors, rend.opacities)
+            if ev is not None: ev[1].record(stream)
+            m = P.vks_bin_sort(cam, rend.means2d, rend.radii, rend.depths, rend.tiles, rend.offsets, rend.keys,
+                               rend.vals, rend.tile_offsets, rend.workspace)
+            rend.num_isects = m
+            if ev is not None: ev[2].record(stream)
+            P.vks_raster_fwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.vals,
+                             rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib)
+            if ev is not None: ev[3].record(stream)
+            rend.g2d.zero_()
+            P.vks_raster_bwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.vals,
+                             rend.tile_offsets, rend.T_final, rend.n_contrib, dLs[v], rend.dmeans2d, rend.dconics,
+                             rend.dcolors, rend.dopacities)
+            if ev is not None: ev[4].record(stream)
+            g = params.grads()
+            P.vks_project_bwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
+                              params.sh, rend.radii, rend.dmeans2d, rend.dconics, rend.dcolors, rend.dopacities,
+                              g["dmeans"], g["dlog_scales"], g["dquats"], g["dopacity_logits"], g["dsh"])
+            if ev is not None: ev[5].record(stream)
+        if world > 1:
+            dist.all_reduce(params.grad_flat)
+        if ev is not None: ev[6].record(stream)
+        params.grad_flat.zero_()  # next batch of views accumulates from zero
+        return m
+
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    Ms = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for s in range(args.steps):
+        Ms.append(step(args.warmup + s, evs[s]))
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+    # per-stage medians (ms) over the timed steps (vpr == 1: one view per step)
+    st_ms = {name: statistics.median([evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)])
+             for i, name in enumerate(stages)}
+    views_total = world * vpr * args.steps
+    value = views_total / (elapsed_ms / 1e3)
+
+    # --- workload statistics (untimed): visible count, M, evaluations, sort-only timing
+    torch.cuda.synchronize()
+    vis = int((rend.tiles > 0).sum().item())
+    m_last = rend.num_isects
+    e_stats = raster_work(rend, c.width, c.height)
+    passes = (32 + max(0, math.ceil(math.log2(rend.n_tiles))) + 7) // 8
+    ab = algorithmic_bytes(n, vis, m_last, c.width * c.height, passes)
+    fl = raster_flops(*e_stats)
+    pk = peaks()
+    clock_mhz = clk["sm_mhz"] or pk["sm_max_mhz"]
+    fp32_peak_tflops = 148 * 128 * 2 * clock_mhz * 1e6 / 1e12
+    per_stage = {}
+    for k in ("project_fwd", "project_bwd"):
+        gbs = ab[k] / (st_ms[k] * 1e-3) / 1e9
+        per_stage[k] = dict(ms=st_ms[k], bound="hbm", achieved=gbs, peak=pk["hbm_gbs"], unit="GB/s",
+                            frac=gbs / pk["hbm_gbs"])
+    for k in ("raster_fwd", "raster_bwd"):
+        tf = fl[k] / (st_ms[k] * 1e-3) / 1e12
+        per_stage[k] = dict(ms=st_ms[k], bound="alu", achieved=tf, peak=fp32_peak_tflops, unit="TFLOP/s",
+                            frac=tf / fp32_peak_tflops)
+    bs_bytes = ab["scan"] + ab["keys"] + ab["sort"] + 8 * m_last
+    gbs = bs_bytes / (st_ms["bin_sort"] * 1e-3) / 1e9
+    per_stage["bin_sort"] = dict(ms=st_ms["bin_sort"], bound="hbm", achieved=gbs, peak=pk["hbm_gbs"],
+                                 unit="GB/s", frac=gbs / pk["hbm_gbs"],
+                                 gkeys_per_s=m_last / (st_ms["bin_sort"] * 1e-3) / 1e9)
+    dom = max((k for k in per_stage), key=lambda k: per_stage[k]["ms"])
+    d = per_stage[dom]
+    roofline = dict(kernel=dom, bound=d["bound"], achieved=round(d["achieved"], 3), peak=round(d["peak"], 3),
+                    unit=d["unit"], frac=round(d["frac"], 4), traffic=None,
+                    peak_source=(pk["src"] + (" HBM copy" if d["bound"] == "hbm" else
+                                              f" FP32 148 SM x 128 lanes x 2 x {clock_mhz:.0f} MHz")))
+    gpu_launches = (1 + (3 + passes) + 1 + 1 + 1) * vpr * args.steps
+
+    out = dict(metric=METRIC, value=round(value, 3), unit="iters/s", n_gpus=world, steps=args.steps,
+               warmup=args.warmup, ms_per_step=round(elapsed_ms / args.steps, 4), higher_is_better=True,
+               scaling="weak", vs_baseline=None, dtype="f32", data="synthetic",
+               config=dict(workload=c.description + ", fwd+bwd", n_gaussians=n, width=c.width,
+                           height=c.height, sh_degree=3, footprint="support", views_per_rank=vpr,
+                           visible=vis, num_isects=m_last, sort_passes=passes,
+                           l2="inputs larger than L2 (params 1.37 GB, keys+vals 0.22 GB per view), no flush",
+                           parallelism=f"view-sharded dp{world}"),
+               stages_ms={k: round(v, 4) for k, v in st_ms.items()},
+               stage_roofline={k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                               for k, v in per_stage.items()},
+               sort_gkeys_per_s=round(per_stage["bin_sort"]["gkeys_per_s"], 3),
+               raster_work=dict(evals_fwd=e_stats[0], composited_fwd=e_stats[1], evals_bwd=e_stats[2],
+                                composited_bwd=e_stats[3]),
+               roofline=roofline, gpu_launches=gpu_launches, clocks=clk)
+
+    if not args.no_e2e:
+        out["e2e"] = run_e2e(args, P, params, rend, cams, my_views, cfg, c, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, c, cfg)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def raster_work(rend, W, H):
+    """Evaluated / composited (pixel, Gaussian) pairs of the last view, from the forward outputs:
+    a pixel evaluates its tile list up to its stop (n_contrib if T < 1e-4, else the whole list)."""
+    import torch
+    TX = (W + 15) // 16
+    to = rend.tile_offsets.view(torch.int32).to(torch.int64)
+    lens = (to[1:] - to[:-1])
+    ys = torch.arange(H, device="cuda").view(-1, 1) // 16
+    xs = torch.arange(W, device="cuda").view(1, -1) // 16
+    tl = lens[(ys * TX + xs)]
+    nc = rend.n_contrib.to(torch.int64)
+    stopped = rend.T_final < 1e-4
+    e_fwd = int(torch.where(stopped, nc, tl).sum().item())
+    e_bwd = int(nc.sum().item())
+    # composited counts are not stored; bound by the evaluated ones (reported as such)
+    return e_fwd, 0, e_bwd, 0
+
+
+def run_e2e(args, P, params, rend, cams, my_views, cfg, c, world):
+    """Same step through the public API with HOST buffers: dL/dimage copied in from pinned host
+    memory and the rendered image copied back out every step, inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    stream = torch.cuda.current_stream()
+    host_dL = {v: torch.from_numpy(synth.upstream_grad(c.height, c.width, c.seed + 1000 + v)).pin_memory()
+               for v in set(my_views)}
+    dev_dL = torch.empty(c.height, c.width, 3, device="cuda")
+    host_img = torch.empty(c.height, c.width, 3, pin_memory=True)
+
+    def step(s):
+        v = my_views[s % len(my_views)]
+        dev_dL.copy_(host_dL[v], non_blocking=True)
+        rend.forward(cfg, cams[v], params)
+        rend.backward(cfg, cams[v], params, dev_dL)
+        if world > 1:
+            dist.all_reduce(params.grad_flat)
+        host_img.copy_(rend.image, non_blocking=True)
+        params.grad_flat.zero_()
+
+    for s in range(min(args.warmup, 3)):
+        step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for s in range(args.steps):
+        step(s)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    nbytes = c.height * c.width * 3 * 4
+    return dict(value=round(world * args.steps / (ms / 1e3), 3), unit="iters/s", h2d_bytes_per_step=nbytes,
+                d2h_bytes_per_step=nbytes, ms_per_step=round(ms / args.steps, 4))
+
+
+# ----------------------------------------------------------------------------------- oracle (CPU)
+def oracle_view_sample(c, cfg, view, rows_every, band_offset=0):
+    """The oracle on one view: projection + binning in full, raster fwd+bwd on every `rows_every`-th
+    tile row (starting at band_offset), projection backward in full.  Returns (seconds, estimate of
+    the full-view seconds, description)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    scene = synth.make_scene(c.n, c.kind, c.seed)
+    cam = synth.ring_cameras(c.width, c.height, c.kind, 8)[view]
+    dL = synth.upstream_grad(c.height, c.width, c.seed + 1000 + view)
+    ty = np.arange(c.height) // 16
+    rm = (((ty - band_offset) % rows_every) == 0).astype(np.uint8)
+    t = {}
+    t0 = time.perf_counter()
+    proj = oracle.project_fwd(cfg, cam, scene)
+    t["project_fwd"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.bin_sort(cfg, cam, proj)
+    t["bin_sort"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r = oracle.render(cfg, cam, scene, dL=dL, row_mask=rm)
+    t["raster_fwd_bwd_sampled"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.project_bwd(cfg, cam, scene, r)
+    t["project_bwd"] = time.perf_counter() - t0
+    frac = float(rm.sum()) / c.height
+    full = t["project_fwd"] + t["bin_sort"] + t["raster_fwd_bwd_sampled"] / frac + t["project_bwd"]
+    return sum(t.values()), full, t, frac
+
+
+def cpu_baseline(args, c, cfg):
+    cores = os.cpu_count()
+    secs, full, t, frac = oracle_view_sample(c, cfg, 0, args.cpu_rows_every)
+    return dict(value=round(1.0 / full, 5), unit="iters/s", cores=cores, kind="oracle",
+                sample=(f"{c.name} view 0: projection, binning and projection-bwd in full; raster fwd+bwd on "
+                        f"every {args.cpu_rows_every}th tile row ({frac:.3f} of pixels, time scaled by "
+                        f"1/{frac:.3f}); {secs:.1f} s of CPU wall time on {cores} threads"),
+                stage_seconds={k: round(v, 3) for k, v in t.items()})
+
+
+def run_reference(args):
+    """Reference arm of this tier: the CPU oracle, as it stands, on the host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    c = synth.CONFIGS[args.config]
+    cfg = synth.default_render_config(3)
+    cores = os.cpu_count()
+    budget_s = 240.0
+    fulls, walls = [], []
+    total = args.warmup + args.steps
+    done = 0
+    t_start = time.perf_counter()
+    rows_every = 32  # one band in 32 per step (rotating), bounded per-step sample
+    for s in range(total):
+        secs, full, _, frac = oracle_view_sample(c, cfg, s % 8, rows_every, band_offset=s % rows_every)
+        done += 1
+        if s >= args.warmup or (s == total - 1 and not fulls):
+            fulls.append(full)
+            walls.append(secs)
+        if time.perf_counter() - t_start > budget_s and fulls:
+            break
+    value = len(fulls) / sum(fulls)
+    out = dict(metric=METRIC, value=round(value, 5), unit="iters/s", n_gpus=world, steps=args.steps,
+               warmup=args.warmup, ms_per_step=round(1e3 * sum(fulls) / len(fulls), 2), higher_is_better=True,
+               scaling="weak", vs_baseline=None, dtype="f32", data="synthetic", impl="reference",
+               config=dict(workload=c.description + ", fwd+bwd", n_gaussians=c.n, width=c.width, height=c.height,
+                           sh_degree=3, footprint="support", parallelism="cpu oracle (rank 0 only)"),
+               cpu_baseline=dict(value=round(value, 5), unit="iters/s", cores=cores, kind="oracle",
+                                 sample=(f"per step one ring view; projection, binning, projection-bwd in full, "
+                                         f"raster fwd+bwd on 1 of every {rows_every} tile rows (rotating), "
+                                         f"time scaled to the full view; {len(fulls)} timed steps run "
+                                         f"(240 s budget), {sum(walls):.1f} s wall")),
+               e2e=dict(value=round(value, 5), unit="iters/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+               gpu_launches=0)
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

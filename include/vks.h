@@ -1,0 +1,188 @@
+/*
+ * vks.h — C ABI of the B200-native VkSplat hot path (libvks.so, sm_100a).
+ *
+ * The five entry points are the per-iteration stages the paper times
+ * (§2 "Timing breakdown"; one call per table row or group):
+ *
+ *   vks_project_fwd  <- "Projection Forward"
+ *   vks_bin_sort     <- "Index Offset", "Generate Keys", "Sorting", "Tile Ranges"
+ *                       (grouped as "tiling/sorting")
+ *   vks_raster_fwd   <- "Rasterization Forward"
+ *   vks_raster_bwd   <- "Rasterization Backward"
+ *   vks_project_bwd  <- "Proj Bwd + Optimizer", projection part
+ *
+ * The paper prints no formulas (PAPER.md is the supplementary timing/metric
+ * tables only).  The operations follow the SPEC written from the paper
+ * and the readings listed in
+ * DESIGN.md §4 (e.g. support footprint, FOV clamp, SH degree 3).
+ *
+ * Conventions (all calls):
+ *  - Every array argument is a DEVICE pointer (caller-owned; e.g. a torch
+ *    tensor's data_ptr) unless marked HOST.  All arrays are dense, row-major,
+ *    fp32 / int32 / uint32 / uint64 as typed, 16-byte aligned base pointers.
+ *  - `stream` is a cudaStream_t (CUstream); every call only enqueues work on
+ *    it and returns, except vks_bin_sort which synchronises `stream` once to
+ *    read the intersection count.
+ *  - The library never allocates or frees device memory and keeps no pointer
+ *    between calls.  It is re-entrant; calls on different streams may overlap.
+ *  - Gradient outputs ACCUMULATE (+=): the caller zeroes them (2D grads once
+ *    per view, parameter grads once per batch of views).
+ *  - Errors: synchronous argument checks return VKS_ERR_INVALID_ARG /
+ *    VKS_ERR_UNSUPPORTED without launching anything; a failed launch returns
+ *    VKS_ERR_CUDA; asynchronous device faults surface at the next sync
+ *    (CUDA convention).  There is no CPU fallback: without a CUDA device
+ *    every compute call returns VKS_ERR_CUDA.
+ *
+ * Coordinates: OpenCV camera axes (x right, y down, z forward); pixel (x,y)
+ * has centre (x+0.5, y+0.5); tiles are 16x16, row-major ids
+ * t = ty*TX + tx with TX = ceil(W/16), TY = ceil(H/16).
+ */
+#ifndef VKS_H
+#define VKS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VKS_VERSION 1
+#define VKS_TILE 16
+
+typedef struct CUstream_st* vks_stream_t; /* == cudaStream_t */
+
+/* Pinhole camera, world->camera p_cam = R p_world + t. */
+typedef struct {
+    float R[9];      /* row-major rotation */
+    float t[3];
+    float fx, fy, cx, cy;
+    int32_t width, height; /* 1 .. 65536 */
+} vks_camera;
+
+enum { VKS_FOOTPRINT_SUPPORT = 0, VKS_FOOTPRINT_3SIGMA = 1 };
+
+typedef struct {
+    int32_t sh_degree;  /* active SH degree D in 0..3 (north_star: degree 3) */
+    int32_t sh_coeffs;  /* coefficients stored per Gaussian, >= (D+1)^2; sh row = 3*sh_coeffs floats */
+    float near_plane;   /* cull if !(t.z > near) (0.01) */
+    float bg[3];        /* background colour (default 0) */
+    int32_t fov_clamp;  /* 1 = clamp tx/tz, ty/tz to 1.3x the image half-FOV inside J (gsplat/3DGS) */
+    int32_t footprint;  /* VKS_FOOTPRINT_SUPPORT (default): exact alpha>=1/255 support bbox;
+                           VKS_FOOTPRINT_3SIGMA: ceil(3 sqrt(lambda_max)) square */
+    uint32_t flags;     /* reserved, must be 0 */
+} vks_config;
+
+enum {
+    VKS_OK = 0,
+    VKS_ERR_INVALID_ARG = 1,
+    VKS_ERR_CAPACITY = 2,   /* vks_bin_sort: M > capacity (or M >= 2^32); *num_isects holds M */
+    VKS_ERR_WORKSPACE = 3,  /* workspace too small */
+    VKS_ERR_CUDA = 4,       /* launch / runtime failure (incl. no CUDA device) */
+    VKS_ERR_UNSUPPORTED = 5
+};
+
+const char* vks_status_string(int status);
+int vks_version(void);
+/* last CUDA error string seen by this thread (for VKS_ERR_CUDA) */
+const char* vks_last_cuda_error(void);
+
+/*
+ * vks_project_fwd — "Projection Forward".
+ * Per Gaussian i: t = R mu + t; cull !(t.z > near); q-hat = q/|q| (w,x,y,z);
+ * Sigma' = J (R Rq S)(R Rq S)^T J^T + 0.3 I; conic = Sigma'^-1 as (a,b,c);
+ * mean2d = (fx tx/tz + cx, fy ty/tz + cy); depth = tz; opacity = sigmoid(o);
+ * colour = max(0, sum_l Y_l(d) f_l + 0.5) (3DGS real SH); footprint radii and
+ * tiles_touched = #16x16 tiles of the footprint rect clipped to the image.
+ *   n                Gaussians (>= 0)
+ *   means [n,3], log_scales [n,3], quats [n,4] (w,x,y,z, need not be unit),
+ *   opacity_logits [n], sh [n, sh_coeffs, 3]
+ *   -> means2d [n,2], conics [n,3], depths [n], radii [n,2] int32,
+ *      tiles_touched [n] int32, colors [n,3], opacities [n]
+ * Rows with tiles_touched == 0 (culled / off-image) have radii = (0,0); their
+ * other outputs are left unwritten.  fp32, operation order pinned (bit-exact
+ * with the oracle's O1).
+ */
+int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
+                    const float* means, const float* log_scales, const float* quats,
+                    const float* opacity_logits, const float* sh,
+                    float* means2d, float* conics, float* depths, int32_t* radii,
+                    int32_t* tiles_touched, float* colors, float* opacities,
+                    vks_stream_t stream);
+
+/*
+ * vks_bin_sort_workspace_bytes — device workspace needed by vks_bin_sort for
+ * n Gaussians, a key capacity `capacity` and n_tiles tiles.
+ */
+size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles);
+
+/*
+ * vks_bin_sort — "Index Offset" + "Generate Keys" + "Sorting" + "Tile Ranges"
+ * (S:124-159).
+ *   offsets [n] u32      <- exclusive prefix sum of tiles_touched
+ *   *num_isects (HOST)   <- M = sum tiles_touched
+ *   for each i with tiles_touched > 0 and each tile (ty outer, tx inner) of its
+ *   rect: slot offsets[i]+k gets key = (tile << 32) | f32bits(depth_i), val = i
+ *   keys/vals [capacity] <- the M pairs stable-sorted ascending by key (u64)
+ *   tile_offsets [n_tiles+1] u32 <- CSR: #entries with tile id < t
+ *   keys_unsorted / vals_unsorted (nullable, debug; [capacity] like keys/vals): the pre-sort pairs.
+ * If M > capacity (or M >= 2^32) returns VKS_ERR_CAPACITY after writing
+ * *num_isects, touching nothing else; the call is idempotent, so the caller
+ * regrows and calls again.  Synchronises `stream` once (to read M).
+ * workspace: device memory of >= vks_bin_sort_workspace_bytes(n, capacity, n_tiles).
+ */
+int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
+                 const float* depths, const int32_t* tiles_touched, uint32_t* offsets,
+                 int64_t capacity, uint64_t* keys, uint32_t* vals, uint64_t* keys_unsorted,
+                 uint32_t* vals_unsorted, uint32_t* tile_offsets, int64_t* num_isects,
+                 void* workspace, size_t workspace_bytes, vks_stream_t stream);
+
+/*
+ * vks_raster_fwd — "Rasterization Forward".
+ * Per pixel, front to back over its tile's sorted list:
+ *   sigma = 1/2 a dx^2 + b dx dy + 1/2 c dy^2 (dx = u - (x+.5));  skip sigma < 0;
+ *   alpha = min(0.99, rho e^-sigma); skip alpha < 1/255;  C += c alpha T;
+ *   T *= 1 - alpha;  stop once T < 1e-4.   out = C + T bg.
+ *   -> image [H,W,3], T_final [H,W], n_contrib [H,W] int32 (1-based position,
+ *      within the tile's list, of the last composited entry; 0 = none).
+ * vals/tile_offsets as produced by vks_bin_sort.
+ */
+int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
+                   const float* means2d, const float* conics, const float* colors,
+                   const float* opacities, const uint32_t* vals, const uint32_t* tile_offsets,
+                   float* image, float* T_final, int32_t* n_contrib, vks_stream_t stream);
+
+/*
+ * vks_raster_bwd — "Rasterization Backward".
+ * Replays each pixel back to front from n_contrib, recovering T by division,
+ * and ACCUMULATES exact gradients of the forward w.r.t. mean2d, conic (a,b,c
+ * as independent scalars), colour and opacity (0 where alpha was clamped).
+ *   dL_dimage [H,W,3] -> dmeans2d [n,2], dconics [n,3], dcolors [n,3], dopacities [n] (+=)
+ */
+int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
+                   const float* means2d, const float* conics, const float* colors,
+                   const float* opacities, const uint32_t* vals, const uint32_t* tile_offsets,
+                   const float* T_final, const int32_t* n_contrib, const float* dL_dimage,
+                   float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
+                   vks_stream_t stream);
+
+/*
+ * vks_project_bwd — projection part of "Proj Bwd + Optimizer".
+ * Chain rule from the 2D gradients to the parameters for every Gaussian with
+ * radii != 0 (others untouched): conic inversion, Sigma' = J W Sigma W^T J^T
+ * (+0.3 passes the gradient), exact FOV-clamp derivative, quaternion
+ * normalisation, exp / sigmoid activations, SH colour (clamped channels give 0).
+ *   -> dmeans [n,3], dlog_scales [n,3], dquats [n,4], dopacity_logits [n],
+ *      dsh [n, sh_coeffs, 3]   (+=)
+ */
+int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
+                    const float* means, const float* log_scales, const float* quats,
+                    const float* opacity_logits, const float* sh, const int32_t* radii,
+                    const float* dmeans2d, const float* dconics, const float* dcolors,
+                    const float* dopacities, float* dmeans, float* dlog_scales, float* dquats,
+                    float* dopacity_logits, float* dsh, vks_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VKS_H */

@@ -222,6 +222,21 @@ def project_bwd(cfg, cam, scene, g2d, nthreads=0, f64=False):
     return out
 
 
+def project_bwd_mass(cfg, cam, scene, m2d, nthreads=0):
+    """Running-error mass of the projection backward for non-negative 2D-gradient masses m2d
+    (dict dmeans2d/dconics/dcolors/dopacities).  Returns fp64 masses shaped like the gradients."""
+    n = scene["means"].shape[0]
+    S = scene["sh"].shape[1]
+    out = dict(dmeans=np.zeros((n, 3)), dlog_scales=np.zeros((n, 3)), dquats=np.zeros((n, 4)),
+               dopacity_logits=np.zeros(n), dsh=np.zeros((n, S, 3)))
+    gi = [np.ascontiguousarray(np.abs(m2d[k]), np.float64) for k in ("dmeans2d", "dconics", "dcolors", "dopacities")]
+    lib().vko_project_bwd_mass(C.byref(make_config(cfg)), C.byref(make_camera(cam)), C.c_int64(n),
+                               *[_p(a) for a in _scene32(scene)], *[_p(a) for a in gi],
+                               *[_p(out[k]) for k in ("dmeans", "dlog_scales", "dquats", "dopacity_logits", "dsh")],
+                               C.c_int(nthreads))
+    return out
+
+
 def full_backward(cfg, cam, scene, dL, row_mask=None, want_mass=False, nthreads=0):
     """End-to-end oracle: render (O1 fwd + O2 bwd) then O2 projection backward."""
     r = render(cfg, cam, scene, dL=dL, row_mask=row_mask, want_mass=want_mass, nthreads=nthreads)

@@ -748,6 +748,175 @@ static void proj_bwd_one(const vko_config* cfg, const vko_camera* cam, int32_t f
     for (int k = 0; k < 3; k++) dmu[k] += R[k] * dt[0] + R[3 + k] * dt[1] + R[6 + k] * dt[2];
 }
 
+/* Running-error "mass" of the projection backward: the same chain as proj_bwd_one, evaluated
+ * with every coefficient replaced by its absolute value and every sum by a sum of absolute terms,
+ * in the evaluation structure of the fp32 CUDA kernel (DESIGN.md §7 P5).  Inputs are non-negative
+ * masses of the 2D gradients; outputs bound sum|terms| of each parameter gradient, so an fp32
+ * evaluation of the chain is accurate to a few hundred ulps of this mass. */
+static void proj_bwd_mass_one(const vko_config* cfg, const vko_camera* cam, int32_t flags,
+                              const double mu[3], const double ls[3], const double q[4], double o,
+                              const double* sh, const double mdm2[2], const double mdcon[3],
+                              const double mdcol[3], double mdrho, double mmu[3], double mls[3],
+                              double mq[4], double* mlogit, double* msh) {
+    double R[9], ct[3];
+    for (int i = 0; i < 9; i++) R[i] = cam->R[i];
+    for (int i = 0; i < 3; i++) ct[i] = cam->t[i];
+    const double fx = cam->fx, fy = cam->fy, cx = cam->cx, cy = cam->cy;
+    const double W = cam->width, H = cam->height;
+    const int K = (cfg->sh_degree + 1) * (cfg->sh_degree + 1);
+    double t[3];
+    for (int j = 0; j < 3; j++) t[j] = R[3 * j] * mu[0] + R[3 * j + 1] * mu[1] + R[3 * j + 2] * mu[2] + ct[j];
+    const double tx = t[0], ty = t[1], tz = t[2];
+    double qn = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    double w = q[0] / qn, x = q[1] / qn, y = q[2] / qn, z = q[3] / qn;
+    double Rq[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                    2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                    2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    double s[3] = {exp(ls[0]), exp(ls[1]), exp(ls[2])};
+    double M[9], Mc[9];
+    for (int j = 0; j < 3; j++)
+        for (int k = 0; k < 3; k++) M[3 * j + k] = Rq[3 * j + k] * s[k];
+    for (int j = 0; j < 3; j++)
+        for (int k = 0; k < 3; k++)
+            Mc[3 * j + k] = R[3 * j] * M[k] + R[3 * j + 1] * M[3 + k] + R[3 * j + 2] * M[6 + k];
+    double Lx = 0, Ly = 0;
+    int clx = 0, cly = 0;
+    if (cfg->fov_clamp) {
+        double lxp = (W - cx) / fx + 0.3 * (0.5 * W / fx), lxn = cx / fx + 0.3 * (0.5 * W / fx);
+        double lyp = (H - cy) / fy + 0.3 * (0.5 * H / fy), lyn = cy / fy + 0.3 * (0.5 * H / fy);
+        if (flags & VKO_F_FOVX_HI) { clx = 1; Lx = lxp; }
+        else if (flags & VKO_F_FOVX_LO) { clx = 1; Lx = -lxn; }
+        if (flags & VKO_F_FOVY_HI) { cly = 1; Ly = lyp; }
+        else if (flags & VKO_F_FOVY_LO) { cly = 1; Ly = -lyn; }
+    }
+    const double txc = clx ? tz * Lx : tx, tyc = cly ? tz * Ly : ty;
+    const double J00 = fx / tz, J02 = -fx * txc / (tz * tz), J11 = fy / tz, J12 = -fy * tyc / (tz * tz);
+    double K0[3], K1[3];
+    for (int k = 0; k < 3; k++) {
+        K0[k] = J00 * Mc[k] + J02 * Mc[6 + k];
+        K1[k] = J11 * Mc[3 + k] + J12 * Mc[6 + k];
+    }
+    const double A = K0[0] * K0[0] + K0[1] * K0[1] + K0[2] * K0[2] + 0.3;
+    const double B = K0[0] * K1[0] + K0[1] * K1[1] + K0[2] * K1[2];
+    const double C = K1[0] * K1[0] + K1[1] * K1[1] + K1[2] * K1[2] + 0.3;
+    const double det = A * C - B * B, det2 = det * det;
+    const double rho = 1.0 / (1.0 + exp(-o));
+    *mlogit = mdrho * rho * (1 - rho);
+    double cp[3];
+    for (int k = 0; k < 3; k++) cp[k] = -(R[k] * ct[0] + R[3 + k] * ct[1] + R[6 + k] * ct[2]);
+    double d[3] = {mu[0] - cp[0], mu[1] - cp[1], mu[2] - cp[2]};
+    double dl = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    double dh[3] = {d[0] / dl, d[1] / dl, d[2] / dl};
+    double Y[16], dY[16][3];
+    sh_basis_grad(dh[0], dh[1], dh[2], K, Y, dY);
+    double mce[3];
+    for (int ch = 0; ch < 3; ch++) mce[ch] = (flags & (VKO_F_CLAMP_R << ch)) ? 0.0 : mdcol[ch];
+    double mdh[3] = {0, 0, 0};
+    for (int l = 0; l < K; l++) {
+        double mg = 0;
+        for (int ch = 0; ch < 3; ch++) {
+            msh[3 * l + ch] = fabs(Y[l]) * mce[ch];
+            mg += mce[ch] * fabs(sh[3 * l + ch]);
+        }
+        for (int k = 0; k < 3; k++) mdh[k] += mg * fabs(dY[l][k]);
+    }
+    const double mpr = fabs(dh[0]) * mdh[0] + fabs(dh[1]) * mdh[1] + fabs(dh[2]) * mdh[2];
+    for (int k = 0; k < 3; k++) mmu[k] = (mdh[k] + fabs(dh[k]) * mpr) / dl;
+    const double ma = mdcon[0], mb = mdcon[1], mc = mdcon[2];
+    const double mA = (C * C * ma + fabs(B * C) * mb + B * B * mc) / det2;
+    const double mB = (2 * fabs(B * C) * ma + (A * C + B * B) * mb + 2 * fabs(A * B) * mc) / det2;
+    const double mC = (B * B * ma + fabs(A * B) * mb + A * A * mc) / det2;
+    double mK0[3], mK1[3];
+    for (int k = 0; k < 3; k++) {
+        mK0[k] = 2 * mA * fabs(K0[k]) + mB * fabs(K1[k]);
+        mK1[k] = mB * fabs(K0[k]) + 2 * mC * fabs(K1[k]);
+    }
+    double mJ00 = 0, mJ02 = 0, mJ11 = 0, mJ12 = 0, mMc[9];
+    for (int k = 0; k < 3; k++) {
+        mJ00 += mK0[k] * fabs(Mc[k]);
+        mJ02 += mK0[k] * fabs(Mc[6 + k]);
+        mJ11 += mK1[k] * fabs(Mc[3 + k]);
+        mJ12 += mK1[k] * fabs(Mc[6 + k]);
+        mMc[k] = fabs(J00) * mK0[k];
+        mMc[3 + k] = fabs(J11) * mK1[k];
+        mMc[6 + k] = fabs(J02) * mK0[k] + fabs(J12) * mK1[k];
+    }
+    double mD[9];
+    for (int k = 0; k < 3; k++) {
+        double ms = 0;
+        for (int j = 0; j < 3; j++) {
+            const double mM = fabs(R[j]) * mMc[k] + fabs(R[3 + j]) * mMc[3 + k] + fabs(R[6 + j]) * mMc[6 + k];
+            ms += mM * fabs(Rq[3 * j + k]);
+            mD[3 * j + k] = mM * s[k];
+        }
+        mls[k] = ms * s[k];
+    }
+    const double aw = fabs(w), ax = fabs(x), ay = fabs(y), az = fabs(z);
+    double mqh[4];
+    mqh[0] = 2 * (az * mD[1] + ay * mD[2] + az * mD[3] + ax * mD[5] + ay * mD[6] + ax * mD[7]);
+    mqh[1] = 2 * (ay * mD[1] + az * mD[2] + ay * mD[3] + 2 * ax * mD[4] + aw * mD[5] + az * mD[6] + aw * mD[7] + 2 * ax * mD[8]);
+    mqh[2] = 2 * (2 * ay * mD[0] + ax * mD[1] + aw * mD[2] + ax * mD[3] + az * mD[5] + aw * mD[6] + az * mD[7] + 2 * ay * mD[8]);
+    mqh[3] = 2 * (2 * az * mD[0] + aw * mD[1] + ax * mD[2] + aw * mD[3] + 2 * az * mD[4] + ay * mD[5] + ax * mD[6] + ay * mD[7]);
+    const double mqd = aw * mqh[0] + ax * mqh[1] + ay * mqh[2] + az * mqh[3];
+    const double aq[4] = {aw, ax, ay, az};
+    for (int k = 0; k < 4; k++) mq[k] = (mqh[k] + aq[k] * mqd) / qn;
+    const double tz2 = tz * tz, tz3 = tz2 * tz;
+    double mt[3];
+    mt[0] = fx / tz * mdm2[0];
+    mt[1] = fy / tz * mdm2[1];
+    mt[2] = fabs(fx * tx) / tz2 * mdm2[0] + fabs(fy * ty) / tz2 * mdm2[1] + fx / tz2 * mJ00 + fy / tz2 * mJ11;
+    if (!clx) { mt[0] += fx / tz2 * mJ02; mt[2] += 2 * fabs(fx * tx) / tz3 * mJ02; }
+    else { mt[2] += fabs(fx * Lx) / tz2 * mJ02; }
+    if (!cly) { mt[1] += fy / tz2 * mJ12; mt[2] += 2 * fabs(fy * ty) / tz3 * mJ12; }
+    else { mt[2] += fabs(fy * Ly) / tz2 * mJ12; }
+    for (int k = 0; k < 3; k++) mmu[k] += fabs(R[k]) * mt[0] + fabs(R[3 + k]) * mt[1] + fabs(R[6 + k]) * mt[2];
+}
+
+typedef struct {
+    const vko_config* cfg;
+    const vko_camera* cam;
+    const float *means, *ls, *q, *o, *sh;
+    const double *dm2, *dcon, *dcol, *dop;
+    double *dmeans, *dls, *dq, *dol, *dsh;
+} pmctx;
+
+static void pmass_range(void* vp, int64_t b, int64_t e, int tid) {
+    (void)tid;
+    pmctx* c = (pmctx*)vp;
+    const int64_t S = c->cfg->sh_coeffs * 3;
+    double* shd = (double*)malloc(sizeof(double) * S);
+    for (int64_t i = b; i < e; i++) {
+        memset(c->dmeans + 3 * i, 0, 3 * sizeof(double));
+        memset(c->dls + 3 * i, 0, 3 * sizeof(double));
+        memset(c->dq + 4 * i, 0, 4 * sizeof(double));
+        c->dol[i] = 0;
+        memset(c->dsh + S * i, 0, S * sizeof(double));
+        proj_t_f32 P;
+        project_one_f32(c->cfg, c->cam, c->means + 3 * i, c->ls + 3 * i, c->q + 4 * i, c->o[i],
+                        c->sh + S * i, &P);
+        if (!(P.flags & VKO_F_VISIBLE)) continue;
+        double mu[3], ls[3], q[4];
+        for (int k = 0; k < 3; k++) { mu[k] = c->means[3 * i + k]; ls[k] = c->ls[3 * i + k]; }
+        for (int k = 0; k < 4; k++) q[k] = c->q[4 * i + k];
+        for (int k = 0; k < S; k++) shd[k] = c->sh[S * i + k];
+        proj_bwd_mass_one(c->cfg, c->cam, P.flags, mu, ls, q, c->o[i], shd, c->dm2 + 2 * i,
+                          c->dcon + 3 * i, c->dcol + 3 * i, c->dop[i], c->dmeans + 3 * i,
+                          c->dls + 3 * i, c->dq + 4 * i, &c->dol[i], c->dsh + S * i);
+    }
+    free(shd);
+}
+
+void vko_project_bwd_mass(const vko_config* cfg, const vko_camera* cam, int64_t n, const float* means,
+                          const float* log_scales, const float* quats, const float* opacity_logits,
+                          const float* sh, const double* m_dmeans2d, const double* m_dconics,
+                          const double* m_dcolors, const double* m_dopacities, double* m_dmeans,
+                          double* m_dlog_scales, double* m_dquats, double* m_dopacity_logits,
+                          double* m_dsh, int nthreads) {
+    pmctx c = {cfg, cam, means, log_scales, quats, opacity_logits, sh, m_dmeans2d, m_dconics,
+               m_dcolors, m_dopacities, m_dmeans, m_dlog_scales, m_dquats, m_dopacity_logits, m_dsh};
+    parallel_for(n, 4096, nthreads, pmass_range, &c);
+}
+
 typedef struct {
     const vko_config* cfg;
     const vko_camera* cam;

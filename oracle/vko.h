@@ -132,6 +132,16 @@ void vko_project_bwd(const vko_config* cfg, const vko_camera* cam, int64_t n,
                      double* dmeans, double* dlog_scales, double* dquats,
                      double* dopacity_logits, double* dsh, int nthreads);
 
+/* Running-error mass of the projection backward (non-negative inputs = masses of the 2D
+ * gradients; outputs = sum of |terms| of each parameter gradient in the CUDA kernel's evaluation
+ * structure).  Used to classify condition-limited elements (DESIGN.md §7 P5). */
+void vko_project_bwd_mass(const vko_config* cfg, const vko_camera* cam, int64_t n,
+                          const float* means, const float* log_scales, const float* quats,
+                          const float* opacity_logits, const float* sh,
+                          const double* m_dmeans2d, const double* m_dconics, const double* m_dcolors,
+                          const double* m_dopacities, double* m_dmeans, double* m_dlog_scales,
+                          double* m_dquats, double* m_dopacity_logits, double* m_dsh, int nthreads);
+
 /* fp64-parameter variant (for FD on double parameters); decisions from the
  * fp64 projection. */
 void vko_project_bwd_f64(const vko_config* cfg, const vko_camera* cam, int64_t n,

@@ -1,0 +1,13 @@
+"""B200-native VkSplat hot path (arxiv/paper_2605_00219): projection, binning/sort, tile
+compositing and their backward as hand-written sm_100a CUDA kernels behind the C ABI in
+include/vks.h.  This package is the thin Python binding (`_vks`, same names as the C entry
+points) plus buffer orchestration (`pipeline`).  There is no CPU fallback: importing fails
+loudly when libvks.so is missing."""
+from ._vks import (EXPORTS, FOOTPRINT_3SIGMA, FOOTPRINT_SUPPORT, VksError, exported_symbols,  # noqa: F401
+                   make_camera, make_config, vks_bin_sort, vks_bin_sort_workspace_bytes, vks_project_bwd,
+                   vks_project_fwd, vks_raster_bwd, vks_raster_fwd, vks_version)
+from .pipeline import GaussianParams, ViewRenderer  # noqa: F401
+
+__all__ = ["vks_project_fwd", "vks_bin_sort", "vks_bin_sort_workspace_bytes", "vks_raster_fwd",
+           "vks_raster_bwd", "vks_project_bwd", "vks_version", "GaussianParams", "ViewRenderer",
+           "VksError", "make_camera", "make_config"]

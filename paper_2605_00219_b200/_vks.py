@@ -1,0 +1,209 @@
+"""ctypes binding of libvks.so — argument marshalling only.
+
+Every function here has the name of the C entry point it wraps (include/vks.h) and does nothing
+but check tensor dtype / device / contiguity, pass raw device pointers and the current CUDA
+stream, and raise on a non-OK status.  All computation happens in the CUDA kernels.  If the
+library is missing or cannot load, importing this module raises: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvks.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2605_00219_b200._build` "
+                      "(or __graft_entry__.build()); the CUDA path has no fallback")
+_lib = C.CDLL(LIB_PATH)
+
+VKS_OK, VKS_ERR_INVALID_ARG, VKS_ERR_CAPACITY, VKS_ERR_WORKSPACE, VKS_ERR_CUDA, VKS_ERR_UNSUPPORTED = range(6)
+FOOTPRINT_SUPPORT, FOOTPRINT_3SIGMA = 0, 1
+
+EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_project_fwd",
+           "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_bwd",
+           "vks_project_bwd")
+
+
+class VksCamera(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class VksConfig(C.Structure):
+    _fields_ = [("sh_degree", C.c_int32), ("sh_coeffs", C.c_int32), ("near_plane", C.c_float),
+                ("bg", C.c_float * 3), ("fov_clamp", C.c_int32), ("footprint", C.c_int32),
+                ("flags", C.c_uint32)]
+
+
+_P = C.c_void_p
+_lib.vks_status_string.restype = C.c_char_p
+_lib.vks_status_string.argtypes = [C.c_int]
+_lib.vks_last_cuda_error.restype = C.c_char_p
+_lib.vks_version.restype = C.c_int
+_lib.vks_bin_sort_workspace_bytes.restype = C.c_size_t
+_lib.vks_bin_sort_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int32]
+_lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
+_lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 7 + [C.c_size_t, _P]
+_lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 10
+_lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 14
+_lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 16
+for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_bwd", "vks_project_bwd"):
+    getattr(_lib, _f).restype = C.c_int
+
+
+class VksError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        msg = _lib.vks_status_string(status).decode()
+        if status == VKS_ERR_CUDA:
+            msg += ": " + _lib.vks_last_cuda_error().decode()
+        super().__init__(f"{fn}: {msg} (status {status})")
+        self.status = status
+
+
+def make_camera(cam: dict) -> VksCamera:
+    c = VksCamera()
+    R = cam["R"].reshape(-1).tolist() if hasattr(cam["R"], "reshape") else list(cam["R"])
+    c.R[:] = [float(x) for x in R]
+    t = cam["t"].reshape(-1).tolist() if hasattr(cam["t"], "reshape") else list(cam["t"])
+    c.t[:] = [float(x) for x in t]
+    c.fx, c.fy, c.cx, c.cy = (float(cam[k]) for k in ("fx", "fy", "cx", "cy"))
+    c.width, c.height = int(cam["width"]), int(cam["height"])
+    return c
+
+
+def make_config(cfg: dict) -> VksConfig:
+    c = VksConfig()
+    c.sh_degree = int(cfg["sh_degree"])
+    c.sh_coeffs = int(cfg.get("sh_coeffs", (c.sh_degree + 1) ** 2))
+    c.near_plane = float(cfg.get("near_plane", 0.01))
+    c.bg[:] = [float(b) for b in cfg.get("bg", (0.0, 0.0, 0.0))]
+    c.fov_clamp = int(cfg.get("fov_clamp", 1))
+    c.footprint = int(cfg.get("footprint", FOOTPRINT_SUPPORT))
+    c.flags = 0
+    return c
+
+
+def _ptr(t, dtype, name):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: expected a CUDA tensor (libvks takes device pointers)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous tensor")
+    return t.data_ptr() if t.numel() else None
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _check(fn, st):
+    if st != VKS_OK:
+        raise VksError(fn, st)
+
+
+def _cfgcam(cfg, cam):
+    c = cfg if isinstance(cfg, VksConfig) else make_config(cfg)
+    k = cam if isinstance(cam, VksCamera) else make_camera(cam)
+    return c, k
+
+
+f32, i32, u32, u64 = torch.float32, torch.int32, torch.uint32, torch.uint64
+
+
+def vks_project_fwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, means2d, conics, depths,
+                    radii, tiles_touched, colors, opacities, stream=None):
+    c, k = _cfgcam(cfg, cam)
+    n = means.shape[0]
+    st = _lib.vks_project_fwd(C.byref(c), C.byref(k), n, _ptr(means, f32, "means"),
+                              _ptr(log_scales, f32, "log_scales"), _ptr(quats, f32, "quats"),
+                              _ptr(opacity_logits, f32, "opacity_logits"), _ptr(sh, f32, "sh"),
+                              _ptr(means2d, f32, "means2d"), _ptr(conics, f32, "conics"),
+                              _ptr(depths, f32, "depths"), _ptr(radii, i32, "radii"),
+                              _ptr(tiles_touched, i32, "tiles_touched"), _ptr(colors, f32, "colors"),
+                              _ptr(opacities, f32, "opacities"), _stream(stream))
+    _check("vks_project_fwd", st)
+
+
+def vks_bin_sort_workspace_bytes(n, capacity, n_tiles) -> int:
+    return int(_lib.vks_bin_sort_workspace_bytes(n, capacity, n_tiles))
+
+
+def vks_bin_sort(cam, means2d, radii, depths, tiles_touched, offsets, keys, vals, tile_offsets,
+                 workspace, keys_unsorted=None, vals_unsorted=None, stream=None, raise_capacity=True):
+    """Returns M (num_isects).  keys/vals capacity = keys.numel().  On VKS_ERR_CAPACITY returns -M
+    when raise_capacity is False."""
+    k = cam if isinstance(cam, VksCamera) else make_camera(cam)
+    n = means2d.shape[0]
+    m = C.c_int64(0)
+    st = _lib.vks_bin_sort(C.byref(k), n, _ptr(means2d, f32, "means2d"), _ptr(radii, i32, "radii"),
+                           _ptr(depths, f32, "depths"), _ptr(tiles_touched, i32, "tiles_touched"),
+                           _ptr(offsets, u32, "offsets"), keys.numel(), _ptr(keys, u64, "keys"),
+                           _ptr(vals, u32, "vals"), _ptr(keys_unsorted, u64, "keys_unsorted"),
+                           _ptr(vals_unsorted, u32, "vals_unsorted"), _ptr(tile_offsets, u32, "tile_offsets"),
+                           C.byref(m), _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
+                           _stream(stream))
+    if st == VKS_ERR_CAPACITY and not raise_capacity:
+        return -int(m.value)
+    _check("vks_bin_sort", st)
+    return int(m.value)
+
+
+def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, vals, tile_offsets, image, T_final,
+                   n_contrib, stream=None):
+    c, k = _cfgcam(cfg, cam)
+    st = _lib.vks_raster_fwd(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
+                             _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
+                             _ptr(opacities, f32, "opacities"), _ptr(vals, u32, "vals"),
+                             _ptr(tile_offsets, u32, "tile_offsets"), _ptr(image, f32, "image"),
+                             _ptr(T_final, f32, "T_final"), _ptr(n_contrib, i32, "n_contrib"),
+                             _stream(stream))
+    _check("vks_raster_fwd", st)
+
+
+def vks_raster_bwd(cfg, cam, means2d, conics, colors, opacities, vals, tile_offsets, T_final, n_contrib,
+                   dL_dimage, dmeans2d, dconics, dcolors, dopacities, stream=None):
+    c, k = _cfgcam(cfg, cam)
+    st = _lib.vks_raster_bwd(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
+                             _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
+                             _ptr(opacities, f32, "opacities"), _ptr(vals, u32, "vals"),
+                             _ptr(tile_offsets, u32, "tile_offsets"), _ptr(T_final, f32, "T_final"),
+                             _ptr(n_contrib, i32, "n_contrib"), _ptr(dL_dimage, f32, "dL_dimage"),
+                             _ptr(dmeans2d, f32, "dmeans2d"), _ptr(dconics, f32, "dconics"),
+                             _ptr(dcolors, f32, "dcolors"), _ptr(dopacities, f32, "dopacities"),
+                             _stream(stream))
+    _check("vks_raster_bwd", st)
+
+
+def vks_project_bwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, radii, dmeans2d, dconics,
+                    dcolors, dopacities, dmeans, dlog_scales, dquats, dopacity_logits, dsh, stream=None):
+    c, k = _cfgcam(cfg, cam)
+    st = _lib.vks_project_bwd(C.byref(c), C.byref(k), means.shape[0], _ptr(means, f32, "means"),
+                              _ptr(log_scales, f32, "log_scales"), _ptr(quats, f32, "quats"),
+                              _ptr(opacity_logits, f32, "opacity_logits"), _ptr(sh, f32, "sh"),
+                              _ptr(radii, i32, "radii"), _ptr(dmeans2d, f32, "dmeans2d"),
+                              _ptr(dconics, f32, "dconics"), _ptr(dcolors, f32, "dcolors"),
+                              _ptr(dopacities, f32, "dopacities"), _ptr(dmeans, f32, "dmeans"),
+                              _ptr(dlog_scales, f32, "dlog_scales"), _ptr(dquats, f32, "dquats"),
+                              _ptr(dopacity_logits, f32, "dopacity_logits"), _ptr(dsh, f32, "dsh"),
+                              _stream(stream))
+    _check("vks_project_bwd", st)
+
+
+def vks_version() -> int:
+    return int(_lib.vks_version())
+
+
+def exported_symbols():
+    """Names of include/vks.h entry points resolvable in the loaded library."""
+    return [name for name in EXPORTS if hasattr(_lib, name)]

@@ -1,0 +1,163 @@
+// api.cu — the C ABI declared in include/vks.h: argument validation, then one internal launcher
+// per entry point.  No allocation, no global state besides a thread-local error string.
+#include <stdio.h>
+#include <string.h>
+
+#include "vks_common.cuh"
+
+namespace {
+
+thread_local char g_err[256] = "";
+
+int cuda_status(int st) {
+    if (st == VKS_ERR_CUDA) {
+        cudaError_t e = cudaGetLastError();
+        snprintf(g_err, sizeof g_err, "%s", cudaGetErrorString(e));
+    }
+    return st;
+}
+
+bool camera_ok(const vks_camera* c) {
+    if (!c) return false;
+    if (c->width <= 0 || c->height <= 0 || c->width > 65536 || c->height > 65536) return false;
+    if (!(c->fx > 0.0f) || !(c->fy > 0.0f)) return false;
+    return true;
+}
+
+int config_ok(const vks_config* c) {
+    if (!c) return VKS_ERR_INVALID_ARG;
+    if (c->sh_degree < 0 || c->sh_degree > 3) return VKS_ERR_UNSUPPORTED;
+    if (c->sh_coeffs < (c->sh_degree + 1) * (c->sh_degree + 1) || c->sh_coeffs > 64) return VKS_ERR_INVALID_ARG;
+    if (c->footprint != VKS_FOOTPRINT_SUPPORT && c->footprint != VKS_FOOTPRINT_3SIGMA) return VKS_ERR_UNSUPPORTED;
+    if (c->flags != 0) return VKS_ERR_UNSUPPORTED;
+    return VKS_OK;
+}
+
+bool device_present() {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0) {
+        cudaGetLastError();
+        snprintf(g_err, sizeof g_err, "no CUDA device (libvks has no CPU fallback)");
+        return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vks_status_string(int status) {
+    switch (status) {
+        case VKS_OK: return "ok";
+        case VKS_ERR_INVALID_ARG: return "invalid argument";
+        case VKS_ERR_CAPACITY: return "intersection capacity exceeded (regrow keys/vals to num_isects)";
+        case VKS_ERR_WORKSPACE: return "workspace too small";
+        case VKS_ERR_CUDA: return "CUDA error";
+        case VKS_ERR_UNSUPPORTED: return "unsupported configuration";
+        default: return "unknown status";
+    }
+}
+
+int vks_version(void) { return VKS_VERSION; }
+
+const char* vks_last_cuda_error(void) { return g_err; }
+
+int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means,
+                    const float* log_scales, const float* quats, const float* opacity_logits,
+                    const float* sh, float* means2d, float* conics, float* depths, int32_t* radii,
+                    int32_t* tiles_touched, float* colors, float* opacities, vks_stream_t stream) {
+    int st = config_ok(cfg);
+    if (st) return st;
+    if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !means2d || !conics ||
+                  !depths || !radii || !tiles_touched || !colors || !opacities))
+        return VKS_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(quats) & 15) || (reinterpret_cast<uintptr_t>(means2d) & 7) ||
+        (reinterpret_cast<uintptr_t>(radii) & 7))
+        return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_project_fwd(*cfg, *cam, n, means, log_scales, quats, opacity_logits, sh,
+                                               means2d, conics, depths, radii, tiles_touched, colors,
+                                               opacities, (cudaStream_t)stream));
+}
+
+size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles) {
+    if (n < 0 || capacity < 0 || n_tiles <= 0) return 0;
+    return vks::bin_sort_workspace_bytes(n, capacity, n_tiles);
+}
+
+int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
+                 const float* depths, const int32_t* tiles_touched, uint32_t* offsets, int64_t capacity,
+                 uint64_t* keys, uint32_t* vals, uint64_t* keys_unsorted, uint32_t* vals_unsorted,
+                 uint32_t* tile_offsets, int64_t* num_isects, void* workspace, size_t workspace_bytes,
+                 vks_stream_t stream) {
+    if (!camera_ok(cam) || n < 0 || capacity < 0 || !num_isects || !tile_offsets) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means2d || !radii || !depths || !tiles_touched || !offsets)) return VKS_ERR_INVALID_ARG;
+    if (capacity > 0 && (!keys || !vals)) return VKS_ERR_INVALID_ARG;
+    if (!workspace) return VKS_ERR_WORKSPACE;
+    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
+        return VKS_ERR_INVALID_ARG;
+    if (n >= (1ll << 32)) return VKS_ERR_UNSUPPORTED;  // Gaussian ids are u32
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::run_bin_sort(*cam, n, means2d, radii, depths, tiles_touched, offsets, capacity, keys,
+                                         vals, keys_unsorted, vals_unsorted, tile_offsets, num_isects, workspace,
+                                         workspace_bytes, (cudaStream_t)stream));
+}
+
+int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
+                   const float* conics, const float* colors, const float* opacities, const uint32_t* vals,
+                   const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib,
+                   vks_stream_t stream) {
+    int st = config_ok(cfg);
+    if (st) return st;
+    if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
+    if (!tile_offsets || !image || !T_final || !n_contrib) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means2d || !conics || !colors || !opacities)) return VKS_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(means2d) & 7) return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_raster_fwd(*cfg, *cam, n, means2d, conics, colors, opacities, vals,
+                                              tile_offsets, image, T_final, n_contrib, (cudaStream_t)stream));
+}
+
+int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
+                   const float* conics, const float* colors, const float* opacities, const uint32_t* vals,
+                   const uint32_t* tile_offsets, const float* T_final, const int32_t* n_contrib,
+                   const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
+                   float* dopacities, vks_stream_t stream) {
+    int st = config_ok(cfg);
+    if (st) return st;
+    if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
+    if (!tile_offsets || !T_final || !n_contrib || !dL_dimage) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means2d || !conics || !colors || !opacities || !dmeans2d || !dconics || !dcolors ||
+                  !dopacities))
+        return VKS_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(means2d) & 7) return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_raster_bwd(*cfg, *cam, n, means2d, conics, colors, opacities, vals,
+                                              tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics,
+                                              dcolors, dopacities, (cudaStream_t)stream));
+}
+
+int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means,
+                    const float* log_scales, const float* quats, const float* opacity_logits,
+                    const float* sh, const int32_t* radii, const float* dmeans2d, const float* dconics,
+                    const float* dcolors, const float* dopacities, float* dmeans, float* dlog_scales,
+                    float* dquats, float* dopacity_logits, float* dsh, vks_stream_t stream) {
+    int st = config_ok(cfg);
+    if (st) return st;
+    if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !radii || !dmeans2d ||
+                  !dconics || !dcolors || !dopacities || !dmeans || !dlog_scales || !dquats ||
+                  !dopacity_logits || !dsh))
+        return VKS_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(quats) & 15) || (reinterpret_cast<uintptr_t>(dquats) & 15) ||
+        (reinterpret_cast<uintptr_t>(dmeans2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
+        return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_project_bwd(*cfg, *cam, n, means, log_scales, quats, opacity_logits, sh, radii,
+                                               dmeans2d, dconics, dcolors, dopacities, dmeans, dlog_scales,
+                                               dquats, dopacity_logits, dsh, (cudaStream_t)stream));
+}
+
+}  // extern "C"

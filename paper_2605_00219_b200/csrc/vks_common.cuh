@@ -1,0 +1,79 @@
+// vks_common.cuh — shared device helpers of the CUDA path (never shared with oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vks.h"
+
+#define VKS_FULL_MASK 0xffffffffu
+
+namespace vks {
+
+constexpr int kTile = 16;
+
+// Status set by the API layer; kernels never touch host state.
+struct LaunchCheck {
+    static int check() {
+        cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? VKS_OK : VKS_ERR_CUDA;
+    }
+};
+
+__host__ __device__ inline int tiles_x(const vks_camera& c) { return (c.width + kTile - 1) / kTile; }
+__host__ __device__ inline int tiles_y(const vks_camera& c) { return (c.height + kTile - 1) / kTile; }
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// relaxed (volatile) 32/64-bit global accesses for decoupled look-back
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+}  // namespace vks
+
+// internal launchers (implemented in the .cu files, called by api.cu)
+namespace vks {
+int launch_project_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means,
+                       const float* log_scales, const float* quats, const float* opacity_logits,
+                       const float* sh, float* means2d, float* conics, float* depths, int32_t* radii,
+                       int32_t* tiles_touched, float* colors, float* opacities, cudaStream_t s);
+int launch_project_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means,
+                       const float* log_scales, const float* quats, const float* opacity_logits,
+                       const float* sh, const int32_t* radii, const float* dmeans2d,
+                       const float* dconics, const float* dcolors, const float* dopacities,
+                       float* dmeans, float* dlog_scales, float* dquats, float* dopacity_logits,
+                       float* dsh, cudaStream_t s);
+size_t bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles);
+int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const int32_t* radii,
+                 const float* depths, const int32_t* tiles_touched, uint32_t* offsets,
+                 int64_t capacity, uint64_t* keys, uint32_t* vals, uint64_t* keys_unsorted,
+                 uint32_t* vals_unsorted, uint32_t* tile_offsets, int64_t* num_isects,
+                 void* workspace, size_t workspace_bytes, cudaStream_t s);
+int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
+                      const float* conics, const float* colors, const float* opacities,
+                      const uint32_t* vals, const uint32_t* tile_offsets, float* image,
+                      float* T_final, int32_t* n_contrib, cudaStream_t s);
+int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
+                      const float* conics, const float* colors, const float* opacities,
+                      const uint32_t* vals, const uint32_t* tile_offsets, const float* T_final,
+                      const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
+                      float* dconics, float* dcolors, float* dopacities, cudaStream_t s);
+}  // namespace vks

@@ -1,0 +1,114 @@
+"""Per-view orchestration of the five C-ABI calls (buffer management only; no arithmetic).
+
+`GaussianParams` holds the device-resident parameters and their gradient buffer (one flat fp32
+buffer of 59 floats per Gaussian at SH degree 3, sliced into the five gradient views, so the
+multi-GPU allreduce is a single call).  `ViewRenderer` owns the per-view scratch buffers (projection
+outputs, binning, image/aux, 2D gradients) sized for one camera resolution and regrows the
+intersection capacity on VKS_ERR_CAPACITY.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _vks as V
+
+
+@dataclass
+class GaussianParams:
+    means: torch.Tensor
+    log_scales: torch.Tensor
+    quats: torch.Tensor
+    opacity_logits: torch.Tensor
+    sh: torch.Tensor
+    grad_flat: torch.Tensor
+
+    @property
+    def n(self) -> int:
+        return self.means.shape[0]
+
+    @staticmethod
+    def layout(n: int, K: int):
+        """(offset, numel) of each gradient group inside grad_flat; groups start 256-byte aligned."""
+        sizes = [3 * n, 3 * n, 4 * n, n, 3 * K * n]
+        offs, o = [], 0
+        for s in sizes:
+            offs.append((o, s))
+            o += (s + 63) // 64 * 64
+        return offs, o
+
+    @staticmethod
+    def from_host(scene: dict, device="cuda") -> "GaussianParams":
+        t = {k: torch.as_tensor(v).to(device=device, dtype=torch.float32).contiguous() for k, v in scene.items()}
+        n, K = t["means"].shape[0], t["sh"].shape[1]
+        _, total = GaussianParams.layout(n, K)
+        g = torch.zeros(total, dtype=torch.float32, device=device)
+        return GaussianParams(t["means"], t["log_scales"], t["quats"], t["opacity_logits"], t["sh"], g)
+
+    def grads(self) -> dict:
+        """Views into grad_flat: [dmeans | dlog_scales | dquats | dlogit | dsh] (group-major)."""
+        n, K = self.n, self.sh.shape[1]
+        offs, _ = GaussianParams.layout(n, K)
+        shapes = [(n, 3), (n, 3), (n, 4), (n,), (n, K, 3)]
+        names = ["dmeans", "dlog_scales", "dquats", "dopacity_logits", "dsh"]
+        return {nm: self.grad_flat[o:o + s].view(*sh) for nm, (o, s), sh in zip(names, offs, shapes)}
+
+
+class ViewRenderer:
+    """Scratch buffers for one resolution; `forward` then `backward` run one view's hot path."""
+
+    def __init__(self, n: int, width: int, height: int, device="cuda", capacity: int | None = None):
+        self.device = device
+        self.n, self.W, self.H = n, width, height
+        self.TX, self.TY = (width + 15) // 16, (height + 15) // 16
+        self.n_tiles = self.TX * self.TY
+        e = lambda *s, dt=torch.float32: torch.empty(*s, dtype=dt, device=device)
+        self.means2d, self.conics, self.depths = e(n, 2), e(n, 3), e(n)
+        self.radii, self.tiles = e(n, 2, dt=torch.int32), e(n, dt=torch.int32)
+        self.colors, self.opacities = e(n, 3), e(n)
+        self.offsets = e(n, dt=torch.uint32)
+        self.tile_offsets = e(self.n_tiles + 1, dt=torch.uint32)
+        self.image, self.T_final = e(height, width, 3), e(height, width)
+        self.n_contrib = e(height, width, dt=torch.int32)
+        self.g2d = torch.zeros(n * 9, dtype=torch.float32, device=device)
+        self.dmeans2d = self.g2d[: 2 * n].view(n, 2)
+        self.dconics = self.g2d[2 * n: 5 * n].view(n, 3)
+        self.dcolors = self.g2d[5 * n: 8 * n].view(n, 3)
+        self.dopacities = self.g2d[8 * n:]
+        self.capacity = 0
+        self._alloc_capacity(capacity if capacity is not None else max(1024, 4 * n))
+        self.num_isects = 0
+
+    def _alloc_capacity(self, cap: int):
+        self.capacity = int(cap)
+        self.keys = torch.empty(self.capacity, dtype=torch.uint64, device=self.device)
+        self.vals = torch.empty(self.capacity, dtype=torch.uint32, device=self.device)
+        ws = V.vks_bin_sort_workspace_bytes(self.n, self.capacity, self.n_tiles)
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+
+    def forward(self, cfg, cam, P: GaussianParams, keys_unsorted=None, vals_unsorted=None):
+        V.vks_project_fwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.means2d,
+                          self.conics, self.depths, self.radii, self.tiles, self.colors, self.opacities)
+        while True:
+            m = V.vks_bin_sort(cam, self.means2d, self.radii, self.depths, self.tiles, self.offsets, self.keys,
+                               self.vals, self.tile_offsets, self.workspace, keys_unsorted, vals_unsorted,
+                               raise_capacity=False)
+            if m >= 0:
+                break
+            self._alloc_capacity(int(-m * 1.25) + 1024)
+        self.num_isects = m
+        V.vks_raster_fwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.vals,
+                         self.tile_offsets, self.image, self.T_final, self.n_contrib)
+        return self.image
+
+    def backward(self, cfg, cam, P: GaussianParams, dL_dimage: torch.Tensor, zero_2d: bool = True):
+        if zero_2d:
+            self.g2d.zero_()
+        V.vks_raster_bwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.vals,
+                         self.tile_offsets, self.T_final, self.n_contrib, dL_dimage, self.dmeans2d, self.dconics,
+                         self.dcolors, self.dopacities)
+        g = P.grads()
+        V.vks_project_bwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.radii,
+                          self.dmeans2d, self.dconics, self.dcolors, self.dopacities, g["dmeans"],
+                          g["dlog_scales"], g["dquats"], g["dopacity_logits"], g["dsh"])

@@ -122,8 +122,12 @@ def make_scene(n: int, kind: str = "outdoor", seed: int = 0, sh_degree: int = 3)
     quats /= np.linalg.norm(quats, axis=1, keepdims=True)
     opacity_logits = 2.0 * rng.standard_normal(n)
     K = (sh_degree + 1) ** 2
-    sh = 0.1 * rng.standard_normal((n, K, 3))
-    sh[:, 0, :] = 0.6 * rng.standard_normal((n, 3))
+    # f0 ~ N(0, 0.6^2); f1..f15 uniform with std 0.1 (a uniform draw is 3x cheaper than a normal
+    # one at 5.8M x 45 samples and only shapes the view-dependent colour)
+    sh = rng.random((n, K, 3), dtype=np.float32)
+    sh -= np.float32(0.5)
+    sh *= np.float32(0.2 * math.sqrt(3.0))
+    sh[:, 0, :] = 0.6 * rng.standard_normal((n, 3), dtype=np.float32)
     f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
     return dict(means=f32(means), log_scales=f32(log_scales), quats=f32(quats),
                 opacity_logits=f32(opacity_logits), sh=f32(sh))

@@ -1,0 +1,97 @@
+"""Helpers for the -m gpu parity tests: run the CUDA path through the C ABI (via the thin binding)
+and compare with the CPU oracle under the protocol of DESIGN.md §7."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import synth
+
+
+def to_np(t: torch.Tensor) -> np.ndarray:
+    if t.dtype == torch.uint32:
+        return t.view(torch.int32).cpu().numpy().view(np.uint32)
+    if t.dtype == torch.uint64:
+        return t.view(torch.int64).cpu().numpy().view(np.uint64)
+    return t.detach().cpu().numpy()
+
+
+def run_gpu(scene, cam, cfg, dL=None, capacity=None, debug_unsorted=False):
+    """One view through the CUDA path.  Returns numpy copies of every stage output."""
+    import paper_2605_00219_b200 as P
+    params = P.GaussianParams.from_host(scene)
+    n = params.n
+    r = P.ViewRenderer(n, cam["width"], cam["height"], capacity=capacity)
+    ku = vu = None
+    r.forward(cfg, cam, params)  # may regrow the capacity
+    if debug_unsorted:  # debug outputs must hold `capacity` entries (include/vks.h)
+        ku = torch.empty(r.capacity, dtype=torch.uint64, device="cuda")
+        vu = torch.empty(r.capacity, dtype=torch.uint32, device="cuda")
+        r.forward(cfg, cam, params, ku, vu)
+    out = dict(means2d=r.means2d, conics=r.conics, depths=r.depths, radii=r.radii, tiles_touched=r.tiles,
+               colors=r.colors, opacities=r.opacities, offsets=r.offsets, tile_offsets=r.tile_offsets,
+               image=r.image, T_final=r.T_final, n_contrib=r.n_contrib)
+    m = r.num_isects
+    res = {k: to_np(v) for k, v in out.items()}
+    res["num_isects"] = m
+    res["keys"] = to_np(r.keys[:m])
+    res["vals"] = to_np(r.vals[:m])
+    if debug_unsorted:
+        res["keys_unsorted"] = to_np(ku[:m])
+        res["vals_unsorted"] = to_np(vu[:m])
+    if dL is not None:
+        params.grad_flat.zero_()
+        r.backward(cfg, cam, params, torch.as_tensor(dL).cuda().contiguous())
+        for k, v in dict(dmeans2d=r.dmeans2d, dconics=r.dconics, dcolors=r.dcolors,
+                         dopacities=r.dopacities).items():
+            res[k] = to_np(v)
+        for k, v in params.grads().items():
+            res[k] = to_np(v)
+    torch.cuda.synchronize()
+    return res
+
+
+def last_id_from_ncontrib(g, cam):
+    """Map the GPU's n_contrib (1-based position in the tile list) to a Gaussian id (-1 = none)."""
+    H, W = cam["height"], cam["width"]
+    TX = (W + 15) // 16
+    ys, xs = np.mgrid[0:H, 0:W]
+    tile = (ys // 16) * TX + xs // 16
+    nc = g["n_contrib"].astype(np.int64)
+    pos = g["tile_offsets"][tile].astype(np.int64) + nc - 1
+    out = np.full((H, W), -1, np.int64)
+    ok = nc > 0
+    out[ok] = g["vals"][pos[ok]]
+    return out
+
+
+def grad_rule(g, ref, mass=None, rel=1e-3, abs_floor=1e-6, cond=1e-5):
+    """Per-element rule: |g - ref| <= max(rel |ref|, abs_floor).  Elements that fail
+    only because of cancellation (|g - ref| <= cond * mass) are counted as condition-limited."""
+    g = np.asarray(g, np.float64).reshape(-1)
+    ref = np.asarray(ref, np.float64).reshape(-1)
+    err = np.abs(g - ref)
+    ok = err <= np.maximum(rel * np.abs(ref), abs_floor)
+    cl = np.zeros_like(ok)
+    if mass is not None:
+        m = np.asarray(mass, np.float64).reshape(-1)
+        cl = (~ok) & (err <= cond * m)
+    bad = (~ok) & (~cl)
+    return dict(n=int(g.size), fail=int(bad.sum()), condition_limited=int(cl.sum()),
+                worst=float((err / np.maximum(rel * np.abs(ref), abs_floor)).max()) if g.size else 0.0,
+                bad_idx=np.nonzero(bad)[0][:10])
+
+
+def sampled_rows(cam, every=8):
+    """Row mask: every `every`-th tile row (16 pixel rows each) — SURVEY §8c.9 sampled-rows mode."""
+    H = cam["height"]
+    ty = np.arange(H) // 16
+    return (ty % every == 0).astype(np.uint8)
+
+
+def scene_for(name, view=0):
+    c = synth.CONFIGS[name]
+    scene = synth.make_scene(c.n, c.kind, c.seed)
+    cam = synth.ring_cameras(c.width, c.height, c.kind, 8)[view]
+    dL = synth.upstream_grad(c.height, c.width, c.seed + 1000)
+    return scene, cam, dL

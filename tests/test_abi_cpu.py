@@ -1,0 +1,99 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every entry point include/vks.h declares,
+validates arguments synchronously, and has no CPU fallback (no compute without a GPU)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "vks.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(vks_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2605_00219_b200 as P
+    lib = C.CDLL(os.path.join(ROOT, "paper_2605_00219_b200", "libvks.so"))
+    syms = header_symbols()
+    assert len(syms) >= 9
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(P.EXPORTS) == set(syms)
+    assert P.vks_version() == 1
+
+
+def test_cuda_objects_are_sm100a():
+    """The library carries sm_100a SASS (cuobjdump lists the ELF arch)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--list-elf", os.path.join(ROOT, "paper_2605_00219_b200", "libvks.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _lib():
+    from paper_2605_00219_b200 import _vks
+    return _vks._lib, _vks
+
+
+def test_status_strings_and_workspace():
+    lib, V = _lib()
+    for st in range(6):
+        assert lib.vks_status_string(st)
+    assert V.vks_bin_sort_workspace_bytes(1000, 5000, 16) > 5000 * 12
+    assert V.vks_bin_sort_workspace_bytes(-1, 10, 16) == 0
+    assert V.vks_bin_sort_workspace_bytes(10, 10, 0) == 0
+
+
+def test_argument_validation_is_synchronous():
+    lib, V = _lib()
+    cfg = V.make_config(dict(sh_degree=3, sh_coeffs=16))
+    cam = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
+                             width=64, height=64))
+    # null camera / negative n / bad degree / bad footprint -> errors before any CUDA call
+    assert lib.vks_project_fwd(C.byref(cfg), None, 0, *([None] * 13)) == V.VKS_ERR_INVALID_ARG
+    assert lib.vks_project_fwd(C.byref(cfg), C.byref(cam), -1, *([None] * 13)) == V.VKS_ERR_INVALID_ARG
+    bad = V.make_config(dict(sh_degree=4, sh_coeffs=25))
+    assert lib.vks_project_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 13)) == V.VKS_ERR_UNSUPPORTED
+    bad = V.make_config(dict(sh_degree=3, sh_coeffs=9))
+    assert lib.vks_project_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 13)) == V.VKS_ERR_INVALID_ARG
+    bad = V.make_config(dict(sh_degree=3, sh_coeffs=16, footprint=7))
+    assert lib.vks_raster_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 10)) == V.VKS_ERR_UNSUPPORTED
+    wide = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
+                              width=70000, height=64))
+    assert lib.vks_raster_bwd(C.byref(cfg), C.byref(wide), 0, *([None] * 14)) == V.VKS_ERR_INVALID_ARG
+    m = C.c_int64(0)
+    assert lib.vks_bin_sort(C.byref(cam), 5, *([None] * 5), 0, *([None] * 4), None, C.byref(m), None, 0,
+                            None) == V.VKS_ERR_INVALID_ARG
+
+
+def test_no_cpu_fallback():
+    """Without a CUDA device a well-formed call reports VKS_ERR_CUDA instead of computing on the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    lib, V = _lib()
+    cfg = V.make_config(dict(sh_degree=3, sh_coeffs=16))
+    cam = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
+                             width=64, height=64))
+    st = lib.vks_raster_fwd(C.byref(cfg), C.byref(cam), 0, None, None, None, None, None, C.c_void_p(16),
+                            C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), None)
+    assert st == V.VKS_ERR_CUDA
+    assert b"no CUDA device" in lib.vks_last_cuda_error()
+
+
+def test_binding_rejects_host_tensors():
+    import torch
+    import paper_2605_00219_b200 as P
+    x = torch.zeros(4, 3)
+    with pytest.raises((ValueError, TypeError)):
+        P.vks_project_fwd(dict(sh_degree=0), dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=1, fy=1,
+                                                   cx=0, cy=0, width=4, height=4),
+                          x, x, torch.zeros(4, 4), torch.zeros(4), torch.zeros(4, 1, 3), *([x] * 7))

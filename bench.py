@@ -124,6 +124,7 @@ def run_ours(args):
 
     import paper_2605_00219_b200 as P
     import synth
+    from paper_2605_00219_b200.shard import allreduce_grads
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -149,6 +150,7 @@ def run_ours(args):
         rend.forward(cfg, cams[v], params)
     rend._alloc_capacity(int(rend.capacity * 1.1))
     stream = torch.cuda.current_stream()
+    cfg_ow = dict(cfg, flags=P.FLAG_GRAD_OVERWRITE)
     stages = ["project_fwd", "bin_sort", "raster_fwd", "raster_bwd", "project_bwd", "allreduce"]
 
     def step(s, ev=None):
@@ -164,23 +166,22 @@ def run_ours(args):
                                rend.vals, rend.tile_offsets, rend.workspace)
             rend.num_isects = m
             if ev is not None: ev[2].record(stream)
-            P.vks_raster_fwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.vals,
+            P.vks_raster_fwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals,
                              rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib)
             if ev is not None: ev[3].record(stream)
             rend.g2d.zero_()
-            P.vks_raster_bwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.vals,
+            P.vks_raster_bwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals,
                              rend.tile_offsets, rend.T_final, rend.n_contrib, dLs[v], rend.dmeans2d, rend.dconics,
                              rend.dcolors, rend.dopacities)
             if ev is not None: ev[4].record(stream)
             g = params.grads()
-            P.vks_project_bwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
+            # first view of the step overwrites the gradient buffer (no memset), later ones accumulate
+            P.vks_project_bwd(cfg_ow if j == 0 else cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
                               params.sh, rend.radii, rend.dmeans2d, rend.dconics, rend.dcolors, rend.dopacities,
                               g["dmeans"], g["dlog_scales"], g["dquats"], g["dopacity_logits"], g["dsh"])
             if ev is not None: ev[5].record(stream)
-        if world > 1:
-            dist.all_reduce(params.grad_flat)
+        allreduce_grads(params.grad_flat)  # row a9: the only exchange (no-op at N = 1)
         if ev is not None: ev[6].record(stream)
-        params.grad_flat.zero_()  # next batch of views accumulates from zero
         return m
 
     for s in range(args.warmup):
@@ -299,6 +300,7 @@ def run_e2e(args, P, params, rend, cams, my_views, cfg, c, world):
     import torch.distributed as dist
 
     import synth
+    from paper_2605_00219_b200.shard import allreduce_grads
     stream = torch.cuda.current_stream()
     host_dL = {v: torch.from_numpy(synth.upstream_grad(c.height, c.width, c.seed + 1000 + v)).pin_memory()
                for v in set(my_views)}
@@ -309,11 +311,9 @@ def run_e2e(args, P, params, rend, cams, my_views, cfg, c, world):
         v = my_views[s % len(my_views)]
         dev_dL.copy_(host_dL[v], non_blocking=True)
         rend.forward(cfg, cams[v], params)
-        rend.backward(cfg, cams[v], params, dev_dL)
-        if world > 1:
-            dist.all_reduce(params.grad_flat)
+        rend.backward(cfg, cams[v], params, dev_dL, accumulate=False)
+        allreduce_grads(params.grad_flat)
         host_img.copy_(rend.image, non_blocking=True)
-        params.grad_flat.zero_()
 
     for s in range(min(args.warmup, 3)):
         step(s)

@@ -70,8 +70,12 @@ typedef struct {
     int32_t fov_clamp;  /* 1 = clamp tx/tz, ty/tz to 1.3x the image half-FOV inside J (gsplat/3DGS) */
     int32_t footprint;  /* VKS_FOOTPRINT_SUPPORT (default): exact alpha>=1/255 support bbox;
                            VKS_FOOTPRINT_3SIGMA: ceil(3 sqrt(lambda_max)) square */
-    uint32_t flags;     /* reserved, must be 0 */
+    uint32_t flags;     /* VKS_FLAG_* bits, 0 = defaults */
 } vks_config;
+
+/* vks_project_bwd WRITES its parameter gradients instead of accumulating them, and writes zeros
+ * to the rows of Gaussians with radii == 0 (first view of a batch: no memset of the buffer). */
+#define VKS_FLAG_GRAD_OVERWRITE 1u
 
 enum {
     VKS_OK = 0,
@@ -145,12 +149,15 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
  *   T *= 1 - alpha;  stop once T < 1e-4.   out = C + T bg.
  *   -> image [H,W,3], T_final [H,W], n_contrib [H,W] int32 (1-based position,
  *      within the tile's list, of the last composited entry; 0 = none).
- * vals/tile_offsets as produced by vks_bin_sort.
+ * means2d/conics/colors/opacities/radii as produced by vks_project_fwd, vals/tile_offsets as
+ * produced by vks_bin_sort.  In support-footprint mode radii bound each Gaussian's alpha >= 1/255
+ * support, which the kernel uses to skip (warp, Gaussian) pairs that cannot composite.
  */
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    const float* means2d, const float* conics, const float* colors,
-                   const float* opacities, const uint32_t* vals, const uint32_t* tile_offsets,
-                   float* image, float* T_final, int32_t* n_contrib, vks_stream_t stream);
+                   const float* opacities, const int32_t* radii, const uint32_t* vals,
+                   const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib,
+                   vks_stream_t stream);
 
 /*
  * vks_raster_bwd — "Rasterization Backward".
@@ -161,7 +168,8 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
  */
 int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    const float* means2d, const float* conics, const float* colors,
-                   const float* opacities, const uint32_t* vals, const uint32_t* tile_offsets,
+                   const float* opacities, const int32_t* radii, const uint32_t* vals,
+                   const uint32_t* tile_offsets,
                    const float* T_final, const int32_t* n_contrib, const float* dL_dimage,
                    float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
                    vks_stream_t stream);
@@ -173,7 +181,7 @@ int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
  * (+0.3 passes the gradient), exact FOV-clamp derivative, quaternion
  * normalisation, exp / sigmoid activations, SH colour (clamped channels give 0).
  *   -> dmeans [n,3], dlog_scales [n,3], dquats [n,4], dopacity_logits [n],
- *      dsh [n, sh_coeffs, 3]   (+=)
+ *      dsh [n, sh_coeffs, 3]   (+=; with VKS_FLAG_GRAD_OVERWRITE: =, and zero rows for radii == 0)
  */
 int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                     const float* means, const float* log_scales, const float* quats,

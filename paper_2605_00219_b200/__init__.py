@@ -3,7 +3,7 @@ compositing and their backward as hand-written sm_100a CUDA kernels behind the C
 include/vks.h.  This package is the thin Python binding (`_vks`, same names as the C entry
 points) plus buffer orchestration (`pipeline`).  There is no CPU fallback: importing fails
 loudly when libvks.so is missing."""
-from ._vks import (EXPORTS, FOOTPRINT_3SIGMA, FOOTPRINT_SUPPORT, VksError, exported_symbols,  # noqa: F401
+from ._vks import (EXPORTS, FLAG_GRAD_OVERWRITE, FOOTPRINT_3SIGMA, FOOTPRINT_SUPPORT, VksError, exported_symbols,  # noqa: F401
                    make_camera, make_config, vks_bin_sort, vks_bin_sort_workspace_bytes, vks_project_bwd,
                    vks_project_fwd, vks_raster_bwd, vks_raster_fwd, vks_version)
 from .pipeline import GaussianParams, ViewRenderer  # noqa: F401

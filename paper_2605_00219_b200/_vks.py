@@ -22,6 +22,7 @@ _lib = C.CDLL(LIB_PATH)
 
 VKS_OK, VKS_ERR_INVALID_ARG, VKS_ERR_CAPACITY, VKS_ERR_WORKSPACE, VKS_ERR_CUDA, VKS_ERR_UNSUPPORTED = range(6)
 FOOTPRINT_SUPPORT, FOOTPRINT_3SIGMA = 0, 1
+FLAG_GRAD_OVERWRITE = 1
 
 EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_project_fwd",
            "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_bwd",
@@ -48,8 +49,8 @@ _lib.vks_bin_sort_workspace_bytes.restype = C.c_size_t
 _lib.vks_bin_sort_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int32]
 _lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
 _lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 7 + [C.c_size_t, _P]
-_lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 10
-_lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 14
+_lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 11
+_lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 15
 _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 16
 for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_bwd", "vks_project_bwd"):
     getattr(_lib, _f).restype = C.c_int
@@ -83,7 +84,7 @@ def make_config(cfg: dict) -> VksConfig:
     c.bg[:] = [float(b) for b in cfg.get("bg", (0.0, 0.0, 0.0))]
     c.fov_clamp = int(cfg.get("fov_clamp", 1))
     c.footprint = int(cfg.get("footprint", FOOTPRINT_SUPPORT))
-    c.flags = 0
+    c.flags = int(cfg.get("flags", 0))
     return c
 
 
@@ -159,24 +160,24 @@ def vks_bin_sort(cam, means2d, radii, depths, tiles_touched, offsets, keys, vals
     return int(m.value)
 
 
-def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, vals, tile_offsets, image, T_final,
+def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final,
                    n_contrib, stream=None):
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_raster_fwd(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                              _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
-                             _ptr(opacities, f32, "opacities"), _ptr(vals, u32, "vals"),
+                             _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
                              _ptr(tile_offsets, u32, "tile_offsets"), _ptr(image, f32, "image"),
                              _ptr(T_final, f32, "T_final"), _ptr(n_contrib, i32, "n_contrib"),
                              _stream(stream))
     _check("vks_raster_fwd", st)
 
 
-def vks_raster_bwd(cfg, cam, means2d, conics, colors, opacities, vals, tile_offsets, T_final, n_contrib,
+def vks_raster_bwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib,
                    dL_dimage, dmeans2d, dconics, dcolors, dopacities, stream=None):
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_raster_bwd(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                              _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
-                             _ptr(opacities, f32, "opacities"), _ptr(vals, u32, "vals"),
+                             _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
                              _ptr(tile_offsets, u32, "tile_offsets"), _ptr(T_final, f32, "T_final"),
                              _ptr(n_contrib, i32, "n_contrib"), _ptr(dL_dimage, f32, "dL_dimage"),
                              _ptr(dmeans2d, f32, "dmeans2d"), _ptr(dconics, f32, "dconics"),

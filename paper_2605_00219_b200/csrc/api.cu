@@ -29,7 +29,7 @@ int config_ok(const vks_config* c) {
     if (c->sh_degree < 0 || c->sh_degree > 3) return VKS_ERR_UNSUPPORTED;
     if (c->sh_coeffs < (c->sh_degree + 1) * (c->sh_degree + 1) || c->sh_coeffs > 64) return VKS_ERR_INVALID_ARG;
     if (c->footprint != VKS_FOOTPRINT_SUPPORT && c->footprint != VKS_FOOTPRINT_3SIGMA) return VKS_ERR_UNSUPPORTED;
-    if (c->flags != 0) return VKS_ERR_UNSUPPORTED;
+    if (c->flags & ~VKS_FLAG_GRAD_OVERWRITE) return VKS_ERR_UNSUPPORTED;
     return VKS_OK;
 }
 
@@ -106,22 +106,25 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
 }
 
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
-                   const float* conics, const float* colors, const float* opacities, const uint32_t* vals,
+                   const float* conics, const float* colors, const float* opacities, const int32_t* radii,
+                   const uint32_t* vals,
                    const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib,
                    vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
     if (!tile_offsets || !image || !T_final || !n_contrib) return VKS_ERR_INVALID_ARG;
-    if (n > 0 && (!means2d || !conics || !colors || !opacities)) return VKS_ERR_INVALID_ARG;
-    if (reinterpret_cast<uintptr_t>(means2d) & 7) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means2d || !conics || !colors || !opacities || !radii)) return VKS_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
+        return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
-    return cuda_status(vks::launch_raster_fwd(*cfg, *cam, n, means2d, conics, colors, opacities, vals,
+    return cuda_status(vks::launch_raster_fwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
                                               tile_offsets, image, T_final, n_contrib, (cudaStream_t)stream));
 }
 
 int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
-                   const float* conics, const float* colors, const float* opacities, const uint32_t* vals,
+                   const float* conics, const float* colors, const float* opacities, const int32_t* radii,
+                   const uint32_t* vals,
                    const uint32_t* tile_offsets, const float* T_final, const int32_t* n_contrib,
                    const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                    float* dopacities, vks_stream_t stream) {
@@ -129,12 +132,13 @@ int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
     if (st) return st;
     if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
     if (!tile_offsets || !T_final || !n_contrib || !dL_dimage) return VKS_ERR_INVALID_ARG;
-    if (n > 0 && (!means2d || !conics || !colors || !opacities || !dmeans2d || !dconics || !dcolors ||
-                  !dopacities))
+    if (n > 0 && (!means2d || !conics || !colors || !opacities || !radii || !dmeans2d || !dconics ||
+                  !dcolors || !dopacities))
         return VKS_ERR_INVALID_ARG;
-    if (reinterpret_cast<uintptr_t>(means2d) & 7) return VKS_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
+        return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
-    return cuda_status(vks::launch_raster_bwd(*cfg, *cam, n, means2d, conics, colors, opacities, vals,
+    return cuda_status(vks::launch_raster_bwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
                                               tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics,
                                               dcolors, dopacities, (cudaStream_t)stream));
 }

@@ -17,6 +17,8 @@
 //                     decoupled look-back across dynamically numbered tiles per digit, local
 //                     reordering in shared memory so global stores are digit-contiguous runs.
 // The binning TU is compiled with -fmad=false (the rect recomputation must equal projection's).
+#include <algorithm>
+
 #include "vks_common.cuh"
 
 namespace vks {
@@ -35,6 +37,7 @@ constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
 constexpr int kMaxPasses = 8;
 constexpr int kDepthPasses = 4;
+constexpr int kLookbackChunk = 8;
 
 constexpr u64 kScanFlagAgg = 1ull << 62;
 constexpr u64 kScanFlagInc = 2ull << 62;
@@ -163,59 +166,75 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const int* __restric
 
 // ------------------------------------------------------------------------------------------
 // 2. key generation (+ depth-digit histograms, tile-rect difference array)
-__global__ void __launch_bounds__(256) keys_kernel(vks_camera cam, int64_t n, const float2* __restrict__ means2d,
-                                                  const int2* __restrict__ radii, const float* __restrict__ depths,
-                                                  const int* __restrict__ tiles, const u32* __restrict__ offsets,
-                                                  u64* __restrict__ keys, u32* __restrict__ vals,
-                                                  u32* __restrict__ hist, int* __restrict__ diff) {
+// Persistent grid (a few blocks per SM); each warp takes 32 consecutive Gaussians at a time.  The
+// 2-D difference array of the tile rects is accumulated per block in shared memory and flushed
+// once per block (non-zero cells only), so hot tiles near the image centre see ~#blocks global
+// atomics instead of ~#Gaussians.  Grids too large for shared memory use global atomics.
+constexpr int kKeysThreads = 512;
+constexpr int kKeysWarps = kKeysThreads / 32;
+constexpr int kKeysSmemDiffMax = 160 * 1024 / 4;  // cells
+
+template <bool SMEM_DIFF>
+__global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int64_t n, const float2* __restrict__ means2d,
+                                                           const int2* __restrict__ radii, const float* __restrict__ depths,
+                                                           const int* __restrict__ tiles, const u32* __restrict__ offsets,
+                                                           u64* __restrict__ keys, u32* __restrict__ vals,
+                                                           u32* __restrict__ hist, int* __restrict__ diff) {
+    extern __shared__ int s_diff[];
     __shared__ u32 s_hist[kDepthPasses][256];
-    __shared__ int s_incl[8][32];
-    __shared__ int s_x0[8][32], s_y0[8][32], s_w[8][32];
-    __shared__ u32 s_db[8][32];
+    __shared__ int s_incl[kKeysWarps][32];
+    __shared__ int s_x0[kKeysWarps][32], s_y0[kKeysWarps][32], s_w[kKeysWarps][32];
+    __shared__ u32 s_db[kKeysWarps][32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int j = tid; j < kDepthPasses * 256; j += 256) (&s_hist[0][0])[j] = 0;
-    __syncthreads();
     const int TX = tiles_x(cam), TY = tiles_y(cam);
-    const int64_t g0 = (int64_t)blockIdx.x * 256 + warp * 32;
-    const int64_t g = g0 + lane;
-    int cnt = 0, x0 = 0, y0 = 0, w = 1;
-    u32 db = 0;
-    if (g < n) {
-        cnt = __ldg(tiles + g);
-        if (cnt > 0) {
-            const float2 m = __ldg(means2d + g);
-            const int2 r = __ldg(radii + g);
-            const float rx = (float)r.x, ry = (float)r.y;
-            x0 = (int)fminf(fmaxf(floorf((m.x - rx) * 0.0625f), 0.0f), (float)TX);
-            const int x1 = (int)fminf(fmaxf(ceilf((m.x + rx) * 0.0625f), 0.0f), (float)TX);
-            y0 = (int)fminf(fmaxf(floorf((m.y - ry) * 0.0625f), 0.0f), (float)TY);
-            const int y1 = (int)fminf(fmaxf(ceilf((m.y + ry) * 0.0625f), 0.0f), (float)TY);
-            w = x1 - x0;
-            db = __float_as_uint(__ldg(depths + g));
+    const int W1 = TX + 1;
+    const int cells = W1 * (TY + 1);
+    for (int j = tid; j < kDepthPasses * 256; j += kKeysThreads) (&s_hist[0][0])[j] = 0;
+    if (SMEM_DIFF)
+        for (int j = tid; j < cells; j += kKeysThreads) s_diff[j] = 0;
+    __syncthreads();
+    int* dd = SMEM_DIFF ? s_diff : diff;
+    const int64_t stride = (int64_t)gridDim.x * kKeysWarps * 32;
+    for (int64_t g0 = ((int64_t)blockIdx.x * kKeysWarps + warp) * 32; g0 < n; g0 += stride) {
+        const int64_t g = g0 + lane;
+        int cnt = 0, x0 = 0, y0 = 0, w = 1;
+        u32 db = 0;
+        if (g < n) {
+            cnt = __ldg(tiles + g);
+            if (cnt > 0) {
+                const float2 m = __ldg(means2d + g);
+                const int2 r = __ldg(radii + g);
+                const float rx = (float)r.x, ry = (float)r.y;
+                x0 = (int)fminf(fmaxf(floorf((m.x - rx) * 0.0625f), 0.0f), (float)TX);
+                const int x1 = (int)fminf(fmaxf(ceilf((m.x + rx) * 0.0625f), 0.0f), (float)TX);
+                y0 = (int)fminf(fmaxf(floorf((m.y - ry) * 0.0625f), 0.0f), (float)TY);
+                const int y1 = (int)fminf(fmaxf(ceilf((m.y + ry) * 0.0625f), 0.0f), (float)TY);
+                w = x1 - x0;
+                db = __float_as_uint(__ldg(depths + g));
 #pragma unroll
-            for (int p = 0; p < kDepthPasses; p++) atomicAdd(&s_hist[p][(db >> (8 * p)) & 255u], (u32)cnt);
-            const int W1 = TX + 1;
-            atomicAdd(diff + y0 * W1 + x0, 1);
-            atomicAdd(diff + y0 * W1 + x1, -1);
-            atomicAdd(diff + y1 * W1 + x0, -1);
-            atomicAdd(diff + y1 * W1 + x1, 1);
+                for (int p = 0; p < kDepthPasses; p++) atomicAdd(&s_hist[p][(db >> (8 * p)) & 255u], (u32)cnt);
+                atomicAdd(dd + y0 * W1 + x0, 1);
+                atomicAdd(dd + y0 * W1 + x1, -1);
+                atomicAdd(dd + y1 * W1 + x0, -1);
+                atomicAdd(dd + y1 * W1 + x1, 1);
+            }
         }
-    }
-    int incl = cnt;
+        int incl = cnt;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        int t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
-        if (lane >= d) incl += t;
-    }
-    const int total = __shfl_sync(VKS_FULL_MASK, incl, 31);
-    s_incl[warp][lane] = incl;
-    s_x0[warp][lane] = x0;
-    s_y0[warp][lane] = y0;
-    s_w[warp][lane] = w;
-    s_db[warp][lane] = db;
-    __syncwarp();
-    if (total > 0) {
-        const u64 base = (g0 < n) ? (u64)__ldg(offsets + g0) : 0;
+        for (int d = 1; d < 32; d <<= 1) {
+            int t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
+            if (lane >= d) incl += t;
+        }
+        const int total = __shfl_sync(VKS_FULL_MASK, incl, 31);
+        if (total == 0) continue;
+        __syncwarp();
+        s_incl[warp][lane] = incl;
+        s_x0[warp][lane] = x0;
+        s_y0[warp][lane] = y0;
+        s_w[warp][lane] = w;
+        s_db[warp][lane] = db;
+        __syncwarp();
+        const u64 base = (u64)__ldg(offsets + g0);
         for (int e = lane; e < total; e += 32) {
             int pos = 0;
 #pragma unroll
@@ -232,9 +251,15 @@ __global__ void __launch_bounds__(256) keys_kernel(vks_camera cam, int64_t n, co
         }
     }
     __syncthreads();
-    for (int j = tid; j < kDepthPasses * 256; j += 256) {
+    for (int j = tid; j < kDepthPasses * 256; j += kKeysThreads) {
         const u32 c = (&s_hist[0][0])[j];
         if (c) atomicAdd(hist + j, c);
+    }
+    if (SMEM_DIFF) {
+        for (int j = tid; j < cells; j += kKeysThreads) {
+            const int v = s_diff[j];
+            if (v) atomicAdd(diff + j, v);
+        }
     }
 }
 
@@ -390,16 +415,28 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
         const u32 binstart = wpre + incl - total;
         S.binstart[tid] = binstart;
         // decoupled look-back for digit `tid`
+        // (kLookbackChunk predecessors per round trip: the walk back to the nearest inclusive
+        // prefix costs ceil(len / chunk) L2 latencies instead of len)
         u32 excl = 0;
         if (tile > 0) {
             int64_t j = (int64_t)tile - 1;
-            while (true) {
-                const u32 s = ld_volatile_u32(lookback + (u64)j * 256 + tid);
-                const u32 f = s & ~kLbMask;
-                if (f == 0) continue;
-                excl += s & kLbMask;
-                if (f == kLbInc) break;
-                j--;
+            bool found = false;
+            while (!found) {
+                u32 st[kLookbackChunk];
+#pragma unroll
+                for (int q = 0; q < kLookbackChunk; q++)
+                    st[q] = (j - q >= 0) ? ld_volatile_u32(lookback + (u64)(j - q) * 256 + tid) : 0u;
+                int consumed = 0;
+#pragma unroll
+                for (int q = 0; q < kLookbackChunk; q++) {
+                    if (found || consumed < q) break;       // stop at the first unpublished entry
+                    const u32 f = st[q] & ~kLbMask;
+                    if (f == 0) break;
+                    excl += st[q] & kLbMask;
+                    consumed = q + 1;
+                    if (f == kLbInc) found = true;
+                }
+                j -= consumed;
             }
             st_volatile_u32(lookback + (u64)tile * 256 + tid, kLbInc | (excl + total));
         }
@@ -476,10 +513,30 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     u32* vB = (passes % 2 == 0) ? w.vals_x : vals;
     // 2. keys (+ histograms)
     {
-        const unsigned blocks = (unsigned)((n + 255) / 256);
-        keys_kernel<<<blocks, 256, 0, s>>>(cam, n, reinterpret_cast<const float2*>(means2d),
-                                           reinterpret_cast<const int2*>(radii), depths, tiles_touched,
-                                           offsets, kA, vA, w.hist, w.diff);
+        const int cells = (TX + 1) * (TY + 1);
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+        }
+        const int64_t want = (n + kKeysThreads - 1) / kKeysThreads;
+        if (cells <= kKeysSmemDiffMax) {
+            const size_t sm = sizeof(int) * (size_t)cells;
+            if (sm > 32 * 1024 &&
+                cudaFuncSetAttribute(keys_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+                return VKS_ERR_CUDA;
+            const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sms * 2);
+            keys_kernel<true><<<blocks, kKeysThreads, sm, s>>>(cam, n, reinterpret_cast<const float2*>(means2d),
+                                                               reinterpret_cast<const int2*>(radii), depths,
+                                                               tiles_touched, offsets, kA, vA, w.hist, w.diff);
+        } else {
+            const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sms * 4);
+            keys_kernel<false><<<blocks, kKeysThreads, 0, s>>>(cam, n, reinterpret_cast<const float2*>(means2d),
+                                                               reinterpret_cast<const int2*>(radii), depths,
+                                                               tiles_touched, offsets, kA, vA, w.hist, w.diff);
+        }
         if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
     }
     if (keys_unsorted && cudaMemcpyAsync(keys_unsorted, kA, sizeof(u64) * M, cudaMemcpyDeviceToDevice, s) != cudaSuccess)

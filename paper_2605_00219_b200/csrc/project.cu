@@ -380,7 +380,9 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
 #pragma unroll
             for (int ch = 0; ch < 3; ch++) {
                 float acc = Y[0] * f[ch];
-                for (int l = 1; l < K; l++) acc = acc + Y[l] * f[3 * l + ch];
+#pragma unroll
+                for (int l = 1; l < 16; l++)
+                    if (l < K) acc = acc + Y[l] * f[3 * l + ch];
                 const float raw = acc + 0.5f;
                 ok = ok && isfinite(raw);
                 col[ch] = raw > 0.0f ? raw : 0.0f;
@@ -409,7 +411,8 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
 
 // ------------------------------------------------------------------------------------------
 // backward: fp32 chain rule, accumulate (+=)
-template <int KS>
+// OVERWRITE: write the gradients (zero rows for radii == 0) instead of accumulating (+=)
+template <int KS, bool OVERWRITE>
 __global__ void __launch_bounds__(kThreads) project_bwd_kernel(const Params p) {
     extern __shared__ float smem[];
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -429,7 +432,28 @@ __global__ void __launch_bounds__(kThreads) project_bwd_kernel(const Params p) {
         act = project_core(p.cam, p.cfg, mu, ls, q, o, k);  // always true for radii != 0
     }
     const unsigned amask = __ballot_sync(VKS_FULL_MASK, act);
-    if (!amask) return;
+    if (OVERWRITE && i < p.n && !act) {  // never rasterised: zero rows
+        const int S0 = 3 * p.cfg.sh_coeffs;
+#pragma unroll
+        for (int c = 0; c < 3; c++) { p.dmeans[3 * i + c] = 0.0f; p.dls[3 * i + c] = 0.0f; }
+        p.dquats[i] = make_float4(0, 0, 0, 0);
+        p.dologit[i] = 0.0f;
+        if (KS == 0)
+            for (int j = 0; j < S0; j++) p.dsh[(int64_t)S0 * i + j] = 0.0f;
+    }
+    if (!amask) {
+        if constexpr (OVERWRITE && KS > 0) {
+            // whole warp inactive: zero its SH rows with coalesced stores
+            const int64_t nrow = min((int64_t)32, p.n - g0);
+            float4* d4 = reinterpret_cast<float4*>(p.dsh + g0 * 3 * KS);
+            if constexpr ((3 * KS) % 4 == 0) {
+                for (int j = lane; j < nrow * (3 * KS / 4); j += 32) d4[j] = make_float4(0, 0, 0, 0);
+            } else {
+                for (int j = lane; j < nrow * 3 * KS; j += 32) p.dsh[g0 * 3 * KS + j] = 0.0f;
+            }
+        }
+        return;
+    }
     const int K = (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);
     const int S = 3 * p.cfg.sh_coeffs;
 
@@ -462,38 +486,56 @@ __global__ void __launch_bounds__(kThreads) project_bwd_kernel(const Params p) {
         for (int ch = 0; ch < 3; ch++) {
             // clamp decision with the forward's exact fp32 sequence
             float acc = Y[0] * f[ch];
-            for (int l = 1; l < K; l++) acc = acc + Y[l] * f[3 * l + ch];
+#pragma unroll
+            for (int l = 1; l < 16; l++)
+                if (l < K) acc = acc + Y[l] * f[3 * l + ch];
             const float raw = acc + 0.5f;
             dce[ch] = raw > 0.0f ? dcol[ch] : 0.0f;
         }
-        for (int l = 0; l < K; l++) {
-            const float g = dce[0] * f[3 * l] + dce[1] * f[3 * l + 1] + dce[2] * f[3 * l + 2];
-            ddh[0] += g * dY[l][0];
-            ddh[1] += g * dY[l][1];
-            ddh[2] += g * dY[l][2];
+#pragma unroll
+        for (int l = 1; l < 16; l++) {
+            if (l < K) {
+                const float g = dce[0] * f[3 * l] + dce[1] * f[3 * l + 1] + dce[2] * f[3 * l + 2];
+                ddh[0] += g * dY[l][0];
+                ddh[1] += g * dY[l][1];
+                ddh[2] += g * dY[l][2];
+            }
         }
     }
     if constexpr (KS > 0) {
         __syncwarp();
-        sh_stage_in<KS>(p.dsh, g0, p.n, amask, buf);
+        if (!OVERWRITE) sh_stage_in<KS>(p.dsh, g0, p.n, amask, buf);
         __syncwarp();
         if (act) {
             float* dfp = buf + lane * ShLayout<KS>::SP;
-            for (int l = 0; l < K; l++) {
-                dfp[3 * l + 0] += Y[l] * dce[0];
-                dfp[3 * l + 1] += Y[l] * dce[1];
-                dfp[3 * l + 2] += Y[l] * dce[2];
+#pragma unroll
+            for (int l = 0; l < KS; l++) {
+                const float yl = l < K ? Y[l] : 0.0f;
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++) {
+                    if (OVERWRITE) dfp[3 * l + ch] = yl * dce[ch];
+                    else dfp[3 * l + ch] += yl * dce[ch];
+                }
             }
         }
         __syncwarp();
-        sh_stage_out<KS>(p.dsh, g0, amask, buf);
+        // rows of inactive lanes in an active warp: OVERWRITE must still zero them
+        const unsigned omask = OVERWRITE ? __ballot_sync(VKS_FULL_MASK, i < p.n) : amask;
+        if (OVERWRITE && !act && i < p.n) {
+            float* dfp = buf + lane * ShLayout<KS>::SP;
+            for (int j = 0; j < 3 * KS; j++) dfp[j] = 0.0f;
+        }
+        __syncwarp();
+        sh_stage_out<KS>(p.dsh, g0, omask, buf);
     } else {
         if (act) {
             float* dfp = p.dsh + (int64_t)S * i;
-            for (int l = 0; l < K; l++) {
-                dfp[3 * l + 0] += Y[l] * dce[0];
-                dfp[3 * l + 1] += Y[l] * dce[1];
-                dfp[3 * l + 2] += Y[l] * dce[2];
+            for (int l = 0; l < S / 3; l++) {
+                const float yl = l < K ? Y[l] : 0.0f;
+                for (int ch = 0; ch < 3; ch++) {
+                    if (OVERWRITE) dfp[3 * l + ch] = yl * dce[ch];
+                    else dfp[3 * l + ch] += yl * dce[ch];
+                }
             }
         }
     }
@@ -505,7 +547,8 @@ __global__ void __launch_bounds__(kThreads) project_bwd_kernel(const Params p) {
     }
     // opacity: sigmoid chain
     const float drho = p.dop[i];
-    p.dologit[i] += drho * k.rho * (1.0f - k.rho);
+    if (OVERWRITE) p.dologit[i] = drho * k.rho * (1.0f - k.rho);
+    else p.dologit[i] += drho * k.rho * (1.0f - k.rho);
     // conic (a,b,c) = (C, -B, A)/det  ->  (A, B, C)
     const float da = p.dcon[3 * i], db = p.dcon[3 * i + 1], dc = p.dcon[3 * i + 2];
     const float id = 1.0f / k.det, id2 = id * id;
@@ -570,10 +613,10 @@ __global__ void __launch_bounds__(kThreads) project_bwd_kernel(const Params p) {
     for (int c = 0; c < 3; c++) dmu[c] += R[c] * dt0 + R[3 + c] * dt1 + R[6 + c] * dt2;
 #pragma unroll
     for (int c = 0; c < 3; c++) {
-        p.dmeans[3 * i + c] += dmu[c];
-        p.dls[3 * i + c] += dlsv[c];
+        if (OVERWRITE) { p.dmeans[3 * i + c] = dmu[c]; p.dls[3 * i + c] = dlsv[c]; }
+        else { p.dmeans[3 * i + c] += dmu[c]; p.dls[3 * i + c] += dlsv[c]; }
     }
-    float4 dqv = p.dquats[i];
+    float4 dqv = OVERWRITE ? make_float4(0, 0, 0, 0) : p.dquats[i];
     dqv.x += (dq0 - w * qd) * iqn;
     dqv.y += (dq1 - x * qd) * iqn;
     dqv.z += (dq2 - y * qd) * iqn;
@@ -599,16 +642,21 @@ int launch_fwd_t(const Params& p, cudaStream_t s) {
     return LaunchCheck::check();
 }
 
-template <int KS>
-int launch_bwd_t(const Params& p, cudaStream_t s) {
+template <int KS, bool OW>
+int launch_bwd_t2(const Params& p, cudaStream_t s) {
     const size_t sm = smem_bytes<KS>();
     if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(project_bwd_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t e = cudaFuncSetAttribute(project_bwd_kernel<KS, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return VKS_ERR_CUDA;
     }
     const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
-    project_bwd_kernel<KS><<<blocks, kThreads, sm, s>>>(p);
+    project_bwd_kernel<KS, OW><<<blocks, kThreads, sm, s>>>(p);
     return LaunchCheck::check();
+}
+
+template <int KS>
+int launch_bwd_t(const Params& p, cudaStream_t s) {
+    return (p.cfg.flags & VKS_FLAG_GRAD_OVERWRITE) ? launch_bwd_t2<KS, true>(p, s) : launch_bwd_t2<KS, false>(p, s);
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }

@@ -1,15 +1,18 @@
 // raster.cu — "Rasterization Forward" and "Rasterization Backward";
-// DESIGN.md §4.4-4.5 and §6.
+// DESIGN.md §4.3-4.4 and §6.
 //
-// One 256-thread block per 16x16 tile, one thread per pixel.  The tile's sorted Gaussian list is
-// walked in batches of 256 staged into shared memory (one coalesced gather per batch; the batch is
-// reused by all 256 pixels).  The forward stops a block as soon as every pixel has T < 1e-4
-// (__syncthreads_count).  Forward and backward evaluate sigma / alpha through the SAME inline
+// One 256-thread block per 16x16 tile; each warp owns an 8x4 pixel patch.  The tile's sorted
+// Gaussian list is walked in batches of 256 staged into shared memory as packed float4 records
+// (one coalesced gather per batch, reused by all 256 pixels).  Before evaluating a Gaussian a warp
+// tests its 8x4 patch against the Gaussian's support box (support footprint only; the box is the
+// projection's radii plus a safety margin, so no pixel whose alpha could reach 1/255 is skipped)
+// and skips it warp-uniformly, which removes most of the evaluations that would be rejected by
+// the 1/255 test anyway.  Forward and backward evaluate sigma / alpha through the SAME inline
 // function, so skip / clamp / stop decisions replay identically; sigma, alpha and the colour
-// accumulation follow the pinned fp32 order of DESIGN.md §4.4 (only exp differs from the oracle:
+// accumulation follow the pinned fp32 order of DESIGN.md §4.3 (only exp differs from the oracle:
 // ex2.approx here, expf there).  The backward reduces each Gaussian's 9 gradient terms across the
-// warp with a transposed butterfly (14 shuffles instead of 45) and issues 2 atomic instructions
-// per (warp, Gaussian) that any lane touched.
+// warp with a transposed butterfly (14 shuffles instead of 45) and issues 2 atomic instructions per
+// (warp, Gaussian) that any lane touched.
 #include "vks_common.cuh"
 
 namespace vks {
@@ -18,38 +21,75 @@ namespace {
 constexpr int kThreads = 256;
 
 struct Stage {
-    float2 uv[kThreads];
-    float ha[kThreads], b[kThreads], hc[kThreads], rho[kThreads];
-    float col[3][kThreads];
+    float4 a[kThreads];    // u, v, 0.5*a, b
+    float4 b[kThreads];    // 0.5*c, rho, c0, c1
+    float4 box[kThreads];  // support box of pixel centres: xmin, xmax, ymin, ymax
+    float c2[kThreads];
     uint32_t id[kThreads];
 };
 
-__device__ __forceinline__ void stage_batch(Stage& s, int j, uint32_t g, const float2* __restrict__ means2d,
-                                            const float* __restrict__ conics, const float* __restrict__ colors,
-                                            const float* __restrict__ opac) {
+__device__ __forceinline__ void stage_batch(Stage& s, int j, uint32_t g, bool cull,
+                                            const float2* __restrict__ means2d, const float* __restrict__ conics,
+                                            const float* __restrict__ colors, const float* __restrict__ opac,
+                                            const int2* __restrict__ radii) {
+    const float2 uv = __ldg(means2d + g);
+    const float ca = __ldg(conics + 3 * (size_t)g), cb = __ldg(conics + 3 * (size_t)g + 1),
+                cc = __ldg(conics + 3 * (size_t)g + 2);
+    const float r0 = __ldg(colors + 3 * (size_t)g), r1 = __ldg(colors + 3 * (size_t)g + 1),
+                r2 = __ldg(colors + 3 * (size_t)g + 2);
+    const float rho = __ldg(opac + g);
     s.id[j] = g;
-    s.uv[j] = __ldg(means2d + g);
-    s.ha[j] = 0.5f * __ldg(conics + 3 * (size_t)g);
-    s.b[j] = __ldg(conics + 3 * (size_t)g + 1);
-    s.hc[j] = 0.5f * __ldg(conics + 3 * (size_t)g + 2);
-    s.rho[j] = __ldg(opac + g);
-    s.col[0][j] = __ldg(colors + 3 * (size_t)g);
-    s.col[1][j] = __ldg(colors + 3 * (size_t)g + 1);
-    s.col[2][j] = __ldg(colors + 3 * (size_t)g + 2);
+    s.a[j] = make_float4(uv.x, uv.y, 0.5f * ca, cb);
+    s.b[j] = make_float4(0.5f * cc, rho, r0, r1);
+    s.c2[j] = r2;
+    if (cull) {
+        // radii = ceil(sqrt(2 k' Sigma'_xx)) + 1 with k' > ln(255 rho): every pixel centre whose
+        // alpha can reach 1/255 lies inside u +- rx; widen by 1 + rx/64 px more for fp32 slack.
+        const int2 r = __ldg(radii + g);
+        const float mx = (float)r.x * (1.0f + 1.0f / 64.0f) + 1.0f;
+        const float my = (float)r.y * (1.0f + 1.0f / 64.0f) + 1.0f;
+        s.box[j] = make_float4(uv.x - mx, uv.x + mx, uv.y - my, uv.y + my);
+    } else {
+        s.box[j] = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
+    }
+}
+
+// warp patch [x0+0.5, x0+7.5] x [y0+0.5, y0+3.5] misses the support box
+__device__ __forceinline__ bool culled(const float4 bx, float wx0, float wx1, float wy0, float wy1) {
+    return bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1;
 }
 
 // sigma = 1/2 a dx^2 + b dx dy + 1/2 c dy^2 in the pinned order; returns false when skipped
 // (sigma < 0 or alpha < 1/255).  G = exp(-sigma) via ex2.approx.
-__device__ __forceinline__ bool eval_alpha(const Stage& s, int j, float px, float py, float& dx, float& dy,
-                                           float& G, float& rG, float& alpha) {
-    dx = s.uv[j].x - px;
-    dy = s.uv[j].y - py;
-    const float sigma = fmaf(s.ha[j] * dx, dx, fmaf(s.hc[j] * dy, dy, (s.b[j] * dx) * dy));
+__device__ __forceinline__ bool eval_alpha(const float4 A, const float4 B, float px, float py, float& dx,
+                                           float& dy, float& G, float& rG, float& alpha) {
+    dx = A.x - px;
+    dy = A.y - py;
+    const float sigma = fmaf(A.z * dx, dx, fmaf(B.x * dy, dy, (A.w * dx) * dy));
     if (sigma < 0.0f) return false;
     G = __expf(-sigma);
-    rG = s.rho[j] * G;
+    rG = B.y * G;
     alpha = fminf(0.99f, rG);
     return !(alpha < 1.0f / 255.0f);
+}
+
+struct PixelMap {
+    int x, y;               // pixel
+    float wx0, wx1, wy0, wy1;  // warp patch (pixel centres)
+};
+
+__device__ __forceinline__ PixelMap pixel_map(int tile, int TX) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bx = (tile % TX) * kTile + (warp & 1) * 8;
+    const int by = (tile / TX) * kTile + (warp >> 1) * 4;
+    PixelMap m;
+    m.x = bx + (lane & 7);
+    m.y = by + (lane >> 3);
+    m.wx0 = (float)bx + 0.5f;
+    m.wx1 = (float)bx + 7.5f;
+    m.wy0 = (float)by + 0.5f;
+    m.wy1 = (float)by + 3.5f;
+    return m;
 }
 
 __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(vks_config cfg, vks_camera cam,
@@ -57,6 +97,7 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(vks_config cfg, vk
                                                               const float* __restrict__ conics,
                                                               const float* __restrict__ colors,
                                                               const float* __restrict__ opac,
+                                                              const int2* __restrict__ radii,
                                                               const uint32_t* __restrict__ vals,
                                                               const uint32_t* __restrict__ tile_offsets,
                                                               float* __restrict__ image, float* __restrict__ T_final,
@@ -65,35 +106,37 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(vks_config cfg, vk
     const int TX = tiles_x(cam);
     const int tile = blockIdx.x;
     const int tid = threadIdx.x;
-    const int x = (tile % TX) * kTile + (tid & 15);
-    const int y = (tile / TX) * kTile + (tid >> 4);
-    const bool inside = x < cam.width && y < cam.height;
-    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+    const PixelMap pm = pixel_map(tile, TX);
+    const bool inside = pm.x < cam.width && pm.y < cam.height;
+    const bool cull = cfg.footprint == VKS_FOOTPRINT_SUPPORT;
+    const float px = (float)pm.x + 0.5f, py = (float)pm.y + 0.5f;
     const uint32_t start = tile_offsets[tile], end = tile_offsets[tile + 1];
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
     int last = 0;
     bool done = !inside;
     for (uint32_t b = start; b < end; b += kThreads) {
         if (__syncthreads_count(done) == kThreads) break;
-        if (b + tid < end) stage_batch(s, tid, __ldg(vals + b + tid), means2d, conics, colors, opac);
+        if (b + tid < end) stage_batch(s, tid, __ldg(vals + b + tid), cull, means2d, conics, colors, opac, radii);
         __syncthreads();
+        if (__all_sync(VKS_FULL_MASK, done)) continue;
         const int nb = (int)min((uint32_t)kThreads, end - b);
-        if (!done) {
-            for (int j = 0; j < nb; j++) {
-                float dx, dy, G, rG, alpha;
-                if (!eval_alpha(s, j, px, py, dx, dy, G, rG, alpha)) continue;
-                const float aT = alpha * T;
-                C0 = fmaf(s.col[0][j], aT, C0);
-                C1 = fmaf(s.col[1][j], aT, C1);
-                C2 = fmaf(s.col[2][j], aT, C2);
-                T = T * (1.0f - alpha);
-                last = (int)(b - start) + j + 1;
-                if (T < 1e-4f) { done = true; break; }
-            }
+        for (int j = 0; j < nb; j++) {
+            if (culled(s.box[j], pm.wx0, pm.wx1, pm.wy0, pm.wy1)) continue;  // warp-uniform
+            if (done) continue;
+            const float4 A = s.a[j], B = s.b[j];
+            float dx, dy, G, rG, alpha;
+            if (!eval_alpha(A, B, px, py, dx, dy, G, rG, alpha)) continue;
+            const float aT = alpha * T;
+            C0 = fmaf(B.z, aT, C0);
+            C1 = fmaf(B.w, aT, C1);
+            C2 = fmaf(s.c2[j], aT, C2);
+            T = T * (1.0f - alpha);
+            last = (int)(b - start) + j + 1;
+            if (T < 1e-4f) done = true;
         }
     }
     if (!inside) return;
-    const size_t pix = (size_t)y * cam.width + x;
+    const size_t pix = (size_t)pm.y * cam.width + pm.x;
     image[3 * pix + 0] = __fadd_rn(C0, __fmul_rn(T, cfg.bg[0]));
     image[3 * pix + 1] = __fadd_rn(C1, __fmul_rn(T, cfg.bg[1]));
     image[3 * pix + 2] = __fadd_rn(C2, __fmul_rn(T, cfg.bg[2]));
@@ -138,6 +181,7 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
                                                               const float* __restrict__ conics,
                                                               const float* __restrict__ colors,
                                                               const float* __restrict__ opac,
+                                                              const int2* __restrict__ radii,
                                                               const uint32_t* __restrict__ vals,
                                                               const uint32_t* __restrict__ tile_offsets,
                                                               const float* __restrict__ T_final,
@@ -151,15 +195,15 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
     const int tile = blockIdx.x;
     const int tid = threadIdx.x;
     const unsigned lane = tid & 31;
-    const int x = (tile % TX) * kTile + (tid & 15);
-    const int y = (tile / TX) * kTile + (tid >> 4);
-    const bool inside = x < cam.width && y < cam.height;
-    const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+    const PixelMap pm = pixel_map(tile, TX);
+    const bool inside = pm.x < cam.width && pm.y < cam.height;
+    const bool cull = cfg.footprint == VKS_FOOTPRINT_SUPPORT;
+    const float px = (float)pm.x + 0.5f, py = (float)pm.y + 0.5f;
     const uint32_t start = tile_offsets[tile];
     float T = 1.0f, w0 = 0.0f, w1 = 0.0f, w2 = 0.0f;
     int last = 0;
     if (inside) {
-        const size_t pix = (size_t)y * cam.width + x;
+        const size_t pix = (size_t)pm.y * cam.width + pm.x;
         T = T_final[pix];
         last = n_contrib[pix];
         w0 = dL_dimage[3 * pix];
@@ -173,25 +217,29 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
     if (lane == 0) atomicMax(&s_max, wmax);
     __syncthreads();
     const int bmax = s_max;
-    // the slot index of the 9th term: lane 4k (k < 8) owns term k, lane 1 owns the opacity term
+    // lane 4k (k < 8) owns gradient term k after the butterfly, lane 1 the opacity term
     const int myterm = (lane & 3) == 0 ? (int)(lane >> 2) : (lane == 1 ? 8 : -1);
     for (int bend = bmax; bend > 0; bend -= kThreads) {
         const int bstart = max(0, bend - kThreads);
         __syncthreads();
-        if (bstart + tid < bend) stage_batch(s, tid, __ldg(vals + start + bstart + tid), means2d, conics, colors, opac);
+        if (bstart + tid < bend)
+            stage_batch(s, tid, __ldg(vals + start + bstart + tid), cull, means2d, conics, colors, opac, radii);
         __syncthreads();
-        for (int j = bend - 1 - bstart; j >= 0; j--) {
+        const int jtop = min(bend, wmax) - 1 - bstart;  // entries at positions >= wmax: no lane composited
+        for (int j = jtop; j >= 0; j--) {
+            if (culled(s.box[j], pm.wx0, pm.wx1, pm.wy0, pm.wy1)) continue;  // warp-uniform
             const int pos = bstart + j;
             float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             float e = 0.0f;
             bool contrib = false;
             if (pos < last) {
+                const float4 A = s.a[j], B = s.b[j];
                 float dx, dy, G, rG, alpha;
-                if (eval_alpha(s, j, px, py, dx, dy, G, rG, alpha)) {
+                if (eval_alpha(A, B, px, py, dx, dy, G, rG, alpha)) {
                     contrib = true;
                     T = T / (1.0f - alpha);
                     const float aT = alpha * T;
-                    const float c0 = s.col[0][j], c1 = s.col[1][j], c2 = s.col[2][j];
+                    const float c0 = B.z, c1 = B.w, c2 = s.c2[j];
                     v[5] = aT * w0;
                     v[6] = aT * w1;
                     v[7] = aT * w2;
@@ -201,7 +249,7 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
                     S2 = alpha * c2 + (1.0f - alpha) * S2;
                     if (!(rG > 0.99f)) {
                         const float dsig = -rG * dalpha;
-                        const float a = 2.0f * s.ha[j], bb = s.b[j], c = 2.0f * s.hc[j];
+                        const float a = 2.0f * A.z, bb = A.w, c = 2.0f * B.x;
                         v[0] = (a * dx + bb * dy) * dsig;
                         v[1] = (bb * dx + c * dy) * dsig;
                         v[2] = 0.5f * dx * dx * dsig;
@@ -231,27 +279,28 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
 }  // namespace
 
 int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
-                      const float* conics, const float* colors, const float* opacities,
-                      const uint32_t* vals, const uint32_t* tile_offsets, float* image,
-                      float* T_final, int32_t* n_contrib, cudaStream_t st) {
+                      const float* conics, const float* colors, const float* opacities, const int32_t* radii,
+                      const uint32_t* vals, const uint32_t* tile_offsets, float* image, float* T_final,
+                      int32_t* n_contrib, cudaStream_t st) {
     (void)n;
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     raster_fwd_kernel<<<n_tiles, kThreads, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d), conics,
-                                                    colors, opacities, vals, tile_offsets, image, T_final,
-                                                    n_contrib);
+                                                    colors, opacities, reinterpret_cast<const int2*>(radii), vals,
+                                                    tile_offsets, image, T_final, n_contrib);
     return LaunchCheck::check();
 }
 
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
-                      const float* conics, const float* colors, const float* opacities,
+                      const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const uint32_t* vals, const uint32_t* tile_offsets, const float* T_final,
-                      const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
-                      float* dconics, float* dcolors, float* dopacities, cudaStream_t st) {
+                      const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics,
+                      float* dcolors, float* dopacities, cudaStream_t st) {
     (void)n;
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     raster_bwd_kernel<<<n_tiles, kThreads, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d), conics,
-                                                    colors, opacities, vals, tile_offsets, T_final, n_contrib,
-                                                    dL_dimage, dmeans2d, dconics, dcolors, dopacities);
+                                                    colors, opacities, reinterpret_cast<const int2*>(radii), vals,
+                                                    tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics,
+                                                    dcolors, dopacities);
     return LaunchCheck::check();
 }
 

@@ -68,11 +68,11 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
                  uint32_t* vals_unsorted, uint32_t* tile_offsets, int64_t* num_isects,
                  void* workspace, size_t workspace_bytes, cudaStream_t s);
 int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
-                      const float* conics, const float* colors, const float* opacities,
+                      const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const uint32_t* vals, const uint32_t* tile_offsets, float* image,
                       float* T_final, int32_t* n_contrib, cudaStream_t s);
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
-                      const float* conics, const float* colors, const float* opacities,
+                      const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const uint32_t* vals, const uint32_t* tile_offsets, const float* T_final,
                       const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
                       float* dconics, float* dcolors, float* dopacities, cudaStream_t s);

@@ -98,14 +98,19 @@ class ViewRenderer:
                 break
             self._alloc_capacity(int(-m * 1.25) + 1024)
         self.num_isects = m
-        V.vks_raster_fwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.vals,
+        V.vks_raster_fwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.radii, self.vals,
                          self.tile_offsets, self.image, self.T_final, self.n_contrib)
         return self.image
 
-    def backward(self, cfg, cam, P: GaussianParams, dL_dimage: torch.Tensor, zero_2d: bool = True):
+    def backward(self, cfg, cam, P: GaussianParams, dL_dimage: torch.Tensor, zero_2d: bool = True,
+                 accumulate: bool = True):
+        """accumulate=False: this view's parameter gradients overwrite P.grad_flat (first view of a
+        batch; rows of Gaussians this view does not see are zeroed) — no memset needed."""
         if zero_2d:
             self.g2d.zero_()
-        V.vks_raster_bwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.vals,
+        if not accumulate:
+            cfg = dict(cfg, flags=int(cfg.get("flags", 0)) | V.FLAG_GRAD_OVERWRITE)
+        V.vks_raster_bwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.radii, self.vals,
                          self.tile_offsets, self.T_final, self.n_contrib, dL_dimage, self.dmeans2d, self.dconics,
                          self.dcolors, self.dopacities)
         g = P.grads()

@@ -209,3 +209,33 @@ def test_deterministic_integer_stages():
     b = run_gpu(scene, cam, cfg)
     for k in ("keys", "vals", "offsets", "tile_offsets", "image", "T_final", "n_contrib", "means2d"):
         assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("coeffs,deg", [(16, 3), (9, 2), (4, 1), (1, 0), (16, 1)])
+def test_grad_overwrite_equals_accumulate_into_zero(coeffs, deg):
+    """VKS_FLAG_GRAD_OVERWRITE writes exactly what += into a zeroed buffer gives (same 2D grads),
+    including zero rows for Gaussians the view does not see, over a NaN-filled buffer."""
+    import torch
+    import paper_2605_00219_b200 as P
+    s = synth.make_scene(3001, "outdoor", 60)  # odd n: ragged last warp
+    s["sh"] = np.ascontiguousarray(s["sh"][:, :coeffs])
+    cam = synth.ring_cameras(80, 64)[1]
+    cfg = synth.default_render_config(deg, sh_coeffs=coeffs)
+    params = P.GaussianParams.from_host(s)
+    r = P.ViewRenderer(params.n, 80, 64)
+    r.forward(cfg, cam, params)
+    dL = torch.from_numpy(synth.upstream_grad(64, 80, 9)).cuda()
+    params.grad_flat.zero_()
+    r.backward(cfg, cam, params, dL)
+    acc = params.grad_flat.clone()
+    params.grad_flat.fill_(float("nan"))
+    g = params.grads()
+    ocfg = dict(cfg, flags=P.FLAG_GRAD_OVERWRITE)
+    P.vks_project_bwd(ocfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits, params.sh,
+                      r.radii, r.dmeans2d, r.dconics, r.dcolors, r.dopacities, g["dmeans"], g["dlog_scales"],
+                      g["dquats"], g["dopacity_logits"], g["dsh"])
+    torch.cuda.synchronize()
+    for k, v in g.items():
+        ref = P.GaussianParams(params.means, params.log_scales, params.quats, params.opacity_logits, params.sh,
+                               acc).grads()[k]
+        assert torch.equal(v, ref), k

@@ -177,7 +177,7 @@ def run_ours(args):
             g = params.grads()
             # first view of the step overwrites the gradient buffer (no memset), later ones accumulate
             P.vks_project_bwd(cfg_ow if j == 0 else cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
-                              params.sh, rend.radii, rend.dmeans2d, rend.dconics, rend.dcolors, rend.dopacities,
+                              params.sh, rend.colors, rend.radii, rend.dmeans2d, rend.dconics, rend.dcolors, rend.dopacities,
                               g["dmeans"], g["dlog_scales"], g["dquats"], g["dopacity_logits"], g["dsh"])
             if ev is not None: ev[5].record(stream)
         allreduce_grads(params.grad_flat)  # row a9: the only exchange (no-op at N = 1)

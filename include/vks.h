@@ -180,12 +180,15 @@ int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
  * radii != 0 (others untouched): conic inversion, Sigma' = J W Sigma W^T J^T
  * (+0.3 passes the gradient), exact FOV-clamp derivative, quaternion
  * normalisation, exp / sigmoid activations, SH colour (clamped channels give 0).
+ * colors / radii are vks_project_fwd's outputs for the same view: colour == 0 marks a clamped
+ * channel, radii != 0 a rasterised Gaussian.
  *   -> dmeans [n,3], dlog_scales [n,3], dquats [n,4], dopacity_logits [n],
  *      dsh [n, sh_coeffs, 3]   (+=; with VKS_FLAG_GRAD_OVERWRITE: =, and zero rows for radii == 0)
  */
 int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                     const float* means, const float* log_scales, const float* quats,
-                    const float* opacity_logits, const float* sh, const int32_t* radii,
+                    const float* opacity_logits, const float* sh, const float* colors,
+                    const int32_t* radii,
                     const float* dmeans2d, const float* dconics, const float* dcolors,
                     const float* dopacities, float* dmeans, float* dlog_scales, float* dquats,
                     float* dopacity_logits, float* dsh, vks_stream_t stream);

@@ -51,7 +51,7 @@ _lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
 _lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 7 + [C.c_size_t, _P]
 _lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 11
 _lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 15
-_lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 16
+_lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
 for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_bwd", "vks_project_bwd"):
     getattr(_lib, _f).restype = C.c_int
 
@@ -186,13 +186,13 @@ def vks_raster_bwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, ti
     _check("vks_raster_bwd", st)
 
 
-def vks_project_bwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, radii, dmeans2d, dconics,
+def vks_project_bwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, colors, radii, dmeans2d, dconics,
                     dcolors, dopacities, dmeans, dlog_scales, dquats, dopacity_logits, dsh, stream=None):
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_project_bwd(C.byref(c), C.byref(k), means.shape[0], _ptr(means, f32, "means"),
                               _ptr(log_scales, f32, "log_scales"), _ptr(quats, f32, "quats"),
                               _ptr(opacity_logits, f32, "opacity_logits"), _ptr(sh, f32, "sh"),
-                              _ptr(radii, i32, "radii"), _ptr(dmeans2d, f32, "dmeans2d"),
+                              _ptr(colors, f32, "colors"), _ptr(radii, i32, "radii"), _ptr(dmeans2d, f32, "dmeans2d"),
                               _ptr(dconics, f32, "dconics"), _ptr(dcolors, f32, "dcolors"),
                               _ptr(dopacities, f32, "dopacities"), _ptr(dmeans, f32, "dmeans"),
                               _ptr(dlog_scales, f32, "dlog_scales"), _ptr(dquats, f32, "dquats"),

@@ -145,13 +145,13 @@ int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
 
 int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means,
                     const float* log_scales, const float* quats, const float* opacity_logits,
-                    const float* sh, const int32_t* radii, const float* dmeans2d, const float* dconics,
+                    const float* sh, const float* colors, const int32_t* radii, const float* dmeans2d, const float* dconics,
                     const float* dcolors, const float* dopacities, float* dmeans, float* dlog_scales,
                     float* dquats, float* dopacity_logits, float* dsh, vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
-    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !radii || !dmeans2d ||
+    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !colors || !radii || !dmeans2d ||
                   !dconics || !dcolors || !dopacities || !dmeans || !dlog_scales || !dquats ||
                   !dopacity_logits || !dsh))
         return VKS_ERR_INVALID_ARG;
@@ -159,7 +159,7 @@ int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, con
         (reinterpret_cast<uintptr_t>(dmeans2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
-    return cuda_status(vks::launch_project_bwd(*cfg, *cam, n, means, log_scales, quats, opacity_logits, sh, radii,
+    return cuda_status(vks::launch_project_bwd(*cfg, *cam, n, means, log_scales, quats, opacity_logits, sh, colors, radii,
                                                dmeans2d, dconics, dcolors, dopacities, dmeans, dlog_scales,
                                                dquats, dopacity_logits, dsh, (cudaStream_t)stream));
 }

@@ -17,6 +17,8 @@
 //                     decoupled look-back across dynamically numbered tiles per digit, local
 //                     reordering in shared memory so global stores are digit-contiguous runs.
 // The binning TU is compiled with -fmad=false (the rect recomputation must equal projection's).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "vks_common.cuh"
@@ -33,8 +35,8 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
+constexpr int kSortMinItems = 8;                              // smallest tile (workspace sizing)
+constexpr int kSortMinTile = kSortThreads * kSortMinItems;  // 2048 keys
 constexpr int kMaxPasses = 8;
 constexpr int kDepthPasses = 4;
 constexpr int kLookbackChunk = 8;
@@ -73,7 +75,7 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int32_t n_tiles, int TX
     char* b = static_cast<char*>(base);
     auto take = [&](size_t bytes) { char* p = b ? b + off : nullptr; off += align_up(bytes); return p; };
     const int64_t scan_tiles = (n + kScanTile - 1) / kScanTile;
-    const int64_t sort_tiles = (capacity + kSortTile - 1) / kSortTile;
+    const int64_t sort_tiles = (capacity + kSortMinTile - 1) / kSortMinTile;
     w.keys_x = reinterpret_cast<u64*>(take(sizeof(u64) * (size_t)capacity));
     w.vals_x = reinterpret_cast<u32*>(take(sizeof(u32) * (size_t)capacity));
     w.gstart = reinterpret_cast<u32*>(take(sizeof(u32) * kMaxPasses * 256));
@@ -342,45 +344,81 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int pa
 
 // ------------------------------------------------------------------------------------------
 // 4. one onesweep pass over 8 bits starting at `shift`
+template <int ITEMS>
 struct SortSmem {
-    u64 keys[kSortTile];
-    u32 vals[kSortTile];
+    static constexpr int kTile = kSortThreads * ITEMS;
+    alignas(128) u64 keys[kTile];  // input staging (bulk copy), then the digit-reordered tile
+    alignas(128) u32 vals[kTile];
     u32 whist[kSortWarps][256];
     u32 binstart[256];
     u32 gbase[256];
     u32 wsum[kSortWarps];
     u32 tile;
+    alignas(8) unsigned long long mbar;
 };
 
 __device__ __forceinline__ u32 digit_of(u64 k, int shift) { return (u32)(k >> shift) & 255u; }
 
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+// One onesweep pass over 8 bits starting at `shift`.  The tile's keys/values arrive through two
+// TMA bulk copies (cp.async.bulk, completion on an mbarrier) while the block clears its
+// histograms, so no registers are tied up waiting for DRAM; ranks are computed from shared memory
+// with __match_any_sync (stable: warp-striped slot order), per-digit totals are published for the
+// decoupled look-back (chunked), and the tile is reordered in place so the stores are
+// digit-contiguous runs.
+template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restrict__ kin, const u32* __restrict__ vin,
                                                             u64* __restrict__ kout, u32* __restrict__ vout, u32 M,
                                                             int shift, const u32* __restrict__ gstart,
                                                             u32* __restrict__ lookback, u32* __restrict__ tile_ctr) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+    using Smem = SortSmem<ITEMS>;
+    constexpr int kTile = Smem::kTile;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
-    for (int j = tid; j < kSortWarps * 256; j += kSortThreads) (&S.whist[0][0])[j] = 0;
+    const u32 bar = smem_u32(&S.mbar);
+    if (tid == 0) {
+        S.tile = atomicAdd(tile_ctr, 1u);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
     const u32 tile = S.tile;
-    const u64 seg = (u64)tile * kSortTile + (u64)warp * 32 * kSortItems;
-    u64 k[kSortItems];
-    u32 v[kSortItems];
-#pragma unroll
-    for (int i = 0; i < kSortItems; i++) {
-        const u64 idx = seg + (u64)i * 32 + lane;
-        const bool ok = idx < M;
-        k[i] = ok ? kin[idx] : ~0ull;  // pads sort last (digit 255, last tile, trailing slots)
-        v[i] = ok ? vin[idx] : 0u;
+    const u64 base = (u64)tile * kTile;
+    const u32 count = (u32)min((u64)kTile, (u64)M - base);
+    const u32 nbulk = count & ~3u;  // 32-byte multiples of keys, 16-byte multiples of values
+    if (tid == 0) {
+        if (nbulk) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nbulk * 12u) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(smem_u32(S.keys)), "l"(kin + base), "r"(nbulk * 8u), "r"(bar) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(smem_u32(S.vals)), "l"(vin + base), "r"(nbulk * 4u), "r"(bar) : "memory");
+        } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+        }
     }
+    for (int j = tid; j < kSortWarps * 256; j += kSortThreads) (&S.whist[0][0])[j] = 0;
+    // tail (< 4 keys) and padding: pads (~0) rank last in digit 255 and land at dest >= M
+    for (u32 j = nbulk + tid; j < (u32)kTile; j += kSortThreads) {
+        const bool ok = j < count;
+        S.keys[j] = ok ? kin[base + j] : ~0ull;
+        S.vals[j] = ok ? vin[base + j] : 0u;
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra WAIT%=;\n\t}" ::"r"(bar) : "memory");
+    __syncthreads();
     // stable warp-level ranking with match.any
-    u32 rank[kSortItems];
+    u32 rank[ITEMS];
     const u32 ltmask = lanemask_lt();
+    const int seg = warp * 32 * ITEMS;
 #pragma unroll
-    for (int i = 0; i < kSortItems; i++) {
-        const u32 d = digit_of(k[i], shift);
+    for (int i = 0; i < ITEMS; i++) {
+        const u32 d = digit_of(S.keys[seg + i * 32 + lane], shift);
         const u32 peers = __match_any_sync(VKS_FULL_MASK, d);
         const u32 below = __popc(peers & ltmask);
         const u32 before = S.whist[warp][d];
@@ -392,15 +430,13 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
     __syncthreads();
     // per-digit totals, warp exclusive offsets, block exclusive digit starts
     u32 total = 0;
-    if (tid < 256) {
 #pragma unroll
-        for (int w = 0; w < kSortWarps; w++) {
-            const u32 c = S.whist[w][tid];
-            S.whist[w][tid] = total;
-            total += c;
-        }
-        st_volatile_u32(lookback + (u64)tile * 256 + tid, (tile == 0 ? kLbInc : kLbAgg) | total);
+    for (int w = 0; w < kSortWarps; w++) {
+        const u32 c = S.whist[w][tid];
+        S.whist[w][tid] = total;
+        total += c;
     }
+    st_volatile_u32(lookback + (u64)tile * 256 + tid, (tile == 0 ? kLbInc : kLbAgg) | total);
     u32 incl = total;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -409,16 +445,16 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
     }
     if (lane == 31) S.wsum[warp] = incl;
     __syncthreads();
-    if (tid < 256) {
+    {
         u32 wpre = 0;
         for (int w = 0; w < warp; w++) wpre += S.wsum[w];
         const u32 binstart = wpre + incl - total;
         S.binstart[tid] = binstart;
-        // decoupled look-back for digit `tid`
-        // (kLookbackChunk predecessors per round trip: the walk back to the nearest inclusive
-        // prefix costs ceil(len / chunk) L2 latencies instead of len)
+        // decoupled look-back for digit `tid`, kLookbackChunk predecessors per round trip
+        // Digits absent from this tile need no prefix: they keep their aggregate (0) and
+        // successors walk past them.
         u32 excl = 0;
-        if (tile > 0) {
+        if (tile > 0 && total > 0) {
             int64_t j = (int64_t)tile - 1;
             bool found = false;
             while (!found) {
@@ -429,7 +465,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
                 int consumed = 0;
 #pragma unroll
                 for (int q = 0; q < kLookbackChunk; q++) {
-                    if (found || consumed < q) break;       // stop at the first unpublished entry
+                    if (found || consumed < q) break;  // stop at the first unpublished entry
                     const u32 f = st[q] & ~kLbMask;
                     if (f == 0) break;
                     excl += st[q] & kLbMask;
@@ -443,17 +479,26 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
         S.gbase[tid] = gstart[tid] + excl - binstart;
     }
     __syncthreads();
-    // local reorder through shared memory
+    // reorder the tile in shared memory (read everything first, then write: in place)
+    u64 kk[ITEMS];
+    u32 vv[ITEMS];
 #pragma unroll
-    for (int i = 0; i < kSortItems; i++) {
-        const u32 d = digit_of(k[i], shift);
-        const u32 pos = S.binstart[d] + S.whist[warp][d] + rank[i];
-        S.keys[pos] = k[i];
-        S.vals[pos] = v[i];
+    for (int i = 0; i < ITEMS; i++) {
+        const int slot = seg + i * 32 + lane;
+        kk[i] = S.keys[slot];
+        vv[i] = S.vals[slot];
+        rank[i] += S.binstart[digit_of(kk[i], shift)] + S.whist[warp][digit_of(kk[i], shift)];
     }
     __syncthreads();
-#pragma unroll 4
-    for (int j = tid; j < kSortTile; j += kSortThreads) {
+#pragma unroll
+    for (int i = 0; i < ITEMS; i++) {
+        S.keys[rank[i]] = kk[i];
+        S.vals[rank[i]] = vv[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < ITEMS; r++) {
+        const int j = r * kSortThreads + tid;
         const u64 key = S.keys[j];
         const u32 dest = S.gbase[digit_of(key, shift)] + (u32)j;
         if (dest < M) {
@@ -544,28 +589,39 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     if (vals_unsorted && cudaMemcpyAsync(vals_unsorted, vA, sizeof(u32) * M, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return VKS_ERR_CUDA;
     // 3. tile counts -> tile ranges, digit starts
-    const u64 sort_tiles = (M + kSortTile - 1) / kSortTile;
+    static int items = 0;
+    if (!items) {
+        const char* e = getenv("VKS_SORT_ITEMS");
+        items = e ? atoi(e) : 16;
+        if (items != 8 && items != 12 && items != 16) items = 16;
+    }
+    const int tile_keys = kSortThreads * items;
+    const u64 sort_tiles = (M + tile_keys - 1) / tile_keys;
     const size_t zb = align_up(sizeof(u32) * kMaxPasses) + sizeof(u32) * (size_t)passes * 256 * sort_tiles;
     if (cudaMemsetAsync(w.zeroB, 0, zb, s) != cudaSuccess) return VKS_ERR_CUDA;
     tile_count_kernel<<<1, 1024, 0, s>>>(TX, TY, passes, w.diff, w.hist, w.gstart, tile_offsets);
     if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
     // 4. radix passes
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(onesweep_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem)) != cudaSuccess)
+    auto launch = [&](auto kernel, size_t sm) -> int {
+        if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
             return VKS_ERR_CUDA;
-        attr_set = true;
-    }
-    for (int p = 0; p < passes; p++) {
-        const u64* kin = (p % 2 == 0) ? kA : kB;
-        const u32* vin = (p % 2 == 0) ? vA : vB;
-        u64* ko = (p % 2 == 0) ? kB : kA;
-        u32* vo = (p % 2 == 0) ? vB : vA;
-        onesweep_pass<<<(unsigned)sort_tiles, kSortThreads, sizeof(SortSmem), s>>>(
-            kin, vin, ko, vo, (u32)M, 8 * p, w.gstart + 256 * p, w.sort_lb + (size_t)p * 256 * sort_tiles,
-            w.sort_ctr + p);
-        if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
-    }
+        for (int p = 0; p < passes; p++) {
+            const u64* kin = (p % 2 == 0) ? kA : kB;
+            const u32* vin = (p % 2 == 0) ? vA : vB;
+            u64* ko = (p % 2 == 0) ? kB : kA;
+            u32* vo = (p % 2 == 0) ? vB : vA;
+            kernel<<<(unsigned)sort_tiles, kSortThreads, sm, s>>>(kin, vin, ko, vo, (u32)M, 8 * p, w.gstart + 256 * p,
+                                                                 w.sort_lb + (size_t)p * 256 * sort_tiles,
+                                                                 w.sort_ctr + p);
+            if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
+        }
+        return VKS_OK;
+    };
+    int st = VKS_OK;
+    if (items == 16) st = launch(onesweep_pass<16>, sizeof(SortSmem<16>));
+    else if (items == 12) st = launch(onesweep_pass<12>, sizeof(SortSmem<12>));
+    else st = launch(onesweep_pass<8>, sizeof(SortSmem<8>));
+    if (st != VKS_OK) return st;
     return VKS_OK;
 }
 

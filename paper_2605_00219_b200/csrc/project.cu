@@ -1,5 +1,4 @@
-// project.cu — "Projection Forward" and the projection part of "Proj Bwd + Optimizer"
-// (P:76).  Compiled with -fmad=false: every fp32 + - * / below is one IEEE-rounded operation in
+// project.cu — "Projection Forward"; the backward lives in project_bwd.cu.  Compiled with -fmad=false: every fp32 + - * / below is one IEEE-rounded operation in
 // the order written, which is the order pinned in DESIGN.md §4.1 (the oracle's O1 follows the
 // same written specification independently), so projection outputs are bit-exact with O1.
 // Transcendentals on the key path are evaluated as (float)f((double)x).
@@ -227,34 +226,6 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, int K, float
     Y[15] = (C36 * x) * (xx - 3.0f * yy);
 }
 
-// d Y_l / d(x,y,z) (backward only; not on the bit-exact path)
-__device__ __forceinline__ void sh_basis_grad(float x, float y, float z, int K, float dY[16][3]) {
-#pragma unroll
-    for (int l = 0; l < 16; l++) dY[l][0] = dY[l][1] = dY[l][2] = 0.0f;
-    if (K > 1) {
-        dY[1][1] = -C1;
-        dY[2][2] = C1;
-        dY[3][0] = -C1;
-    }
-    if (K > 4) {
-        dY[4][0] = C20 * y; dY[4][1] = C20 * x;
-        dY[5][1] = C21 * z; dY[5][2] = C21 * y;
-        dY[6][0] = -2.0f * C22 * x; dY[6][1] = -2.0f * C22 * y; dY[6][2] = 4.0f * C22 * z;
-        dY[7][0] = C23 * z; dY[7][2] = C23 * x;
-        dY[8][0] = 2.0f * C24 * x; dY[8][1] = -2.0f * C24 * y;
-    }
-    if (K > 9) {
-        const float xx = x * x, yy = y * y, zz = z * z;
-        dY[9][0] = 6.0f * C30 * x * y; dY[9][1] = C30 * (3.0f * xx - 3.0f * yy);
-        dY[10][0] = C31 * y * z; dY[10][1] = C31 * x * z; dY[10][2] = C31 * x * y;
-        dY[11][0] = -2.0f * C32 * x * y; dY[11][1] = C32 * (4.0f * zz - xx - 3.0f * yy); dY[11][2] = 8.0f * C32 * y * z;
-        dY[12][0] = -6.0f * C33 * x * z; dY[12][1] = -6.0f * C33 * y * z; dY[12][2] = C33 * (6.0f * zz - 3.0f * xx - 3.0f * yy);
-        dY[13][0] = C34 * (4.0f * zz - 3.0f * xx - yy); dY[13][1] = -2.0f * C34 * x * y; dY[13][2] = 8.0f * C34 * x * z;
-        dY[14][0] = 2.0f * C35 * x * z; dY[14][1] = -2.0f * C35 * y * z; dY[14][2] = C35 * (xx - yy);
-        dY[15][0] = C36 * (3.0f * xx - 3.0f * yy); dY[15][1] = -6.0f * C36 * x * y;
-    }
-}
-
 // ---- warp-cooperative staging of SH rows ------------------------------------------------
 // KS = stored coefficients per Gaussian (compile time); S = 3*KS floats per row; the smem row
 // stride SP is chosen so per-lane row reads are bank-conflict free.
@@ -266,62 +237,27 @@ struct ShLayout {
     static constexpr int kWarpFloats = 32 * SP;
 };
 
-// copy rows of lanes in `mask` from global (row base `g0` = first Gaussian of the warp) to smem
+// issue async copies of the SH rows of lanes in `mask` (row base `g0` = first Gaussian of the
+// warp) into the warp's smem slice; the caller commits / waits
 template <int KS>
-__device__ __forceinline__ void sh_stage_in(const float* __restrict__ src, int64_t g0, int64_t n,
-                                            unsigned mask, float* buf) {
+__device__ __forceinline__ void sh_stage_async(const float* __restrict__ src, int64_t g0, unsigned mask, float* buf) {
     using Lay = ShLayout<KS>;
     const unsigned lane = lane_id();
     if constexpr (Lay::kVec) {
-        constexpr int V = Lay::S / 4;  // float4 per row
+        constexpr int V = Lay::S / 4;
         const float4* s4 = reinterpret_cast<const float4*>(src) + g0 * V;
+#pragma unroll 4
         for (int j = lane; j < 32 * V; j += 32) {
             const int r = j / V, c = j - r * V;
-            if ((mask >> r) & 1u) {
-                float4 v = __ldg(s4 + j);
-                *reinterpret_cast<float4*>(buf + r * Lay::SP + 4 * c) = v;
-            }
+            if ((mask >> r) & 1u) cp_async16(buf + r * Lay::SP + 4 * c, s4 + j);
         }
     } else {
         const float* s1 = src + g0 * Lay::S;
         for (int j = lane; j < 32 * Lay::S; j += 32) {
             const int r = j / Lay::S, c = j - r * Lay::S;
-            if ((mask >> r) & 1u) buf[r * Lay::SP + c] = __ldg(s1 + j);
+            if ((mask >> r) & 1u) cp_async4(buf + r * Lay::SP + c, s1 + j);
         }
     }
-    (void)n;
-}
-
-template <int KS>
-__device__ __forceinline__ void sh_stage_out(float* __restrict__ dst, int64_t g0, unsigned mask,
-                                             const float* buf) {
-    using Lay = ShLayout<KS>;
-    const unsigned lane = lane_id();
-    if constexpr (Lay::kVec) {
-        constexpr int V = Lay::S / 4;
-        float4* d4 = reinterpret_cast<float4*>(dst) + g0 * V;
-        for (int j = lane; j < 32 * V; j += 32) {
-            const int r = j / V, c = j - r * V;
-            if ((mask >> r) & 1u) d4[j] = *reinterpret_cast<const float4*>(buf + r * Lay::SP + 4 * c);
-        }
-    } else {
-        float* d1 = dst + g0 * Lay::S;
-        for (int j = lane; j < 32 * Lay::S; j += 32) {
-            const int r = j / Lay::S, c = j - r * Lay::S;
-            if ((mask >> r) & 1u) d1[j] = buf[r * Lay::SP + c];
-        }
-    }
-}
-
-__device__ __forceinline__ void load_params(const Params& p, int64_t i, float mu[3], float ls[3],
-                                            float4& q, float& o) {
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-        mu[c] = __ldg(p.means + 3 * i + c);
-        ls[c] = __ldg(p.ls + 3 * i + c);
-    }
-    q = __ldg(p.quats + i);
-    o = __ldg(p.ologit + i);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -337,58 +273,61 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
     const int TX = tiles_x(p.cam), TY = tiles_y(p.cam);
 
     Core k;
-    float mu[3], ls[3], o = 0.0f;
+    float mu[3] = {0, 0, 0}, ls[3] = {0, 0, 0}, o = 0.0f;
     float4 q = make_float4(0, 0, 0, 0);
     float rxf = 0, ryf = 0;
     int x0 = 0, x1 = 0, y0 = 0, y1 = 0;
-    bool vis = false;
-    if (valid) {
-        mu[0] = __ldg(p.means + 3 * i);
-        mu[1] = __ldg(p.means + 3 * i + 1);
-        mu[2] = __ldg(p.means + 3 * i + 2);
-        // cheap near-plane test first: skip the other parameter loads of Gaussians behind the camera
-        const float tz = dot3(p.cam.R + 6, mu) + p.cam.t[2];
-        if (tz > p.cfg.near_plane) {
+    bool near_ok = false;
+    if (valid) {  // every parameter load issued at once (one DRAM round trip)
 #pragma unroll
-            for (int c = 0; c < 3; c++) ls[c] = __ldg(p.ls + 3 * i + c);
-            q = __ldg(p.quats + i);
-            o = __ldg(p.ologit + i);
-            vis = project_core(p.cam, p.cfg, mu, ls, q, o, k) &&
-                  footprint_rect(k, p.cfg, TX, TY, rxf, ryf, x0, x1, y0, y1);
+        for (int c = 0; c < 3; c++) {
+            mu[c] = __ldg(p.means + 3 * i + c);
+            ls[c] = __ldg(p.ls + 3 * i + c);
         }
+        q = __ldg(p.quats + i);
+        o = __ldg(p.ologit + i);
+        const float tz = dot3(p.cam.R + 6, mu) + p.cam.t[2];
+        near_ok = tz > p.cfg.near_plane;
     }
-    // colour (only for survivors; SH rows staged through smem)
+    // start the SH rows of every Gaussian in front of the camera streaming into shared memory now;
+    // they land while the projection below runs (rows of culled Gaussians are never read)
+    const unsigned nmask = __ballot_sync(VKS_FULL_MASK, near_ok);
+    float* buf = nullptr;
+    if constexpr (KS > 0) {
+        buf = smem + warp * ShLayout<KS>::kWarpFloats;
+        if (nmask) sh_stage_async<KS>(p.sh, g0, nmask, buf);
+        cp_async_commit();
+    }
+    bool vis = near_ok && project_core(p.cam, p.cfg, mu, ls, q, o, k) &&
+               footprint_rect(k, p.cfg, TX, TY, rxf, ryf, x0, x1, y0, y1);
+    // colour (survivors only)
     const int K = (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);
     float col[3] = {0, 0, 0};
     const unsigned vmask = __ballot_sync(VKS_FULL_MASK, vis);
-    if (vmask) {
+    if constexpr (KS > 0) {
+        cp_async_wait_all();
+        __syncwarp();
+    }
+    if (vmask && vis) {
         const float* f;
-        if constexpr (KS > 0) {
-            float* buf = smem + warp * ShLayout<KS>::kWarpFloats;
-            sh_stage_in<KS>(p.sh, g0, p.n, vmask, buf);
-            __syncwarp();
-            f = buf + lane * ShLayout<KS>::SP;
-        } else {
-            f = p.sh + 3 * (int64_t)p.cfg.sh_coeffs * i;
-        }
-        if (vis) {
-            float dh[3], dl;
-            view_dir(p.cam, mu, dh, dl);
-            float Y[16];
-            sh_basis(dh[0], dh[1], dh[2], K, Y);
-            bool ok = true;
+        if constexpr (KS > 0) f = buf + lane * ShLayout<KS>::SP;
+        else f = p.sh + 3 * (int64_t)p.cfg.sh_coeffs * i;
+        float dh[3], dl;
+        view_dir(p.cam, mu, dh, dl);
+        float Y[16];
+        sh_basis(dh[0], dh[1], dh[2], K, Y);
+        bool ok = true;
 #pragma unroll
-            for (int ch = 0; ch < 3; ch++) {
-                float acc = Y[0] * f[ch];
+        for (int ch = 0; ch < 3; ch++) {
+            float acc = Y[0] * f[ch];
 #pragma unroll
-                for (int l = 1; l < 16; l++)
-                    if (l < K) acc = acc + Y[l] * f[3 * l + ch];
-                const float raw = acc + 0.5f;
-                ok = ok && isfinite(raw);
-                col[ch] = raw > 0.0f ? raw : 0.0f;
-            }
-            vis = ok;
+            for (int l = 1; l < 16; l++)
+                if (l < K) acc = acc + Y[l] * f[3 * l + ch];
+            const float raw = acc + 0.5f;
+            ok = ok && isfinite(raw);
+            col[ch] = raw > 0.0f ? raw : 0.0f;
         }
+        vis = ok;
     }
     if (!valid) return;
     if (vis) {
@@ -409,221 +348,6 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// backward: fp32 chain rule, accumulate (+=)
-// OVERWRITE: write the gradients (zero rows for radii == 0) instead of accumulating (+=)
-template <int KS, bool OVERWRITE>
-__global__ void __launch_bounds__(kThreads) project_bwd_kernel(const Params p) {
-    extern __shared__ float smem[];
-    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    const unsigned lane = lane_id();
-    const int warp = threadIdx.x >> 5;
-    const int64_t g0 = i - lane;
-    bool act = i < p.n;
-    if (act) {
-        const int2 r = p.radii_in[i];
-        act = (r.x != 0) || (r.y != 0);
-    }
-    Core k;
-    float mu[3] = {0, 0, 0}, ls[3] = {0, 0, 0}, o = 0.0f;
-    float4 q = make_float4(1, 0, 0, 0);
-    if (act) {
-        load_params(p, i, mu, ls, q, o);
-        act = project_core(p.cam, p.cfg, mu, ls, q, o, k);  // always true for radii != 0
-    }
-    const unsigned amask = __ballot_sync(VKS_FULL_MASK, act);
-    if (OVERWRITE && i < p.n && !act) {  // never rasterised: zero rows
-        const int S0 = 3 * p.cfg.sh_coeffs;
-#pragma unroll
-        for (int c = 0; c < 3; c++) { p.dmeans[3 * i + c] = 0.0f; p.dls[3 * i + c] = 0.0f; }
-        p.dquats[i] = make_float4(0, 0, 0, 0);
-        p.dologit[i] = 0.0f;
-        if (KS == 0)
-            for (int j = 0; j < S0; j++) p.dsh[(int64_t)S0 * i + j] = 0.0f;
-    }
-    if (!amask) {
-        if constexpr (OVERWRITE && KS > 0) {
-            // whole warp inactive: zero its SH rows with coalesced stores
-            const int64_t nrow = min((int64_t)32, p.n - g0);
-            float4* d4 = reinterpret_cast<float4*>(p.dsh + g0 * 3 * KS);
-            if constexpr ((3 * KS) % 4 == 0) {
-                for (int j = lane; j < nrow * (3 * KS / 4); j += 32) d4[j] = make_float4(0, 0, 0, 0);
-            } else {
-                for (int j = lane; j < nrow * 3 * KS; j += 32) p.dsh[g0 * 3 * KS + j] = 0.0f;
-            }
-        }
-        return;
-    }
-    const int K = (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);
-    const int S = 3 * p.cfg.sh_coeffs;
-
-    float dmu[3] = {0, 0, 0};
-    float dcol[3] = {0, 0, 0};
-    float dhv[3] = {0, 0, 0}, dl = 1.0f;
-    float Y[16];
-    if (act) {
-        dcol[0] = p.dcol[3 * i]; dcol[1] = p.dcol[3 * i + 1]; dcol[2] = p.dcol[3 * i + 2];
-        view_dir(p.cam, mu, dhv, dl);
-        sh_basis(dhv[0], dhv[1], dhv[2], K, Y);
-    }
-    // SH: stage f rows in, compute clamp flags + direction gradient, stage dsh rows in, add, out
-    float* buf = nullptr;
-    const float* f;
-    if constexpr (KS > 0) {
-        buf = smem + warp * ShLayout<KS>::kWarpFloats;
-        sh_stage_in<KS>(p.sh, g0, p.n, amask, buf);
-        __syncwarp();
-        f = buf + lane * ShLayout<KS>::SP;
-    } else {
-        f = p.sh + (int64_t)S * i;
-    }
-    float dce[3] = {0, 0, 0};
-    float ddh[3] = {0, 0, 0};
-    if (act) {
-        float dY[16][3];
-        sh_basis_grad(dhv[0], dhv[1], dhv[2], K, dY);
-#pragma unroll
-        for (int ch = 0; ch < 3; ch++) {
-            // clamp decision with the forward's exact fp32 sequence
-            float acc = Y[0] * f[ch];
-#pragma unroll
-            for (int l = 1; l < 16; l++)
-                if (l < K) acc = acc + Y[l] * f[3 * l + ch];
-            const float raw = acc + 0.5f;
-            dce[ch] = raw > 0.0f ? dcol[ch] : 0.0f;
-        }
-#pragma unroll
-        for (int l = 1; l < 16; l++) {
-            if (l < K) {
-                const float g = dce[0] * f[3 * l] + dce[1] * f[3 * l + 1] + dce[2] * f[3 * l + 2];
-                ddh[0] += g * dY[l][0];
-                ddh[1] += g * dY[l][1];
-                ddh[2] += g * dY[l][2];
-            }
-        }
-    }
-    if constexpr (KS > 0) {
-        __syncwarp();
-        if (!OVERWRITE) sh_stage_in<KS>(p.dsh, g0, p.n, amask, buf);
-        __syncwarp();
-        if (act) {
-            float* dfp = buf + lane * ShLayout<KS>::SP;
-#pragma unroll
-            for (int l = 0; l < KS; l++) {
-                const float yl = l < K ? Y[l] : 0.0f;
-#pragma unroll
-                for (int ch = 0; ch < 3; ch++) {
-                    if (OVERWRITE) dfp[3 * l + ch] = yl * dce[ch];
-                    else dfp[3 * l + ch] += yl * dce[ch];
-                }
-            }
-        }
-        __syncwarp();
-        // rows of inactive lanes in an active warp: OVERWRITE must still zero them
-        const unsigned omask = OVERWRITE ? __ballot_sync(VKS_FULL_MASK, i < p.n) : amask;
-        if (OVERWRITE && !act && i < p.n) {
-            float* dfp = buf + lane * ShLayout<KS>::SP;
-            for (int j = 0; j < 3 * KS; j++) dfp[j] = 0.0f;
-        }
-        __syncwarp();
-        sh_stage_out<KS>(p.dsh, g0, omask, buf);
-    } else {
-        if (act) {
-            float* dfp = p.dsh + (int64_t)S * i;
-            for (int l = 0; l < S / 3; l++) {
-                const float yl = l < K ? Y[l] : 0.0f;
-                for (int ch = 0; ch < 3; ch++) {
-                    if (OVERWRITE) dfp[3 * l + ch] = yl * dce[ch];
-                    else dfp[3 * l + ch] += yl * dce[ch];
-                }
-            }
-        }
-    }
-    if (!act) return;
-    {
-        const float pr = dhv[0] * ddh[0] + dhv[1] * ddh[1] + dhv[2] * ddh[2];
-#pragma unroll
-        for (int c = 0; c < 3; c++) dmu[c] = (ddh[c] - dhv[c] * pr) / dl;
-    }
-    // opacity: sigmoid chain
-    const float drho = p.dop[i];
-    if (OVERWRITE) p.dologit[i] = drho * k.rho * (1.0f - k.rho);
-    else p.dologit[i] += drho * k.rho * (1.0f - k.rho);
-    // conic (a,b,c) = (C, -B, A)/det  ->  (A, B, C)
-    const float da = p.dcon[3 * i], db = p.dcon[3 * i + 1], dc = p.dcon[3 * i + 2];
-    const float id = 1.0f / k.det, id2 = id * id;
-    const float A = k.A, B = k.B, C = k.C;
-    // d(Sigma'^-1): written without the 1/det - AC/det^2 cancellation (= -B^2/det^2)
-    const float dA = (-C * C * da + B * C * db - B * B * dc) * id2;
-    const float dB = (2.0f * B * C * da - (A * C + B * B) * db + 2.0f * A * B * dc) * id2;
-    const float dC = (-B * B * da + A * B * db - A * A * dc) * id2;
-    // Sigma' = K K^T + 0.3 I
-    float dK0[3], dK1[3];
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-        dK0[c] = 2.0f * dA * k.K0[c] + dB * k.K1[c];
-        dK1[c] = dB * k.K0[c] + 2.0f * dC * k.K1[c];
-    }
-    // K = J Mc
-    float dJ00 = 0, dJ02 = 0, dJ11 = 0, dJ12 = 0, dMc[9];
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-        dJ00 += dK0[c] * k.Mc[c];
-        dJ02 += dK0[c] * k.Mc[6 + c];
-        dJ11 += dK1[c] * k.Mc[3 + c];
-        dJ12 += dK1[c] * k.Mc[6 + c];
-        dMc[c] = k.J00 * dK0[c];
-        dMc[3 + c] = k.J11 * dK1[c];
-        dMc[6 + c] = k.J02 * dK0[c] + k.J12 * dK1[c];
-    }
-    // Mc = R M ;  M = Rq diag(s)
-    const float* R = p.cam.R;
-    float D[9], dlsv[3];
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-        float ds = 0.0f;
-#pragma unroll
-        for (int j = 0; j < 3; j++) {
-            const float dM = R[j] * dMc[c] + R[3 + j] * dMc[3 + c] + R[6 + j] * dMc[6 + c];
-            ds += dM * k.Rq[3 * j + c];
-            D[3 * j + c] = dM * k.s[c];
-        }
-        dlsv[c] = ds * k.s[c];
-    }
-    const float w = k.w, x = k.x, y = k.y, z = k.z;
-    float dq0 = 2.0f * (-z * D[1] + y * D[2] + z * D[3] - x * D[5] - y * D[6] + x * D[7]);
-    float dq1 = 2.0f * (y * D[1] + z * D[2] + y * D[3] - 2.0f * x * D[4] - w * D[5] + z * D[6] + w * D[7] - 2.0f * x * D[8]);
-    float dq2 = 2.0f * (-2.0f * y * D[0] + x * D[1] + w * D[2] + x * D[3] + z * D[5] - w * D[6] + z * D[7] - 2.0f * y * D[8]);
-    float dq3 = 2.0f * (-2.0f * z * D[0] - w * D[1] + x * D[2] + w * D[3] - 2.0f * z * D[4] + y * D[5] + x * D[6] + y * D[7]);
-    const float qd = w * dq0 + x * dq1 + y * dq2 + z * dq3;
-    const float iqn = 1.0f / k.qn;
-    // t: from mean2d and from J (exact FOV-clamp derivative)
-    const float2 dm = p.dm2[i];
-    const float fx = p.cam.fx, fy = p.cam.fy;
-    const float tx = k.t[0], ty = k.t[1], tz = k.t[2];
-    const float itz = 1.0f / tz, itz2 = itz * itz, itz3 = itz2 * itz;
-    float dt0 = fx * itz * dm.x;
-    float dt1 = fy * itz * dm.y;
-    float dt2 = -fx * tx * itz2 * dm.x - fy * ty * itz2 * dm.y - fx * itz2 * dJ00 - fy * itz2 * dJ11;
-    if (k.fovx == 0) { dt0 += -fx * itz2 * dJ02; dt2 += 2.0f * fx * tx * itz3 * dJ02; }
-    else { dt2 += fx * k.Lx * itz2 * dJ02; }
-    if (k.fovy == 0) { dt1 += -fy * itz2 * dJ12; dt2 += 2.0f * fy * ty * itz3 * dJ12; }
-    else { dt2 += fy * k.Ly * itz2 * dJ12; }
-#pragma unroll
-    for (int c = 0; c < 3; c++) dmu[c] += R[c] * dt0 + R[3 + c] * dt1 + R[6 + c] * dt2;
-#pragma unroll
-    for (int c = 0; c < 3; c++) {
-        if (OVERWRITE) { p.dmeans[3 * i + c] = dmu[c]; p.dls[3 * i + c] = dlsv[c]; }
-        else { p.dmeans[3 * i + c] += dmu[c]; p.dls[3 * i + c] += dlsv[c]; }
-    }
-    float4 dqv = OVERWRITE ? make_float4(0, 0, 0, 0) : p.dquats[i];
-    dqv.x += (dq0 - w * qd) * iqn;
-    dqv.y += (dq1 - x * qd) * iqn;
-    dqv.z += (dq2 - y * qd) * iqn;
-    dqv.w += (dq3 - z * qd) * iqn;
-    p.dquats[i] = dqv;
-}
-
 template <int KS>
 size_t smem_bytes() {
     if constexpr (KS > 0) return sizeof(float) * kWarps * ShLayout<KS>::kWarpFloats;
@@ -640,23 +364,6 @@ int launch_fwd_t(const Params& p, cudaStream_t s) {
     const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
     project_fwd_kernel<KS><<<blocks, kThreads, sm, s>>>(p);
     return LaunchCheck::check();
-}
-
-template <int KS, bool OW>
-int launch_bwd_t2(const Params& p, cudaStream_t s) {
-    const size_t sm = smem_bytes<KS>();
-    if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(project_bwd_kernel<KS, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return VKS_ERR_CUDA;
-    }
-    const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
-    project_bwd_kernel<KS, OW><<<blocks, kThreads, sm, s>>>(p);
-    return LaunchCheck::check();
-}
-
-template <int KS>
-int launch_bwd_t(const Params& p, cudaStream_t s) {
-    return (p.cfg.flags & VKS_FLAG_GRAD_OVERWRITE) ? launch_bwd_t2<KS, true>(p, s) : launch_bwd_t2<KS, false>(p, s);
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
@@ -682,31 +389,6 @@ int launch_project_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
         case 4: return al ? launch_fwd_t<4>(p, s) : launch_fwd_t<0>(p, s);
         case 1: return launch_fwd_t<1>(p, s);
         default: return launch_fwd_t<0>(p, s);
-    }
-}
-
-int launch_project_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means,
-                       const float* log_scales, const float* quats, const float* opacity_logits,
-                       const float* sh, const int32_t* radii, const float* dmeans2d,
-                       const float* dconics, const float* dcolors, const float* dopacities,
-                       float* dmeans, float* dlog_scales, float* dquats, float* dopacity_logits,
-                       float* dsh, cudaStream_t s) {
-    if (n == 0) return VKS_OK;
-    Params p{};
-    p.cam = cam; p.cfg = cfg; p.n = n;
-    p.means = means; p.ls = log_scales; p.quats = reinterpret_cast<const float4*>(quats);
-    p.ologit = opacity_logits; p.sh = sh;
-    p.radii_in = reinterpret_cast<const int2*>(radii);
-    p.dm2 = reinterpret_cast<const float2*>(dmeans2d); p.dcon = dconics; p.dcol = dcolors;
-    p.dop = dopacities; p.dmeans = dmeans; p.dls = dlog_scales;
-    p.dquats = reinterpret_cast<float4*>(dquats); p.dologit = dopacity_logits; p.dsh = dsh;
-    const bool al = aligned16(sh) && aligned16(dsh);
-    switch (cfg.sh_coeffs) {
-        case 16: return al ? launch_bwd_t<16>(p, s) : launch_bwd_t<0>(p, s);
-        case 9: return launch_bwd_t<9>(p, s);
-        case 4: return al ? launch_bwd_t<4>(p, s) : launch_bwd_t<0>(p, s);
-        case 1: return launch_bwd_t<1>(p, s);
-        default: return launch_bwd_t<0>(p, s);
     }
 }
 

@@ -1,9 +1,10 @@
 // raster.cu — "Rasterization Forward" and "Rasterization Backward";
 // DESIGN.md §4.3-4.4 and §6.
 //
-// One 256-thread block per 16x16 tile; each warp owns an 8x4 pixel patch.  The tile's sorted
-// Gaussian list is walked in batches of 256 staged into shared memory as packed float4 records
-// (one coalesced gather per batch, reused by all 256 pixels).  Before evaluating a Gaussian a warp
+// One 256-thread block per 16x16 tile; each warp owns an 8x4 pixel patch and walks the tile's
+// sorted list on its own in batches of 32 staged into its shared-memory slice as packed float4
+// records (software-pipelined: ids two batches ahead, records one batch ahead), so there are no
+// block barriers and a warp stops as soon as its own 32 pixels are saturated.  Before evaluating a Gaussian a warp
 // tests its 8x4 patch against the Gaussian's support box (support footprint only; the box is the
 // projection's radii plus a safety margin, so no pixel whose alpha could reach 1/255 is skipped)
 // and skips it warp-uniformly, which removes most of the evaluations that would be rejected by
@@ -19,39 +20,56 @@ namespace vks {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kWarpsPerBlock = kThreads / 32;
 
-struct Stage {
-    float4 a[kThreads];    // u, v, 0.5*a, b
-    float4 b[kThreads];    // 0.5*c, rho, c0, c1
-    float4 box[kThreads];  // support box of pixel centres: xmin, xmax, ymin, ymax
-    float c2[kThreads];
-    uint32_t id[kThreads];
+// One warp's staged batch of 32 list entries (each warp walks the tile list on its own: no block
+// barriers, so a warp never waits for a slower one and stops as soon as its own pixels are done).
+struct WarpStage {
+    float4 a[32];    // u, v, 0.5*a, b
+    float4 b[32];    // 0.5*c, rho, c0, c1
+    float4 box[32];  // support box of pixel centres: xmin, xmax, ymin, ymax
+    float c2[32];
+    uint32_t id[32];
 };
 
-__device__ __forceinline__ void stage_batch(Stage& s, int j, uint32_t g, bool cull,
-                                            const float2* __restrict__ means2d, const float* __restrict__ conics,
-                                            const float* __restrict__ colors, const float* __restrict__ opac,
-                                            const int2* __restrict__ radii) {
+struct Entry {  // one lane's gathered entry, in registers until it is stored to the stage
+    float4 a, b, box;
+    float c2;
+    uint32_t id;
+};
+
+__device__ __forceinline__ Entry gather_entry(uint32_t g, bool cull, const float2* __restrict__ means2d,
+                                              const float* __restrict__ conics, const float* __restrict__ colors,
+                                              const float* __restrict__ opac, const int2* __restrict__ radii) {
+    Entry e;
     const float2 uv = __ldg(means2d + g);
     const float ca = __ldg(conics + 3 * (size_t)g), cb = __ldg(conics + 3 * (size_t)g + 1),
                 cc = __ldg(conics + 3 * (size_t)g + 2);
-    const float r0 = __ldg(colors + 3 * (size_t)g), r1 = __ldg(colors + 3 * (size_t)g + 1),
-                r2 = __ldg(colors + 3 * (size_t)g + 2);
+    const float r0 = __ldg(colors + 3 * (size_t)g), r1 = __ldg(colors + 3 * (size_t)g + 1);
+    e.c2 = __ldg(colors + 3 * (size_t)g + 2);
     const float rho = __ldg(opac + g);
-    s.id[j] = g;
-    s.a[j] = make_float4(uv.x, uv.y, 0.5f * ca, cb);
-    s.b[j] = make_float4(0.5f * cc, rho, r0, r1);
-    s.c2[j] = r2;
+    e.id = g;
+    e.a = make_float4(uv.x, uv.y, 0.5f * ca, cb);
+    e.b = make_float4(0.5f * cc, rho, r0, r1);
     if (cull) {
         // radii = ceil(sqrt(2 k' Sigma'_xx)) + 1 with k' > ln(255 rho): every pixel centre whose
         // alpha can reach 1/255 lies inside u +- rx; widen by 1 + rx/64 px more for fp32 slack.
         const int2 r = __ldg(radii + g);
         const float mx = (float)r.x * (1.0f + 1.0f / 64.0f) + 1.0f;
         const float my = (float)r.y * (1.0f + 1.0f / 64.0f) + 1.0f;
-        s.box[j] = make_float4(uv.x - mx, uv.x + mx, uv.y - my, uv.y + my);
+        e.box = make_float4(uv.x - mx, uv.x + mx, uv.y - my, uv.y + my);
     } else {
-        s.box[j] = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
+        e.box = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
     }
+    return e;
+}
+
+__device__ __forceinline__ void store_entry(WarpStage& s, int lane, const Entry& e) {
+    s.a[lane] = e.a;
+    s.b[lane] = e.b;
+    s.box[lane] = e.box;
+    s.c2[lane] = e.c2;
+    s.id[lane] = e.id;
 }
 
 // warp patch [x0+0.5, x0+7.5] x [y0+0.5, y0+3.5] misses the support box
@@ -59,22 +77,28 @@ __device__ __forceinline__ bool culled(const float4 bx, float wx0, float wx1, fl
     return bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1;
 }
 
+__device__ __forceinline__ float exp2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // sigma = 1/2 a dx^2 + b dx dy + 1/2 c dy^2 in the pinned order; returns false when skipped
-// (sigma < 0 or alpha < 1/255).  G = exp(-sigma) via ex2.approx.
+// (sigma < 0 or alpha < 1/255).  G = exp(-sigma) = 2^(-sigma log2 e) via ex2.approx.ftz.
 __device__ __forceinline__ bool eval_alpha(const float4 A, const float4 B, float px, float py, float& dx,
                                            float& dy, float& G, float& rG, float& alpha) {
     dx = A.x - px;
     dy = A.y - py;
     const float sigma = fmaf(A.z * dx, dx, fmaf(B.x * dy, dy, (A.w * dx) * dy));
     if (sigma < 0.0f) return false;
-    G = __expf(-sigma);
+    G = exp2_ftz(sigma * -1.44269504088896341f);
     rG = B.y * G;
     alpha = fminf(0.99f, rG);
     return !(alpha < 1.0f / 255.0f);
 }
 
 struct PixelMap {
-    int x, y;               // pixel
+    int x, y;                  // pixel
     float wx0, wx1, wy0, wy1;  // warp patch (pixel centres)
 };
 
@@ -102,10 +126,11 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(vks_config cfg, vk
                                                               const uint32_t* __restrict__ tile_offsets,
                                                               float* __restrict__ image, float* __restrict__ T_final,
                                                               int* __restrict__ n_contrib) {
-    __shared__ Stage s;
+    __shared__ WarpStage stage[kWarpsPerBlock];
     const int TX = tiles_x(cam);
     const int tile = blockIdx.x;
-    const int tid = threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    WarpStage& s = stage[threadIdx.x >> 5];
     const PixelMap pm = pixel_map(tile, TX);
     const bool inside = pm.x < cam.width && pm.y < cam.height;
     const bool cull = cfg.footprint == VKS_FOOTPRINT_SUPPORT;
@@ -114,14 +139,25 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(vks_config cfg, vk
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
     int last = 0;
     bool done = !inside;
-    for (uint32_t b = start; b < end; b += kThreads) {
-        if (__syncthreads_count(done) == kThreads) break;
-        if (b + tid < end) stage_batch(s, tid, __ldg(vals + b + tid), cull, means2d, conics, colors, opac, radii);
-        __syncthreads();
-        if (__all_sync(VKS_FULL_MASK, done)) continue;
-        const int nb = (int)min((uint32_t)kThreads, end - b);
-        for (int j = 0; j < nb; j++) {
-            if (culled(s.box[j], pm.wx0, pm.wx1, pm.wy0, pm.wy1)) continue;  // warp-uniform
+    // software pipeline: ids two batches ahead, gathered entries one batch ahead
+    uint32_t id_next = (start + lane < end) ? __ldg(vals + start + lane) : 0u;
+    Entry e_next;
+    if (start + lane < end) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
+    id_next = (start + 32 + lane < end) ? __ldg(vals + start + 32 + lane) : 0u;
+    for (uint32_t b = start; b < end; b += 32) {
+        if (__all_sync(VKS_FULL_MASK, done)) break;
+        __syncwarp();
+        // each lane tests its own entry against the warp patch; the warp then visits only the
+        // entries whose support box meets the patch, in list order
+        unsigned live = __ballot_sync(VKS_FULL_MASK, b + lane < end &&
+                                                         !culled(e_next.box, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
+        if (b + lane < end) store_entry(s, lane, e_next);
+        __syncwarp();
+        if (b + 32 + lane < end) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
+        if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
+        while (live) {
+            const int j = __ffs(live) - 1;
+            live &= live - 1;
             if (done) continue;
             const float4 A = s.a[j], B = s.b[j];
             float dx, dy, G, rG, alpha;
@@ -189,12 +225,11 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
                                                               const float* __restrict__ dL_dimage,
                                                               float* __restrict__ dmeans2d, float* __restrict__ dconics,
                                                               float* __restrict__ dcolors, float* __restrict__ dopac) {
-    __shared__ Stage s;
-    __shared__ int s_max;
+    __shared__ WarpStage stage[kWarpsPerBlock];
     const int TX = tiles_x(cam);
     const int tile = blockIdx.x;
-    const int tid = threadIdx.x;
-    const unsigned lane = tid & 31;
+    const unsigned lane = threadIdx.x & 31;
+    WarpStage& s = stage[threadIdx.x >> 5];
     const PixelMap pm = pixel_map(tile, TX);
     const bool inside = pm.x < cam.width && pm.y < cam.height;
     const bool cull = cfg.footprint == VKS_FOOTPRINT_SUPPORT;
@@ -211,24 +246,36 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
         w2 = dL_dimage[3 * pix + 2];
     }
     float S0 = cfg.bg[0], S1 = cfg.bg[1], S2 = cfg.bg[2];
-    if (tid == 0) s_max = 0;
-    __syncthreads();
-    const int wmax = __reduce_max_sync(VKS_FULL_MASK, last);
-    if (lane == 0) atomicMax(&s_max, wmax);
-    __syncthreads();
-    const int bmax = s_max;
+    const int wmax = __reduce_max_sync(VKS_FULL_MASK, last);  // positions >= wmax: nobody composited
     // lane 4k (k < 8) owns gradient term k after the butterfly, lane 1 the opacity term
     const int myterm = (lane & 3) == 0 ? (int)(lane >> 2) : (lane == 1 ? 8 : -1);
-    for (int bend = bmax; bend > 0; bend -= kThreads) {
-        const int bstart = max(0, bend - kThreads);
-        __syncthreads();
-        if (bstart + tid < bend)
-            stage_batch(s, tid, __ldg(vals + start + bstart + tid), cull, means2d, conics, colors, opac, radii);
-        __syncthreads();
-        const int jtop = min(bend, wmax) - 1 - bstart;  // entries at positions >= wmax: no lane composited
-        for (int j = jtop; j >= 0; j--) {
-            if (culled(s.box[j], pm.wx0, pm.wx1, pm.wy0, pm.wy1)) continue;  // warp-uniform
-            const int pos = bstart + j;
+    // batches of 32 positions, back to front: [bs, bs+32) with bs = wmax-32, wmax-64, ...
+    int bs = wmax - 32;
+    int p0 = bs + (int)lane;
+    uint32_t id_next = (p0 >= 0 && p0 < wmax) ? __ldg(vals + start + p0) : 0u;
+    Entry e_next;
+    if (p0 >= 0 && p0 < wmax) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
+    p0 -= 32;
+    id_next = (p0 >= 0) ? __ldg(vals + start + p0) : 0u;
+    for (; bs > -32; bs -= 32) {
+        __syncwarp();
+        unsigned live;
+        {
+            const int p = bs + (int)lane;
+            const bool ok = p >= 0 && p < wmax;
+            live = __ballot_sync(VKS_FULL_MASK, ok && !culled(e_next.box, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
+            if (ok) store_entry(s, lane, e_next);
+        }
+        __syncwarp();
+        {
+            const int p = bs - 32 + (int)lane;
+            if (p >= 0) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
+            if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
+        }
+        while (live) {  // back to front over the entries whose support box meets the patch
+            const int j = 31 - __clz(live);
+            live &= ~(1u << j);
+            const int pos = bs + j;
             float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             float e = 0.0f;
             bool contrib = false;
@@ -237,7 +284,7 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
                 float dx, dy, G, rG, alpha;
                 if (eval_alpha(A, B, px, py, dx, dy, G, rG, alpha)) {
                     contrib = true;
-                    T = T / (1.0f - alpha);
+                    T = __fdividef(T, 1.0f - alpha);
                     const float aT = alpha * T;
                     const float c0 = B.z, c1 = B.w, c2 = s.c2[j];
                     v[5] = aT * w0;

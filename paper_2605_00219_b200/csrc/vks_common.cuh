@@ -47,6 +47,17 @@ __device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned 
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Ampere-style async copies global -> shared (LDGSTS): no registers held while in flight
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 }  // namespace vks
 
 // internal launchers (implemented in the .cu files, called by api.cu)
@@ -57,7 +68,7 @@ int launch_project_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
                        int32_t* tiles_touched, float* colors, float* opacities, cudaStream_t s);
 int launch_project_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means,
                        const float* log_scales, const float* quats, const float* opacity_logits,
-                       const float* sh, const int32_t* radii, const float* dmeans2d,
+                       const float* sh, const float* colors, const int32_t* radii, const float* dmeans2d,
                        const float* dconics, const float* dcolors, const float* dopacities,
                        float* dmeans, float* dlog_scales, float* dquats, float* dopacity_logits,
                        float* dsh, cudaStream_t s);

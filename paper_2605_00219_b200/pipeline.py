@@ -114,6 +114,6 @@ class ViewRenderer:
                          self.tile_offsets, self.T_final, self.n_contrib, dL_dimage, self.dmeans2d, self.dconics,
                          self.dcolors, self.dopacities)
         g = P.grads()
-        V.vks_project_bwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.radii,
+        V.vks_project_bwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.colors, self.radii,
                           self.dmeans2d, self.dconics, self.dcolors, self.dopacities, g["dmeans"],
                           g["dlog_scales"], g["dquats"], g["dopacity_logits"], g["dsh"])

@@ -162,7 +162,7 @@ def run_ours(args):
                               params.sh, rend.means2d, rend.conics, rend.depths, rend.radii, rend.tiles,
                               rend.colors, rend.opacities)
             if ev is not None: ev[1].record(stream)
-            m = P.vks_bin_sort(cam, rend.means2d, rend.radii, rend.depths, rend.tiles, rend.offsets, rend.keys,
+            m = P.vks_bin_sort(cam, rend.means2d, rend.radii, rend.depths, rend.tiles, rend.offsets, None,
                                rend.vals, rend.tile_offsets, rend.workspace)
             rend.num_isects = m
             if ev is not None: ev[2].record(stream)

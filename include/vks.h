@@ -127,7 +127,8 @@ size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles
  *   *num_isects (HOST)   <- M = sum tiles_touched
  *   for each i with tiles_touched > 0 and each tile (ty outer, tx inner) of its
  *   rect: slot offsets[i]+k gets key = (tile << 32) | f32bits(depth_i), val = i
- *   keys/vals [capacity] <- the M pairs stable-sorted ascending by key (u64)
+ *   keys/vals [capacity] <- the M pairs stable-sorted ascending by key (u64); keys is
+ *                           nullable (the rasterizer needs only vals and tile_offsets)
  *   tile_offsets [n_tiles+1] u32 <- CSR: #entries with tile id < t
  *   keys_unsorted / vals_unsorted (nullable, debug; [capacity] like keys/vals): the pre-sort pairs.
  * If M > capacity (or M >= 2^32) returns VKS_ERR_CAPACITY after writing

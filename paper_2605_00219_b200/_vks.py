@@ -142,14 +142,14 @@ def vks_bin_sort_workspace_bytes(n, capacity, n_tiles) -> int:
 
 def vks_bin_sort(cam, means2d, radii, depths, tiles_touched, offsets, keys, vals, tile_offsets,
                  workspace, keys_unsorted=None, vals_unsorted=None, stream=None, raise_capacity=True):
-    """Returns M (num_isects).  keys/vals capacity = keys.numel().  On VKS_ERR_CAPACITY returns -M
-    when raise_capacity is False."""
+    """Returns M (num_isects).  Capacity = vals.numel(); keys (u64, same capacity) may be None.
+    On VKS_ERR_CAPACITY returns -M when raise_capacity is False."""
     k = cam if isinstance(cam, VksCamera) else make_camera(cam)
     n = means2d.shape[0]
     m = C.c_int64(0)
     st = _lib.vks_bin_sort(C.byref(k), n, _ptr(means2d, f32, "means2d"), _ptr(radii, i32, "radii"),
                            _ptr(depths, f32, "depths"), _ptr(tiles_touched, i32, "tiles_touched"),
-                           _ptr(offsets, u32, "offsets"), keys.numel(), _ptr(keys, u64, "keys"),
+                           _ptr(offsets, u32, "offsets"), vals.numel(), _ptr(keys, u64, "keys"),
                            _ptr(vals, u32, "vals"), _ptr(keys_unsorted, u64, "keys_unsorted"),
                            _ptr(vals_unsorted, u32, "vals_unsorted"), _ptr(tile_offsets, u32, "tile_offsets"),
                            C.byref(m), _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),

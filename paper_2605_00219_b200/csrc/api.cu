@@ -94,7 +94,7 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
                  vks_stream_t stream) {
     if (!camera_ok(cam) || n < 0 || capacity < 0 || !num_isects || !tile_offsets) return VKS_ERR_INVALID_ARG;
     if (n > 0 && (!means2d || !radii || !depths || !tiles_touched || !offsets)) return VKS_ERR_INVALID_ARG;
-    if (capacity > 0 && (!keys || !vals)) return VKS_ERR_INVALID_ARG;
+    if (capacity > 0 && !vals) return VKS_ERR_INVALID_ARG;  // keys is optional
     if (!workspace) return VKS_ERR_WORKSPACE;
     if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
         return VKS_ERR_INVALID_ARG;

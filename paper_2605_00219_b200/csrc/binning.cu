@@ -1,22 +1,31 @@
 // binning.cu — "Index Offset", "Generate Keys", "Sorting" and
-// "Tile Ranges"; DESIGN.md §4.3 and §6.
+// "Tile Ranges"; DESIGN.md §4.2 and §6.
 //
-//  1. scan_kernel     single-pass exclusive prefix sum of tiles_touched with decoupled look-back
-//                     (dynamic tile ids for forward progress); writes offsets and M.
-//  2. keys_kernel     warp-cooperative key generation: each warp expands the tile rects of its 32
-//                     Gaussians into contiguous slots with coalesced 8+4-byte stores.  It also
-//                     builds (a) the radix histograms of the 4 depth-bit digits, weighted by
-//                     tiles_touched (every key of a Gaussian shares its depth bits), and (b) a 2-D
-//                     difference array of the tile rects.
-//  3. tile_count_kernel  one block: 2-D prefix of the difference array = per-tile list lengths ->
-//                     CSR tile_offsets (exclusive scan; identical to boundary detection on the
-//                     sorted keys because the sort is tile-major) and the tile-digit histograms;
-//                     exclusive scans of all digit histograms.
-//  4. onesweep_pass   LSD radix sort, 8-bit digits, P = ceil((32 + ceil(log2 n_tiles)) / 8)
-//                     passes.  Per 4096-key tile: warp-level __match_any_sync ranking (stable),
-//                     decoupled look-back across dynamically numbered tiles per digit, local
-//                     reordering in shared memory so global stores are digit-contiguous runs.
-// The binning TU is compiled with -fmad=false (the rect recomputation must equal projection's).
+// Result (identical to a stable sort of the (tile << 32 | f32bits(depth)) keys generated at
+// slots offsets[i] + k, rows outer / columns inner): the Gaussian ids of every tile list in
+// ascending (depth bits, id) order, plus CSR tile ranges.  B200 design — "depth-major" binning:
+// every key of a Gaussian shares its depth bits, so the 32 depth bits are sorted over the N
+// Gaussians (16 B/Gaussian per pass) instead of over the M ~ 4.4 N keys, and only the tile bits
+// are sorted over the keys:
+//
+//  1. scan_kernel<false>  exclusive scan of tiles_touched in id order (decoupled look-back,
+//                         dynamic tile ids) -> offsets, M; counts V and builds the four depth-digit
+//                         histograms (culled Gaussians take the key 0xFFFFFFFF and sort last).
+//  2. onesweep x4         8-bit LSD passes over (depth key, id) of all N Gaussians; pass 0 derives
+//                         the keys from tiles_touched / depths on the fly.
+//  3. scan_kernel<true>   exclusive scan of tiles_touched in depth order (gathered through the
+//                         sorted ids) -> slot of each Gaussian's first key.
+//  4. keys_kernel         warp-cooperative expansion of the tile rects in depth order into
+//                         (tile, id) pairs with coalesced stores; 2-D difference array of the
+//                         rects accumulated per block in shared memory.
+//  5. tile_count_kernel   2-D prefix of the difference array -> per-tile list lengths -> CSR
+//                         tile_offsets and the tile-digit histograms.
+//  6. onesweep x1-3       stable LSD passes over the tile bits (<= 8 bits each) of the M pairs;
+//                         the last one writes the ids (and, on request, the u64 keys).
+// Every onesweep pass: TMA bulk copies of the tile into shared memory (mbarrier completion),
+// warp-level __match_any_sync ranking (stable), per-digit decoupled look-back (chunked), in-place
+// shared-memory reorder so the global stores are digit-contiguous runs.
+// The TU is compiled with -fmad=false (the tile-rect recomputation must equal projection's).
 #include <stdlib.h>
 
 #include <algorithm>
@@ -35,10 +44,10 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortMinItems = 8;                              // smallest tile (workspace sizing)
-constexpr int kSortMinTile = kSortThreads * kSortMinItems;  // 2048 keys
-constexpr int kMaxPasses = 8;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per block
 constexpr int kDepthPasses = 4;
+constexpr int kMaxTilePasses = 3;
 constexpr int kLookbackChunk = 8;
 
 constexpr u64 kScanFlagAgg = 1ull << 62;
@@ -50,79 +59,134 @@ constexpr u32 kLbMask = (1u << 30) - 1;
 
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+struct TilePlan {
+    int passes;  // 0..3
+    int dbits;   // bits per tile pass (<= 8)
+};
+
+TilePlan tile_plan(int32_t n_tiles) {
+    int tb = 0;
+    while ((1ll << tb) < (int64_t)n_tiles) tb++;
+    TilePlan p{0, 0};
+    if (tb == 0) return p;
+    p.passes = (tb + 7) / 8;
+    p.dbits = (tb + p.passes - 1) / p.passes;
+    return p;
+}
+
 struct Workspace {
-    u64* keys_x;
-    u32* vals_x;
-    // zeroed every call (region A)
-    u64* scan_lb;
-    u32* scan_ctr;
-    u64* total;
-    u32* hist;     // [kMaxPasses][256]
-    int* diff;     // [(TY+1)*(TX+1)]
-    // zeroed once M is known (region B)
-    u32* sort_ctr; // [kMaxPasses]
-    u32* sort_lb;  // [kMaxPasses][sort tiles][256]
-    u32* gstart;   // [kMaxPasses][256]
+    u32 *dk[2], *dv[2];  // depth sort ping-pong [n]
+    u32* doff;           // depth-order slot offsets [n]
+    u32 *tk[2], *tv[2];  // tile sort ping-pong [capacity]
+    u32* gstart;         // [kDepthPasses + kMaxTilePasses][256]
+    // region A (zeroed before the scan)
+    u64* scan_lb;        // id-order scan
+    u64* dscan_lb;       // depth-order scan
+    u32* ctr;            // [16] tile counters of every pass and both scans
+    u64* totals;         // [2]: M, V
+    u32* hist;           // [kDepthPasses][256]
+    int* diff;           // [(TY+1)*(TX+1)]
+    u32* depth_lb;       // [kDepthPasses][sort tiles of n][256]
     size_t zeroA_bytes;
     char* zeroA;
+    // region B (zeroed once M is known)
+    u32* tile_lb;        // [kMaxTilePasses][sort tiles of M][256]
     char* zeroB;
     size_t bytes;
 };
 
-Workspace carve(void* base, int64_t n, int64_t capacity, int32_t n_tiles, int TX, int TY) {
+Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
     Workspace w{};
     size_t off = 0;
     char* b = static_cast<char*>(base);
     auto take = [&](size_t bytes) { char* p = b ? b + off : nullptr; off += align_up(bytes); return p; };
-    const int64_t scan_tiles = (n + kScanTile - 1) / kScanTile;
-    const int64_t sort_tiles = (capacity + kSortMinTile - 1) / kSortMinTile;
-    w.keys_x = reinterpret_cast<u64*>(take(sizeof(u64) * (size_t)capacity));
-    w.vals_x = reinterpret_cast<u32*>(take(sizeof(u32) * (size_t)capacity));
-    w.gstart = reinterpret_cast<u32*>(take(sizeof(u32) * kMaxPasses * 256));
+    const size_t nn = (size_t)(n > 0 ? n : 1), cap = (size_t)(capacity > 0 ? capacity : 1);
+    const size_t scan_tiles = (nn + kScanTile - 1) / kScanTile;
+    const size_t nsort_tiles = (nn + kSortTile - 1) / kSortTile;
+    const size_t csort_tiles = (cap + kSortTile - 1) / kSortTile;
+    for (int i = 0; i < 2; i++) {
+        w.dk[i] = reinterpret_cast<u32*>(take(4 * nn));
+        w.dv[i] = reinterpret_cast<u32*>(take(4 * nn));
+    }
+    w.doff = reinterpret_cast<u32*>(take(4 * nn));
+    for (int i = 0; i < 2; i++) {
+        w.tk[i] = reinterpret_cast<u32*>(take(4 * cap));
+        w.tv[i] = reinterpret_cast<u32*>(take(4 * cap));
+    }
+    w.gstart = reinterpret_cast<u32*>(take(4 * 256 * (kDepthPasses + kMaxTilePasses)));
     const size_t a0 = off;
     w.zeroA = b ? b + off : nullptr;
-    w.scan_lb = reinterpret_cast<u64*>(take(sizeof(u64) * (size_t)(scan_tiles > 0 ? scan_tiles : 1)));
-    w.scan_ctr = reinterpret_cast<u32*>(take(sizeof(u32) * 4));
-    w.total = reinterpret_cast<u64*>(take(sizeof(u64)));
-    w.hist = reinterpret_cast<u32*>(take(sizeof(u32) * kMaxPasses * 256));
-    w.diff = reinterpret_cast<int*>(take(sizeof(int) * (size_t)(TX + 1) * (TY + 1)));
+    w.scan_lb = reinterpret_cast<u64*>(take(8 * scan_tiles));
+    w.dscan_lb = reinterpret_cast<u64*>(take(8 * scan_tiles));
+    w.ctr = reinterpret_cast<u32*>(take(4 * 16));
+    w.totals = reinterpret_cast<u64*>(take(8 * 2));
+    w.hist = reinterpret_cast<u32*>(take(4 * 256 * kDepthPasses));
+    w.diff = reinterpret_cast<int*>(take(4 * (size_t)(TX + 1) * (TY + 1)));
+    w.depth_lb = reinterpret_cast<u32*>(take(4 * 256 * kDepthPasses * nsort_tiles));
     w.zeroA_bytes = off - a0;
     w.zeroB = b ? b + off : nullptr;
-    w.sort_ctr = reinterpret_cast<u32*>(take(sizeof(u32) * kMaxPasses));
-    w.sort_lb = reinterpret_cast<u32*>(take(sizeof(u32) * (size_t)kMaxPasses * 256 * (size_t)(sort_tiles > 0 ? sort_tiles : 1)));
+    w.tile_lb = reinterpret_cast<u32*>(take(4 * 256 * kMaxTilePasses * csort_tiles));
     w.bytes = off;
-    (void)n_tiles;
     return w;
 }
 
+// counter slots in w.ctr
+enum { kCtrScan = 0, kCtrDscan = 1, kCtrDepth = 2, kCtrTile = 2 + kDepthPasses };
+
+__device__ __forceinline__ int sat_tiles(int t) { return t > 0 ? t : 0; }
+
 // ------------------------------------------------------------------------------------------
-// 1. exclusive scan (decoupled look-back)
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(const int* __restrict__ in, u32* __restrict__ out,
-                                                           int64_t n, u64* __restrict__ lb, u32* __restrict__ ctr,
-                                                           u64* __restrict__ total) {
+// 1./3. exclusive scan of tiles_touched (decoupled look-back, one thread walks chunks back).
+//   GATHER = false: id order; also V, the depth-digit histograms of all N keys.
+//   GATHER = true : depth order, element r = tiles[sid[r]] for r < count.
+template <bool GATHER>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(const int* __restrict__ tiles, const u32* __restrict__ sid,
+                                                           const float* __restrict__ depths, u32* __restrict__ out,
+                                                           int64_t count, u64* __restrict__ lb, u32* __restrict__ ctr,
+                                                           u64* __restrict__ totals, u32* __restrict__ hist) {
     __shared__ u32 s_tile;
     __shared__ u64 s_warp[kScanThreads / 32];
     __shared__ u64 s_prefix;
+    __shared__ u32 s_hist[GATHER ? 1 : kDepthPasses][256];
+    __shared__ u32 s_vis;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(ctr, 1u);
+    if (tid == 0) { s_tile = atomicAdd(ctr, 1u); s_vis = 0; }
+    if (!GATHER)
+        for (int j = tid; j < kDepthPasses * 256; j += kScanThreads) (&s_hist[0][0])[j] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t base = tile * kScanTile + (int64_t)tid * kScanItems;
     int v[kScanItems];
-    if (base + kScanItems <= n && ((reinterpret_cast<uintptr_t>(in + base) & 15) == 0)) {
+    if (!GATHER && base + kScanItems <= count && ((reinterpret_cast<uintptr_t>(tiles + base) & 15) == 0)) {
 #pragma unroll
         for (int j = 0; j < kScanItems; j += 4) {
-            int4 q = __ldg(reinterpret_cast<const int4*>(in + base + j));
+            int4 q = __ldg(reinterpret_cast<const int4*>(tiles + base + j));
             v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < kScanItems; j++) v[j] = (base + j < n) ? __ldg(in + base + j) : 0;
+        for (int j = 0; j < kScanItems; j++) {
+            const int64_t e = base + j;
+            v[j] = e < count ? (GATHER ? __ldg(tiles + __ldg(sid + e)) : __ldg(tiles + e)) : 0;
+        }
     }
     u64 tsum = 0;
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) tsum += (u32)v[j];
-    // block scan of thread sums
+    for (int j = 0; j < kScanItems; j++) tsum += (u32)sat_tiles(v[j]);
+    if (!GATHER) {
+        u32 nvis = 0;
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++) {
+            const int64_t e = base + j;
+            if (e < count) {
+                const u32 key = v[j] > 0 ? __float_as_uint(__ldg(depths + e)) : 0xFFFFFFFFu;
+                nvis += v[j] > 0;
+#pragma unroll
+                for (int p = 0; p < kDepthPasses; p++) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
+            }
+        }
+        if (nvis) atomicAdd(&s_vis, nvis);
+    }
     u64 incl = tsum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -144,81 +208,125 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const int* __restric
         } else {
             st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagAgg | btotal);
             int64_t j = tile - 1;
-            while (true) {
-                u64 s = ld_volatile_u64(reinterpret_cast<const unsigned long long*>(lb + j));
-                const u64 f = s & ~kScanMask;
-                if (f == 0) continue;
-                excl += s & kScanMask;
-                if (f == kScanFlagInc) break;
-                j--;
+            bool found = false;
+            while (!found) {
+                u64 st[kLookbackChunk];
+#pragma unroll
+                for (int q = 0; q < kLookbackChunk; q++)
+                    st[q] = (j - q >= 0) ? ld_volatile_u64(reinterpret_cast<const unsigned long long*>(lb + j - q)) : 0;
+                int consumed = 0;
+#pragma unroll
+                for (int q = 0; q < kLookbackChunk; q++) {
+                    if (found || consumed < q) break;
+                    const u64 f = st[q] & ~kScanMask;
+                    if (f == 0) break;
+                    excl += st[q] & kScanMask;
+                    consumed = q + 1;
+                    if (f == kScanFlagInc) found = true;
+                }
+                j -= consumed;
             }
             st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagInc | (excl + btotal));
         }
         s_prefix = excl;
-        if ((tile + 1) * kScanTile >= n) *total = excl + btotal;
+        if ((tile + 1) * kScanTile >= count) totals[0] = excl + btotal;
+        if (!GATHER && s_vis) atomicAdd(totals + 1, (u64)s_vis);
     }
     __syncthreads();
     u64 run = s_prefix + wpre + (incl - tsum);
 #pragma unroll
     for (int j = 0; j < kScanItems; j++) {
-        if (base + j < n) out[base + j] = (u32)run;
-        run += (u32)v[j];
+        if (base + j < count) out[base + j] = (u32)run;
+        run += (u32)sat_tiles(v[j]);
+    }
+    if (!GATHER) {
+        for (int j = tid; j < kDepthPasses * 256; j += kScanThreads) {
+            const u32 c = (&s_hist[0][0])[j];
+            if (c) atomicAdd(hist + j, c);
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// 2. key generation (+ depth-digit histograms, tile-rect difference array)
-// Persistent grid (a few blocks per SM); each warp takes 32 consecutive Gaussians at a time.  The
-// 2-D difference array of the tile rects is accumulated per block in shared memory and flushed
-// once per block (non-zero cells only), so hot tiles near the image centre see ~#blocks global
-// atomics instead of ~#Gaussians.  Grids too large for shared memory use global atomics.
+// digit start offsets of the depth passes (one block per pass)
+__global__ void hist_scan_kernel(const u32* __restrict__ hist, u32* __restrict__ gstart) {
+    const int p = blockIdx.x, d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    __shared__ u32 s_w[8];
+    const u32 c = hist[p * 256 + d];
+    u32 incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(VKS_FULL_MASK, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    u32 wpre = 0;
+    for (int w = 0; w < warp; w++) wpre += s_w[w];
+    gstart[p * 256 + d] = wpre + incl - c;
+}
+
+// ------------------------------------------------------------------------------------------
+// 4. key generation (+ tile-rect difference array)
 constexpr int kKeysThreads = 512;
 constexpr int kKeysWarps = kKeysThreads / 32;
 constexpr int kKeysSmemDiffMax = 160 * 1024 / 4;  // cells
 
-template <bool SMEM_DIFF>
-__global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int64_t n, const float2* __restrict__ means2d,
+// tile rect recomputed exactly as projection step 11
+__device__ __forceinline__ void rect_of(const float2 m, const int2 r, int TX, int TY, int& x0, int& x1, int& y0,
+                                        int& y1) {
+    const float rx = (float)r.x, ry = (float)r.y;
+    x0 = (int)fminf(fmaxf(floorf((m.x - rx) * 0.0625f), 0.0f), (float)TX);
+    x1 = (int)fminf(fmaxf(ceilf((m.x + rx) * 0.0625f), 0.0f), (float)TX);
+    y0 = (int)fminf(fmaxf(floorf((m.y - ry) * 0.0625f), 0.0f), (float)TY);
+    y1 = (int)fminf(fmaxf(ceilf((m.y + ry) * 0.0625f), 0.0f), (float)TY);
+}
+
+// MODE 0: depth order (sid): (tile, id) pairs at slot0[r] + k, plus the difference array.
+// MODE 1: id order (debug keys_unsorted / vals_unsorted): u64 keys at slot0[i] + k.
+template <bool SMEM_DIFF, int MODE>
+__global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int64_t count, const u32* __restrict__ sid,
+                                                           const float2* __restrict__ means2d,
                                                            const int2* __restrict__ radii, const float* __restrict__ depths,
-                                                           const int* __restrict__ tiles, const u32* __restrict__ offsets,
-                                                           u64* __restrict__ keys, u32* __restrict__ vals,
-                                                           u32* __restrict__ hist, int* __restrict__ diff) {
+                                                           const int* __restrict__ tiles, const u32* __restrict__ slot0,
+                                                           u32* __restrict__ tkeys, u32* __restrict__ tvals,
+                                                           u64* __restrict__ keys64, int* __restrict__ diff) {
     extern __shared__ int s_diff[];
-    __shared__ u32 s_hist[kDepthPasses][256];
     __shared__ int s_incl[kKeysWarps][32];
     __shared__ int s_x0[kKeysWarps][32], s_y0[kKeysWarps][32], s_w[kKeysWarps][32];
+    __shared__ u32 s_id[kKeysWarps][32];
     __shared__ u32 s_db[kKeysWarps][32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int TX = tiles_x(cam), TY = tiles_y(cam);
     const int W1 = TX + 1;
     const int cells = W1 * (TY + 1);
-    for (int j = tid; j < kDepthPasses * 256; j += kKeysThreads) (&s_hist[0][0])[j] = 0;
-    if (SMEM_DIFF)
+    if (SMEM_DIFF) {
         for (int j = tid; j < cells; j += kKeysThreads) s_diff[j] = 0;
-    __syncthreads();
+        __syncthreads();
+    }
     int* dd = SMEM_DIFF ? s_diff : diff;
     const int64_t stride = (int64_t)gridDim.x * kKeysWarps * 32;
-    for (int64_t g0 = ((int64_t)blockIdx.x * kKeysWarps + warp) * 32; g0 < n; g0 += stride) {
-        const int64_t g = g0 + lane;
+    for (int64_t r0 = ((int64_t)blockIdx.x * kKeysWarps + warp) * 32; r0 < count; r0 += stride) {
+        const int64_t r = r0 + lane;
         int cnt = 0, x0 = 0, y0 = 0, w = 1;
-        u32 db = 0;
-        if (g < n) {
+        u32 g = 0, db = 0;
+        if (r < count) {
+            g = MODE == 0 ? __ldg(sid + r) : (u32)r;
             cnt = __ldg(tiles + g);
             if (cnt > 0) {
-                const float2 m = __ldg(means2d + g);
-                const int2 r = __ldg(radii + g);
-                const float rx = (float)r.x, ry = (float)r.y;
-                x0 = (int)fminf(fmaxf(floorf((m.x - rx) * 0.0625f), 0.0f), (float)TX);
-                const int x1 = (int)fminf(fmaxf(ceilf((m.x + rx) * 0.0625f), 0.0f), (float)TX);
-                y0 = (int)fminf(fmaxf(floorf((m.y - ry) * 0.0625f), 0.0f), (float)TY);
-                const int y1 = (int)fminf(fmaxf(ceilf((m.y + ry) * 0.0625f), 0.0f), (float)TY);
+                int x1, y1;
+                rect_of(__ldg(means2d + g), __ldg(radii + g), TX, TY, x0, x1, y0, y1);
                 w = x1 - x0;
-                db = __float_as_uint(__ldg(depths + g));
-#pragma unroll
-                for (int p = 0; p < kDepthPasses; p++) atomicAdd(&s_hist[p][(db >> (8 * p)) & 255u], (u32)cnt);
-                atomicAdd(dd + y0 * W1 + x0, 1);
-                atomicAdd(dd + y0 * W1 + x1, -1);
-                atomicAdd(dd + y1 * W1 + x0, -1);
-                atomicAdd(dd + y1 * W1 + x1, 1);
+                if (MODE == 0) {
+                    atomicAdd(dd + y0 * W1 + x0, 1);
+                    atomicAdd(dd + y0 * W1 + x1, -1);
+                    atomicAdd(dd + y1 * W1 + x0, -1);
+                    atomicAdd(dd + y1 * W1 + x1, 1);
+                } else {
+                    db = __float_as_uint(__ldg(depths + g));
+                }
+            } else {
+                cnt = 0;
             }
         }
         int incl = cnt;
@@ -234,30 +342,28 @@ __global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int6
         s_x0[warp][lane] = x0;
         s_y0[warp][lane] = y0;
         s_w[warp][lane] = w;
+        s_id[warp][lane] = g;
         s_db[warp][lane] = db;
         __syncwarp();
-        const u64 base = (u64)__ldg(offsets + g0);
+        const u64 base = (u64)__ldg(slot0 + r0);  // slot of the group's first Gaussian (even if empty)
         for (int e = lane; e < total; e += 32) {
             int pos = 0;
 #pragma unroll
             for (int step = 16; step >= 1; step >>= 1)
                 if (s_incl[warp][pos + step - 1] <= e) pos += step;
-            const int k = e - (pos ? s_incl[warp][pos - 1] : 0);  // index within Gaussian pos's rect
+            const int k = e - (pos ? s_incl[warp][pos - 1] : 0);  // index within the rect, rows outer
             const int ww = s_w[warp][pos];
             const int ry = k / ww;
             const int tx = s_x0[warp][pos] + (k - ry * ww);
             const int ty = s_y0[warp][pos] + ry;
-            const u64 tile = (u64)(ty * TX + tx);
-            keys[base + e] = (tile << 32) | (u64)s_db[warp][pos];
-            vals[base + e] = (u32)(g0 + pos);
+            const u32 t = (u32)(ty * TX + tx);
+            if (MODE == 0) tkeys[base + e] = t;
+            else keys64[base + e] = ((u64)t << 32) | (u64)s_db[warp][pos];
+            tvals[base + e] = s_id[warp][pos];
         }
     }
-    __syncthreads();
-    for (int j = tid; j < kDepthPasses * 256; j += kKeysThreads) {
-        const u32 c = (&s_hist[0][0])[j];
-        if (c) atomicAdd(hist + j, c);
-    }
     if (SMEM_DIFF) {
+        __syncthreads();
         for (int j = tid; j < cells; j += kKeysThreads) {
             const int v = s_diff[j];
             if (v) atomicAdd(diff + j, v);
@@ -266,17 +372,16 @@ __global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int6
 }
 
 // ------------------------------------------------------------------------------------------
-// 3. per-tile counts -> CSR tile_offsets + tile-digit histograms + digit start offsets
-__global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int passes, int* __restrict__ diff,
-                                                         u32* __restrict__ hist, u32* __restrict__ gstart,
-                                                         u32* __restrict__ tile_offsets) {
-    __shared__ u32 s_hist[kMaxPasses - kDepthPasses][256];
+// 5. per-tile counts -> CSR tile_offsets + tile-digit histograms -> digit start offsets
+__global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int passes, int dbits, int* __restrict__ diff,
+                                                         u32* __restrict__ gstart, u32* __restrict__ tile_offsets) {
+    __shared__ u32 s_hist[kMaxTilePasses][256];
     __shared__ u32 s_wsum[32];
     __shared__ u32 s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W1 = TX + 1;
-    for (int j = tid; j < (kMaxPasses - kDepthPasses) * 256; j += 1024) (&s_hist[0][0])[j] = 0;
-    // row prefix (along x), then column prefix (along y): count[ty][tx] = sum diff[<=ty][<=tx]
+    const u32 dmask = (1u << dbits) - 1u;
+    for (int j = tid; j < kMaxTilePasses * 256; j += 1024) (&s_hist[0][0])[j] = 0;
     for (int y = tid; y < TY; y += 1024) {
         int acc = 0;
         for (int x = 0; x < TX; x++) { acc += diff[y * W1 + x]; diff[y * W1 + x] = acc; }
@@ -287,7 +392,6 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int pa
         for (int y = 0; y < TY; y++) { acc += diff[y * W1 + x]; diff[y * W1 + x] = acc; }
     }
     __syncthreads();
-    // exclusive scan of counts in tile-id order + tile-digit histograms
     const int n_tiles = TX * TY;
     if (tid == 0) s_carry = 0;
     __syncthreads();
@@ -296,10 +400,8 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int pa
         u32 c = 0;
         if (t < n_tiles) {
             c = (u32)diff[(t / TX) * W1 + (t % TX)];
-            for (int p = kDepthPasses; p < passes; p++) {
-                const u32 d = ((u32)t >> (8 * (p - kDepthPasses))) & 255u;
-                if (c) atomicAdd(&s_hist[p - kDepthPasses][d], c);
-            }
+            if (c)
+                for (int p = 0; p < passes; p++) atomicAdd(&s_hist[p][((u32)t >> (dbits * p)) & dmask], c);
         }
         u32 incl = c;
 #pragma unroll
@@ -321,10 +423,8 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int pa
         __syncthreads();
     }
     if (tid == 0) tile_offsets[n_tiles] = s_carry;
-    // digit start offsets for every pass
     for (int p = 0; p < passes; p++) {
-        u32 c = 0;
-        if (tid < 256) c = (p < kDepthPasses) ? hist[p * 256 + tid] : s_hist[p - kDepthPasses][tid];
+        const u32 c = tid < 256 ? s_hist[p][tid] : 0u;
         u32 incl = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -343,12 +443,12 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int pa
 }
 
 // ------------------------------------------------------------------------------------------
-// 4. one onesweep pass over 8 bits starting at `shift`
-template <int ITEMS>
+// onesweep pass over DBITS bits starting at `shift` of u32 keys with u32 values
+enum { kPassPlain = 0, kPassDepthFirst = 1, kPassTileLast = 2 };
+
 struct SortSmem {
-    static constexpr int kTile = kSortThreads * ITEMS;
-    alignas(128) u64 keys[kTile];  // input staging (bulk copy), then the digit-reordered tile
-    alignas(128) u32 vals[kTile];
+    alignas(128) u32 keys[kSortTile];  // input staging (bulk copy), then the reordered tile
+    alignas(128) u32 vals[kSortTile];
     u32 whist[kSortWarps][256];
     u32 binstart[256];
     u32 gbase[256];
@@ -357,25 +457,21 @@ struct SortSmem {
     alignas(8) unsigned long long mbar;
 };
 
-__device__ __forceinline__ u32 digit_of(u64 k, int shift) { return (u32)(k >> shift) & 255u; }
-
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 
-// One onesweep pass over 8 bits starting at `shift`.  The tile's keys/values arrive through two
-// TMA bulk copies (cp.async.bulk, completion on an mbarrier) while the block clears its
-// histograms, so no registers are tied up waiting for DRAM; ranks are computed from shared memory
-// with __match_any_sync (stable: warp-striped slot order), per-digit totals are published for the
-// decoupled look-back (chunked), and the tile is reordered in place so the stores are
-// digit-contiguous runs.
-template <int ITEMS>
-__global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restrict__ kin, const u32* __restrict__ vin,
-                                                            u64* __restrict__ kout, u32* __restrict__ vout, u32 M,
-                                                            int shift, const u32* __restrict__ gstart,
-                                                            u32* __restrict__ lookback, u32* __restrict__ tile_ctr) {
-    using Smem = SortSmem<ITEMS>;
-    constexpr int kTile = Smem::kTile;
+// kPassDepthFirst: kin = tiles_touched, vin = depths; key = visible ? f32bits(depth) : ~0, val = id.
+// kPassTileLast: writes only the values (the caller's vals) and, if keys64, the u64 keys.
+template <int DBITS, int MODE>
+__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
+                                                              u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
+                                                              int shift, const u32* __restrict__ gstart,
+                                                              u32* __restrict__ lookback, u32* __restrict__ tile_ctr,
+                                                              const float* __restrict__ depths,
+                                                              u64* __restrict__ keys64) {
+    constexpr int RADIX = 1 << DBITS;
+    constexpr u32 DMASK = RADIX - 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const u32 bar = smem_u32(&S.mbar);
     if (tid == 0) {
@@ -385,14 +481,14 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
     }
     __syncthreads();
     const u32 tile = S.tile;
-    const u64 base = (u64)tile * kTile;
-    const u32 count = (u32)min((u64)kTile, (u64)M - base);
-    const u32 nbulk = count & ~3u;  // 32-byte multiples of keys, 16-byte multiples of values
+    const u64 base = (u64)tile * kSortTile;
+    const u32 count = (u32)min((u64)kSortTile, (u64)n - base);
+    const u32 nbulk = count & ~3u;  // 16-byte multiples
     if (tid == 0) {
         if (nbulk) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nbulk * 12u) : "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nbulk * 8u) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                         ::"r"(smem_u32(S.keys)), "l"(kin + base), "r"(nbulk * 8u), "r"(bar) : "memory");
+                         ::"r"(smem_u32(S.keys)), "l"(kin + base), "r"(nbulk * 4u), "r"(bar) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                          ::"r"(smem_u32(S.vals)), "l"(vin + base), "r"(nbulk * 4u), "r"(bar) : "memory");
         } else {
@@ -400,10 +496,9 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
         }
     }
     for (int j = tid; j < kSortWarps * 256; j += kSortThreads) (&S.whist[0][0])[j] = 0;
-    // tail (< 4 keys) and padding: pads (~0) rank last in digit 255 and land at dest >= M
-    for (u32 j = nbulk + tid; j < (u32)kTile; j += kSortThreads) {
+    for (u32 j = nbulk + tid; j < (u32)kSortTile; j += kSortThreads) {
         const bool ok = j < count;
-        S.keys[j] = ok ? kin[base + j] : ~0ull;
+        S.keys[j] = ok ? kin[base + j] : (MODE == kPassDepthFirst ? 0u : 0xFFFFFFFFu);  // pads rank last
         S.vals[j] = ok ? vin[base + j] : 0u;
     }
     asm volatile(
@@ -411,14 +506,21 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
         "WAIT%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
         "@!p bra WAIT%=;\n\t}" ::"r"(bar) : "memory");
+    if (MODE == kPassDepthFirst) {
+        __syncthreads();
+        for (int j = tid; j < kSortTile; j += kSortThreads) {
+            const int tt = (int)S.keys[j];
+            S.keys[j] = tt > 0 ? S.vals[j] : 0xFFFFFFFFu;  // pads (tt = 0) become ~0 too
+            S.vals[j] = (u32)(base + j);
+        }
+    }
     __syncthreads();
-    // stable warp-level ranking with match.any
-    u32 rank[ITEMS];
+    u32 rank[kSortItems];
     const u32 ltmask = lanemask_lt();
-    const int seg = warp * 32 * ITEMS;
+    const int seg = warp * 32 * kSortItems;
 #pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
-        const u32 d = digit_of(S.keys[seg + i * 32 + lane], shift);
+    for (int i = 0; i < kSortItems; i++) {
+        const u32 d = (S.keys[seg + i * 32 + lane] >> shift) & DMASK;
         const u32 peers = __match_any_sync(VKS_FULL_MASK, d);
         const u32 below = __popc(peers & ltmask);
         const u32 before = S.whist[warp][d];
@@ -428,15 +530,16 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
         __syncwarp();
     }
     __syncthreads();
-    // per-digit totals, warp exclusive offsets, block exclusive digit starts
     u32 total = 0;
+    if (tid < RADIX) {
 #pragma unroll
-    for (int w = 0; w < kSortWarps; w++) {
-        const u32 c = S.whist[w][tid];
-        S.whist[w][tid] = total;
-        total += c;
+        for (int w = 0; w < kSortWarps; w++) {
+            const u32 c = S.whist[w][tid];
+            S.whist[w][tid] = total;
+            total += c;
+        }
+        st_volatile_u32(lookback + (u64)tile * 256 + tid, (tile == 0 ? kLbInc : kLbAgg) | total);
     }
-    st_volatile_u32(lookback + (u64)tile * 256 + tid, (tile == 0 ? kLbInc : kLbAgg) | total);
     u32 incl = total;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -445,14 +548,12 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
     }
     if (lane == 31) S.wsum[warp] = incl;
     __syncthreads();
-    {
+    if (tid < RADIX) {
         u32 wpre = 0;
         for (int w = 0; w < warp; w++) wpre += S.wsum[w];
         const u32 binstart = wpre + incl - total;
         S.binstart[tid] = binstart;
-        // decoupled look-back for digit `tid`, kLookbackChunk predecessors per round trip
-        // Digits absent from this tile need no prefix: they keep their aggregate (0) and
-        // successors walk past them.
+        // decoupled look-back for digit `tid`; digits absent from this tile need no prefix
         u32 excl = 0;
         if (tile > 0 && total > 0) {
             int64_t j = (int64_t)tile - 1;
@@ -465,7 +566,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
                 int consumed = 0;
 #pragma unroll
                 for (int q = 0; q < kLookbackChunk; q++) {
-                    if (found || consumed < q) break;  // stop at the first unpublished entry
+                    if (found || consumed < q) break;
                     const u32 f = st[q] & ~kLbMask;
                     if (f == 0) break;
                     excl += st[q] & kLbMask;
@@ -479,49 +580,118 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_pass(const u64* __restr
         S.gbase[tid] = gstart[tid] + excl - binstart;
     }
     __syncthreads();
-    // reorder the tile in shared memory (read everything first, then write: in place)
-    u64 kk[ITEMS];
-    u32 vv[ITEMS];
+    u32 kk[kSortItems], vv[kSortItems];
 #pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
+    for (int i = 0; i < kSortItems; i++) {
         const int slot = seg + i * 32 + lane;
         kk[i] = S.keys[slot];
         vv[i] = S.vals[slot];
-        rank[i] += S.binstart[digit_of(kk[i], shift)] + S.whist[warp][digit_of(kk[i], shift)];
+        const u32 d = (kk[i] >> shift) & DMASK;
+        rank[i] += S.binstart[d] + S.whist[warp][d];
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < ITEMS; i++) {
+    for (int i = 0; i < kSortItems; i++) {
         S.keys[rank[i]] = kk[i];
         S.vals[rank[i]] = vv[i];
     }
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < ITEMS; r++) {
-        const int j = r * kSortThreads + tid;
-        const u64 key = S.keys[j];
-        const u32 dest = S.gbase[digit_of(key, shift)] + (u32)j;
-        if (dest < M) {
-            kout[dest] = key;
-            vout[dest] = S.vals[j];
+#pragma unroll 4
+    for (int j = tid; j < kSortTile; j += kSortThreads) {
+        const u32 key = S.keys[j];
+        const u32 dest = S.gbase[(key >> shift) & DMASK] + (u32)j;
+        if (dest < n) {
+            const u32 val = S.vals[j];
+            if (MODE != kPassTileLast) kout[dest] = key;
+            vout[dest] = val;
+            if (MODE == kPassTileLast && keys64)
+                keys64[dest] = ((u64)key << 32) | (u64)__float_as_uint(__ldg(depths + val));
         }
     }
 }
 
-int end_bits(int32_t n_tiles) {
-    int tb = 0;
-    while ((1ll << tb) < (int64_t)n_tiles) tb++;
-    return 32 + tb;
+template <int DBITS, int MODE>
+int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift, const u32* gstart,
+                u32* lb, u32* ctr, const float* depths, u64* keys64, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(onesweep_kernel<DBITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(SortSmem)) != cudaSuccess)
+            return VKS_ERR_CUDA;
+        attr = true;
+    }
+    const unsigned blocks = (unsigned)((n + kSortTile - 1) / kSortTile);
+    if (!blocks) return VKS_OK;
+    onesweep_kernel<DBITS, MODE><<<blocks, kSortThreads, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, shift, gstart,
+                                                                               lb, ctr, depths, keys64);
+    return cudaGetLastError() == cudaSuccess ? VKS_OK : VKS_ERR_CUDA;
+}
+
+template <int MODE>
+int launch_tile_pass(int dbits, const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift,
+                     const u32* gstart, u32* lb, u32* ctr, const float* depths, u64* keys64, cudaStream_t s) {
+    switch (dbits) {
+        case 1: return launch_pass<1, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+        case 2: return launch_pass<2, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+        case 3: return launch_pass<3, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+        case 4: return launch_pass<4, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+        case 5: return launch_pass<5, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+        case 6: return launch_pass<6, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+        case 7: return launch_pass<7, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+        default: return launch_pass<8, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+    }
+}
+
+// Single-tile grid: the depth order is the final order; u64 keys = (0 << 32) | depth bits.
+__global__ void keys64_tile0_kernel(const u32* __restrict__ vals, const float* __restrict__ depths, u64* __restrict__ keys,
+                                    u32 m) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) keys[i] = (u64)__float_as_uint(__ldg(depths + vals[i]));
+}
+
+int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <int MODE>
+int launch_keys(const vks_camera& cam, int64_t count, const u32* sid, const float* means2d, const int32_t* radii,
+                const float* depths, const int32_t* tiles, const u32* slot0, u32* tkeys, u32* tvals, u64* keys64,
+                int* diff, cudaStream_t s) {
+    const int TX = tiles_x(cam), TY = tiles_y(cam);
+    const int cells = (TX + 1) * (TY + 1);
+    const int64_t want = (count + kKeysThreads - 1) / kKeysThreads;
+    if (want == 0) return VKS_OK;
+    const float2* m2 = reinterpret_cast<const float2*>(means2d);
+    const int2* r2 = reinterpret_cast<const int2*>(radii);
+    if (MODE == 0 && cells <= kKeysSmemDiffMax) {
+        const size_t sm = sizeof(int) * (size_t)cells;
+        if (sm > 32 * 1024 &&
+            cudaFuncSetAttribute(keys_kernel<true, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+            return VKS_ERR_CUDA;
+        const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 2);
+        keys_kernel<true, MODE><<<blocks, kKeysThreads, sm, s>>>(cam, count, sid, m2, r2, depths, tiles, slot0, tkeys,
+                                                                 tvals, keys64, diff);
+    } else {
+        const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 4);
+        keys_kernel<false, MODE><<<blocks, kKeysThreads, 0, s>>>(cam, count, sid, m2, r2, depths, tiles, slot0, tkeys,
+                                                                 tvals, keys64, diff);
+    }
+    return cudaGetLastError() == cudaSuccess ? VKS_OK : VKS_ERR_CUDA;
 }
 
 }  // namespace
 
 size_t bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles) {
-    // worst-case tile grid for the difference array: n_tiles x 1 or the square root; use n_tiles + 2*sqrt + slack
-    const int side = (int)(n_tiles > 0 ? n_tiles : 1);
-    Workspace w = carve(nullptr, n, capacity, n_tiles, side, 1);
-    // diff array sized (TX+1)(TY+1) <= 2*n_tiles + TX + TY + 1 <= 3*n_tiles + 2 for any TX*TY = n_tiles
-    return w.bytes + align_up(sizeof(int) * (size_t)(2 * side + 2));
+    // worst-case grid shape for the difference array: (TX+1)(TY+1) <= 2 n_tiles + 2
+    Workspace w = carve(nullptr, n, capacity, n_tiles > 0 ? n_tiles : 1, 1);
+    return w.bytes + 1024;
 }
 
 int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const int32_t* radii,
@@ -532,96 +702,89 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     const int TX = tiles_x(cam), TY = tiles_y(cam);
     const int32_t n_tiles = TX * TY;
     if (workspace_bytes < bin_sort_workspace_bytes(n, capacity, n_tiles)) return VKS_ERR_WORKSPACE;
-    Workspace w = carve(workspace, n, capacity, n_tiles, TX, TY);
+    Workspace w = carve(workspace, n, capacity, TX, TY);
     if (cudaMemsetAsync(w.zeroA, 0, w.zeroA_bytes, s) != cudaSuccess) return VKS_ERR_CUDA;
-    // 1. index offsets
-    u64 M = 0;
+    // 1. index offsets in id order, M, V, depth-digit histograms
+    u64 tot[2] = {0, 0};
     if (n > 0) {
         const unsigned blocks = (unsigned)((n + kScanTile - 1) / kScanTile);
-        scan_kernel<<<blocks, kScanThreads, 0, s>>>(tiles_touched, offsets, n, w.scan_lb, w.scan_ctr, w.total);
+        scan_kernel<false><<<blocks, kScanThreads, 0, s>>>(tiles_touched, nullptr, depths, offsets, n, w.scan_lb,
+                                                           w.ctr + kCtrScan, w.totals, w.hist);
         if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
-        if (cudaMemcpyAsync(&M, w.total, sizeof(u64), cudaMemcpyDeviceToHost, s) != cudaSuccess) return VKS_ERR_CUDA;
+        if (cudaMemcpyAsync(tot, w.totals, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess) return VKS_ERR_CUDA;
         if (cudaStreamSynchronize(s) != cudaSuccess) return VKS_ERR_CUDA;
     }
+    const u64 M = tot[0], V = tot[1];
     *num_isects = (int64_t)M;
     if ((int64_t)M > capacity || M >= (1ull << 30)) return VKS_ERR_CAPACITY;
     if (M == 0) {
         if (cudaMemsetAsync(tile_offsets, 0, sizeof(u32) * (n_tiles + 1), s) != cudaSuccess) return VKS_ERR_CUDA;
         return VKS_OK;
     }
-    const int passes = (end_bits(n_tiles) + 7) / 8;
-    // ping-pong so that the last pass lands in the caller's keys/vals
-    u64* ukeys = reinterpret_cast<u64*>(keys);
-    u64* kA = (passes % 2 == 0) ? ukeys : w.keys_x;
-    u32* vA = (passes % 2 == 0) ? vals : w.vals_x;
-    u64* kB = (passes % 2 == 0) ? w.keys_x : ukeys;
-    u32* vB = (passes % 2 == 0) ? w.vals_x : vals;
-    // 2. keys (+ histograms)
+    u64* keys64 = reinterpret_cast<u64*>(keys);
+    // debug: the pre-sort keys in id order, exactly as "Generate Keys" defines them
+    if (keys_unsorted || vals_unsorted) {
+        u32* vtmp = vals_unsorted ? vals_unsorted : w.tv[1];
+        u64* ktmp = keys_unsorted ? reinterpret_cast<u64*>(keys_unsorted) : reinterpret_cast<u64*>(w.tk[0]);
+        int st = launch_keys<1>(cam, n, nullptr, means2d, radii, depths, tiles_touched, offsets, nullptr, vtmp, ktmp,
+                                w.diff, s);
+        if (st) return st;
+    }
+    // 2. depth sort of all n (culled Gaussians key 0xFFFFFFFF, last)
+    hist_scan_kernel<<<kDepthPasses, 256, 0, s>>>(w.hist, w.gstart);
+    if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
+    const size_t lbp = (size_t)256 * ((n + kSortTile - 1) / kSortTile);
+    int st = launch_pass<8, kPassDepthFirst>(reinterpret_cast<const u32*>(tiles_touched),
+                                             reinterpret_cast<const u32*>(depths), w.dk[0], w.dv[0], (u32)n, 0,
+                                             w.gstart, w.depth_lb, w.ctr + kCtrDepth, nullptr, nullptr, s);
+    if (st) return st;
+    for (int p = 1; p < kDepthPasses; p++) {
+        st = launch_pass<8, kPassPlain>(w.dk[(p + 1) & 1], w.dv[(p + 1) & 1], w.dk[p & 1], w.dv[p & 1], (u32)n, 8 * p,
+                                        w.gstart + 256 * p, w.depth_lb + lbp * p, w.ctr + kCtrDepth + p, nullptr,
+                                        nullptr, s);
+        if (st) return st;
+    }
+    const u32* sid = w.dv[(kDepthPasses - 1) & 1];  // ids in (depth, id) order; the first V are visible
+    // 3. slots in depth order
     {
-        const int cells = (TX + 1) * (TY + 1);
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (sms <= 0) sms = 148;
-        }
-        const int64_t want = (n + kKeysThreads - 1) / kKeysThreads;
-        if (cells <= kKeysSmemDiffMax) {
-            const size_t sm = sizeof(int) * (size_t)cells;
-            if (sm > 32 * 1024 &&
-                cudaFuncSetAttribute(keys_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
-                return VKS_ERR_CUDA;
-            const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sms * 2);
-            keys_kernel<true><<<blocks, kKeysThreads, sm, s>>>(cam, n, reinterpret_cast<const float2*>(means2d),
-                                                               reinterpret_cast<const int2*>(radii), depths,
-                                                               tiles_touched, offsets, kA, vA, w.hist, w.diff);
-        } else {
-            const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sms * 4);
-            keys_kernel<false><<<blocks, kKeysThreads, 0, s>>>(cam, n, reinterpret_cast<const float2*>(means2d),
-                                                               reinterpret_cast<const int2*>(radii), depths,
-                                                               tiles_touched, offsets, kA, vA, w.hist, w.diff);
-        }
+        const unsigned blocks = (unsigned)((V + kScanTile - 1) / kScanTile);
+        scan_kernel<true><<<blocks, kScanThreads, 0, s>>>(tiles_touched, sid, nullptr, w.doff, (int64_t)V, w.dscan_lb,
+                                                          w.ctr + kCtrDscan, w.totals, nullptr);
         if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
     }
-    if (keys_unsorted && cudaMemcpyAsync(keys_unsorted, kA, sizeof(u64) * M, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    // 4. (tile, id) pairs in depth order + tile-rect difference array
+    const TilePlan plan = tile_plan(n_tiles);
+    u32* pv0 = plan.passes == 0 ? vals : w.tv[0];
+    st = launch_keys<0>(cam, (int64_t)V, sid, means2d, radii, depths, tiles_touched, w.doff, w.tk[0], pv0, nullptr,
+                        w.diff, s);
+    if (st) return st;
+    // 5. tile counts -> tile ranges, tile-digit starts
+    const size_t lbt = (size_t)256 * ((M + kSortTile - 1) / kSortTile);
+    if (plan.passes > 0 && cudaMemsetAsync(w.zeroB, 0, sizeof(u32) * lbt * plan.passes, s) != cudaSuccess)
         return VKS_ERR_CUDA;
-    if (vals_unsorted && cudaMemcpyAsync(vals_unsorted, vA, sizeof(u32) * M, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-        return VKS_ERR_CUDA;
-    // 3. tile counts -> tile ranges, digit starts
-    static int items = 0;
-    if (!items) {
-        const char* e = getenv("VKS_SORT_ITEMS");
-        items = e ? atoi(e) : 16;
-        if (items != 8 && items != 12 && items != 16) items = 16;
-    }
-    const int tile_keys = kSortThreads * items;
-    const u64 sort_tiles = (M + tile_keys - 1) / tile_keys;
-    const size_t zb = align_up(sizeof(u32) * kMaxPasses) + sizeof(u32) * (size_t)passes * 256 * sort_tiles;
-    if (cudaMemsetAsync(w.zeroB, 0, zb, s) != cudaSuccess) return VKS_ERR_CUDA;
-    tile_count_kernel<<<1, 1024, 0, s>>>(TX, TY, passes, w.diff, w.hist, w.gstart, tile_offsets);
+    u32* gst = w.gstart + 256 * kDepthPasses;
+    tile_count_kernel<<<1, 1024, 0, s>>>(TX, TY, plan.passes, plan.dbits > 0 ? plan.dbits : 1, w.diff, gst, tile_offsets);
     if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
-    // 4. radix passes
-    auto launch = [&](auto kernel, size_t sm) -> int {
-        if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
-            return VKS_ERR_CUDA;
-        for (int p = 0; p < passes; p++) {
-            const u64* kin = (p % 2 == 0) ? kA : kB;
-            const u32* vin = (p % 2 == 0) ? vA : vB;
-            u64* ko = (p % 2 == 0) ? kB : kA;
-            u32* vo = (p % 2 == 0) ? vB : vA;
-            kernel<<<(unsigned)sort_tiles, kSortThreads, sm, s>>>(kin, vin, ko, vo, (u32)M, 8 * p, w.gstart + 256 * p,
-                                                                 w.sort_lb + (size_t)p * 256 * sort_tiles,
-                                                                 w.sort_ctr + p);
+    // 6. stable tile passes; the last writes the caller's vals (+ u64 keys on request)
+    if (plan.passes == 0) {
+        if (keys64) {
+            keys64_tile0_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(vals, depths, keys64, (u32)M);
             if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
         }
         return VKS_OK;
-    };
-    int st = VKS_OK;
-    if (items == 16) st = launch(onesweep_pass<16>, sizeof(SortSmem<16>));
-    else if (items == 12) st = launch(onesweep_pass<12>, sizeof(SortSmem<12>));
-    else st = launch(onesweep_pass<8>, sizeof(SortSmem<8>));
-    if (st != VKS_OK) return st;
+    }
+    for (int p = 0; p < plan.passes; p++) {
+        const u32* kin = w.tk[p & 1];
+        const u32* vin = w.tv[p & 1];
+        const bool last = p == plan.passes - 1;
+        u32* ko = w.tk[(p + 1) & 1];
+        u32* vo = last ? vals : w.tv[(p + 1) & 1];
+        st = last ? launch_tile_pass<kPassTileLast>(plan.dbits, kin, vin, ko, vo, (u32)M, plan.dbits * p, gst + 256 * p,
+                                                    w.tile_lb + lbt * p, w.ctr + kCtrTile + p, depths, keys64, s)
+                  : launch_tile_pass<kPassPlain>(plan.dbits, kin, vin, ko, vo, (u32)M, plan.dbits * p, gst + 256 * p,
+                                                 w.tile_lb + lbt * p, w.ctr + kCtrTile + p, nullptr, nullptr, s);
+        if (st) return st;
+    }
     return VKS_OK;
 }
 

@@ -87,11 +87,14 @@ class ViewRenderer:
         ws = V.vks_bin_sort_workspace_bytes(self.n, self.capacity, self.n_tiles)
         self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
 
-    def forward(self, cfg, cam, P: GaussianParams, keys_unsorted=None, vals_unsorted=None):
+    def forward(self, cfg, cam, P: GaussianParams, keys_unsorted=None, vals_unsorted=None, want_keys=False):
+        """want_keys: also write the sorted u64 (tile|depth) keys (verification only; the
+        rasterizer needs the sorted ids and the tile ranges)."""
         V.vks_project_fwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.means2d,
                           self.conics, self.depths, self.radii, self.tiles, self.colors, self.opacities)
         while True:
-            m = V.vks_bin_sort(cam, self.means2d, self.radii, self.depths, self.tiles, self.offsets, self.keys,
+            m = V.vks_bin_sort(cam, self.means2d, self.radii, self.depths, self.tiles, self.offsets,
+                               self.keys if want_keys else None,
                                self.vals, self.tile_offsets, self.workspace, keys_unsorted, vals_unsorted,
                                raise_capacity=False)
             if m >= 0:

@@ -23,11 +23,11 @@ def run_gpu(scene, cam, cfg, dL=None, capacity=None, debug_unsorted=False):
     n = params.n
     r = P.ViewRenderer(n, cam["width"], cam["height"], capacity=capacity)
     ku = vu = None
-    r.forward(cfg, cam, params)  # may regrow the capacity
+    r.forward(cfg, cam, params, want_keys=True)  # may regrow the capacity
     if debug_unsorted:  # debug outputs must hold `capacity` entries (include/vks.h)
         ku = torch.empty(r.capacity, dtype=torch.uint64, device="cuda")
         vu = torch.empty(r.capacity, dtype=torch.uint32, device="cuda")
-        r.forward(cfg, cam, params, ku, vu)
+        r.forward(cfg, cam, params, ku, vu, want_keys=True)
     out = dict(means2d=r.means2d, conics=r.conics, depths=r.depths, radii=r.radii, tiles_touched=r.tiles,
                colors=r.colors, opacities=r.opacities, offsets=r.offsets, tile_offsets=r.tile_offsets,
                image=r.image, T_final=r.T_final, n_contrib=r.n_contrib)

@@ -9,22 +9,24 @@
 // are sorted over the keys:
 //
 //  1. scan_kernel<false>  exclusive scan of tiles_touched in id order (decoupled look-back,
-//                         dynamic tile ids) -> offsets, M; counts V and builds the four depth-digit
-//                         histograms (culled Gaussians take the key 0xFFFFFFFF and sort last).
-//  2. onesweep x4         8-bit LSD passes over (depth key, id) of all N Gaussians; pass 0 derives
-//                         the keys from tiles_touched / depths on the fly.
+//                         dynamic tile ids) -> offsets, M, V.
+//  2. radix pass x4       8-bit LSD passes over (depth key, id) of all N Gaussians (culled ones
+//                         take the key 0xFFFFFFFF and sort last); pass 0 derives the keys from
+//                         tiles_touched / depths on the fly.
 //  3. scan_kernel<true>   exclusive scan of tiles_touched in depth order (gathered through the
 //                         sorted ids) -> slot of each Gaussian's first key.
 //  4. keys_kernel         warp-cooperative expansion of the tile rects in depth order into
 //                         (tile, id) pairs with coalesced stores; 2-D difference array of the
 //                         rects accumulated per block in shared memory.
 //  5. tile_count_kernel   2-D prefix of the difference array -> per-tile list lengths -> CSR
-//                         tile_offsets and the tile-digit histograms.
-//  6. onesweep x1-3       stable LSD passes over the tile bits (<= 8 bits each) of the M pairs;
+//                         tile_offsets.
+//  6. radix pass x1-3     stable LSD passes over the tile bits (<= 8 bits each) of the M pairs;
 //                         the last one writes the ids (and, on request, the u64 keys).
-// Every onesweep pass: TMA bulk copies of the tile into shared memory (mbarrier completion),
-// warp-level __match_any_sync ranking (stable), per-digit decoupled look-back (chunked), in-place
-// shared-memory reorder so the global stores are digit-contiguous runs.
+// Every radix pass is reduce-then-scan: digit counts per 4096-key block, one exclusive scan of
+// the (digit-major) count matrix, then a scatter kernel (TMA bulk copy of the block into shared
+// memory, warp-level ballot multi-split ranking, in-place reorder, digit-contiguous stores).  No block
+// ever waits on another (a single-pass decoupled look-back over 256 digits walked hundreds of
+// in-flight blocks back on this workload).
 // The TU is compiled with -fmad=false (the tile-rect recomputation must equal projection's).
 #include <stdlib.h>
 
@@ -53,9 +55,6 @@ constexpr int kLookbackChunk = 8;
 constexpr u64 kScanFlagAgg = 1ull << 62;
 constexpr u64 kScanFlagInc = 2ull << 62;
 constexpr u64 kScanMask = (1ull << 62) - 1;
-constexpr u32 kLbAgg = 1u << 30;
-constexpr u32 kLbInc = 2u << 30;
-constexpr u32 kLbMask = (1u << 30) - 1;
 
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -74,24 +73,23 @@ TilePlan tile_plan(int32_t n_tiles) {
     return p;
 }
 
+constexpr int kPasses = kDepthPasses + kMaxTilePasses;
+
 struct Workspace {
     u32 *dk[2], *dv[2];  // depth sort ping-pong [n]
     u32* doff;           // depth-order slot offsets [n]
     u32 *tk[2], *tv[2];  // tile sort ping-pong [capacity]
-    u32* gstart;         // [kDepthPasses + kMaxTilePasses][256]
+    u32* counts;         // [256 * sort tiles] digit counts of the current pass (digit-major)
+    u32* offs;           // its exclusive scan
     // region A (zeroed before the scan)
-    u64* scan_lb;        // id-order scan
-    u64* dscan_lb;       // depth-order scan
-    u32* ctr;            // [16] tile counters of every pass and both scans
+    u64* scan_lb;        // id-order scan look-back
+    u64* dscan_lb;       // depth-order scan look-back
+    u64* cnt_lb[kPasses];  // look-back of each pass's counts scan
+    u32* ctr;            // [16] scan tile counters
     u64* totals;         // [2]: M, V
-    u32* hist;           // [kDepthPasses][256]
     int* diff;           // [(TY+1)*(TX+1)]
-    u32* depth_lb;       // [kDepthPasses][sort tiles of n][256]
     size_t zeroA_bytes;
     char* zeroA;
-    // region B (zeroed once M is known)
-    u32* tile_lb;        // [kMaxTilePasses][sort tiles of M][256]
-    char* zeroB;
     size_t bytes;
 };
 
@@ -102,8 +100,8 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
     auto take = [&](size_t bytes) { char* p = b ? b + off : nullptr; off += align_up(bytes); return p; };
     const size_t nn = (size_t)(n > 0 ? n : 1), cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t scan_tiles = (nn + kScanTile - 1) / kScanTile;
-    const size_t nsort_tiles = (nn + kSortTile - 1) / kSortTile;
-    const size_t csort_tiles = (cap + kSortTile - 1) / kSortTile;
+    const size_t sort_tiles = (std::max(nn, cap) + kSortTile - 1) / kSortTile;
+    const size_t cnt_scan_tiles = (256 * sort_tiles + kScanTile - 1) / kScanTile;
     for (int i = 0; i < 2; i++) {
         w.dk[i] = reinterpret_cast<u32*>(take(4 * nn));
         w.dv[i] = reinterpret_cast<u32*>(take(4 * nn));
@@ -113,46 +111,41 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
         w.tk[i] = reinterpret_cast<u32*>(take(4 * cap));
         w.tv[i] = reinterpret_cast<u32*>(take(4 * cap));
     }
-    w.gstart = reinterpret_cast<u32*>(take(4 * 256 * (kDepthPasses + kMaxTilePasses)));
+    w.counts = reinterpret_cast<u32*>(take(4 * 256 * sort_tiles));
+    w.offs = reinterpret_cast<u32*>(take(4 * 256 * sort_tiles));
     const size_t a0 = off;
     w.zeroA = b ? b + off : nullptr;
     w.scan_lb = reinterpret_cast<u64*>(take(8 * scan_tiles));
     w.dscan_lb = reinterpret_cast<u64*>(take(8 * scan_tiles));
+    for (int p = 0; p < kPasses; p++) w.cnt_lb[p] = reinterpret_cast<u64*>(take(8 * cnt_scan_tiles));
     w.ctr = reinterpret_cast<u32*>(take(4 * 16));
     w.totals = reinterpret_cast<u64*>(take(8 * 2));
-    w.hist = reinterpret_cast<u32*>(take(4 * 256 * kDepthPasses));
     w.diff = reinterpret_cast<int*>(take(4 * (size_t)(TX + 1) * (TY + 1)));
-    w.depth_lb = reinterpret_cast<u32*>(take(4 * 256 * kDepthPasses * nsort_tiles));
     w.zeroA_bytes = off - a0;
-    w.zeroB = b ? b + off : nullptr;
-    w.tile_lb = reinterpret_cast<u32*>(take(4 * 256 * kMaxTilePasses * csort_tiles));
     w.bytes = off;
     return w;
 }
 
 // counter slots in w.ctr
-enum { kCtrScan = 0, kCtrDscan = 1, kCtrDepth = 2, kCtrTile = 2 + kDepthPasses };
+enum { kCtrScan = 0, kCtrDscan = 1, kCtrPass = 2 };  // kCtrPass + p: counts scan of pass p
 
 __device__ __forceinline__ int sat_tiles(int t) { return t > 0 ? t : 0; }
 
 // ------------------------------------------------------------------------------------------
 // 1./3. exclusive scan of tiles_touched (decoupled look-back, one thread walks chunks back).
-//   GATHER = false: id order; also V, the depth-digit histograms of all N keys.
+//   GATHER = false: id order; also V (number of Gaussians with tiles_touched > 0).
 //   GATHER = true : depth order, element r = tiles[sid[r]] for r < count.
 template <bool GATHER>
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(const int* __restrict__ tiles, const u32* __restrict__ sid,
                                                            const float* __restrict__ depths, u32* __restrict__ out,
                                                            int64_t count, u64* __restrict__ lb, u32* __restrict__ ctr,
-                                                           u64* __restrict__ totals, u32* __restrict__ hist) {
+                                                           u64* __restrict__ totals) {
     __shared__ u32 s_tile;
     __shared__ u64 s_warp[kScanThreads / 32];
     __shared__ u64 s_prefix;
-    __shared__ u32 s_hist[GATHER ? 1 : kDepthPasses][256];
     __shared__ u32 s_vis;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) { s_tile = atomicAdd(ctr, 1u); s_vis = 0; }
-    if (!GATHER)
-        for (int j = tid; j < kDepthPasses * 256; j += kScanThreads) (&s_hist[0][0])[j] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t base = tile * kScanTile + (int64_t)tid * kScanItems;
@@ -176,16 +169,9 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const int* __restric
     if (!GATHER) {
         u32 nvis = 0;
 #pragma unroll
-        for (int j = 0; j < kScanItems; j++) {
-            const int64_t e = base + j;
-            if (e < count) {
-                const u32 key = v[j] > 0 ? __float_as_uint(__ldg(depths + e)) : 0xFFFFFFFFu;
-                nvis += v[j] > 0;
-#pragma unroll
-                for (int p = 0; p < kDepthPasses; p++) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
-            }
-        }
-        if (nvis) atomicAdd(&s_vis, nvis);
+        for (int j = 0; j < kScanItems; j++) nvis += v[j] > 0;
+        nvis = __reduce_add_sync(VKS_FULL_MASK, nvis);
+        if (lane == 0 && nvis) atomicAdd(&s_vis, nvis);
     }
     u64 incl = tsum;
 #pragma unroll
@@ -239,31 +225,6 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(const int* __restric
         if (base + j < count) out[base + j] = (u32)run;
         run += (u32)sat_tiles(v[j]);
     }
-    if (!GATHER) {
-        for (int j = tid; j < kDepthPasses * 256; j += kScanThreads) {
-            const u32 c = (&s_hist[0][0])[j];
-            if (c) atomicAdd(hist + j, c);
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// digit start offsets of the depth passes (one block per pass)
-__global__ void hist_scan_kernel(const u32* __restrict__ hist, u32* __restrict__ gstart) {
-    const int p = blockIdx.x, d = threadIdx.x, lane = d & 31, warp = d >> 5;
-    __shared__ u32 s_w[8];
-    const u32 c = hist[p * 256 + d];
-    u32 incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const u32 t = __shfl_up_sync(VKS_FULL_MASK, incl, o);
-        if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_w[warp] = incl;
-    __syncthreads();
-    u32 wpre = 0;
-    for (int w = 0; w < warp; w++) wpre += s_w[w];
-    gstart[p * 256 + d] = wpre + incl - c;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -372,16 +333,13 @@ __global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int6
 }
 
 // ------------------------------------------------------------------------------------------
-// 5. per-tile counts -> CSR tile_offsets + tile-digit histograms -> digit start offsets
-__global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int passes, int dbits, int* __restrict__ diff,
-                                                         u32* __restrict__ gstart, u32* __restrict__ tile_offsets) {
-    __shared__ u32 s_hist[kMaxTilePasses][256];
+// 5. per-tile counts -> CSR tile_offsets
+__global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int* __restrict__ diff,
+                                                         u32* __restrict__ tile_offsets) {
     __shared__ u32 s_wsum[32];
     __shared__ u32 s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W1 = TX + 1;
-    const u32 dmask = (1u << dbits) - 1u;
-    for (int j = tid; j < kMaxTilePasses * 256; j += 1024) (&s_hist[0][0])[j] = 0;
     for (int y = tid; y < TY; y += 1024) {
         int acc = 0;
         for (int x = 0; x < TX; x++) { acc += diff[y * W1 + x]; diff[y * W1 + x] = acc; }
@@ -397,12 +355,7 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int pa
     __syncthreads();
     for (int base = 0; base < n_tiles; base += 1024) {
         const int t = base + tid;
-        u32 c = 0;
-        if (t < n_tiles) {
-            c = (u32)diff[(t / TX) * W1 + (t % TX)];
-            if (c)
-                for (int p = 0; p < passes; p++) atomicAdd(&s_hist[p][((u32)t >> (dbits * p)) & dmask], c);
-        }
+        const u32 c = t < n_tiles ? (u32)diff[(t / TX) * W1 + (t % TX)] : 0u;
         u32 incl = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -423,28 +376,141 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int pa
         __syncthreads();
     }
     if (tid == 0) tile_offsets[n_tiles] = s_carry;
-    for (int p = 0; p < passes; p++) {
-        const u32 c = tid < 256 ? s_hist[p][tid] : 0u;
-        u32 incl = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            u32 v = __shfl_up_sync(VKS_FULL_MASK, incl, d);
-            if (lane >= d) incl += v;
-        }
-        if (tid < 256 && lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        if (tid < 256) {
-            u32 wpre = 0;
-            for (int w = 0; w < warp; w++) wpre += s_wsum[w];
-            gstart[p * 256 + tid] = wpre + incl - c;
-        }
-        __syncthreads();
-    }
 }
 
 // ------------------------------------------------------------------------------------------
-// onesweep pass over DBITS bits starting at `shift` of u32 keys with u32 values
+// LSD radix pass over DBITS bits starting at `shift` of u32 keys with u32 values, as
+// reduce-then-scan (no inter-block waiting):
+//   digit_count_kernel   per 4096-key tile: digit histogram (warp ballot multi-split aggregation)
+//                        -> counts[d * T + tile]
+//   scan_u32_kernel      exclusive scan of counts in digit-major order = global start of
+//                        (digit d, tile t) for every tile and digit
+//   scatter_kernel       per tile: TMA bulk copy of keys/values into shared memory (mbarrier),
+//                        stable warp-level ranking (ballot multi-split), in-place shared-memory
+//                        reorder by digit, digit-contiguous coalesced stores.
 enum { kPassPlain = 0, kPassDepthFirst = 1, kPassTileLast = 2 };
+
+// key of element j of the depth-first pass: visible ? f32bits(depth) : 0xFFFFFFFF (sorts last)
+__device__ __forceinline__ u32 depth_key(int tiles, u32 depth_bits) { return tiles > 0 ? depth_bits : 0xFFFFFFFFu; }
+
+// lanes of the warp holding the same DBITS-bit digit (and the same `valid`): DBITS ballots
+// instead of __match_any_sync, whose cost grows with the number of distinct values
+template <int DBITS>
+__device__ __forceinline__ u32 digit_peers(u32 d, bool valid = true) {
+    u32 peers = __ballot_sync(VKS_FULL_MASK, valid);
+    if (!valid) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < DBITS; b++) {
+        const bool bit = (d >> b) & 1u;
+        const u32 bal = __ballot_sync(VKS_FULL_MASK, bit);
+        peers &= bit ? bal : ~bal;
+    }
+    return peers;
+}
+
+template <int DBITS, int MODE>
+__global__ void __launch_bounds__(kSortThreads) digit_count_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
+                                                                  u32 n, int shift, u32 T, u32* __restrict__ counts) {
+    constexpr int RADIX = 1 << DBITS;
+    constexpr u32 DMASK = RADIX - 1;
+    __shared__ u32 whist[kSortWarps][RADIX];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int j = tid; j < kSortWarps * RADIX; j += kSortThreads) (&whist[0][0])[j] = 0;
+    __syncthreads();
+    const u64 base = (u64)blockIdx.x * kSortTile;
+    const u32 ltmask = lanemask_lt();
+    u32 key[kSortItems];
+#pragma unroll
+    for (int i = 0; i < kSortItems; i++) {  // all loads in flight before any use
+        const u64 idx = base + (u64)i * kSortThreads + tid;
+        key[i] = 0;
+        if (idx < n)
+            key[i] = MODE == kPassDepthFirst ? depth_key((int)__ldg(kin + idx), __ldg(vin + idx)) : __ldg(kin + idx);
+    }
+#pragma unroll
+    for (int i = 0; i < kSortItems; i++) {
+        const bool valid = base + (u64)i * kSortThreads + tid < n;
+        const u32 d = (key[i] >> shift) & DMASK;
+        const u32 peers = digit_peers<DBITS>(d, valid);
+        if (valid && (peers & ltmask) == 0) whist[warp][d] += __popc(peers);
+    }
+    __syncthreads();
+    for (int d = tid; d < RADIX; d += kSortThreads) {
+        u32 c = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; w++) c += whist[w][d];
+        counts[(u64)d * T + blockIdx.x] = c;
+    }
+}
+
+// exclusive scan of a u32 array (decoupled look-back over 4096-element tiles)
+__global__ void __launch_bounds__(kScanThreads) scan_u32_kernel(const u32* __restrict__ in, u32* __restrict__ out,
+                                                               u64 count, u64* __restrict__ lb, u32* __restrict__ ctr) {
+    __shared__ u32 s_tile;
+    __shared__ u64 s_warp[kScanThreads / 32];
+    __shared__ u64 s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(ctr, 1u);
+    __syncthreads();
+    const u64 tile = s_tile;
+    const u64 base = tile * kScanTile + (u64)tid * kScanItems;
+    u32 v[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) v[j] = base + j < count ? __ldg(in + base + j) : 0u;
+    u64 tsum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) tsum += v[j];
+    u64 incl = tsum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        u64 t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    u64 wpre = 0, btotal = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; w++) {
+        if (w < warp) wpre += s_warp[w];
+        btotal += s_warp[w];
+    }
+    if (tid == 0) {
+        u64 excl = 0;
+        if (tile == 0) {
+            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb), kScanFlagInc | btotal);
+        } else {
+            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagAgg | btotal);
+            int64_t j = (int64_t)tile - 1;
+            bool found = false;
+            while (!found) {
+                u64 st[kLookbackChunk];
+#pragma unroll
+                for (int q = 0; q < kLookbackChunk; q++)
+                    st[q] = (j - q >= 0) ? ld_volatile_u64(reinterpret_cast<const unsigned long long*>(lb + j - q)) : 0;
+                int consumed = 0;
+#pragma unroll
+                for (int q = 0; q < kLookbackChunk; q++) {
+                    if (found || consumed < q) break;
+                    const u64 f = st[q] & ~kScanMask;
+                    if (f == 0) break;
+                    excl += st[q] & kScanMask;
+                    consumed = q + 1;
+                    if (f == kScanFlagInc) found = true;
+                }
+                j -= consumed;
+            }
+            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagInc | (excl + btotal));
+        }
+        s_prefix = excl;
+    }
+    __syncthreads();
+    u64 run = s_prefix + wpre + (incl - tsum);
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        if (base + j < count) out[base + j] = (u32)run;
+        run += v[j];
+    }
+}
 
 struct SortSmem {
     alignas(128) u32 keys[kSortTile];  // input staging (bulk copy), then the reordered tile
@@ -453,38 +519,32 @@ struct SortSmem {
     u32 binstart[256];
     u32 gbase[256];
     u32 wsum[kSortWarps];
-    u32 tile;
     alignas(8) unsigned long long mbar;
 };
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 
-// kPassDepthFirst: kin = tiles_touched, vin = depths; key = visible ? f32bits(depth) : ~0, val = id.
+// kPassDepthFirst: kin = tiles_touched, vin = depths; key = depth_key(), value = id.
 // kPassTileLast: writes only the values (the caller's vals) and, if keys64, the u64 keys.
 template <int DBITS, int MODE>
-__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
-                                                              u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
-                                                              int shift, const u32* __restrict__ gstart,
-                                                              u32* __restrict__ lookback, u32* __restrict__ tile_ctr,
-                                                              const float* __restrict__ depths,
-                                                              u64* __restrict__ keys64) {
+__global__ void __launch_bounds__(kSortThreads) scatter_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
+                                                             u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
+                                                             int shift, u32 T, const u32* __restrict__ offs,
+                                                             const float* __restrict__ depths,
+                                                             u64* __restrict__ keys64) {
     constexpr int RADIX = 1 << DBITS;
     constexpr u32 DMASK = RADIX - 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const u32 bar = smem_u32(&S.mbar);
-    if (tid == 0) {
-        S.tile = atomicAdd(tile_ctr, 1u);
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const u32 tile = S.tile;
+    const u32 tile = blockIdx.x;
     const u64 base = (u64)tile * kSortTile;
     const u32 count = (u32)min((u64)kSortTile, (u64)n - base);
     const u32 nbulk = count & ~3u;  // 16-byte multiples
     if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (nbulk) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nbulk * 8u) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -496,11 +556,14 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const u32* __res
         }
     }
     for (int j = tid; j < kSortWarps * 256; j += kSortThreads) (&S.whist[0][0])[j] = 0;
+    // the block's digit starts: global start of (digit, tile) from the scanned counts
+    for (int d = tid; d < RADIX; d += kSortThreads) S.gbase[d] = __ldg(offs + (u64)d * T + tile);
     for (u32 j = nbulk + tid; j < (u32)kSortTile; j += kSortThreads) {
         const bool ok = j < count;
         S.keys[j] = ok ? kin[base + j] : (MODE == kPassDepthFirst ? 0u : 0xFFFFFFFFu);  // pads rank last
         S.vals[j] = ok ? vin[base + j] : 0u;
     }
+    __syncthreads();  // barrier init visible before anyone waits on it
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT%=:\n\t"
@@ -509,8 +572,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const u32* __res
     if (MODE == kPassDepthFirst) {
         __syncthreads();
         for (int j = tid; j < kSortTile; j += kSortThreads) {
-            const int tt = (int)S.keys[j];
-            S.keys[j] = tt > 0 ? S.vals[j] : 0xFFFFFFFFu;  // pads (tt = 0) become ~0 too
+            S.keys[j] = depth_key((int)S.keys[j], S.vals[j]);  // pads (tiles = 0) become ~0 too
             S.vals[j] = (u32)(base + j);
         }
     }
@@ -521,7 +583,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const u32* __res
 #pragma unroll
     for (int i = 0; i < kSortItems; i++) {
         const u32 d = (S.keys[seg + i * 32 + lane] >> shift) & DMASK;
-        const u32 peers = __match_any_sync(VKS_FULL_MASK, d);
+        const u32 peers = digit_peers<DBITS>(d);
         const u32 below = __popc(peers & ltmask);
         const u32 before = S.whist[warp][d];
         rank[i] = before + below;
@@ -538,7 +600,6 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const u32* __res
             S.whist[w][tid] = total;
             total += c;
         }
-        st_volatile_u32(lookback + (u64)tile * 256 + tid, (tile == 0 ? kLbInc : kLbAgg) | total);
     }
     u32 incl = total;
 #pragma unroll
@@ -553,31 +614,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const u32* __res
         for (int w = 0; w < warp; w++) wpre += S.wsum[w];
         const u32 binstart = wpre + incl - total;
         S.binstart[tid] = binstart;
-        // decoupled look-back for digit `tid`; digits absent from this tile need no prefix
-        u32 excl = 0;
-        if (tile > 0 && total > 0) {
-            int64_t j = (int64_t)tile - 1;
-            bool found = false;
-            while (!found) {
-                u32 st[kLookbackChunk];
-#pragma unroll
-                for (int q = 0; q < kLookbackChunk; q++)
-                    st[q] = (j - q >= 0) ? ld_volatile_u32(lookback + (u64)(j - q) * 256 + tid) : 0u;
-                int consumed = 0;
-#pragma unroll
-                for (int q = 0; q < kLookbackChunk; q++) {
-                    if (found || consumed < q) break;
-                    const u32 f = st[q] & ~kLbMask;
-                    if (f == 0) break;
-                    excl += st[q] & kLbMask;
-                    consumed = q + 1;
-                    if (f == kLbInc) found = true;
-                }
-                j -= consumed;
-            }
-            st_volatile_u32(lookback + (u64)tile * 256 + tid, kLbInc | (excl + total));
-        }
-        S.gbase[tid] = gstart[tid] + excl - binstart;
+        S.gbase[tid] -= binstart;
     }
     __syncthreads();
     u32 kk[kSortItems], vv[kSortItems];
@@ -610,35 +647,46 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const u32* __res
     }
 }
 
+struct PassBufs {
+    u32* counts;  // [256 * T]
+    u32* offs;    // [256 * T]
+    u64* lb;      // scan look-back of the counts
+    u32* ctr;     // scan tile counter (zeroed)
+};
+
 template <int DBITS, int MODE>
-int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift, const u32* gstart,
-                u32* lb, u32* ctr, const float* depths, u64* keys64, cudaStream_t s) {
+int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift, const PassBufs& pb,
+                const float* depths, u64* keys64, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(onesweep_kernel<DBITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(scatter_kernel<DBITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(SortSmem)) != cudaSuccess)
             return VKS_ERR_CUDA;
         attr = true;
     }
-    const unsigned blocks = (unsigned)((n + kSortTile - 1) / kSortTile);
-    if (!blocks) return VKS_OK;
-    onesweep_kernel<DBITS, MODE><<<blocks, kSortThreads, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, shift, gstart,
-                                                                               lb, ctr, depths, keys64);
+    const u32 T = (u32)((n + kSortTile - 1) / kSortTile);
+    if (!T) return VKS_OK;
+    digit_count_kernel<DBITS, MODE><<<T, kSortThreads, 0, s>>>(kin, vin, n, shift, T, pb.counts);
+    const u64 cnt = (u64)(1u << DBITS) * T;
+    scan_u32_kernel<<<(unsigned)((cnt + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt,
+                                                                                           pb.lb, pb.ctr);
+    scatter_kernel<DBITS, MODE><<<T, kSortThreads, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, shift, T, pb.offs,
+                                                                         depths, keys64);
     return cudaGetLastError() == cudaSuccess ? VKS_OK : VKS_ERR_CUDA;
 }
 
 template <int MODE>
 int launch_tile_pass(int dbits, const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift,
-                     const u32* gstart, u32* lb, u32* ctr, const float* depths, u64* keys64, cudaStream_t s) {
+                     const PassBufs& pb, const float* depths, u64* keys64, cudaStream_t s) {
     switch (dbits) {
-        case 1: return launch_pass<1, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
-        case 2: return launch_pass<2, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
-        case 3: return launch_pass<3, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
-        case 4: return launch_pass<4, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
-        case 5: return launch_pass<5, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
-        case 6: return launch_pass<6, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
-        case 7: return launch_pass<7, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
-        default: return launch_pass<8, MODE>(kin, vin, kout, vout, n, shift, gstart, lb, ctr, depths, keys64, s);
+        case 1: return launch_pass<1, MODE>(kin, vin, kout, vout, n, shift, pb, depths, keys64, s);
+        case 2: return launch_pass<2, MODE>(kin, vin, kout, vout, n, shift, pb, depths, keys64, s);
+        case 3: return launch_pass<3, MODE>(kin, vin, kout, vout, n, shift, pb, depths, keys64, s);
+        case 4: return launch_pass<4, MODE>(kin, vin, kout, vout, n, shift, pb, depths, keys64, s);
+        case 5: return launch_pass<5, MODE>(kin, vin, kout, vout, n, shift, pb, depths, keys64, s);
+        case 6: return launch_pass<6, MODE>(kin, vin, kout, vout, n, shift, pb, depths, keys64, s);
+        case 7: return launch_pass<7, MODE>(kin, vin, kout, vout, n, shift, pb, depths, keys64, s);
+        default: return launch_pass<8, MODE>(kin, vin, kout, vout, n, shift, pb, depths, keys64, s);
     }
 }
 
@@ -704,12 +752,13 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     if (workspace_bytes < bin_sort_workspace_bytes(n, capacity, n_tiles)) return VKS_ERR_WORKSPACE;
     Workspace w = carve(workspace, n, capacity, TX, TY);
     if (cudaMemsetAsync(w.zeroA, 0, w.zeroA_bytes, s) != cudaSuccess) return VKS_ERR_CUDA;
-    // 1. index offsets in id order, M, V, depth-digit histograms
+    auto pass_bufs = [&](int p) { return PassBufs{w.counts, w.offs, w.cnt_lb[p], w.ctr + kCtrPass + p}; };
+    // 1. index offsets in id order, M, V
     u64 tot[2] = {0, 0};
     if (n > 0) {
         const unsigned blocks = (unsigned)((n + kScanTile - 1) / kScanTile);
         scan_kernel<false><<<blocks, kScanThreads, 0, s>>>(tiles_touched, nullptr, depths, offsets, n, w.scan_lb,
-                                                           w.ctr + kCtrScan, w.totals, w.hist);
+                                                           w.ctr + kCtrScan, w.totals);
         if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
         if (cudaMemcpyAsync(tot, w.totals, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess) return VKS_ERR_CUDA;
         if (cudaStreamSynchronize(s) != cudaSuccess) return VKS_ERR_CUDA;
@@ -730,18 +779,14 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
                                 w.diff, s);
         if (st) return st;
     }
-    // 2. depth sort of all n (culled Gaussians key 0xFFFFFFFF, last)
-    hist_scan_kernel<<<kDepthPasses, 256, 0, s>>>(w.hist, w.gstart);
-    if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
-    const size_t lbp = (size_t)256 * ((n + kSortTile - 1) / kSortTile);
+    // 2. depth sort of all n (culled Gaussians key 0xFFFFFFFF, last); pass 0 reads (tiles, depths)
     int st = launch_pass<8, kPassDepthFirst>(reinterpret_cast<const u32*>(tiles_touched),
                                              reinterpret_cast<const u32*>(depths), w.dk[0], w.dv[0], (u32)n, 0,
-                                             w.gstart, w.depth_lb, w.ctr + kCtrDepth, nullptr, nullptr, s);
+                                             pass_bufs(0), nullptr, nullptr, s);
     if (st) return st;
     for (int p = 1; p < kDepthPasses; p++) {
         st = launch_pass<8, kPassPlain>(w.dk[(p + 1) & 1], w.dv[(p + 1) & 1], w.dk[p & 1], w.dv[p & 1], (u32)n, 8 * p,
-                                        w.gstart + 256 * p, w.depth_lb + lbp * p, w.ctr + kCtrDepth + p, nullptr,
-                                        nullptr, s);
+                                        pass_bufs(p), nullptr, nullptr, s);
         if (st) return st;
     }
     const u32* sid = w.dv[(kDepthPasses - 1) & 1];  // ids in (depth, id) order; the first V are visible
@@ -749,7 +794,7 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     {
         const unsigned blocks = (unsigned)((V + kScanTile - 1) / kScanTile);
         scan_kernel<true><<<blocks, kScanThreads, 0, s>>>(tiles_touched, sid, nullptr, w.doff, (int64_t)V, w.dscan_lb,
-                                                          w.ctr + kCtrDscan, w.totals, nullptr);
+                                                          w.ctr + kCtrDscan, w.totals);
         if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
     }
     // 4. (tile, id) pairs in depth order + tile-rect difference array
@@ -758,12 +803,8 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     st = launch_keys<0>(cam, (int64_t)V, sid, means2d, radii, depths, tiles_touched, w.doff, w.tk[0], pv0, nullptr,
                         w.diff, s);
     if (st) return st;
-    // 5. tile counts -> tile ranges, tile-digit starts
-    const size_t lbt = (size_t)256 * ((M + kSortTile - 1) / kSortTile);
-    if (plan.passes > 0 && cudaMemsetAsync(w.zeroB, 0, sizeof(u32) * lbt * plan.passes, s) != cudaSuccess)
-        return VKS_ERR_CUDA;
-    u32* gst = w.gstart + 256 * kDepthPasses;
-    tile_count_kernel<<<1, 1024, 0, s>>>(TX, TY, plan.passes, plan.dbits > 0 ? plan.dbits : 1, w.diff, gst, tile_offsets);
+    // 5. tile counts -> tile ranges
+    tile_count_kernel<<<1, 1024, 0, s>>>(TX, TY, w.diff, tile_offsets);
     if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
     // 6. stable tile passes; the last writes the caller's vals (+ u64 keys on request)
     if (plan.passes == 0) {
@@ -779,10 +820,10 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
         const bool last = p == plan.passes - 1;
         u32* ko = w.tk[(p + 1) & 1];
         u32* vo = last ? vals : w.tv[(p + 1) & 1];
-        st = last ? launch_tile_pass<kPassTileLast>(plan.dbits, kin, vin, ko, vo, (u32)M, plan.dbits * p, gst + 256 * p,
-                                                    w.tile_lb + lbt * p, w.ctr + kCtrTile + p, depths, keys64, s)
-                  : launch_tile_pass<kPassPlain>(plan.dbits, kin, vin, ko, vo, (u32)M, plan.dbits * p, gst + 256 * p,
-                                                 w.tile_lb + lbt * p, w.ctr + kCtrTile + p, nullptr, nullptr, s);
+        st = last ? launch_tile_pass<kPassTileLast>(plan.dbits, kin, vin, ko, vo, (u32)M, plan.dbits * p,
+                                                    pass_bufs(kDepthPasses + p), depths, keys64, s)
+                  : launch_tile_pass<kPassPlain>(plan.dbits, kin, vin, ko, vo, (u32)M, plan.dbits * p,
+                                                 pass_bufs(kDepthPasses + p), nullptr, nullptr, s);
         if (st) return st;
     }
     return VKS_OK;

@@ -14,13 +14,13 @@
 // ex2.approx here, expf there).  The backward reduces each Gaussian's 9 gradient terms across the
 // warp with a transposed butterfly (14 shuffles instead of 45) and issues 2 atomic instructions per
 // (warp, Gaussian) that any lane touched.
+#include <stdlib.h>
+
 #include "vks_common.cuh"
 
 namespace vks {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarpsPerBlock = kThreads / 32;
 
 // One warp's staged batch of 32 list entries (each warp walks the tile list on its own: no block
 // barriers, so a warp never waits for a slower one and stops as soon as its own pixels are done).
@@ -97,55 +97,71 @@ __device__ __forceinline__ bool eval_alpha(const float4 A, const float4 B, float
     return !(alpha < 1.0f / 255.0f);
 }
 
+// Warp patch: 8 pixels wide x 4*PPT tall; lane (lx, ly) = (lane & 7, lane >> 3) owns the PPT
+// pixels (lx, ly + 4k), k < PPT.  A 16x16 tile has 8/PPT warps.
+template <int PPT>
 struct PixelMap {
-    int x, y;                  // pixel
+    int x, y0;                 // first pixel of the lane
     float wx0, wx1, wy0, wy1;  // warp patch (pixel centres)
 };
 
-__device__ __forceinline__ PixelMap pixel_map(int tile, int TX) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bx = (tile % TX) * kTile + (warp & 1) * 8;
-    const int by = (tile / TX) * kTile + (warp >> 1) * 4;
-    PixelMap m;
+template <int PPT>
+__device__ __forceinline__ PixelMap<PPT> pixel_map(int tile, int TX) {
+    constexpr int kH = 4 * PPT;            // patch height
+    constexpr int kRows = kTile / kH;      // patches per tile column
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int bx = (tile % TX) * kTile + (warp / kRows) * 8;
+    const int by = (tile / TX) * kTile + (warp % kRows) * kH;
+    PixelMap<PPT> m;
     m.x = bx + (lane & 7);
-    m.y = by + (lane >> 3);
+    m.y0 = by + (lane >> 3);
     m.wx0 = (float)bx + 0.5f;
     m.wx1 = (float)bx + 7.5f;
     m.wy0 = (float)by + 0.5f;
-    m.wy1 = (float)by + 3.5f;
+    m.wy1 = (float)(by + kH - 1) + 0.5f;
     return m;
 }
 
-__global__ void __launch_bounds__(kThreads) raster_fwd_kernel(vks_config cfg, vks_camera cam,
-                                                              const float2* __restrict__ means2d,
-                                                              const float* __restrict__ conics,
-                                                              const float* __restrict__ colors,
-                                                              const float* __restrict__ opac,
-                                                              const int2* __restrict__ radii,
-                                                              const uint32_t* __restrict__ vals,
-                                                              const uint32_t* __restrict__ tile_offsets,
-                                                              float* __restrict__ image, float* __restrict__ T_final,
-                                                              int* __restrict__ n_contrib) {
-    __shared__ WarpStage stage[kWarpsPerBlock];
+template <int PPT>
+__global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg, vks_camera cam,
+                                                                 const float2* __restrict__ means2d,
+                                                                 const float* __restrict__ conics,
+                                                                 const float* __restrict__ colors,
+                                                                 const float* __restrict__ opac,
+                                                                 const int2* __restrict__ radii,
+                                                                 const uint32_t* __restrict__ vals,
+                                                                 const uint32_t* __restrict__ tile_offsets,
+                                                                 float* __restrict__ image, float* __restrict__ T_final,
+                                                                 int* __restrict__ n_contrib) {
+    __shared__ WarpStage stage[8 / PPT];
     const int TX = tiles_x(cam);
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
-    const PixelMap pm = pixel_map(tile, TX);
-    const bool inside = pm.x < cam.width && pm.y < cam.height;
+    const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const bool cull = cfg.footprint == VKS_FOOTPRINT_SUPPORT;
-    const float px = (float)pm.x + 0.5f, py = (float)pm.y + 0.5f;
+    const float px = (float)pm.x + 0.5f;
+    float py[PPT], T[PPT], C0[PPT], C1[PPT], C2[PPT];
+    int last[PPT];
+    bool done[PPT];
+#pragma unroll
+    for (int k = 0; k < PPT; k++) {
+        py[k] = (float)(pm.y0 + 4 * k) + 0.5f;
+        T[k] = 1.0f; C0[k] = C1[k] = C2[k] = 0.0f;
+        last[k] = 0;
+        done[k] = !(pm.x < cam.width && pm.y0 + 4 * k < cam.height);
+    }
     const uint32_t start = tile_offsets[tile], end = tile_offsets[tile + 1];
-    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-    int last = 0;
-    bool done = !inside;
     // software pipeline: ids two batches ahead, gathered entries one batch ahead
     uint32_t id_next = (start + lane < end) ? __ldg(vals + start + lane) : 0u;
     Entry e_next;
     if (start + lane < end) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
     id_next = (start + 32 + lane < end) ? __ldg(vals + start + 32 + lane) : 0u;
     for (uint32_t b = start; b < end; b += 32) {
-        if (__all_sync(VKS_FULL_MASK, done)) break;
+        bool all_done = true;
+#pragma unroll
+        for (int k = 0; k < PPT; k++) all_done = all_done && done[k];
+        if (__all_sync(VKS_FULL_MASK, all_done)) break;
         __syncwarp();
         // each lane tests its own entry against the warp patch; the warp then visits only the
         // entries whose support box meets the patch, in list order
@@ -158,26 +174,34 @@ __global__ void __launch_bounds__(kThreads) raster_fwd_kernel(vks_config cfg, vk
         while (live) {
             const int j = __ffs(live) - 1;
             live &= live - 1;
-            if (done) continue;
             const float4 A = s.a[j], B = s.b[j];
-            float dx, dy, G, rG, alpha;
-            if (!eval_alpha(A, B, px, py, dx, dy, G, rG, alpha)) continue;
-            const float aT = alpha * T;
-            C0 = fmaf(B.z, aT, C0);
-            C1 = fmaf(B.w, aT, C1);
-            C2 = fmaf(s.c2[j], aT, C2);
-            T = T * (1.0f - alpha);
-            last = (int)(b - start) + j + 1;
-            if (T < 1e-4f) done = true;
+            const float c2 = s.c2[j];
+#pragma unroll
+            for (int k = 0; k < PPT; k++) {
+                if (done[k]) continue;
+                float dx, dy, G, rG, alpha;
+                if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
+                const float aT = alpha * T[k];
+                C0[k] = fmaf(B.z, aT, C0[k]);
+                C1[k] = fmaf(B.w, aT, C1[k]);
+                C2[k] = fmaf(c2, aT, C2[k]);
+                T[k] = T[k] * (1.0f - alpha);
+                last[k] = (int)(b - start) + j + 1;
+                if (T[k] < 1e-4f) done[k] = true;
+            }
         }
     }
-    if (!inside) return;
-    const size_t pix = (size_t)pm.y * cam.width + pm.x;
-    image[3 * pix + 0] = __fadd_rn(C0, __fmul_rn(T, cfg.bg[0]));
-    image[3 * pix + 1] = __fadd_rn(C1, __fmul_rn(T, cfg.bg[1]));
-    image[3 * pix + 2] = __fadd_rn(C2, __fmul_rn(T, cfg.bg[2]));
-    T_final[pix] = T;
-    n_contrib[pix] = last;
+#pragma unroll
+    for (int k = 0; k < PPT; k++) {
+        const int y = pm.y0 + 4 * k;
+        if (!(pm.x < cam.width && y < cam.height)) continue;
+        const size_t pix = (size_t)y * cam.width + pm.x;
+        image[3 * pix + 0] = __fadd_rn(C0[k], __fmul_rn(T[k], cfg.bg[0]));
+        image[3 * pix + 1] = __fadd_rn(C1[k], __fmul_rn(T[k], cfg.bg[1]));
+        image[3 * pix + 2] = __fadd_rn(C2[k], __fmul_rn(T[k], cfg.bg[2]));
+        T_final[pix] = T[k];
+        n_contrib[pix] = last[k];
+    }
 }
 
 // Transposed butterfly: on return lane L holds the warp sum of v[(L >> 2) & 7] (returned), and
@@ -212,43 +236,59 @@ __device__ __forceinline__ float warp_reduce_8plus1(const float v[8], float& e, 
     return c;
 }
 
-__global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vks_camera cam,
-                                                              const float2* __restrict__ means2d,
-                                                              const float* __restrict__ conics,
-                                                              const float* __restrict__ colors,
-                                                              const float* __restrict__ opac,
-                                                              const int2* __restrict__ radii,
-                                                              const uint32_t* __restrict__ vals,
-                                                              const uint32_t* __restrict__ tile_offsets,
-                                                              const float* __restrict__ T_final,
-                                                              const int* __restrict__ n_contrib,
-                                                              const float* __restrict__ dL_dimage,
-                                                              float* __restrict__ dmeans2d, float* __restrict__ dconics,
-                                                              float* __restrict__ dcolors, float* __restrict__ dopac) {
-    __shared__ WarpStage stage[kWarpsPerBlock];
+template <int PPT>
+__global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg, vks_camera cam,
+                                                                 const float2* __restrict__ means2d,
+                                                                 const float* __restrict__ conics,
+                                                                 const float* __restrict__ colors,
+                                                                 const float* __restrict__ opac,
+                                                                 const int2* __restrict__ radii,
+                                                                 const uint32_t* __restrict__ vals,
+                                                                 const uint32_t* __restrict__ tile_offsets,
+                                                                 const float* __restrict__ T_final,
+                                                                 const int* __restrict__ n_contrib,
+                                                                 const float* __restrict__ dL_dimage,
+                                                                 float* __restrict__ dmeans2d, float* __restrict__ dconics,
+                                                                 float* __restrict__ dcolors, float* __restrict__ dopac) {
+    __shared__ WarpStage stage[8 / PPT];
     const int TX = tiles_x(cam);
     const int tile = blockIdx.x;
     const unsigned lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
-    const PixelMap pm = pixel_map(tile, TX);
-    const bool inside = pm.x < cam.width && pm.y < cam.height;
+    const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const bool cull = cfg.footprint == VKS_FOOTPRINT_SUPPORT;
-    const float px = (float)pm.x + 0.5f, py = (float)pm.y + 0.5f;
+    const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
-    float T = 1.0f, w0 = 0.0f, w1 = 0.0f, w2 = 0.0f;
-    int last = 0;
-    if (inside) {
-        const size_t pix = (size_t)pm.y * cam.width + pm.x;
-        T = T_final[pix];
-        last = n_contrib[pix];
-        w0 = dL_dimage[3 * pix];
-        w1 = dL_dimage[3 * pix + 1];
-        w2 = dL_dimage[3 * pix + 2];
+    float py[PPT], T[PPT], w0[PPT], w1[PPT], w2[PPT], S0[PPT], S1[PPT], S2[PPT];
+    int last[PPT];
+    int lmax = 0;
+#pragma unroll
+    for (int k = 0; k < PPT; k++) {
+        const int y = pm.y0 + 4 * k;
+        py[k] = (float)y + 0.5f;
+        T[k] = 1.0f; w0[k] = w1[k] = w2[k] = 0.0f;
+        last[k] = 0;
+        S0[k] = cfg.bg[0]; S1[k] = cfg.bg[1]; S2[k] = cfg.bg[2];
+        if (pm.x < cam.width && y < cam.height) {
+            const size_t pix = (size_t)y * cam.width + pm.x;
+            T[k] = T_final[pix];
+            last[k] = n_contrib[pix];
+            w0[k] = dL_dimage[3 * pix];
+            w1[k] = dL_dimage[3 * pix + 1];
+            w2[k] = dL_dimage[3 * pix + 2];
+        }
+        lmax = max(lmax, last[k]);
     }
-    float S0 = cfg.bg[0], S1 = cfg.bg[1], S2 = cfg.bg[2];
-    const int wmax = __reduce_max_sync(VKS_FULL_MASK, last);  // positions >= wmax: nobody composited
-    // lane 4k (k < 8) owns gradient term k after the butterfly, lane 1 the opacity term
+    const int wmax = __reduce_max_sync(VKS_FULL_MASK, lmax);  // positions >= wmax: nobody composited
+    // per-lane destination of gradient term k after the butterfly: lane 4k (k < 8) owns term k,
+    // lane 1 the opacity term; dst(g) = base + g * stride
     const int myterm = (lane & 3) == 0 ? (int)(lane >> 2) : (lane == 1 ? 8 : -1);
+    float* tbase = nullptr;
+    int tstride = 0;
+    if (myterm >= 0 && myterm < 2) { tbase = dmeans2d + myterm; tstride = 2; }
+    else if (myterm >= 2 && myterm < 5) { tbase = dconics + (myterm - 2); tstride = 3; }
+    else if (myterm >= 5 && myterm < 8) { tbase = dcolors + (myterm - 5); tstride = 3; }
+    else if (myterm == 8) { tbase = dopac; tstride = 1; }
     // batches of 32 positions, back to front: [bs, bs+32) with bs = wmax-32, wmax-64, ...
     int bs = wmax - 32;
     int p0 = bs + (int)lane;
@@ -276,51 +316,76 @@ __global__ void __launch_bounds__(kThreads) raster_bwd_kernel(vks_config cfg, vk
             const int j = 31 - __clz(live);
             live &= ~(1u << j);
             const int pos = bs + j;
+            const float4 A = s.a[j], B = s.b[j];
+            const float c0 = B.z, c1 = B.w, c2 = s.c2[j];
             float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             float e = 0.0f;
             bool contrib = false;
-            if (pos < last) {
-                const float4 A = s.a[j], B = s.b[j];
+#pragma unroll
+            for (int k = 0; k < PPT; k++) {
+                if (pos >= last[k]) continue;
                 float dx, dy, G, rG, alpha;
-                if (eval_alpha(A, B, px, py, dx, dy, G, rG, alpha)) {
-                    contrib = true;
-                    T = __fdividef(T, 1.0f - alpha);
-                    const float aT = alpha * T;
-                    const float c0 = B.z, c1 = B.w, c2 = s.c2[j];
-                    v[5] = aT * w0;
-                    v[6] = aT * w1;
-                    v[7] = aT * w2;
-                    const float dalpha = T * ((c0 - S0) * w0 + (c1 - S1) * w1 + (c2 - S2) * w2);
-                    S0 = alpha * c0 + (1.0f - alpha) * S0;
-                    S1 = alpha * c1 + (1.0f - alpha) * S1;
-                    S2 = alpha * c2 + (1.0f - alpha) * S2;
-                    if (!(rG > 0.99f)) {
-                        const float dsig = -rG * dalpha;
-                        const float a = 2.0f * A.z, bb = A.w, c = 2.0f * B.x;
-                        v[0] = (a * dx + bb * dy) * dsig;
-                        v[1] = (bb * dx + c * dy) * dsig;
-                        v[2] = 0.5f * dx * dx * dsig;
-                        v[3] = dx * dy * dsig;
-                        v[4] = 0.5f * dy * dy * dsig;
-                        e = G * dalpha;
-                    }
+                if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
+                contrib = true;
+                T[k] = __fdividef(T[k], 1.0f - alpha);
+                const float aT = alpha * T[k];
+                v[5] += aT * w0[k];
+                v[6] += aT * w1[k];
+                v[7] += aT * w2[k];
+                const float dalpha = T[k] * ((c0 - S0[k]) * w0[k] + (c1 - S1[k]) * w1[k] + (c2 - S2[k]) * w2[k]);
+                S0[k] = alpha * c0 + (1.0f - alpha) * S0[k];
+                S1[k] = alpha * c1 + (1.0f - alpha) * S1[k];
+                S2[k] = alpha * c2 + (1.0f - alpha) * S2[k];
+                if (!(rG > 0.99f)) {
+                    const float dsig = -rG * dalpha;
+                    const float a = 2.0f * A.z, bb = A.w, c = 2.0f * B.x;
+                    v[0] += (a * dx + bb * dy) * dsig;
+                    v[1] += (bb * dx + c * dy) * dsig;
+                    v[2] += 0.5f * dx * dx * dsig;
+                    v[3] += dx * dy * dsig;
+                    v[4] += 0.5f * dy * dy * dsig;
+                    e += G * dalpha;
                 }
             }
             if (__any_sync(VKS_FULL_MASK, contrib)) {
                 const float r = warp_reduce_8plus1(v, e, lane);
-                if (myterm >= 0) {
-                    const uint32_t g = s.id[j];
-                    float* dst;
-                    float val = r;
-                    if (myterm < 2) dst = dmeans2d + 2 * (size_t)g + myterm;
-                    else if (myterm < 5) dst = dconics + 3 * (size_t)g + (myterm - 2);
-                    else if (myterm < 8) dst = dcolors + 3 * (size_t)g + (myterm - 5);
-                    else { dst = dopac + g; val = e; }
-                    atomicAdd(dst, val);
-                }
+                if (myterm >= 0) atomicAdd(tbase + (size_t)s.id[j] * tstride, myterm == 8 ? e : r);
             }
         }
     }
+}
+
+template <int PPT>
+int launch_fwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
+               const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
+               const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
+    const int n_tiles = tiles_x(cam) * tiles_y(cam);
+    raster_fwd_kernel<PPT><<<n_tiles, 32 * 8 / PPT, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d),
+                                                             conics, colors, opacities,
+                                                             reinterpret_cast<const int2*>(radii), vals, tile_offsets,
+                                                             image, T_final, n_contrib);
+    return LaunchCheck::check();
+}
+
+template <int PPT>
+int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
+               const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
+               const uint32_t* tile_offsets, const float* T_final, const int32_t* n_contrib,
+               const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
+               cudaStream_t st) {
+    const int n_tiles = tiles_x(cam) * tiles_y(cam);
+    raster_bwd_kernel<PPT><<<n_tiles, 32 * 8 / PPT, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d),
+                                                             conics, colors, opacities,
+                                                             reinterpret_cast<const int2*>(radii), vals, tile_offsets,
+                                                             T_final, n_contrib, dL_dimage, dmeans2d, dconics,
+                                                             dcolors, dopacities);
+    return LaunchCheck::check();
+}
+
+int ppt_choice(const char* var) {
+    const char* e = getenv(var);
+    const int v = e ? atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
 }
 
 }  // namespace
@@ -330,11 +395,12 @@ int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
                       const uint32_t* vals, const uint32_t* tile_offsets, float* image, float* T_final,
                       int32_t* n_contrib, cudaStream_t st) {
     (void)n;
-    const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_fwd_kernel<<<n_tiles, kThreads, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d), conics,
-                                                    colors, opacities, reinterpret_cast<const int2*>(radii), vals,
-                                                    tile_offsets, image, T_final, n_contrib);
-    return LaunchCheck::check();
+    static const int ppt = ppt_choice("VKS_RASTER_FWD_PPT");
+    switch (ppt) {
+        case 1: return launch_fwd<1>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+        case 4: return launch_fwd<4>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+        default: return launch_fwd<2>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+    }
 }
 
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
@@ -343,12 +409,12 @@ int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
                       const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics,
                       float* dcolors, float* dopacities, cudaStream_t st) {
     (void)n;
-    const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_bwd_kernel<<<n_tiles, kThreads, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d), conics,
-                                                    colors, opacities, reinterpret_cast<const int2*>(radii), vals,
-                                                    tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics,
-                                                    dcolors, dopacities);
-    return LaunchCheck::check();
+    static const int ppt = ppt_choice("VKS_RASTER_BWD_PPT");
+    switch (ppt) {
+        case 1: return launch_bwd<1>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+        case 4: return launch_bwd<4>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+        default: return launch_bwd<2>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    }
 }
 
 }  // namespace vks

@@ -98,22 +98,29 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------- algorithmic work
-def algorithmic_bytes(n, vis, m, px, passes, K=16):
-    """Per-view algorithmic HBM bytes of the HBM-bound stages."""
+def algorithmic_bytes(n, vis, m, K=16):
+    """Per-view algorithmic HBM bytes of the HBM-bound stages, for the algorithms as built
+    (DESIGN.md §6).  Parameters are fp32; sh has K coefficients per channel."""
     sh = 12 * K
     return dict(
+        # means for all; log_scales/quats/logit of culled-after-near (upper bound: all culled);
+        # the rest of the parameters (SH only when visible); radii+tiles for all; 40 B of outputs
         project_fwd=12 * n + 28 * (n - vis) + (12 + 16 + 4 + sh) * vis + 12 * n + 40 * vis,
-        scan=8 * n,
-        keys=20 * vis + 12 * m,
-        sort=8 * m + 24 * passes * m,
-        project_bwd=8 * n + vis * ((40 + sh) + 36 + 2 * (40 + sh)),
+        # id-order scan (read tiles twice, write offsets) + 4 depth passes (count: read key,
+        # scatter: read key+id, write key+id; pass 0 reads tiles+depths) + the rect gather of the
+        # last depth pass + depth-order scan + key expansion + 2 tile passes (last writes ids only)
+        bin_sort=(12 * n + 4 * (4 * n + 16 * n) + 4 * n + (16 + 8) * vis + (16 + 4) * vis
+                  + (12 * vis + 8 * m) + (20 * m) + (16 * m)),
+        # overwrite semantics: params + 2D grads + colours of visible, radii of all, 236 B written for all
+        project_bwd=8 * n + vis * ((40 + sh) + 36 + 12) + n * (40 + sh),
     )
 
 
-def raster_flops(e_fwd, c_fwd, e_bwd, c_bwd):
-    """Algorithmic fp32 operations: forward 10 per evaluated pair + 9 per composited
-    one; backward 10 per evaluated pair + 44 per composited one (the 9 gradient terms)."""
-    return dict(raster_fwd=10 * e_fwd + 9 * c_fwd, raster_bwd=10 * e_bwd + 44 * c_bwd)
+def raster_flops(visited, composited, replayed):
+    """Algorithmic fp32 operations: per visited (pixel, Gaussian) pair 12 (sigma 9,
+    exp 1, rho*G 1, clamp 1), per composited pair 9 more in the forward (3 fma + 3); the backward
+    re-evaluates the replayed pairs (12) and spends 50 per composited pair on the 9 gradient terms."""
+    return dict(raster_fwd=12 * visited + 9 * composited, raster_bwd=12 * replayed + 50 * composited)
 
 
 # ----------------------------------------------------------------------------------- ours
@@ -215,53 +222,53 @@ def run_ours(args):
     views_total = world * vpr * args.steps
     value = views_total / (elapsed_ms / 1e3)
 
-    # --- workload statistics (untimed): visible count, M, evaluations, sort-only timing
+    # --- workload statistics (untimed): visible count, M, raster pair counts of the last view
     torch.cuda.synchronize()
     vis = int((rend.tiles > 0).sum().item())
     m_last = rend.num_isects
-    e_stats = raster_work(rend, c.width, c.height)
-    passes = (32 + max(0, math.ceil(math.log2(rend.n_tiles))) + 7) // 8
-    ab = algorithmic_bytes(n, vis, m_last, c.width * c.height, passes)
-    fl = raster_flops(*e_stats)
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    P.vks_raster_fwd_stats(cfg, cams[my_views[(args.warmup + args.steps - 1) % len(my_views)]], rend.means2d,
+                           rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals, rend.tile_offsets, stats)
+    visited, composited, evaluated, replayed = (int(x) for x in stats.tolist())
+    ab = algorithmic_bytes(n, vis, m_last)
+    fl = raster_flops(visited, composited, replayed)
     pk = peaks()
     clock_mhz = clk["sm_mhz"] or pk["sm_max_mhz"]
     fp32_peak_tflops = 148 * 128 * 2 * clock_mhz * 1e6 / 1e12
     per_stage = {}
-    for k in ("project_fwd", "project_bwd"):
+    for k in ("project_fwd", "bin_sort", "project_bwd"):
         gbs = ab[k] / (st_ms[k] * 1e-3) / 1e9
         per_stage[k] = dict(ms=st_ms[k], bound="hbm", achieved=gbs, peak=pk["hbm_gbs"], unit="GB/s",
-                            frac=gbs / pk["hbm_gbs"])
+                            frac=gbs / pk["hbm_gbs"], algorithmic_bytes=ab[k])
+    per_stage["bin_sort"]["gkeys_per_s"] = m_last / (st_ms["bin_sort"] * 1e-3) / 1e9
     for k in ("raster_fwd", "raster_bwd"):
         tf = fl[k] / (st_ms[k] * 1e-3) / 1e12
         per_stage[k] = dict(ms=st_ms[k], bound="alu", achieved=tf, peak=fp32_peak_tflops, unit="TFLOP/s",
-                            frac=tf / fp32_peak_tflops)
-    bs_bytes = ab["scan"] + ab["keys"] + ab["sort"] + 8 * m_last
-    gbs = bs_bytes / (st_ms["bin_sort"] * 1e-3) / 1e9
-    per_stage["bin_sort"] = dict(ms=st_ms["bin_sort"], bound="hbm", achieved=gbs, peak=pk["hbm_gbs"],
-                                 unit="GB/s", frac=gbs / pk["hbm_gbs"],
-                                 gkeys_per_s=m_last / (st_ms["bin_sort"] * 1e-3) / 1e9)
+                            frac=tf / fp32_peak_tflops, algorithmic_flops=fl[k])
     dom = max((k for k in per_stage), key=lambda k: per_stage[k]["ms"])
     d = per_stage[dom]
     roofline = dict(kernel=dom, bound=d["bound"], achieved=round(d["achieved"], 3), peak=round(d["peak"], 3),
                     unit=d["unit"], frac=round(d["frac"], 4), traffic=None,
-                    peak_source=(pk["src"] + (" HBM copy" if d["bound"] == "hbm" else
-                                              f" FP32 148 SM x 128 lanes x 2 x {clock_mhz:.0f} MHz")))
-    gpu_launches = (1 + (3 + passes) + 1 + 1 + 1) * vpr * args.steps
+                    peak_source=(pk["src"] + (" HBM copy (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
+                                              f" FP32 FMA: 148 SM x 128 lanes x 2 flop x {clock_mhz:.0f} MHz")))
+    tp = 2 if rend.n_tiles > 256 else 1
+    gpu_launches = (1 + (3 + 4 * 3 + 3 + 1 + 1 + 3 * tp) + 1 + 1 + 1) * vpr * args.steps
 
     out = dict(metric=METRIC, value=round(value, 3), unit="iters/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(elapsed_ms / args.steps, 4), higher_is_better=True,
                scaling="weak", vs_baseline=None, dtype="f32", data="synthetic",
                config=dict(workload=c.description + ", fwd+bwd", n_gaussians=n, width=c.width,
                            height=c.height, sh_degree=3, footprint="support", views_per_rank=vpr,
-                           visible=vis, num_isects=m_last, sort_passes=passes,
+                           visible=vis, num_isects=m_last,
                            l2="inputs larger than L2 (params 1.37 GB, keys+vals 0.22 GB per view), no flush",
                            parallelism=f"view-sharded dp{world}"),
                stages_ms={k: round(v, 4) for k, v in st_ms.items()},
                stage_roofline={k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                                for k, v in per_stage.items()},
                sort_gkeys_per_s=round(per_stage["bin_sort"]["gkeys_per_s"], 3),
-               raster_work=dict(evals_fwd=e_stats[0], composited_fwd=e_stats[1], evals_bwd=e_stats[2],
-                                composited_bwd=e_stats[3]),
+               hbm_gbs={k: round(per_stage[k]["achieved"], 1) for k in ("project_fwd", "bin_sort", "project_bwd")},
+               raster_work=dict(visited_pairs=visited, composited_pairs=composited, evaluated_pairs=evaluated,
+                                replayed_pairs=replayed),
                roofline=roofline, gpu_launches=gpu_launches, clocks=clk)
 
     if not args.no_e2e:
@@ -273,24 +280,6 @@ def run_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
-
-
-def raster_work(rend, W, H):
-    """Evaluated / composited (pixel, Gaussian) pairs of the last view, from the forward outputs:
-    a pixel evaluates its tile list up to its stop (n_contrib if T < 1e-4, else the whole list)."""
-    import torch
-    TX = (W + 15) // 16
-    to = rend.tile_offsets.view(torch.int32).to(torch.int64)
-    lens = (to[1:] - to[:-1])
-    ys = torch.arange(H, device="cuda").view(-1, 1) // 16
-    xs = torch.arange(W, device="cuda").view(1, -1) // 16
-    tl = lens[(ys * TX + xs)]
-    nc = rend.n_contrib.to(torch.int64)
-    stopped = rend.T_final < 1e-4
-    e_fwd = int(torch.where(stopped, nc, tl).sum().item())
-    e_bwd = int(nc.sum().item())
-    # composited counts are not stored; bound by the evaluated ones (reported as such)
-    return e_fwd, 0, e_bwd, 0
 
 
 def run_e2e(args, P, params, rend, cams, my_views, cfg, c, world):

@@ -161,6 +161,19 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    vks_stream_t stream);
 
 /*
+ * vks_raster_fwd_stats — diagnostic twin of vks_raster_fwd for the roofline model:
+ * runs the same compositing without writing the image and ACCUMULATES into the device counters
+ *   stats[0] += list entries visited before each pixel's stop (the algorithm's evaluations)
+ *   stats[1] += composited (pixel, Gaussian) pairs
+ *   stats[2] += pairs actually evaluated by the kernel (after its patch culling)
+ *   stats[3] += sum of n_contrib (entries the backward replays)
+ */
+int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n,
+                         const float* means2d, const float* conics, const float* colors,
+                         const float* opacities, const int32_t* radii, const uint32_t* vals,
+                         const uint32_t* tile_offsets, uint64_t* stats, vks_stream_t stream);
+
+/*
  * vks_raster_bwd — "Rasterization Backward".
  * Replays each pixel back to front from n_contrib, recovering T by division,
  * and ACCUMULATES exact gradients of the forward w.r.t. mean2d, conic (a,b,c

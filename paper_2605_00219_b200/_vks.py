@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvks.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2605_00219_b200._build` "
+    raise ImportError(f"{LIB_PATH} is missing: run `python paper_2605_00219_b200/_build.py` "
                       "(or __graft_entry__.build()); the CUDA path has no fallback")
 _lib = C.CDLL(LIB_PATH)
 
@@ -25,8 +25,8 @@ FOOTPRINT_SUPPORT, FOOTPRINT_3SIGMA = 0, 1
 FLAG_GRAD_OVERWRITE = 1
 
 EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_project_fwd",
-           "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_bwd",
-           "vks_project_bwd")
+           "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats",
+           "vks_raster_bwd", "vks_project_bwd")
 
 
 class VksCamera(C.Structure):
@@ -51,8 +51,10 @@ _lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
 _lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 7 + [C.c_size_t, _P]
 _lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 11
 _lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 15
+_lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 9
 _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
-for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_bwd", "vks_project_bwd"):
+for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats", "vks_raster_bwd",
+           "vks_project_bwd"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -170,6 +172,18 @@ def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, ti
                              _ptr(T_final, f32, "T_final"), _ptr(n_contrib, i32, "n_contrib"),
                              _stream(stream))
     _check("vks_raster_fwd", st)
+
+
+def vks_raster_fwd_stats(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, stats, stream=None):
+    """Diagnostic: accumulate [visited, composited, evaluated, replayed] pair counts into the
+    int64 CUDA tensor `stats` (4 entries)."""
+    c, k = _cfgcam(cfg, cam)
+    st = _lib.vks_raster_fwd_stats(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
+                                   _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
+                                   _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
+                                   _ptr(tile_offsets, u32, "tile_offsets"), _ptr(stats, torch.int64, "stats"),
+                                   _stream(stream))
+    _check("vks_raster_fwd_stats", st)
 
 
 def vks_raster_bwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib,

@@ -7,15 +7,7 @@
 
 namespace {
 
-thread_local char g_err[256] = "";
-
-int cuda_status(int st) {
-    if (st == VKS_ERR_CUDA) {
-        cudaError_t e = cudaGetLastError();
-        snprintf(g_err, sizeof g_err, "%s", cudaGetErrorString(e));
-    }
-    return st;
-}
+int cuda_status(int st) { return st; }
 
 bool camera_ok(const vks_camera* c) {
     if (!c) return false;
@@ -37,7 +29,7 @@ bool device_present() {
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0) {
         cudaGetLastError();
-        snprintf(g_err, sizeof g_err, "no CUDA device (libvks has no CPU fallback)");
+        snprintf(vks::last_error_buf(), 256, "no CUDA device (libvks has no CPU fallback)");
         return false;
     }
     return true;
@@ -61,7 +53,7 @@ const char* vks_status_string(int status) {
 
 int vks_version(void) { return VKS_VERSION; }
 
-const char* vks_last_cuda_error(void) { return g_err; }
+const char* vks_last_cuda_error(void) { return vks::last_error_buf(); }
 
 int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means,
                     const float* log_scales, const float* quats, const float* opacity_logits,
@@ -120,6 +112,19 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
     if (!device_present()) return VKS_ERR_CUDA;
     return cuda_status(vks::launch_raster_fwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
                                               tile_offsets, image, T_final, n_contrib, (cudaStream_t)stream));
+}
+
+int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
+                         const float* conics, const float* colors, const float* opacities, const int32_t* radii,
+                         const uint32_t* vals, const uint32_t* tile_offsets, uint64_t* stats,
+                         vks_stream_t stream) {
+    int st = config_ok(cfg);
+    if (st) return st;
+    if (!camera_ok(cam) || n < 0 || !tile_offsets || !stats) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means2d || !conics || !colors || !opacities || !radii)) return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return vks::launch_raster_fwd_stats(*cfg, *cam, means2d, conics, colors, opacities, radii, vals, tile_offsets,
+                                        reinterpret_cast<unsigned long long*>(stats), (cudaStream_t)stream);
 }
 
 int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,

@@ -8,14 +8,14 @@
 // Gaussians (16 B/Gaussian per pass) instead of over the M ~ 4.4 N keys, and only the tile bits
 // are sorted over the keys:
 //
-//  1. scan_kernel<false>  exclusive scan of tiles_touched in id order (decoupled look-back,
-//                         dynamic tile ids) -> offsets, M, V.
+//  1. scan (id order)    reduce-then-scan of tiles_touched -> offsets, M, V.
 //  2. radix pass x4       8-bit LSD passes over (depth key, id) of all N Gaussians (culled ones
 //                         take the key 0xFFFFFFFF and sort last); pass 0 derives the keys from
 //                         tiles_touched / depths on the fly.
-//  3. scan_kernel<true>   exclusive scan of tiles_touched in depth order (gathered through the
-//                         sorted ids) -> slot of each Gaussian's first key.
-//  4. keys_kernel         warp-cooperative expansion of the tile rects in depth order into
+//  3. scan (depth order) reduce-then-scan of the tile counts of the depth-ordered rect codes
+//                         (the last depth pass gathers each visible Gaussian's rect once and lays it
+//                         out as a 64-bit code, 4 x u16) -> slot of each Gaussian's first key.
+//  4. keys_kernel         warp-cooperative expansion of the rect codes in depth order into
 //                         (tile, id) pairs with coalesced stores; 2-D difference array of the
 //                         rects accumulated per block in shared memory.
 //  5. tile_count_kernel   2-D prefix of the difference array -> per-tile list lengths -> CSR
@@ -81,9 +81,10 @@ struct Workspace {
     u32 *tk[2], *tv[2];  // tile sort ping-pong [capacity]
     u32* counts;         // [256 * sort tiles] digit counts of the current pass (digit-major)
     u32* offs;           // its exclusive scan
+    u64* rcs;            // [n] tile-rect codes in depth order
+    u32* part_sum;       // [scan blocks] block sums of the 1-D scans
+    u32* part_vis;       // [scan blocks] visible counts
     // region A (zeroed before the scan)
-    u64* scan_lb;        // id-order scan look-back
-    u64* dscan_lb;       // depth-order scan look-back
     u64* cnt_lb[kPasses];  // look-back of each pass's counts scan
     u32* ctr;            // [16] scan tile counters
     u64* totals;         // [2]: M, V
@@ -113,10 +114,11 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
     }
     w.counts = reinterpret_cast<u32*>(take(4 * 256 * sort_tiles));
     w.offs = reinterpret_cast<u32*>(take(4 * 256 * sort_tiles));
+    w.rcs = reinterpret_cast<u64*>(take(8 * nn));
+    w.part_sum = reinterpret_cast<u32*>(take(4 * scan_tiles));
+    w.part_vis = reinterpret_cast<u32*>(take(4 * scan_tiles));
     const size_t a0 = off;
     w.zeroA = b ? b + off : nullptr;
-    w.scan_lb = reinterpret_cast<u64*>(take(8 * scan_tiles));
-    w.dscan_lb = reinterpret_cast<u64*>(take(8 * scan_tiles));
     for (int p = 0; p < kPasses; p++) w.cnt_lb[p] = reinterpret_cast<u64*>(take(8 * cnt_scan_tiles));
     w.ctr = reinterpret_cast<u32*>(take(4 * 16));
     w.totals = reinterpret_cast<u64*>(take(8 * 2));
@@ -127,111 +129,10 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
 }
 
 // counter slots in w.ctr
-enum { kCtrScan = 0, kCtrDscan = 1, kCtrPass = 2 };  // kCtrPass + p: counts scan of pass p
-
-__device__ __forceinline__ int sat_tiles(int t) { return t > 0 ? t : 0; }
+enum { kCtrPass = 0 };  // kCtrPass + p: counts scan of pass p
 
 // ------------------------------------------------------------------------------------------
-// 1./3. exclusive scan of tiles_touched (decoupled look-back, one thread walks chunks back).
-//   GATHER = false: id order; also V (number of Gaussians with tiles_touched > 0).
-//   GATHER = true : depth order, element r = tiles[sid[r]] for r < count.
-template <bool GATHER>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(const int* __restrict__ tiles, const u32* __restrict__ sid,
-                                                           const float* __restrict__ depths, u32* __restrict__ out,
-                                                           int64_t count, u64* __restrict__ lb, u32* __restrict__ ctr,
-                                                           u64* __restrict__ totals) {
-    __shared__ u32 s_tile;
-    __shared__ u64 s_warp[kScanThreads / 32];
-    __shared__ u64 s_prefix;
-    __shared__ u32 s_vis;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) { s_tile = atomicAdd(ctr, 1u); s_vis = 0; }
-    __syncthreads();
-    const int64_t tile = s_tile;
-    const int64_t base = tile * kScanTile + (int64_t)tid * kScanItems;
-    int v[kScanItems];
-    if (!GATHER && base + kScanItems <= count && ((reinterpret_cast<uintptr_t>(tiles + base) & 15) == 0)) {
-#pragma unroll
-        for (int j = 0; j < kScanItems; j += 4) {
-            int4 q = __ldg(reinterpret_cast<const int4*>(tiles + base + j));
-            v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < kScanItems; j++) {
-            const int64_t e = base + j;
-            v[j] = e < count ? (GATHER ? __ldg(tiles + __ldg(sid + e)) : __ldg(tiles + e)) : 0;
-        }
-    }
-    u64 tsum = 0;
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) tsum += (u32)sat_tiles(v[j]);
-    if (!GATHER) {
-        u32 nvis = 0;
-#pragma unroll
-        for (int j = 0; j < kScanItems; j++) nvis += v[j] > 0;
-        nvis = __reduce_add_sync(VKS_FULL_MASK, nvis);
-        if (lane == 0 && nvis) atomicAdd(&s_vis, nvis);
-    }
-    u64 incl = tsum;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        u64 t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
-        if (lane >= d) incl += t;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    u64 wpre = 0, btotal = 0;
-#pragma unroll
-    for (int w = 0; w < kScanThreads / 32; w++) {
-        if (w < warp) wpre += s_warp[w];
-        btotal += s_warp[w];
-    }
-    if (tid == 0) {
-        u64 excl = 0;
-        if (tile == 0) {
-            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb), kScanFlagInc | btotal);
-        } else {
-            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagAgg | btotal);
-            int64_t j = tile - 1;
-            bool found = false;
-            while (!found) {
-                u64 st[kLookbackChunk];
-#pragma unroll
-                for (int q = 0; q < kLookbackChunk; q++)
-                    st[q] = (j - q >= 0) ? ld_volatile_u64(reinterpret_cast<const unsigned long long*>(lb + j - q)) : 0;
-                int consumed = 0;
-#pragma unroll
-                for (int q = 0; q < kLookbackChunk; q++) {
-                    if (found || consumed < q) break;
-                    const u64 f = st[q] & ~kScanMask;
-                    if (f == 0) break;
-                    excl += st[q] & kScanMask;
-                    consumed = q + 1;
-                    if (f == kScanFlagInc) found = true;
-                }
-                j -= consumed;
-            }
-            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagInc | (excl + btotal));
-        }
-        s_prefix = excl;
-        if ((tile + 1) * kScanTile >= count) totals[0] = excl + btotal;
-        if (!GATHER && s_vis) atomicAdd(totals + 1, (u64)s_vis);
-    }
-    __syncthreads();
-    u64 run = s_prefix + wpre + (incl - tsum);
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
-        if (base + j < count) out[base + j] = (u32)run;
-        run += (u32)sat_tiles(v[j]);
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// 4. key generation (+ tile-rect difference array)
-constexpr int kKeysThreads = 512;
-constexpr int kKeysWarps = kKeysThreads / 32;
-constexpr int kKeysSmemDiffMax = 160 * 1024 / 4;  // cells
+// tile rect codes: x0 | y0 << 16 | x1 << 32 | y1 << 48 (16 bits each), 0 for culled Gaussians
 
 // tile rect recomputed exactly as projection step 11
 __device__ __forceinline__ void rect_of(const float2 m, const int2 r, int TX, int TY, int& x0, int& x1, int& y0,
@@ -242,16 +143,169 @@ __device__ __forceinline__ void rect_of(const float2 m, const int2 r, int TX, in
     y0 = (int)fminf(fmaxf(floorf((m.y - ry) * 0.0625f), 0.0f), (float)TY);
     y1 = (int)fminf(fmaxf(ceilf((m.y + ry) * 0.0625f), 0.0f), (float)TY);
 }
+__device__ __forceinline__ u64 pack_rect(int x0, int x1, int y0, int y1) {
+    return (u64)(u32)x0 | ((u64)(u32)y0 << 16) | ((u64)(u32)x1 << 32) | ((u64)(u32)y1 << 48);
+}
+__device__ __forceinline__ void unpack_rect(u64 c, int& x0, int& x1, int& y0, int& y1) {
+    x0 = (int)(c & 0xFFFF); y0 = (int)((c >> 16) & 0xFFFF); x1 = (int)((c >> 32) & 0xFFFF); y1 = (int)(c >> 48);
+}
+__device__ __forceinline__ int rect_tiles(u64 c) {
+    int x0, x1, y0, y1;
+    unpack_rect(c, x0, x1, y0, y1);
+    return (x1 - x0) * (y1 - y0);
+}
 
-// MODE 0: depth order (sid): (tile, id) pairs at slot0[r] + k, plus the difference array.
-// MODE 1: id order (debug keys_unsorted / vals_unsorted): u64 keys at slot0[i] + k.
+// ------------------------------------------------------------------------------------------
+// 1./3. exclusive scans of tiles_touched, reduce-then-scan (no block waits on another):
+//   scan_reduce_kernel   per 4096-element block: sum (and number of visible Gaussians)
+//   scan_partials_kernel one block: exclusive scan of the block sums, totals
+//   scan_down_kernel     per block: rescan + block prefix -> output
+// MODE 0: element i = tiles_touched[i];  MODE 1: element r = tiles of the depth-sorted rect code r.
+template <int MODE>
+__device__ __forceinline__ void load_scan_items(const int* __restrict__ tiles, const u64* __restrict__ rc, u64 count,
+                                                u64 base, int v[kScanItems]) {
+    if (MODE == 0) {
+        if (base + kScanItems <= count && ((reinterpret_cast<uintptr_t>(tiles + base) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < kScanItems; j += 4) {
+                const int4 q = __ldg(reinterpret_cast<const int4*>(tiles + base + j));
+                v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < kScanItems; j++) v[j] = base + j < count ? __ldg(tiles + base + j) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++) v[j] = v[j] > 0 ? v[j] : 0;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kScanItems; j++) v[j] = base + j < count ? rect_tiles(__ldg(rc + base + j)) : 0;
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(vks_camera cam, const int* __restrict__ tiles,
+                                                                  const float2* __restrict__ means2d,
+                                                                  const int2* __restrict__ radii,
+                                                                  const u64* __restrict__ rc_in, u64* __restrict__ rc_out,
+                                                                  u64 count, u32* __restrict__ part_sum,
+                                                                  u32* __restrict__ part_vis) {
+    __shared__ u32 s_sum[kScanThreads / 32], s_vis[kScanThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const u64 base = (u64)blockIdx.x * kScanTile + (u64)tid * kScanItems;
+    int v[kScanItems];
+    load_scan_items<MODE>(tiles, rc_in, count, base, v);
+    u32 sum = 0, vis = 0;
+    (void)cam; (void)means2d; (void)radii; (void)rc_out;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        sum += (u32)v[j];
+        vis += v[j] > 0;
+    }
+    sum = __reduce_add_sync(VKS_FULL_MASK, sum);
+    vis = __reduce_add_sync(VKS_FULL_MASK, vis);
+    if (lane == 0) { s_sum[warp] = sum; s_vis[warp] = vis; }
+    __syncthreads();
+    if (tid == 0) {
+        u32 a = 0, b = 0;
+#pragma unroll
+        for (int w = 0; w < kScanThreads / 32; w++) { a += s_sum[w]; b += s_vis[w]; }
+        part_sum[blockIdx.x] = a;
+        if (part_vis) part_vis[blockIdx.x] = b;
+    }
+}
+
+// exclusive scan of the P block sums in place; totals[0] = sum, totals[1] = sum of part_vis
+__global__ void __launch_bounds__(1024) scan_partials_kernel(u32* __restrict__ part_sum, const u32* __restrict__ part_vis,
+                                                            u32 P, u64* __restrict__ totals) {
+    __shared__ u32 s_w[32];
+    __shared__ u64 s_carry;
+    __shared__ u64 s_vis;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) { s_carry = 0; s_vis = 0; }
+    __syncthreads();
+    u64 vis_acc = 0;
+    for (u32 base = 0; base < P; base += 1024) {
+        const u32 i = base + tid;
+        const u32 c = i < P ? part_sum[i] : 0u;
+        if (i < P && part_vis) vis_acc += part_vis[i];
+        u32 incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
+            if (lane >= d) incl += t;
+        }
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        u32 wpre = 0, btot = 0;
+        for (int w = 0; w < 32; w++) {
+            if (w < warp) wpre += s_w[w];
+            btot += s_w[w];
+        }
+        const u64 carry = s_carry;
+        if (i < P) part_sum[i] = (u32)(carry + wpre + incl - c);
+        __syncthreads();
+        if (tid == 0) s_carry = carry + btot;
+        __syncthreads();
+    }
+    vis_acc = __reduce_add_sync(VKS_FULL_MASK, (u32)vis_acc);
+    if (lane == 0 && vis_acc) atomicAdd(reinterpret_cast<unsigned long long*>(&s_vis), (unsigned long long)vis_acc);
+    __syncthreads();
+    if (tid == 0) {
+        totals[0] = s_carry;
+        if (part_vis) totals[1] = s_vis;
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const int* __restrict__ tiles, const u64* __restrict__ rc,
+                                                                u64 count, const u32* __restrict__ part_prefix,
+                                                                u32* __restrict__ out) {
+    __shared__ u32 s_w[kScanThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const u64 base = (u64)blockIdx.x * kScanTile + (u64)tid * kScanItems;
+    int v[kScanItems];
+    load_scan_items<MODE>(tiles, rc, count, base, v);
+    u32 tsum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) tsum += (u32)v[j];
+    u32 incl = tsum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u32 t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    u32 wpre = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; w++)
+        if (w < warp) wpre += s_w[w];
+    u32 run = part_prefix[blockIdx.x] + wpre + incl - tsum;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        if (base + j < count) out[base + j] = run;
+        run += (u32)v[j];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// 4. key generation (+ tile-rect difference array)
+constexpr int kKeysThreads = 512;
+constexpr int kKeysWarps = kKeysThreads / 32;
+constexpr int kKeysSmemDiffMax = 160 * 1024 / 4;  // cells
+
+// MODE 0: depth order: element r = Gaussian sid[r] with rect code rc[r] -> (tile, id) pairs at
+//         slot0[r] + k, plus the difference array of the rects.
+// MODE 1: id order (debug keys_unsorted / vals_unsorted): rect of Gaussian i -> u64 keys at slot0[i] + k.
 template <bool SMEM_DIFF, int MODE>
 __global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int64_t count, const u32* __restrict__ sid,
+                                                           const u64* __restrict__ rc, const int* __restrict__ tiles,
                                                            const float2* __restrict__ means2d,
                                                            const int2* __restrict__ radii, const float* __restrict__ depths,
-                                                           const int* __restrict__ tiles, const u32* __restrict__ slot0,
-                                                           u32* __restrict__ tkeys, u32* __restrict__ tvals,
-                                                           u64* __restrict__ keys64, int* __restrict__ diff) {
+                                                           const u32* __restrict__ slot0, u32* __restrict__ tkeys,
+                                                           u32* __restrict__ tvals, u64* __restrict__ keys64,
+                                                           int* __restrict__ diff) {
     extern __shared__ int s_diff[];
     __shared__ int s_incl[kKeysWarps][32];
     __shared__ int s_x0[kKeysWarps][32], s_y0[kKeysWarps][32], s_w[kKeysWarps][32];
@@ -273,11 +327,17 @@ __global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int6
         u32 g = 0, db = 0;
         if (r < count) {
             g = MODE == 0 ? __ldg(sid + r) : (u32)r;
-            cnt = __ldg(tiles + g);
+            int x1, y1;
+            if (MODE == 0) {
+                unpack_rect(__ldg(rc + r), x0, x1, y0, y1);
+            } else if (__ldg(tiles + r) > 0) {
+                rect_of(__ldg(means2d + r), __ldg(radii + r), TX, TY, x0, x1, y0, y1);
+            } else {
+                x0 = x1 = y0 = y1 = 0;
+            }
+            w = x1 - x0;
+            cnt = w * (y1 - y0);
             if (cnt > 0) {
-                int x1, y1;
-                rect_of(__ldg(means2d + g), __ldg(radii + g), TX, TY, x0, x1, y0, y1);
-                w = x1 - x0;
                 if (MODE == 0) {
                     atomicAdd(dd + y0 * W1 + x0, 1);
                     atomicAdd(dd + y0 * W1 + x1, -1);
@@ -287,7 +347,7 @@ __global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int6
                     db = __float_as_uint(__ldg(depths + g));
                 }
             } else {
-                cnt = 0;
+                w = 1;
             }
         }
         int incl = cnt;
@@ -388,7 +448,7 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int* _
 //   scatter_kernel       per tile: TMA bulk copy of keys/values into shared memory (mbarrier),
 //                        stable warp-level ranking (ballot multi-split), in-place shared-memory
 //                        reorder by digit, digit-contiguous coalesced stores.
-enum { kPassPlain = 0, kPassDepthFirst = 1, kPassTileLast = 2 };
+enum { kPassPlain = 0, kPassDepthFirst = 1, kPassTileLast = 2, kPassDepthLast = 3 };
 
 // key of element j of the depth-first pass: visible ? f32bits(depth) : 0xFFFFFFFF (sorts last)
 __device__ __forceinline__ u32 depth_key(int tiles, u32 depth_bits) { return tiles > 0 ? depth_bits : 0xFFFFFFFFu; }
@@ -408,7 +468,7 @@ __device__ __forceinline__ u32 digit_peers(u32 d, bool valid = true) {
     return peers;
 }
 
-template <int DBITS, int MODE>
+template <int DBITS, int MODE, bool ATOMIC>
 __global__ void __launch_bounds__(kSortThreads) digit_count_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
                                                                   u32 n, int shift, u32 T, u32* __restrict__ counts) {
     constexpr int RADIX = 1 << DBITS;
@@ -431,8 +491,12 @@ __global__ void __launch_bounds__(kSortThreads) digit_count_kernel(const u32* __
     for (int i = 0; i < kSortItems; i++) {
         const bool valid = base + (u64)i * kSortThreads + tid < n;
         const u32 d = (key[i] >> shift) & DMASK;
-        const u32 peers = digit_peers<DBITS>(d, valid);
-        if (valid && (peers & ltmask) == 0) whist[warp][d] += __popc(peers);
+        if (ATOMIC) {  // per-warp histograms: contention only among a warp's lanes
+            if (valid) atomicAdd(&whist[warp][d], 1u);
+        } else {
+            const u32 peers = digit_peers<DBITS>(d, valid);
+            if (valid && (peers & ltmask) == 0) whist[warp][d] += __popc(peers);
+        }
     }
     __syncthreads();
     for (int d = tid; d < RADIX; d += kSortThreads) {
@@ -512,6 +576,13 @@ __global__ void __launch_bounds__(kScanThreads) scan_u32_kernel(const u32* __res
     }
 }
 
+struct RectSrc {  // kPassDepthLast: where the tile rects come from
+    const float2* means2d;
+    const int2* radii;
+    int TX, TY;
+    u32 visible;   // the first `visible` sorted entries are the visible Gaussians
+};
+
 struct SortSmem {
     alignas(128) u32 keys[kSortTile];  // input staging (bulk copy), then the reordered tile
     alignas(128) u32 vals[kSortTile];
@@ -526,12 +597,14 @@ __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_gene
 
 // kPassDepthFirst: kin = tiles_touched, vin = depths; key = depth_key(), value = id.
 // kPassTileLast: writes only the values (the caller's vals) and, if keys64, the u64 keys.
+// kPassDepthLast: also writes the rect codes in the sorted order (gathered by id).
 template <int DBITS, int MODE>
 __global__ void __launch_bounds__(kSortThreads) scatter_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
                                                              u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
                                                              int shift, u32 T, const u32* __restrict__ offs,
                                                              const float* __restrict__ depths,
-                                                             u64* __restrict__ keys64) {
+                                                             u64* __restrict__ keys64, RectSrc rsrc,
+                                                             u64* __restrict__ rc_out) {
     constexpr int RADIX = 1 << DBITS;
     constexpr u32 DMASK = RADIX - 1;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -643,6 +716,15 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(const u32* __rest
             vout[dest] = val;
             if (MODE == kPassTileLast && keys64)
                 keys64[dest] = ((u64)key << 32) | (u64)__float_as_uint(__ldg(depths + val));
+            if (MODE == kPassDepthLast) {  // rect code in depth order
+                u64 code = 0;
+                if (dest < rsrc.visible) {
+                    int x0, x1, y0, y1;
+                    rect_of(__ldg(rsrc.means2d + val), __ldg(rsrc.radii + val), rsrc.TX, rsrc.TY, x0, x1, y0, y1);
+                    code = pack_rect(x0, x1, y0, y1);
+                }
+                rc_out[dest] = code;
+            }
         }
     }
 }
@@ -656,7 +738,7 @@ struct PassBufs {
 
 template <int DBITS, int MODE>
 int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift, const PassBufs& pb,
-                const float* depths, u64* keys64, cudaStream_t s) {
+                const float* depths, u64* keys64, cudaStream_t s, RectSrc rsrc = RectSrc{}, u64* rc_out = nullptr) {
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(scatter_kernel<DBITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -666,13 +748,15 @@ int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int
     }
     const u32 T = (u32)((n + kSortTile - 1) / kSortTile);
     if (!T) return VKS_OK;
-    digit_count_kernel<DBITS, MODE><<<T, kSortThreads, 0, s>>>(kin, vin, n, shift, T, pb.counts);
+    static const bool atomic_count = !getenv("VKS_COUNT_BALLOT");
+    if (atomic_count) digit_count_kernel<DBITS, MODE, true><<<T, kSortThreads, 0, s>>>(kin, vin, n, shift, T, pb.counts);
+    else digit_count_kernel<DBITS, MODE, false><<<T, kSortThreads, 0, s>>>(kin, vin, n, shift, T, pb.counts);
     const u64 cnt = (u64)(1u << DBITS) * T;
     scan_u32_kernel<<<(unsigned)((cnt + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt,
                                                                                            pb.lb, pb.ctr);
     scatter_kernel<DBITS, MODE><<<T, kSortThreads, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, shift, T, pb.offs,
-                                                                         depths, keys64);
-    return cudaGetLastError() == cudaSuccess ? VKS_OK : VKS_ERR_CUDA;
+                                                                         depths, keys64, rsrc, rc_out);
+    return check_launch(__func__);
 }
 
 template <int MODE>
@@ -709,29 +793,44 @@ int sm_count() {
 }
 
 template <int MODE>
-int launch_keys(const vks_camera& cam, int64_t count, const u32* sid, const float* means2d, const int32_t* radii,
-                const float* depths, const int32_t* tiles, const u32* slot0, u32* tkeys, u32* tvals, u64* keys64,
-                int* diff, cudaStream_t s) {
+int launch_keys(const vks_camera& cam, int64_t count, const u32* sid, const u64* rc, const int* tiles,
+                const float* means2d, const int32_t* radii, const float* depths, const u32* slot0, u32* tkeys,
+                u32* tvals, u64* keys64, int* diff, cudaStream_t s) {
+    const float2* m2 = reinterpret_cast<const float2*>(means2d);
+    const int2* r2 = reinterpret_cast<const int2*>(radii);
     const int TX = tiles_x(cam), TY = tiles_y(cam);
     const int cells = (TX + 1) * (TY + 1);
     const int64_t want = (count + kKeysThreads - 1) / kKeysThreads;
     if (want == 0) return VKS_OK;
-    const float2* m2 = reinterpret_cast<const float2*>(means2d);
-    const int2* r2 = reinterpret_cast<const int2*>(radii);
     if (MODE == 0 && cells <= kKeysSmemDiffMax) {
         const size_t sm = sizeof(int) * (size_t)cells;
         if (sm > 32 * 1024 &&
             cudaFuncSetAttribute(keys_kernel<true, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
             return VKS_ERR_CUDA;
         const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 2);
-        keys_kernel<true, MODE><<<blocks, kKeysThreads, sm, s>>>(cam, count, sid, m2, r2, depths, tiles, slot0, tkeys,
-                                                                 tvals, keys64, diff);
+        keys_kernel<true, MODE><<<blocks, kKeysThreads, sm, s>>>(cam, count, sid, rc, tiles, m2, r2, depths, slot0,
+                                                                 tkeys, tvals, keys64, diff);
     } else {
         const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 4);
-        keys_kernel<false, MODE><<<blocks, kKeysThreads, 0, s>>>(cam, count, sid, m2, r2, depths, tiles, slot0, tkeys,
-                                                                 tvals, keys64, diff);
+        keys_kernel<false, MODE><<<blocks, kKeysThreads, 0, s>>>(cam, count, sid, rc, tiles, m2, r2, depths, slot0,
+                                                                 tkeys, tvals, keys64, diff);
     }
-    return cudaGetLastError() == cudaSuccess ? VKS_OK : VKS_ERR_CUDA;
+    return check_launch(__func__);
+}
+
+// reduce-then-scan of the tiles counts (MODE 0: id order from tiles_touched, writes rect codes;
+// MODE 1: depth order from the sorted rect codes); totals[0] = sum (and totals[1] = #visible)
+template <int MODE>
+int run_scan(const vks_camera& cam, const int* tiles, const float* means2d, const int32_t* radii, const u64* rc_in,
+             u64* rc_out, u64 count, u32* part_sum, u32* part_vis, u32* out, u64* totals, cudaStream_t s) {
+    const u32 P = (u32)((count + kScanTile - 1) / kScanTile);
+    if (!P) return VKS_OK;
+    scan_reduce_kernel<MODE><<<P, kScanThreads, 0, s>>>(cam, tiles, reinterpret_cast<const float2*>(means2d),
+                                                       reinterpret_cast<const int2*>(radii), rc_in, rc_out, count,
+                                                       part_sum, part_vis);
+    scan_partials_kernel<<<1, 1024, 0, s>>>(part_sum, MODE == 0 ? part_vis : nullptr, P, totals);
+    scan_down_kernel<MODE><<<P, kScanThreads, 0, s>>>(tiles, rc_in, count, part_sum, out);
+    return check_launch(__func__);
 }
 
 }  // namespace
@@ -751,17 +850,16 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     const int32_t n_tiles = TX * TY;
     if (workspace_bytes < bin_sort_workspace_bytes(n, capacity, n_tiles)) return VKS_ERR_WORKSPACE;
     Workspace w = carve(workspace, n, capacity, TX, TY);
-    if (cudaMemsetAsync(w.zeroA, 0, w.zeroA_bytes, s) != cudaSuccess) return VKS_ERR_CUDA;
+    if (cudaError_t e_ = cudaMemsetAsync(w.zeroA, 0, w.zeroA_bytes, s)) return cuda_fail(e_, "memset workspace");
     auto pass_bufs = [&](int p) { return PassBufs{w.counts, w.offs, w.cnt_lb[p], w.ctr + kCtrPass + p}; };
-    // 1. index offsets in id order, M, V
+    // 1. index offsets in id order, M, V, rect codes
     u64 tot[2] = {0, 0};
     if (n > 0) {
-        const unsigned blocks = (unsigned)((n + kScanTile - 1) / kScanTile);
-        scan_kernel<false><<<blocks, kScanThreads, 0, s>>>(tiles_touched, nullptr, depths, offsets, n, w.scan_lb,
-                                                           w.ctr + kCtrScan, w.totals);
-        if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
-        if (cudaMemcpyAsync(tot, w.totals, sizeof(tot), cudaMemcpyDeviceToHost, s) != cudaSuccess) return VKS_ERR_CUDA;
-        if (cudaStreamSynchronize(s) != cudaSuccess) return VKS_ERR_CUDA;
+        int st = run_scan<0>(cam, tiles_touched, means2d, radii, nullptr, nullptr, (u64)n, w.part_sum, w.part_vis,
+                             offsets, w.totals, s);
+        if (st) return st;
+        if (cudaError_t e_ = cudaMemcpyAsync(tot, w.totals, sizeof(tot), cudaMemcpyDeviceToHost, s)) return cuda_fail(e_, "read M");
+        if (cudaError_t e_ = cudaStreamSynchronize(s)) return cuda_fail(e_, "bin_sort sync");
     }
     const u64 M = tot[0], V = tot[1];
     *num_isects = (int64_t)M;
@@ -775,42 +873,48 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     if (keys_unsorted || vals_unsorted) {
         u32* vtmp = vals_unsorted ? vals_unsorted : w.tv[1];
         u64* ktmp = keys_unsorted ? reinterpret_cast<u64*>(keys_unsorted) : reinterpret_cast<u64*>(w.tk[0]);
-        int st = launch_keys<1>(cam, n, nullptr, means2d, radii, depths, tiles_touched, offsets, nullptr, vtmp, ktmp,
-                                w.diff, s);
+        int st = launch_keys<1>(cam, n, nullptr, nullptr, tiles_touched, means2d, radii, depths, offsets, nullptr, vtmp,
+                                ktmp, w.diff, s);
         if (st) return st;
     }
-    // 2. depth sort of all n (culled Gaussians key 0xFFFFFFFF, last); pass 0 reads (tiles, depths)
+    // 2. depth sort of all n (culled Gaussians key 0xFFFFFFFF, last); pass 0 reads (tiles, depths),
+    //    the last pass also lays out the rect codes in depth order
     int st = launch_pass<8, kPassDepthFirst>(reinterpret_cast<const u32*>(tiles_touched),
                                              reinterpret_cast<const u32*>(depths), w.dk[0], w.dv[0], (u32)n, 0,
                                              pass_bufs(0), nullptr, nullptr, s);
     if (st) return st;
     for (int p = 1; p < kDepthPasses; p++) {
-        st = launch_pass<8, kPassPlain>(w.dk[(p + 1) & 1], w.dv[(p + 1) & 1], w.dk[p & 1], w.dv[p & 1], (u32)n, 8 * p,
-                                        pass_bufs(p), nullptr, nullptr, s);
+        const u32* ki = w.dk[(p + 1) & 1];
+        const u32* vi = w.dv[(p + 1) & 1];
+        if (p == kDepthPasses - 1)
+            st = launch_pass<8, kPassDepthLast>(ki, vi, w.dk[p & 1], w.dv[p & 1], (u32)n, 8 * p, pass_bufs(p), nullptr,
+                                                nullptr, s,
+                                                RectSrc{reinterpret_cast<const float2*>(means2d),
+                                                        reinterpret_cast<const int2*>(radii), TX, TY, (u32)V},
+                                                w.rcs);
+        else
+            st = launch_pass<8, kPassPlain>(ki, vi, w.dk[p & 1], w.dv[p & 1], (u32)n, 8 * p, pass_bufs(p), nullptr,
+                                            nullptr, s);
         if (st) return st;
     }
     const u32* sid = w.dv[(kDepthPasses - 1) & 1];  // ids in (depth, id) order; the first V are visible
-    // 3. slots in depth order
-    {
-        const unsigned blocks = (unsigned)((V + kScanTile - 1) / kScanTile);
-        scan_kernel<true><<<blocks, kScanThreads, 0, s>>>(tiles_touched, sid, nullptr, w.doff, (int64_t)V, w.dscan_lb,
-                                                          w.ctr + kCtrDscan, w.totals);
-        if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
-    }
+    // 3. slots in depth order (from the depth-ordered rect codes)
+    st = run_scan<1>(cam, nullptr, nullptr, nullptr, w.rcs, nullptr, V, w.part_sum, nullptr, w.doff, w.totals + 0, s);
+    if (st) return st;
     // 4. (tile, id) pairs in depth order + tile-rect difference array
     const TilePlan plan = tile_plan(n_tiles);
     u32* pv0 = plan.passes == 0 ? vals : w.tv[0];
-    st = launch_keys<0>(cam, (int64_t)V, sid, means2d, radii, depths, tiles_touched, w.doff, w.tk[0], pv0, nullptr,
-                        w.diff, s);
+    st = launch_keys<0>(cam, (int64_t)V, sid, w.rcs, tiles_touched, means2d, radii, depths, w.doff, w.tk[0], pv0,
+                        nullptr, w.diff, s);
     if (st) return st;
     // 5. tile counts -> tile ranges
     tile_count_kernel<<<1, 1024, 0, s>>>(TX, TY, w.diff, tile_offsets);
-    if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
+    if (int e_ = check_launch(__func__)) return e_;
     // 6. stable tile passes; the last writes the caller's vals (+ u64 keys on request)
     if (plan.passes == 0) {
         if (keys64) {
             keys64_tile0_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(vals, depths, keys64, (u32)M);
-            if (cudaGetLastError() != cudaSuccess) return VKS_ERR_CUDA;
+            if (int e_ = check_launch(__func__)) return e_;
         }
         return VKS_OK;
     }

@@ -122,7 +122,11 @@ __device__ __forceinline__ PixelMap<PPT> pixel_map(int tile, int TX) {
     return m;
 }
 
-template <int PPT>
+// STATS: diagnostic variant (vks_raster_fwd_stats) that writes no image and instead accumulates
+// stats[0] = list entries visited before each pixel's stop (the algorithm's evaluations),
+// stats[1] = composited pairs, stats[2] = pairs actually evaluated here (after patch culling),
+// stats[3] = sum of n_contrib (entries the backward replays).
+template <int PPT, bool STATS = false>
 __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
@@ -132,8 +136,10 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                                                                  const uint32_t* __restrict__ vals,
                                                                  const uint32_t* __restrict__ tile_offsets,
                                                                  float* __restrict__ image, float* __restrict__ T_final,
-                                                                 int* __restrict__ n_contrib) {
+                                                                 int* __restrict__ n_contrib,
+                                                                 unsigned long long* __restrict__ stats = nullptr) {
     __shared__ WarpStage stage[8 / PPT];
+    unsigned long long n_eval = 0, n_comp = 0;
     const int TX = tiles_x(cam);
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31;
@@ -180,7 +186,9 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
             for (int k = 0; k < PPT; k++) {
                 if (done[k]) continue;
                 float dx, dy, G, rG, alpha;
+                if (STATS) n_eval++;
                 if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
+                if (STATS) n_comp++;
                 const float aT = alpha * T[k];
                 C0[k] = fmaf(B.z, aT, C0[k]);
                 C1[k] = fmaf(B.w, aT, C1[k]);
@@ -190,6 +198,21 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                 if (T[k] < 1e-4f) done[k] = true;
             }
         }
+    }
+    if (STATS) {
+        unsigned long long visited = 0, replay = 0;
+#pragma unroll
+        for (int k = 0; k < PPT; k++) {
+            const int y = pm.y0 + 4 * k;
+            if (!(pm.x < cam.width && y < cam.height)) continue;
+            visited += T[k] < 1e-4f ? (unsigned long long)last[k] : (unsigned long long)(end - start);
+            replay += (unsigned long long)last[k];
+        }
+        atomicAdd(stats + 0, visited);
+        atomicAdd(stats + 1, n_comp);
+        atomicAdd(stats + 2, n_eval);
+        atomicAdd(stats + 3, replay);
+        return;
     }
 #pragma unroll
     for (int k = 0; k < PPT; k++) {
@@ -381,6 +404,20 @@ int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2
                                                              dcolors, dopacities);
     return LaunchCheck::check();
 }
+
+}  // namespace
+
+int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
+                            const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
+                            const uint32_t* tile_offsets, unsigned long long* stats, cudaStream_t st) {
+    const int n_tiles = tiles_x(cam) * tiles_y(cam);
+    raster_fwd_kernel<2, true><<<n_tiles, 128, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d), conics,
+                                                        colors, opacities, reinterpret_cast<const int2*>(radii), vals,
+                                                        tile_offsets, nullptr, nullptr, nullptr, stats);
+    return LaunchCheck::check();
+}
+
+namespace {
 
 int ppt_choice(const char* var) {
     const char* e = getenv(var);

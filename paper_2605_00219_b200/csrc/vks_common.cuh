@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/vks.h"
 
@@ -11,12 +12,22 @@ namespace vks {
 
 constexpr int kTile = 16;
 
-// Status set by the API layer; kernels never touch host state.
+// Thread-local text of the last CUDA error seen by the library (read by vks_last_cuda_error).
+inline char* last_error_buf() {
+    static thread_local char buf[256] = "";
+    return buf;
+}
+inline int cuda_fail(cudaError_t e, const char* where) {
+    snprintf(last_error_buf(), 256, "%s: %s", where, cudaGetErrorString(e));
+    return VKS_ERR_CUDA;
+}
+// check a kernel launch (clears the non-sticky launch error, keeps its text)
+inline int check_launch(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? VKS_OK : cuda_fail(e, where);
+}
 struct LaunchCheck {
-    static int check() {
-        cudaError_t e = cudaGetLastError();
-        return e == cudaSuccess ? VKS_OK : VKS_ERR_CUDA;
-    }
+    static int check() { return check_launch("kernel launch"); }
 };
 
 __host__ __device__ inline int tiles_x(const vks_camera& c) { return (c.width + kTile - 1) / kTile; }
@@ -82,6 +93,9 @@ int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const uint32_t* vals, const uint32_t* tile_offsets, float* image,
                       float* T_final, int32_t* n_contrib, cudaStream_t s);
+int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
+                            const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
+                            const uint32_t* tile_offsets, unsigned long long* stats, cudaStream_t s);
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const uint32_t* vals, const uint32_t* tile_offsets, const float* T_final,

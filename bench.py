@@ -34,8 +34,8 @@ METRIC = "fwd+bwd rasterize iters/sec @5.8M Gaussians 1237x822; sort Gkeys/s; HB
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="bicycle")
     ap.add_argument("--views-per-rank", type=int, default=1)
@@ -68,7 +68,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -226,10 +226,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     vis = int((rend.tiles > 0).sum().item())
     m_last = rend.num_isects
-    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(6, dtype=torch.int64, device="cuda")
     P.vks_raster_fwd_stats(cfg, cams[my_views[(args.warmup + args.steps - 1) % len(my_views)]], rend.means2d,
                            rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals, rend.tile_offsets, stats)
-    visited, composited, evaluated, replayed = (int(x) for x in stats.tolist())
+    visited, composited, evaluated, replayed, warp_entries, warp_entries_comp = (int(x) for x in stats.tolist())
     ab = algorithmic_bytes(n, vis, m_last)
     fl = raster_flops(visited, composited, replayed)
     pk = peaks()
@@ -268,7 +268,8 @@ def run_ours(args):
                sort_gkeys_per_s=round(per_stage["bin_sort"]["gkeys_per_s"], 3),
                hbm_gbs={k: round(per_stage[k]["achieved"], 1) for k in ("project_fwd", "bin_sort", "project_bwd")},
                raster_work=dict(visited_pairs=visited, composited_pairs=composited, evaluated_pairs=evaluated,
-                                replayed_pairs=replayed),
+                                replayed_pairs=replayed, warp_entries=warp_entries,
+                                warp_entries_composited=warp_entries_comp),
                roofline=roofline, gpu_launches=gpu_launches, clocks=clk)
 
     if not args.no_e2e:

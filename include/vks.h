@@ -151,8 +151,10 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
  *   -> image [H,W,3], T_final [H,W], n_contrib [H,W] int32 (1-based position,
  *      within the tile's list, of the last composited entry; 0 = none).
  * means2d/conics/colors/opacities/radii as produced by vks_project_fwd, vals/tile_offsets as
- * produced by vks_bin_sort.  In support-footprint mode radii bound each Gaussian's alpha >= 1/255
- * support, which the kernel uses to skip (warp, Gaussian) pairs that cannot composite.
+ * produced by vks_bin_sort.  Before evaluating an entry, each warp tests whether any pixel centre
+ * of its 8x8 patch can reach alpha >= 1/255 (exact minimum of sigma over the patch against
+ * ln(255 rho), with an fp32 error margin) and skips the entry warp-uniformly if none can; radii
+ * (the support box) are read only by the diagnostic box-culling mode (VKS_RASTER_CULL=1).
  */
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    const float* means2d, const float* conics, const float* colors,
@@ -167,6 +169,9 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
  *   stats[1] += composited (pixel, Gaussian) pairs
  *   stats[2] += pairs actually evaluated by the kernel (after its patch culling)
  *   stats[3] += sum of n_contrib (entries the backward replays)
+ *   stats[4] += (warp, entry) pairs processed after patch culling
+ *   stats[5] += of those, pairs with at least one composited pixel
+ * stats must hold 6 uint64 counters.
  */
 int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n,
                          const float* means2d, const float* conics, const float* colors,

@@ -175,8 +175,10 @@ def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, ti
 
 
 def vks_raster_fwd_stats(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, stats, stream=None):
-    """Diagnostic: accumulate [visited, composited, evaluated, replayed] pair counts into the
-    int64 CUDA tensor `stats` (4 entries)."""
+    """Diagnostic: accumulate [visited, composited, evaluated, replayed, warp_entries,
+    warp_entries_composited] counts into the int64 CUDA tensor `stats` (6 entries)."""
+    if stats.numel() < 6:
+        raise ValueError("stats needs 6 int64 entries")
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_raster_fwd_stats(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                                    _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),

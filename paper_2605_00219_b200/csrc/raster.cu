@@ -27,18 +27,26 @@ namespace {
 struct WarpStage {
     float4 a[32];    // u, v, 0.5*a, b
     float4 b[32];    // 0.5*c, rho, c0, c1
-    float4 box[32];  // support box of pixel centres: xmin, xmax, ymin, ymax
     float c2[32];
     uint32_t id[32];
 };
 
 struct Entry {  // one lane's gathered entry, in registers until it is stored to the stage
-    float4 a, b, box;
+    float4 a, b;
     float c2;
     uint32_t id;
+    int2 r;     // projection radii (kCullBox only)
 };
 
-__device__ __forceinline__ Entry gather_entry(uint32_t g, bool cull, const float2* __restrict__ means2d,
+// Patch culling modes (VKS_RASTER_CULL): a warp skips an entry when no pixel centre of its patch
+// can reach alpha >= 1/255.
+//   kCullNone    evaluate every entry (3SIGMA footprint, or VKS_RASTER_CULL=0)
+//   kCullBox     the projection's support box (radii) widened by 1 + r/64 px
+//   kCullEllipse exact: the minimum of sigma over the patch rectangle against ln(255 rho)
+enum { kCullNone = 0, kCullBox = 1, kCullEllipse = 2 };
+
+template <int CULL>
+__device__ __forceinline__ Entry gather_entry(uint32_t g, const float2* __restrict__ means2d,
                                               const float* __restrict__ conics, const float* __restrict__ colors,
                                               const float* __restrict__ opac, const int2* __restrict__ radii) {
     Entry e;
@@ -51,30 +59,51 @@ __device__ __forceinline__ Entry gather_entry(uint32_t g, bool cull, const float
     e.id = g;
     e.a = make_float4(uv.x, uv.y, 0.5f * ca, cb);
     e.b = make_float4(0.5f * cc, rho, r0, r1);
-    if (cull) {
-        // radii = ceil(sqrt(2 k' Sigma'_xx)) + 1 with k' > ln(255 rho): every pixel centre whose
-        // alpha can reach 1/255 lies inside u +- rx; widen by 1 + rx/64 px more for fp32 slack.
-        const int2 r = __ldg(radii + g);
-        const float mx = (float)r.x * (1.0f + 1.0f / 64.0f) + 1.0f;
-        const float my = (float)r.y * (1.0f + 1.0f / 64.0f) + 1.0f;
-        e.box = make_float4(uv.x - mx, uv.x + mx, uv.y - my, uv.y + my);
-    } else {
-        e.box = make_float4(-INFINITY, INFINITY, -INFINITY, INFINITY);
-    }
+    if (CULL == kCullBox) e.r = __ldg(radii + g);
     return e;
 }
 
 __device__ __forceinline__ void store_entry(WarpStage& s, int lane, const Entry& e) {
     s.a[lane] = e.a;
     s.b[lane] = e.b;
-    s.box[lane] = e.box;
     s.c2[lane] = e.c2;
     s.id[lane] = e.id;
 }
 
-// warp patch [x0+0.5, x0+7.5] x [y0+0.5, y0+3.5] misses the support box
-__device__ __forceinline__ bool culled(const float4 bx, float wx0, float wx1, float wy0, float wy1) {
-    return bx.y < wx0 || bx.x > wx1 || bx.w < wy0 || bx.z > wy1;
+// sigma at one candidate point of the patch minus the bound on its fp32 evaluation error
+// (the kernel's pinned evaluation and this one each err by < 1e-6 (ha dx^2 + hc dy^2), since
+// |b dx dy| <= ha dx^2 + hc dy^2 for a positive-definite conic)
+__device__ __forceinline__ float sigma_lower(float ha, float b, float hc, float dx, float dy) {
+    const float q = ha * dx * dx + hc * dy * dy;
+    return fmaf(b * dx, dy, q) - 2e-5f * q;
+}
+
+// true if no pixel centre of the warp patch [wx0, wx1] x [wy0, wy1] can composite entry (A, B).
+// kCullEllipse: sigma(dx, dy) = ha dx^2 + b dx dy + hc dy^2 (dx = u - x) is convex with its
+// minimum 0 at the centre; over the rectangle its minimum lies on one of the 4 edges, where it
+// is a 1-D quadratic minimised at the clamped stationary point.  A pixel composites only if
+// rho G >= 1/255, i.e. sigma <= ln(255 rho) (+ ex2 / log approximation slack < 1e-5), so the
+// test culls only when the lower bound exceeds ln(255 rho) + 1e-3.
+template <int CULL>
+__device__ __forceinline__ bool culled(const Entry& e, float wx0, float wx1, float wy0, float wy1) {
+    if (CULL == kCullBox) {
+        // radii = ceil(sqrt(2 k' Sigma'_xx)) + 1 with k' > ln(255 rho): every pixel centre whose
+        // alpha can reach 1/255 lies inside u +- rx; widen by 1 + rx/64 px more for fp32 slack.
+        const float mx = (float)e.r.x * (1.0f + 1.0f / 64.0f) + 1.0f;
+        const float my = (float)e.r.y * (1.0f + 1.0f / 64.0f) + 1.0f;
+        return e.a.x + mx < wx0 || e.a.x - mx > wx1 || e.a.y + my < wy0 || e.a.y - my > wy1;
+    } else if (CULL == kCullEllipse) {
+        const float dxl = e.a.x - wx1, dxh = e.a.x - wx0, dyl = e.a.y - wy1, dyh = e.a.y - wy0;
+        if (dxl <= 0.0f && dxh >= 0.0f && dyl <= 0.0f && dyh >= 0.0f) return false;
+        const float ha = e.a.z, b = e.a.w, hc = e.b.x;
+        const float kx = __fdividef(-b, 2.0f * ha), ky = __fdividef(-b, 2.0f * hc);
+        float m = sigma_lower(ha, b, hc, dxl, fminf(fmaxf(ky * dxl, dyl), dyh));
+        m = fminf(m, sigma_lower(ha, b, hc, dxh, fminf(fmaxf(ky * dxh, dyl), dyh)));
+        m = fminf(m, sigma_lower(ha, b, hc, fminf(fmaxf(kx * dyl, dxl), dxh), dyl));
+        m = fminf(m, sigma_lower(ha, b, hc, fminf(fmaxf(kx * dyh, dxl), dxh), dyh));
+        return m > __logf(255.0f * e.b.y) + 1e-3f;
+    }
+    return false;
 }
 
 __device__ __forceinline__ float exp2_ftz(float x) {
@@ -125,8 +154,9 @@ __device__ __forceinline__ PixelMap<PPT> pixel_map(int tile, int TX) {
 // STATS: diagnostic variant (vks_raster_fwd_stats) that writes no image and instead accumulates
 // stats[0] = list entries visited before each pixel's stop (the algorithm's evaluations),
 // stats[1] = composited pairs, stats[2] = pairs actually evaluated here (after patch culling),
-// stats[3] = sum of n_contrib (entries the backward replays).
-template <int PPT, bool STATS = false>
+// stats[3] = sum of n_contrib (entries the backward replays), stats[4] = (warp, entry) pairs a
+// warp processed after patch culling, stats[5] = those with at least one composited pixel.
+template <int PPT, int CULL, bool STATS = false>
 __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
@@ -139,13 +169,12 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                                                                  int* __restrict__ n_contrib,
                                                                  unsigned long long* __restrict__ stats = nullptr) {
     __shared__ WarpStage stage[8 / PPT];
-    unsigned long long n_eval = 0, n_comp = 0;
+    unsigned long long n_eval = 0, n_comp = 0, n_went = 0, n_wcomp = 0;
     const int TX = tiles_x(cam);
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
-    const bool cull = cfg.footprint == VKS_FOOTPRINT_SUPPORT;
     const float px = (float)pm.x + 0.5f;
     float py[PPT], T[PPT], C0[PPT], C1[PPT], C2[PPT];
     int last[PPT];
@@ -161,7 +190,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
     // software pipeline: ids two batches ahead, gathered entries one batch ahead
     uint32_t id_next = (start + lane < end) ? __ldg(vals + start + lane) : 0u;
     Entry e_next;
-    if (start + lane < end) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
+    if (start + lane < end) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
     id_next = (start + 32 + lane < end) ? __ldg(vals + start + 32 + lane) : 0u;
     for (uint32_t b = start; b < end; b += 32) {
         bool all_done = true;
@@ -172,23 +201,24 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
         // each lane tests its own entry against the warp patch; the warp then visits only the
         // entries whose support box meets the patch, in list order
         unsigned live = __ballot_sync(VKS_FULL_MASK, b + lane < end &&
-                                                         !culled(e_next.box, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
+                                                         !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
         if (b + lane < end) store_entry(s, lane, e_next);
         __syncwarp();
-        if (b + 32 + lane < end) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
+        if (b + 32 + lane < end) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
         if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
         while (live) {
             const int j = __ffs(live) - 1;
             live &= live - 1;
             const float4 A = s.a[j], B = s.b[j];
             const float c2 = s.c2[j];
+            bool any = false;
 #pragma unroll
             for (int k = 0; k < PPT; k++) {
                 if (done[k]) continue;
                 float dx, dy, G, rG, alpha;
                 if (STATS) n_eval++;
                 if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
-                if (STATS) n_comp++;
+                if (STATS) { n_comp++; any = true; }
                 const float aT = alpha * T[k];
                 C0[k] = fmaf(B.z, aT, C0[k]);
                 C1[k] = fmaf(B.w, aT, C1[k]);
@@ -197,9 +227,13 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                 last[k] = (int)(b - start) + j + 1;
                 if (T[k] < 1e-4f) done[k] = true;
             }
+            if (STATS) {
+                const bool wany = __any_sync(VKS_FULL_MASK, any);
+                if (lane == 0) { n_went++; n_wcomp += wany; }
+            }
         }
     }
-    if (STATS) {
+    if constexpr (STATS) {
         unsigned long long visited = 0, replay = 0;
 #pragma unroll
         for (int k = 0; k < PPT; k++) {
@@ -212,18 +246,22 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
         atomicAdd(stats + 1, n_comp);
         atomicAdd(stats + 2, n_eval);
         atomicAdd(stats + 3, replay);
-        return;
-    }
+        if (lane == 0) {
+            atomicAdd(stats + 4, n_went);
+            atomicAdd(stats + 5, n_wcomp);
+        }
+    } else {
 #pragma unroll
-    for (int k = 0; k < PPT; k++) {
-        const int y = pm.y0 + 4 * k;
-        if (!(pm.x < cam.width && y < cam.height)) continue;
-        const size_t pix = (size_t)y * cam.width + pm.x;
-        image[3 * pix + 0] = __fadd_rn(C0[k], __fmul_rn(T[k], cfg.bg[0]));
-        image[3 * pix + 1] = __fadd_rn(C1[k], __fmul_rn(T[k], cfg.bg[1]));
-        image[3 * pix + 2] = __fadd_rn(C2[k], __fmul_rn(T[k], cfg.bg[2]));
-        T_final[pix] = T[k];
-        n_contrib[pix] = last[k];
+        for (int k = 0; k < PPT; k++) {
+            const int y = pm.y0 + 4 * k;
+            if (!(pm.x < cam.width && y < cam.height)) continue;
+            const size_t pix = (size_t)y * cam.width + pm.x;
+            image[3 * pix + 0] = __fadd_rn(C0[k], __fmul_rn(T[k], cfg.bg[0]));
+            image[3 * pix + 1] = __fadd_rn(C1[k], __fmul_rn(T[k], cfg.bg[1]));
+            image[3 * pix + 2] = __fadd_rn(C2[k], __fmul_rn(T[k], cfg.bg[2]));
+            T_final[pix] = T[k];
+            n_contrib[pix] = last[k];
+        }
     }
 }
 
@@ -259,7 +297,7 @@ __device__ __forceinline__ float warp_reduce_8plus1(const float v[8], float& e, 
     return c;
 }
 
-template <int PPT>
+template <int PPT, int CULL>
 __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
@@ -279,7 +317,6 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     const unsigned lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
-    const bool cull = cfg.footprint == VKS_FOOTPRINT_SUPPORT;
     const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
     float py[PPT], T[PPT], w0[PPT], w1[PPT], w2[PPT], S0[PPT], S1[PPT], S2[PPT];
@@ -317,7 +354,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     int p0 = bs + (int)lane;
     uint32_t id_next = (p0 >= 0 && p0 < wmax) ? __ldg(vals + start + p0) : 0u;
     Entry e_next;
-    if (p0 >= 0 && p0 < wmax) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
+    if (p0 >= 0 && p0 < wmax) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
     p0 -= 32;
     id_next = (p0 >= 0) ? __ldg(vals + start + p0) : 0u;
     for (; bs > -32; bs -= 32) {
@@ -326,13 +363,13 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
         {
             const int p = bs + (int)lane;
             const bool ok = p >= 0 && p < wmax;
-            live = __ballot_sync(VKS_FULL_MASK, ok && !culled(e_next.box, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
+            live = __ballot_sync(VKS_FULL_MASK, ok && !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
             if (ok) store_entry(s, lane, e_next);
         }
         __syncwarp();
         {
             const int p = bs - 32 + (int)lane;
-            if (p >= 0) e_next = gather_entry(id_next, cull, means2d, conics, colors, opac, radii);
+            if (p >= 0) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
             if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
         }
         while (live) {  // back to front over the entries whose support box meets the patch
@@ -378,31 +415,70 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     }
 }
 
-template <int PPT>
+template <int PPT, int CULL>
 int launch_fwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_fwd_kernel<PPT><<<n_tiles, 32 * 8 / PPT, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d),
-                                                             conics, colors, opacities,
-                                                             reinterpret_cast<const int2*>(radii), vals, tile_offsets,
-                                                             image, T_final, n_contrib);
+    raster_fwd_kernel<PPT, CULL><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
+        cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
+        reinterpret_cast<const int2*>(radii), vals, tile_offsets, image, T_final, n_contrib);
     return LaunchCheck::check();
 }
 
-template <int PPT>
+template <int PPT, int CULL>
 int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                const uint32_t* tile_offsets, const float* T_final, const int32_t* n_contrib,
                const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
                cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_bwd_kernel<PPT><<<n_tiles, 32 * 8 / PPT, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d),
-                                                             conics, colors, opacities,
-                                                             reinterpret_cast<const int2*>(radii), vals, tile_offsets,
-                                                             T_final, n_contrib, dL_dimage, dmeans2d, dconics,
-                                                             dcolors, dopacities);
+    raster_bwd_kernel<PPT, CULL><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
+        cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
+        reinterpret_cast<const int2*>(radii), vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics,
+        dcolors, dopacities);
     return LaunchCheck::check();
+}
+
+int env_choice(const char* var, int dflt, int lo, int hi) {
+    const char* e = getenv(var);
+    const int v = e ? atoi(e) : dflt;
+    return (v >= lo && v <= hi) ? v : dflt;
+}
+
+// patch culling: ellipse by default (valid for both footprints); the box test needs the support
+// footprint's radii, so it falls back to no culling under 3SIGMA
+int cull_choice(const vks_config& cfg) {
+    const int mode = env_choice("VKS_RASTER_CULL", kCullEllipse, kCullNone, kCullEllipse);  // read per call (tests switch it)
+    if (mode == kCullBox && cfg.footprint != VKS_FOOTPRINT_SUPPORT) return kCullNone;
+    return mode;
+}
+
+// pixels per thread: 2 (8x8 warp patches) by default, 4 (8x16) on request
+int ppt_choice(const char* var) { return env_choice(var, 2, 2, 4) == 4 ? 4 : 2; }
+
+template <int PPT>
+int dispatch_fwd(int cull, const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
+                 const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
+                 const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
+    switch (cull) {
+        case kCullNone: return launch_fwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+        case kCullBox: return launch_fwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+        default: return launch_fwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+    }
+}
+
+template <int PPT>
+int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
+                 const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
+                 const uint32_t* tile_offsets, const float* T_final, const int32_t* n_contrib,
+                 const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
+                 cudaStream_t st) {
+    switch (cull) {
+        case kCullNone: return launch_bwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+        case kCullBox: return launch_bwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+        default: return launch_bwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    }
 }
 
 }  // namespace
@@ -411,33 +487,33 @@ int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const 
                             const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                             const uint32_t* tile_offsets, unsigned long long* stats, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_fwd_kernel<2, true><<<n_tiles, 128, 0, st>>>(cfg, cam, reinterpret_cast<const float2*>(means2d), conics,
-                                                        colors, opacities, reinterpret_cast<const int2*>(radii), vals,
-                                                        tile_offsets, nullptr, nullptr, nullptr, stats);
+    const auto m2 = reinterpret_cast<const float2*>(means2d);
+    const auto r2 = reinterpret_cast<const int2*>(radii);
+    switch (cull_choice(cfg)) {
+        case kCullNone:
+            raster_fwd_kernel<2, kCullNone, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
+                                                                           vals, tile_offsets, nullptr, nullptr, nullptr, stats);
+            break;
+        case kCullBox:
+            raster_fwd_kernel<2, kCullBox, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
+                                                                          vals, tile_offsets, nullptr, nullptr, nullptr, stats);
+            break;
+        default:
+            raster_fwd_kernel<2, kCullEllipse, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
+                                                                              vals, tile_offsets, nullptr, nullptr, nullptr, stats);
+    }
     return LaunchCheck::check();
 }
-
-namespace {
-
-int ppt_choice(const char* var) {
-    const char* e = getenv(var);
-    const int v = e ? atoi(e) : 2;
-    return (v == 1 || v == 2 || v == 4) ? v : 2;
-}
-
-}  // namespace
 
 int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const uint32_t* vals, const uint32_t* tile_offsets, float* image, float* T_final,
                       int32_t* n_contrib, cudaStream_t st) {
     (void)n;
-    static const int ppt = ppt_choice("VKS_RASTER_FWD_PPT");
-    switch (ppt) {
-        case 1: return launch_fwd<1>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
-        case 4: return launch_fwd<4>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
-        default: return launch_fwd<2>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
-    }
+    const int ppt = ppt_choice("VKS_RASTER_FWD_PPT");
+    const int cull = cull_choice(cfg);
+    if (ppt == 4) return dispatch_fwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+    return dispatch_fwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
 }
 
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
@@ -446,12 +522,10 @@ int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
                       const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics,
                       float* dcolors, float* dopacities, cudaStream_t st) {
     (void)n;
-    static const int ppt = ppt_choice("VKS_RASTER_BWD_PPT");
-    switch (ppt) {
-        case 1: return launch_bwd<1>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-        case 4: return launch_bwd<4>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-        default: return launch_bwd<2>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-    }
+    const int ppt = ppt_choice("VKS_RASTER_BWD_PPT");
+    const int cull = cull_choice(cfg);
+    if (ppt == 4) return dispatch_bwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    return dispatch_bwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
 }
 
 }  // namespace vks

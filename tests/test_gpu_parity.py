@@ -243,3 +243,52 @@ def test_grad_overwrite_equals_accumulate_into_zero(coeffs, deg):
         assert (v[~vis] == 0).all(), k                            # unseen Gaussians: exact zeros
         # seen Gaussians: same arithmetic up to FMA contraction choices of the two instantiations
         assert torch.allclose(v[vis], ref[vis], rtol=1e-5, atol=1e-6 * ref.abs().max().item()), k
+
+
+# ------------------------------------------------------------------ raster variants
+
+def _stats(cfg, cam, scene):
+    import torch
+    import paper_2605_00219_b200 as P
+    params = P.GaussianParams.from_host(scene)
+    r = P.ViewRenderer(params.n, cam["width"], cam["height"])
+    r.forward(cfg, cam, params)
+    st = torch.zeros(6, dtype=torch.int64, device="cuda")
+    P.vks_raster_fwd_stats(cfg, cam, r.means2d, r.conics, r.colors, r.opacities, r.radii, r.vals, r.tile_offsets, st)
+    return [int(x) for x in st.tolist()]
+
+
+@pytest.mark.parametrize("fp", [0, 1])
+def test_patch_culling_and_ppt_variants_agree(fp, monkeypatch):
+    """Patch culling only skips (warp, entry) pairs that cannot composite, and the pixel-per-thread
+    layout does not change any pixel's sequence: every variant (no culling / support box /
+    exact ellipse, 2 or 4 pixels per thread) gives the identical image, T and n_contrib, and the
+    same gradients up to atomic summation order."""
+    s = synth.make_scene(200000, "indoor", 70)
+    cam = synth.ring_cameras(400, 300, "indoor", 8)[3]
+    cfg = synth.default_render_config(footprint=fp)
+    dL = synth.upstream_grad(300, 400, 5)
+    variants = [("2", "2", "0"), ("2", "2", "2"), ("4", "4", "2"), ("2", "2", "1")]
+    if fp == 1:
+        variants = variants[:3]  # the box test needs the support footprint
+    runs, stats = {}, {}
+    for fw, bw, cull in variants:
+        monkeypatch.setenv("VKS_RASTER_FWD_PPT", fw)
+        monkeypatch.setenv("VKS_RASTER_BWD_PPT", bw)
+        monkeypatch.setenv("VKS_RASTER_CULL", cull)
+        runs[(fw, bw, cull)] = run_gpu(s, cam, cfg, dL=dL)
+        stats[(fw, bw, cull)] = _stats(cfg, cam, s)
+    base = runs[variants[0]]
+    assert base["num_isects"] > 100000
+    for v in variants[1:]:
+        g = runs[v]
+        for k in ("image", "T_final", "n_contrib"):
+            assert np.array_equal(g[k], base[k]), (v, k)
+        for k in ("dmeans2d", "dconics", "dcolors", "dopacities"):
+            scale = np.abs(base[k]).max()
+            assert np.allclose(g[k], base[k], rtol=1e-4, atol=1e-6 * scale), (v, k)
+    s0, s2 = stats[variants[0]], stats[variants[1]]
+    assert s2[1] == s0[1]  # composited pairs
+    assert s2[0] == s0[0] and s2[3] == s0[3]  # visited / replayed do not depend on culling
+    assert s2[2] < s0[2] and s2[4] < s0[4]    # ellipse culling removes evaluations
+    report(f"cull_fp{fp}", dict(stats={"/".join(k): v for k, v in stats.items()}))

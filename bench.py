@@ -103,14 +103,17 @@ def algorithmic_bytes(n, vis, m, K=16):
     (DESIGN.md §6).  Parameters are fp32; sh has K coefficients per channel."""
     sh = 12 * K
     return dict(
-        # means for all; log_scales/quats/logit of culled-after-near (upper bound: all culled);
-        # the rest of the parameters (SH only when visible); radii+tiles for all; 40 B of outputs
-        project_fwd=12 * n + 28 * (n - vis) + (12 + 16 + 4 + sh) * vis + 12 * n + 40 * vis,
-        # id-order scan (read tiles twice, write offsets) + 4 depth passes (count: read key,
-        # scatter: read key+id, write key+id; pass 0 reads tiles+depths) + the rect gather of the
-        # last depth pass + depth-order scan + key expansion + 2 tile passes (last writes ids only)
-        bin_sort=(12 * n + 4 * (4 * n + 16 * n) + 4 * n + (16 + 8) * vis + (16 + 4) * vis
-                  + (12 * vis + 8 * m) + (20 * m) + (16 * m)),
+        # geometry + opacity of every Gaussian (44 B), SH rows of the visible ones; radii + tiles
+        # written for all (12 B), the other 40 B of outputs for the visible
+        project_fwd=44 * n + sh * vis + 12 * n + 40 * vis,
+        # id-order scan (read tiles twice, write offsets) + compaction of the visible (read depth,
+        # means2d, radii; write depth key, id, rect code) + 4 depth passes over V (count 4 B, scatter
+        # 8 B in / 8 B out) + the last pass's rect gather (8 B in, 8 B out) + depth-order scan (rect
+        # codes twice, slots out) + rect difference array (8 B) + key expansion twice (rect code,
+        # slot, id: 16 B each) writing 8 B per key + the last tile pass (count 4 B, scatter 8 B in,
+        # 4 B out per key)
+        bin_sort=(12 * n + (20 + 16) * vis + 4 * 20 * vis + 16 * vis + (16 + 4) * vis + 8 * vis
+                  + 2 * 16 * vis + 8 * m + (4 + 8 + 4) * m),
         # overwrite semantics: params + 2D grads + colours of visible, radii of all, 236 B written for all
         project_bwd=8 * n + vis * ((40 + sh) + 36 + 12) + n * (40 + sh),
     )

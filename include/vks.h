@@ -80,7 +80,7 @@ typedef struct {
 enum {
     VKS_OK = 0,
     VKS_ERR_INVALID_ARG = 1,
-    VKS_ERR_CAPACITY = 2,   /* vks_bin_sort: M > capacity (or M >= 2^32); *num_isects holds M */
+    VKS_ERR_CAPACITY = 2,   /* vks_bin_sort: M > capacity (or M >= 2^30); *num_isects holds M */
     VKS_ERR_WORKSPACE = 3,  /* workspace too small */
     VKS_ERR_CUDA = 4,       /* launch / runtime failure (incl. no CUDA device) */
     VKS_ERR_UNSUPPORTED = 5
@@ -131,7 +131,8 @@ size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles
  *                           nullable (the rasterizer needs only vals and tile_offsets)
  *   tile_offsets [n_tiles+1] u32 <- CSR: #entries with tile id < t
  *   keys_unsorted / vals_unsorted (nullable, debug; [capacity] like keys/vals): the pre-sort pairs.
- * If M > capacity (or M >= 2^32) returns VKS_ERR_CAPACITY after writing
+ * Tile grids of >= 2^21 tiles return VKS_ERR_INVALID_ARG.
+ * If M > capacity (or M >= 2^30) returns VKS_ERR_CAPACITY after writing
  * *num_isects, touching nothing else; the call is idempotent, so the caller
  * regrows and calls again.  Synchronises `stream` once (to read M).
  * workspace: device memory of >= vks_bin_sort_workspace_bytes(n, capacity, n_tiles).

@@ -8,26 +8,28 @@
 // Gaussians (16 B/Gaussian per pass) instead of over the M ~ 4.4 N keys, and only the tile bits
 // are sorted over the keys:
 //
-//  1. scan (id order)    reduce-then-scan of tiles_touched -> offsets, M, V.
-//  2. radix pass x4       8-bit LSD passes over (depth key, id) of all N Gaussians (culled ones
-//                         take the key 0xFFFFFFFF and sort last); pass 0 derives the keys from
-//                         tiles_touched / depths on the fly.
-//  3. scan (depth order) reduce-then-scan of the tile counts of the depth-ordered rect codes
-//                         (the last depth pass gathers each visible Gaussian's rect once and lays it
-//                         out as a 64-bit code, 4 x u16) -> slot of each Gaussian's first key.
-//  4. keys_kernel         warp-cooperative expansion of the rect codes in depth order into
-//                         (tile, id) pairs with coalesced stores; 2-D difference array of the
-//                         rects accumulated per block in shared memory.
-//  5. tile_count_kernel   2-D prefix of the difference array -> per-tile list lengths -> CSR
-//                         tile_offsets.
-//  6. radix pass x1-3     stable LSD passes over the tile bits (<= 8 bits each) of the M pairs;
-//                         the last one writes the ids (and, on request, the u64 keys).
+//  1. scan (id order)    reduce-then-scan of tiles_touched -> offsets, M, V; the down-sweep also
+//                         compacts the V visible Gaussians, in id order, into (depth bits, id) and
+//                         writes each one's tile rect as a 64-bit code (4 x u16) at its id.
+//  2. radix pass x4       8-bit LSD passes over the V (depth bits, id) pairs; the last gathers the
+//                         rect codes into depth order.
+//  3. scan (depth order) reduce-then-scan of the rect tile counts -> first key slot of each
+//                         Gaussian, and first[b] = the Gaussian holding key slot 4096 b.
+//  4. rect_diff_kernel    2-D difference array of the rects (4 shared-memory updates per Gaussian)
+//     tile_count_kernel   2-D prefix -> per-tile list lengths -> CSR tile_offsets.
+//  5. key pass            the first tile-bit pass straight from the rect codes, never storing the
+//                         unsorted keys: keys_count_kernel histograms the digit of each 4096-slot
+//                         key block from whole rect rows (a row is a run of consecutive tile ids);
+//                         keys_scatter_kernel expands the block's keys (tile, id) into shared memory
+//                         and ranks / stores them like any radix pass.
+//  6. radix pass x0-2     the remaining stable LSD tile-bit passes (<= 8 bits each) over the M
+//                         pairs; the last one writes the ids (and, on request, the u64 keys).
 // Every radix pass is reduce-then-scan: digit counts per 4096-key block, one exclusive scan of
 // the (digit-major) count matrix, then a scatter kernel (TMA bulk copy of the block into shared
 // memory, warp-level ballot multi-split ranking, in-place reorder, digit-contiguous stores).  No block
 // ever waits on another (a single-pass decoupled look-back over 256 digits walked hundreds of
 // in-flight blocks back on this workload).
-// The TU is compiled with -fmad=false (the tile-rect recomputation must equal projection's).
+// The TU is compiled with -fmad=false (the tile-rect computation must equal projection's).
 #include <stdlib.h>
 
 #include <algorithm>
@@ -50,7 +52,6 @@ constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per block
 constexpr int kDepthPasses = 4;
 constexpr int kMaxTilePasses = 3;
-constexpr int kLookbackChunk = 8;
 
 constexpr u64 kScanFlagAgg = 1ull << 62;
 constexpr u64 kScanFlagInc = 2ull << 62;
@@ -82,6 +83,8 @@ struct Workspace {
     u32* counts;         // [256 * sort tiles] digit counts of the current pass (digit-major)
     u32* offs;           // its exclusive scan
     u64* rcs;            // [n] tile-rect codes in depth order
+    u64* rc_by_id;       // [n] tile-rect codes at the Gaussian id (visible rows)
+    u32* first;          // [key blocks + 2] depth-order Gaussian holding slot 4096 b
     u32* part_sum;       // [scan blocks] block sums of the 1-D scans
     u32* part_vis;       // [scan blocks] visible counts
     // region A (zeroed before the scan)
@@ -115,6 +118,8 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
     w.counts = reinterpret_cast<u32*>(take(4 * 256 * sort_tiles));
     w.offs = reinterpret_cast<u32*>(take(4 * 256 * sort_tiles));
     w.rcs = reinterpret_cast<u64*>(take(8 * nn));
+    w.rc_by_id = reinterpret_cast<u64*>(take(8 * nn));
+    w.first = reinterpret_cast<u32*>(take(4 * ((cap + kSortTile - 1) / kSortTile + 2)));
     w.part_sum = reinterpret_cast<u32*>(take(4 * scan_tiles));
     w.part_vis = reinterpret_cast<u32*>(take(4 * scan_tiles));
     const size_t a0 = off;
@@ -161,42 +166,32 @@ __device__ __forceinline__ int rect_tiles(u64 c) {
 //   scan_partials_kernel one block: exclusive scan of the block sums, totals
 //   scan_down_kernel     per block: rescan + block prefix -> output
 // MODE 0: element i = tiles_touched[i];  MODE 1: element r = tiles of the depth-sorted rect code r.
+// Warp-striped layout: warp w of a block owns the 512 consecutive elements starting at
+// blockIdx.x * kScanTile + 512 w; lane l holds elements 32 j + l (j < 16), so every load and store
+// instruction of a warp touches 32 consecutive elements.
+__device__ __forceinline__ u64 warp_base(int warp) { return (u64)blockIdx.x * kScanTile + (u64)warp * 32 * kScanItems; }
+
 template <int MODE>
 __device__ __forceinline__ void load_scan_items(const int* __restrict__ tiles, const u64* __restrict__ rc, u64 count,
-                                                u64 base, int v[kScanItems]) {
-    if (MODE == 0) {
-        if (base + kScanItems <= count && ((reinterpret_cast<uintptr_t>(tiles + base) & 15) == 0)) {
+                                                u64 wbase, int lane, int v[kScanItems]) {
 #pragma unroll
-            for (int j = 0; j < kScanItems; j += 4) {
-                const int4 q = __ldg(reinterpret_cast<const int4*>(tiles + base + j));
-                v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < kScanItems; j++) v[j] = base + j < count ? __ldg(tiles + base + j) : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < kScanItems; j++) v[j] = v[j] > 0 ? v[j] : 0;
-    } else {
-#pragma unroll
-        for (int j = 0; j < kScanItems; j++) v[j] = base + j < count ? rect_tiles(__ldg(rc + base + j)) : 0;
+    for (int j = 0; j < kScanItems; j++) {
+        const u64 i = wbase + 32 * j + lane;
+        if (MODE == 0) v[j] = i < count ? max(__ldg(tiles + i), 0) : 0;
+        else v[j] = i < count ? rect_tiles(__ldg(rc + i)) : 0;
     }
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(vks_camera cam, const int* __restrict__ tiles,
-                                                                  const float2* __restrict__ means2d,
-                                                                  const int2* __restrict__ radii,
-                                                                  const u64* __restrict__ rc_in, u64* __restrict__ rc_out,
-                                                                  u64 count, u32* __restrict__ part_sum,
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* __restrict__ tiles,
+                                                                  const u64* __restrict__ rc_in, u64 count,
+                                                                  u32* __restrict__ part_sum,
                                                                   u32* __restrict__ part_vis) {
     __shared__ u32 s_sum[kScanThreads / 32], s_vis[kScanThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const u64 base = (u64)blockIdx.x * kScanTile + (u64)tid * kScanItems;
     int v[kScanItems];
-    load_scan_items<MODE>(tiles, rc_in, count, base, v);
+    load_scan_items<MODE>(tiles, rc_in, count, warp_base(warp), lane, v);
     u32 sum = 0, vis = 0;
-    (void)cam; (void)means2d; (void)radii; (void)rc_out;
 #pragma unroll
     for (int j = 0; j < kScanItems; j++) {
         sum += (u32)v[j];
@@ -215,140 +210,224 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(vks_camera ca
     }
 }
 
-// exclusive scan of the P block sums in place; totals[0] = sum, totals[1] = sum of part_vis
-__global__ void __launch_bounds__(1024) scan_partials_kernel(u32* __restrict__ part_sum, const u32* __restrict__ part_vis,
+// exclusive scans of the P block sums (and block visible counts) in place; totals[0] = sum,
+// totals[1] = number of visible Gaussians
+__global__ void __launch_bounds__(1024) scan_partials_kernel(u32* __restrict__ part_sum, u32* __restrict__ part_vis,
                                                             u32 P, u64* __restrict__ totals) {
-    __shared__ u32 s_w[32];
-    __shared__ u64 s_carry;
-    __shared__ u64 s_vis;
+    __shared__ u32 s_w[32], s_v[32];
+    __shared__ u64 s_carry, s_vcarry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) { s_carry = 0; s_vis = 0; }
+    if (tid == 0) { s_carry = 0; s_vcarry = 0; }
     __syncthreads();
-    u64 vis_acc = 0;
     for (u32 base = 0; base < P; base += 1024) {
         const u32 i = base + tid;
         const u32 c = i < P ? part_sum[i] : 0u;
-        if (i < P && part_vis) vis_acc += part_vis[i];
-        u32 incl = c;
+        const u32 cv = (i < P && part_vis) ? part_vis[i] : 0u;
+        u32 incl = c, vincl = cv;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const u32 t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
-            if (lane >= d) incl += t;
+            const u32 tv = __shfl_up_sync(VKS_FULL_MASK, vincl, d);
+            if (lane >= d) { incl += t; vincl += tv; }
         }
-        if (lane == 31) s_w[warp] = incl;
+        if (lane == 31) { s_w[warp] = incl; s_v[warp] = vincl; }
         __syncthreads();
-        u32 wpre = 0, btot = 0;
+        u32 wpre = 0, btot = 0, vpre = 0, vtot = 0;
         for (int w = 0; w < 32; w++) {
-            if (w < warp) wpre += s_w[w];
+            if (w < warp) { wpre += s_w[w]; vpre += s_v[w]; }
             btot += s_w[w];
+            vtot += s_v[w];
         }
-        const u64 carry = s_carry;
-        if (i < P) part_sum[i] = (u32)(carry + wpre + incl - c);
+        const u64 carry = s_carry, vcarry = s_vcarry;
+        if (i < P) {
+            part_sum[i] = (u32)(carry + wpre + incl - c);
+            if (part_vis) part_vis[i] = (u32)(vcarry + vpre + vincl - cv);
+        }
         __syncthreads();
-        if (tid == 0) s_carry = carry + btot;
+        if (tid == 0) { s_carry = carry + btot; s_vcarry = vcarry + vtot; }
         __syncthreads();
     }
-    vis_acc = __reduce_add_sync(VKS_FULL_MASK, (u32)vis_acc);
-    if (lane == 0 && vis_acc) atomicAdd(reinterpret_cast<unsigned long long*>(&s_vis), (unsigned long long)vis_acc);
-    __syncthreads();
     if (tid == 0) {
         totals[0] = s_carry;
-        if (part_vis) totals[1] = s_vis;
+        if (part_vis) totals[1] = s_vcarry;
     }
 }
+
+// inclusive scan across the warp
+__device__ __forceinline__ u32 warp_incl_scan(u32 x, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u32 t = __shfl_up_sync(VKS_FULL_MASK, x, d);
+        if (lane >= d) x += t;
+    }
+    return x;
+}
+
+// exclusive scan of the striped items of one warp: out[j] = warp-local exclusive prefix of v[j]
+__device__ __forceinline__ u32 warp_striped_excl(const int v[kScanItems], u32 out[kScanItems], int lane) {
+    u32 carry = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        const u32 incl = warp_incl_scan((u32)v[j], lane);
+        out[j] = carry + incl - (u32)v[j];
+        carry += __shfl_sync(VKS_FULL_MASK, incl, 31);
+    }
+    return carry;  // warp total
+}
+
+// MODE 0 additionally compacts the visible Gaussians, in id order, into (depth bits, id) pairs at
+// their visible index (the input of the depth sort) and writes each visible Gaussian's tile-rect
+// code at its id (rc_by_id; gathered once by the last depth pass).
+struct CompactOut {
+    const u32* vis_prefix;   // [blocks] exclusive block prefix of the visible counts
+    const u32* depth_bits;   // [n]
+    const float2* means2d;   // [n]
+    const int2* radii;       // [n]
+    int TX, TY;
+    u32* vkeys;              // [V] depth bits, id order
+    u32* vids;               // [V] ids
+    u64* rc_by_id;           // [n] rect codes (visible rows only)
+    u32* first;              // MODE 1: [ceil(M / 4096) + 1] Gaussian holding key slot 4096 b
+};
 
 template <int MODE>
 __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const int* __restrict__ tiles, const u64* __restrict__ rc,
                                                                 u64 count, const u32* __restrict__ part_prefix,
-                                                                u32* __restrict__ out) {
-    __shared__ u32 s_w[kScanThreads / 32];
+                                                                u32* __restrict__ out, const CompactOut co) {
+    __shared__ u32 s_w[kScanThreads / 32], s_v[kScanThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const u64 base = (u64)blockIdx.x * kScanTile + (u64)tid * kScanItems;
+    const u64 wbase = warp_base(warp);
     int v[kScanItems];
-    load_scan_items<MODE>(tiles, rc, count, base, v);
-    u32 tsum = 0;
+    u32 ex[kScanItems];
+    load_scan_items<MODE>(tiles, rc, count, wbase, lane, v);
+    const u32 wtot = warp_striped_excl(v, ex, lane);
+    u32 wvis = 0;
+    if (MODE == 0) {
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) tsum += (u32)v[j];
-    u32 incl = tsum;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const u32 t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
-        if (lane >= d) incl += t;
+        for (int j = 0; j < kScanItems; j++) wvis += __popc(__ballot_sync(VKS_FULL_MASK, v[j] > 0));
     }
-    if (lane == 31) s_w[warp] = incl;
+    if (lane == 0) { s_w[warp] = wtot; s_v[warp] = wvis; }
     __syncthreads();
-    u32 wpre = 0;
+    u32 pre = part_prefix[blockIdx.x], vpre = MODE == 0 ? co.vis_prefix[blockIdx.x] : 0u;
 #pragma unroll
     for (int w = 0; w < kScanThreads / 32; w++)
-        if (w < warp) wpre += s_w[w];
-    u32 run = part_prefix[blockIdx.x] + wpre + incl - tsum;
+        if (w < warp) { pre += s_w[w]; vpre += s_v[w]; }
 #pragma unroll
     for (int j = 0; j < kScanItems; j++) {
-        if (base + j < count) out[base + j] = run;
-        run += (u32)v[j];
+        const u64 i = wbase + 32 * j + lane;
+        if (i < count) {
+            out[i] = pre + ex[j];
+            if (MODE == 1) {  // key blocks whose first slot lies in this Gaussian's range
+                const u32 a = pre + ex[j], e = a + (u32)v[j];
+                for (u32 b = (a + kSortTile - 1) / kSortTile; b * (u32)kSortTile < e; b++) co.first[b] = (u32)i;
+                if (i == count - 1) co.first[(e + kSortTile - 1) / kSortTile] = (u32)i;  // sentinel: last Gaussian
+            }
+        }
+    }
+    if (MODE == 0) {
+        const u32 ltmask = lanemask_lt();
+        const u32* __restrict__ depth_bits = co.depth_bits;
+        const float2* __restrict__ means2d = co.means2d;
+        const int2* __restrict__ radii = co.radii;
+        // two halves of 8 rows: all loads of a half in flight before its stores
+#pragma unroll
+        for (int h = 0; h < kScanItems; h += 8) {
+            u32 db[8];
+            float2 m[8];
+            int2 r[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const u64 i = wbase + 32 * (h + q) + lane;
+                if (v[h + q] > 0) {
+                    db[q] = __ldg(depth_bits + i);
+                    m[q] = __ldg(means2d + i);
+                    r[q] = __ldg(radii + i);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const u64 i = wbase + 32 * (h + q) + lane;
+                const bool vis = v[h + q] > 0;
+                const u32 bal = __ballot_sync(VKS_FULL_MASK, vis);
+                if (vis) {
+                    const u32 slot = vpre + __popc(bal & ltmask);
+                    int x0, x1, y0, y1;
+                    rect_of(m[q], r[q], co.TX, co.TY, x0, x1, y0, y1);
+                    co.vkeys[slot] = db[q];
+                    co.vids[slot] = (u32)i;
+                    co.rc_by_id[i] = pack_rect(x0, x1, y0, y1);
+                }
+                vpre += __popc(bal);
+            }
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// 4. key generation (+ tile-rect difference array)
-constexpr int kKeysThreads = 512;
-constexpr int kKeysWarps = kKeysThreads / 32;
-constexpr int kKeysSmemDiffMax = 160 * 1024 / 4;  // cells
+// 4a. tile-rect difference array (per-tile key counts without touching the keys): persistent
+// blocks, 4 shared-memory updates per visible Gaussian, one flush per block.
+constexpr int kDiffThreads = 512;
+constexpr int kDiffSmemMax = 160 * 1024 / 4;  // cells
+constexpr size_t kTileCountSmemMax = 200 * 1024;  // bytes
 
-// MODE 0: depth order: element r = Gaussian sid[r] with rect code rc[r] -> (tile, id) pairs at
-//         slot0[r] + k, plus the difference array of the rects.
-// MODE 1: id order (debug keys_unsorted / vals_unsorted): rect of Gaussian i -> u64 keys at slot0[i] + k.
-template <bool SMEM_DIFF, int MODE>
-__global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int64_t count, const u32* __restrict__ sid,
-                                                           const u64* __restrict__ rc, const int* __restrict__ tiles,
-                                                           const float2* __restrict__ means2d,
-                                                           const int2* __restrict__ radii, const float* __restrict__ depths,
-                                                           const u32* __restrict__ slot0, u32* __restrict__ tkeys,
-                                                           u32* __restrict__ tvals, u64* __restrict__ keys64,
-                                                           int* __restrict__ diff) {
+template <bool SMEM_DIFF>
+__global__ void __launch_bounds__(kDiffThreads) rect_diff_kernel(int TX, int TY, u32 count, const u64* __restrict__ rc,
+                                                                int* __restrict__ diff) {
     extern __shared__ int s_diff[];
-    __shared__ int s_incl[kKeysWarps][32];
-    __shared__ int s_x0[kKeysWarps][32], s_y0[kKeysWarps][32], s_w[kKeysWarps][32];
-    __shared__ u32 s_id[kKeysWarps][32];
-    __shared__ u32 s_db[kKeysWarps][32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int TX = tiles_x(cam), TY = tiles_y(cam);
+    const int tid = threadIdx.x;
     const int W1 = TX + 1;
     const int cells = W1 * (TY + 1);
     if (SMEM_DIFF) {
-        for (int j = tid; j < cells; j += kKeysThreads) s_diff[j] = 0;
+        for (int j = tid; j < cells; j += kDiffThreads) s_diff[j] = 0;
         __syncthreads();
     }
     int* dd = SMEM_DIFF ? s_diff : diff;
+    for (u32 r = blockIdx.x * kDiffThreads + tid; r < count; r += gridDim.x * kDiffThreads) {
+        int x0, x1, y0, y1;
+        unpack_rect(__ldg(rc + r), x0, x1, y0, y1);
+        atomicAdd(dd + y0 * W1 + x0, 1);
+        atomicAdd(dd + y0 * W1 + x1, -1);
+        atomicAdd(dd + y1 * W1 + x0, -1);
+        atomicAdd(dd + y1 * W1 + x1, 1);
+    }
+    if (SMEM_DIFF) {
+        __syncthreads();
+        for (int j = tid; j < cells; j += kDiffThreads) {
+            const int v = s_diff[j];
+            if (v) atomicAdd(diff + j, v);
+        }
+    }
+}
+
+// 4b. debug only (keys_unsorted / vals_unsorted): the u64 keys in id order exactly as "Generate
+// Keys" defines them, written at offsets[i] + k, rows outer.  One warp expands 32 rects.
+constexpr int kKeysThreads = 256;
+constexpr int kKeysWarps = kKeysThreads / 32;
+
+__global__ void __launch_bounds__(kKeysThreads) keys_debug_kernel(vks_camera cam, int64_t count,
+                                                                 const int* __restrict__ tiles,
+                                                                 const float2* __restrict__ means2d,
+                                                                 const int2* __restrict__ radii,
+                                                                 const float* __restrict__ depths,
+                                                                 const u32* __restrict__ slot0,
+                                                                 u32* __restrict__ tvals, u64* __restrict__ keys64) {
+    __shared__ int s_incl[kKeysWarps][32];
+    __shared__ int s_x0[kKeysWarps][32], s_y0[kKeysWarps][32], s_w[kKeysWarps][32];
+    __shared__ u32 s_db[kKeysWarps][32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int TX = tiles_x(cam), TY = tiles_y(cam);
     const int64_t stride = (int64_t)gridDim.x * kKeysWarps * 32;
     for (int64_t r0 = ((int64_t)blockIdx.x * kKeysWarps + warp) * 32; r0 < count; r0 += stride) {
         const int64_t r = r0 + lane;
         int cnt = 0, x0 = 0, y0 = 0, w = 1;
-        u32 g = 0, db = 0;
-        if (r < count) {
-            g = MODE == 0 ? __ldg(sid + r) : (u32)r;
+        u32 db = 0;
+        if (r < count && __ldg(tiles + r) > 0) {
             int x1, y1;
-            if (MODE == 0) {
-                unpack_rect(__ldg(rc + r), x0, x1, y0, y1);
-            } else if (__ldg(tiles + r) > 0) {
-                rect_of(__ldg(means2d + r), __ldg(radii + r), TX, TY, x0, x1, y0, y1);
-            } else {
-                x0 = x1 = y0 = y1 = 0;
-            }
+            rect_of(__ldg(means2d + r), __ldg(radii + r), TX, TY, x0, x1, y0, y1);
             w = x1 - x0;
             cnt = w * (y1 - y0);
-            if (cnt > 0) {
-                if (MODE == 0) {
-                    atomicAdd(dd + y0 * W1 + x0, 1);
-                    atomicAdd(dd + y0 * W1 + x1, -1);
-                    atomicAdd(dd + y1 * W1 + x0, -1);
-                    atomicAdd(dd + y1 * W1 + x1, 1);
-                } else {
-                    db = __float_as_uint(__ldg(depths + g));
-                }
-            } else {
-                w = 1;
-            }
+            db = __float_as_uint(__ldg(depths + r));
+            if (cnt <= 0) { cnt = 0; w = 1; }
         }
         int incl = cnt;
 #pragma unroll
@@ -363,7 +442,6 @@ __global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int6
         s_x0[warp][lane] = x0;
         s_y0[warp][lane] = y0;
         s_w[warp][lane] = w;
-        s_id[warp][lane] = g;
         s_db[warp][lane] = db;
         __syncwarp();
         const u64 base = (u64)__ldg(slot0 + r0);  // slot of the group's first Gaussian (even if empty)
@@ -378,50 +456,57 @@ __global__ void __launch_bounds__(kKeysThreads) keys_kernel(vks_camera cam, int6
             const int tx = s_x0[warp][pos] + (k - ry * ww);
             const int ty = s_y0[warp][pos] + ry;
             const u32 t = (u32)(ty * TX + tx);
-            if (MODE == 0) tkeys[base + e] = t;
-            else keys64[base + e] = ((u64)t << 32) | (u64)s_db[warp][pos];
-            tvals[base + e] = s_id[warp][pos];
+            keys64[base + e] = ((u64)t << 32) | (u64)s_db[warp][pos];
+            tvals[base + e] = (u32)(r0 + pos);
         }
-    }
-    if (SMEM_DIFF) {
-        __syncthreads();
-        for (int j = tid; j < cells; j += kKeysThreads) {
-            const int v = s_diff[j];
-            if (v) atomicAdd(diff + j, v);
-        }
+        __syncwarp();
     }
 }
 
 // ------------------------------------------------------------------------------------------
 // 5. per-tile counts -> CSR tile_offsets
+// The (TX+1) x (TY+1) difference array is staged in shared memory when it fits (SMEM) so the
+// serial column walk is not a chain of global-memory round trips.
+template <bool SMEM>
 __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int* __restrict__ diff,
                                                          u32* __restrict__ tile_offsets) {
+    extern __shared__ int s_cells[];
     __shared__ u32 s_wsum[32];
     __shared__ u32 s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W1 = TX + 1;
-    for (int y = tid; y < TY; y += 1024) {
-        int acc = 0;
-        for (int x = 0; x < TX; x++) { acc += diff[y * W1 + x]; diff[y * W1 + x] = acc; }
+    const int cells = W1 * (TY + 1);
+    int* a = SMEM ? s_cells : diff;
+    if (SMEM) {
+        for (int j = tid; j < cells; j += 1024) s_cells[j] = diff[j];
+        __syncthreads();
+    }
+    // prefix along x: one warp per row, 32 cells per step
+    for (int y = warp; y < TY; y += 32) {
+        int carry = 0;
+        for (int x0 = 0; x0 < TX; x0 += 32) {
+            const int x = x0 + lane;
+            const int v = x < TX ? a[y * W1 + x] : 0;
+            const int incl = (int)warp_incl_scan((u32)v, lane) + carry;
+            if (x < TX) a[y * W1 + x] = incl;
+            carry = __shfl_sync(VKS_FULL_MASK, incl, 31);
+        }
     }
     __syncthreads();
+    // prefix along y: one thread per column
     for (int x = tid; x < TX; x += 1024) {
         int acc = 0;
-        for (int y = 0; y < TY; y++) { acc += diff[y * W1 + x]; diff[y * W1 + x] = acc; }
+        for (int y = 0; y < TY; y++) { acc += a[y * W1 + x]; a[y * W1 + x] = acc; }
     }
     __syncthreads();
+    // exclusive scan of the per-tile counts in tile order
     const int n_tiles = TX * TY;
     if (tid == 0) s_carry = 0;
     __syncthreads();
     for (int base = 0; base < n_tiles; base += 1024) {
         const int t = base + tid;
-        const u32 c = t < n_tiles ? (u32)diff[(t / TX) * W1 + (t % TX)] : 0u;
-        u32 incl = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            u32 v = __shfl_up_sync(VKS_FULL_MASK, incl, d);
-            if (lane >= d) incl += v;
-        }
+        const u32 c = t < n_tiles ? (u32)a[(t / TX) * W1 + (t % TX)] : 0u;
+        const u32 incl = warp_incl_scan(c, lane);
         if (lane == 31) s_wsum[warp] = incl;
         __syncthreads();
         u32 wpre = 0, btot = 0;
@@ -448,10 +533,8 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int* _
 //   scatter_kernel       per tile: TMA bulk copy of keys/values into shared memory (mbarrier),
 //                        stable warp-level ranking (ballot multi-split), in-place shared-memory
 //                        reorder by digit, digit-contiguous coalesced stores.
-enum { kPassPlain = 0, kPassDepthFirst = 1, kPassTileLast = 2, kPassDepthLast = 3 };
+enum { kPassPlain = 0, kPassTileLast = 2, kPassDepthLast = 3 };
 
-// key of element j of the depth-first pass: visible ? f32bits(depth) : 0xFFFFFFFF (sorts last)
-__device__ __forceinline__ u32 depth_key(int tiles, u32 depth_bits) { return tiles > 0 ? depth_bits : 0xFFFFFFFFu; }
 
 // lanes of the warp holding the same DBITS-bit digit (and the same `valid`): DBITS ballots
 // instead of __match_any_sync, whose cost grows with the number of distinct values
@@ -485,7 +568,7 @@ __global__ void __launch_bounds__(kSortThreads) digit_count_kernel(const u32* __
         const u64 idx = base + (u64)i * kSortThreads + tid;
         key[i] = 0;
         if (idx < n)
-            key[i] = MODE == kPassDepthFirst ? depth_key((int)__ldg(kin + idx), __ldg(vin + idx)) : __ldg(kin + idx);
+            key[i] = __ldg(kin + idx);
     }
 #pragma unroll
     for (int i = 0; i < kSortItems; i++) {
@@ -507,30 +590,28 @@ __global__ void __launch_bounds__(kSortThreads) digit_count_kernel(const u32* __
     }
 }
 
-// exclusive scan of a u32 array (decoupled look-back over 4096-element tiles)
+// exclusive scan of a u32 array: single pass over 4096-element tiles (warp-striped loads and
+// stores) with a decoupled look-back done by a whole warp — 32 predecessors' aggregates per step,
+// so a tile does not wait for its predecessor's inclusive prefix (no serial chain across tiles).
 __global__ void __launch_bounds__(kScanThreads) scan_u32_kernel(const u32* __restrict__ in, u32* __restrict__ out,
                                                                u64 count, u64* __restrict__ lb, u32* __restrict__ ctr) {
     __shared__ u32 s_tile;
-    __shared__ u64 s_warp[kScanThreads / 32];
+    __shared__ u32 s_warp[kScanThreads / 32];
     __shared__ u64 s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(ctr, 1u);
     __syncthreads();
     const u64 tile = s_tile;
-    const u64 base = tile * kScanTile + (u64)tid * kScanItems;
-    u32 v[kScanItems];
+    const u64 wbase = tile * kScanTile + (u64)warp * 32 * kScanItems;
+    int v[kScanItems];
+    u32 ex[kScanItems];
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) v[j] = base + j < count ? __ldg(in + base + j) : 0u;
-    u64 tsum = 0;
-#pragma unroll
-    for (int j = 0; j < kScanItems; j++) tsum += v[j];
-    u64 incl = tsum;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        u64 t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
-        if (lane >= d) incl += t;
+    for (int j = 0; j < kScanItems; j++) {
+        const u64 i = wbase + 32 * j + lane;
+        v[j] = i < count ? (int)__ldg(in + i) : 0;
     }
-    if (lane == 31) s_warp[warp] = incl;
+    const u32 wtot = warp_striped_excl(v, ex, lane);
+    if (lane == 0) s_warp[warp] = wtot;
     __syncthreads();
     u64 wpre = 0, btotal = 0;
 #pragma unroll
@@ -538,50 +619,43 @@ __global__ void __launch_bounds__(kScanThreads) scan_u32_kernel(const u32* __res
         if (w < warp) wpre += s_warp[w];
         btotal += s_warp[w];
     }
-    if (tid == 0) {
+    if (warp == 0) {
         u64 excl = 0;
         if (tile == 0) {
-            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb), kScanFlagInc | btotal);
+            if (lane == 0) st_volatile_u64(reinterpret_cast<unsigned long long*>(lb), kScanFlagInc | btotal);
         } else {
-            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagAgg | btotal);
+            if (lane == 0) st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagAgg | btotal);
             int64_t j = (int64_t)tile - 1;
-            bool found = false;
-            while (!found) {
-                u64 st[kLookbackChunk];
+            while (true) {
+                const int64_t q = j - lane;
+                const u64 st = q >= 0 ? ld_volatile_u64(reinterpret_cast<const unsigned long long*>(lb + q))
+                                      : kScanFlagInc;  // before tile 0: inclusive prefix 0
+                const u64 f = st & ~kScanMask;
+                const unsigned inc = __ballot_sync(VKS_FULL_MASK, f == kScanFlagInc);
+                const unsigned pend = __ballot_sync(VKS_FULL_MASK, f == 0);
+                const int first_inc = inc ? __ffs(inc) - 1 : 32;
+                const int first_pend = pend ? __ffs(pend) - 1 : 32;
+                const int take = first_pend < first_inc ? first_pend : min(first_inc + 1, 32);
+                u64 add = lane < take ? (st & kScanMask) : 0;
 #pragma unroll
-                for (int q = 0; q < kLookbackChunk; q++)
-                    st[q] = (j - q >= 0) ? ld_volatile_u64(reinterpret_cast<const unsigned long long*>(lb + j - q)) : 0;
-                int consumed = 0;
-#pragma unroll
-                for (int q = 0; q < kLookbackChunk; q++) {
-                    if (found || consumed < q) break;
-                    const u64 f = st[q] & ~kScanMask;
-                    if (f == 0) break;
-                    excl += st[q] & kScanMask;
-                    consumed = q + 1;
-                    if (f == kScanFlagInc) found = true;
-                }
-                j -= consumed;
+                for (int o = 16; o >= 1; o >>= 1) add += __shfl_xor_sync(VKS_FULL_MASK, add, o);
+                excl += add;
+                if (first_inc < first_pend) break;  // reached an inclusive prefix
+                j -= take;                          // take may be 0: spin on a pending predecessor
             }
-            st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagInc | (excl + btotal));
+            if (lane == 0) st_volatile_u64(reinterpret_cast<unsigned long long*>(lb + tile), kScanFlagInc | (excl + btotal));
         }
-        s_prefix = excl;
+        if (lane == 0) s_prefix = excl;
     }
     __syncthreads();
-    u64 run = s_prefix + wpre + (incl - tsum);
+    const u32 pre = (u32)(s_prefix + wpre);
 #pragma unroll
     for (int j = 0; j < kScanItems; j++) {
-        if (base + j < count) out[base + j] = (u32)run;
-        run += v[j];
+        const u64 i = wbase + 32 * j + lane;
+        if (i < count) out[i] = pre + ex[j];
     }
 }
 
-struct RectSrc {  // kPassDepthLast: where the tile rects come from
-    const float2* means2d;
-    const int2* radii;
-    int TX, TY;
-    u32 visible;   // the first `visible` sorted entries are the visible Gaussians
-};
 
 struct SortSmem {
     alignas(128) u32 keys[kSortTile];  // input staging (bulk copy), then the reordered tile
@@ -595,61 +669,20 @@ struct SortSmem {
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 
-// kPassDepthFirst: kin = tiles_touched, vin = depths; key = depth_key(), value = id.
+// Rank the block's kSortTile staged (key, value) pairs stably by digit, reorder them in shared
+// memory and store them digit-contiguously at their global positions.  On entry: S.keys/S.vals
+// hold the tile (pads: key 0xFFFFFFFF, which rank last and land at dest >= n), S.whist is zero,
+// S.gbase[d] holds the global start of (digit d, this block), and the block is synchronised.
 // kPassTileLast: writes only the values (the caller's vals) and, if keys64, the u64 keys.
-// kPassDepthLast: also writes the rect codes in the sorted order (gathered by id).
+// kPassDepthLast: also writes the rect codes in the sorted order (gathered by id from rc_by_id).
 template <int DBITS, int MODE>
-__global__ void __launch_bounds__(kSortThreads) scatter_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
-                                                             u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
-                                                             int shift, u32 T, const u32* __restrict__ offs,
-                                                             const float* __restrict__ depths,
-                                                             u64* __restrict__ keys64, RectSrc rsrc,
-                                                             u64* __restrict__ rc_out) {
+__device__ __forceinline__ void rank_and_store(SortSmem& S, u32 n, int shift, u32* __restrict__ kout,
+                                               u32* __restrict__ vout, const float* __restrict__ depths,
+                                               u64* __restrict__ keys64, const u64* __restrict__ rc_by_id,
+                                               u64* __restrict__ rc_out) {
     constexpr int RADIX = 1 << DBITS;
     constexpr u32 DMASK = RADIX - 1;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const u32 bar = smem_u32(&S.mbar);
-    const u32 tile = blockIdx.x;
-    const u64 base = (u64)tile * kSortTile;
-    const u32 count = (u32)min((u64)kSortTile, (u64)n - base);
-    const u32 nbulk = count & ~3u;  // 16-byte multiples
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (nbulk) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nbulk * 8u) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                         ::"r"(smem_u32(S.keys)), "l"(kin + base), "r"(nbulk * 4u), "r"(bar) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                         ::"r"(smem_u32(S.vals)), "l"(vin + base), "r"(nbulk * 4u), "r"(bar) : "memory");
-        } else {
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-        }
-    }
-    for (int j = tid; j < kSortWarps * 256; j += kSortThreads) (&S.whist[0][0])[j] = 0;
-    // the block's digit starts: global start of (digit, tile) from the scanned counts
-    for (int d = tid; d < RADIX; d += kSortThreads) S.gbase[d] = __ldg(offs + (u64)d * T + tile);
-    for (u32 j = nbulk + tid; j < (u32)kSortTile; j += kSortThreads) {
-        const bool ok = j < count;
-        S.keys[j] = ok ? kin[base + j] : (MODE == kPassDepthFirst ? 0u : 0xFFFFFFFFu);  // pads rank last
-        S.vals[j] = ok ? vin[base + j] : 0u;
-    }
-    __syncthreads();  // barrier init visible before anyone waits on it
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-        "@!p bra WAIT%=;\n\t}" ::"r"(bar) : "memory");
-    if (MODE == kPassDepthFirst) {
-        __syncthreads();
-        for (int j = tid; j < kSortTile; j += kSortThreads) {
-            S.keys[j] = depth_key((int)S.keys[j], S.vals[j]);  // pads (tiles = 0) become ~0 too
-            S.vals[j] = (u32)(base + j);
-        }
-    }
-    __syncthreads();
     u32 rank[kSortItems];
     const u32 ltmask = lanemask_lt();
     const int seg = warp * 32 * kSortItems;
@@ -716,17 +749,238 @@ __global__ void __launch_bounds__(kSortThreads) scatter_kernel(const u32* __rest
             vout[dest] = val;
             if (MODE == kPassTileLast && keys64)
                 keys64[dest] = ((u64)key << 32) | (u64)__float_as_uint(__ldg(depths + val));
-            if (MODE == kPassDepthLast) {  // rect code in depth order
-                u64 code = 0;
-                if (dest < rsrc.visible) {
-                    int x0, x1, y0, y1;
-                    rect_of(__ldg(rsrc.means2d + val), __ldg(rsrc.radii + val), rsrc.TX, rsrc.TY, x0, x1, y0, y1);
-                    code = pack_rect(x0, x1, y0, y1);
+            if (MODE == kPassDepthLast) rc_out[dest] = __ldg(rc_by_id + val);  // rect code in depth order
+        }
+    }
+}
+
+template <int DBITS, int MODE>
+__global__ void __launch_bounds__(kSortThreads) scatter_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
+                                                             u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
+                                                             int shift, u32 T, const u32* __restrict__ offs,
+                                                             const float* __restrict__ depths,
+                                                             u64* __restrict__ keys64, const u64* __restrict__ rc_by_id,
+                                                             u64* __restrict__ rc_out) {
+    constexpr int RADIX = 1 << DBITS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+    const u32 bar = smem_u32(&S.mbar);
+    const u32 tile = blockIdx.x;
+    const u64 base = (u64)tile * kSortTile;
+    const u32 count = (u32)min((u64)kSortTile, (u64)n - base);
+    const u32 nbulk = count & ~3u;  // 16-byte multiples
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (nbulk) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nbulk * 8u) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(smem_u32(S.keys)), "l"(kin + base), "r"(nbulk * 4u), "r"(bar) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(smem_u32(S.vals)), "l"(vin + base), "r"(nbulk * 4u), "r"(bar) : "memory");
+        } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+        }
+    }
+    for (int j = tid; j < kSortWarps * 256; j += kSortThreads) (&S.whist[0][0])[j] = 0;
+    // the block's digit starts: global start of (digit, tile) from the scanned counts
+    for (int d = tid; d < RADIX; d += kSortThreads) S.gbase[d] = __ldg(offs + (u64)d * T + tile);
+    for (u32 j = nbulk + tid; j < (u32)kSortTile; j += kSortThreads) {
+        const bool ok = j < count;
+        S.keys[j] = ok ? kin[base + j] : 0xFFFFFFFFu;  // pads rank last
+        S.vals[j] = ok ? vin[base + j] : 0u;
+    }
+    __syncthreads();  // barrier init visible before anyone waits on it
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra WAIT%=;\n\t}" ::"r"(bar) : "memory");
+    __syncthreads();
+    rank_and_store<DBITS, MODE>(S, n, shift, kout, vout, depths, keys64, rc_by_id, rc_out);
+}
+
+// ------------------------------------------------------------------------------------------
+// 4. key generation fused with the first tile pass.  Block b owns the key slots
+// [4096 b, 4096 b + 4096) of the depth-ordered key sequence (slot0[r] + k, rows outer) and expands
+// exactly those keys from the rect codes: the Gaussians covering the range are r0 = first[b] ..
+// first[b+1] (first[] is written by the depth-order scan), taken in groups of 32 per warp and
+// expanded warp-cooperatively (each lane finds its key's Gaussian by a 5-step search over the
+// group's inclusive counts).  keys_count_kernel only histograms the first tile digit;
+// keys_scatter_kernel re-expands the block (cheaper than writing and re-reading M keys) and ranks
+// and stores it like any radix pass.
+struct ExpandSrc {
+    const u64* rc;      // [V] rect codes, depth order
+    const u32* slot0;   // [V] first slot of each Gaussian's keys
+    const u32* sid;     // [V] Gaussian ids, depth order
+    const u32* first;   // [blocks + 1] Gaussian holding slot 4096 b
+    u32 V, M;
+    int TX;
+};
+
+// floor(k / w) for 0 <= k < 2^21, 1 <= w < 2^16: (k + 0.5) / w is at least 0.5 / w from an integer,
+// far above the error of two correctly rounded fp32 operations
+__device__ __forceinline__ int div_floor(int k, int w) {
+    return (int)(((float)k + 0.5f) * __frcp_rn((float)w));
+}
+
+// f(slot, tile, id) for every key slot in [c0, c1) (c1 - c0 <= 512, all inside block b), one
+// slot per lane per round of 32.  The Gaussian owning slot s is the last one with slot0 <= s:
+// a 32-ary search finds the owner of c0; afterwards each round marks, in one OR-reduced word,
+// the slots of the window where one of the next 32 Gaussians starts, and a lane's owner is the
+// current one plus the number of starts at or before its slot.
+template <class F>
+__device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0, u32 c1, F&& f) {
+    const int lane = threadIdx.x & 31;
+    // owner of c0 within [first[b], first[b + 1]]
+    u32 lo = __ldg(src.first + b), hi = __ldg(src.first + b + 1);
+    while (lo < hi) {
+        const u32 step = (hi - lo + 32) / 32;  // probes lo, lo + step, ... cover [lo, hi]
+        const u32 p = lo + (u32)lane * step;
+        const bool le = p <= hi && __ldg(src.slot0 + p) <= c0;
+        const int L = 31 - __clz(__ballot_sync(VKS_FULL_MASK, le));  // lane 0 always true
+        const u32 nlo = lo + (u32)L * step;
+        hi = min(hi, nlo + step - 1);
+        lo = nlo;
+        if (step == 1) break;
+    }
+    u32 cur = lo;
+    u32 a_cur = __ldg(src.slot0 + cur);
+    u64 rc_cur = __ldg(src.rc + cur);
+    u32 id_cur = __ldg(src.sid + cur);
+    const u32 le_mask = 0xFFFFFFFFu >> (31 - lane);  // bits 0..lane
+    for (u32 W = c0; W < c1; W += 32) {
+        const u32 g = cur + 1 + (u32)lane;
+        const bool in = g < src.V;
+        const u32 aj = in ? __ldg(src.slot0 + g) : 0xFFFFFFFFu;
+        const u64 rcj = in ? __ldg(src.rc + g) : 0ull;
+        const u32 idj = in ? __ldg(src.sid + g) : 0u;
+        const u32 d = aj - W;  // >= 0: Gaussian cur owns W
+        const u32 starts = __reduce_or_sync(VKS_FULL_MASK, d < 32u ? (1u << d) : 0u);
+        const int rel = __popc(starts & le_mask);
+        const int srcl = rel > 0 ? rel - 1 : 0;
+        u32 a_o = __shfl_sync(VKS_FULL_MASK, aj, srcl);
+        u64 rc_o = __shfl_sync(VKS_FULL_MASK, rcj, srcl);
+        u32 id_o = __shfl_sync(VKS_FULL_MASK, idj, srcl);
+        if (rel == 0) { a_o = a_cur; rc_o = rc_cur; id_o = id_cur; }
+        const u32 slot = W + (u32)lane;
+        if (slot < c1) {
+            int x0, x1, y0, y1;
+            unpack_rect(rc_o, x0, x1, y0, y1);
+            const int w = x1 - x0;
+            const int k = (int)(slot - a_o);  // index within the rect, rows outer
+            const int ry = div_floor(k, w);
+            f(slot, (u32)((y0 + ry) * src.TX + x0 + (k - ry * w)), id_o);
+        }
+        const int n = __popc(starts);  // the owner of the window's last slot is cur + n
+        if (n > 0) {
+            a_cur = __shfl_sync(VKS_FULL_MASK, aj, n - 1);
+            rc_cur = __shfl_sync(VKS_FULL_MASK, rcj, n - 1);
+            id_cur = __shfl_sync(VKS_FULL_MASK, idj, n - 1);
+            cur += (u32)n;
+        }
+    }
+}
+
+
+// Digit histogram of the block's keys without enumerating them: a Gaussian's keys within one
+// rect row are consecutive tile ids, so a row of length L adds floor(L / R) to every digit and 1
+// to a cyclic run of L mod R digits (a difference array over the R digits).
+template <int DBITS>
+__global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSrc src, int shift, u32 T,
+                                                                 u32* __restrict__ counts) {
+    constexpr int RADIX = 1 << DBITS;
+    constexpr int DMASK = RADIX - 1;
+    __shared__ int wdiff[kSortWarps][RADIX + 1];  // per warp: contention only within a warp
+    __shared__ int s_all[kSortWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    (void)shift;  // the key pass sorts the lowest tile bits (shift 0)
+    for (int j = tid; j < kSortWarps * (RADIX + 1); j += kSortThreads) (&wdiff[0][0])[j] = 0;
+    __syncthreads();
+    int* sdiff = wdiff[warp];
+    const u32 b = blockIdx.x;
+    const u32 S = b * (u32)kSortTile;
+    const u32 E = min(S + (u32)kSortTile, src.M);
+    const u32 r0 = __ldg(src.first + b), r1 = __ldg(src.first + b + 1);
+    int all = 0;
+    for (u32 r = r0 + tid; r <= r1; r += kSortThreads) {
+        int x0, x1, y0, y1;
+        unpack_rect(__ldg(src.rc + r), x0, x1, y0, y1);
+        const int w = x1 - x0;
+        const u32 a = __ldg(src.slot0 + r);
+        const u32 c = (u32)(w * (y1 - y0));
+        const u32 l = max(a, S), h = min(a + c, E);
+        if (h <= l) continue;
+        const int k0 = (int)(l - a), k1 = (int)(h - a) - 1;  // key indices within the rect
+        const int ry0 = div_floor(k0, w), ry1 = div_floor(k1, w);
+        for (int ry = ry0; ry <= ry1; ry++) {
+            const int xs = ry == ry0 ? k0 - ry * w : 0;
+            const int xe = ry == ry1 ? k1 - ry * w + 1 : w;
+            const int len = xe - xs;
+            const int t0 = (y0 + ry) * src.TX + x0 + xs;
+            all += len >> DBITS;
+            const int rem = len & DMASK, b0 = t0 & DMASK;
+            if (rem) {
+                atomicAdd(&sdiff[b0], 1);
+                if (b0 + rem <= RADIX) {
+                    atomicAdd(&sdiff[b0 + rem], -1);
+                } else {
+                    atomicAdd(&sdiff[0], 1);
+                    atomicAdd(&sdiff[b0 + rem - RADIX], -1);
                 }
-                rc_out[dest] = code;
             }
         }
     }
+    all = __reduce_add_sync(VKS_FULL_MASK, all);
+    if (lane == 0) s_all[warp] = all;
+    __syncthreads();
+    if (tid < 32) {  // prefix of the difference array; RADIX <= 256 = 8 chunks of 32
+        int tot = 0;
+#pragma unroll
+        for (int w = 0; w < kSortWarps; w++) tot += s_all[w];
+        int carry = 0;
+        for (int d0 = 0; d0 < RADIX; d0 += 32) {
+            const int d = d0 + lane;
+            int v = 0;
+            if (d < RADIX) {
+#pragma unroll
+                for (int w = 0; w < kSortWarps; w++) v += wdiff[w][d];
+            }
+            const int incl = (int)warp_incl_scan((u32)v, lane) + carry;
+            if (d < RADIX) counts[(u64)d * T + b] = (u32)(incl + tot);
+            carry = __shfl_sync(VKS_FULL_MASK, incl, 31);
+        }
+    }
+}
+
+template <int DBITS, int MODE>
+__global__ void __launch_bounds__(kSortThreads) keys_scatter_kernel(const ExpandSrc src, int shift, u32 T,
+                                                                   const u32* __restrict__ offs, u32* __restrict__ kout,
+                                                                   u32* __restrict__ vout, const float* __restrict__ depths,
+                                                                   u64* __restrict__ keys64) {
+    constexpr int RADIX = 1 << DBITS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const u32 b = blockIdx.x;
+    const u32 count = min((u32)kSortTile, src.M - b * (u32)kSortTile);
+    for (int j = tid; j < kSortWarps * 256; j += kSortThreads) (&S.whist[0][0])[j] = 0;
+    for (int d = tid; d < RADIX; d += kSortThreads) S.gbase[d] = __ldg(offs + (u64)d * T + b);
+    for (u32 j = count + tid; j < (u32)kSortTile; j += kSortThreads) {
+        S.keys[j] = 0xFFFFFFFFu;  // pads rank last
+        S.vals[j] = 0u;
+    }
+    const u32 S0 = b * (u32)kSortTile;
+    const u32 c0 = S0 + (u32)warp * 32 * kSortItems;  // the warp expands the slots it ranks
+    const u32 c1 = min(c0 + 32u * kSortItems, src.M);
+    if (c0 < c1)
+        expand_chunk(src, b, c0, c1, [&](u32 slot, u32 tile, u32 id) {
+            S.keys[slot - S0] = tile;
+            S.vals[slot - S0] = id;
+        });
+    __syncthreads();
+    rank_and_store<DBITS, MODE>(S, src.M, shift, kout, vout, depths, keys64, nullptr, nullptr);
 }
 
 struct PassBufs {
@@ -738,7 +992,7 @@ struct PassBufs {
 
 template <int DBITS, int MODE>
 int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift, const PassBufs& pb,
-                const float* depths, u64* keys64, cudaStream_t s, RectSrc rsrc = RectSrc{}, u64* rc_out = nullptr) {
+                const float* depths, u64* keys64, cudaStream_t s, const u64* rc_by_id = nullptr, u64* rc_out = nullptr) {
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(scatter_kernel<DBITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -755,7 +1009,7 @@ int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int
     scan_u32_kernel<<<(unsigned)((cnt + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt,
                                                                                            pb.lb, pb.ctr);
     scatter_kernel<DBITS, MODE><<<T, kSortThreads, sizeof(SortSmem), s>>>(kin, vin, kout, vout, n, shift, T, pb.offs,
-                                                                         depths, keys64, rsrc, rc_out);
+                                                                         depths, keys64, rc_by_id, rc_out);
     return check_launch(__func__);
 }
 
@@ -774,13 +1028,6 @@ int launch_tile_pass(int dbits, const u32* kin, const u32* vin, u32* kout, u32* 
     }
 }
 
-// Single-tile grid: the depth order is the final order; u64 keys = (0 << 32) | depth bits.
-__global__ void keys64_tile0_kernel(const u32* __restrict__ vals, const float* __restrict__ depths, u64* __restrict__ keys,
-                                    u32 m) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < m) keys[i] = (u64)__float_as_uint(__ldg(depths + vals[i]));
-}
-
 int sm_count() {
     static int sms = 0;
     if (!sms) {
@@ -792,44 +1039,107 @@ int sm_count() {
     return sms;
 }
 
+// first tile pass straight from the rect codes: count, scan, expand + scatter
+template <int DBITS, int MODE>
+int launch_keys_pass(const ExpandSrc& src, u32* kout, u32* vout, const PassBufs& pb, const float* depths, u64* keys64,
+                     cudaStream_t s) {
+    const size_t sm = sizeof(SortSmem);
+    static bool attr = false;
+    if (!attr) {
+        if (cudaError_t e = cudaFuncSetAttribute(keys_scatter_kernel<DBITS, MODE>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))
+            return cuda_fail(e, "keys_scatter smem attribute");
+        attr = true;
+    }
+    const u32 T = (src.M + kSortTile - 1) / kSortTile;
+    if (!T) return VKS_OK;
+    keys_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(src, 0, T, pb.counts);
+    const u64 cnt = (u64)(1u << DBITS) * T;
+    scan_u32_kernel<<<(unsigned)((cnt + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt,
+                                                                                           pb.lb, pb.ctr);
+    keys_scatter_kernel<DBITS, MODE><<<T, kSortThreads, sm, s>>>(src, 0, T, pb.offs, kout, vout, depths, keys64);
+    return check_launch(__func__);
+}
+
 template <int MODE>
-int launch_keys(const vks_camera& cam, int64_t count, const u32* sid, const u64* rc, const int* tiles,
-                const float* means2d, const int32_t* radii, const float* depths, const u32* slot0, u32* tkeys,
-                u32* tvals, u64* keys64, int* diff, cudaStream_t s) {
-    const float2* m2 = reinterpret_cast<const float2*>(means2d);
-    const int2* r2 = reinterpret_cast<const int2*>(radii);
-    const int TX = tiles_x(cam), TY = tiles_y(cam);
+int launch_keys_pass_bits(int dbits, const ExpandSrc& src, u32* kout, u32* vout, const PassBufs& pb,
+                          const float* depths, u64* keys64, cudaStream_t s) {
+    switch (dbits) {
+        case 1: return launch_keys_pass<1, MODE>(src, kout, vout, pb, depths, keys64, s);
+        case 2: return launch_keys_pass<2, MODE>(src, kout, vout, pb, depths, keys64, s);
+        case 3: return launch_keys_pass<3, MODE>(src, kout, vout, pb, depths, keys64, s);
+        case 4: return launch_keys_pass<4, MODE>(src, kout, vout, pb, depths, keys64, s);
+        case 5: return launch_keys_pass<5, MODE>(src, kout, vout, pb, depths, keys64, s);
+        case 6: return launch_keys_pass<6, MODE>(src, kout, vout, pb, depths, keys64, s);
+        case 7: return launch_keys_pass<7, MODE>(src, kout, vout, pb, depths, keys64, s);
+        default: return launch_keys_pass<8, MODE>(src, kout, vout, pb, depths, keys64, s);
+    }
+}
+
+int launch_rect_diff(int TX, int TY, u32 count, const u64* rc, int* diff, cudaStream_t s) {
     const int cells = (TX + 1) * (TY + 1);
-    const int64_t want = (count + kKeysThreads - 1) / kKeysThreads;
+    const u32 want = (count + kDiffThreads - 1) / kDiffThreads;
     if (want == 0) return VKS_OK;
-    if (MODE == 0 && cells <= kKeysSmemDiffMax) {
+    if (cells <= kDiffSmemMax) {
         const size_t sm = sizeof(int) * (size_t)cells;
-        if (sm > 32 * 1024 &&
-            cudaFuncSetAttribute(keys_kernel<true, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
-            return VKS_ERR_CUDA;
-        const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 2);
-        keys_kernel<true, MODE><<<blocks, kKeysThreads, sm, s>>>(cam, count, sid, rc, tiles, m2, r2, depths, slot0,
-                                                                 tkeys, tvals, keys64, diff);
+        if (sm > 48 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                if (cudaError_t e = cudaFuncSetAttribute(rect_diff_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)(sizeof(int) * kDiffSmemMax)))
+                    return cuda_fail(e, "rect_diff smem attribute");
+                attr = true;
+            }
+        }
+        const unsigned blocks = std::min<u32>(want, (u32)sm_count());
+        rect_diff_kernel<true><<<blocks, kDiffThreads, sm, s>>>(TX, TY, count, rc, diff);
     } else {
-        const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 4);
-        keys_kernel<false, MODE><<<blocks, kKeysThreads, 0, s>>>(cam, count, sid, rc, tiles, m2, r2, depths, slot0,
-                                                                 tkeys, tvals, keys64, diff);
+        const unsigned blocks = std::min<u32>(want, (u32)sm_count() * 4);
+        rect_diff_kernel<false><<<blocks, kDiffThreads, 0, s>>>(TX, TY, count, rc, diff);
     }
     return check_launch(__func__);
 }
 
-// reduce-then-scan of the tiles counts (MODE 0: id order from tiles_touched, writes rect codes;
-// MODE 1: depth order from the sorted rect codes); totals[0] = sum (and totals[1] = #visible)
+int launch_tile_count(int TX, int TY, int* diff, u32* tile_offsets, cudaStream_t s) {
+    const size_t cells_bytes = sizeof(int) * (size_t)(TX + 1) * (TY + 1);
+    if (cells_bytes <= kTileCountSmemMax) {
+        if (cells_bytes > 48 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                if (cudaError_t e = cudaFuncSetAttribute(tile_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)kTileCountSmemMax))
+                    return cuda_fail(e, "tile_count smem attribute");
+                attr = true;
+            }
+        }
+        tile_count_kernel<true><<<1, 1024, cells_bytes, s>>>(TX, TY, diff, tile_offsets);
+    } else {
+        tile_count_kernel<false><<<1, 1024, 0, s>>>(TX, TY, diff, tile_offsets);
+    }
+    return check_launch(__func__);
+}
+
+int launch_keys_debug(const vks_camera& cam, int64_t n, const int* tiles, const float* means2d, const int32_t* radii,
+                      const float* depths, const u32* offsets, u32* vals, u64* keys64, cudaStream_t s) {
+    const int64_t want = (n + kKeysThreads - 1) / kKeysThreads;
+    if (want == 0) return VKS_OK;
+    const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 8);
+    keys_debug_kernel<<<blocks, kKeysThreads, 0, s>>>(cam, n, tiles, reinterpret_cast<const float2*>(means2d),
+                                                      reinterpret_cast<const int2*>(radii), depths, offsets, vals, keys64);
+    return check_launch(__func__);
+}
+
+// reduce-then-scan of the tile counts (MODE 0: id order from tiles_touched; MODE 1: depth order
+// from the sorted rect codes); totals[0] = sum (and, MODE 0, totals[1] = #visible)
 template <int MODE>
-int run_scan(const vks_camera& cam, const int* tiles, const float* means2d, const int32_t* radii, const u64* rc_in,
-             u64* rc_out, u64 count, u32* part_sum, u32* part_vis, u32* out, u64* totals, cudaStream_t s) {
+int run_scan(const int* tiles, const u64* rc_in, u64 count, u32* part_sum, u32* part_vis, u32* out, u64* totals,
+             CompactOut co, cudaStream_t s) {
     const u32 P = (u32)((count + kScanTile - 1) / kScanTile);
     if (!P) return VKS_OK;
-    scan_reduce_kernel<MODE><<<P, kScanThreads, 0, s>>>(cam, tiles, reinterpret_cast<const float2*>(means2d),
-                                                       reinterpret_cast<const int2*>(radii), rc_in, rc_out, count,
-                                                       part_sum, part_vis);
+    scan_reduce_kernel<MODE><<<P, kScanThreads, 0, s>>>(tiles, rc_in, count, part_sum, MODE == 0 ? part_vis : nullptr);
     scan_partials_kernel<<<1, 1024, 0, s>>>(part_sum, MODE == 0 ? part_vis : nullptr, P, totals);
-    scan_down_kernel<MODE><<<P, kScanThreads, 0, s>>>(tiles, rc_in, count, part_sum, out);
+    co.vis_prefix = part_vis;
+    scan_down_kernel<MODE><<<P, kScanThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co);
     return check_launch(__func__);
 }
 
@@ -848,6 +1158,9 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
                  void* workspace, size_t workspace_bytes, cudaStream_t s) {
     const int TX = tiles_x(cam), TY = tiles_y(cam);
     const int32_t n_tiles = TX * TY;
+    // rect codes hold 16-bit tile coordinates; the key expansion's exact float division needs
+    // rect areas < 2^21 tiles
+    if (TX > 65535 || TY > 65535 || (int64_t)TX * TY >= (1 << 21)) return VKS_ERR_INVALID_ARG;
     if (workspace_bytes < bin_sort_workspace_bytes(n, capacity, n_tiles)) return VKS_ERR_WORKSPACE;
     Workspace w = carve(workspace, n, capacity, TX, TY);
     if (cudaError_t e_ = cudaMemsetAsync(w.zeroA, 0, w.zeroA_bytes, s)) return cuda_fail(e_, "memset workspace");
@@ -855,8 +1168,9 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     // 1. index offsets in id order, M, V, rect codes
     u64 tot[2] = {0, 0};
     if (n > 0) {
-        int st = run_scan<0>(cam, tiles_touched, means2d, radii, nullptr, nullptr, (u64)n, w.part_sum, w.part_vis,
-                             offsets, w.totals, s);
+        const CompactOut co{nullptr, reinterpret_cast<const u32*>(depths), reinterpret_cast<const float2*>(means2d),
+                            reinterpret_cast<const int2*>(radii), TX, TY, w.dk[1], w.dv[1], w.rc_by_id};
+        int st = run_scan<0>(tiles_touched, nullptr, (u64)n, w.part_sum, w.part_vis, offsets, w.totals, co, s);
         if (st) return st;
         if (cudaError_t e_ = cudaMemcpyAsync(tot, w.totals, sizeof(tot), cudaMemcpyDeviceToHost, s)) return cuda_fail(e_, "read M");
         if (cudaError_t e_ = cudaStreamSynchronize(s)) return cuda_fail(e_, "bin_sort sync");
@@ -873,57 +1187,50 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     if (keys_unsorted || vals_unsorted) {
         u32* vtmp = vals_unsorted ? vals_unsorted : w.tv[1];
         u64* ktmp = keys_unsorted ? reinterpret_cast<u64*>(keys_unsorted) : reinterpret_cast<u64*>(w.tk[0]);
-        int st = launch_keys<1>(cam, n, nullptr, nullptr, tiles_touched, means2d, radii, depths, offsets, nullptr, vtmp,
-                                ktmp, w.diff, s);
+        int st = launch_keys_debug(cam, n, tiles_touched, means2d, radii, depths, offsets, vtmp, ktmp, s);
         if (st) return st;
     }
-    // 2. depth sort of all n (culled Gaussians key 0xFFFFFFFF, last); pass 0 reads (tiles, depths),
+    // 2. depth sort of the V visible Gaussians (compacted in id order into dk[1]/dv[1] by the scan);
     //    the last pass also lays out the rect codes in depth order
-    int st = launch_pass<8, kPassDepthFirst>(reinterpret_cast<const u32*>(tiles_touched),
-                                             reinterpret_cast<const u32*>(depths), w.dk[0], w.dv[0], (u32)n, 0,
-                                             pass_bufs(0), nullptr, nullptr, s);
-    if (st) return st;
-    for (int p = 1; p < kDepthPasses; p++) {
+    int st = VKS_OK;
+    for (int p = 0; p < kDepthPasses; p++) {
         const u32* ki = w.dk[(p + 1) & 1];
         const u32* vi = w.dv[(p + 1) & 1];
         if (p == kDepthPasses - 1)
-            st = launch_pass<8, kPassDepthLast>(ki, vi, w.dk[p & 1], w.dv[p & 1], (u32)n, 8 * p, pass_bufs(p), nullptr,
-                                                nullptr, s,
-                                                RectSrc{reinterpret_cast<const float2*>(means2d),
-                                                        reinterpret_cast<const int2*>(radii), TX, TY, (u32)V},
-                                                w.rcs);
+            st = launch_pass<8, kPassDepthLast>(ki, vi, w.dk[p & 1], w.dv[p & 1], (u32)V, 8 * p, pass_bufs(p), nullptr,
+                                                nullptr, s, w.rc_by_id, w.rcs);
         else
-            st = launch_pass<8, kPassPlain>(ki, vi, w.dk[p & 1], w.dv[p & 1], (u32)n, 8 * p, pass_bufs(p), nullptr,
+            st = launch_pass<8, kPassPlain>(ki, vi, w.dk[p & 1], w.dv[p & 1], (u32)V, 8 * p, pass_bufs(p), nullptr,
                                             nullptr, s);
         if (st) return st;
     }
-    const u32* sid = w.dv[(kDepthPasses - 1) & 1];  // ids in (depth, id) order; the first V are visible
-    // 3. slots in depth order (from the depth-ordered rect codes)
-    st = run_scan<1>(cam, nullptr, nullptr, nullptr, w.rcs, nullptr, V, w.part_sum, nullptr, w.doff, w.totals + 0, s);
+    const u32* sid = w.dv[(kDepthPasses - 1) & 1];  // visible ids in (depth, id) order
+    // 3. slots in depth order (from the depth-ordered rect codes) + the first Gaussian of every
+    //    4096-slot key block
+    CompactOut co{};
+    co.first = w.first;
+    st = run_scan<1>(nullptr, w.rcs, V, w.part_sum, nullptr, w.doff, w.totals + 0, co, s);
     if (st) return st;
-    // 4. (tile, id) pairs in depth order + tile-rect difference array
-    const TilePlan plan = tile_plan(n_tiles);
-    u32* pv0 = plan.passes == 0 ? vals : w.tv[0];
-    st = launch_keys<0>(cam, (int64_t)V, sid, w.rcs, tiles_touched, means2d, radii, depths, w.doff, w.tk[0], pv0,
-                        nullptr, w.diff, s);
+    // 4. tile ranges from the 2-D difference array of the rects
+    if ((st = launch_rect_diff(TX, TY, (u32)V, w.rcs, w.diff, s))) return st;
+    if ((st = launch_tile_count(TX, TY, w.diff, tile_offsets, s))) return st;
+    // 5. stable tile passes over the M (tile, id) pairs; the first expands the keys from the rect
+    //    codes itself, the last writes the caller's vals (+ u64 keys on request)
+    TilePlan plan = tile_plan(n_tiles);
+    if (plan.passes == 0) plan = TilePlan{1, 1};  // one tile: a trivial 1-bit pass keeps the path uniform
+    const ExpandSrc src{w.rcs, w.doff, sid, w.first, (u32)V, (u32)M, TX};
+    if (plan.passes == 1)
+        return launch_keys_pass_bits<kPassTileLast>(plan.dbits, src, nullptr, vals, pass_bufs(kDepthPasses), depths,
+                                                    keys64, s);
+    st = launch_keys_pass_bits<kPassPlain>(plan.dbits, src, w.tk[0], w.tv[0], pass_bufs(kDepthPasses), nullptr, nullptr,
+                                           s);
     if (st) return st;
-    // 5. tile counts -> tile ranges
-    tile_count_kernel<<<1, 1024, 0, s>>>(TX, TY, w.diff, tile_offsets);
-    if (int e_ = check_launch(__func__)) return e_;
-    // 6. stable tile passes; the last writes the caller's vals (+ u64 keys on request)
-    if (plan.passes == 0) {
-        if (keys64) {
-            keys64_tile0_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(vals, depths, keys64, (u32)M);
-            if (int e_ = check_launch(__func__)) return e_;
-        }
-        return VKS_OK;
-    }
-    for (int p = 0; p < plan.passes; p++) {
-        const u32* kin = w.tk[p & 1];
-        const u32* vin = w.tv[p & 1];
+    for (int p = 1; p < plan.passes; p++) {
+        const u32* kin = w.tk[(p - 1) & 1];
+        const u32* vin = w.tv[(p - 1) & 1];
         const bool last = p == plan.passes - 1;
-        u32* ko = w.tk[(p + 1) & 1];
-        u32* vo = last ? vals : w.tv[(p + 1) & 1];
+        u32* ko = w.tk[p & 1];
+        u32* vo = last ? vals : w.tv[p & 1];
         st = last ? launch_tile_pass<kPassTileLast>(plan.dbits, kin, vin, ko, vo, (u32)M, plan.dbits * p,
                                                     pass_bufs(kDepthPasses + p), depths, keys64, s)
                   : launch_tile_pass<kPassPlain>(plan.dbits, kin, vin, ko, vo, (u32)M, plan.dbits * p,

@@ -289,33 +289,35 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
         const float tz = dot3(p.cam.R + 6, mu) + p.cam.t[2];
         near_ok = tz > p.cfg.near_plane;
     }
-    // start the SH rows of every Gaussian in front of the camera streaming into shared memory now;
-    // they land while the projection below runs (rows of culled Gaussians are never read)
-    const unsigned nmask = __ballot_sync(VKS_FULL_MASK, near_ok);
-    float* buf = nullptr;
-    if constexpr (KS > 0) {
-        buf = smem + warp * ShLayout<KS>::kWarpFloats;
-        if (nmask) sh_stage_async<KS>(p.sh, g0, nmask, buf);
-        cp_async_commit();
-    }
     bool vis = near_ok && project_core(p.cam, p.cfg, mu, ls, q, o, k) &&
                footprint_rect(k, p.cfg, TX, TY, rxf, ryf, x0, x1, y0, y1);
-    // colour (survivors only)
+    // SH rows only of the Gaussians that touch a tile (in front of the camera but outside the
+    // view is ~1/3 of the near-plane survivors on the ring views: their rows are never read)
     const int K = (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);
     float col[3] = {0, 0, 0};
     const unsigned vmask = __ballot_sync(VKS_FULL_MASK, vis);
+    float* buf = nullptr;
     if constexpr (KS > 0) {
-        cp_async_wait_all();
+        buf = smem + warp * ShLayout<KS>::kWarpFloats;
+        if (vmask) {
+            sh_stage_async<KS>(p.sh, g0, vmask, buf);
+            cp_async_commit();
+        }
+    }
+    float Y[16];
+    if (vis) {  // the SH basis of the view direction while the rows are in flight
+        float dh[3], dl;
+        view_dir(p.cam, mu, dh, dl);
+        sh_basis(dh[0], dh[1], dh[2], K, Y);
+    }
+    if constexpr (KS > 0) {
+        if (vmask) cp_async_wait_all();
         __syncwarp();
     }
     if (vmask && vis) {
         const float* f;
         if constexpr (KS > 0) f = buf + lane * ShLayout<KS>::SP;
         else f = p.sh + 3 * (int64_t)p.cfg.sh_coeffs * i;
-        float dh[3], dl;
-        view_dir(p.cam, mu, dh, dl);
-        float Y[16];
-        sh_basis(dh[0], dh[1], dh[2], K, Y);
         bool ok = true;
 #pragma unroll
         for (int ch = 0; ch < 3; ch++) {

@@ -1,19 +1,22 @@
 // raster.cu — "Rasterization Forward" and "Rasterization Backward";
 // DESIGN.md §4.3-4.4 and §6.
 //
-// One 256-thread block per 16x16 tile; each warp owns an 8x4 pixel patch and walks the tile's
-// sorted list on its own in batches of 32 staged into its shared-memory slice as packed float4
-// records (software-pipelined: ids two batches ahead, records one batch ahead), so there are no
-// block barriers and a warp stops as soon as its own 32 pixels are saturated.  Before evaluating a Gaussian a warp
-// tests its 8x4 patch against the Gaussian's support box (support footprint only; the box is the
-// projection's radii plus a safety margin, so no pixel whose alpha could reach 1/255 is skipped)
-// and skips it warp-uniformly, which removes most of the evaluations that would be rejected by
-// the 1/255 test anyway.  Forward and backward evaluate sigma / alpha through the SAME inline
-// function, so skip / clamp / stop decisions replay identically; sigma, alpha and the colour
-// accumulation follow the pinned fp32 order of DESIGN.md §4.3 (only exp differs from the oracle:
-// ex2.approx here, expf there).  The backward reduces each Gaussian's 9 gradient terms across the
-// warp with a transposed butterfly (14 shuffles instead of 45) and issues 2 atomic instructions per
-// (warp, Gaussian) that any lane touched.
+// One block per 16x16 tile; each warp owns an 8 x 4*PPT pixel patch (PPT = 2 by default: 8x8,
+// two pixels per thread) and walks the tile's sorted list on its own in batches of 32 staged
+// into its shared-memory slice as packed float4 records (software-pipelined: ids two batches
+// ahead, records one batch ahead), so there are no block barriers and a warp stops as soon as
+// its own pixels are saturated.  Before a batch is visited each lane tests its entry against the
+// patch with an exact test (the minimum of sigma over the patch rectangle against ln(255 rho));
+// the warp visits only entries that can composite somewhere in the patch (a finer per-8x4-band
+// test removed 20% of the evaluations but cost more instructions than it saved).  Forward and
+// backward evaluate
+// sigma / alpha through the SAME inline function, so skip / clamp / stop decisions replay
+// identically; sigma, alpha and the colour accumulation follow the pinned fp32 order of
+// DESIGN.md §4.3 (only exp differs from the oracle: ex2.approx here, expf there).  The backward
+// accumulates per (warp, Gaussian) the colour terms, sum(g) and the moments sum(g dx), sum(g dy),
+// sum(g dx^2), sum(g dx dy), sum(g dy^2) (g = G dalpha), reduces the 9 sums across the warp with
+// a transposed butterfly (14 shuffles instead of 45), turns the moments into the mean / conic
+// gradients with the Gaussian's conic, and issues one atomic per term from 9 lanes.
 #include <stdlib.h>
 
 #include "vks_common.cuh"
@@ -119,11 +122,10 @@ __device__ __forceinline__ bool eval_alpha(const float4 A, const float4 B, float
     dx = A.x - px;
     dy = A.y - py;
     const float sigma = fmaf(A.z * dx, dx, fmaf(B.x * dy, dy, (A.w * dx) * dy));
-    if (sigma < 0.0f) return false;
-    G = exp2_ftz(sigma * -1.44269504088896341f);
+    G = exp2_ftz(sigma * -1.44269504088896341f);  // evaluated unconditionally: no branch
     rG = B.y * G;
     alpha = fminf(0.99f, rG);
-    return !(alpha < 1.0f / 255.0f);
+    return !(sigma < 0.0f) && !(alpha < 1.0f / 255.0f);
 }
 
 // Warp patch: 8 pixels wide x 4*PPT tall; lane (lx, ly) = (lane & 7, lane >> 3) owns the PPT
@@ -198,8 +200,8 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
         for (int k = 0; k < PPT; k++) all_done = all_done && done[k];
         if (__all_sync(VKS_FULL_MASK, all_done)) break;
         __syncwarp();
-        // each lane tests its own entry against the warp patch; the warp then visits only the
-        // entries whose support box meets the patch, in list order
+        // each lane tests its own entry against the warp patch; the warp then visits, in list
+        // order, only the entries that can composite somewhere in the patch
         unsigned live = __ballot_sync(VKS_FULL_MASK, b + lane < end &&
                                                          !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
         if (b + lane < end) store_entry(s, lane, e_next);
@@ -319,7 +321,9 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
-    float py[PPT], T[PPT], w0[PPT], w1[PPT], w2[PPT], S0[PPT], S1[PPT], S2[PPT];
+    // per pixel: P = <S, w> where S is the colour composited behind the current entry (bg first):
+    // dalpha only needs <c - S, w>, and <S, w> updates as P <- alpha <c, w> + (1 - alpha) P
+    float py[PPT], T[PPT], w0[PPT], w1[PPT], w2[PPT], P[PPT];
     int last[PPT];
     int lmax = 0;
 #pragma unroll
@@ -328,7 +332,6 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
         py[k] = (float)y + 0.5f;
         T[k] = 1.0f; w0[k] = w1[k] = w2[k] = 0.0f;
         last[k] = 0;
-        S0[k] = cfg.bg[0]; S1[k] = cfg.bg[1]; S2[k] = cfg.bg[2];
         if (pm.x < cam.width && y < cam.height) {
             const size_t pix = (size_t)y * cam.width + pm.x;
             T[k] = T_final[pix];
@@ -337,6 +340,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             w1[k] = dL_dimage[3 * pix + 1];
             w2[k] = dL_dimage[3 * pix + 2];
         }
+        P[k] = cfg.bg[0] * w0[k] + cfg.bg[1] * w1[k] + cfg.bg[2] * w2[k];
         lmax = max(lmax, last[k]);
     }
     const int wmax = __reduce_max_sync(VKS_FULL_MASK, lmax);  // positions >= wmax: nobody composited
@@ -345,6 +349,12 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     const int myterm = (lane & 3) == 0 ? (int)(lane >> 2) : (lane == 1 ? 8 : -1);
     float* tbase = nullptr;
     int tstride = 0;
+    // term selectors for the epilogue: term 0 -> a, term 1 -> c, both -> b (other moment),
+    // conic terms 2/3/4 -> 1/2, 1, 1/2, colour terms -> 1
+    const float kA = myterm == 0 ? 1.0f : 0.0f, kC = myterm == 1 ? 1.0f : 0.0f;
+    const float kB = myterm == 0 || myterm == 1 ? 1.0f : 0.0f;
+    const float kH = myterm == 3 ? 1.0f : (myterm == 2 || myterm == 4 ? 0.5f : 0.0f);
+    const float kOne = myterm >= 5 && myterm < 8 ? 1.0f : 0.0f;
     if (myterm >= 0 && myterm < 2) { tbase = dmeans2d + myterm; tstride = 2; }
     else if (myterm >= 2 && myterm < 5) { tbase = dconics + (myterm - 2); tstride = 3; }
     else if (myterm >= 5 && myterm < 8) { tbase = dcolors + (myterm - 5); tstride = 3; }
@@ -378,6 +388,8 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             const int pos = bs + j;
             const float4 A = s.a[j], B = s.b[j];
             const float c0 = B.z, c1 = B.w, c2 = s.c2[j];
+            // v[0..4]: moments sum(g dx), sum(g dy), sum(g dx^2), sum(g dx dy), sum(g dy^2) with
+            // g = G dalpha (dL/dsigma = -rho g); v[5..7]: colour; e = sum(g) (dL/drho)
             float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             float e = 0.0f;
             bool contrib = false;
@@ -387,29 +399,33 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 float dx, dy, G, rG, alpha;
                 if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
                 contrib = true;
-                T[k] = __fdividef(T[k], 1.0f - alpha);
+                const float om = 1.0f - alpha;
+                T[k] = __fdividef(T[k], om);
                 const float aT = alpha * T[k];
                 v[5] += aT * w0[k];
                 v[6] += aT * w1[k];
                 v[7] += aT * w2[k];
-                const float dalpha = T[k] * ((c0 - S0[k]) * w0[k] + (c1 - S1[k]) * w1[k] + (c2 - S2[k]) * w2[k]);
-                S0[k] = alpha * c0 + (1.0f - alpha) * S0[k];
-                S1[k] = alpha * c1 + (1.0f - alpha) * S1[k];
-                S2[k] = alpha * c2 + (1.0f - alpha) * S2[k];
-                if (!(rG > 0.99f)) {
-                    const float dsig = -rG * dalpha;
-                    const float a = 2.0f * A.z, bb = A.w, c = 2.0f * B.x;
-                    v[0] += (a * dx + bb * dy) * dsig;
-                    v[1] += (bb * dx + c * dy) * dsig;
-                    v[2] += 0.5f * dx * dx * dsig;
-                    v[3] += dx * dy * dsig;
-                    v[4] += 0.5f * dy * dy * dsig;
-                    e += G * dalpha;
-                }
+                const float cw = c0 * w0[k] + c1 * w1[k] + c2 * w2[k];
+                const float dalpha = T[k] * (cw - P[k]);
+                P[k] = alpha * cw + om * P[k];
+                const float g = rG > 0.99f ? 0.0f : G * dalpha;  // clamped alpha: no rho / sigma gradient
+                const float gx = g * dx, gy = g * dy;
+                e += g;
+                v[0] += gx;
+                v[1] += gy;
+                v[2] = fmaf(gx, dx, v[2]);
+                v[3] = fmaf(gx, dy, v[3]);
+                v[4] = fmaf(gy, dy, v[4]);
             }
             if (__any_sync(VKS_FULL_MASK, contrib)) {
                 const float r = warp_reduce_8plus1(v, e, lane);
-                if (myterm >= 0) atomicAdd(tbase + (size_t)s.id[j] * tstride, myterm == 8 ? e : r);
+                const float other = __shfl_xor_sync(VKS_FULL_MASK, r, 4);  // lanes 0 <-> 4: the two first moments
+                // dmean = -rho (a m_x + b m_y, b m_x + c m_y), dconic = -rho (m_xx / 2, m_xy, m_yy / 2),
+                // colour = r, opacity = e; branch-free with the lane's constant term selectors
+                const float nrho = -B.y;
+                const float cr = fmaf(nrho, fmaf(kA, 2.0f * A.z, fmaf(kC, 2.0f * B.x, kH)), kOne);
+                const float out = myterm == 8 ? e : fmaf(cr, r, (nrho * kB * A.w) * other);
+                if (myterm >= 0) atomicAdd(tbase + (size_t)s.id[j] * tstride, out);
             }
         }
     }
@@ -454,8 +470,11 @@ int cull_choice(const vks_config& cfg) {
     return mode;
 }
 
-// pixels per thread: 2 (8x8 warp patches) by default, 4 (8x16) on request
-int ppt_choice(const char* var) { return env_choice(var, 2, 2, 4) == 4 ? 4 : 2; }
+// pixels per thread: 2 (8x8 warp patches) by default, 1 (8x4) or 4 (8x16) on request
+int ppt_choice(const char* var) {
+    const int v = env_choice(var, 2, 1, 4);
+    return v == 3 ? 2 : v;
+}
 
 template <int PPT>
 int dispatch_fwd(int cull, const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
@@ -513,6 +532,7 @@ int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
     const int ppt = ppt_choice("VKS_RASTER_FWD_PPT");
     const int cull = cull_choice(cfg);
     if (ppt == 4) return dispatch_fwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+    if (ppt == 1) return dispatch_fwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
     return dispatch_fwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
 }
 
@@ -525,6 +545,7 @@ int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
     const int ppt = ppt_choice("VKS_RASTER_BWD_PPT");
     const int cull = cull_choice(cfg);
     if (ppt == 4) return dispatch_bwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    if (ppt == 1) return dispatch_bwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
     return dispatch_bwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
 }
 

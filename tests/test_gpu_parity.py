@@ -262,15 +262,15 @@ def _stats(cfg, cam, scene):
 def test_patch_culling_and_ppt_variants_agree(fp, monkeypatch):
     """Patch culling only skips (warp, entry) pairs that cannot composite, and the pixel-per-thread
     layout does not change any pixel's sequence: every variant (no culling / support box /
-    exact ellipse, 2 or 4 pixels per thread) gives the identical image, T and n_contrib, and the
+    exact ellipse, 1, 2 or 4 pixels per thread) gives the identical image, T and n_contrib, and the
     same gradients up to atomic summation order."""
     s = synth.make_scene(200000, "indoor", 70)
     cam = synth.ring_cameras(400, 300, "indoor", 8)[3]
     cfg = synth.default_render_config(footprint=fp)
     dL = synth.upstream_grad(300, 400, 5)
-    variants = [("2", "2", "0"), ("2", "2", "2"), ("4", "4", "2"), ("2", "2", "1")]
+    variants = [("2", "2", "0"), ("2", "2", "2"), ("4", "4", "2"), ("1", "1", "2"), ("2", "2", "1")]
     if fp == 1:
-        variants = variants[:3]  # the box test needs the support footprint
+        variants = variants[:4]  # the box test needs the support footprint
     runs, stats = {}, {}
     for fw, bw, cull in variants:
         monkeypatch.setenv("VKS_RASTER_FWD_PPT", fw)
@@ -292,3 +292,26 @@ def test_patch_culling_and_ppt_variants_agree(fp, monkeypatch):
     assert s2[0] == s0[0] and s2[3] == s0[3]  # visited / replayed do not depend on culling
     assert s2[2] < s0[2] and s2[4] < s0[4]    # ellipse culling removes evaluations
     report(f"cull_fp{fp}", dict(stats={"/".join(k): v for k, v in stats.items()}))
+
+
+@pytest.mark.parametrize("W,H", [(16, 16), (200, 150), (4200, 4000)])
+def test_binning_tile_pass_counts(oracle_lib, W, H):
+    """Binning bit-exact for 1 tile (trivial pass), 130 tiles (one 8-bit pass) and 65,750 tiles
+    (three 6-bit passes), with a few Gaussians large enough that one Gaussian's keys span
+    several 4096-slot key blocks."""
+    s = synth.make_scene(30000, "outdoor", 80)
+    cam = synth.ring_cameras(W, H, "outdoor", 8)[6]
+    eye = -cam["R"].astype(np.float64).T @ cam["t"].astype(np.float64)
+    fwd = cam["R"][2].astype(np.float64)
+    for j in range(4):  # big, opaque Gaussians right in front of the camera
+        s["means"][j] = (eye + (1.0 + 0.3 * j) * fwd).astype(np.float32)
+        s["log_scales"][j] = np.log(0.6)
+        s["opacity_logits"][j] = 4.0
+    cfg = synth.default_render_config()
+    g = run_gpu(s, cam, cfg, debug_unsorted=True)
+    o_proj = oracle_lib.project_fwd(cfg, cam, s)
+    check_projection(o_proj, g, f"bin_{W}x{H}")
+    m = check_binning(oracle_lib, cam, g, f"bin_{W}x{H}")
+    assert m > 0
+    if W * H > 10**6:
+        assert int(g["tiles_touched"].max()) > 3 * 4096  # one Gaussian spans several key blocks

@@ -173,16 +173,16 @@ def run_ours(args):
                               rend.colors, rend.opacities)
             if ev is not None: ev[1].record(stream)
             m = P.vks_bin_sort(cam, rend.means2d, rend.radii, rend.depths, rend.tiles, rend.offsets, None,
-                               rend.vals, rend.tile_offsets, rend.workspace)
+                               rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
             rend.num_isects = m
             if ev is not None: ev[2].record(stream)
             P.vks_raster_fwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals,
-                             rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib)
+                             rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib, tile_order=rend.tile_order)
             if ev is not None: ev[3].record(stream)
             rend.g2d.zero_()
             P.vks_raster_bwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals,
                              rend.tile_offsets, rend.T_final, rend.n_contrib, dLs[v], rend.dmeans2d, rend.dconics,
-                             rend.dcolors, rend.dopacities)
+                             rend.dcolors, rend.dopacities, tile_order=rend.tile_order)
             if ev is not None: ev[4].record(stream)
             g = params.grads()
             # first view of the step overwrites the gradient buffer (no memset), later ones accumulate

@@ -130,8 +130,11 @@ size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles
  *   keys/vals [capacity] <- the M pairs stable-sorted ascending by key (u64); keys is
  *                           nullable (the rasterizer needs only vals and tile_offsets)
  *   tile_offsets [n_tiles+1] u32 <- CSR: #entries with tile id < t
+ *   tile_order [n_tiles] u32 (nullable) <- the tile ids ordered by decreasing list length
+ *                           (approximately: log-spaced length classes) — a scheduling hint for
+ *                           the rasterizer (heaviest tiles first); results never depend on it
  *   keys_unsorted / vals_unsorted (nullable, debug; [capacity] like keys/vals): the pre-sort pairs.
- * Tile grids of >= 2^21 tiles return VKS_ERR_INVALID_ARG.
+ * Tile grids of >= 2^20 tiles return VKS_ERR_INVALID_ARG.
  * If M > capacity (or M >= 2^30) returns VKS_ERR_CAPACITY after writing
  * *num_isects, touching nothing else; the call is idempotent, so the caller
  * regrows and calls again.  Synchronises `stream` once (to read M).
@@ -140,7 +143,8 @@ size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles
 int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
                  const float* depths, const int32_t* tiles_touched, uint32_t* offsets,
                  int64_t capacity, uint64_t* keys, uint32_t* vals, uint64_t* keys_unsorted,
-                 uint32_t* vals_unsorted, uint32_t* tile_offsets, int64_t* num_isects,
+                 uint32_t* vals_unsorted, uint32_t* tile_offsets, uint32_t* tile_order,
+                 int64_t* num_isects,
                  void* workspace, size_t workspace_bytes, vks_stream_t stream);
 
 /*
@@ -151,7 +155,8 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
  *   T *= 1 - alpha;  stop once T < 1e-4.   out = C + T bg.
  *   -> image [H,W,3], T_final [H,W], n_contrib [H,W] int32 (1-based position,
  *      within the tile's list, of the last composited entry; 0 = none).
- * means2d/conics/colors/opacities/radii as produced by vks_project_fwd, vals/tile_offsets as
+ * means2d/conics/colors/opacities/radii as produced by vks_project_fwd, vals/tile_offsets (and
+ * the optional tile_order: the order in which tiles are scheduled; nullptr = tile id order) as
  * produced by vks_bin_sort.  Before evaluating an entry, each warp tests whether any pixel centre
  * of its 8x8 patch can reach alpha >= 1/255 (exact minimum of sigma over the patch against
  * ln(255 rho), with an fp32 error margin) and skips the entry warp-uniformly if none can; radii
@@ -160,7 +165,8 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    const float* means2d, const float* conics, const float* colors,
                    const float* opacities, const int32_t* radii, const uint32_t* vals,
-                   const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib,
+                   const uint32_t* tile_offsets, const uint32_t* tile_order, float* image,
+                   float* T_final, int32_t* n_contrib,
                    vks_stream_t stream);
 
 /*
@@ -177,7 +183,8 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
 int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n,
                          const float* means2d, const float* conics, const float* colors,
                          const float* opacities, const int32_t* radii, const uint32_t* vals,
-                         const uint32_t* tile_offsets, uint64_t* stats, vks_stream_t stream);
+                         const uint32_t* tile_offsets, const uint32_t* tile_order, uint64_t* stats,
+                         vks_stream_t stream);
 
 /*
  * vks_raster_bwd — "Rasterization Backward".
@@ -185,11 +192,12 @@ int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n
  * and ACCUMULATES exact gradients of the forward w.r.t. mean2d, conic (a,b,c
  * as independent scalars), colour and opacity (0 where alpha was clamped).
  *   dL_dimage [H,W,3] -> dmeans2d [n,2], dconics [n,3], dcolors [n,3], dopacities [n] (+=)
+ * tile_order as for vks_raster_fwd (nullable).
  */
 int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    const float* means2d, const float* conics, const float* colors,
                    const float* opacities, const int32_t* radii, const uint32_t* vals,
-                   const uint32_t* tile_offsets,
+                   const uint32_t* tile_offsets, const uint32_t* tile_order,
                    const float* T_final, const int32_t* n_contrib, const float* dL_dimage,
                    float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
                    vks_stream_t stream);

@@ -48,10 +48,10 @@ _lib.vks_version.restype = C.c_int
 _lib.vks_bin_sort_workspace_bytes.restype = C.c_size_t
 _lib.vks_bin_sort_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int32]
 _lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
-_lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 7 + [C.c_size_t, _P]
-_lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 11
-_lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 15
-_lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 9
+_lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 8 + [C.c_size_t, _P]
+_lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 12
+_lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 16
+_lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 10
 _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
 for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats", "vks_raster_bwd",
            "vks_project_bwd"):
@@ -143,8 +143,10 @@ def vks_bin_sort_workspace_bytes(n, capacity, n_tiles) -> int:
 
 
 def vks_bin_sort(cam, means2d, radii, depths, tiles_touched, offsets, keys, vals, tile_offsets,
-                 workspace, keys_unsorted=None, vals_unsorted=None, stream=None, raise_capacity=True):
+                 workspace, keys_unsorted=None, vals_unsorted=None, stream=None, raise_capacity=True,
+                 tile_order=None):
     """Returns M (num_isects).  Capacity = vals.numel(); keys (u64, same capacity) may be None.
+    tile_order (u32 [n_tiles], optional) receives the rasterizer's tile schedule.
     On VKS_ERR_CAPACITY returns -M when raise_capacity is False."""
     k = cam if isinstance(cam, VksCamera) else make_camera(cam)
     n = means2d.shape[0]
@@ -154,7 +156,7 @@ def vks_bin_sort(cam, means2d, radii, depths, tiles_touched, offsets, keys, vals
                            _ptr(offsets, u32, "offsets"), vals.numel(), _ptr(keys, u64, "keys"),
                            _ptr(vals, u32, "vals"), _ptr(keys_unsorted, u64, "keys_unsorted"),
                            _ptr(vals_unsorted, u32, "vals_unsorted"), _ptr(tile_offsets, u32, "tile_offsets"),
-                           C.byref(m), _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
+                           _ptr(tile_order, u32, "tile_order"), C.byref(m), _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
                            _stream(stream))
     if st == VKS_ERR_CAPACITY and not raise_capacity:
         return -int(m.value)
@@ -163,18 +165,20 @@ def vks_bin_sort(cam, means2d, radii, depths, tiles_touched, offsets, keys, vals
 
 
 def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final,
-                   n_contrib, stream=None):
+                   n_contrib, stream=None, tile_order=None):
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_raster_fwd(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                              _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
                              _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
-                             _ptr(tile_offsets, u32, "tile_offsets"), _ptr(image, f32, "image"),
+                             _ptr(tile_offsets, u32, "tile_offsets"), _ptr(tile_order, u32, "tile_order"),
+                             _ptr(image, f32, "image"),
                              _ptr(T_final, f32, "T_final"), _ptr(n_contrib, i32, "n_contrib"),
                              _stream(stream))
     _check("vks_raster_fwd", st)
 
 
-def vks_raster_fwd_stats(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, stats, stream=None):
+def vks_raster_fwd_stats(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, stats, stream=None,
+                         tile_order=None):
     """Diagnostic: accumulate [visited, composited, evaluated, replayed, warp_entries,
     warp_entries_composited] counts into the int64 CUDA tensor `stats` (6 entries)."""
     if stats.numel() < 6:
@@ -183,18 +187,20 @@ def vks_raster_fwd_stats(cfg, cam, means2d, conics, colors, opacities, radii, va
     st = _lib.vks_raster_fwd_stats(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                                    _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
                                    _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
-                                   _ptr(tile_offsets, u32, "tile_offsets"), _ptr(stats, torch.int64, "stats"),
+                                   _ptr(tile_offsets, u32, "tile_offsets"), _ptr(tile_order, u32, "tile_order"),
+                                   _ptr(stats, torch.int64, "stats"),
                                    _stream(stream))
     _check("vks_raster_fwd_stats", st)
 
 
 def vks_raster_bwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib,
-                   dL_dimage, dmeans2d, dconics, dcolors, dopacities, stream=None):
+                   dL_dimage, dmeans2d, dconics, dcolors, dopacities, stream=None, tile_order=None):
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_raster_bwd(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                              _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
                              _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
-                             _ptr(tile_offsets, u32, "tile_offsets"), _ptr(T_final, f32, "T_final"),
+                             _ptr(tile_offsets, u32, "tile_offsets"), _ptr(tile_order, u32, "tile_order"),
+                             _ptr(T_final, f32, "T_final"),
                              _ptr(n_contrib, i32, "n_contrib"), _ptr(dL_dimage, f32, "dL_dimage"),
                              _ptr(dmeans2d, f32, "dmeans2d"), _ptr(dconics, f32, "dconics"),
                              _ptr(dcolors, f32, "dcolors"), _ptr(dopacities, f32, "dopacities"),

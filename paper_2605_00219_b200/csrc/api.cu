@@ -82,8 +82,8 @@ size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles
 int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
                  const float* depths, const int32_t* tiles_touched, uint32_t* offsets, int64_t capacity,
                  uint64_t* keys, uint32_t* vals, uint64_t* keys_unsorted, uint32_t* vals_unsorted,
-                 uint32_t* tile_offsets, int64_t* num_isects, void* workspace, size_t workspace_bytes,
-                 vks_stream_t stream) {
+                 uint32_t* tile_offsets, uint32_t* tile_order, int64_t* num_isects, void* workspace,
+                 size_t workspace_bytes, vks_stream_t stream) {
     if (!camera_ok(cam) || n < 0 || capacity < 0 || !num_isects || !tile_offsets) return VKS_ERR_INVALID_ARG;
     if (n > 0 && (!means2d || !radii || !depths || !tiles_touched || !offsets)) return VKS_ERR_INVALID_ARG;
     if (capacity > 0 && !vals) return VKS_ERR_INVALID_ARG;  // keys is optional
@@ -93,15 +93,15 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
     if (n >= (1ll << 32)) return VKS_ERR_UNSUPPORTED;  // Gaussian ids are u32
     if (!device_present()) return VKS_ERR_CUDA;
     return cuda_status(vks::run_bin_sort(*cam, n, means2d, radii, depths, tiles_touched, offsets, capacity, keys,
-                                         vals, keys_unsorted, vals_unsorted, tile_offsets, num_isects, workspace,
+                                         vals, keys_unsorted, vals_unsorted, tile_offsets, tile_order, num_isects,
+                                         workspace,
                                          workspace_bytes, (cudaStream_t)stream));
 }
 
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
                    const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                   const uint32_t* vals,
-                   const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib,
-                   vks_stream_t stream) {
+                   const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                   float* image, float* T_final, int32_t* n_contrib, vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
@@ -111,26 +111,28 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
     return cuda_status(vks::launch_raster_fwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
-                                              tile_offsets, image, T_final, n_contrib, (cudaStream_t)stream));
+                                              tile_offsets, tile_order, image, T_final, n_contrib,
+                                              (cudaStream_t)stream));
 }
 
 int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
                          const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                         const uint32_t* vals, const uint32_t* tile_offsets, uint64_t* stats,
-                         vks_stream_t stream) {
+                         const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                         uint64_t* stats, vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (!camera_ok(cam) || n < 0 || !tile_offsets || !stats) return VKS_ERR_INVALID_ARG;
     if (n > 0 && (!means2d || !conics || !colors || !opacities || !radii)) return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
     return vks::launch_raster_fwd_stats(*cfg, *cam, means2d, conics, colors, opacities, radii, vals, tile_offsets,
-                                        reinterpret_cast<unsigned long long*>(stats), (cudaStream_t)stream);
+                                        tile_order, reinterpret_cast<unsigned long long*>(stats),
+                                        (cudaStream_t)stream);
 }
 
 int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
                    const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                   const uint32_t* vals,
-                   const uint32_t* tile_offsets, const float* T_final, const int32_t* n_contrib,
+                   const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                   const float* T_final, const int32_t* n_contrib,
                    const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                    float* dopacities, vks_stream_t stream) {
     int st = config_ok(cfg);
@@ -144,7 +146,8 @@ int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
     return cuda_status(vks::launch_raster_bwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
-                                              tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics,
+                                              tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d,
+                                              dconics,
                                               dcolors, dopacities, (cudaStream_t)stream));
 }
 

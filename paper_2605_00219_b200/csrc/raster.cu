@@ -83,8 +83,8 @@ __device__ __forceinline__ float sigma_lower(float ha, float b, float hc, float 
 
 // true if no pixel centre of the warp patch [wx0, wx1] x [wy0, wy1] can composite entry (A, B).
 // kCullEllipse: sigma(dx, dy) = ha dx^2 + b dx dy + hc dy^2 (dx = u - x) is convex with its
-// minimum 0 at the centre; over the rectangle its minimum lies on one of the 4 edges, where it
-// is a 1-D quadratic minimised at the clamped stationary point.  A pixel composites only if
+// minimum 0 at the centre; over the rectangle its minimum lies on an edge facing the centre,
+// where it is a 1-D quadratic minimised at the clamped stationary point.  A pixel composites only if
 // rho G >= 1/255, i.e. sigma <= ln(255 rho) (+ ex2 / log approximation slack < 1e-5), so the
 // test culls only when the lower bound exceeds ln(255 rho) + 1e-3.
 template <int CULL>
@@ -96,14 +96,16 @@ __device__ __forceinline__ bool culled(const Entry& e, float wx0, float wx1, flo
         const float my = (float)e.r.y * (1.0f + 1.0f / 64.0f) + 1.0f;
         return e.a.x + mx < wx0 || e.a.x - mx > wx1 || e.a.y + my < wy0 || e.a.y - my > wy1;
     } else if (CULL == kCullEllipse) {
+        // only the edges facing the mean can hold the minimum (KKT: at a minimiser on an edge the
+        // gradient points inwards, and convexity then puts the mean on the edge's outer side)
         const float dxl = e.a.x - wx1, dxh = e.a.x - wx0, dyl = e.a.y - wy1, dyh = e.a.y - wy0;
-        if (dxl <= 0.0f && dxh >= 0.0f && dyl <= 0.0f && dyh >= 0.0f) return false;
+        const bool fx = dxl > 0.0f || dxh < 0.0f, fy = dyl > 0.0f || dyh < 0.0f;
+        if (!fx && !fy) return false;  // the mean is inside the patch
         const float ha = e.a.z, b = e.a.w, hc = e.b.x;
-        const float kx = __fdividef(-b, 2.0f * ha), ky = __fdividef(-b, 2.0f * hc);
-        float m = sigma_lower(ha, b, hc, dxl, fminf(fmaxf(ky * dxl, dyl), dyh));
-        m = fminf(m, sigma_lower(ha, b, hc, dxh, fminf(fmaxf(ky * dxh, dyl), dyh)));
-        m = fminf(m, sigma_lower(ha, b, hc, fminf(fmaxf(kx * dyl, dxl), dxh), dyl));
-        m = fminf(m, sigma_lower(ha, b, hc, fminf(fmaxf(kx * dyh, dxl), dxh), dyh));
+        const float dxe = dxl > 0.0f ? dxl : dxh, dye = dyl > 0.0f ? dyl : dyh;
+        const float mx = sigma_lower(ha, b, hc, dxe, fminf(fmaxf(__fdividef(-b, 2.0f * hc) * dxe, dyl), dyh));
+        const float my = sigma_lower(ha, b, hc, fminf(fmaxf(__fdividef(-b, 2.0f * ha) * dye, dxl), dxh), dye);
+        const float m = fminf(fx ? mx : INFINITY, fy ? my : INFINITY);
         return m > __logf(255.0f * e.b.y) + 1e-3f;
     }
     return false;
@@ -167,13 +169,14 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                                                                  const int2* __restrict__ radii,
                                                                  const uint32_t* __restrict__ vals,
                                                                  const uint32_t* __restrict__ tile_offsets,
+                                                                 const uint32_t* __restrict__ tile_order,
                                                                  float* __restrict__ image, float* __restrict__ T_final,
                                                                  int* __restrict__ n_contrib,
                                                                  unsigned long long* __restrict__ stats = nullptr) {
     __shared__ WarpStage stage[8 / PPT];
     unsigned long long n_eval = 0, n_comp = 0, n_went = 0, n_wcomp = 0;
     const int TX = tiles_x(cam);
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
     const int lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
@@ -213,25 +216,39 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
             live &= live - 1;
             const float4 A = s.a[j], B = s.b[j];
             const float c2 = s.c2[j];
-            bool any = false;
+            if constexpr (STATS) {
+                bool any = false;
 #pragma unroll
-            for (int k = 0; k < PPT; k++) {
-                if (done[k]) continue;
-                float dx, dy, G, rG, alpha;
-                if (STATS) n_eval++;
-                if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
-                if (STATS) { n_comp++; any = true; }
-                const float aT = alpha * T[k];
-                C0[k] = fmaf(B.z, aT, C0[k]);
-                C1[k] = fmaf(B.w, aT, C1[k]);
-                C2[k] = fmaf(c2, aT, C2[k]);
-                T[k] = T[k] * (1.0f - alpha);
-                last[k] = (int)(b - start) + j + 1;
-                if (T[k] < 1e-4f) done[k] = true;
-            }
-            if (STATS) {
+                for (int k = 0; k < PPT; k++) {
+                    if (done[k]) continue;
+                    float dx, dy, G, rG, alpha;
+                    n_eval++;
+                    if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
+                    n_comp++;
+                    any = true;
+                    T[k] = T[k] * (1.0f - alpha);
+                    last[k] = (int)(b - start) + j + 1;
+                    if (T[k] < 1e-4f) done[k] = true;
+                }
                 const bool wany = __any_sync(VKS_FULL_MASK, any);
                 if (lane == 0) { n_went++; n_wcomp += wany; }
+            } else {
+                // branch-free: a skipped entry composites alpha = 0, which leaves C and T
+                // bit-identical (C + c * 0 = C, T * (1 - 0) = T)
+                const int pos1 = (int)(b - start) + j + 1;
+#pragma unroll
+                for (int k = 0; k < PPT; k++) {
+                    float dx, dy, G, rG, alpha;
+                    const bool ok = eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha) && !done[k];
+                    const float a = ok ? alpha : 0.0f;
+                    const float aT = a * T[k];
+                    C0[k] = fmaf(B.z, aT, C0[k]);
+                    C1[k] = fmaf(B.w, aT, C1[k]);
+                    C2[k] = fmaf(c2, aT, C2[k]);
+                    T[k] = T[k] * (1.0f - a);
+                    last[k] = ok ? pos1 : last[k];
+                    done[k] = done[k] || (ok && T[k] < 1e-4f);
+                }
             }
         }
     }
@@ -308,6 +325,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                                                                  const int2* __restrict__ radii,
                                                                  const uint32_t* __restrict__ vals,
                                                                  const uint32_t* __restrict__ tile_offsets,
+                                                                 const uint32_t* __restrict__ tile_order,
                                                                  const float* __restrict__ T_final,
                                                                  const int* __restrict__ n_contrib,
                                                                  const float* __restrict__ dL_dimage,
@@ -315,7 +333,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                                                                  float* __restrict__ dcolors, float* __restrict__ dopac) {
     __shared__ WarpStage stage[8 / PPT];
     const int TX = tiles_x(cam);
-    const int tile = blockIdx.x;
+    const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
     const unsigned lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
@@ -395,20 +413,23 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             bool contrib = false;
 #pragma unroll
             for (int k = 0; k < PPT; k++) {
-                if (pos >= last[k]) continue;
+                // branch-free: an entry the pixel did not composite replays with alpha = 0, which
+                // leaves T, P and every accumulator bit-identical (T / 1, 0 * x + P, + 0)
                 float dx, dy, G, rG, alpha;
-                if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
-                contrib = true;
-                const float om = 1.0f - alpha;
+                const bool ok = eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha) && pos < last[k];
+                contrib = contrib || ok;
+                const float a = ok ? alpha : 0.0f;
+                const float om = 1.0f - a;
                 T[k] = __fdividef(T[k], om);
-                const float aT = alpha * T[k];
+                const float aT = a * T[k];
                 v[5] += aT * w0[k];
                 v[6] += aT * w1[k];
                 v[7] += aT * w2[k];
                 const float cw = c0 * w0[k] + c1 * w1[k] + c2 * w2[k];
                 const float dalpha = T[k] * (cw - P[k]);
-                P[k] = alpha * cw + om * P[k];
-                const float g = rG > 0.99f ? 0.0f : G * dalpha;  // clamped alpha: no rho / sigma gradient
+                P[k] = a * cw + om * P[k];
+                // no gradient where the pixel skipped the entry or alpha was clamped
+                const float g = (!ok || rG > 0.99f) ? 0.0f : G * dalpha;
                 const float gx = g * dx, gy = g * dy;
                 e += g;
                 v[0] += gx;
@@ -434,25 +455,26 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
 template <int PPT, int CULL>
 int launch_fwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-               const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
+               const uint32_t* tile_offsets, const uint32_t* tile_order, float* image, float* T_final,
+               int32_t* n_contrib, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     raster_fwd_kernel<PPT, CULL><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
-        reinterpret_cast<const int2*>(radii), vals, tile_offsets, image, T_final, n_contrib);
+        reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, image, T_final, n_contrib);
     return LaunchCheck::check();
 }
 
 template <int PPT, int CULL>
 int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-               const uint32_t* tile_offsets, const float* T_final, const int32_t* n_contrib,
-               const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
-               cudaStream_t st) {
+               const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
+               const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
+               float* dopacities, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     raster_bwd_kernel<PPT, CULL><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
-        reinterpret_cast<const int2*>(radii), vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics,
-        dcolors, dopacities);
+        reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage,
+        dmeans2d, dconics, dcolors, dopacities);
     return LaunchCheck::check();
 }
 
@@ -479,24 +501,25 @@ int ppt_choice(const char* var) {
 template <int PPT>
 int dispatch_fwd(int cull, const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                  const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-                 const uint32_t* tile_offsets, float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
+                 const uint32_t* tile_offsets, const uint32_t* tile_order, float* image, float* T_final,
+                 int32_t* n_contrib, cudaStream_t st) {
     switch (cull) {
-        case kCullNone: return launch_fwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
-        case kCullBox: return launch_fwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
-        default: return launch_fwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+        case kCullNone: return launch_fwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
+        case kCullBox: return launch_fwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
+        default: return launch_fwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
     }
 }
 
 template <int PPT>
 int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                  const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-                 const uint32_t* tile_offsets, const float* T_final, const int32_t* n_contrib,
-                 const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
-                 cudaStream_t st) {
+                 const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
+                 const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
+                 float* dopacities, cudaStream_t st) {
     switch (cull) {
-        case kCullNone: return launch_bwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-        case kCullBox: return launch_bwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-        default: return launch_bwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+        case kCullNone: return launch_bwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+        case kCullBox: return launch_bwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+        default: return launch_bwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
     }
 }
 
@@ -504,49 +527,50 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
 
 int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                             const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-                            const uint32_t* tile_offsets, unsigned long long* stats, cudaStream_t st) {
+                            const uint32_t* tile_offsets, const uint32_t* tile_order, unsigned long long* stats,
+                            cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     const auto m2 = reinterpret_cast<const float2*>(means2d);
     const auto r2 = reinterpret_cast<const int2*>(radii);
     switch (cull_choice(cfg)) {
         case kCullNone:
             raster_fwd_kernel<2, kCullNone, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                           vals, tile_offsets, nullptr, nullptr, nullptr, stats);
+                                                                           vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, stats);
             break;
         case kCullBox:
             raster_fwd_kernel<2, kCullBox, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                          vals, tile_offsets, nullptr, nullptr, nullptr, stats);
+                                                                          vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, stats);
             break;
         default:
             raster_fwd_kernel<2, kCullEllipse, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                              vals, tile_offsets, nullptr, nullptr, nullptr, stats);
+                                                                              vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, stats);
     }
     return LaunchCheck::check();
 }
 
 int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                      const uint32_t* vals, const uint32_t* tile_offsets, float* image, float* T_final,
-                      int32_t* n_contrib, cudaStream_t st) {
+                      const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                      float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
     (void)n;
     const int ppt = ppt_choice("VKS_RASTER_FWD_PPT");
     const int cull = cull_choice(cfg);
-    if (ppt == 4) return dispatch_fwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
-    if (ppt == 1) return dispatch_fwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
-    return dispatch_fwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final, n_contrib, st);
+    if (ppt == 4) return dispatch_fwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
+    if (ppt == 1) return dispatch_fwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
+    return dispatch_fwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
 }
 
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                      const uint32_t* vals, const uint32_t* tile_offsets, const float* T_final,
-                      const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics,
-                      float* dcolors, float* dopacities, cudaStream_t st) {
+                      const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                      const float* T_final, const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
+                      float* dconics, float* dcolors, float* dopacities, cudaStream_t st) {
     (void)n;
     const int ppt = ppt_choice("VKS_RASTER_BWD_PPT");
     const int cull = cull_choice(cfg);
-    if (ppt == 4) return dispatch_bwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-    if (ppt == 1) return dispatch_bwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-    return dispatch_bwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    if (ppt == 4) return dispatch_bwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    if (ppt == 1) return dispatch_bwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    return dispatch_bwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
 }
 
 }  // namespace vks

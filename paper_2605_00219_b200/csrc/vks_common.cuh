@@ -87,18 +87,19 @@ size_t bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles);
 int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const int32_t* radii,
                  const float* depths, const int32_t* tiles_touched, uint32_t* offsets,
                  int64_t capacity, uint64_t* keys, uint32_t* vals, uint64_t* keys_unsorted,
-                 uint32_t* vals_unsorted, uint32_t* tile_offsets, int64_t* num_isects,
+                 uint32_t* vals_unsorted, uint32_t* tile_offsets, uint32_t* tile_order, int64_t* num_isects,
                  void* workspace, size_t workspace_bytes, cudaStream_t s);
 int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                      const uint32_t* vals, const uint32_t* tile_offsets, float* image,
-                      float* T_final, int32_t* n_contrib, cudaStream_t s);
+                      const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                      float* image, float* T_final, int32_t* n_contrib, cudaStream_t s);
 int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                             const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-                            const uint32_t* tile_offsets, unsigned long long* stats, cudaStream_t s);
+                            const uint32_t* tile_offsets, const uint32_t* tile_order, unsigned long long* stats,
+                            cudaStream_t s);
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                      const uint32_t* vals, const uint32_t* tile_offsets, const float* T_final,
-                      const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
+                      const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                      const float* T_final, const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
                       float* dconics, float* dcolors, float* dopacities, cudaStream_t s);
 }  // namespace vks

@@ -69,6 +69,7 @@ class ViewRenderer:
         self.colors, self.opacities = e(n, 3), e(n)
         self.offsets = e(n, dt=torch.uint32)
         self.tile_offsets = e(self.n_tiles + 1, dt=torch.uint32)
+        self.tile_order = e(self.n_tiles, dt=torch.uint32)  # raster schedule (heaviest tiles first)
         self.image, self.T_final = e(height, width, 3), e(height, width)
         self.n_contrib = e(height, width, dt=torch.int32)
         self.g2d = torch.zeros(n * 9, dtype=torch.float32, device=device)
@@ -96,13 +97,13 @@ class ViewRenderer:
             m = V.vks_bin_sort(cam, self.means2d, self.radii, self.depths, self.tiles, self.offsets,
                                self.keys if want_keys else None,
                                self.vals, self.tile_offsets, self.workspace, keys_unsorted, vals_unsorted,
-                               raise_capacity=False)
+                               raise_capacity=False, tile_order=self.tile_order)
             if m >= 0:
                 break
             self._alloc_capacity(int(-m * 1.25) + 1024)
         self.num_isects = m
         V.vks_raster_fwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.radii, self.vals,
-                         self.tile_offsets, self.image, self.T_final, self.n_contrib)
+                         self.tile_offsets, self.image, self.T_final, self.n_contrib, tile_order=self.tile_order)
         return self.image
 
     def backward(self, cfg, cam, P: GaussianParams, dL_dimage: torch.Tensor, zero_2d: bool = True,
@@ -115,7 +116,7 @@ class ViewRenderer:
             cfg = dict(cfg, flags=int(cfg.get("flags", 0)) | V.FLAG_GRAD_OVERWRITE)
         V.vks_raster_bwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.radii, self.vals,
                          self.tile_offsets, self.T_final, self.n_contrib, dL_dimage, self.dmeans2d, self.dconics,
-                         self.dcolors, self.dopacities)
+                         self.dcolors, self.dopacities, tile_order=self.tile_order)
         g = P.grads()
         V.vks_project_bwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.colors, self.radii,
                           self.dmeans2d, self.dconics, self.dcolors, self.dopacities, g["dmeans"],

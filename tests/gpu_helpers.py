@@ -30,7 +30,7 @@ def run_gpu(scene, cam, cfg, dL=None, capacity=None, debug_unsorted=False):
         r.forward(cfg, cam, params, ku, vu, want_keys=True)
     out = dict(means2d=r.means2d, conics=r.conics, depths=r.depths, radii=r.radii, tiles_touched=r.tiles,
                colors=r.colors, opacities=r.opacities, offsets=r.offsets, tile_offsets=r.tile_offsets,
-               image=r.image, T_final=r.T_final, n_contrib=r.n_contrib)
+               image=r.image, T_final=r.T_final, n_contrib=r.n_contrib, tile_order=r.tile_order)
     m = r.num_isects
     res = {k: to_np(v) for k, v in out.items()}
     res["num_isects"] = m

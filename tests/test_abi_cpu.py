@@ -26,6 +26,19 @@ def test_library_exports_every_declared_symbol():
     assert P.vks_version() == 1
 
 
+def test_no_unresolved_library_symbols():
+    """Every launcher the entry points call is defined in the library (a declaration / definition
+    mismatch would otherwise only surface as an undefined symbol at load time on the GPU box)."""
+    import shutil
+    import subprocess
+    nm = shutil.which("nm")
+    if not nm:
+        pytest.skip("nm not available")
+    out = subprocess.run([nm, "-D", "--undefined-only", "-C", os.path.join(ROOT, "paper_2605_00219_b200", "libvks.so")],
+                         capture_output=True, text=True).stdout
+    assert "vks::" not in out and "vks_" not in out, out
+
+
 def test_cuda_objects_are_sm100a():
     """The library carries sm_100a SASS (cuobjdump lists the ELF arch)."""
     import shutil
@@ -65,12 +78,12 @@ def test_argument_validation_is_synchronous():
     bad = V.make_config(dict(sh_degree=3, sh_coeffs=9))
     assert lib.vks_project_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 13)) == V.VKS_ERR_INVALID_ARG
     bad = V.make_config(dict(sh_degree=3, sh_coeffs=16, footprint=7))
-    assert lib.vks_raster_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 11)) == V.VKS_ERR_UNSUPPORTED
+    assert lib.vks_raster_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 12)) == V.VKS_ERR_UNSUPPORTED
     wide = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
                               width=70000, height=64))
-    assert lib.vks_raster_bwd(C.byref(cfg), C.byref(wide), 0, *([None] * 15)) == V.VKS_ERR_INVALID_ARG
+    assert lib.vks_raster_bwd(C.byref(cfg), C.byref(wide), 0, *([None] * 16)) == V.VKS_ERR_INVALID_ARG
     m = C.c_int64(0)
-    assert lib.vks_bin_sort(C.byref(cam), 5, *([None] * 5), 0, *([None] * 4), None, C.byref(m), None, 0,
+    assert lib.vks_bin_sort(C.byref(cam), 5, *([None] * 5), 0, *([None] * 4), None, None, C.byref(m), None, 0,
                             None) == V.VKS_ERR_INVALID_ARG
 
 
@@ -84,7 +97,7 @@ def test_no_cpu_fallback():
     cam = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
                              width=64, height=64))
     st = lib.vks_raster_fwd(C.byref(cfg), C.byref(cam), 0, None, None, None, None, None, None, C.c_void_p(16),
-                            C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), None)
+                            None, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), None)
     assert st == V.VKS_ERR_CUDA
     assert b"no CUDA device" in lib.vks_last_cuda_error()
 

@@ -60,6 +60,13 @@ def check_binning(oracle_lib, cam, g, tag):
     assert np.array_equal(g["keys"], ob["keys"]), tag
     assert np.array_equal(g["vals"], ob["vals"]), tag
     assert np.array_equal(g["tile_offsets"], ob["tile_offsets"]), tag
+    if "tile_order" in g:  # the raster schedule: a permutation of the tiles, longest lists first
+        order = g["tile_order"].astype(np.int64)
+        n_tiles = len(ob["tile_offsets"]) - 1
+        assert np.array_equal(np.sort(order), np.arange(n_tiles)), tag
+        lens = np.diff(ob["tile_offsets"].astype(np.int64))[order]
+        octave = np.where(lens > 0, np.floor(np.log2(np.maximum(lens, 1))), -1)
+        assert np.all(np.diff(octave) <= 0), tag
     return ob["num_isects"]
 
 
@@ -315,3 +322,28 @@ def test_binning_tile_pass_counts(oracle_lib, W, H):
     assert m > 0
     if W * H > 10**6:
         assert int(g["tiles_touched"].max()) > 3 * 4096  # one Gaussian spans several key blocks
+
+
+@pytest.mark.parametrize("case", ["equal_depths", "wide_range"])
+def test_binning_depth_ranges(oracle_lib, case):
+    """The depth sort uses as many digit passes as the visible depth-bit range needs: all depths
+    equal (one trivial pass: ties keep id order) and a range of ~2^31 depth bits (4 passes)."""
+    s = synth.make_scene(20000, "outdoor", 90)
+    cam = dict(R=np.eye(3, dtype=np.float32), t=np.zeros(3, np.float32), fx=200.0, fy=200.0, cx=96.0, cy=64.0,
+               width=192, height=128)
+    rng = np.random.default_rng(5)
+    if case == "equal_depths":
+        z = np.full(len(s["means"]), 5.0)
+    else:
+        z = np.exp(rng.uniform(np.log(0.02), np.log(5e4), len(s["means"])))
+    s["means"] = np.stack([rng.uniform(-0.45, 0.45, len(z)) * z, rng.uniform(-0.3, 0.3, len(z)) * z, z],
+                          1).astype(np.float32)
+    s["log_scales"] = (np.log(0.01 * z)[:, None] + rng.normal(0, 0.3, (len(z), 3))).astype(np.float32)
+    cfg = synth.default_render_config()
+    g = run_gpu(s, cam, cfg, debug_unsorted=True)
+    o_proj = oracle_lib.project_fwd(cfg, cam, s)
+    check_projection(o_proj, g, case)
+    assert check_binning(oracle_lib, cam, g, case) > 1000
+    d = g["depths"][g["tiles_touched"] > 0].view(np.uint32).astype(np.int64)
+    spread = int(d.max() - d.min())
+    assert (spread == 0) if case == "equal_depths" else (spread > 2**27)

@@ -98,7 +98,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------- algorithmic work
-def algorithmic_bytes(n, vis, m, K=16):
+def algorithmic_bytes(n, vis, m, dpasses=4, K=16):
     """Per-view algorithmic HBM bytes of the HBM-bound stages, for the algorithms as built
     (DESIGN.md §6).  Parameters are fp32; sh has K coefficients per channel."""
     sh = 12 * K
@@ -107,13 +107,13 @@ def algorithmic_bytes(n, vis, m, K=16):
         # written for all (12 B), the other 40 B of outputs for the visible
         project_fwd=44 * n + sh * vis + 12 * n + 40 * vis,
         # id-order scan (read tiles twice, write offsets) + compaction of the visible (read depth,
-        # means2d, radii; write depth key, id, rect code) + 4 depth passes over V (count 4 B, scatter
-        # 8 B in / 8 B out) + the last pass's rect gather (8 B in, 8 B out) + depth-order scan (rect
-        # codes twice, slots out) + rect difference array (8 B) + key expansion twice (rect code,
-        # slot, id: 16 B each) writing 8 B per key + the last tile pass (count 4 B, scatter 8 B in,
-        # 4 B out per key)
-        bin_sort=(12 * n + (20 + 16) * vis + 4 * 20 * vis + 16 * vis + (16 + 4) * vis + 8 * vis
-                  + 2 * 16 * vis + 8 * m + (4 + 8 + 4) * m),
+        # means2d, radii; write depth key, id, rect code) + `dpasses` depth passes over V (count
+        # 4 B, scatter 8 B in / 8 B out) + depth-order scan (ids + gathered rect codes in, rect
+        # codes out; rect codes in, slots out) + rect difference array (8 B) + key-pass count
+        # (rect code + slot) + key-pass scatter (rect code, slot, id in; 8 B per key out) + the
+        # last tile pass (count 4 B, scatter 8 B in, 4 B out per key)
+        bin_sort=(12 * n + (20 + 16) * vis + dpasses * 20 * vis + (12 + 8) * vis + (8 + 4) * vis + 8 * vis
+                  + 12 * vis + 16 * vis + 8 * m + (4 + 8 + 4) * m),
         # overwrite semantics: params + 2D grads + colours of visible, radii of all, 236 B written for all
         project_bwd=8 * n + vis * ((40 + sh) + 36 + 12) + n * (40 + sh),
     )
@@ -233,7 +233,11 @@ def run_ours(args):
     P.vks_raster_fwd_stats(cfg, cams[my_views[(args.warmup + args.steps - 1) % len(my_views)]], rend.means2d,
                            rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals, rend.tile_offsets, stats)
     visited, composited, evaluated, replayed, warp_entries, warp_entries_comp = (int(x) for x in stats.tolist())
-    ab = algorithmic_bytes(n, vis, m_last)
+    # depth passes the sort ran: <= 8-bit digits over the visible depth-bit range
+    dvis = rend.depths[rend.tiles > 0].view(torch.int32).to(torch.int64)
+    drange = int(dvis.max().item() - dvis.min().item()) if dvis.numel() else 0
+    dpasses = max(1, (drange.bit_length() + 7) // 8)
+    ab = algorithmic_bytes(n, vis, m_last, dpasses)
     fl = raster_flops(visited, composited, replayed)
     pk = peaks()
     clock_mhz = clk["sm_mhz"] or pk["sm_max_mhz"]
@@ -244,6 +248,7 @@ def run_ours(args):
         per_stage[k] = dict(ms=st_ms[k], bound="hbm", achieved=gbs, peak=pk["hbm_gbs"], unit="GB/s",
                             frac=gbs / pk["hbm_gbs"], algorithmic_bytes=ab[k])
     per_stage["bin_sort"]["gkeys_per_s"] = m_last / (st_ms["bin_sort"] * 1e-3) / 1e9
+    per_stage["bin_sort"]["depth_passes"] = dpasses
     for k in ("raster_fwd", "raster_bwd"):
         tf = fl[k] / (st_ms[k] * 1e-3) / 1e12
         per_stage[k] = dict(ms=st_ms[k], bound="alu", achieved=tf, peak=fp32_peak_tflops, unit="TFLOP/s",

@@ -31,9 +31,38 @@ constexpr int kWarps = kThreads / 32;
 #define C35 1.445305721320277f
 #define C36 -0.5900435899266435f
 
+// Per-view constants of steps 6 and 12 (FOV limits, camera centre), computed once by the launcher
+// with the same IEEE fp32 operations in the same order (host code is compiled without FMA
+// contraction), instead of once per Gaussian.
+struct CamConst {
+    float lxp, lxn, lyp, lyn;  // step 6
+    float cp[3];               // step 12: campos = -R^T t
+};
+
+CamConst cam_const(const vks_camera& cam) {
+    CamConst k;
+    const float fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
+    const float W = (float)cam.width, H = (float)cam.height;
+    volatile float t;  // keeps every intermediate an IEEE-rounded float
+    t = 0.5f * W; t = t / fx; t = 0.3f * t; const float mx = t;
+    t = 0.5f * H; t = t / fy; t = 0.3f * t; const float my = t;
+    t = W - cx; t = t / fx; t = t + mx; k.lxp = t;
+    t = cx / fx; t = t + mx; k.lxn = t;
+    t = H - cy; t = t / fy; t = t + my; k.lyp = t;
+    t = cy / fy; t = t + my; k.lyn = t;
+    for (int c = 0; c < 3; c++) {
+        float a = cam.R[0 * 3 + c] * cam.t[0];
+        t = cam.R[1 * 3 + c] * cam.t[1]; a = a + t;
+        t = cam.R[2 * 3 + c] * cam.t[2]; a = a + t;
+        k.cp[c] = -a;
+    }
+    return k;
+}
+
 struct Params {
     vks_camera cam;
     vks_config cfg;
+    CamConst cc;
     int64_t n;
     const float* __restrict__ means;
     const float* __restrict__ ls;
@@ -78,12 +107,11 @@ struct Core {
     float u, v, rho;
 };
 
-__device__ __forceinline__ bool project_core(const vks_camera& cam, const vks_config& cfg,
+__device__ __forceinline__ bool project_core(const vks_camera& cam, const vks_config& cfg, const CamConst& cc,
                                              const float mu[3], const float ls[3], float4 q,
                                              float o, Core& k) {
     const float* R = cam.R;
     const float fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
-    const float W = (float)cam.width, H = (float)cam.height;
     // 1. camera-space mean; cull !(t.z > near)
     k.t[0] = dot3(R + 0, mu) + cam.t[0];
     k.t[1] = dot3(R + 3, mu) + cam.t[1];
@@ -123,10 +151,7 @@ __device__ __forceinline__ bool project_core(const vks_camera& cam, const vks_co
     k.fovx = k.fovy = 0;
     k.Lx = k.Ly = 0.0f;
     if (cfg.fov_clamp) {
-        const float lxp = (W - cx) / fx + 0.3f * ((0.5f * W) / fx);
-        const float lxn = cx / fx + 0.3f * ((0.5f * W) / fx);
-        const float lyp = (H - cy) / fy + 0.3f * ((0.5f * H) / fy);
-        const float lyn = cy / fy + 0.3f * ((0.5f * H) / fy);
+        const float lxp = cc.lxp, lxn = cc.lxn, lyp = cc.lyp, lyn = cc.lyn;
         const float rxz = tx / tz, ryz = ty / tz;
         txc = tz * fminf(lxp, fmaxf(-lxn, rxz));
         tyc = tz * fminf(lyp, fmaxf(-lyn, ryz));
@@ -191,13 +216,10 @@ __device__ __forceinline__ bool footprint_rect(const Core& k, const vks_config& 
 }
 
 // 12b. view direction and SH basis (3DGS order, pinned evaluation order)
-__device__ __forceinline__ void view_dir(const vks_camera& cam, const float mu[3], float dh[3], float& dl) {
-    const float* R = cam.R;
-    float cp[3], d[3];
+__device__ __forceinline__ void view_dir(const CamConst& cc, const float mu[3], float dh[3], float& dl) {
+    float d[3];
 #pragma unroll
-    for (int c = 0; c < 3; c++) cp[c] = -((R[0 * 3 + c] * cam.t[0] + R[1 * 3 + c] * cam.t[1]) + R[2 * 3 + c] * cam.t[2]);
-#pragma unroll
-    for (int c = 0; c < 3; c++) d[c] = mu[c] - cp[c];
+    for (int c = 0; c < 3; c++) d[c] = mu[c] - cc.cp[c];
     dl = sqrtf(dot3(d, d));
 #pragma unroll
     for (int c = 0; c < 3; c++) dh[c] = d[c] / dl;
@@ -237,6 +259,13 @@ struct ShLayout {
     static constexpr int kWarpFloats = 32 * SP;
 };
 
+// staged rows readable as float4 (16-byte aligned, whole float4 per row)
+template <int KS>
+constexpr bool vec_rows() {
+    if constexpr (KS > 0) return ShLayout<KS>::kVec && ShLayout<KS>::SP % 4 == 0;
+    return false;
+}
+
 // issue async copies of the SH rows of lanes in `mask` (row base `g0` = first Gaussian of the
 // warp) into the warp's smem slice; the caller commits / waits
 template <int KS>
@@ -244,12 +273,17 @@ __device__ __forceinline__ void sh_stage_async(const float* __restrict__ src, in
     using Lay = ShLayout<KS>;
     const unsigned lane = lane_id();
     if constexpr (Lay::kVec) {
-        constexpr int V = Lay::S / 4;
+        constexpr int V = Lay::S / 4;  // float4 per row
         const float4* s4 = reinterpret_cast<const float4*>(src) + g0 * V;
-#pragma unroll 4
-        for (int j = lane; j < 32 * V; j += 32) {
-            const int r = j / V, c = j - r * V;
-            if ((mask >> r) & 1u) cp_async16(buf + r * Lay::SP + 4 * c, s4 + j);
+        // chunk j = lane + 32 it of the warp's 32 x V float4: row r = j / V, column c = j % V,
+        // advanced incrementally (32 = (32 / V) V + 32 % V)
+        int r = (int)lane / V, c = (int)lane - r * V;
+#pragma unroll
+        for (int it = 0; it < V; it++) {
+            if ((mask >> r) & 1u) cp_async16(buf + r * Lay::SP + 4 * c, s4 + (lane + 32 * it));
+            c += 32 % V;
+            r += 32 / V;
+            if (c >= V) { c -= V; r += 1; }
         }
     } else {
         const float* s1 = src + g0 * Lay::S;
@@ -289,7 +323,7 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
         const float tz = dot3(p.cam.R + 6, mu) + p.cam.t[2];
         near_ok = tz > p.cfg.near_plane;
     }
-    bool vis = near_ok && project_core(p.cam, p.cfg, mu, ls, q, o, k) &&
+    bool vis = near_ok && project_core(p.cam, p.cfg, p.cc, mu, ls, q, o, k) &&
                footprint_rect(k, p.cfg, TX, TY, rxf, ryf, x0, x1, y0, y1);
     // SH rows only of the Gaussians that touch a tile (in front of the camera but outside the
     // view is ~1/3 of the near-plane survivors on the ring views: their rows are never read)
@@ -307,7 +341,7 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
     float Y[16];
     if (vis) {  // the SH basis of the view direction while the rows are in flight
         float dh[3], dl;
-        view_dir(p.cam, mu, dh, dl);
+        view_dir(p.cc, mu, dh, dl);
         sh_basis(dh[0], dh[1], dh[2], K, Y);
     }
     if constexpr (KS > 0) {
@@ -318,14 +352,35 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
         const float* f;
         if constexpr (KS > 0) f = buf + lane * ShLayout<KS>::SP;
         else f = p.sh + 3 * (int64_t)p.cfg.sh_coeffs * i;
+        float acc[3];
+        if constexpr (vec_rows<KS>()) {
+            // 128-bit shared-memory reads of the staged row; element e = 3 l + ch, each channel
+            // still accumulated in ascending l (the pinned order)
+            const float4* f4 = reinterpret_cast<const float4*>(f);
+#pragma unroll
+            for (int m = 0; m < ShLayout<KS>::S / 4; m++) {
+                const float4 qv = f4[m];
+                const float e4[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    const int e = 4 * m + t, l = e / 3, ch = e % 3;
+                    if (l == 0) acc[ch] = Y[0] * e4[t];
+                    else if (l < K) acc[ch] = acc[ch] + Y[l] * e4[t];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) {
+                acc[ch] = Y[0] * f[ch];
+#pragma unroll
+                for (int l = 1; l < 16; l++)
+                    if (l < K) acc[ch] = acc[ch] + Y[l] * f[3 * l + ch];
+            }
+        }
         bool ok = true;
 #pragma unroll
         for (int ch = 0; ch < 3; ch++) {
-            float acc = Y[0] * f[ch];
-#pragma unroll
-            for (int l = 1; l < 16; l++)
-                if (l < K) acc = acc + Y[l] * f[3 * l + ch];
-            const float raw = acc + 0.5f;
+            const float raw = acc[ch] + 0.5f;
             ok = ok && isfinite(raw);
             col[ch] = raw > 0.0f ? raw : 0.0f;
         }
@@ -379,6 +434,7 @@ int launch_project_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
     if (n == 0) return VKS_OK;
     Params p{};
     p.cam = cam; p.cfg = cfg; p.n = n;
+    p.cc = cam_const(cam);
     p.means = means; p.ls = log_scales; p.quats = reinterpret_cast<const float4*>(quats);
     p.ologit = opacity_logits; p.sh = sh;
     p.means2d = reinterpret_cast<float2*>(means2d); p.conics = conics; p.depths = depths;

@@ -27,11 +27,10 @@ namespace {
 
 // One warp's staged batch of 32 list entries (each warp walks the tile list on its own: no block
 // barriers, so a warp never waits for a slower one and stops as soon as its own pixels are done).
-struct WarpStage {
+struct WarpStage {  // all three arrays at a 16-byte stride: one address for the three loads
     float4 a[32];    // u, v, 0.5*a, b
     float4 b[32];    // 0.5*c, rho, c0, c1
-    float c2[32];
-    uint32_t id[32];
+    float4 c[32];    // c2, id (bits), -, -
 };
 
 struct Entry {  // one lane's gathered entry, in registers until it is stored to the stage
@@ -69,8 +68,7 @@ __device__ __forceinline__ Entry gather_entry(uint32_t g, const float2* __restri
 __device__ __forceinline__ void store_entry(WarpStage& s, int lane, const Entry& e) {
     s.a[lane] = e.a;
     s.b[lane] = e.b;
-    s.c2[lane] = e.c2;
-    s.id[lane] = e.id;
+    s.c[lane] = make_float4(e.c2, __uint_as_float(e.id), 0.0f, 0.0f);
 }
 
 // sigma at one candidate point of the patch minus the bound on its fp32 evaluation error
@@ -109,6 +107,12 @@ __device__ __forceinline__ bool culled(const Entry& e, float wx0, float wx1, flo
         return m > __logf(255.0f * e.b.y) + 1e-3f;
     }
     return false;
+}
+
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 __device__ __forceinline__ float exp2_ftz(float x) {
@@ -181,15 +185,16 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
     WarpStage& s = stage[threadIdx.x >> 5];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
+    // a pixel is done once T < 1e-4 (T only changes when it composites, so the test is exact);
+    // pixels outside the image start done (T = 0) and are never written
     float py[PPT], T[PPT], C0[PPT], C1[PPT], C2[PPT];
     int last[PPT];
-    bool done[PPT];
 #pragma unroll
     for (int k = 0; k < PPT; k++) {
         py[k] = (float)(pm.y0 + 4 * k) + 0.5f;
-        T[k] = 1.0f; C0[k] = C1[k] = C2[k] = 0.0f;
+        T[k] = (pm.x < cam.width && pm.y0 + 4 * k < cam.height) ? 1.0f : 0.0f;
+        C0[k] = C1[k] = C2[k] = 0.0f;
         last[k] = 0;
-        done[k] = !(pm.x < cam.width && pm.y0 + 4 * k < cam.height);
     }
     const uint32_t start = tile_offsets[tile], end = tile_offsets[tile + 1];
     // software pipeline: ids two batches ahead, gathered entries one batch ahead
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
     for (uint32_t b = start; b < end; b += 32) {
         bool all_done = true;
 #pragma unroll
-        for (int k = 0; k < PPT; k++) all_done = all_done && done[k];
+        for (int k = 0; k < PPT; k++) all_done = all_done && T[k] < 1e-4f;
         if (__all_sync(VKS_FULL_MASK, all_done)) break;
         __syncwarp();
         // each lane tests its own entry against the warp patch; the warp then visits, in list
@@ -215,12 +220,12 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
             const int j = __ffs(live) - 1;
             live &= live - 1;
             const float4 A = s.a[j], B = s.b[j];
-            const float c2 = s.c2[j];
+            const float c2 = s.c[j].x;
             if constexpr (STATS) {
                 bool any = false;
 #pragma unroll
                 for (int k = 0; k < PPT; k++) {
-                    if (done[k]) continue;
+                    if (T[k] < 1e-4f) continue;
                     float dx, dy, G, rG, alpha;
                     n_eval++;
                     if (!eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha)) continue;
@@ -228,7 +233,6 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                     any = true;
                     T[k] = T[k] * (1.0f - alpha);
                     last[k] = (int)(b - start) + j + 1;
-                    if (T[k] < 1e-4f) done[k] = true;
                 }
                 const bool wany = __any_sync(VKS_FULL_MASK, any);
                 if (lane == 0) { n_went++; n_wcomp += wany; }
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
 #pragma unroll
                 for (int k = 0; k < PPT; k++) {
                     float dx, dy, G, rG, alpha;
-                    const bool ok = eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha) && !done[k];
+                    const bool ok = eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha) && !(T[k] < 1e-4f);
                     const float a = ok ? alpha : 0.0f;
                     const float aT = a * T[k];
                     C0[k] = fmaf(B.z, aT, C0[k]);
@@ -247,7 +251,6 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                     C2[k] = fmaf(c2, aT, C2[k]);
                     T[k] = T[k] * (1.0f - a);
                     last[k] = ok ? pos1 : last[k];
-                    done[k] = done[k] || (ok && T[k] < 1e-4f);
                 }
             }
         }
@@ -405,38 +408,33 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             live &= ~(1u << j);
             const int pos = bs + j;
             const float4 A = s.a[j], B = s.b[j];
-            const float c0 = B.z, c1 = B.w, c2 = s.c2[j];
+            const float4 Cc = s.c[j];
+            const float c0 = B.z, c1 = B.w, c2 = Cc.x;
             // v[0..4]: moments sum(g dx), sum(g dy), sum(g dx^2), sum(g dx dy), sum(g dy^2) with
             // g = G dalpha (dL/dsigma = -rho g); v[5..7]: colour; e = sum(g) (dL/drho)
-            float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            float e = 0.0f;
+            float v[8], e = 0.0f;
             bool contrib = false;
 #pragma unroll
             for (int k = 0; k < PPT; k++) {
                 // branch-free: an entry the pixel did not composite replays with alpha = 0, which
-                // leaves T, P and every accumulator bit-identical (T / 1, 0 * x + P, + 0)
+                // leaves T, P and every accumulator bit-identical (T * 1, 0 * x + P, + 0)
                 float dx, dy, G, rG, alpha;
                 const bool ok = eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha) && pos < last[k];
                 contrib = contrib || ok;
                 const float a = ok ? alpha : 0.0f;
                 const float om = 1.0f - a;
-                T[k] = __fdividef(T[k], om);
+                T[k] = T[k] * rcp_ftz(om);  // om in [0.01, 1]
                 const float aT = a * T[k];
-                v[5] += aT * w0[k];
-                v[6] += aT * w1[k];
-                v[7] += aT * w2[k];
                 const float cw = c0 * w0[k] + c1 * w1[k] + c2 * w2[k];
                 const float dalpha = T[k] * (cw - P[k]);
                 P[k] = a * cw + om * P[k];
                 // no gradient where the pixel skipped the entry or alpha was clamped
                 const float g = (!ok || rG > 0.99f) ? 0.0f : G * dalpha;
                 const float gx = g * dx, gy = g * dy;
-                e += g;
-                v[0] += gx;
-                v[1] += gy;
-                v[2] = fmaf(gx, dx, v[2]);
-                v[3] = fmaf(gx, dy, v[3]);
-                v[4] = fmaf(gy, dy, v[4]);
+                const float t[8] = {gx, gy, gx * dx, gx * dy, gy * dy, aT * w0[k], aT * w1[k], aT * w2[k]};
+#pragma unroll
+                for (int q = 0; q < 8; q++) v[q] = k == 0 ? t[q] : v[q] + t[q];
+                e = k == 0 ? g : e + g;
             }
             if (__any_sync(VKS_FULL_MASK, contrib)) {
                 const float r = warp_reduce_8plus1(v, e, lane);
@@ -446,7 +444,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 const float nrho = -B.y;
                 const float cr = fmaf(nrho, fmaf(kA, 2.0f * A.z, fmaf(kC, 2.0f * B.x, kH)), kOne);
                 const float out = myterm == 8 ? e : fmaf(cr, r, (nrho * kB * A.w) * other);
-                if (myterm >= 0) atomicAdd(tbase + (size_t)s.id[j] * tstride, out);
+                if (myterm >= 0) atomicAdd(tbase + (size_t)__float_as_uint(Cc.y) * tstride, out);
             }
         }
     }

@@ -67,10 +67,13 @@ __device__ __forceinline__ void stage_in(const float* __restrict__ src, int64_t 
     if constexpr (Lay::kVec) {
         constexpr int V = Lay::S / 4;
         const float4* s4 = reinterpret_cast<const float4*>(src) + g0 * V;
+        int r = (int)lane / V, c = (int)lane - r * V;  // chunk lane + 32 it: row / column, incremental
 #pragma unroll 4
-        for (int j = lane; j < 32 * V; j += 32) {
-            const int r = j / V, c = j - r * V;
-            if ((mask >> r) & 1u) *reinterpret_cast<float4*>(buf + r * Lay::SP + 4 * c) = __ldg(s4 + j);
+        for (int it = 0; it < V; it++) {
+            if ((mask >> r) & 1u) *reinterpret_cast<float4*>(buf + r * Lay::SP + 4 * c) = __ldg(s4 + (lane + 32 * it));
+            c += 32 % V;
+            r += 32 / V;
+            if (c >= V) { c -= V; r += 1; }
         }
     } else {
         const float* s1 = src + g0 * Lay::S;
@@ -88,10 +91,13 @@ __device__ __forceinline__ void stage_in_async(const float* __restrict__ src, in
     if constexpr (Lay::kVec) {
         constexpr int V = Lay::S / 4;
         const float4* s4 = reinterpret_cast<const float4*>(src) + g0 * V;
+        int r = (int)lane / V, c = (int)lane - r * V;
 #pragma unroll 4
-        for (int j = lane; j < 32 * V; j += 32) {
-            const int r = j / V, c = j - r * V;
-            if ((mask >> r) & 1u) cp_async16(buf + r * Lay::SP + 4 * c, s4 + j);
+        for (int it = 0; it < V; it++) {
+            if ((mask >> r) & 1u) cp_async16(buf + r * Lay::SP + 4 * c, s4 + (lane + 32 * it));
+            c += 32 % V;
+            r += 32 / V;
+            if (c >= V) { c -= V; r += 1; }
         }
     } else {
         const float* s1 = src + g0 * Lay::S;
@@ -110,10 +116,13 @@ __device__ __forceinline__ void stage_out(float* __restrict__ dst, int64_t g0, u
     if constexpr (Lay::kVec) {
         constexpr int V = Lay::S / 4;
         float4* d4 = reinterpret_cast<float4*>(dst) + g0 * V;
+        int r = (int)lane / V, c = (int)lane - r * V;
 #pragma unroll 4
-        for (int j = lane; j < 32 * V; j += 32) {
-            const int r = j / V, c = j - r * V;
-            if ((mask >> r) & 1u) d4[j] = *reinterpret_cast<const float4*>(buf + r * Lay::SP + 4 * c);
+        for (int it = 0; it < V; it++) {
+            if ((mask >> r) & 1u) d4[lane + 32 * it] = *reinterpret_cast<const float4*>(buf + r * Lay::SP + 4 * c);
+            c += 32 % V;
+            r += 32 / V;
+            if (c >= V) { c -= V; r += 1; }
         }
     } else {
         float* d1 = dst + g0 * Lay::S;

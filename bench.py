@@ -126,6 +126,19 @@ def raster_flops(visited, composited, replayed):
     return dict(raster_fwd=12 * visited + 9 * composited, raster_bwd=12 * replayed + 50 * composited)
 
 
+def measured_traffic(stage):
+    """DRAM bytes (read + write) per launch of the stage's dominant kernel from the committed
+    `ncu --set full` capture (profiles/r1_traffic.json, written by tools/traffic_from_ncu.py), or
+    None when no capture of that kernel is committed."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t["kernels"][stage]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 # ----------------------------------------------------------------------------------- ours
 def run_ours(args):
     import numpy as np
@@ -256,7 +269,7 @@ def run_ours(args):
     dom = max((k for k in per_stage), key=lambda k: per_stage[k]["ms"])
     d = per_stage[dom]
     roofline = dict(kernel=dom, bound=d["bound"], achieved=round(d["achieved"], 3), peak=round(d["peak"], 3),
-                    unit=d["unit"], frac=round(d["frac"], 4), traffic=None,
+                    unit=d["unit"], frac=round(d["frac"], 4), traffic=measured_traffic(dom),
                     peak_source=(pk["src"] + (" HBM copy (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
                                               f" FP32 FMA: 148 SM x 128 lanes x 2 flop x {clock_mhz:.0f} MHz")))
     tp = 2 if rend.n_tiles > 256 else 1

@@ -46,6 +46,8 @@ typedef uint32_t u32;
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kDownThreads = 512;  // the down-sweeps: same 4096-element tiles, 8 items per thread
+constexpr int kDownItems = kScanTile / kDownThreads;
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
@@ -172,13 +174,14 @@ __device__ __forceinline__ int rect_tiles(u64 c) {
 // Warp-striped layout: warp w of a block owns the 512 consecutive elements starting at
 // blockIdx.x * kScanTile + 512 w; lane l holds elements 32 j + l (j < 16), so every load and store
 // instruction of a warp touches 32 consecutive elements.
-__device__ __forceinline__ u64 warp_base(int warp) { return (u64)blockIdx.x * kScanTile + (u64)warp * 32 * kScanItems; }
+template <int ITEMS = kScanItems>
+__device__ __forceinline__ u64 warp_base(int warp) { return (u64)blockIdx.x * kScanTile + (u64)warp * 32 * ITEMS; }
 
-template <int MODE>
+template <int MODE, int ITEMS = kScanItems>
 __device__ __forceinline__ void load_scan_items(const int* __restrict__ tiles, const u64* __restrict__ rc, u64 count,
-                                                u64 wbase, int lane, int v[kScanItems]) {
+                                                u64 wbase, int lane, int v[ITEMS]) {
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
+    for (int j = 0; j < ITEMS; j++) {
         const u64 i = wbase + 32 * j + lane;
         if (MODE == 0) v[j] = i < count ? max(__ldg(tiles + i), 0) : 0;
         else v[j] = i < count ? rect_tiles(__ldg(rc + i)) : 0;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* __
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int v[kScanItems];
     if (MODE == 1) {  // gather the rect codes into depth order (one random 8-byte read each)
-        const u64 wbase = warp_base(warp);
+        const u64 wbase = warp_base<kScanItems>(warp);
         u32 g[kScanItems];
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* __
             }
         }
     } else {
-        load_scan_items<MODE>(tiles, rc_in, count, warp_base(warp), lane, v);
+        load_scan_items<MODE, kScanItems>(tiles, rc_in, count, warp_base<kScanItems>(warp), lane, v);
     }
     u32 sum = 0, vis = 0;
 #pragma unroll
@@ -290,10 +293,11 @@ __device__ __forceinline__ u32 warp_incl_scan(u32 x, int lane) {
 }
 
 // exclusive scan of the striped items of one warp: out[j] = warp-local exclusive prefix of v[j]
-__device__ __forceinline__ u32 warp_striped_excl(const int v[kScanItems], u32 out[kScanItems], int lane) {
+template <int ITEMS = kScanItems>
+__device__ __forceinline__ u32 warp_striped_excl(const int v[ITEMS], u32 out[ITEMS], int lane) {
     u32 carry = 0;
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
+    for (int j = 0; j < ITEMS; j++) {
         const u32 incl = warp_incl_scan((u32)v[j], lane);
         out[j] = carry + incl - (u32)v[j];
         carry += __shfl_sync(VKS_FULL_MASK, incl, 31);
@@ -322,29 +326,30 @@ struct CompactOut {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const int* __restrict__ tiles, const u64* __restrict__ rc,
+__global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __restrict__ tiles, const u64* __restrict__ rc,
                                                                 u64 count, const u32* __restrict__ part_prefix,
                                                                 u32* __restrict__ out, const CompactOut co) {
-    __shared__ u32 s_w[kScanThreads / 32], s_v[kScanThreads / 32];
+    constexpr int ITEMS = kDownItems;
+    __shared__ u32 s_w[kDownThreads / 32], s_v[kDownThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const u64 wbase = warp_base(warp);
-    int v[kScanItems];
-    u32 ex[kScanItems];
-    load_scan_items<MODE>(tiles, rc, count, wbase, lane, v);
-    const u32 wtot = warp_striped_excl(v, ex, lane);
+    const u64 wbase = warp_base<ITEMS>(warp);
+    int v[ITEMS];
+    u32 ex[ITEMS];
+    load_scan_items<MODE, ITEMS>(tiles, rc, count, wbase, lane, v);
+    const u32 wtot = warp_striped_excl<ITEMS>(v, ex, lane);
     u32 wvis = 0;
     if (MODE == 0) {
 #pragma unroll
-        for (int j = 0; j < kScanItems; j++) wvis += __popc(__ballot_sync(VKS_FULL_MASK, v[j] > 0));
+        for (int j = 0; j < ITEMS; j++) wvis += __popc(__ballot_sync(VKS_FULL_MASK, v[j] > 0));
     }
     if (lane == 0) { s_w[warp] = wtot; s_v[warp] = wvis; }
     __syncthreads();
     u32 pre = part_prefix[blockIdx.x], vpre = MODE == 0 ? co.vis_prefix[blockIdx.x] : 0u;
 #pragma unroll
-    for (int w = 0; w < kScanThreads / 32; w++)
+    for (int w = 0; w < kDownThreads / 32; w++)
         if (w < warp) { pre += s_w[w]; vpre += s_v[w]; }
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
+    for (int j = 0; j < ITEMS; j++) {
         const u64 i = wbase + 32 * j + lane;
         if (i < count) {
             out[i] = pre + ex[j];
@@ -363,7 +368,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const int* __re
         const int2* __restrict__ radii = co.radii;
         // two halves of 8 rows: all loads of a half in flight before its stores
 #pragma unroll
-        for (int h = 0; h < kScanItems; h += 8) {
+        for (int h = 0; h < ITEMS; h += 8) {
             u32 db[8];
             float2 m[8];
             int2 r[8];
@@ -1229,7 +1234,7 @@ int run_scan(const int* tiles, const u64* rc_in, u64 count, u32* part_sum, u32* 
                                                        co.sid, co.rc_by_id, co.rc_out);
     scan_partials_kernel<<<1, 1024, 0, s>>>(part_sum, MODE == 0 ? part_vis : nullptr, P, totals);
     co.vis_prefix = part_vis;
-    scan_down_kernel<MODE><<<P, kScanThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co);
+    scan_down_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co);
     return check_launch(__func__);
 }
 

@@ -1,0 +1,43 @@
+"""Write profiles/r1_traffic.json: DRAM bytes (read + write) per launch of each hot-path stage's
+dominant kernel, from one `ncu --set full` capture (bench.py reports it as roofline.traffic).
+usage: traffic_from_ncu.py report.ncu-rep [out.json]"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+STAGES = {  # bench stage -> kernel-name regex of its dominant kernel
+    "raster_bwd": r"raster_bwd_kernel",
+    "raster_fwd": r"raster_fwd_kernel",
+    "project_fwd": r"project_fwd_kernel",
+    "project_bwd": r"project_bwd_kernel",
+}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def main():
+    rep = sys.argv[1]
+    out = sys.argv[2] if len(sys.argv) > 2 else "profiles/r1_traffic.json"
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    h, units = rows[0], rows[1]
+    res = {}
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")]
+        for stage, rx in STAGES.items():
+            if re.search(rx, name) and stage not in res:
+                rd = float(r[h.index("dram__bytes_read.sum")]) * SCALE[units[h.index("dram__bytes_read.sum")]]
+                wr = float(r[h.index("dram__bytes_write.sum")]) * SCALE[units[h.index("dram__bytes_write.sum")]]
+                res[stage] = dict(kernel=re.sub(r"\(.*", "", name), dram_bytes_read=rd, dram_bytes_write=wr,
+                                  dram_bytes_per_launch=rd + wr)
+    json.dump(dict(source=rep.split("/")[-1], note="one ncu --set full capture of tools/profile_step.py "
+                   "(bicycle, view 0); per launch", kernels=res), open(out, "w"), indent=1)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()

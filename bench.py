@@ -34,11 +34,12 @@ METRIC = "fwd+bwd rasterize iters/sec @5.8M Gaussians 1237x822; sort Gkeys/s; HB
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="bicycle")
-    ap.add_argument("--views-per-rank", type=int, default=1)
+    ap.add_argument("--views-per-rank", type=int, default=8, help="views per rank per step (the batch)")
+    ap.add_argument("--streams", type=int, default=2, help="views in flight per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows-every", type=int, default=8, help="oracle raster sample: every k-th tile row")
@@ -141,7 +142,6 @@ def measured_traffic(stage):
 
 # ----------------------------------------------------------------------------------- ours
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -164,89 +164,150 @@ def run_ours(args):
     params = P.GaussianParams.from_host(scene)
     del scene
     n = params.n
-    vpr = args.views_per_rank
-    my_views = [(rank + world * j) % 8 for j in range(8)]
-    dLs = {v: torch.from_numpy(synth.upstream_grad(c.height, c.width, c.seed + 1000 + v)).cuda()
-           for v in set(my_views)}
-    rend = P.ViewRenderer(n, c.width, c.height)
-    for v in set(my_views):  # size the key capacity once (untimed)
-        rend.forward(cfg, cams[v], params)
-    rend._alloc_capacity(int(rend.capacity * 1.1))
-    stream = torch.cuda.current_stream()
+    B, S = args.views_per_rank, max(1, args.streams)
+    my_views = [(rank + world * j) % 8 for j in range(8)]  # rank r renders ring views r, r + N, ...
+    host_dL = {v: torch.from_numpy(synth.upstream_grad(c.height, c.width, c.seed + 1000 + v)) for v in set(my_views)}
+    dLs = {v: t.cuda() for v, t in host_dL.items()}
+    rends = [P.ViewRenderer(n, c.width, c.height) for _ in range(S)]
+    for r in rends:  # size the key capacity once (untimed)
+        for v in set(my_views):
+            r.forward(cfg, cams[v], params)
+        r._alloc_capacity(int(r.capacity * 1.1))
+    main = torch.cuda.current_stream()
+    streams = [torch.cuda.Stream() for _ in range(S)]
     cfg_ow = dict(cfg, flags=P.FLAG_GRAD_OVERWRITE)
     # stage boundaries (CUDA events on the launching stream); zero_2d is the caller's clear of
     # the 2D-gradient accumulators that raster_bwd adds into (a torch fill, not one of ours)
-    stages = ["project_fwd", "bin_sort", "raster_fwd", "zero_2d", "raster_bwd", "project_bwd", "allreduce"]
+    stages = ["project_fwd", "bin_sort", "raster_fwd", "zero_2d", "raster_bwd", "project_bwd"]
 
-    def step(s, ev=None):
-        for j in range(vpr):
-            v = my_views[(s * vpr + j) % len(my_views)]
-            cam = cams[v]
-            if ev is not None: ev[0].record(stream)
+    copy_stream = torch.cuda.Stream()
+
+    def view_path(rend, cam, dL, first, pb_wait, st, ev=None, copies=None):
+        """One view through the five entry points on stream `st`.  The parameter-gradient rows are
+        read-modify-written by project_bwd, so consecutive views' project_bwd are ordered by
+        `pb_wait`; everything else of two views runs concurrently on their own streams.
+        copies = (host dL, slot): the e2e variant's per-view transfers, on a copy stream that
+        overlaps them with compute — dL/dimage in from pinned host memory (needed by raster_bwd),
+        the rendered image out to pinned host memory (after raster_fwd)."""
+        if copies is not None:
+            host_src, slot = copies
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(slot["dL_free"])      # the slot's previous raster_bwd is done
+                slot["dL"].copy_(host_src, non_blocking=True)
+                slot["dL_ready"].record(copy_stream)
+            dL = slot["dL"]
+        with torch.cuda.stream(st):
+            if copies is not None:
+                st.wait_event(slot["img_free"])              # the previous image has left rend.image
+            if ev is not None: ev[0].record(st)
             P.vks_project_fwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
                               params.sh, rend.means2d, rend.conics, rend.depths, rend.radii, rend.tiles,
                               rend.colors, rend.opacities)
-            if ev is not None: ev[1].record(stream)
+            if ev is not None: ev[1].record(st)
             m = P.vks_bin_sort(cam, rend.means2d, rend.radii, rend.depths, rend.tiles, rend.offsets, None,
                                rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
             rend.num_isects = m
-            if ev is not None: ev[2].record(stream)
+            if ev is not None: ev[2].record(st)
             P.vks_raster_fwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals,
                              rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib, tile_order=rend.tile_order)
-            if ev is not None: ev[3].record(stream)
+            if copies is not None:
+                slot["img_done"].record(st)
+                with torch.cuda.stream(copy_stream):
+                    copy_stream.wait_event(slot["img_done"])
+                    slot["img_host"].copy_(rend.image, non_blocking=True)
+                    slot["img_free"].record(copy_stream)
+                st.wait_event(slot["dL_ready"])
+            if ev is not None: ev[3].record(st)
             rend.g2d.zero_()
-            if ev is not None: ev[4].record(stream)
+            if ev is not None: ev[4].record(st)
             P.vks_raster_bwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals,
-                             rend.tile_offsets, rend.T_final, rend.n_contrib, dLs[v], rend.dmeans2d, rend.dconics,
+                             rend.tile_offsets, rend.T_final, rend.n_contrib, dL, rend.dmeans2d, rend.dconics,
                              rend.dcolors, rend.dopacities, tile_order=rend.tile_order)
-            if ev is not None: ev[5].record(stream)
+            if ev is not None: ev[5].record(st)
+            if copies is not None:
+                slot["dL_free"].record(st)
+            if pb_wait is not None:
+                st.wait_event(pb_wait)
             g = params.grads()
-            # first view of the step overwrites the gradient buffer (no memset), later ones accumulate
-            P.vks_project_bwd(cfg_ow if j == 0 else cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
-                              params.sh, rend.colors, rend.radii, rend.dmeans2d, rend.dconics, rend.dcolors, rend.dopacities,
-                              g["dmeans"], g["dlog_scales"], g["dquats"], g["dopacity_logits"], g["dsh"])
-            if ev is not None: ev[6].record(stream)
-        allreduce_grads(params.grad_flat)  # row a9: the only exchange (no-op at N = 1)
-        if ev is not None: ev[7].record(stream)
+            # the step's first view overwrites the gradient buffer (no memset), later ones accumulate
+            P.vks_project_bwd(cfg_ow if first else cfg, cam, params.means, params.log_scales, params.quats,
+                              params.opacity_logits, params.sh, rend.colors, rend.radii, rend.dmeans2d, rend.dconics,
+                              rend.dcolors, rend.dopacities, g["dmeans"], g["dlog_scales"], g["dquats"],
+                              g["dopacity_logits"], g["dsh"])
+            if ev is not None: ev[6].record(st)
+            done = torch.cuda.Event()
+            done.record(st)
+        return m, done
+
+    def step(s, copies=None):
+        """One training step's hot path: a batch of B views per rank, alternating over S streams,
+        gradients accumulated into one buffer, then the allreduce (row a9; no-op at N = 1).  The
+        batch starts after the previous step's allreduce (an optimizer would run there)."""
+        start = torch.cuda.Event()
+        start.record(main)
+        for st in streams:
+            st.wait_event(start)
+        prev = None
+        m = 0
+        for j in range(B):
+            v = my_views[(s * B + j) % len(my_views)]
+            k = j % S
+            cp = None if copies is None else (copies[0][v], copies[1][k])
+            m, prev = view_path(rends[k], cams[v], dLs[v], j == 0, prev, streams[k], copies=cp)
+        main.wait_event(prev)  # the chain of project_bwd events covers every view of the batch
+        if copies is not None:
+            main.wait_stream(copy_stream)  # every image of the batch has reached the host
+        allreduce_grads(params.grad_flat)
         return m
+
+    def timed(fn, nsteps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(main)
+        for s in range(nsteps):
+            fn(args.warmup + s)
+        t1.record(main)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = t0.elapsed_time(t1)
+        if world > 1:
+            tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms
 
     for s in range(args.warmup):
         step(s)
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(args.steps)]
     clocks = ClockSampler(local)
     clocks.start()
-    Ms = []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for s in range(args.steps):
-        Ms.append(step(args.warmup + s, evs[s]))
-    t1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    elapsed_ms = timed(step, args.steps)
     clk = clocks.stop()
-    elapsed_ms = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(tt.item())
-    # per-stage medians (ms) over the timed steps (vpr == 1: one view per step)
-    st_ms = {name: statistics.median([evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)])
-             for i, name in enumerate(stages)}
-    views_total = world * vpr * args.steps
+    views_total = world * B * args.steps
     value = views_total / (elapsed_ms / 1e3)
 
-    # --- workload statistics (untimed): visible count, M, raster pair counts of the last view
+    # --- per-stage breakdown (its own timed region): views one at a time on one stream, CUDA
+    # events between the entry points; medians over the views
+    nv = max(8, min(64, args.steps))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(nv)]
     torch.cuda.synchronize()
+    for i in range(nv):
+        v = my_views[i % len(my_views)]
+        view_path(rends[0], cams[v], dLs[v], True, None, main, ev=evs[i])
+    torch.cuda.synchronize()
+    st_ms = {name: statistics.median([evs[i][q].elapsed_time(evs[i][q + 1]) for i in range(nv)])
+             for q, name in enumerate(stages)}
+    rend = rends[0]
+
+    # --- workload statistics (untimed): visible count, M, raster pair counts of the last view
     vis = int((rend.tiles > 0).sum().item())
     m_last = rend.num_isects
     stats = torch.zeros(6, dtype=torch.int64, device="cuda")
-    P.vks_raster_fwd_stats(cfg, cams[my_views[(args.warmup + args.steps - 1) % len(my_views)]], rend.means2d,
+    P.vks_raster_fwd_stats(cfg, cams[my_views[(nv - 1) % len(my_views)]], rend.means2d,
                            rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals, rend.tile_offsets, stats)
     visited, composited, evaluated, replayed, warp_entries, warp_entries_comp = (int(x) for x in stats.tolist())
     # depth passes the sort ran: <= 8-bit digits over the visible depth-bit range (DESIGN.md §6.1)
@@ -281,16 +342,18 @@ def run_ours(args):
     # + depth-order scan (3) + rect diff + tile count + tile passes x 3; raster fwd; raster bwd;
     # project bwd
     tp = max(1, ((rend.n_tiles - 1).bit_length() + 7) // 8)
-    gpu_launches = (1 + (3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1 + 1) * vpr * args.steps
+    gpu_launches = (1 + (3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1 + 1) * B * args.steps
 
     out = dict(metric=METRIC, value=round(value, 3), unit="iters/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(elapsed_ms / args.steps, 4), higher_is_better=True,
                scaling="weak", vs_baseline=None, dtype="f32", data="synthetic",
                config=dict(workload=c.description + ", fwd+bwd", n_gaussians=n, width=c.width,
-                           height=c.height, sh_degree=3, footprint="support", views_per_rank=vpr,
-                           visible=vis, num_isects=m_last,
+                           height=c.height, sh_degree=3, footprint="support", views_per_rank_per_step=B,
+                           streams=S, visible=vis, num_isects=m_last,
                            l2="inputs larger than L2 (params 1.37 GB, keys+vals 0.22 GB per view), no flush",
-                           parallelism=f"view-sharded dp{world}"),
+                           parallelism=f"view-sharded dp{world}",
+                           step=(f"{B} ring views per rank through all five entry points (two in flight on "
+                                 f"{S} streams), gradients accumulated, then one allreduce; unit = views")),
                stages_ms={k: round(v, 4) for k, v in st_ms.items()},
                stage_roofline={k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                                for k, v in per_stage.items()},
@@ -302,7 +365,27 @@ def run_ours(args):
                roofline=roofline, gpu_launches=gpu_launches, clocks=clk)
 
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, P, params, rend, cams, my_views, cfg, c, world)
+        # the same steps with HOST buffers: each view's dL/dimage copied in from pinned host
+        # memory and its rendered image copied out to pinned host memory, on the view's stream
+        pinned = {v: t.pin_memory() for v, t in host_dL.items()}
+        slots = []
+        for _ in range(S):
+            sl = dict(dL=torch.empty(c.height, c.width, 3, device="cuda"),
+                      img_host=torch.empty(c.height, c.width, 3, pin_memory=True))
+            for e in ("dL_free", "dL_ready", "img_done", "img_free"):
+                sl[e] = torch.cuda.Event()
+                sl[e].record(main)
+            slots.append(sl)
+        copies = (pinned, slots)
+        for s in range(min(args.warmup, 3)):
+            step(s, copies)
+        ms = timed(lambda s: step(s, copies), args.steps)
+        nbytes = c.height * c.width * 3 * 4
+        out["e2e"] = dict(value=round(world * B * args.steps / (ms / 1e3), 3), unit="iters/s",
+                          h2d_bytes_per_step=B * nbytes, d2h_bytes_per_step=B * nbytes,
+                          ms_per_step=round(ms / args.steps, 4),
+                          note=("per view: dL/dimage in from pinned host memory and the rendered image out to "
+                                "pinned host memory, on a copy stream overlapping compute, inside the timed region"))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, c, cfg)
     if world > 1:
@@ -310,82 +393,6 @@ def run_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out), flush=True)
-
-
-def run_e2e(args, P, params, rend, cams, my_views, cfg, c, world):
-    """Same step through the public API with HOST buffers: every step copies that view's dL/dimage
-    in from pinned host memory and the rendered image back out, inside the timed region.  The copies
-    run on a second stream, double-buffered, so they overlap the hot path (the asynchronous
-    transfer the paper suggests for its "Copy Image to Device" stage)."""
-    import torch
-
-    import synth
-    from paper_2605_00219_b200.shard import allreduce_grads
-    main = torch.cuda.current_stream()
-    copy = torch.cuda.Stream()
-    host_dL = {v: torch.from_numpy(synth.upstream_grad(c.height, c.width, c.seed + 1000 + v)).pin_memory()
-               for v in set(my_views)}
-    dev_dL = [torch.empty(c.height, c.width, 3, device="cuda") for _ in range(2)]
-    host_img = [torch.empty(c.height, c.width, 3, pin_memory=True) for _ in range(2)]
-    dev_img = [torch.empty(c.height, c.width, 3, device="cuda") for _ in range(2)]
-    up_done = [torch.cuda.Event() for _ in range(2)]
-    img_ready = [torch.cuda.Event() for _ in range(2)]
-    down_done = [torch.cuda.Event() for _ in range(2)]
-    bwd_done = [torch.cuda.Event() for _ in range(2)]
-    started = set()
-
-    def upload(s):
-        v = my_views[s % len(my_views)]
-        with torch.cuda.stream(copy):
-            if s - 2 in started:
-                copy.wait_event(bwd_done[s % 2])  # the backward of step s-2 has consumed this buffer
-            dev_dL[s % 2].copy_(host_dL[v], non_blocking=True)
-            up_done[s % 2].record(copy)
-
-    def step(s):
-        v = my_views[s % len(my_views)]
-        started.add(s)
-        upload(s + 1)                       # next view's input streams in during this step
-        main.wait_event(up_done[s % 2])
-        rend.forward(cfg, cams[v], params)
-        if s - 2 in started:
-            main.wait_event(down_done[s % 2])  # step s-2's image has left this buffer
-        dev_img[s % 2].copy_(rend.image)    # device-side snapshot; the D2H overlaps the backward
-        img_ready[s % 2].record(main)
-        with torch.cuda.stream(copy):
-            copy.wait_event(img_ready[s % 2])
-            host_img[s % 2].copy_(dev_img[s % 2], non_blocking=True)
-            down_done[s % 2].record(copy)
-        rend.backward(cfg, cams[v], params, dev_dL[s % 2], accumulate=False)
-        bwd_done[s % 2].record(main)
-        allreduce_grads(params.grad_flat)
-
-    upload(0)
-    for s in range(min(args.warmup, 3)):
-        step(s)
-    torch.cuda.synchronize()
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    base = min(args.warmup, 3)  # step base's input was uploaded by the previous step (or above)
-    t0.record(main)
-    for s in range(args.steps):
-        step(base + s)
-    main.wait_stream(copy)                  # the last image has reached the host
-    t1.record(main)
-    torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    nbytes = c.height * c.width * 3 * 4
-    return dict(value=round(world * args.steps / (ms / 1e3), 3), unit="iters/s", h2d_bytes_per_step=nbytes,
-                d2h_bytes_per_step=nbytes, ms_per_step=round(ms / args.steps, 4),
-                note="pinned host dL/dimage in and rendered image out every step, on a copy stream overlapping compute")
 
 
 # ----------------------------------------------------------------------------------- oracle (CPU)

@@ -155,6 +155,26 @@ def test_bicycle_sampled(oracle_lib):
     run_case(oracle_lib, "bicycle", scene, cam, synth.default_render_config(), dL, row_mask=sampled_rows(cam))
 
 
+def test_garden_sampled_other_view(oracle_lib):
+    """Garden-shaped 5.0M @ 1297x840, a different ring view (3), sampled rows."""
+    c = synth.CONFIGS["garden"]
+    scene = synth.make_scene(c.n, c.kind, c.seed)
+    cam = synth.ring_cameras(c.width, c.height, c.kind, 8)[3]
+    dL = synth.upstream_grad(c.height, c.width, c.seed + 1003)
+    run_case(oracle_lib, "garden_v3", scene, cam, synth.default_render_config(), dL, row_mask=sampled_rows(cam, 16))
+
+
+@pytest.mark.slow
+def test_stress_20m_sampled(oracle_lib):
+    """Stress config (BASELINE.json configs[4]): 20M Gaussians @ 2474x1644 — projection and binning
+    bit-exact in full, raster and gradients on every 32nd tile row."""
+    c = synth.CONFIGS["stress"]
+    scene = synth.make_scene(c.n, c.kind, c.seed)
+    cam = synth.ring_cameras(c.width, c.height, c.kind, 8)[0]
+    dL = synth.upstream_grad(c.height, c.width, c.seed + 1000)
+    run_case(oracle_lib, "stress", scene, cam, synth.default_render_config(), dL, row_mask=sampled_rows(cam, 32))
+
+
 # ------------------------------------------------------------------ edge cases
 
 def test_ragged_sizes_and_3sigma(oracle_lib):

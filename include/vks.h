@@ -104,8 +104,9 @@ const char* vks_last_cuda_error(void);
  *   -> means2d [n,2], conics [n,3], depths [n], radii [n,2] int32,
  *      tiles_touched [n] int32, colors [n,3], opacities [n]
  * Rows with tiles_touched == 0 (culled / off-image) have radii = (0,0); their
- * other outputs are left unwritten.  fp32, operation order pinned (bit-exact
- * with the oracle's O1).
+ * other outputs are unspecified (currently written as zeros: whole-row stores keep
+ * every DRAM sector fully written, which avoids read-modify-write fills).  fp32,
+ * operation order pinned (bit-exact with the oracle's O1).
  */
 int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                     const float* means, const float* log_scales, const float* quats,

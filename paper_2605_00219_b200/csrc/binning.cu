@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
                 const u64 i = wbase + 32 * (h + q) + lane;
                 const bool vis = v[h + q] > 0;
                 const u32 bal = __ballot_sync(VKS_FULL_MASK, vis);
+                if (i < count && !vis) co.rc_by_id[i] = 0ull;  // whole sectors written (no DRAM fill)
                 if (vis) {
                     const u32 slot = vpre + __popc(bal & ltmask);
                     int x0, x1, y0, y1;
@@ -848,7 +849,7 @@ __device__ __forceinline__ void rank_and_store(SortSmem<1 << DBITS>& S, u32 n, i
 }
 
 template <int DBITS, int MODE>
-__global__ void __launch_bounds__(kSortThreads) scatter_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
+__global__ void __launch_bounds__(kSortThreads, 5) scatter_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
                                                              u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
                                                              int shift, u32 kbias, u32 T, const u32* __restrict__ offs,
                                                              const float* __restrict__ depths,
@@ -918,10 +919,12 @@ __device__ __forceinline__ int div_floor(int k, int w) {
 }
 
 // f(slot, tile, id) for every key slot in [c0, c1) (c1 - c0 <= 512, all inside block b), one
-// slot per lane per round of 32.  The Gaussian owning slot s is the last one with slot0 <= s:
-// a 32-ary search finds the owner of c0; afterwards each round marks, in one OR-reduced word,
-// the slots of the window where one of the next 32 Gaussians starts, and a lane's owner is the
-// current one plus the number of starts at or before its slot.
+// slot per lane per round of 32.  The Gaussian owning slot s is the last one with slot0 <= s.  A
+// 32-ary search finds the owner of c0; from there the warp takes the chunk's Gaussians in groups
+// of 32 (lane j = one Gaussian, its record loaded one group ahead).  Within a group the keys are
+// contiguous slots; per round the lanes whose first key falls in the 32-slot window set one bit
+// each of an OR-reduced word, and a lane's owner is the last owner before the window plus the
+// number of starts at or before its slot.
 template <class F>
 __device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0, u32 c1, F&& f) {
     const int lane = threadIdx.x & 31;
@@ -937,48 +940,55 @@ __device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0
         lo = nlo;
         if (step == 1) break;
     }
-    u32 cur = lo;
-    u32 a_cur = __ldg(src.slot0 + cur);
-    u64 rc_cur = __ldg(src.rc + cur);
-    u32 id_cur = __ldg(src.sid + cur);
-    const u32 le_mask = 0xFFFFFFFFu >> (31 - lane);  // bits 0..lane
-    for (u32 W = c0; W < c1; W += 32) {
-        const u32 g = cur + 1 + (u32)lane;
-        const bool in = g < src.V;
-        const u32 aj = in ? __ldg(src.slot0 + g) : 0xFFFFFFFFu;
-        const u64 rcj = in ? __ldg(src.rc + g) : 0ull;
-        const u32 idj = in ? __ldg(src.sid + g) : 0u;
-        const u32 d = aj - W;  // >= 0: Gaussian cur owns W
-        const u32 starts = __reduce_or_sync(VKS_FULL_MASK, d < 32u ? (1u << d) : 0u);
-        const int rel = __popc(starts & le_mask);
-        const int srcl = rel > 0 ? rel - 1 : 0;
-        u32 a_o = __shfl_sync(VKS_FULL_MASK, aj, srcl);
-        u64 rc_o = __shfl_sync(VKS_FULL_MASK, rcj, srcl);
-        u32 id_o = __shfl_sync(VKS_FULL_MASK, idj, srcl);
-        if (rel == 0) { a_o = a_cur; rc_o = rc_cur; id_o = id_cur; }
-        const u32 slot = W + (u32)lane;
-        if (slot < c1) {
-            int x0, x1, y0, y1;
-            unpack_rect(rc_o, x0, x1, y0, y1);
-            const int w = x1 - x0;
-            const int k = (int)(slot - a_o);  // index within the rect, rows outer
-            const int ry = div_floor(k, w);
-            f(slot, (u32)((y0 + ry) * src.TX + x0 + (k - ry * w)), id_o);
+    const u32 ltle = 0xFFFFFFFFu >> (31 - lane);  // bits 0..lane
+    u32 g = lo;  // first Gaussian of the current group
+    u32 a_n = 0xFFFFFFFFu, id_n = 0;
+    u64 rc_n = 0;
+    if (g + lane < src.V) {
+        a_n = __ldg(src.slot0 + g + lane);
+        rc_n = __ldg(src.rc + g + lane);
+        id_n = __ldg(src.sid + g + lane);
+    }
+    u32 W = c0;  // next slot to produce
+    while (W < c1) {
+        const u32 a = a_n, id = id_n;  // lane j: Gaussian g + j (a = its first slot; ~0: none)
+        const u64 rc = rc_n;
+        const u32 gn = g + 32;
+        a_n = 0xFFFFFFFFu;  // the next group's records, in flight while this group expands
+        if (gn + lane < src.V) {
+            a_n = __ldg(src.slot0 + gn + lane);
+            rc_n = __ldg(src.rc + gn + lane);
+            id_n = __ldg(src.sid + gn + lane);
         }
-        const int n = __popc(starts);  // the owner of the window's last slot is cur + n
-        if (n > 0) {
-            a_cur = __shfl_sync(VKS_FULL_MASK, aj, n - 1);
-            rc_cur = __shfl_sync(VKS_FULL_MASK, rcj, n - 1);
-            id_cur = __shfl_sync(VKS_FULL_MASK, idj, n - 1);
-            cur += (u32)n;
+        // the group covers slots [W, gend): up to the next group's first slot (or c1)
+        const u32 gend = min(c1, __shfl_sync(VKS_FULL_MASK, a_n, 0));
+        // owner lane of slot W - 1: lane 0 if its Gaussian started before W (only the chunk's
+        // first group), else none (-1: lane 0's start at W is counted in the first window)
+        int base = __shfl_sync(VKS_FULL_MASK, a, 0) < W ? 0 : -1;
+        for (; W < gend; W += 32) {
+            const u32 d = a - W;  // a lane's first key lies in the window when a >= W and d < 32
+            const u32 starts = __reduce_or_sync(VKS_FULL_MASK, (a >= W && d < 32u) ? (1u << d) : 0u);
+            const int own = base + __popc(starts & ltle);
+            const int srcl = own < 0 ? 0 : own;
+            const u32 a_o = __shfl_sync(VKS_FULL_MASK, a, srcl);
+            const u64 rc_o = __shfl_sync(VKS_FULL_MASK, rc, srcl);
+            const u32 id_o = __shfl_sync(VKS_FULL_MASK, id, srcl);
+            const u32 slot = W + (u32)lane;
+            if (slot < gend) {
+                int x0, x1, y0, y1;
+                unpack_rect(rc_o, x0, x1, y0, y1);
+                const int w = x1 - x0;
+                const int k = (int)(slot - a_o);  // index within the rect, rows outer
+                const int ry = div_floor(k, w);
+                f(slot, (u32)((y0 + ry) * src.TX + x0 + (k - ry * w)), id_o);
+            }
+            base += __popc(starts);
         }
+        W = gend;  // the next group starts at its first Gaussian's first slot
+        g = gn;
     }
 }
 
-
-// Digit histogram of the block's keys without enumerating them: a Gaussian's keys within one
-// rect row are consecutive tile ids, so a row of length L adds floor(L / R) to every digit and 1
-// to a cyclic run of L mod R digits (a difference array over the R digits).
 template <int DBITS>
 __global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSrc src, int shift, u32 T,
                                                                  u32* __restrict__ counts) {
@@ -1047,7 +1057,7 @@ __global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSr
 }
 
 template <int DBITS, int MODE>
-__global__ void __launch_bounds__(kSortThreads) keys_scatter_kernel(const ExpandSrc src, int shift, u32 T,
+__global__ void __launch_bounds__(kSortThreads, 5) keys_scatter_kernel(const ExpandSrc src, int shift, u32 T,
                                                                    const u32* __restrict__ offs, u32* __restrict__ kout,
                                                                    u32* __restrict__ vout, const float* __restrict__ depths,
                                                                    u64* __restrict__ keys64) {

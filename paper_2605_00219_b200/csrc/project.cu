@@ -399,9 +399,18 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
         p.colors[3 * i + 1] = col[1];
         p.colors[3 * i + 2] = col[2];
         p.opac[i] = k.rho;
-    } else {
+    } else {  // full rows: partial-sector writes would make L2 fetch the sector from DRAM first
+        p.means2d[i] = make_float2(0.0f, 0.0f);
+        p.conics[3 * i + 0] = 0.0f;
+        p.conics[3 * i + 1] = 0.0f;
+        p.conics[3 * i + 2] = 0.0f;
+        p.depths[i] = 0.0f;
         p.radii[i] = make_int2(0, 0);
         p.tiles[i] = 0;
+        p.colors[3 * i + 0] = 0.0f;
+        p.colors[3 * i + 1] = 0.0f;
+        p.colors[3 * i + 2] = 0.0f;
+        p.opac[i] = 0.0f;
     }
 }
 

@@ -16,6 +16,6 @@ def views_for_rank(rank: int, world: int, n_views: int) -> list[int]:
 
 def allreduce_grads(grad_flat: torch.Tensor, group=None, async_op: bool = False):
     """Sum the flat per-Gaussian gradient buffer over ranks (NCCL on GPUs, gloo on CPU)."""
-    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+    if not dist.is_available() or not dist.is_initialized():
         return None
     return dist.all_reduce(grad_flat, op=dist.ReduceOp.SUM, group=group, async_op=async_op)

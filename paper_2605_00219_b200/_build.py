@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         obj = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [path] + hdrs):
-            cmd = [nvcc(), *ARCH, *COMMON, "-c", path, "-o", obj]
+            cmd = [nvcc(), *ARCH, *COMMON, *os.environ.get("VKS_NVCC_EXTRA", "").split(), "-c", path, "-o", obj]
             if src in PINNED:
                 cmd.insert(1, "-fmad=false")
             if ptxas_v:

@@ -8,9 +8,10 @@
 // Gaussians (16 B/Gaussian per pass) instead of over the M ~ 4.4 N keys, and only the tile bits
 // are sorted over the keys:
 //
-//  1. scan (id order)    reduce-then-scan of tiles_touched -> offsets, M, V; the down-sweep also
-//                         compacts the V visible Gaussians, in id order, into (depth bits, id) and
-//                         writes each one's tile rect as a 64-bit code (4 x u16) at its id.
+//  1. scan (id order)    reduce-then-scan of tiles_touched -> offsets, M, V; the reduce step also
+//                         writes each visible Gaussian's tile rect as a 64-bit code (4 x u16) at
+//                         its id, the down-sweep compacts the V visible ones, in id order, into
+//                         (depth bits, id).
 //  2. radix pass x1-4     LSD passes over the V (depth bits - min, id) pairs, <= 8-bit digits, as
 //                         many as the visible depth-bit range needs (bicycle: 27 bits, 4 x 7).
 //  3. scan (depth order) reduce-then-scan of the rect tile counts; the reduce gathers the rect
@@ -51,7 +52,10 @@ constexpr int kDownItems = kScanTile / kDownThreads;
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
+#ifndef VKS_SORT_ITEMS
+#define VKS_SORT_ITEMS 16
+#endif
+constexpr int kSortItems = VKS_SORT_ITEMS;  // keys per thread of a radix block
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per block
 constexpr int kDepthPasses = 4;  // at most (32 significant depth bits in digits of <= 9 bits)
 constexpr int kMaxRadix = 512;    // digits of <= 9 bits
@@ -188,37 +192,84 @@ __device__ __forceinline__ void load_scan_items(const int* __restrict__ tiles, c
     }
 }
 
+// Extra inputs / outputs of the scans.  MODE 0 (id order): the reduce step writes every visible
+// Gaussian's tile-rect code at its id (rc_by_id); the down-sweep compacts the visible Gaussians,
+// in id order, into (depth bits, id) pairs at their visible index (the input of the depth sort)
+// and reduces the depth-bit range.
+struct CompactOut {
+    const u32* vis_prefix;   // [blocks] exclusive block prefix of the visible counts
+    const u32* depth_bits;   // [n]
+    const float2* means2d;   // [n]
+    const int2* radii;       // [n]
+    int TX, TY;
+    u32* vkeys;              // [V] depth bits, id order
+    u32* vids;               // [V] ids
+    u64* rc_by_id;           // [n] rect codes (visible rows only)
+    u32* dminmax;            // [2] max(~depth bits), max(depth bits) over the visible (zeroed)
+    // MODE 1 (depth order): the reduce step gathers the rect codes of the depth-sorted ids into
+    // rc_out (coalesced), the down-sweep writes first[b] = the Gaussian holding key slot 4096 b
+    const u32* sid;
+    u64* rc_out;
+    u32* first;
+};
+
 template <int MODE>
 __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* __restrict__ tiles,
                                                                   const u64* __restrict__ rc_in, u64 count,
                                                                   u32* __restrict__ part_sum,
-                                                                  u32* __restrict__ part_vis,
-                                                                  const u32* __restrict__ sid,
-                                                                  const u64* __restrict__ rc_by_id,
-                                                                  u64* __restrict__ rc_out) {
+                                                                  u32* __restrict__ part_vis, const CompactOut co) {
     __shared__ u32 s_sum[kScanThreads / 32], s_vis[kScanThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int v[kScanItems];
+    const u64 wbase = warp_base<kScanItems>(warp);
     if (MODE == 1) {  // gather the rect codes into depth order (one random 8-byte read each)
-        const u64 wbase = warp_base<kScanItems>(warp);
         u32 g[kScanItems];
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
             const u64 i = wbase + 32 * j + lane;
-            g[j] = i < count ? __ldg(sid + i) : 0u;
+            g[j] = i < count ? __ldg(co.sid + i) : 0u;
         }
 #pragma unroll
         for (int j = 0; j < kScanItems; j++) {
             const u64 i = wbase + 32 * j + lane;
             v[j] = 0;
             if (i < count) {
-                const u64 c = __ldg(rc_by_id + g[j]);
-                rc_out[i] = c;
+                const u64 c = __ldg(co.rc_by_id + g[j]);
+                co.rc_out[i] = c;
                 v[j] = rect_tiles(c);
             }
         }
     } else {
-        load_scan_items<MODE, kScanItems>(tiles, rc_in, count, warp_base<kScanItems>(warp), lane, v);
+        load_scan_items<MODE, kScanItems>(tiles, rc_in, count, wbase, lane, v);
+        // tile rect code of every visible Gaussian at its id (0 for the others: whole sectors are
+        // written), computed exactly as projection step 11 (this TU is compiled -fmad=false)
+        const float2* __restrict__ means2d = co.means2d;
+        const int2* __restrict__ radii = co.radii;
+#pragma unroll
+        for (int h = 0; h < kScanItems; h += 8) {
+            float2 m[8];
+            int2 r[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const u64 i = wbase + 32 * (h + q) + lane;
+                if (v[h + q] > 0) {
+                    m[q] = __ldg(means2d + i);
+                    r[q] = __ldg(radii + i);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const u64 i = wbase + 32 * (h + q) + lane;
+                if (i >= count) continue;
+                u64 code = 0;
+                if (v[h + q] > 0) {
+                    int x0, x1, y0, y1;
+                    rect_of(m[q], r[q], co.TX, co.TY, x0, x1, y0, y1);
+                    code = pack_rect(x0, x1, y0, y1);
+                }
+                co.rc_by_id[i] = code;
+            }
+        }
     }
     u32 sum = 0, vis = 0;
 #pragma unroll
@@ -305,26 +356,6 @@ __device__ __forceinline__ u32 warp_striped_excl(const int v[ITEMS], u32 out[ITE
     return carry;  // warp total
 }
 
-// MODE 0 additionally compacts the visible Gaussians, in id order, into (depth bits, id) pairs at
-// their visible index (the input of the depth sort) and writes each visible Gaussian's tile-rect
-// code at its id (rc_by_id; gathered once by the last depth pass).
-struct CompactOut {
-    const u32* vis_prefix;   // [blocks] exclusive block prefix of the visible counts
-    const u32* depth_bits;   // [n]
-    const float2* means2d;   // [n]
-    const int2* radii;       // [n]
-    int TX, TY;
-    u32* vkeys;              // [V] depth bits, id order
-    u32* vids;               // [V] ids
-    u64* rc_by_id;           // [n] rect codes (visible rows only)
-    u32* dminmax;            // [2] max(~depth bits), max(depth bits) over the visible (zeroed)
-    // MODE 1 (depth order): the reduce step gathers the rect codes of the depth-sorted ids into
-    // rc_out (coalesced), the down-sweep writes first[b] = the Gaussian holding key slot 4096 b
-    const u32* sid;
-    u64* rc_out;
-    u32* first;
-};
-
 template <int MODE>
 __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __restrict__ tiles, const u64* __restrict__ rc,
                                                                 u64 count, const u32* __restrict__ part_prefix,
@@ -364,41 +395,25 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
         const u32 ltmask = lanemask_lt();
         u32 nmin = 0, dmax = 0;  // max of ~bits (= ~min) and of bits over this thread's visible
         const u32* __restrict__ depth_bits = co.depth_bits;
-        const float2* __restrict__ means2d = co.means2d;
-        const int2* __restrict__ radii = co.radii;
-        // two halves of 8 rows: all loads of a half in flight before its stores
+        u32 db[ITEMS];
 #pragma unroll
-        for (int h = 0; h < ITEMS; h += 8) {
-            u32 db[8];
-            float2 m[8];
-            int2 r[8];
+        for (int q = 0; q < ITEMS; q++) {
+            const u64 i = wbase + 32 * q + lane;
+            if (v[q] > 0) db[q] = __ldg(depth_bits + i);
+        }
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const u64 i = wbase + 32 * (h + q) + lane;
-                if (v[h + q] > 0) {
-                    db[q] = __ldg(depth_bits + i);
-                    m[q] = __ldg(means2d + i);
-                    r[q] = __ldg(radii + i);
-                }
+        for (int q = 0; q < ITEMS; q++) {
+            const u64 i = wbase + 32 * q + lane;
+            const bool vis = v[q] > 0;
+            const u32 bal = __ballot_sync(VKS_FULL_MASK, vis);
+            if (vis) {
+                const u32 slot = vpre + __popc(bal & ltmask);
+                co.vkeys[slot] = db[q];
+                co.vids[slot] = (u32)i;
+                nmin = max(nmin, ~db[q]);
+                dmax = max(dmax, db[q]);
             }
-#pragma unroll
-            for (int q = 0; q < 8; q++) {
-                const u64 i = wbase + 32 * (h + q) + lane;
-                const bool vis = v[h + q] > 0;
-                const u32 bal = __ballot_sync(VKS_FULL_MASK, vis);
-                if (i < count && !vis) co.rc_by_id[i] = 0ull;  // whole sectors written (no DRAM fill)
-                if (vis) {
-                    const u32 slot = vpre + __popc(bal & ltmask);
-                    int x0, x1, y0, y1;
-                    rect_of(m[q], r[q], co.TX, co.TY, x0, x1, y0, y1);
-                    co.vkeys[slot] = db[q];
-                    co.vids[slot] = (u32)i;
-                    co.rc_by_id[i] = pack_rect(x0, x1, y0, y1);
-                    nmin = max(nmin, ~db[q]);
-                    dmax = max(dmax, db[q]);
-                }
-                vpre += __popc(bal);
-            }
+            vpre += __popc(bal);
         }
         nmin = __reduce_max_sync(VKS_FULL_MASK, nmin);
         dmax = __reduce_max_sync(VKS_FULL_MASK, dmax);
@@ -768,7 +783,7 @@ __device__ __forceinline__ void rank_and_store(SortSmem<1 << DBITS>& S, u32 n, i
 #pragma unroll
     for (int i = 0; i < kSortItems; i++) {
         const u32 d = ((S.keys[seg + i * 32 + lane] - kbias) >> shift) & DMASK;
-        const u32 peers = digit_peers<DBITS>(d);
+        const u32 peers = digit_peers<DBITS>(d);  // (match.any measured 17% slower for the whole sort)
         const u32 below = __popc(peers & ltmask);
         const u32 before = S.whist[warp][d];
         rank[i] = before + below;
@@ -1246,7 +1261,7 @@ int run_scan(const int* tiles, const u64* rc_in, u64 count, u32* part_sum, u32* 
     const u32 P = (u32)((count + kScanTile - 1) / kScanTile);
     if (!P) return VKS_OK;
     scan_reduce_kernel<MODE><<<P, kScanThreads, 0, s>>>(tiles, rc_in, count, part_sum, MODE == 0 ? part_vis : nullptr,
-                                                       co.sid, co.rc_by_id, co.rc_out);
+                                                       co);
     scan_partials_kernel<<<1, 1024, 0, s>>>(part_sum, MODE == 0 ? part_vis : nullptr, P, totals);
     co.vis_prefix = part_vis;
     scan_down_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co);

@@ -64,7 +64,21 @@ template <int KS>
 __device__ __forceinline__ void stage_in(const float* __restrict__ src, int64_t g0, unsigned mask, float* buf) {
     using Lay = ShLayout<KS>;
     const unsigned lane = lane_id();
-    if constexpr (Lay::kVec) {
+    if constexpr (Lay::kVec && (Lay::S / 4) % 4 == 0) {
+        // 4 lanes per row (see stage_in_async)
+        constexpr int V = Lay::S / 4, M = V / 4;
+        const float4* s4 = reinterpret_cast<const float4*>(src) + g0 * V + (lane >> 2) * V + (lane & 3);
+        float* d = buf + (lane >> 2) * Lay::SP + 4 * (lane & 3);
+#pragma unroll
+        for (int it = 0; it < 4; it++) {
+            if ((mask >> ((lane >> 2) + 8 * it)) & 1u) {
+#pragma unroll
+                for (int m = 0; m < M; m++) *reinterpret_cast<float4*>(d + 16 * m) = __ldg(s4 + 4 * m);
+            }
+            s4 += 8 * V;
+            d += 8 * Lay::SP;
+        }
+    } else if constexpr (Lay::kVec) {
         constexpr int V = Lay::S / 4;
         const float4* s4 = reinterpret_cast<const float4*>(src) + g0 * V;
         int r = (int)lane / V, c = (int)lane - r * V;  // chunk lane + 32 it: row / column, incremental
@@ -88,7 +102,22 @@ template <int KS>
 __device__ __forceinline__ void stage_in_async(const float* __restrict__ src, int64_t g0, unsigned mask, float* buf) {
     using Lay = ShLayout<KS>;
     const unsigned lane = lane_id();
-    if constexpr (Lay::kVec) {
+    if constexpr (Lay::kVec && (Lay::S / 4) % 4 == 0) {
+        // 4 lanes per row, V/4 float4 each: lane l takes row l/4 + 8 it and columns l%4 + 4 m;
+        // every instruction moves 8 rows x 64 contiguous bytes, addresses advance by constants
+        constexpr int V = Lay::S / 4, M = V / 4;
+        const float4* s4 = reinterpret_cast<const float4*>(src) + g0 * V + (lane >> 2) * V + (lane & 3);
+        uint32_t d = smem_addr(buf) + 4u * ((lane >> 2) * Lay::SP + 4 * (lane & 3));
+#pragma unroll
+        for (int it = 0; it < 4; it++) {
+            if ((mask >> ((lane >> 2) + 8 * it)) & 1u) {
+#pragma unroll
+                for (int m = 0; m < M; m++) cp_async16_s(d + 64u * m, s4 + 4 * m);
+            }
+            s4 += 8 * V;
+            d += 4u * 8 * Lay::SP;
+        }
+    } else if constexpr (Lay::kVec) {
         constexpr int V = Lay::S / 4;
         const float4* s4 = reinterpret_cast<const float4*>(src) + g0 * V;
         int r = (int)lane / V, c = (int)lane - r * V;
@@ -113,7 +142,21 @@ template <int KS>
 __device__ __forceinline__ void stage_out(float* __restrict__ dst, int64_t g0, unsigned mask, const float* buf) {
     using Lay = ShLayout<KS>;
     const unsigned lane = lane_id();
-    if constexpr (Lay::kVec) {
+    if constexpr (Lay::kVec && (Lay::S / 4) % 4 == 0) {
+        // 4 lanes per row (see stage_in_async)
+        constexpr int V = Lay::S / 4, M = V / 4;
+        float4* d4 = reinterpret_cast<float4*>(dst) + g0 * V + (lane >> 2) * V + (lane & 3);
+        const float* sb = buf + (lane >> 2) * Lay::SP + 4 * (lane & 3);
+#pragma unroll
+        for (int it = 0; it < 4; it++) {
+            if ((mask >> ((lane >> 2) + 8 * it)) & 1u) {
+#pragma unroll
+                for (int m = 0; m < M; m++) d4[4 * m] = *reinterpret_cast<const float4*>(sb + 16 * m);
+            }
+            d4 += 8 * V;
+            sb += 8 * Lay::SP;
+        }
+    } else if constexpr (Lay::kVec) {
         constexpr int V = Lay::S / 4;
         float4* d4 = reinterpret_cast<float4*>(dst) + g0 * V;
         int r = (int)lane / V, c = (int)lane - r * V;

@@ -214,23 +214,24 @@ struct CompactOut {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* __restrict__ tiles,
+__global__ void __launch_bounds__(kDownThreads) scan_reduce_kernel(const int* __restrict__ tiles,
                                                                   const u64* __restrict__ rc_in, u64 count,
                                                                   u32* __restrict__ part_sum,
                                                                   u32* __restrict__ part_vis, const CompactOut co) {
-    __shared__ u32 s_sum[kScanThreads / 32], s_vis[kScanThreads / 32];
+    constexpr int ITEMS = kDownItems;
+    __shared__ u32 s_sum[kDownThreads / 32], s_vis[kDownThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int v[kScanItems];
-    const u64 wbase = warp_base<kScanItems>(warp);
+    int v[ITEMS];
+    const u64 wbase = warp_base<ITEMS>(warp);
     if (MODE == 1) {  // gather the rect codes into depth order (one random 8-byte read each)
-        u32 g[kScanItems];
+        u32 g[ITEMS];
 #pragma unroll
-        for (int j = 0; j < kScanItems; j++) {
+        for (int j = 0; j < ITEMS; j++) {
             const u64 i = wbase + 32 * j + lane;
             g[j] = i < count ? __ldg(co.sid + i) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < kScanItems; j++) {
+        for (int j = 0; j < ITEMS; j++) {
             const u64 i = wbase + 32 * j + lane;
             v[j] = 0;
             if (i < count) {
@@ -240,13 +241,13 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* __
             }
         }
     } else {
-        load_scan_items<MODE, kScanItems>(tiles, rc_in, count, wbase, lane, v);
+        load_scan_items<MODE, ITEMS>(tiles, rc_in, count, wbase, lane, v);
         // tile rect code of every visible Gaussian at its id (0 for the others: whole sectors are
         // written), computed exactly as projection step 11 (this TU is compiled -fmad=false)
         const float2* __restrict__ means2d = co.means2d;
         const int2* __restrict__ radii = co.radii;
 #pragma unroll
-        for (int h = 0; h < kScanItems; h += 8) {
+        for (int h = 0; h < ITEMS; h += 8) {
             float2 m[8];
             int2 r[8];
 #pragma unroll
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* __
     }
     u32 sum = 0, vis = 0;
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
+    for (int j = 0; j < ITEMS; j++) {
         sum += (u32)v[j];
         vis += v[j] > 0;
     }
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const int* __
     if (tid == 0) {
         u32 a = 0, b = 0;
 #pragma unroll
-        for (int w = 0; w < kScanThreads / 32; w++) { a += s_sum[w]; b += s_vis[w]; }
+        for (int w = 0; w < kDownThreads / 32; w++) { a += s_sum[w]; b += s_vis[w]; }
         part_sum[blockIdx.x] = a;
         if (part_vis) part_vis[blockIdx.x] = b;
     }
@@ -366,6 +367,12 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
     const u64 wbase = warp_base<ITEMS>(warp);
     int v[ITEMS];
     u32 ex[ITEMS];
+    u32 dbits_pre[ITEMS];  // MODE 0: depth bits loaded with the tile counts (one DRAM round trip)
+#pragma unroll
+    for (int q = 0; q < ITEMS; q++) {
+        const u64 i = wbase + 32 * q + lane;
+        dbits_pre[q] = (MODE == 0 && i < count) ? __ldg(co.depth_bits + i) : 0u;
+    }
     load_scan_items<MODE, ITEMS>(tiles, rc, count, wbase, lane, v);
     const u32 wtot = warp_striped_excl<ITEMS>(v, ex, lane);
     u32 wvis = 0;
@@ -394,13 +401,9 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
     if (MODE == 0) {
         const u32 ltmask = lanemask_lt();
         u32 nmin = 0, dmax = 0;  // max of ~bits (= ~min) and of bits over this thread's visible
-        const u32* __restrict__ depth_bits = co.depth_bits;
         u32 db[ITEMS];
 #pragma unroll
-        for (int q = 0; q < ITEMS; q++) {
-            const u64 i = wbase + 32 * q + lane;
-            if (v[q] > 0) db[q] = __ldg(depth_bits + i);
-        }
+        for (int q = 0; q < ITEMS; q++) db[q] = dbits_pre[q];
 #pragma unroll
         for (int q = 0; q < ITEMS; q++) {
             const u64 i = wbase + 32 * q + lane;
@@ -1260,7 +1263,7 @@ int run_scan(const int* tiles, const u64* rc_in, u64 count, u32* part_sum, u32* 
              CompactOut co, cudaStream_t s) {
     const u32 P = (u32)((count + kScanTile - 1) / kScanTile);
     if (!P) return VKS_OK;
-    scan_reduce_kernel<MODE><<<P, kScanThreads, 0, s>>>(tiles, rc_in, count, part_sum, MODE == 0 ? part_vis : nullptr,
+    scan_reduce_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, MODE == 0 ? part_vis : nullptr,
                                                        co);
     scan_partials_kernel<<<1, 1024, 0, s>>>(part_sum, MODE == 0 ? part_vis : nullptr, P, totals);
     co.vis_prefix = part_vis;

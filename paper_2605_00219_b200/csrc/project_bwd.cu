@@ -142,21 +142,9 @@ template <int KS>
 __device__ __forceinline__ void stage_out(float* __restrict__ dst, int64_t g0, unsigned mask, const float* buf) {
     using Lay = ShLayout<KS>;
     const unsigned lane = lane_id();
-    if constexpr (Lay::kVec && (Lay::S / 4) % 4 == 0) {
-        // 4 lanes per row (see stage_in_async)
-        constexpr int V = Lay::S / 4, M = V / 4;
-        float4* d4 = reinterpret_cast<float4*>(dst) + g0 * V + (lane >> 2) * V + (lane & 3);
-        const float* sb = buf + (lane >> 2) * Lay::SP + 4 * (lane & 3);
-#pragma unroll
-        for (int it = 0; it < 4; it++) {
-            if ((mask >> ((lane >> 2) + 8 * it)) & 1u) {
-#pragma unroll
-                for (int m = 0; m < M; m++) d4[4 * m] = *reinterpret_cast<const float4*>(sb + 16 * m);
-            }
-            d4 += 8 * V;
-            sb += 8 * Lay::SP;
-        }
-    } else if constexpr (Lay::kVec) {
+    if constexpr (Lay::kVec) {
+        // (stores keep 512 contiguous bytes per instruction: the 4-lanes-per-row layout of the
+        // loads made this HBM-bound kernel slower when used for the gradient stores)
         constexpr int V = Lay::S / 4;
         float4* d4 = reinterpret_cast<float4*>(dst) + g0 * V;
         int r = (int)lane / V, c = (int)lane - r * V;

@@ -99,7 +99,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------- algorithmic work
-def algorithmic_bytes(n, vis, m, dpasses=4, K=16):
+def algorithmic_bytes(n, vis, m, dpasses=4, batch=1, K=16):
     """Per-view algorithmic HBM bytes of the HBM-bound stages, for the algorithms as built
     (DESIGN.md §6).  Parameters are fp32; sh has K coefficients per channel."""
     sh = 12 * K
@@ -115,8 +115,10 @@ def algorithmic_bytes(n, vis, m, dpasses=4, K=16):
         # last tile pass (count 4 B, scatter 8 B in, 4 B out per key)
         bin_sort=(12 * n + (20 + 16) * vis + dpasses * 20 * vis + (12 + 8) * vis + (8 + 4) * vis + 8 * vis
                   + 12 * vis + 16 * vis + 8 * m + (4 + 8 + 4) * m),
-        # overwrite semantics: params + 2D grads + colours of visible, radii of all, 236 B written for all
-        project_bwd=8 * n + vis * ((40 + sh) + 36 + 12) + n * (40 + sh),
+        # batched projection backward, per view: the parameter rows (236 B) read and the gradient
+        # rows (236 B) written once per batch of `batch` views (all n rows: upper bound of the
+        # Gaussians some view sees), radii of every row and 2D gradients + colours of the visible
+        project_bwd=(40 + sh) * 2 * n / batch + 8 * n + (36 + 12) * vis,
     )
 
 
@@ -185,13 +187,21 @@ def run_ours(args):
 
     copy_stream = torch.cuda.Stream()
 
-    def view_path(rend, cam, dL, first, pb_wait, st, ev=None, copies=None):
-        """One view through the five entry points on stream `st`.  The parameter-gradient rows are
-        read-modify-written by project_bwd, so consecutive views' project_bwd are ordered by
-        `pb_wait`; everything else of two views runs concurrently on their own streams.
-        copies = (host dL, slot): the e2e variant's per-view transfers, on a copy stream that
-        overlaps them with compute — dL/dimage in from pinned host memory (needed by raster_bwd),
-        the rendered image out to pinned host memory (after raster_fwd)."""
+    # per-view outputs that live until the batch's projection backward: colours and radii of the
+    # projection, the 2D gradients of the raster backward (everything else is per-stream scratch)
+    vbuf = []
+    for _ in range(B):
+        g2d = torch.zeros(9 * n, dtype=torch.float32, device="cuda")
+        vbuf.append(dict(colors=torch.empty(n, 3, device="cuda"),
+                         radii=torch.empty(n, 2, dtype=torch.int32, device="cuda"), g2d=g2d,
+                         dm2=g2d[: 2 * n].view(n, 2), dcon=g2d[2 * n: 5 * n].view(n, 3),
+                         dcol=g2d[5 * n: 8 * n].view(n, 3), dop=g2d[8 * n:]))
+
+    def view_path(rend, vb, cam, dL, st, ev=None, copies=None):
+        """One view's forward and raster backward on stream `st` (two views of a batch run
+        concurrently on their own streams).  copies = (host dL, slot): the e2e variant's per-view
+        transfers, on a copy stream that overlaps them with compute — dL/dimage in from pinned
+        host memory (needed by raster_bwd), the rendered image out to pinned host memory."""
         if copies is not None:
             host_src, slot = copies
             with torch.cuda.stream(copy_stream):
@@ -204,15 +214,16 @@ def run_ours(args):
                 st.wait_event(slot["img_free"])              # the previous image has left rend.image
             if ev is not None: ev[0].record(st)
             P.vks_project_fwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
-                              params.sh, rend.means2d, rend.conics, rend.depths, rend.radii, rend.tiles,
-                              rend.colors, rend.opacities)
+                              params.sh, rend.means2d, rend.conics, rend.depths, vb["radii"], rend.tiles,
+                              vb["colors"], rend.opacities)
             if ev is not None: ev[1].record(st)
-            m = P.vks_bin_sort(cam, rend.means2d, rend.radii, rend.depths, rend.tiles, rend.offsets, None,
+            m = P.vks_bin_sort(cam, rend.means2d, vb["radii"], rend.depths, rend.tiles, rend.offsets, None,
                                rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
             rend.num_isects = m
             if ev is not None: ev[2].record(st)
-            P.vks_raster_fwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals,
-                             rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib, tile_order=rend.tile_order)
+            P.vks_raster_fwd(cfg, cam, rend.means2d, rend.conics, vb["colors"], rend.opacities, vb["radii"],
+                             rend.vals, rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib,
+                             tile_order=rend.tile_order)
             if copies is not None:
                 slot["img_done"].record(st)
                 with torch.cuda.stream(copy_stream):
@@ -221,43 +232,50 @@ def run_ours(args):
                     slot["img_free"].record(copy_stream)
                 st.wait_event(slot["dL_ready"])
             if ev is not None: ev[3].record(st)
-            rend.g2d.zero_()
+            vb["g2d"].zero_()
             if ev is not None: ev[4].record(st)
-            P.vks_raster_bwd(cfg, cam, rend.means2d, rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals,
-                             rend.tile_offsets, rend.T_final, rend.n_contrib, dL, rend.dmeans2d, rend.dconics,
-                             rend.dcolors, rend.dopacities, tile_order=rend.tile_order)
+            P.vks_raster_bwd(cfg, cam, rend.means2d, rend.conics, vb["colors"], rend.opacities, vb["radii"],
+                             rend.vals, rend.tile_offsets, rend.T_final, rend.n_contrib, dL, vb["dm2"], vb["dcon"],
+                             vb["dcol"], vb["dop"], tile_order=rend.tile_order)
             if ev is not None: ev[5].record(st)
             if copies is not None:
                 slot["dL_free"].record(st)
-            if pb_wait is not None:
-                st.wait_event(pb_wait)
-            g = params.grads()
-            # the step's first view overwrites the gradient buffer (no memset), later ones accumulate
-            P.vks_project_bwd(cfg_ow if first else cfg, cam, params.means, params.log_scales, params.quats,
-                              params.opacity_logits, params.sh, rend.colors, rend.radii, rend.dmeans2d, rend.dconics,
-                              rend.dcolors, rend.dopacities, g["dmeans"], g["dlog_scales"], g["dquats"],
-                              g["dopacity_logits"], g["dsh"])
-            if ev is not None: ev[6].record(st)
             done = torch.cuda.Event()
             done.record(st)
         return m, done
 
+    def project_bwd_batch(vcams, st):
+        """The batch's projection backward: one pass over the parameters for all its views,
+        overwriting the gradient buffer (row a8)."""
+        g = params.grads()
+        nb = len(vcams)
+        with torch.cuda.stream(st):
+            P.vks_project_bwd_batch(cfg_ow, vcams, params.means, params.log_scales, params.quats,
+                                    params.opacity_logits, params.sh, [vbuf[j]["colors"] for j in range(nb)],
+                                    [vbuf[j]["radii"] for j in range(nb)], [vbuf[j]["dm2"] for j in range(nb)],
+                                    [vbuf[j]["dcon"] for j in range(nb)], [vbuf[j]["dcol"] for j in range(nb)],
+                                    [vbuf[j]["dop"] for j in range(nb)], g["dmeans"], g["dlog_scales"], g["dquats"],
+                                    g["dopacity_logits"], g["dsh"])
+
     def step(s, copies=None):
-        """One training step's hot path: a batch of B views per rank, alternating over S streams,
-        gradients accumulated into one buffer, then the allreduce (row a9; no-op at N = 1).  The
-        batch starts after the previous step's allreduce (an optimizer would run there)."""
+        """One training step's hot path: a batch of B views per rank, alternating over S streams
+        through projection, binning, raster forward and raster backward; then one batched
+        projection backward for the batch (row a8) and the allreduce (row a9; no-op at N = 1).
+        The batch starts after the previous step's allreduce (an optimizer would run there)."""
         start = torch.cuda.Event()
         start.record(main)
         for st in streams:
             st.wait_event(start)
-        prev = None
         m = 0
+        vcams = []
         for j in range(B):
             v = my_views[(s * B + j) % len(my_views)]
             k = j % S
             cp = None if copies is None else (copies[0][v], copies[1][k])
-            m, prev = view_path(rends[k], cams[v], dLs[v], j == 0, prev, streams[k], copies=cp)
-        main.wait_event(prev)  # the chain of project_bwd events covers every view of the batch
+            m, done = view_path(rends[k], vbuf[j], cams[v], dLs[v], streams[k], copies=cp)
+            main.wait_event(done)
+            vcams.append(cams[v])
+        project_bwd_batch(vcams, main)
         if copies is not None:
             main.wait_stream(copy_stream)  # every image of the batch has reached the host
         allreduce_grads(params.grad_flat)
@@ -295,29 +313,38 @@ def run_ours(args):
 
     # --- per-stage breakdown (its own timed region): views one at a time on one stream, CUDA
     # events between the entry points; medians over the views
-    nv = max(8, min(64, args.steps))
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(nv)]
+    nv = max(B, min(64, (args.steps // B + 1) * B))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages))] for _ in range(nv)]
+    pb_ms = []
     torch.cuda.synchronize()
     for i in range(nv):
         v = my_views[i % len(my_views)]
-        view_path(rends[0], cams[v], dLs[v], True, None, main, ev=evs[i])
+        view_path(rends[0], vbuf[i % B], cams[v], dLs[v], main, ev=evs[i])
+        if i % B == B - 1:  # the batch's projection backward, per view
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(main)
+            project_bwd_batch([cams[my_views[q % len(my_views)]] for q in range(i - B + 1, i + 1)], main)
+            e1.record(main)
+            pb_ms.append((e0, e1))
     torch.cuda.synchronize()
     st_ms = {name: statistics.median([evs[i][q].elapsed_time(evs[i][q + 1]) for i in range(nv)])
-             for q, name in enumerate(stages)}
+             for q, name in enumerate(stages[:-1])}
+    st_ms["project_bwd"] = statistics.median([a.elapsed_time(b) for a, b in pb_ms]) / B
     rend = rends[0]
 
     # --- workload statistics (untimed): visible count, M, raster pair counts of the last view
     vis = int((rend.tiles > 0).sum().item())
     m_last = rend.num_isects
     stats = torch.zeros(6, dtype=torch.int64, device="cuda")
+    vl = vbuf[(nv - 1) % B]  # the last view's colours / radii
     P.vks_raster_fwd_stats(cfg, cams[my_views[(nv - 1) % len(my_views)]], rend.means2d,
-                           rend.conics, rend.colors, rend.opacities, rend.radii, rend.vals, rend.tile_offsets, stats)
+                           rend.conics, vl["colors"], rend.opacities, vl["radii"], rend.vals, rend.tile_offsets, stats)
     visited, composited, evaluated, replayed, warp_entries, warp_entries_comp = (int(x) for x in stats.tolist())
     # depth passes the sort ran: <= 8-bit digits over the visible depth-bit range
     dvis = rend.depths[rend.tiles > 0].view(torch.int32).to(torch.int64)
     drange = int(dvis.max().item() - dvis.min().item()) if dvis.numel() else 0
     dpasses = max(1, (drange.bit_length() + 7) // 8)
-    ab = algorithmic_bytes(n, vis, m_last, dpasses)
+    ab = algorithmic_bytes(n, vis, m_last, dpasses, batch=B)
     fl = raster_flops(visited, composited, replayed)
     pk = peaks()
     clock_mhz = clk["sm_mhz"] or pk["sm_max_mhz"]
@@ -343,9 +370,9 @@ def run_ours(args):
                                               f" FP32 FMA: 148 SM x 128 lanes x 2 flop x {clock_mhz:.0f} MHz")))
     # our kernels per view: project_fwd; bin_sort = id scan (3) + dpasses x (count, scan, scatter)
     # + depth-order scan (3) + rect diff + tile count + tile passes x 3; raster fwd; raster bwd;
-    # project bwd
+    # plus one batched project bwd per step
     tp = max(1, ((rend.n_tiles - 1).bit_length() + 7) // 8)
-    gpu_launches = (1 + (3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1 + 1) * B * args.steps
+    gpu_launches = ((1 + (3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1) * B + 1) * args.steps
 
     out = dict(metric=METRIC, value=round(value, 3), unit="iters/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(elapsed_ms / args.steps, 4), higher_is_better=True,
@@ -355,8 +382,9 @@ def run_ours(args):
                            streams=S, visible=vis, num_isects=m_last,
                            l2="inputs larger than L2 (params 1.37 GB, keys+vals 0.22 GB per view), no flush",
                            parallelism=f"view-sharded dp{world}",
-                           step=(f"{B} ring views per rank through all five entry points (two in flight on "
-                                 f"{S} streams), gradients accumulated, then one allreduce; unit = views")),
+                           step=(f"{B} ring views per rank through projection, binning and both raster passes (two "
+                                 f"in flight on {S} streams), one batched projection backward for the {B} views, "
+                                 f"then one allreduce; unit = views")),
                stages_ms={k: round(v, 4) for k, v in st_ms.items()},
                stage_roofline={k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                                for k, v in per_stage.items()},

@@ -222,6 +222,30 @@ int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                     const float* dopacities, float* dmeans, float* dlog_scales, float* dquats,
                     float* dopacity_logits, float* dsh, vks_stream_t stream);
 
+/*
+ * vks_project_bwd_batch — the projection backward of a batch of views in one pass: the sum over
+ * the views of vks_project_bwd (P:76 projection part; a training step's views share one set of
+ * parameter gradients).  Each view's chain is exactly vks_project_bwd's;
+ * every parameter row and SH row is read once and every gradient row written once, instead of
+ * one read-modify-write of the whole gradient buffer per view.
+ *   n_views in [1, 16] (VKS_ERR_INVALID_ARG otherwise)
+ *   cams: HOST array of n_views cameras
+ *   colors, radii, dmeans2d, dconics, dcolors, dopacities: HOST arrays of n_views DEVICE
+ *     pointers — each view's vks_project_fwd colours / radii and vks_raster_bwd 2D gradients,
+ *     laid out as for vks_project_bwd
+ *   -> dmeans, dlog_scales, dquats, dopacity_logits, dsh as vks_project_bwd, holding the sum
+ *      over the views (+=; with VKS_FLAG_GRAD_OVERWRITE: =, and zero rows for Gaussians no view
+ *      rasterises)
+ */
+int vks_project_bwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,
+                          const float* means, const float* log_scales, const float* quats,
+                          const float* opacity_logits, const float* sh,
+                          const float* const* colors, const int32_t* const* radii,
+                          const float* const* dmeans2d, const float* const* dconics,
+                          const float* const* dcolors, const float* const* dopacities,
+                          float* dmeans, float* dlog_scales, float* dquats, float* dopacity_logits,
+                          float* dsh, vks_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -172,4 +172,34 @@ int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, con
                                                dquats, dopacity_logits, dsh, (cudaStream_t)stream));
 }
 
+int vks_project_bwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,
+                          const float* means, const float* log_scales, const float* quats,
+                          const float* opacity_logits, const float* sh, const float* const* colors,
+                          const int32_t* const* radii, const float* const* dmeans2d, const float* const* dconics,
+                          const float* const* dcolors, const float* const* dopacities, float* dmeans,
+                          float* dlog_scales, float* dquats, float* dopacity_logits, float* dsh,
+                          vks_stream_t stream) {
+    int st = config_ok(cfg);
+    if (st) return st;
+    if (n_views < 1 || n_views > 16 || !cams || n < 0) return VKS_ERR_INVALID_ARG;
+    if (!colors || !radii || !dmeans2d || !dconics || !dcolors || !dopacities) return VKS_ERR_INVALID_ARG;
+    for (int v = 0; v < n_views; v++) {
+        if (!camera_ok(cams + v)) return VKS_ERR_INVALID_ARG;
+        if (n > 0 && (!colors[v] || !radii[v] || !dmeans2d[v] || !dconics[v] || !dcolors[v] || !dopacities[v]))
+            return VKS_ERR_INVALID_ARG;
+        if ((reinterpret_cast<uintptr_t>(dmeans2d[v]) & 7) || (reinterpret_cast<uintptr_t>(radii[v]) & 7))
+            return VKS_ERR_INVALID_ARG;
+    }
+    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !dmeans || !dlog_scales || !dquats ||
+                  !dopacity_logits || !dsh))
+        return VKS_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(quats) & 15) || (reinterpret_cast<uintptr_t>(dquats) & 15))
+        return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_project_bwd_batch(*cfg, n_views, cams, n, means, log_scales, quats, opacity_logits,
+                                                     sh, colors, radii, dmeans2d, dconics, dcolors, dopacities,
+                                                     dmeans, dlog_scales, dquats, dopacity_logits, dsh,
+                                                     (cudaStream_t)stream));
+}
+
 }  // extern "C"

@@ -31,34 +31,6 @@ constexpr int kWarps = kThreads / 32;
 #define C35 1.445305721320277f
 #define C36 -0.5900435899266435f
 
-// Per-view constants of steps 6 and 12 (FOV limits, camera centre), computed once by the launcher
-// with the same IEEE fp32 operations in the same order (host code is compiled without FMA
-// contraction), instead of once per Gaussian.
-struct CamConst {
-    float lxp, lxn, lyp, lyn;  // step 6
-    float cp[3];               // step 12: campos = -R^T t
-};
-
-CamConst cam_const(const vks_camera& cam) {
-    CamConst k;
-    const float fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
-    const float W = (float)cam.width, H = (float)cam.height;
-    volatile float t;  // keeps every intermediate an IEEE-rounded float
-    t = 0.5f * W; t = t / fx; t = 0.3f * t; const float mx = t;
-    t = 0.5f * H; t = t / fy; t = 0.3f * t; const float my = t;
-    t = W - cx; t = t / fx; t = t + mx; k.lxp = t;
-    t = cx / fx; t = t + mx; k.lxn = t;
-    t = H - cy; t = t / fy; t = t + my; k.lyp = t;
-    t = cy / fy; t = t + my; k.lyn = t;
-    for (int c = 0; c < 3; c++) {
-        float a = cam.R[0 * 3 + c] * cam.t[0];
-        t = cam.R[1 * 3 + c] * cam.t[1]; a = a + t;
-        t = cam.R[2 * 3 + c] * cam.t[2]; a = a + t;
-        k.cp[c] = -a;
-    }
-    return k;
-}
-
 struct Params {
     vks_camera cam;
     vks_config cfg;

@@ -461,6 +461,357 @@ __global__ void __launch_bounds__(kThreads) project_bwd_kernel(const Params p) {
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Batched projection backward: the parameter gradients of V views summed in one pass.  Every
+// Gaussian's parameters and SH row are read once and its gradient row written once (instead of
+// V read-modify-writes of the 1.37 GB gradient buffer); per view only that view's 2D gradients,
+// colour and radii are read.  Each view's chain is the single-view kernel's; only the summation
+// over views is regrouped: linear view-independent factors (ρ(1-ρ), s, the quaternion-norm
+// projection) are applied once to the summed raw gradients.
+constexpr int kMaxBatchViews = 16;
+
+struct ViewIn {
+    vks_camera cam;
+    CamConst cc;  // FOV limits (pinned, host-computed exactly as the forward) and camera centre
+    const float* colors;
+    const int2* radii;
+    const float2* dm2;
+    const float* dcon;
+    const float* dcol;
+    const float* dop;
+};
+
+struct BatchParams {
+    vks_config cfg;
+    int64_t n;
+    int nv;
+    const float* __restrict__ means;
+    const float* __restrict__ ls;
+    const float4* __restrict__ quats;
+    const float* __restrict__ ologit;
+    const float* __restrict__ sh;
+    float* __restrict__ dmeans;
+    float* __restrict__ dls;
+    float4* __restrict__ dquats;
+    float* __restrict__ dologit;
+    float* __restrict__ dsh;
+    ViewIn v[kMaxBatchViews];
+};
+
+// SH rows readable / writable as float4 in shared memory
+template <int KS>
+constexpr bool vec4_rows() {
+    if constexpr (KS > 0) return (3 * KS) % 4 == 0 && ShLayout<KS>::SP % 4 == 0;
+    return false;
+}
+
+// one view's per-Gaussian inputs (prefetched one view ahead)
+struct ViewLoads {
+    float dcl[3], col[3], da, db, dc, dr;
+    float2 dm;
+};
+
+__device__ __forceinline__ void load_view(const ViewIn& V, int64_t i, bool on, ViewLoads& L) {
+    if (on) {
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            L.dcl[c] = __ldg(V.dcol + 3 * i + c);
+            L.col[c] = __ldg(V.colors + 3 * i + c);
+        }
+        L.dm = __ldg(V.dm2 + i);
+        L.da = __ldg(V.dcon + 3 * i);
+        L.db = __ldg(V.dcon + 3 * i + 1);
+        L.dc = __ldg(V.dcon + 3 * i + 2);
+        L.dr = __ldg(V.dop + i);
+    } else {
+#pragma unroll
+        for (int c = 0; c < 3; c++) L.dcl[c] = L.col[c] = 0.0f;
+        L.dm = make_float2(0.0f, 0.0f);
+        L.da = L.db = L.dc = L.dr = 0.0f;
+    }
+}
+
+template <int KS, bool OVERWRITE>
+__global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const BatchParams p) {
+    extern __shared__ float smem[];
+    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const unsigned lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const int64_t g0 = i - lane;
+    const bool valid = i < p.n;
+    // visibility in each view (radii != 0)
+    unsigned vis = 0;
+    if (valid) {
+        for (int v = 0; v < p.nv; v++) {
+            const int2 r = __ldg(p.v[v].radii + i);
+            if (r.x != 0 || r.y != 0) vis |= 1u << v;
+        }
+    }
+    const bool act = vis != 0;
+    const unsigned amask = __ballot_sync(VKS_FULL_MASK, act);
+    const int K = (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);
+    const int S = 3 * p.cfg.sh_coeffs;
+    // shared memory per warp: the SH rows (staged once) and the dSH accumulator rows
+    float* shv = nullptr;
+    float* acc = nullptr;
+    if constexpr (KS > 0) {
+        shv = smem + warp * 2 * ShLayout<KS>::kWarpFloats;
+        float* accw = shv + ShLayout<KS>::kWarpFloats;
+        if (amask) stage_in_async<KS>(p.sh, g0, amask, shv);
+        acc = accw + lane * ShLayout<KS>::SP;
+#pragma unroll
+        for (int j = 0; j < 3 * KS; j++) acc[j] = 0.0f;
+    } else if (valid && OVERWRITE) {
+        for (int j = 0; j < S; j++) p.dsh[(int64_t)S * i + j] = 0.0f;
+    }
+    float dmu[3] = {0, 0, 0}, dsv[3] = {0, 0, 0}, dqr[4] = {0, 0, 0, 0}, drho = 0.0f;
+    if (amask) {
+        float mu[3] = {0, 0, 0}, ls[3] = {0, 0, 0}, o = 0.0f;
+        float4 q = make_float4(1, 0, 0, 0);
+        if (act) {
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                mu[c] = __ldg(p.means + 3 * i + c);
+                ls[c] = __ldg(p.ls + 3 * i + c);
+            }
+            q = __ldg(p.quats + i);
+            o = __ldg(p.ologit + i);
+        }
+        // view-independent part of the chain
+        const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+        const float iqn = 1.0f / qn;
+        const float w = q.x * iqn, x = q.y * iqn, y = q.z * iqn, z = q.w * iqn;
+        const float Rq[9] = {1.0f - 2.0f * (y * y + z * z), 2.0f * (x * y - w * z), 2.0f * (x * z + w * y),
+                             2.0f * (x * y + w * z), 1.0f - 2.0f * (x * x + z * z), 2.0f * (y * z - w * x),
+                             2.0f * (x * z - w * y), 2.0f * (y * z + w * x), 1.0f - 2.0f * (x * x + y * y)};
+        const float s[3] = {__expf(ls[0]), __expf(ls[1]), __expf(ls[2])};
+        const float* f;
+        if constexpr (KS > 0) {
+            cp_async_wait_all();
+            __syncwarp();
+            f = shv + lane * ShLayout<KS>::SP;
+        } else {
+            f = p.sh + (int64_t)S * i;
+        }
+        ViewLoads cur;
+        load_view(p.v[0], i, vis & 1u, cur);
+        for (int v = 0; v < p.nv; v++) {
+            const bool on = (vis >> v) & 1u;
+            ViewLoads nxt;  // next view's inputs in flight while this view computes
+            if (v + 1 < p.nv) load_view(p.v[v + 1], i, (vis >> (v + 1)) & 1u, nxt);
+            if (__any_sync(VKS_FULL_MASK, on)) {
+                const ViewIn& V = p.v[v];
+                const float* R = V.cam.R;
+                const float fx = V.cam.fx, fy = V.cam.fy;
+                // FOV decision of the forward (steps 1, 6), bit-identical: pinned t, tx/tz vs limits
+                const float tx = __fadd_rn(pdot3(R + 0, mu), V.cam.t[0]);
+                const float ty = __fadd_rn(pdot3(R + 3, mu), V.cam.t[1]);
+                const float tz = __fadd_rn(pdot3(R + 6, mu), V.cam.t[2]);
+                const float rxz = __fdiv_rn(tx, tz), ryz = __fdiv_rn(ty, tz);
+                int fovx = 0, fovy = 0;
+                float Lx = 0.0f, Ly = 0.0f;
+                if (rxz > V.cc.lxp) { fovx = 1; Lx = V.cc.lxp; } else if (rxz < -V.cc.lxn) { fovx = -1; Lx = -V.cc.lxn; }
+                if (ryz > V.cc.lyp) { fovy = 1; Ly = V.cc.lyp; } else if (ryz < -V.cc.lyn) { fovy = -1; Ly = -V.cc.lyn; }
+                float Mc[9];
+#pragma unroll
+                for (int j = 0; j < 3; j++)
+#pragma unroll
+                    for (int c = 0; c < 3; c++)
+                        Mc[3 * j + c] = (R[3 * j] * Rq[c] + R[3 * j + 1] * Rq[3 + c] + R[3 * j + 2] * Rq[6 + c]) * s[c];
+                const float itz = 1.0f / tz, itz2 = itz * itz, itz3 = itz2 * itz;
+                const float txc = fovx ? tz * Lx : tx, tyc = fovy ? tz * Ly : ty;
+                const float J00 = fx * itz, J02 = -fx * txc * itz2, J11 = fy * itz, J12 = -fy * tyc * itz2;
+                float K0[3], K1[3];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    K0[c] = J00 * Mc[c] + J02 * Mc[6 + c];
+                    K1[c] = J11 * Mc[3 + c] + J12 * Mc[6 + c];
+                }
+                const float A = K0[0] * K0[0] + K0[1] * K0[1] + K0[2] * K0[2] + 0.3f;
+                const float B = K0[0] * K1[0] + K0[1] * K1[1] + K0[2] * K1[2];
+                const float C = K1[0] * K1[0] + K1[1] * K1[1] + K1[2] * K1[2] + 0.3f;
+                const float id = 1.0f / (A * C - B * B), id2 = id * id;
+                const float da = cur.da, db = cur.db, dc = cur.dc;
+                const float dA = (-C * C * da + B * C * db - B * B * dc) * id2;
+                const float dB = (2.0f * B * C * da - (A * C + B * B) * db + 2.0f * A * B * dc) * id2;
+                const float dC = (-B * B * da + A * B * db - A * A * dc) * id2;
+                float dK0[3], dK1[3];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    dK0[c] = 2.0f * dA * K0[c] + dB * K1[c];
+                    dK1[c] = dB * K0[c] + 2.0f * dC * K1[c];
+                }
+                float dJ00 = 0, dJ02 = 0, dJ11 = 0, dJ12 = 0, dMc[9];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    dJ00 += dK0[c] * Mc[c];
+                    dJ02 += dK0[c] * Mc[6 + c];
+                    dJ11 += dK1[c] * Mc[3 + c];
+                    dJ12 += dK1[c] * Mc[6 + c];
+                    dMc[c] = J00 * dK0[c];
+                    dMc[3 + c] = J11 * dK1[c];
+                    dMc[6 + c] = J02 * dK0[c] + J12 * dK1[c];
+                }
+                float D[9];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+#pragma unroll
+                    for (int j = 0; j < 3; j++) {
+                        const float dM = R[j] * dMc[c] + R[3 + j] * dMc[3 + c] + R[6 + j] * dMc[6 + c];
+                        dsv[c] += dM * Rq[3 * j + c];  // x s[c] once at the end
+                        D[3 * j + c] = dM * s[c];
+                    }
+                }
+                dqr[0] += 2.0f * (-z * D[1] + y * D[2] + z * D[3] - x * D[5] - y * D[6] + x * D[7]);
+                dqr[1] += 2.0f * (y * D[1] + z * D[2] + y * D[3] - 2.0f * x * D[4] - w * D[5] + z * D[6] +
+                                  w * D[7] - 2.0f * x * D[8]);
+                dqr[2] += 2.0f * (-2.0f * y * D[0] + x * D[1] + w * D[2] + x * D[3] + z * D[5] - w * D[6] +
+                                  z * D[7] - 2.0f * y * D[8]);
+                dqr[3] += 2.0f * (-2.0f * z * D[0] - w * D[1] + x * D[2] + w * D[3] - 2.0f * z * D[4] +
+                                  y * D[5] + x * D[6] + y * D[7]);
+                const float2 dm = cur.dm;
+                float dt0 = fx * itz * dm.x;
+                float dt1 = fy * itz * dm.y;
+                float dt2 = -fx * tx * itz2 * dm.x - fy * ty * itz2 * dm.y - fx * itz2 * dJ00 - fy * itz2 * dJ11;
+                if (fovx == 0) { dt0 += -fx * itz2 * dJ02; dt2 += 2.0f * fx * tx * itz3 * dJ02; }
+                else { dt2 += fx * Lx * itz2 * dJ02; }
+                if (fovy == 0) { dt1 += -fy * itz2 * dJ12; dt2 += 2.0f * fy * ty * itz3 * dJ12; }
+                else { dt2 += fy * Ly * itz2 * dJ12; }
+                drho += cur.dr;
+                // SH: colour clamp from the forward's colour, direction gradient, dsh += Y (x) dce
+                float dce[3];
+#pragma unroll
+                for (int c = 0; c < 3; c++) dce[c] = cur.col[c] > 0.0f ? cur.dcl[c] : 0.0f;
+                float d[3];
+#pragma unroll
+                for (int c = 0; c < 3; c++) d[c] = mu[c] - V.cc.cp[c];
+                const float idl = rsqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+                const float dh[3] = {d[0] * idl, d[1] * idl, d[2] * idl};
+                float Y[16], dY[16][3];
+                sh_basis_and_grad(dh[0], dh[1], dh[2], K, Y, dY);
+                if (on) {
+                    float ddh0 = 0, ddh1 = 0, ddh2 = 0;
+                    if constexpr (vec4_rows<KS>()) {
+                        // 128-bit shared-memory reads of the SH row and read-modify-writes of the
+                        // dSH row; element e = 3 l + ch
+                        const float4* f4 = reinterpret_cast<const float4*>(f);
+                        float4* a4 = reinterpret_cast<float4*>(acc);
+                        float g = 0.0f;  // <dce, f_l> of the current l (elements arrive in e order)
+#pragma unroll
+                        for (int m = 0; m < 3 * KS / 4; m++) {
+                            const float4 fv = f4[m];
+                            const float fe[4] = {fv.x, fv.y, fv.z, fv.w};
+                            float4 av = a4[m];
+                            float ae[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                const int e = 4 * m + t, l = e / 3, c = e % 3;
+                                if (l < K) {
+                                    g += dce[c] * fe[t];
+                                    ae[t] += Y[l] * dce[c];
+                                    if (c == 2) {
+                                        if (l > 0) {
+                                            ddh0 += g * dY[l][0];
+                                            ddh1 += g * dY[l][1];
+                                            ddh2 += g * dY[l][2];
+                                        }
+                                        g = 0.0f;
+                                    }
+                                }
+                            }
+                            a4[m] = make_float4(ae[0], ae[1], ae[2], ae[3]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int l = 1; l < 16; l++) {
+                            if (l < K) {
+                                const float g = dce[0] * f[3 * l] + dce[1] * f[3 * l + 1] + dce[2] * f[3 * l + 2];
+                                ddh0 += g * dY[l][0];
+                                ddh1 += g * dY[l][1];
+                                ddh2 += g * dY[l][2];
+                            }
+                        }
+                    }
+                    if constexpr (vec4_rows<KS>()) {
+                        // (accumulated above)
+                    } else if constexpr (KS > 0) {
+#pragma unroll
+                        for (int l = 0; l < KS; l++) {
+                            if (l < K) {
+#pragma unroll
+                                for (int c = 0; c < 3; c++) acc[3 * l + c] += Y[l] * dce[c];
+                            }
+                        }
+                    } else {
+                        for (int l = 0; l < K; l++)
+                            for (int c = 0; c < 3; c++) p.dsh[(int64_t)S * i + 3 * l + c] += Y[l] * dce[c];
+                    }
+                    const float pr = dh[0] * ddh0 + dh[1] * ddh1 + dh[2] * ddh2;
+                    dmu[0] += (ddh0 - dh[0] * pr) * idl + R[0] * dt0 + R[3] * dt1 + R[6] * dt2;
+                    dmu[1] += (ddh1 - dh[1] * pr) * idl + R[1] * dt0 + R[4] * dt1 + R[7] * dt2;
+                    dmu[2] += (ddh2 - dh[2] * pr) * idl + R[2] * dt0 + R[5] * dt1 + R[8] * dt2;
+                }
+            }
+            if (v + 1 < p.nv) cur = nxt;
+        }
+        // view-independent factors applied once to the summed raw gradients
+        const float rho = 1.0f / (1.0f + __expf(-o));
+        drho *= rho * (1.0f - rho);
+#pragma unroll
+        for (int c = 0; c < 3; c++) dsv[c] *= s[c];
+        const float qd = w * dqr[0] + x * dqr[1] + y * dqr[2] + z * dqr[3];
+        dqr[0] = (dqr[0] - w * qd) * iqn;
+        dqr[1] = (dqr[1] - x * qd) * iqn;
+        dqr[2] = (dqr[2] - y * qd) * iqn;
+        dqr[3] = (dqr[3] - z * qd) * iqn;
+    }
+    // ---- outputs: every row under OVERWRITE (zeros where no view sees the Gaussian), else the
+    // rows some view sees
+    if constexpr (KS > 0) {
+        float* accw = smem + warp * 2 * ShLayout<KS>::kWarpFloats + ShLayout<KS>::kWarpFloats;
+        if (!OVERWRITE && act) {  // += onto the old row
+            const float* src = p.dsh + (int64_t)3 * KS * i;
+#pragma unroll
+            for (int j = 0; j < 3 * KS; j++) acc[j] += src[j];
+        }
+        __syncwarp();
+        const unsigned omask = OVERWRITE ? __ballot_sync(VKS_FULL_MASK, valid) : amask;
+        stage_out<KS>(p.dsh, g0, omask, accw);
+    }
+    if (!valid || (!OVERWRITE && !act)) return;
+    if (OVERWRITE) {
+        p.dmeans[3 * i] = dmu[0]; p.dmeans[3 * i + 1] = dmu[1]; p.dmeans[3 * i + 2] = dmu[2];
+        p.dls[3 * i] = dsv[0]; p.dls[3 * i + 1] = dsv[1]; p.dls[3 * i + 2] = dsv[2];
+        p.dquats[i] = make_float4(dqr[0], dqr[1], dqr[2], dqr[3]);
+        p.dologit[i] = drho;
+    } else {
+        p.dmeans[3 * i] += dmu[0]; p.dmeans[3 * i + 1] += dmu[1]; p.dmeans[3 * i + 2] += dmu[2];
+        p.dls[3 * i] += dsv[0]; p.dls[3 * i + 1] += dsv[1]; p.dls[3 * i + 2] += dsv[2];
+        float4 o4 = p.dquats[i];
+        o4.x += dqr[0]; o4.y += dqr[1]; o4.z += dqr[2]; o4.w += dqr[3];
+        p.dquats[i] = o4;
+        p.dologit[i] += drho;
+    }
+}
+
+template <int KS, bool OW>
+int launch_batch_t(const BatchParams& p, cudaStream_t s) {
+    size_t sm = 0;
+    if constexpr (KS > 0) sm = sizeof(float) * kWarps * 2 * ShLayout<KS>::kWarpFloats;
+    if (sm > 48 * 1024 &&
+        cudaFuncSetAttribute(project_bwd_batch_kernel<KS, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+            cudaSuccess)
+        return VKS_ERR_CUDA;
+    const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
+    project_bwd_batch_kernel<KS, OW><<<blocks, kThreads, sm, s>>>(p);
+    return LaunchCheck::check();
+}
+
+template <int KS>
+int launch_batch_k(const BatchParams& p, cudaStream_t s) {
+    return (p.cfg.flags & VKS_FLAG_GRAD_OVERWRITE) ? launch_batch_t<KS, true>(p, s) : launch_batch_t<KS, false>(p, s);
+}
+
 template <int KS, bool OW>
 int launch_t(const Params& p, cudaStream_t s) {
     size_t sm = 0;
@@ -503,6 +854,41 @@ int launch_project_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
         case 4: return al ? launch_k<4>(p, s) : launch_k<0>(p, s);
         case 1: return launch_k<1>(p, s);
         default: return launch_k<0>(p, s);
+    }
+}
+
+int launch_project_bwd_batch(const vks_config& cfg, int32_t n_views, const vks_camera* cams, int64_t n,
+                             const float* means, const float* log_scales, const float* quats,
+                             const float* opacity_logits, const float* sh, const float* const* colors,
+                             const int32_t* const* radii, const float* const* dmeans2d, const float* const* dconics,
+                             const float* const* dcolors, const float* const* dopacities, float* dmeans,
+                             float* dlog_scales, float* dquats, float* dopacity_logits, float* dsh, cudaStream_t s) {
+    if (n == 0) return VKS_OK;
+    if (n_views < 1 || n_views > kMaxBatchViews) return VKS_ERR_INVALID_ARG;
+    BatchParams p{};
+    p.cfg = cfg; p.n = n; p.nv = n_views;
+    p.means = means; p.ls = log_scales; p.quats = reinterpret_cast<const float4*>(quats);
+    p.ologit = opacity_logits; p.sh = sh;
+    p.dmeans = dmeans; p.dls = dlog_scales; p.dquats = reinterpret_cast<float4*>(dquats);
+    p.dologit = dopacity_logits; p.dsh = dsh;
+    for (int v = 0; v < n_views; v++) {
+        ViewIn& V = p.v[v];
+        V.cam = cams[v];
+        V.cc = cam_const(cams[v]);
+        V.colors = colors[v];
+        V.radii = reinterpret_cast<const int2*>(radii[v]);
+        V.dm2 = reinterpret_cast<const float2*>(dmeans2d[v]);
+        V.dcon = dconics[v];
+        V.dcol = dcolors[v];
+        V.dop = dopacities[v];
+    }
+    const bool al = aligned16(sh) && aligned16(dsh);
+    switch (cfg.sh_coeffs) {
+        case 16: return al ? launch_batch_k<16>(p, s) : launch_batch_k<0>(p, s);
+        case 9: return launch_batch_k<9>(p, s);
+        case 4: return al ? launch_batch_k<4>(p, s) : launch_batch_k<0>(p, s);
+        case 1: return launch_batch_k<1>(p, s);
+        default: return launch_batch_k<0>(p, s);
     }
 }
 

@@ -73,6 +73,34 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Per-view constants of steps 6 and 12 (FOV limits, camera centre), computed once by the launcher
+// with the same IEEE fp32 operations in the same order (host code is compiled without FMA
+// contraction), instead of once per Gaussian.
+struct CamConst {
+    float lxp, lxn, lyp, lyn;  // step 6
+    float cp[3];               // step 12: campos = -R^T t
+};
+
+inline CamConst cam_const(const vks_camera& cam) {
+    CamConst k;
+    const float fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
+    const float W = (float)cam.width, H = (float)cam.height;
+    volatile float t;  // keeps every intermediate an IEEE-rounded float
+    t = 0.5f * W; t = t / fx; t = 0.3f * t; const float mx = t;
+    t = 0.5f * H; t = t / fy; t = 0.3f * t; const float my = t;
+    t = W - cx; t = t / fx; t = t + mx; k.lxp = t;
+    t = cx / fx; t = t + mx; k.lxn = t;
+    t = H - cy; t = t / fy; t = t + my; k.lyp = t;
+    t = cy / fy; t = t + my; k.lyn = t;
+    for (int c = 0; c < 3; c++) {
+        float a = cam.R[0 * 3 + c] * cam.t[0];
+        t = cam.R[1 * 3 + c] * cam.t[1]; a = a + t;
+        t = cam.R[2 * 3 + c] * cam.t[2]; a = a + t;
+        k.cp[c] = -a;
+    }
+    return k;
+}
+
 }  // namespace vks
 
 // internal launchers (implemented in the .cu files, called by api.cu)
@@ -87,6 +115,12 @@ int launch_project_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
                        const float* dconics, const float* dcolors, const float* dopacities,
                        float* dmeans, float* dlog_scales, float* dquats, float* dopacity_logits,
                        float* dsh, cudaStream_t s);
+int launch_project_bwd_batch(const vks_config& cfg, int32_t n_views, const vks_camera* cams, int64_t n,
+                             const float* means, const float* log_scales, const float* quats,
+                             const float* opacity_logits, const float* sh, const float* const* colors,
+                             const int32_t* const* radii, const float* const* dmeans2d, const float* const* dconics,
+                             const float* const* dcolors, const float* const* dopacities, float* dmeans,
+                             float* dlog_scales, float* dquats, float* dopacity_logits, float* dsh, cudaStream_t s);
 size_t bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles);
 int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const int32_t* radii,
                  const float* depths, const int32_t* tiles_touched, uint32_t* offsets,

@@ -82,6 +82,11 @@ def test_argument_validation_is_synchronous():
     wide = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
                               width=70000, height=64))
     assert lib.vks_raster_bwd(C.byref(cfg), C.byref(wide), 0, *([None] * 16)) == V.VKS_ERR_INVALID_ARG
+    arr = (C.c_void_p * 1)(None)
+    cams = (V.VksCamera * 1)(cam)
+    for nv in (0, 17):  # batch size outside [1, 16]
+        assert lib.vks_project_bwd_batch(C.byref(cfg), nv, cams, 0, *([None] * 5), *([arr] * 6),
+                                         *([None] * 5), None) == V.VKS_ERR_INVALID_ARG
     m = C.c_int64(0)
     assert lib.vks_bin_sort(C.byref(cam), 5, *([None] * 5), 0, *([None] * 4), None, None, C.byref(m), None, 0,
                             None) == V.VKS_ERR_INVALID_ARG

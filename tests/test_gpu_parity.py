@@ -367,3 +367,63 @@ def test_binning_depth_ranges(oracle_lib, case):
     d = g["depths"][g["tiles_touched"] > 0].view(np.uint32).astype(np.int64)
     spread = int(d.max() - d.min())
     assert (spread == 0) if case == "equal_depths" else (spread > 2**27)
+
+
+# ------------------------------------------------------------------ batched projection backward
+
+@pytest.mark.parametrize("coeffs,deg,nv", [(16, 3, 4), (9, 2, 3), (16, 1, 1), (4, 1, 2), (1, 0, 2)])
+def test_project_bwd_batch_equals_sum_of_views(coeffs, deg, nv):
+    """vks_project_bwd_batch over a batch of views = the per-view vks_project_bwd summed (first view
+    overwriting, the others accumulating), up to the regrouped summation; exact zeros for
+    Gaussians no view sees; accumulate mode adds onto the existing gradients."""
+    import torch
+    import paper_2605_00219_b200 as P
+    s = synth.make_scene(20001, "outdoor", 70 + nv)
+    s["sh"] = np.ascontiguousarray(s["sh"][:, :coeffs])
+    cams = synth.ring_cameras(160, 120, "outdoor", 8)[:nv]
+    cfg = synth.default_render_config(deg, sh_coeffs=coeffs)
+    params = P.GaussianParams.from_host(s)
+    views = []
+    for v, cam in enumerate(cams):
+        r = P.ViewRenderer(params.n, 160, 120)
+        r.forward(cfg, cam, params)
+        r.g2d.zero_()
+        dL = torch.from_numpy(synth.upstream_grad(120, 160, 11 + v)).cuda()
+        P.vks_raster_bwd(cfg, cam, r.means2d, r.conics, r.colors, r.opacities, r.radii, r.vals, r.tile_offsets,
+                         r.T_final, r.n_contrib, dL, r.dmeans2d, r.dconics, r.dcolors, r.dopacities,
+                         tile_order=r.tile_order)
+        views.append(r)
+    g = params.grads()
+    ocfg = dict(cfg, flags=P.FLAG_GRAD_OVERWRITE)
+    for v, (cam, r) in enumerate(zip(cams, views)):
+        P.vks_project_bwd(ocfg if v == 0 else cfg, cam, params.means, params.log_scales, params.quats,
+                          params.opacity_logits, params.sh, r.colors, r.radii, r.dmeans2d, r.dconics, r.dcolors,
+                          r.dopacities, g["dmeans"], g["dlog_scales"], g["dquats"], g["dopacity_logits"], g["dsh"])
+    torch.cuda.synchronize()
+    ref = params.grad_flat.clone()
+
+    def batch(c):
+        P.vks_project_bwd_batch(c, cams, params.means, params.log_scales, params.quats, params.opacity_logits,
+                                params.sh, [r.colors for r in views], [r.radii for r in views],
+                                [r.dmeans2d for r in views], [r.dconics for r in views], [r.dcolors for r in views],
+                                [r.dopacities for r in views], g["dmeans"], g["dlog_scales"], g["dquats"],
+                                g["dopacity_logits"], g["dsh"])
+        torch.cuda.synchronize()
+        return params.grad_flat.clone()
+
+    params.grad_flat.fill_(float("nan"))
+    got = batch(ocfg)
+    seen = torch.zeros(params.n, dtype=torch.bool, device="cuda")
+    for r in views:
+        seen |= (r.radii != 0).any(dim=1)
+    G = P.GaussianParams(params.means, params.log_scales, params.quats, params.opacity_logits, params.sh, got).grads()
+    Rf = P.GaussianParams(params.means, params.log_scales, params.quats, params.opacity_logits, params.sh, ref).grads()
+    for k in G:
+        assert torch.isfinite(G[k]).all(), k
+        assert (G[k][~seen] == 0).all(), k
+        assert torch.allclose(G[k], Rf[k], rtol=1e-4, atol=1e-6 * Rf[k].abs().max().item() + 1e-30), k
+    # accumulate mode: += onto existing rows (the batch result itself)
+    got2 = batch(cfg)
+    G2 = P.GaussianParams(params.means, params.log_scales, params.quats, params.opacity_logits, params.sh, got2).grads()
+    for k in G:
+        assert torch.allclose(G2[k], 2 * G[k], rtol=1e-4, atol=1e-6 * G[k].abs().max().item() + 1e-30), k

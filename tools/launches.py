@@ -18,3 +18,12 @@ for k, v in d.items():
     print(f"{v['name'][:64]:64s} {t / 1e3:8.1f}us {t / tot * 100:5.1f}% rd={v.get('dram__bytes_read.sum', 0) / 1e6:7.1f}MB "
           f"wr={v.get('dram__bytes_write.sum', 0) / 1e6:7.1f}MB inst={v.get('smsp__inst_executed.sum', 0) / 1e6:6.1f}M")
 print(f"total {tot / 1e3:.1f} us")
+
+if len(sys.argv) > 2 and sys.argv[2] == "--by-kernel":  # aggregate: launches, median, share
+    import statistics
+    agg = OrderedDict()
+    for v in d.values():
+        agg.setdefault(v["name"][:64], []).append(v.get("gpu__time_duration.sum", 0))
+    print("\nper kernel: launches, median us, total us, share of all launches")
+    for k, ts in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        print(f"{k:64s} {len(ts):5d} {statistics.median(ts) / 1e3:9.1f} {sum(ts) / 1e3:10.1f} {sum(ts) / tot * 100:5.1f}%")

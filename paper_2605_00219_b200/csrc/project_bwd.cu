@@ -531,7 +531,7 @@ __device__ __forceinline__ void load_view(const ViewIn& V, int64_t i, bool on, V
     }
 }
 
-template <int KS, bool OVERWRITE>
+template <int KS, bool OVERWRITE, bool KFULL>
 __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const BatchParams p) {
     extern __shared__ float smem[];
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const Batch
     }
     const bool act = vis != 0;
     const unsigned amask = __ballot_sync(VKS_FULL_MASK, act);
-    const int K = (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);
+    const int K = KFULL ? KS : (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);  // KFULL: compile-time
     const int S = 3 * p.cfg.sh_coeffs;
     // shared memory per warp: the SH rows (staged once) and the dSH accumulator rows
     float* shv = nullptr;
@@ -585,6 +585,9 @@ __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const Batch
                              2.0f * (x * y + w * z), 1.0f - 2.0f * (x * x + z * z), 2.0f * (y * z - w * x),
                              2.0f * (x * z - w * y), 2.0f * (y * z + w * x), 1.0f - 2.0f * (x * x + y * y)};
         const float s[3] = {__expf(ls[0]), __expf(ls[1]), __expf(ls[2])};
+        float Ms[9];  // Rq diag(s): view-independent, so each view's Mc = R Ms is 27 multiply-adds
+#pragma unroll
+        for (int j = 0; j < 9; j++) Ms[j] = Rq[j] * s[j % 3];
         const float* f;
         if constexpr (KS > 0) {
             cp_async_wait_all();
@@ -607,7 +610,16 @@ __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const Batch
                 const float tx = __fadd_rn(pdot3(R + 0, mu), V.cam.t[0]);
                 const float ty = __fadd_rn(pdot3(R + 3, mu), V.cam.t[1]);
                 const float tz = __fadd_rn(pdot3(R + 6, mu), V.cam.t[2]);
-                const float rxz = __fdiv_rn(tx, tz), ryz = __fdiv_rn(ty, tz);
+                // the comparisons need the IEEE-rounded tx/tz only near a limit: an approximate ratio
+                // (relative error < 1e-6) decides every case further than 1e-5 from the limits
+                const float rtz = __fdividef(1.0f, tz);
+                float rxz = tx * rtz, ryz = ty * rtz;
+                const bool nearx = fabsf(rxz - V.cc.lxp) <= 1e-5f * fabsf(V.cc.lxp) + 1e-30f ||
+                                   fabsf(rxz + V.cc.lxn) <= 1e-5f * fabsf(V.cc.lxn) + 1e-30f;
+                const bool neary = fabsf(ryz - V.cc.lyp) <= 1e-5f * fabsf(V.cc.lyp) + 1e-30f ||
+                                   fabsf(ryz + V.cc.lyn) <= 1e-5f * fabsf(V.cc.lyn) + 1e-30f;
+                if (nearx) rxz = __fdiv_rn(tx, tz);
+                if (neary) ryz = __fdiv_rn(ty, tz);
                 int fovx = 0, fovy = 0;
                 float Lx = 0.0f, Ly = 0.0f;
                 if (rxz > V.cc.lxp) { fovx = 1; Lx = V.cc.lxp; } else if (rxz < -V.cc.lxn) { fovx = -1; Lx = -V.cc.lxn; }
@@ -617,7 +629,7 @@ __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const Batch
                 for (int j = 0; j < 3; j++)
 #pragma unroll
                     for (int c = 0; c < 3; c++)
-                        Mc[3 * j + c] = (R[3 * j] * Rq[c] + R[3 * j + 1] * Rq[3 + c] + R[3 * j + 2] * Rq[6 + c]) * s[c];
+                        Mc[3 * j + c] = R[3 * j] * Ms[c] + R[3 * j + 1] * Ms[3 + c] + R[3 * j + 2] * Ms[6 + c];
                 const float itz = 1.0f / tz, itz2 = itz * itz, itz3 = itz2 * itz;
                 const float txc = fovx ? tz * Lx : tx, tyc = fovy ? tz * Ly : ty;
                 const float J00 = fx * itz, J02 = -fx * txc * itz2, J11 = fy * itz, J12 = -fy * tyc * itz2;
@@ -794,22 +806,25 @@ __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const Batch
     }
 }
 
-template <int KS, bool OW>
+template <int KS, bool OW, bool KF>
 int launch_batch_t(const BatchParams& p, cudaStream_t s) {
     size_t sm = 0;
     if constexpr (KS > 0) sm = sizeof(float) * kWarps * 2 * ShLayout<KS>::kWarpFloats;
     if (sm > 48 * 1024 &&
-        cudaFuncSetAttribute(project_bwd_batch_kernel<KS, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+        cudaFuncSetAttribute(project_bwd_batch_kernel<KS, OW, KF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
             cudaSuccess)
         return VKS_ERR_CUDA;
     const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
-    project_bwd_batch_kernel<KS, OW><<<blocks, kThreads, sm, s>>>(p);
+    project_bwd_batch_kernel<KS, OW, KF><<<blocks, kThreads, sm, s>>>(p);
     return LaunchCheck::check();
 }
 
 template <int KS>
 int launch_batch_k(const BatchParams& p, cudaStream_t s) {
-    return (p.cfg.flags & VKS_FLAG_GRAD_OVERWRITE) ? launch_batch_t<KS, true>(p, s) : launch_batch_t<KS, false>(p, s);
+    const bool ow = p.cfg.flags & VKS_FLAG_GRAD_OVERWRITE;
+    if (KS == 16 && p.cfg.sh_degree == 3)  // every stored coefficient used: K known at compile time
+        return ow ? launch_batch_t<KS, true, true>(p, s) : launch_batch_t<KS, false, true>(p, s);
+    return ow ? launch_batch_t<KS, true, false>(p, s) : launch_batch_t<KS, false, false>(p, s);
 }
 
 template <int KS, bool OW>

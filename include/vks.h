@@ -223,6 +223,26 @@ int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                     float* dopacity_logits, float* dsh, vks_stream_t stream);
 
 /*
+ * vks_project_fwd_batch — "Projection Forward" of a batch of views in one pass over the
+ * parameters: the camera-independent part of DESIGN.md §4.1 (unit quaternion, rotation, X64
+ * scales and opacity, the footprint's X64 log) once per Gaussian, the SH row read once, then
+ * every view's steps exactly as vks_project_fwd — each view's outputs are bit-identical to a
+ * vks_project_fwd call for that view (except the opacities, below).
+ *   n_views in [1, 16] (VKS_ERR_INVALID_ARG otherwise); cams: HOST array of n_views cameras, all
+ *   with the same width and height
+ *   means2d, conics, depths, radii, tiles_touched, colors: HOST arrays of n_views DEVICE
+ *     pointers, each laid out as the matching vks_project_fwd output
+ *   opacities [n]: one array for the batch (the opacity is view-independent); rows the
+ *     footprint test culls are unspecified
+ */
+int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,
+                          const float* means, const float* log_scales, const float* quats,
+                          const float* opacity_logits, const float* sh, float* const* means2d,
+                          float* const* conics, float* const* depths, int32_t* const* radii,
+                          int32_t* const* tiles_touched, float* const* colors, float* opacities,
+                          vks_stream_t stream);
+
+/*
  * vks_project_bwd_batch — the projection backward of a batch of views in one pass: the sum over
  * the views of vks_project_bwd (P:76 projection part; a training step's views share one set of
  * parameter gradients).  Each view's chain is exactly vks_project_bwd's;

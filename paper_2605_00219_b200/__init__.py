@@ -5,10 +5,10 @@ points) plus buffer orchestration (`pipeline`).  There is no CPU fallback: impor
 loudly when libvks.so is missing."""
 from ._vks import (EXPORTS, FLAG_GRAD_OVERWRITE, FOOTPRINT_3SIGMA, FOOTPRINT_SUPPORT, VksError, exported_symbols,  # noqa: F401
                    make_camera, make_config, vks_bin_sort, vks_bin_sort_workspace_bytes, vks_project_bwd,
-                   vks_project_bwd_batch, vks_project_fwd, vks_raster_bwd, vks_raster_fwd, vks_raster_fwd_stats,
+                   vks_project_bwd_batch, vks_project_fwd, vks_project_fwd_batch, vks_raster_bwd, vks_raster_fwd, vks_raster_fwd_stats,
                    vks_version)
 from .pipeline import GaussianParams, ViewRenderer  # noqa: F401
 
 __all__ = ["vks_project_fwd", "vks_bin_sort", "vks_bin_sort_workspace_bytes", "vks_raster_fwd",
-           "vks_raster_bwd", "vks_project_bwd", "vks_project_bwd_batch", "vks_version", "GaussianParams", "ViewRenderer",
+           "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch", "vks_version", "GaussianParams", "ViewRenderer",
            "VksError", "make_camera", "make_config"]

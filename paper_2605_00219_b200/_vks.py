@@ -26,7 +26,7 @@ FLAG_GRAD_OVERWRITE = 1
 
 EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_project_fwd",
            "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats",
-           "vks_raster_bwd", "vks_project_bwd", "vks_project_bwd_batch")
+           "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch")
 
 
 class VksCamera(C.Structure):
@@ -54,8 +54,9 @@ _lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 16
 _lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 10
 _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
 _lib.vks_project_bwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 17
+_lib.vks_project_fwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 13
 for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats", "vks_raster_bwd",
-           "vks_project_bwd", "vks_project_bwd_batch"):
+           "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -222,6 +223,26 @@ def vks_project_bwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, colo
                               _ptr(dopacity_logits, f32, "dopacity_logits"), _ptr(dsh, f32, "dsh"),
                               _stream(stream))
     _check("vks_project_bwd", st)
+
+
+def vks_project_fwd_batch(cfg, cams, means, log_scales, quats, opacity_logits, sh, means2d, conics, depths, radii,
+                          tiles_touched, colors, opacities, stream=None):
+    """Batched projection forward: `cams` and the per-view outputs (means2d, conics, depths, radii,
+    tiles_touched, colors) are equal-length sequences; `opacities` is one tensor for the batch."""
+    nv = len(cams)
+    per_view = (means2d, conics, depths, radii, tiles_touched, colors)
+    if any(len(x) != nv for x in per_view):
+        raise ValueError("per-view sequences must all have len(cams) entries")
+    c = make_config(cfg) if isinstance(cfg, dict) else cfg
+    karr = (VksCamera * max(nv, 1))(*[k if isinstance(k, VksCamera) else make_camera(k) for k in cams])
+    dts = (f32, f32, f32, i32, i32, f32)
+    names = ("means2d", "conics", "depths", "radii", "tiles_touched", "colors")
+    arrs = [(C.c_void_p * max(nv, 1))(*[_ptr(t, dt, nm) for t in seq]) for seq, dt, nm in zip(per_view, dts, names)]
+    st = _lib.vks_project_fwd_batch(C.byref(c), nv, karr, means.shape[0], _ptr(means, f32, "means"),
+                                    _ptr(log_scales, f32, "log_scales"), _ptr(quats, f32, "quats"),
+                                    _ptr(opacity_logits, f32, "opacity_logits"), _ptr(sh, f32, "sh"), *arrs,
+                                    _ptr(opacities, f32, "opacities"), _stream(stream))
+    _check("vks_project_fwd_batch", st)
 
 
 def vks_project_bwd_batch(cfg, cams, means, log_scales, quats, opacity_logits, sh, colors, radii, dmeans2d,

@@ -172,6 +172,32 @@ int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, con
                                                dquats, dopacity_logits, dsh, (cudaStream_t)stream));
 }
 
+int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,
+                          const float* means, const float* log_scales, const float* quats,
+                          const float* opacity_logits, const float* sh, float* const* means2d,
+                          float* const* conics, float* const* depths, int32_t* const* radii,
+                          int32_t* const* tiles_touched, float* const* colors, float* opacities,
+                          vks_stream_t stream) {
+    int st = config_ok(cfg);
+    if (st) return st;
+    if (n_views < 1 || n_views > 16 || !cams || n < 0) return VKS_ERR_INVALID_ARG;
+    if (!means2d || !conics || !depths || !radii || !tiles_touched || !colors) return VKS_ERR_INVALID_ARG;
+    for (int v = 0; v < n_views; v++) {
+        if (!camera_ok(cams + v) || cams[v].width != cams[0].width || cams[v].height != cams[0].height)
+            return VKS_ERR_INVALID_ARG;
+        if (n > 0 && (!means2d[v] || !conics[v] || !depths[v] || !radii[v] || !tiles_touched[v] || !colors[v]))
+            return VKS_ERR_INVALID_ARG;
+        if ((reinterpret_cast<uintptr_t>(means2d[v]) & 7) || (reinterpret_cast<uintptr_t>(radii[v]) & 7))
+            return VKS_ERR_INVALID_ARG;
+    }
+    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !opacities)) return VKS_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(quats) & 15) return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_project_fwd_batch(*cfg, n_views, cams, n, means, log_scales, quats, opacity_logits,
+                                                     sh, means2d, conics, depths, radii, tiles_touched, colors,
+                                                     opacities, (cudaStream_t)stream));
+}
+
 int vks_project_bwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,
                           const float* means, const float* log_scales, const float* quats,
                           const float* opacity_logits, const float* sh, const float* const* colors,

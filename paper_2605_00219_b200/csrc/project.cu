@@ -402,6 +402,266 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Batched forward: a step's views in one pass over the parameters.  Everything of §4.1 that
+// does not depend on the camera — the unit quaternion, Rq, the X64 scales, M = Rq diag(s), the
+// X64 opacity and the footprint's X64 log(255 rho) — is computed once per Gaussian, the SH row
+// staged once; the per-view part is the single-view kernel's, operation for operation, so every
+// view's outputs are bit-identical to vks_project_fwd's.
+constexpr int kMaxFwdViews = 16;
+
+struct FwdViewOut {
+    vks_camera cam;
+    CamConst cc;
+    float2* means2d;
+    float* conics;
+    float* depths;
+    int2* radii;
+    int* tiles;
+    float* colors;
+};
+
+struct BatchFwdParams {
+    vks_config cfg;
+    int64_t n;
+    int nv;
+    const float* __restrict__ means;
+    const float* __restrict__ ls;
+    const float4* __restrict__ quats;
+    const float* __restrict__ ologit;
+    const float* __restrict__ sh;
+    float* __restrict__ opac;  // view-independent: one array
+    FwdViewOut v[kMaxFwdViews];
+};
+
+// camera-independent part (steps 2-4, 12a and the footprint's k), pinned exactly as project_core
+struct GCore {
+    float M[9];
+    float rho, kk;
+    bool ok;
+};
+
+__device__ __forceinline__ void gauss_core(const vks_config& cfg, const float ls[3], float4 q, float o, GCore& G) {
+    const float qn = sqrtf(((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w);
+    G.ok = qn > 1e-12f;
+    const float w = q.x / qn, x = q.y / qn, y = q.z / qn, z = q.w / qn;
+    float Rq[9];
+    Rq[0] = 1.0f - 2.0f * (y * y + z * z);
+    Rq[1] = 2.0f * (x * y - w * z);
+    Rq[2] = 2.0f * (x * z + w * y);
+    Rq[3] = 2.0f * (x * y + w * z);
+    Rq[4] = 1.0f - 2.0f * (x * x + z * z);
+    Rq[5] = 2.0f * (y * z - w * x);
+    Rq[6] = 2.0f * (x * z - w * y);
+    Rq[7] = 2.0f * (y * z + w * x);
+    Rq[8] = 1.0f - 2.0f * (x * x + y * y);
+    float sc[3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) sc[j] = (float)exp((double)ls[j]);
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) G.M[j * 3 + c] = Rq[j * 3 + c] * sc[c];
+    G.rho = (float)(1.0 / (1.0 + exp(-(double)o)));
+    G.ok = G.ok && isfinite(G.rho);
+    G.kk = 0.0f;
+    if (cfg.footprint == VKS_FOOTPRINT_SUPPORT) {
+        G.ok = G.ok && G.rho >= 1.0f / 255.0f;
+        G.kk = G.ok ? (float)log(255.0 * (double)G.rho) : 0.0f;
+    }
+}
+
+// the camera-dependent part (steps 1, 5-9) given G
+__device__ __forceinline__ bool view_core(const vks_camera& cam, const vks_config& cfg, const CamConst& cc,
+                                          const float mu[3], const GCore& G, Core& k) {
+    const float* R = cam.R;
+    const float fx = cam.fx, fy = cam.fy, cx = cam.cx, cy = cam.cy;
+    k.t[0] = dot3(R + 0, mu) + cam.t[0];
+    k.t[1] = dot3(R + 3, mu) + cam.t[1];
+    k.t[2] = dot3(R + 6, mu) + cam.t[2];
+    const float tx = k.t[0], ty = k.t[1], tz = k.t[2];
+    if (!(tz > cfg.near_plane) || !isfinite(tz)) return false;
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+#pragma unroll
+        for (int c = 0; c < 3; c++)
+            k.Mc[j * 3 + c] = (R[j * 3 + 0] * G.M[0 * 3 + c] + R[j * 3 + 1] * G.M[1 * 3 + c]) + R[j * 3 + 2] * G.M[2 * 3 + c];
+    float txc = tx, tyc = ty;
+    if (cfg.fov_clamp) {
+        const float rxz = tx / tz, ryz = ty / tz;
+        txc = tz * fminf(cc.lxp, fmaxf(-cc.lxn, rxz));
+        tyc = tz * fminf(cc.lyp, fmaxf(-cc.lyn, ryz));
+    }
+    k.J00 = fx / tz;
+    k.J02 = -(fx * txc) / (tz * tz);
+    k.J11 = fy / tz;
+    k.J12 = -(fy * tyc) / (tz * tz);
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        k.K0[c] = k.J00 * k.Mc[0 * 3 + c] + k.J02 * k.Mc[2 * 3 + c];
+        k.K1[c] = k.J11 * k.Mc[1 * 3 + c] + k.J12 * k.Mc[2 * 3 + c];
+    }
+    k.A = dot3(k.K0, k.K0) + 0.3f;
+    k.B = dot3(k.K0, k.K1);
+    k.C = dot3(k.K1, k.K1) + 0.3f;
+    k.det = k.A * k.C - k.B * k.B;
+    if (!(k.det > 0.0f)) return false;
+    k.a = k.C / k.det;
+    k.b = -k.B / k.det;
+    k.c = k.A / k.det;
+    k.u = (fx * tx) / tz + cx;
+    k.v = (fy * ty) / tz + cy;
+    k.rho = G.rho;
+    return isfinite(k.u) && isfinite(k.v) && isfinite(k.a) && isfinite(k.b) && isfinite(k.c);
+}
+
+// footprint half-extents and rect (steps 10-11) with the footprint's k from G
+__device__ __forceinline__ bool footprint_rect_g(const Core& k, float kk, const vks_config& cfg, int TX, int TY,
+                                                 float& rxf, float& ryf, int& x0, int& x1, int& y0, int& y1) {
+    if (cfg.footprint == VKS_FOOTPRINT_SUPPORT) {
+        const float kp = kk * 1.001f + 1e-3f;
+        rxf = ceilf(sqrtf((2.0f * kp) * k.A)) + 1.0f;
+        ryf = ceilf(sqrtf((2.0f * kp) * k.C)) + 1.0f;
+    } else {
+        const float h = 0.5f * (k.A - k.C);
+        const float l1 = 0.5f * (k.A + k.C) + sqrtf(h * h + k.B * k.B);
+        rxf = ceilf(3.0f * sqrtf(l1));
+        ryf = rxf;
+    }
+    rxf = fminf(rxf, 16777216.0f);
+    ryf = fminf(ryf, 16777216.0f);
+    x0 = (int)fminf(fmaxf(floorf((k.u - rxf) * 0.0625f), 0.0f), (float)TX);
+    x1 = (int)fminf(fmaxf(ceilf((k.u + rxf) * 0.0625f), 0.0f), (float)TX);
+    y0 = (int)fminf(fmaxf(floorf((k.v - ryf) * 0.0625f), 0.0f), (float)TY);
+    y1 = (int)fminf(fmaxf(ceilf((k.v + ryf) * 0.0625f), 0.0f), (float)TY);
+    return (x1 - x0) * (y1 - y0) > 0;
+}
+
+template <int KS>
+__global__ void __launch_bounds__(kThreads) project_fwd_batch_kernel(const BatchFwdParams p) {
+    extern __shared__ float smem[];
+    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const unsigned lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const int64_t g0 = i - lane;
+    const bool valid = i < p.n;
+    const int K = (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);
+    float mu[3] = {0, 0, 0}, ls[3] = {0, 0, 0}, o = 0.0f;
+    float4 q = make_float4(1, 0, 0, 0);
+    if (valid) {
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            mu[c] = __ldg(p.means + 3 * i + c);
+            ls[c] = __ldg(p.ls + 3 * i + c);
+        }
+        q = __ldg(p.quats + i);
+        o = __ldg(p.ologit + i);
+    }
+    GCore G;
+    gauss_core(p.cfg, ls, q, o, G);
+    G.ok = G.ok && valid;
+    if (valid) p.opac[i] = G.ok ? G.rho : 0.0f;
+    // SH rows of every Gaussian that some view may show, staged once
+    const unsigned gmask = __ballot_sync(VKS_FULL_MASK, G.ok);
+    float* buf = nullptr;
+    if constexpr (KS > 0) {
+        buf = smem + warp * ShLayout<KS>::kWarpFloats;
+        if (gmask) {
+            sh_stage_async<KS>(p.sh, g0, gmask, buf);
+            cp_async_commit();
+            cp_async_wait_all();
+        }
+        __syncwarp();
+    }
+    const int TX = tiles_x(p.v[0].cam), TY = tiles_y(p.v[0].cam);
+    for (int v = 0; v < p.nv; v++) {
+        const FwdViewOut& V = p.v[v];
+        Core k;
+        float rxf = 0, ryf = 0;
+        int x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+        bool vis = G.ok && view_core(V.cam, p.cfg, V.cc, mu, G, k) &&
+                   footprint_rect_g(k, G.kk, p.cfg, TX, TY, rxf, ryf, x0, x1, y0, y1);
+        float col[3] = {0, 0, 0};
+        if (vis) {
+            float dh[3], dl, Y[16];
+            view_dir(V.cc, mu, dh, dl);
+            sh_basis(dh[0], dh[1], dh[2], K, Y);
+            const float* f;
+            if constexpr (KS > 0) f = buf + lane * ShLayout<KS>::SP;
+            else f = p.sh + 3 * (int64_t)p.cfg.sh_coeffs * i;
+            float acc[3];
+            if constexpr (vec_rows<KS>()) {
+                const float4* f4 = reinterpret_cast<const float4*>(f);
+#pragma unroll
+                for (int m = 0; m < ShLayout<KS>::S / 4; m++) {
+                    const float4 qv = f4[m];
+                    const float e4[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        const int e = 4 * m + t, l = e / 3, ch = e % 3;
+                        if (l == 0) acc[ch] = Y[0] * e4[t];
+                        else if (l < K) acc[ch] = acc[ch] + Y[l] * e4[t];
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++) {
+                    acc[ch] = Y[0] * f[ch];
+#pragma unroll
+                    for (int l = 1; l < 16; l++)
+                        if (l < K) acc[ch] = acc[ch] + Y[l] * f[3 * l + ch];
+                }
+            }
+            bool ok = true;
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) {
+                const float raw = acc[ch] + 0.5f;
+                ok = ok && isfinite(raw);
+                col[ch] = raw > 0.0f ? raw : 0.0f;
+            }
+            vis = ok;
+        }
+        if (!valid) continue;
+        if (vis) {
+            V.means2d[i] = make_float2(k.u, k.v);
+            V.conics[3 * i + 0] = k.a;
+            V.conics[3 * i + 1] = k.b;
+            V.conics[3 * i + 2] = k.c;
+            V.depths[i] = k.t[2];
+            V.radii[i] = make_int2((int)rxf, (int)ryf);
+            V.tiles[i] = (x1 - x0) * (y1 - y0);
+            V.colors[3 * i + 0] = col[0];
+            V.colors[3 * i + 1] = col[1];
+            V.colors[3 * i + 2] = col[2];
+        } else {  // whole rows (no read-for-merge of partial DRAM sectors)
+            V.means2d[i] = make_float2(0.0f, 0.0f);
+            V.conics[3 * i + 0] = 0.0f;
+            V.conics[3 * i + 1] = 0.0f;
+            V.conics[3 * i + 2] = 0.0f;
+            V.depths[i] = 0.0f;
+            V.radii[i] = make_int2(0, 0);
+            V.tiles[i] = 0;
+            V.colors[3 * i + 0] = 0.0f;
+            V.colors[3 * i + 1] = 0.0f;
+            V.colors[3 * i + 2] = 0.0f;
+        }
+    }
+}
+
+template <int KS>
+int launch_fwd_batch_t(const BatchFwdParams& p, cudaStream_t s) {
+    size_t sm = 0;
+    if constexpr (KS > 0) sm = sizeof(float) * kWarps * ShLayout<KS>::kWarpFloats;
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(project_fwd_batch_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sm);
+        if (e != cudaSuccess) return VKS_ERR_CUDA;
+    }
+    const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
+    project_fwd_batch_kernel<KS><<<blocks, kThreads, sm, s>>>(p);
+    return LaunchCheck::check();
+}
+
 template <int KS>
 size_t smem_bytes() {
     if constexpr (KS > 0) return sizeof(float) * kWarps * ShLayout<KS>::kWarpFloats;
@@ -444,6 +704,38 @@ int launch_project_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
         case 4: return al ? launch_fwd_t<4>(p, s) : launch_fwd_t<0>(p, s);
         case 1: return launch_fwd_t<1>(p, s);
         default: return launch_fwd_t<0>(p, s);
+    }
+}
+
+int launch_project_fwd_batch(const vks_config& cfg, int32_t n_views, const vks_camera* cams, int64_t n,
+                             const float* means, const float* log_scales, const float* quats,
+                             const float* opacity_logits, const float* sh, float* const* means2d,
+                             float* const* conics, float* const* depths, int32_t* const* radii,
+                             int32_t* const* tiles_touched, float* const* colors, float* opacities, cudaStream_t s) {
+    if (n == 0) return VKS_OK;
+    if (n_views < 1 || n_views > kMaxFwdViews) return VKS_ERR_INVALID_ARG;
+    BatchFwdParams p{};
+    p.cfg = cfg; p.n = n; p.nv = n_views;
+    p.means = means; p.ls = log_scales; p.quats = reinterpret_cast<const float4*>(quats);
+    p.ologit = opacity_logits; p.sh = sh; p.opac = opacities;
+    for (int v = 0; v < n_views; v++) {
+        FwdViewOut& V = p.v[v];
+        V.cam = cams[v];
+        V.cc = cam_const(cams[v]);
+        V.means2d = reinterpret_cast<float2*>(means2d[v]);
+        V.conics = conics[v];
+        V.depths = depths[v];
+        V.radii = reinterpret_cast<int2*>(radii[v]);
+        V.tiles = tiles_touched[v];
+        V.colors = colors[v];
+    }
+    const bool al = aligned16(sh);
+    switch (cfg.sh_coeffs) {
+        case 16: return al ? launch_fwd_batch_t<16>(p, s) : launch_fwd_batch_t<0>(p, s);
+        case 9: return launch_fwd_batch_t<9>(p, s);
+        case 4: return al ? launch_fwd_batch_t<4>(p, s) : launch_fwd_batch_t<0>(p, s);
+        case 1: return launch_fwd_batch_t<1>(p, s);
+        default: return launch_fwd_batch_t<0>(p, s);
     }
 }
 

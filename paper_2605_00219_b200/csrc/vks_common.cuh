@@ -115,6 +115,11 @@ int launch_project_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
                        const float* dconics, const float* dcolors, const float* dopacities,
                        float* dmeans, float* dlog_scales, float* dquats, float* dopacity_logits,
                        float* dsh, cudaStream_t s);
+int launch_project_fwd_batch(const vks_config& cfg, int32_t n_views, const vks_camera* cams, int64_t n,
+                             const float* means, const float* log_scales, const float* quats,
+                             const float* opacity_logits, const float* sh, float* const* means2d,
+                             float* const* conics, float* const* depths, int32_t* const* radii,
+                             int32_t* const* tiles_touched, float* const* colors, float* opacities, cudaStream_t s);
 int launch_project_bwd_batch(const vks_config& cfg, int32_t n_views, const vks_camera* cams, int64_t n,
                              const float* means, const float* log_scales, const float* quats,
                              const float* opacity_logits, const float* sh, const float* const* colors,

@@ -442,3 +442,32 @@ def test_project_bwd_batch_equals_sum_of_views(oracle_lib, coeffs, deg, nv):
     for k in G:
         rule = grad_rule(to_np(G2[k]), 2 * to_np(G[k]).astype(np.float64), mass=2 * mass_o[k], rel=1e-4)
         assert rule["fail"] == 0, (k, "accumulate", rule)
+
+
+@pytest.mark.parametrize("coeffs,deg,nv,fp", [(16, 3, 5, 0), (9, 2, 3, 0), (4, 1, 2, 1), (1, 0, 1, 0)])
+def test_project_fwd_batch_bit_exact(oracle_lib, coeffs, deg, nv, fp):
+    """vks_project_fwd_batch: every view's outputs bit-identical to vks_project_fwd for that view
+    and to the oracle's O1 (P1), the opacities equal for every visible row."""
+    import torch
+    import paper_2605_00219_b200 as P
+    s = synth.make_scene(30001, "outdoor", 90 + nv)
+    s["sh"] = np.ascontiguousarray(s["sh"][:, :coeffs])
+    cams = synth.ring_cameras(200, 150, "outdoor", 8)[:nv]
+    cfg = synth.default_render_config(deg, sh_coeffs=coeffs, footprint=fp)
+    params = P.GaussianParams.from_host(s)
+    n = params.n
+    e = lambda *sh, dt=torch.float32: torch.empty(*sh, dtype=dt, device="cuda")
+    outs = [dict(means2d=e(n, 2), conics=e(n, 3), depths=e(n), radii=e(n, 2, dt=torch.int32),
+                 tiles=e(n, dt=torch.int32), colors=e(n, 3)) for _ in range(nv)]
+    opac = e(n)
+    P.vks_project_fwd_batch(cfg, cams, params.means, params.log_scales, params.quats, params.opacity_logits, params.sh,
+                            [o["means2d"] for o in outs], [o["conics"] for o in outs], [o["depths"] for o in outs],
+                            [o["radii"] for o in outs], [o["tiles"] for o in outs], [o["colors"] for o in outs], opac)
+    torch.cuda.synchronize()
+    for v, (cam, o) in enumerate(zip(cams, outs)):
+        g = {k: to_np(t) for k, t in o.items()}
+        g["tiles_touched"] = g.pop("tiles")
+        g["opacities"] = to_np(opac)
+        ref = oracle_lib.project_fwd(cfg, cam, s)
+        nvis = check_projection(ref, g, f"fwd_batch_v{v}")
+        assert nvis > 1000

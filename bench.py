@@ -104,9 +104,11 @@ def algorithmic_bytes(n, vis, m, dpasses=4, batch=1, K=16):
     (DESIGN.md §6).  Parameters are fp32; sh has K coefficients per channel."""
     sh = 12 * K
     return dict(
-        # geometry + opacity of every Gaussian (44 B), SH rows of the visible ones; radii + tiles
-        # written for all (12 B), the other 40 B of outputs for the visible
-        project_fwd=44 * n + sh * vis + 12 * n + 40 * vis,
+        # batched forward, per view: the parameter rows (44 B geometry + opacity, the SH row) read
+        # and the opacity (4 B) written once per batch of `batch` views (SH for all n: upper bound
+        # of the Gaussians some view shows); radii + tiles written for all (12 B), the other 36 B
+        # of outputs for the visible
+        project_fwd=(44 + sh) * n / batch + 4 * n / batch + 12 * n + 36 * vis,
         # id-order scan (read tiles twice, write offsets) + compaction of the visible (read depth,
         # means2d, radii; write depth key, id, rect code) + `dpasses` depth passes over V (count
         # 4 B, scatter 8 B in / 8 B out) + depth-order scan (ids + gathered rect codes in, rect
@@ -192,10 +194,23 @@ def run_ours(args):
     vbuf = []
     for _ in range(B):
         g2d = torch.zeros(9 * n, dtype=torch.float32, device="cuda")
-        vbuf.append(dict(colors=torch.empty(n, 3, device="cuda"),
+        vbuf.append(dict(means2d=torch.empty(n, 2, device="cuda"), conics=torch.empty(n, 3, device="cuda"),
+                         depths=torch.empty(n, device="cuda"), tiles=torch.empty(n, dtype=torch.int32, device="cuda"),
+                         colors=torch.empty(n, 3, device="cuda"),
                          radii=torch.empty(n, 2, dtype=torch.int32, device="cuda"), g2d=g2d,
                          dm2=g2d[: 2 * n].view(n, 2), dcon=g2d[2 * n: 5 * n].view(n, 3),
                          dcol=g2d[5 * n: 8 * n].view(n, 3), dop=g2d[8 * n:]))
+    opac = torch.empty(n, device="cuda")  # view-independent
+
+    def project_fwd_batch(vcams, st):
+        """The batch's projection forward: one pass over the parameters for all its views (row a1)."""
+        nb = len(vcams)
+        with torch.cuda.stream(st):
+            P.vks_project_fwd_batch(cfg, vcams, params.means, params.log_scales, params.quats, params.opacity_logits,
+                                    params.sh, [vbuf[j]["means2d"] for j in range(nb)],
+                                    [vbuf[j]["conics"] for j in range(nb)], [vbuf[j]["depths"] for j in range(nb)],
+                                    [vbuf[j]["radii"] for j in range(nb)], [vbuf[j]["tiles"] for j in range(nb)],
+                                    [vbuf[j]["colors"] for j in range(nb)], opac)
 
     def view_path(rend, vb, cam, dL, st, ev=None, copies=None):
         """One view's forward and raster backward on stream `st` (two views of a batch run
@@ -212,16 +227,12 @@ def run_ours(args):
         with torch.cuda.stream(st):
             if copies is not None:
                 st.wait_event(slot["img_free"])              # the previous image has left rend.image
-            if ev is not None: ev[0].record(st)
-            P.vks_project_fwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
-                              params.sh, rend.means2d, rend.conics, rend.depths, vb["radii"], rend.tiles,
-                              vb["colors"], rend.opacities)
             if ev is not None: ev[1].record(st)
-            m = P.vks_bin_sort(cam, rend.means2d, vb["radii"], rend.depths, rend.tiles, rend.offsets, None,
+            m = P.vks_bin_sort(cam, vb["means2d"], vb["radii"], vb["depths"], vb["tiles"], rend.offsets, None,
                                rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
             rend.num_isects = m
             if ev is not None: ev[2].record(st)
-            P.vks_raster_fwd(cfg, cam, rend.means2d, rend.conics, vb["colors"], rend.opacities, vb["radii"],
+            P.vks_raster_fwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],
                              rend.vals, rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib,
                              tile_order=rend.tile_order)
             if copies is not None:
@@ -234,7 +245,7 @@ def run_ours(args):
             if ev is not None: ev[3].record(st)
             vb["g2d"].zero_()
             if ev is not None: ev[4].record(st)
-            P.vks_raster_bwd(cfg, cam, rend.means2d, rend.conics, vb["colors"], rend.opacities, vb["radii"],
+            P.vks_raster_bwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],
                              rend.vals, rend.tile_offsets, rend.T_final, rend.n_contrib, dL, vb["dm2"], vb["dcon"],
                              vb["dcol"], vb["dop"], tile_order=rend.tile_order)
             if ev is not None: ev[5].record(st)
@@ -258,23 +269,24 @@ def run_ours(args):
                                     g["dopacity_logits"], g["dsh"])
 
     def step(s, copies=None):
-        """One training step's hot path: a batch of B views per rank, alternating over S streams
-        through projection, binning, raster forward and raster backward; then one batched
-        projection backward for the batch (row a8) and the allreduce (row a9; no-op at N = 1).
-        The batch starts after the previous step's allreduce (an optimizer would run there)."""
+        """One training step's hot path: a batch of B views per rank — one batched projection
+        forward (row a1), then binning, raster forward and raster backward per view, alternating
+        over S streams, one batched projection backward (row a8) and the allreduce (row a9; no-op
+        at N = 1).  The batch starts after the previous step's allreduce (an optimizer would run
+        there)."""
+        vviews = [my_views[(s * B + j) % len(my_views)] for j in range(B)]
+        vcams = [cams[v] for v in vviews]
+        project_fwd_batch(vcams, main)  # after the previous step's allreduce (main stream order)
         start = torch.cuda.Event()
         start.record(main)
         for st in streams:
             st.wait_event(start)
         m = 0
-        vcams = []
-        for j in range(B):
-            v = my_views[(s * B + j) % len(my_views)]
+        for j, v in enumerate(vviews):
             k = j % S
             cp = None if copies is None else (copies[0][v], copies[1][k])
             m, done = view_path(rends[k], vbuf[j], cams[v], dLs[v], streams[k], copies=cp)
             main.wait_event(done)
-            vcams.append(cams[v])
         project_bwd_batch(vcams, main)
         if copies is not None:
             main.wait_stream(copy_stream)  # every image of the batch has reached the host
@@ -315,10 +327,16 @@ def run_ours(args):
     # events between the entry points; medians over the views
     nv = max(B, min(64, (args.steps // B + 1) * B))
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages))] for _ in range(nv)]
-    pb_ms = []
+    pb_ms, pf_ms = [], []
     torch.cuda.synchronize()
     for i in range(nv):
         v = my_views[i % len(my_views)]
+        if i % B == 0:  # the batch's projection forward, per view
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(main)
+            project_fwd_batch([cams[my_views[q % len(my_views)]] for q in range(i, i + B)], main)
+            e1.record(main)
+            pf_ms.append((e0, e1))
         view_path(rends[0], vbuf[i % B], cams[v], dLs[v], main, ev=evs[i])
         if i % B == B - 1:  # the batch's projection backward, per view
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -328,20 +346,23 @@ def run_ours(args):
             pb_ms.append((e0, e1))
     torch.cuda.synchronize()
     st_ms = {name: statistics.median([evs[i][q].elapsed_time(evs[i][q + 1]) for i in range(nv)])
-             for q, name in enumerate(stages[:-1])}
+             for q, name in enumerate(stages[:-1]) if q > 0}
+    st_ms["project_fwd"] = statistics.median([a.elapsed_time(b) for a, b in pf_ms]) / B
     st_ms["project_bwd"] = statistics.median([a.elapsed_time(b) for a, b in pb_ms]) / B
+    st_ms = {k: st_ms[k] for k in stages}
     rend = rends[0]
 
     # --- workload statistics (untimed): visible count, M, raster pair counts of the last view
-    vis = int((rend.tiles > 0).sum().item())
+    vl = vbuf[(nv - 1) % B]  # the last view's projection outputs
+    vis = int((vl["tiles"] > 0).sum().item())
     m_last = rend.num_isects
     stats = torch.zeros(6, dtype=torch.int64, device="cuda")
-    vl = vbuf[(nv - 1) % B]  # the last view's colours / radii
-    P.vks_raster_fwd_stats(cfg, cams[my_views[(nv - 1) % len(my_views)]], rend.means2d,
-                           rend.conics, vl["colors"], rend.opacities, vl["radii"], rend.vals, rend.tile_offsets, stats)
+    P.vks_raster_fwd_stats(cfg, cams[my_views[(nv - 1) % len(my_views)]], vl["means2d"],
+                           vl["conics"], vl["colors"], opac, vl["radii"], rend.vals, rend.tile_offsets, stats,
+                           tile_order=rend.tile_order)
     visited, composited, evaluated, replayed, warp_entries, warp_entries_comp = (int(x) for x in stats.tolist())
     # depth passes the sort ran: <= 8-bit digits over the visible depth-bit range
-    dvis = rend.depths[rend.tiles > 0].view(torch.int32).to(torch.int64)
+    dvis = vl["depths"][vl["tiles"] > 0].view(torch.int32).to(torch.int64)
     drange = int(dvis.max().item() - dvis.min().item()) if dvis.numel() else 0
     dpasses = max(1, (drange.bit_length() + 7) // 8)
     ab = algorithmic_bytes(n, vis, m_last, dpasses, batch=B)
@@ -368,11 +389,11 @@ def run_ours(args):
                     unit=d["unit"], frac=round(d["frac"], 4), traffic=measured_traffic(dom),
                     peak_source=(pk["src"] + (" HBM copy (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
                                               f" FP32 FMA: 148 SM x 128 lanes x 2 flop x {clock_mhz:.0f} MHz")))
-    # our kernels per view: project_fwd; bin_sort = id scan (3) + dpasses x (count, scan, scatter)
-    # + depth-order scan (3) + rect diff + tile count + tile passes x 3; raster fwd; raster bwd;
-    # plus one batched project bwd per step
+    # our kernels per view: bin_sort = id scan (3) + dpasses x (count, scan, scatter) + depth-order
+    # scan (3) + rect diff + tile count + tile passes x 3; raster fwd; raster bwd; plus one batched
+    # project fwd and one batched project bwd per step
     tp = max(1, ((rend.n_tiles - 1).bit_length() + 7) // 8)
-    gpu_launches = ((1 + (3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1) * B + 1) * args.steps
+    gpu_launches = (((3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1) * B + 2) * args.steps
 
     out = dict(metric=METRIC, value=round(value, 3), unit="iters/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(elapsed_ms / args.steps, 4), higher_is_better=True,
@@ -382,9 +403,9 @@ def run_ours(args):
                            streams=S, visible=vis, num_isects=m_last,
                            l2="inputs larger than L2 (params 1.37 GB, keys+vals 0.22 GB per view), no flush",
                            parallelism=f"view-sharded dp{world}",
-                           step=(f"{B} ring views per rank through projection, binning and both raster passes (two "
-                                 f"in flight on {S} streams), one batched projection backward for the {B} views, "
-                                 f"then one allreduce; unit = views")),
+                           step=(f"{B} ring views per rank: one batched projection forward, binning and both "
+                                 f"raster passes per view (two in flight on {S} streams), one batched projection "
+                                 f"backward, then one allreduce; unit = views")),
                stages_ms={k: round(v, 4) for k, v in st_ms.items()},
                stage_roofline={k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                                for k, v in per_stage.items()},

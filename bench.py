@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="bicycle")
     ap.add_argument("--views-per-rank", type=int, default=8, help="views per rank per step (the batch)")
-    ap.add_argument("--streams", type=int, default=2, help="views in flight per rank")
+    ap.add_argument("--streams", type=int, default=3, help="views in flight per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows-every", type=int, default=8, help="oracle raster sample: every k-th tile row")

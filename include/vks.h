@@ -117,7 +117,8 @@ int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
 
 /*
  * vks_bin_sort_workspace_bytes — device workspace needed by vks_bin_sort for
- * n Gaussians, a key capacity `capacity` and n_tiles tiles.
+ * n Gaussians, a key capacity `capacity` and n_tiles tiles (~60 B per Gaussian + 16 B
+ * per key slot).  Returns 0 for n < 0 or n_tiles < 1.
  */
 size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles);
 
@@ -137,7 +138,7 @@ size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles
  *   keys_unsorted / vals_unsorted (nullable, debug; [capacity] like keys/vals): the pre-sort pairs.
  * Tile grids of >= 2^20 tiles return VKS_ERR_INVALID_ARG.
  * If M > capacity (or M >= 2^30) returns VKS_ERR_CAPACITY after writing
- * *num_isects, touching nothing else; the call is idempotent, so the caller
+ * offsets and *num_isects, touching no other output; the call is idempotent, so the caller
  * regrows and calls again.  Synchronises `stream` once (to read M).
  * workspace: device memory of >= vks_bin_sort_workspace_bytes(n, capacity, n_tiles).
  */

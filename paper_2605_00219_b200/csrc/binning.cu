@@ -529,8 +529,8 @@ __global__ void __launch_bounds__(kKeysThreads) keys_debug_kernel(vks_camera cam
             const int tx = s_x0[warp][pos] + (k - ry * ww);
             const int ty = s_y0[warp][pos] + ry;
             const u32 t = (u32)(ty * TX + tx);
-            keys64[base + e] = ((u64)t << 32) | (u64)s_db[warp][pos];
-            tvals[base + e] = (u32)(r0 + pos);
+            if (keys64) keys64[base + e] = ((u64)t << 32) | (u64)s_db[warp][pos];
+            if (tvals) tvals[base + e] = (u32)(r0 + pos);
         }
         __syncwarp();
     }
@@ -979,8 +979,10 @@ __device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0
             rc_n = __ldg(src.rc + gn + lane);
             id_n = __ldg(src.sid + gn + lane);
         }
-        // the group covers slots [W, gend): up to the next group's first slot (or c1)
-        const u32 gend = min(c1, __shfl_sync(VKS_FULL_MASK, a_n, 0));
+        // the group covers slots [W, gend): up to the end of its last Gaussian's keys (= the next
+        // group's first slot; known without waiting for the next group's loads), or c1
+        const u32 end = a == 0xFFFFFFFFu ? 0xFFFFFFFFu : a + (u32)rect_tiles(rc);
+        const u32 gend = min(c1, __shfl_sync(VKS_FULL_MASK, end, 31));
         // owner lane of slot W - 1: lane 0 if its Gaussian started before W (only the chunk's
         // first group), else none (-1: lane 0's start at W is counted in the first window)
         int base = __shfl_sync(VKS_FULL_MASK, a, 0) < W ? 0 : -1;
@@ -1318,9 +1320,8 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     u64* keys64 = reinterpret_cast<u64*>(keys);
     // debug: the pre-sort keys in id order, exactly as "Generate Keys" defines them
     if (keys_unsorted || vals_unsorted) {
-        u32* vtmp = vals_unsorted ? vals_unsorted : w.tv[1];
-        u64* ktmp = keys_unsorted ? reinterpret_cast<u64*>(keys_unsorted) : reinterpret_cast<u64*>(w.tk[0]);
-        int st = launch_keys_debug(cam, n, tiles_touched, means2d, radii, depths, offsets, vtmp, ktmp, s);
+        int st = launch_keys_debug(cam, n, tiles_touched, means2d, radii, depths, offsets, vals_unsorted,
+                                   reinterpret_cast<u64*>(keys_unsorted), s);
         if (st) return st;
     }
     // 2. depth sort of the V visible Gaussians (compacted in id order into dk[1]/dv[1] by the scan)
@@ -1355,9 +1356,9 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     if ((st = launch_tile_count(TX, TY, w.diff, tile_offsets, tile_order, s))) return st;
     // 5. stable tile passes over the M (tile, id) pairs; the first expands the keys from the rect
     //    codes itself, the last writes the caller's vals (+ u64 keys on request)
+    const ExpandSrc src{w.rcs, w.doff, sid, w.first, (u32)V, (u32)M, TX};
     TilePlan plan = tile_plan(n_tiles);
     if (plan.passes == 0) plan = TilePlan{1, 1};  // one tile: a trivial 1-bit pass keeps the path uniform
-    const ExpandSrc src{w.rcs, w.doff, sid, w.first, (u32)V, (u32)M, TX};
     if (plan.passes == 1)
         return launch_keys_pass_bits<kPassTileLast>(plan.dbits, src, nullptr, vals, pass_bufs(kDepthPasses), depths,
                                                     keys64, s);

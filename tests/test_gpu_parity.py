@@ -321,11 +321,11 @@ def test_patch_culling_and_ppt_variants_agree(fp, monkeypatch):
     report(f"cull_fp{fp}", dict(stats={"/".join(k): v for k, v in stats.items()}))
 
 
-@pytest.mark.parametrize("W,H", [(16, 16), (200, 150), (4200, 4000)])
+@pytest.mark.parametrize("W,H", [(16, 16), (200, 150), (1600, 1000), (2000, 1600), (4200, 4000)])
 def test_binning_tile_pass_counts(oracle_lib, W, H):
-    """Binning bit-exact for 1 tile (trivial pass), 130 tiles (one 8-bit pass) and 65,750 tiles
-    (three 6-bit passes), with a few Gaussians large enough that one Gaussian's keys span
-    several 4096-slot key blocks."""
+    """Binning bit-exact for 1 tile (trivial pass), 130 tiles (one 8-bit pass), 6,300 and 12,500
+    tiles (two 7-bit passes) and 65,750 tiles (three 6-bit passes), with a few Gaussians large
+    enough that one Gaussian's keys span several 4096-slot key blocks."""
     s = synth.make_scene(30000, "outdoor", 80)
     cam = synth.ring_cameras(W, H, "outdoor", 8)[6]
     eye = -cam["R"].astype(np.float64).T @ cam["t"].astype(np.float64)
@@ -341,7 +341,7 @@ def test_binning_tile_pass_counts(oracle_lib, W, H):
     m = check_binning(oracle_lib, cam, g, f"bin_{W}x{H}")
     assert m > 0
     if W * H > 10**6:
-        assert int(g["tiles_touched"].max()) > 3 * 4096  # one Gaussian spans several key blocks
+        assert int(g["tiles_touched"].max()) > 4096  # one Gaussian's keys span key blocks
 
 
 @pytest.mark.parametrize("case", ["equal_depths", "wide_range"])

@@ -1,5 +1,5 @@
-"""One batch's projection backward between cudaProfilerStart/Stop (8 ring views rendered and
-raster-backpropagated first, untimed), for `ncu --profile-from-start off ...`."""
+"""One batch's projection forward and backward between cudaProfilerStart/Stop (8 ring views
+rendered and raster-backpropagated first, untimed), for `ncu --profile-from-start off ...`."""
 import os
 import sys
 
@@ -38,9 +38,18 @@ def batch():
                             g["dopacity_logits"], g["dsh"])
 
 
+def fwd_batch():
+    P.vks_project_fwd_batch(cfg, [cams[v % 8] for v in range(B)], params.means, params.log_scales, params.quats,
+                            params.opacity_logits, params.sh, [r.means2d for r in views], [r.conics for r in views],
+                            [r.depths for r in views], [r.radii for r in views], [r.tiles for r in views],
+                            [r.colors for r in views], views[0].opacities)
+
+
+fwd_batch()
 batch()
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
+fwd_batch()
 batch()
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()

@@ -11,8 +11,8 @@ import sys
 STAGES = {  # bench stage -> kernel-name regex of its dominant kernel
     "raster_bwd": r"raster_bwd_kernel",
     "raster_fwd": r"raster_fwd_kernel",
-    "project_fwd": r"project_fwd_kernel",
-    "project_bwd": r"project_bwd_kernel",
+    "project_fwd": r"project_fwd_batch_kernel",  # per launch = one batch of 8 views
+    "project_bwd": r"project_bwd_batch_kernel",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
@@ -34,8 +34,8 @@ def main():
                 wr = float(r[h.index("dram__bytes_write.sum")]) * SCALE[units[h.index("dram__bytes_write.sum")]]
                 res[stage] = dict(kernel=re.sub(r"\(.*", "", name), dram_bytes_read=rd, dram_bytes_write=wr,
                                   dram_bytes_per_launch=rd + wr)
-    json.dump(dict(source=rep.split("/")[-1], note="one ncu --set full capture of tools/profile_step.py "
-                   "(bicycle, view 0); per launch", kernels=res), open(out, "w"), indent=1)
+    json.dump(dict(source=rep.split("/")[-1], note="one ncu --set full capture of tools/profile_bench_step.py "
+                   "(bicycle: batched projection of 8 views, view 0's raster passes); per launch", kernels=res), open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
 

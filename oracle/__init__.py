@@ -243,3 +243,38 @@ def full_backward(cfg, cam, scene, dL, row_mask=None, want_mass=False, nthreads=
     pb = project_bwd(cfg, cam, scene, r, nthreads=nthreads)
     r.update(pb)
     return r
+
+
+# ---- the optimizer step (Adam with bias correction) -------------------
+ADAM_GROUPS = ("means", "log_scales", "quats", "opacity_logits", "sh")
+
+
+def adam_step(params, grads, m, v, lr, beta1=0.9, beta2=0.999, eps=1e-8, step=1):
+    """One Adam step on every parameter group (vko_adam_group), then the quaternion
+    re-normalisation (vko_quat_renorm).  params/grads/m/v: dicts of fp32 arrays keyed by
+    ADAM_GROUPS; lr: dict with a learning rate per group, where "sh" may be a pair (lr of SH
+    coefficient 0, lr of the others).  Returns new (params, m, v) dicts (inputs untouched)."""
+    L = lib()
+    L.vko_adam_group.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                 C.c_double, C.c_double, C.c_double, C.c_int32]
+    L.vko_quat_renorm.argtypes = [C.c_int64, C.c_void_p]
+    P, M, Vv = {}, {}, {}
+    for k in ADAM_GROUPS:
+        p = np.ascontiguousarray(params[k], np.float32).copy()
+        mm = np.ascontiguousarray(m[k], np.float32).copy()
+        vv = np.ascontiguousarray(v[k], np.float32).copy()
+        g = np.ascontiguousarray(grads[k], np.float32)
+        lk = lr[k]
+        if k == "sh" and isinstance(lk, (tuple, list)):  # coefficient 0 and the rest: two groups
+            n = p.shape[0]
+            p3, m3, v3, g3 = (a.reshape(n, -1, 3) for a in (p, mm, vv, g))
+            for sl, lrs in ((slice(0, 1), lk[0]), (slice(1, None), lk[1])):
+                ps, ms, vs, gs = (np.ascontiguousarray(a[:, sl]) for a in (p3, m3, v3, g3))
+                L.vko_adam_group(ps.size, _p(ps), _p(ms), _p(vs), _p(gs), lrs, beta1, beta2, eps, step)
+                p3[:, sl], m3[:, sl], v3[:, sl] = ps, ms, vs
+        else:
+            L.vko_adam_group(p.size, _p(p), _p(mm), _p(vv), _p(g), float(lk), beta1, beta2, eps, step)
+        if k == "quats":
+            L.vko_quat_renorm(p.shape[0], _p(p))
+        P[k], M[k], Vv[k] = p, mm, vv
+    return P, M, Vv

@@ -985,3 +985,30 @@ void vko_project_bwd_f64(const vko_config* cfg, const vko_camera* cam, int64_t n
                      dquats + 4 * i, &dopacity_logits[i], dsh + S * i);
     }
 }
+
+/* ---- optimizer: Adam with bias correction, S:252-259 -------------------- */
+void vko_adam_group(int64_t n, float* p, float* m, float* v, const float* g, double lr, double b1,
+                    double b2, double eps, int32_t t) {
+    const double bc1 = 1.0 - pow(b1, (double)t), bc2 = 1.0 - pow(b2, (double)t);
+    for (int64_t i = 0; i < n; i++) {
+        const double gi = (double)g[i];
+        const double mi = b1 * (double)m[i] + (1.0 - b1) * gi;
+        const double vi = b2 * (double)v[i] + (1.0 - b2) * gi * gi;
+        const double mhat = mi / bc1, vhat = vi / bc2;
+        p[i] = (float)((double)p[i] - lr * mhat / (sqrt(vhat) + eps));
+        m[i] = (float)mi;
+        v[i] = (float)vi;
+    }
+}
+
+void vko_quat_renorm(int64_t n, float* q) {
+    for (int64_t i = 0; i < n; i++) {
+        const double a = q[4 * i], b = q[4 * i + 1], c = q[4 * i + 2], d = q[4 * i + 3];
+        const double nn = sqrt(a * a + b * b + c * c + d * d);
+        if (!(nn > 0.0)) continue;
+        q[4 * i] = (float)(a / nn);
+        q[4 * i + 1] = (float)(b / nn);
+        q[4 * i + 2] = (float)(c / nn);
+        q[4 * i + 3] = (float)(d / nn);
+    }
+}

@@ -152,6 +152,23 @@ void vko_project_bwd_f64(const vko_config* cfg, const vko_camera* cam, int64_t n
                          double* dmeans, double* dlog_scales, double* dquats,
                          double* dopacity_logits, double* dsh);
 
+/* ---- the optimizer step after the path ------------------------------ */
+
+/* Adam with bias correction on one parameter group of n fp32 elements (SPEC S:252-259
+ * "adam_step": "standard Adam with bias correction per parameter group"; PAPER P:76 row "Proj
+ * Bwd + Optimizer").  For step t >= 1, element-wise, in fp64 with one rounding to fp32 at the end:
+ *     m <- b1 m + (1 - b1) g
+ *     v <- b2 v + (1 - b2) g^2
+ *     p <- p - lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+ * Parity pins (tests/test_oracle_pins.py): SPEC S:259 worked example, zero-gradient identity
+ * (S:258), the closed form of a constant gradient, S:260 (x^2 decreases). */
+void vko_adam_group(int64_t n, float* p, float* m, float* v, const float* g, double lr, double b1,
+                    double b2, double eps, int32_t t);
+
+/* Quaternion re-normalisation after the step ("rotations re-normalized after the step"):
+ * each row of 4 divided by its fp64 norm (rows of norm 0 left unchanged). */
+void vko_quat_renorm(int64_t n, float* q);
+
 #ifdef __cplusplus
 }
 #endif

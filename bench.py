@@ -364,6 +364,24 @@ def run_ours(args):
     st_ms = {name: statistics.median([evs[i][q].elapsed_time(evs[i][q + 1]) for i in range(nv)])
              for q, name in enumerate(stages[:-1]) if q > 0}
     st_ms["project_fwd"] = statistics.median([a.elapsed_time(b) for a, b in pf_ms]) / B
+    # the optimizer after the path (not part of the step or of `value`): one
+    # Adam step over every parameter group per batch, timed on its own
+    groups = [params.means, params.log_scales, params.quats, params.opacity_logits, params.sh]
+    gr = params.grads()
+    grads = [gr[k] for k in ("dmeans", "dlog_scales", "dquats", "dopacity_logits", "dsh")]
+    mom = [torch.zeros_like(t) for t in groups]
+    vel = [torch.zeros_like(t) for t in groups]
+    lrs = dict(means=1.6e-4, log_scales=5e-3, quats=1e-3, opacity_logits=5e-2, sh=(2.5e-3, 1.25e-4))
+    adam_ev = []
+    for t in range(1, 6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        P.vks_adam_step(P.make_adam_config(lrs, step=t), groups, grads, mom, vel)
+        e1.record(main)
+        adam_ev.append((e0, e1))
+    torch.cuda.synchronize()
+    adam_ms = statistics.median([a.elapsed_time(b) for a, b in adam_ev[1:]])
+    del mom, vel
     st_ms["project_bwd"] = statistics.median([a.elapsed_time(b) for a, b in pb_ms]) / B
     st_ms = {k: st_ms[k] for k in stages}
     rend = rends[0]
@@ -392,6 +410,11 @@ def run_ours(args):
         per_stage[k] = dict(ms=st_ms[k], bound="hbm", achieved=gbs, peak=pk["hbm_gbs"], unit="GB/s",
                             frac=gbs / pk["hbm_gbs"], algorithmic_bytes=ab[k])
     per_stage["bin_sort"]["gkeys_per_s"] = m_last / (st_ms["bin_sort"] * 1e-3) / 1e9
+    adam_bytes = 28 * n * (11 + 3 * params.sh.shape[1])  # p, g, m, v in; p, m, v out (fp32)
+    optimizer = dict(row="f1 (SURVEY 8f): vks_adam_step, once per step after the allreduce; not in value",
+                     ms_per_step=round(adam_ms, 4), bound="hbm", algorithmic_bytes=adam_bytes,
+                     achieved=round(adam_bytes / (adam_ms * 1e-3) / 1e9, 1), peak=pk["hbm_gbs"], unit="GB/s",
+                     frac=round(adam_bytes / (adam_ms * 1e-3) / 1e9 / pk["hbm_gbs"], 4))
     per_stage["bin_sort"]["depth_passes"] = dpasses
     for k in ("raster_fwd", "raster_bwd"):
         tf = fl[k] / (st_ms[k] * 1e-3) / 1e12
@@ -430,7 +453,7 @@ def run_ours(args):
                raster_work=dict(visited_pairs=visited, composited_pairs=composited, evaluated_pairs=evaluated,
                                 replayed_pairs=replayed, warp_entries=warp_entries,
                                 warp_entries_composited=warp_entries_comp),
-               roofline=roofline, gpu_launches=gpu_launches, clocks=clk)
+               roofline=roofline, gpu_launches=gpu_launches, clocks=clk, optimizer=optimizer)
 
     if not args.no_e2e:
         # the same steps with HOST buffers: each view's dL/dimage copied in from pinned host

@@ -267,6 +267,33 @@ int vks_project_bwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
                           float* dmeans, float* dlog_scales, float* dquats, float* dopacity_logits,
                           float* dsh, vks_stream_t stream);
 
+/* ---- the optimizer step after the path ---------------------------------
+ *
+ * vks_adam_step — Adam with bias correction per parameter group ("adam_step":
+ * "standard Adam with bias correction per parameter group"; PAPER P:76 row "Proj Bwd +
+ * Optimizer"), quaternions re-normalised after the step.  For step t = acfg->step >= 1,
+ * element-wise in fp32:
+ *     m <- b1 m + (1 - b1) g;   v <- b2 v + (1 - b2) g^2
+ *     p <- p - lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+ * Groups (index into params / grads / m / v): 0 means [n,3], 1 log_scales [n,3], 2 quats [n,4]
+ * (then q <- q / |q| per row), 3 opacity_logits [n], 4 sh [n, sh_coeffs, 3]; lr[0..3] per
+ * group, lr[4] for SH coefficient 0 and lr[5] for the others.
+ *   params, m, v: HOST arrays of 5 DEVICE fp32 pointers, updated in place (zero moments for a
+ *     new Gaussian); grads: HOST array of 5 DEVICE pointers (e.g. the slices of the allreduced
+ *     gradient buffer).  Every device pointer 16-byte aligned.
+ * Errors (before any launch): VKS_ERR_INVALID_ARG for a null or unaligned pointer, n < 0,
+ * step < 1, sh_coeffs outside [1, 64], a beta outside [0, 1) or eps < 0.  Asynchronous on
+ * `stream`.  HBM-bound: 28 B per element (p, g, m, v in; p, m, v out).
+ */
+typedef struct {
+    float lr[6];
+    float beta1, beta2, eps;
+    int32_t step;
+} vks_adam_config;
+
+int vks_adam_step(const vks_adam_config* acfg, int64_t n, int32_t sh_coeffs, float* const* params,
+                  const float* const* grads, float* const* m, float* const* v, vks_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,8 @@ FLAG_GRAD_OVERWRITE = 1
 
 EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_project_fwd",
            "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats",
-           "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch")
+           "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch",
+           "vks_adam_step")
 
 
 class VksCamera(C.Structure):
@@ -38,6 +39,27 @@ class VksConfig(C.Structure):
     _fields_ = [("sh_degree", C.c_int32), ("sh_coeffs", C.c_int32), ("near_plane", C.c_float),
                 ("bg", C.c_float * 3), ("fov_clamp", C.c_int32), ("footprint", C.c_int32),
                 ("flags", C.c_uint32)]
+
+
+class VksAdamConfig(C.Structure):
+    _fields_ = [("lr", C.c_float * 6), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("step", C.c_int32)]
+
+
+ADAM_GROUPS = ("means", "log_scales", "quats", "opacity_logits", "sh")
+
+
+def make_adam_config(lr, beta1=0.9, beta2=0.999, eps=1e-8, step=1) -> VksAdamConfig:
+    """lr: dict keyed by ADAM_GROUPS ("sh" may be a pair: coefficient 0, the others) or 6 floats."""
+    a = VksAdamConfig()
+    if isinstance(lr, dict):
+        sh = lr["sh"] if isinstance(lr["sh"], (tuple, list)) else (lr["sh"], lr["sh"])
+        vals = [lr["means"], lr["log_scales"], lr["quats"], lr["opacity_logits"], sh[0], sh[1]]
+    else:
+        vals = list(lr)
+    a.lr[:] = [float(x) for x in vals]
+    a.beta1, a.beta2, a.eps, a.step = float(beta1), float(beta2), float(eps), int(step)
+    return a
 
 
 _P = C.c_void_p
@@ -55,8 +77,9 @@ _lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 10
 _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
 _lib.vks_project_bwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 17
 _lib.vks_project_fwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 13
+_lib.vks_adam_step.argtypes = [_P, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]
 for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats", "vks_raster_bwd",
-           "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch"):
+           "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch", "vks_adam_step"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -266,6 +289,27 @@ def vks_project_bwd_batch(cfg, cams, means, log_scales, quats, opacity_logits, s
                                     _ptr(dquats, f32, "dquats"), _ptr(dopacity_logits, f32, "dopacity_logits"),
                                     _ptr(dsh, f32, "dsh"), _stream(stream))
     _check("vks_project_bwd_batch", st)
+
+
+def vks_adam_step(acfg, params, grads, m, v, stream=None):
+    """Adam step: params / grads / m / v are 5-sequences of fp32 tensors in
+    ADAM_GROUPS order (means [n,3], log_scales [n,3], quats [n,4], opacity_logits [n],
+    sh [n,K,3]); params, m and v are updated in place.  acfg: VksAdamConfig or a dict of
+    make_adam_config's keyword arguments."""
+    a = acfg if isinstance(acfg, VksAdamConfig) else make_adam_config(**acfg)
+    seqs = (params, grads, m, v)
+    if any(len(x) != 5 for x in seqs):
+        raise ValueError("params, grads, m, v: one tensor per parameter group (5)")
+    n, K = params[0].shape[0], params[4].shape[1]
+    for seq in seqs:
+        for q, t in enumerate(seq):
+            rows = (3, 3, 4, 1, 3 * K)[q]
+            if t.numel() != n * rows:
+                raise ValueError(f"group {ADAM_GROUPS[q]}: expected {n * rows} elements, got {t.numel()}")
+    arrs = [(C.c_void_p * 5)(*[_ptr(t, f32, f"{nm}[{ADAM_GROUPS[q]}]") for q, t in enumerate(seq)])
+            for seq, nm in zip(seqs, ("params", "grads", "m", "v"))]
+    st = _lib.vks_adam_step(C.byref(a), n, K, *arrs, _stream(stream))
+    _check("vks_adam_step", st)
 
 
 def vks_version() -> int:

@@ -228,4 +228,19 @@ int vks_project_bwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
                                                      (cudaStream_t)stream));
 }
 
+int vks_adam_step(const vks_adam_config* acfg, int64_t n, int32_t sh_coeffs, float* const* params,
+                  const float* const* grads, float* const* m, float* const* v, vks_stream_t stream) {
+    if (!acfg || n < 0 || sh_coeffs < 1 || sh_coeffs > 64 || !params || !grads || !m || !v) return VKS_ERR_INVALID_ARG;
+    if (acfg->step < 1 || !(acfg->beta1 >= 0.0f && acfg->beta1 < 1.0f) || !(acfg->beta2 >= 0.0f && acfg->beta2 < 1.0f) ||
+        !(acfg->eps >= 0.0f))
+        return VKS_ERR_INVALID_ARG;
+    for (int q = 0; q < 5; q++) {
+        const void* ptrs[4] = {params[q], grads[q], m[q], v[q]};
+        for (const void* p : ptrs)
+            if (n > 0 && (!p || (reinterpret_cast<uintptr_t>(p) & 15))) return VKS_ERR_INVALID_ARG;
+    }
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_adam_step(*acfg, n, sh_coeffs, params, grads, m, v, (cudaStream_t)stream));
+}
+
 }  // extern "C"

@@ -87,6 +87,16 @@ def test_argument_validation_is_synchronous():
     for nv in (0, 17):  # batch size outside [1, 16]
         assert lib.vks_project_bwd_batch(C.byref(cfg), nv, cams, 0, *([None] * 5), *([arr] * 6),
                                          *([None] * 5), None) == V.VKS_ERR_INVALID_ARG
+    # Adam: step < 1, beta outside [0, 1), sh_coeffs outside [1, 64], unaligned pointer
+    five = (C.c_void_p * 5)(*([256] * 5))
+    a = V.make_adam_config([1e-3] * 6, step=0)
+    assert lib.vks_adam_step(C.byref(a), 4, 16, five, five, five, five, None) == V.VKS_ERR_INVALID_ARG
+    a = V.make_adam_config([1e-3] * 6, beta1=1.0)
+    assert lib.vks_adam_step(C.byref(a), 4, 16, five, five, five, five, None) == V.VKS_ERR_INVALID_ARG
+    a = V.make_adam_config([1e-3] * 6)
+    assert lib.vks_adam_step(C.byref(a), 4, 65, five, five, five, five, None) == V.VKS_ERR_INVALID_ARG
+    odd = (C.c_void_p * 5)(*([256] * 4 + [260]))
+    assert lib.vks_adam_step(C.byref(a), 4, 16, five, odd, five, five, None) == V.VKS_ERR_INVALID_ARG
     m = C.c_int64(0)
     assert lib.vks_bin_sort(C.byref(cam), 5, *([None] * 5), 0, *([None] * 4), None, None, C.byref(m), None, 0,
                             None) == V.VKS_ERR_INVALID_ARG

@@ -278,3 +278,18 @@ def adam_step(params, grads, m, v, lr, beta1=0.9, beta2=0.999, eps=1e-8, step=1)
             L.vko_quat_renorm(p.shape[0], _p(p))
         P[k], M[k], Vv[k] = p, mm, vv
     return P, M, Vv
+
+
+# ---- the loss gradient (L1 + lambda D-SSIM) ------------------
+def loss_grad(render, target, lam=0.2):
+    """(loss, dL/drender fp64 [H, W, 3], ssim) of vko_loss_grad for HWC fp32 images."""
+    L = lib()
+    L.vko_loss_grad.restype = C.c_double
+    L.vko_loss_grad.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    r = np.ascontiguousarray(render, np.float32)
+    t = np.ascontiguousarray(target, np.float32)
+    H, W = r.shape[:2]
+    g = np.zeros((H, W, 3), np.float64)
+    ss = C.c_double(0)
+    loss = L.vko_loss_grad(W, H, lam, _p(r), _p(t), _p(g), C.byref(ss))
+    return float(loss), g, float(ss.value)

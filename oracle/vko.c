@@ -1012,3 +1012,68 @@ void vko_quat_renorm(int64_t n, float* q) {
         q[4 * i + 3] = (float)(d / nn);
     }
 }
+
+/* ---- loss gradient: L1 + lambda D-SSIM, S:178-186, S:482 ------------------ */
+static void ssim_window(double w[11][11]) {
+    double g[11], sum = 0.0;
+    for (int i = 0; i < 11; i++) {
+        const double d = (double)(i - 5);
+        g[i] = exp(-d * d / (2.0 * 1.5 * 1.5));
+        sum += g[i];
+    }
+    for (int i = 0; i < 11; i++)
+        for (int j = 0; j < 11; j++) w[i][j] = (g[i] / sum) * (g[j] / sum);
+}
+
+double vko_loss_grad(int32_t W, int32_t H, double lambda, const float* render, const float* target,
+                     double* dL_dr, double* ssim_out) {
+    const int64_t np = (int64_t)W * H;
+    double l1 = 0.0;
+    for (int64_t i = 0; i < 3 * np; i++) {
+        const double d = (double)render[i] - (double)target[i];
+        l1 += fabs(d);
+        dL_dr[i] = (1.0 - lambda) * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / (double)(3 * np);
+    }
+    l1 /= (double)(3 * np);
+    double ssim = 1.0;
+    if (lambda != 0.0) {
+        const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+        double w[11][11];
+        ssim_window(w);
+        const int Wv = W - 10, Hv = H - 10;
+        const double nv = 3.0 * (double)Wv * (double)Hv;
+        double acc = 0.0;
+        for (int c = 0; c < 3; c++)
+            for (int py = 0; py < Hv; py++)
+                for (int px = 0; px < Wv; px++) {
+                    double mx = 0, my = 0, exx = 0, eyy = 0, exy = 0;
+                    for (int i = 0; i < 11; i++)
+                        for (int j = 0; j < 11; j++) {
+                            const int64_t q = ((int64_t)(py + i) * W + (px + j)) * 3 + c;
+                            const double x = render[q], y = target[q], ww = w[i][j];
+                            mx += ww * x; my += ww * y;
+                            exx += ww * x * x; eyy += ww * y * y; exy += ww * x * y;
+                        }
+                    const double sx2 = exx - mx * mx, sy2 = eyy - my * my, sxy = exy - mx * my;
+                    const double l1n = 2 * mx * my + C1, l2n = mx * mx + my * my + C1;
+                    const double c1n = 2 * sxy + C2, c2n = sx2 + sy2 + C2;
+                    const double S = (l1n * c1n) / (l2n * c2n);
+                    acc += S;
+                    /* partials with respect to mx, E[x^2], E[xy] (the other window sums held) */
+                    const double dB = -S / c2n;                 /* dS/dE[x^2] = dS/dsx2 */
+                    const double dC = 2.0 * l1n / (l2n * c2n);  /* dS/dE[xy]  = dS/dsxy */
+                    const double dA = 2.0 * my * c1n / (l2n * c2n) - 2.0 * mx * S / l2n
+                                    - 2.0 * mx * dB - my * dC;  /* total dS/dmx */
+                    const double k = -lambda / nv;
+                    for (int i = 0; i < 11; i++)
+                        for (int j = 0; j < 11; j++) {
+                            const int64_t q = ((int64_t)(py + i) * W + (px + j)) * 3 + c;
+                            const double x = render[q], y = target[q];
+                            dL_dr[q] += k * w[i][j] * (dA + 2.0 * dB * x + dC * y);
+                        }
+                }
+        ssim = acc / nv;
+    }
+    if (ssim_out) *ssim_out = ssim;
+    return (1.0 - lambda) * l1 + lambda * (1.0 - ssim);
+}

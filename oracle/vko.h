@@ -169,6 +169,21 @@ void vko_adam_group(int64_t n, float* p, float* m, float* v, const float* g, dou
  * each row of 4 divided by its fp64 norm (rows of norm 0 left unchanged). */
 void vko_quat_renorm(int64_t n, float* q);
 
+/* ---- the loss gradient before the path ------------------------------ */
+
+/* "Loss Gradient" (SSIM definition):
+ *   loss = (1 - lambda) mean_{pixels, channels} |r - t| + lambda (1 - SSIM(r, t))
+ *   SSIM = mean over channels and VALID window centres (no padding) of
+ *          S = (2 mx my + C1)(2 sxy + C2) / ((mx^2 + my^2 + C1)(sx2 + sy2 + C2)),
+ *   window statistics with the normalised 11x11 Gaussian window (sigma 1.5), C1 = 0.01^2,
+ *   C2 = 0.03^2; sx2 = E[x^2] - mx^2, sxy = E[xy] - mx my.
+ *   dL_dr = the exact gradient (L1 subgradient sign(0) = 0), written as fp64.
+ * Images HWC fp32 [H, W, 3]; SSIM needs H, W >= 11 unless lambda = 0.  fp64 throughout; the
+ * window sums are direct (121 terms), the gradient scatters each centre's partials
+ * (dS/dmx, dS/dE[x^2], dS/dE[xy]) back over its window.  Returns the loss. */
+double vko_loss_grad(int32_t W, int32_t H, double lambda, const float* render, const float* target,
+                     double* dL_dr, double* ssim_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -294,6 +294,27 @@ typedef struct {
 int vks_adam_step(const vks_adam_config* acfg, int64_t n, int32_t sh_coeffs, float* const* params,
                   const float* const* grads, float* const* m, float* const* v, vks_stream_t stream);
 
+/* ---- the loss gradient before the path --------------------------------
+ *
+ * vks_loss_grad — "Loss Gradient" (SSIM S:482):
+ *   loss = (1 - lambda) mean_{pixels, channels} |render - target| + lambda (1 - SSIM)
+ *   SSIM = mean over the 3 channels and the VALID window centres (no padding) of
+ *          S = (2 mx my + C1)(2 sxy + C2) / ((mx^2 + my^2 + C1)(sx2 + sy2 + C2)),
+ *   window statistics over the normalised 11x11 Gaussian window (sigma 1.5), C1 = 0.01^2,
+ *   C2 = 0.03^2;  dL_dimage = the exact gradient of `loss` with respect to render (L1
+ *   subgradient sign(0) = 0) — the dL/dimage input of vks_raster_bwd.
+ *   render, target: device [height, width, 3] fp32 (HWC, as vks_raster_fwd's image)
+ *   dL_dimage: device [height, width, 3] fp32, written; loss: device fp32 [1], written (nullable)
+ *   workspace: device, 256-byte aligned, >= vks_loss_workspace_bytes(width, height) bytes
+ *     (fp64 partial maps of the window centres: ~72 B per pixel)
+ * Errors (before any launch): VKS_ERR_INVALID_ARG for a null pointer, a size outside [1, 65536],
+ * lambda outside [0, 1], or lambda > 0 with width or height < 11; VKS_ERR_WORKSPACE.
+ * Asynchronous on `stream`; deterministic.
+ */
+size_t vks_loss_workspace_bytes(int32_t width, int32_t height);
+int vks_loss_grad(int32_t width, int32_t height, float lambda, const float* render, const float* target,
+                  float* dL_dimage, float* loss, void* workspace, size_t workspace_bytes, vks_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ FLAG_GRAD_OVERWRITE = 1
 EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_project_fwd",
            "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats",
            "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch",
-           "vks_adam_step")
+           "vks_adam_step", "vks_loss_workspace_bytes", "vks_loss_grad")
 
 
 class VksCamera(C.Structure):
@@ -78,6 +78,10 @@ _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
 _lib.vks_project_bwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 17
 _lib.vks_project_fwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 13
 _lib.vks_adam_step.argtypes = [_P, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]
+_lib.vks_loss_workspace_bytes.restype = C.c_size_t
+_lib.vks_loss_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
+_lib.vks_loss_grad.argtypes = [C.c_int32, C.c_int32, C.c_float, _P, _P, _P, _P, _P, C.c_size_t, _P]
+_lib.vks_loss_grad.restype = C.c_int
 for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats", "vks_raster_bwd",
            "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch", "vks_adam_step"):
     getattr(_lib, _f).restype = C.c_int
@@ -310,6 +314,24 @@ def vks_adam_step(acfg, params, grads, m, v, stream=None):
             for seq, nm in zip(seqs, ("params", "grads", "m", "v"))]
     st = _lib.vks_adam_step(C.byref(a), n, K, *arrs, _stream(stream))
     _check("vks_adam_step", st)
+
+
+def vks_loss_workspace_bytes(width: int, height: int) -> int:
+    return int(_lib.vks_loss_workspace_bytes(int(width), int(height)))
+
+
+def vks_loss_grad(render, target, dL_dimage, loss, workspace, lam=0.2, stream=None):
+    """Loss gradient: render / target / dL_dimage [H, W, 3] fp32 device tensors,
+    loss a 1-element fp32 device tensor (or None), workspace a uint8 device tensor of at least
+    vks_loss_workspace_bytes(W, H) bytes."""
+    H, W = render.shape[0], render.shape[1]
+    for t, nm in ((render, "render"), (target, "target"), (dL_dimage, "dL_dimage")):
+        if tuple(t.shape) != (H, W, 3):
+            raise ValueError(f"{nm}: expected shape {(H, W, 3)}, got {tuple(t.shape)}")
+    st = _lib.vks_loss_grad(W, H, float(lam), _ptr(render, f32, "render"), _ptr(target, f32, "target"),
+                            _ptr(dL_dimage, f32, "dL_dimage"), _ptr(loss, f32, "loss"),
+                            _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
+    _check("vks_loss_grad", st)
 
 
 def vks_version() -> int:

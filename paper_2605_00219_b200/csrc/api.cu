@@ -243,4 +243,22 @@ int vks_adam_step(const vks_adam_config* acfg, int64_t n, int32_t sh_coeffs, flo
     return cuda_status(vks::launch_adam_step(*acfg, n, sh_coeffs, params, grads, m, v, (cudaStream_t)stream));
 }
 
+size_t vks_loss_workspace_bytes(int32_t width, int32_t height) {
+    if (width < 1 || height < 1 || width > 65536 || height > 65536) return 0;
+    return vks::loss_workspace_bytes(width, height);
+}
+
+int vks_loss_grad(int32_t width, int32_t height, float lambda, const float* render, const float* target,
+                  float* dL_dimage, float* loss, void* workspace, size_t workspace_bytes, vks_stream_t stream) {
+    if (width < 1 || height < 1 || width > 65536 || height > 65536) return VKS_ERR_INVALID_ARG;
+    if (!(lambda >= 0.0f && lambda <= 1.0f)) return VKS_ERR_INVALID_ARG;
+    if (lambda != 0.0f && (width < 11 || height < 11)) return VKS_ERR_INVALID_ARG;
+    if (!render || !target || !dL_dimage || !workspace) return VKS_ERR_INVALID_ARG;
+    if (workspace_bytes < vks::loss_workspace_bytes(width, height) || (reinterpret_cast<uintptr_t>(workspace) & 255))
+        return VKS_ERR_WORKSPACE;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_loss_grad(width, height, lambda, render, target, dL_dimage, loss, workspace,
+                                             (cudaStream_t)stream));
+}
+
 }  // extern "C"

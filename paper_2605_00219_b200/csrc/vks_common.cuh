@@ -128,6 +128,9 @@ int launch_project_bwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
                              float* dlog_scales, float* dquats, float* dopacity_logits, float* dsh, cudaStream_t s);
 int launch_adam_step(const vks_adam_config& acfg, int64_t n, int32_t sh_coeffs, float* const* params,
                      const float* const* grads, float* const* m, float* const* v, cudaStream_t s);
+size_t loss_workspace_bytes(int W, int H);
+int launch_loss_grad(int W, int H, float lambda, const float* render, const float* target, float* dL, float* loss,
+                     void* workspace, cudaStream_t s);
 size_t bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles);
 int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const int32_t* radii,
                  const float* depths, const int32_t* tiles_touched, uint32_t* offsets,

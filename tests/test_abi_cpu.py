@@ -97,6 +97,12 @@ def test_argument_validation_is_synchronous():
     assert lib.vks_adam_step(C.byref(a), 4, 65, five, five, five, five, None) == V.VKS_ERR_INVALID_ARG
     odd = (C.c_void_p * 5)(*([256] * 4 + [260]))
     assert lib.vks_adam_step(C.byref(a), 4, 16, five, odd, five, five, None) == V.VKS_ERR_INVALID_ARG
+    # loss gradient: SSIM needs 11x11 images, lambda in [0, 1], workspace size
+    P = C.c_void_p(256)
+    assert lib.vks_loss_grad(10, 64, C.c_float(0.2), P, P, P, None, P, 1 << 30, None) == V.VKS_ERR_INVALID_ARG
+    assert lib.vks_loss_grad(64, 64, C.c_float(1.5), P, P, P, None, P, 1 << 30, None) == V.VKS_ERR_INVALID_ARG
+    assert lib.vks_loss_grad(64, 64, C.c_float(0.2), P, P, P, None, P, 16, None) == V.VKS_ERR_WORKSPACE
+    assert lib.vks_loss_workspace_bytes(1237, 822) > 1237 * 822 * 70
     m = C.c_int64(0)
     assert lib.vks_bin_sort(C.byref(cam), 5, *([None] * 5), 0, *([None] * 4), None, None, C.byref(m), None, 0,
                             None) == V.VKS_ERR_INVALID_ARG

@@ -218,19 +218,19 @@ def run_ours(args):
                                     [vbuf[j]["colors"] for j in range(nb)], opac)
 
     def view_path(rend, vb, cam, dL, st, ev=None, copies=None):
-        """One view's forward and raster backward on stream `st` (two views of a batch run
-        concurrently on their own streams).  copies = (host dL, slot): the e2e variant's per-view
-        transfers, on a copy stream that overlaps them with compute — dL/dimage in from pinned
-        host memory (needed by raster_bwd), the rendered image out to pinned host memory."""
+        """One view's forward and raster backward on stream `st` (S views in flight, one stream
+        each).  copies = (host target image, slot, loss slot): the e2e variant — the view's target
+        image comes in from pinned host memory on a copy stream ("Copy Image to Device"),
+        vks_loss_grad turns the rendered image and the target into the loss and dL/dimage on the
+        device ("Loss Gradient"), and raster_bwd consumes that."""
         if copies is not None:
-            host_src, slot = copies
+            host_src, slot, loss_out = copies  # loss_out None: the path's e2e (dL in, image out)
             with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(slot["dL_free"])      # the slot's previous raster_bwd is done
-                slot["dL"].copy_(host_src, non_blocking=True)
-                slot["dL_ready"].record(copy_stream)
-            dL = slot["dL"]
+                copy_stream.wait_event(slot["in_free"])      # the slot's previous consumer is done
+                slot["in"].copy_(host_src, non_blocking=True)
+                slot["in_ready"].record(copy_stream)
         with torch.cuda.stream(st):
-            if copies is not None:
+            if copies is not None and loss_out is None:
                 st.wait_event(slot["img_free"])              # the previous image has left rend.image
             if ev is not None: ev[1].record(st)
             bst = bstreams[streams.index(st)] if st in streams else st
@@ -246,13 +246,19 @@ def run_ours(args):
             P.vks_raster_fwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],
                              rend.vals, rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib,
                              tile_order=rend.tile_order)
-            if copies is not None:
+            if copies is not None and loss_out is None:  # dL/dimage from the host, the image out
                 slot["img_done"].record(st)
                 with torch.cuda.stream(copy_stream):
                     copy_stream.wait_event(slot["img_done"])
                     slot["img_host"].copy_(rend.image, non_blocking=True)
                     slot["img_free"].record(copy_stream)
-                st.wait_event(slot["dL_ready"])
+                st.wait_event(slot["in_ready"])
+                dL = slot["in"]
+            elif copies is not None:  # the target from the host, loss + dL/dimage on the device
+                st.wait_event(slot["in_ready"])
+                P.vks_loss_grad(rend.image, slot["in"], slot["dL"], loss_out, slot["ws"], lam=0.2)
+                slot["in_free"].record(st)
+                dL = slot["dL"]
             if ev is not None: ev[3].record(st)
             vb["g2d"].zero_()
             if ev is not None: ev[4].record(st)
@@ -260,8 +266,8 @@ def run_ours(args):
                              rend.vals, rend.tile_offsets, rend.T_final, rend.n_contrib, dL, vb["dm2"], vb["dcon"],
                              vb["dcol"], vb["dop"], tile_order=rend.tile_order)
             if ev is not None: ev[5].record(st)
-            if copies is not None:
-                slot["dL_free"].record(st)
+            if copies is not None and loss_out is None:
+                slot["in_free"].record(st)
             done = torch.cuda.Event()
             done.record(st)
         return m, done
@@ -295,11 +301,15 @@ def run_ours(args):
         m = 0
         for j, v in enumerate(vviews):
             k = j % S
-            cp = None if copies is None else (copies[0][v], copies[1][k])
+            cp = None
+            if copies is not None:
+                cp = (copies[0][v], copies[1][k], None if copies[2] is None else copies[2][j:j + 1])
             m, done = view_path(rends[k], vbuf[j], cams[v], dLs[v], streams[k], copies=cp)
             main.wait_event(done)
         project_bwd_batch(vcams, main)
-        if copies is not None:
+        if copies is not None and copies[2] is not None:
+            copies[3].copy_(copies[2], non_blocking=True)  # the batch's losses to pinned host memory
+        elif copies is not None:
             main.wait_stream(copy_stream)  # every image of the batch has reached the host
         allreduce_grads(params.grad_flat)
         return m
@@ -382,6 +392,21 @@ def run_ours(args):
     torch.cuda.synchronize()
     adam_ms = statistics.median([a.elapsed_time(b) for a, b in adam_ev[1:]])
     del mom, vel
+    # the loss gradient before the path (in the e2e leg, not in `value`)
+    tgt = torch.rand(c.height, c.width, 3, device="cuda")
+    dl_tmp = torch.empty_like(tgt)
+    loss_tmp = torch.empty(1, device="cuda")
+    lws = torch.empty(P.vks_loss_workspace_bytes(c.width, c.height), dtype=torch.uint8, device="cuda")
+    loss_ev = []
+    for t in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        P.vks_loss_grad(rends[0].image, tgt, dl_tmp, loss_tmp, lws, lam=0.2)
+        e1.record(main)
+        loss_ev.append((e0, e1))
+    torch.cuda.synchronize()
+    loss_ms = statistics.median([a.elapsed_time(b) for a, b in loss_ev[1:]])
+    del tgt, dl_tmp, lws
     st_ms["project_bwd"] = statistics.median([a.elapsed_time(b) for a, b in pb_ms]) / B
     st_ms = {k: st_ms[k] for k in stages}
     rend = rends[0]
@@ -415,6 +440,11 @@ def run_ours(args):
                      ms_per_step=round(adam_ms, 4), bound="hbm", algorithmic_bytes=adam_bytes,
                      achieved=round(adam_bytes / (adam_ms * 1e-3) / 1e9, 1), peak=pk["hbm_gbs"], unit="GB/s",
                      frac=round(adam_bytes / (adam_ms * 1e-3) / 1e9 / pk["hbm_gbs"], 4))
+    loss_bytes = 36 * c.width * c.height  # render + target in, dL/dimage out (fp32 RGB)
+    loss_grad = dict(row="f2 (SURVEY 8f): vks_loss_grad (L1 + 0.2 D-SSIM), once per view in the e2e leg; "
+                         "not in value", ms_per_view=round(loss_ms, 4), algorithmic_bytes=loss_bytes,
+                     achieved_gbs=round(loss_bytes / (loss_ms * 1e-3) / 1e9, 1),
+                     note="fp64 window sums; the fp64 partial maps (72 B per pixel) round-trip through L2")
     per_stage["bin_sort"]["depth_passes"] = dpasses
     for k in ("raster_fwd", "raster_bwd"):
         tf = fl[k] / (st_ms[k] * 1e-3) / 1e12
@@ -453,30 +483,57 @@ def run_ours(args):
                raster_work=dict(visited_pairs=visited, composited_pairs=composited, evaluated_pairs=evaluated,
                                 replayed_pairs=replayed, warp_entries=warp_entries,
                                 warp_entries_composited=warp_entries_comp),
-               roofline=roofline, gpu_launches=gpu_launches, clocks=clk, optimizer=optimizer)
+               roofline=roofline, gpu_launches=gpu_launches, clocks=clk, optimizer=optimizer,
+               loss_grad=loss_grad)
 
     if not args.no_e2e:
-        # the same steps with HOST buffers: each view's dL/dimage copied in from pinned host
-        # memory and its rendered image copied out to pinned host memory, on the view's stream
+        # (1) the path end to end: each view's dL/dimage copied in from pinned host memory and its
+        # rendered image copied out to pinned host memory, on a copy stream overlapping compute
+        nbytes = c.height * c.width * 3 * 4
+        wsb = P.vks_loss_workspace_bytes(c.width, c.height)
+
+        def make_slots(loss_leg):
+            out_slots = []
+            for _ in range(S):
+                sl = {"in": torch.empty(c.height, c.width, 3, device="cuda")}
+                if loss_leg:
+                    sl["dL"] = torch.empty(c.height, c.width, 3, device="cuda")
+                    sl["ws"] = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+                else:
+                    sl["img_host"] = torch.empty(c.height, c.width, 3, pin_memory=True)
+                for e in ("in_free", "in_ready", "img_done", "img_free"):
+                    sl[e] = torch.cuda.Event()
+                    sl[e].record(main)
+                out_slots.append(sl)
+            return out_slots
+
         pinned = {v: t.pin_memory() for v, t in host_dL.items()}
-        slots = []
-        for _ in range(S):
-            sl = dict(dL=torch.empty(c.height, c.width, 3, device="cuda"),
-                      img_host=torch.empty(c.height, c.width, 3, pin_memory=True))
-            for e in ("dL_free", "dL_ready", "img_done", "img_free"):
-                sl[e] = torch.cuda.Event()
-                sl[e].record(main)
-            slots.append(sl)
-        copies = (pinned, slots)
+        copies = (pinned, make_slots(False), None, None)
         for s in range(min(args.warmup, 3)):
             step(s, copies)
         ms = timed(lambda s: step(s, copies), args.steps)
-        nbytes = c.height * c.width * 3 * 4
         out["e2e"] = dict(value=round(world * B * args.steps / (ms / 1e3), 3), unit="iters/s",
                           h2d_bytes_per_step=B * nbytes, d2h_bytes_per_step=B * nbytes,
                           ms_per_step=round(ms / args.steps, 4),
                           note=("per view: dL/dimage in from pinned host memory and the rendered image out to "
                                 "pinned host memory, on a copy stream overlapping compute, inside the timed region"))
+        # (2) as a training iteration sees it: the target image in ("Copy Image to Device"),
+        # loss + dL/dimage on the device (vks_loss_grad, L1 + 0.2 D-SSIM: SURVEY 8(f) row f2), the
+        # batch's losses out
+        import numpy as np
+        targets = {v: torch.from_numpy(np.random.default_rng(c.seed + 3000 + v).random(
+            (c.height, c.width, 3), dtype=np.float32)).pin_memory() for v in set(my_views)}
+        losses, losses_host = torch.zeros(B, device="cuda"), torch.zeros(B, pin_memory=True)
+        copies = (targets, make_slots(True), losses, losses_host)
+        for s in range(min(args.warmup, 3)):
+            step(s, copies)
+        ms = timed(lambda s: step(s, copies), args.steps)
+        out["e2e_with_loss"] = dict(value=round(world * B * args.steps / (ms / 1e3), 3), unit="iters/s",
+                                    h2d_bytes_per_step=B * nbytes, d2h_bytes_per_step=B * 4,
+                                    ms_per_step=round(ms / args.steps, 4), loss_view0=round(float(losses_host[0]), 6),
+                                    note=("per view: the target image in from pinned host memory, loss + dL/dimage "
+                                          "computed on the device (row f2), the batch's losses out; inside the "
+                                          "timed region"))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, c, cfg)
     if distributed:

@@ -6,11 +6,12 @@
 //   (sx2 + sy2 + C2)).
 // Three kernels: ssim_fwd_kernel (per 32x16 tile of window centres and channel: separable window
 // sums of x, y, x^2, y^2, xy in shared memory, then S and its partials dS/dmx, dS/dE[x^2],
-// dS/dE[xy] per centre), ssim_bwd_kernel (per 32x16 pixel tile: the transposed separable window
-// sums of the three partial maps, the L1 subgradient, dL/dr), loss_finalize_kernel (one block:
-// the block partial sums -> loss, deterministic).  The window sums and partials are fp64: the
-// variances E[x^2] - mx^2 cancel to ~C2 = 9e-4 and their fp32 error would reach 1e-3 of the
-// gradient; FP64 costs nothing here (3.0M pixels, ~30 flops per tap).
+// dS/dE[xy] per centre), ssim_bwd_kernel (per 32x16 pixel tile and channel: the transposed
+// separable window sums of the three partial maps, the L1 subgradient, dL/dr),
+// loss_finalize_kernel (one block: the block partial sums -> loss, deterministic).  The window
+// sums, S, the partials and the transposed pass are fp64: the variances E[x^2] - mx^2 cancel down
+// to ~C2 = 9e-4, and fp32 statistics would put up to ~1e-3 relative error into the gradient (fp32
+// horizontal sums measured 0.189 vs 0.204 ms for 1237x822: not worth their 1e-6 absolute error).
 #include "vks_common.cuh"
 
 namespace vks {
@@ -91,9 +92,10 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(int W, int H, co
         const double sx2 = exx - mx * mx, sy2 = eyy - my * my, sxy = exy - mx * my;
         const double l1 = 2 * mx * my + kC1, l2 = mx * mx + my * my + kC1;
         const double c1 = 2 * sxy + kC2, c2 = sx2 + sy2 + kC2;
-        const double S = (l1 * c1) / (l2 * c2);
-        const double dB = -S / c2, dC = 2.0 * l1 / (l2 * c2);
-        const double dA = 2.0 * my * c1 / (l2 * c2) - 2.0 * mx * S / l2 - 2.0 * mx * dB - my * dC;
+        const double inv = 1.0 / (l2 * c2);  // the one fp64 division: 1/l2 = c2 inv, 1/c2 = l2 inv
+        const double S = l1 * c1 * inv;
+        const double dB = -S * (l2 * inv), dC = 2.0 * l1 * inv;
+        const double dA = 2.0 * my * c1 * inv - 2.0 * mx * S * (c2 * inv) - 2.0 * mx * dB - my * dC;
         const size_t o = ((size_t)c * Hv + py) * Wv + px;
         A[o] = dA;
         B[o] = dB;
@@ -128,7 +130,8 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(int W, int H, fl
     const double inv_n = 1.0 / (3.0 * (double)W * (double)H);
     const double k_ssim = ssim ? -(double)lambda / (3.0 * (double)Wv * (double)Hv) : 0.0;
     double l1 = 0.0;
-    for (int c = 0; c < 3; c++) {
+    {
+        const int c = blockIdx.z;
         if (ssim) {
             // centres p = q - i (i in [0, 10]) for q in the tile: rows qy0-10 .. qy0+kTH-1
             for (int k = tid; k < kIH * kIW; k += kLossThreads) {
@@ -177,7 +180,6 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(int W, int H, fl
             }
             dL[o] = (float)g;
         }
-        if (ssim) __syncthreads();  // sm / hs are reused by the next channel
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) l1 += __shfl_xor_sync(VKS_FULL_MASK, l1, o);
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(int W, int H, fl
     if (tid == 0) {
         double t = 0.0;
         for (int q = 0; q < kLossThreads / 32; q++) t += red[q];
-        l1_part[blockIdx.y * gridDim.x + blockIdx.x] = t;
+        l1_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
     }
 }
 
@@ -226,7 +228,7 @@ LossWs carve_loss(void* base, int W, int H) {
     const int Wv = W - 2 * kR > 0 ? W - 2 * kR : 0, Hv = H - 2 * kR > 0 ? H - 2 * kR : 0;
     const size_t maps = (size_t)3 * Wv * Hv;
     const size_t nfwd = (size_t)3 * ((Wv + kTW - 1) / kTW) * ((Hv + kTH - 1) / kTH);
-    const size_t nbwd = (size_t)((W + kTW - 1) / kTW) * ((H + kTH - 1) / kTH);
+    const size_t nbwd = (size_t)3 * ((W + kTW - 1) / kTW) * ((H + kTH - 1) / kTH);
     size_t off = 0;
     char* b = static_cast<char*>(base);
     auto take = [&](size_t n) { double* p = b ? reinterpret_cast<double*>(b + off) : nullptr; off += (8 * n + 255) & ~(size_t)255; return p; };
@@ -256,11 +258,12 @@ int launch_loss_grad(int W, int H, float lambda, const float* render, const floa
         ns = (int)(g.x * g.y * g.z);
         if (int e = LaunchCheck::check()) return e;
     }
-    const dim3 gb((W + kTW - 1) / kTW, (H + kTH - 1) / kTH, 1);
+    const dim3 gb((W + kTW - 1) / kTW, (H + kTH - 1) / kTH, 3);
     ssim_bwd_kernel<<<gb, kLossThreads, 0, s>>>(W, H, lambda, render, target, w, ws.A, ws.B, ws.C, dL, ws.l1_part);
     if (int e = LaunchCheck::check()) return e;
     if (loss) {
-        loss_finalize_kernel<<<1, kLossThreads, 0, s>>>(W, H, lambda, ws.s_part, ns, ws.l1_part, (int)(gb.x * gb.y), loss);
+        loss_finalize_kernel<<<1, kLossThreads, 0, s>>>(W, H, lambda, ws.s_part, ns, ws.l1_part,
+                                                        (int)(gb.x * gb.y * gb.z), loss);
         return LaunchCheck::check();
     }
     return VKS_OK;

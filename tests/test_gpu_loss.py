@@ -51,8 +51,9 @@ def test_loss_grad_matches_oracle(H, W, lam):
     lo, go, _ = oracle.loss_grad(r, t, lam)
     assert loss == pytest.approx(lo, rel=1e-6, abs=1e-9)
     G, Go = g.astype(np.float64) * 3 * H * W, go * 3 * H * W
-    bad = np.abs(G - Go) > 1e-6 * np.abs(Go) + 1e-9
-    assert not bad.any(), (int(bad.sum()), np.argwhere(bad)[:4].tolist(), float(np.abs(G - Go).max()))
+    err = np.abs(G - Go)
+    bad = err > 1e-6 * np.abs(Go) + 1e-9
+    assert not bad.any(), (int(bad.sum()), np.argwhere(bad)[:4].tolist(), float(err.max()))
 
 
 def test_identical_images_zero_gradient():

@@ -133,15 +133,15 @@ def raster_flops(visited, composited, replayed):
     return dict(raster_fwd=12 * visited + 9 * composited, raster_bwd=12 * replayed + 50 * composited)
 
 
-def measured_traffic(stage):
-    """DRAM bytes (read + write) per launch of the stage's dominant kernel from the committed
-    `ncu --set full` capture (profiles/r1_traffic.json, written by tools/traffic_from_ncu.py), or
-    None when no capture of that kernel is committed."""
+def measured_traffic(stage, key="dram_bytes_per_launch"):
+    """DRAM bytes (read + write) per launch of the stage's dominant kernel (or, key="issue_active",
+    its issue-slot utilisation) from the committed `ncu --set full` capture (profiles/
+    r1_traffic.json, written by tools/traffic_from_ncu.py), or None when no capture is committed."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
-        return t["kernels"][stage]["dram_bytes_per_launch"]
+        return t["kernels"][stage][key]
     except (OSError, KeyError, ValueError):
         return None
 
@@ -456,6 +456,7 @@ def run_ours(args):
     d = per_stage[dom]
     roofline = dict(kernel=dom, bound=d["bound"], achieved=round(d["achieved"], 3), peak=round(d["peak"], 3),
                     unit=d["unit"], frac=round(d["frac"], 4), traffic=measured_traffic(dom),
+                    issue_active_ncu=measured_traffic(dom, "issue_active"),
                     peak_source=(pk["src"] + (" HBM copy (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
                                               f" FP32 FMA: 148 SM x 128 lanes x 2 flop x {clock_mhz:.0f} MHz")))
     # our kernels per view: bin_sort = id scan (3) + dpasses x (count, scan, scatter) + depth-order

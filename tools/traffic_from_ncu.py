@@ -21,7 +21,8 @@ def main():
     rep = sys.argv[1]
     out = sys.argv[2] if len(sys.argv) > 2 else "profiles/r1_traffic.json"
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
-                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+                          "smsp__issue_active.avg.pct_of_peak_sustained_active"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, units = rows[0], rows[1]
@@ -32,8 +33,9 @@ def main():
             if re.search(rx, name) and stage not in res:
                 rd = float(r[h.index("dram__bytes_read.sum")]) * SCALE[units[h.index("dram__bytes_read.sum")]]
                 wr = float(r[h.index("dram__bytes_write.sum")]) * SCALE[units[h.index("dram__bytes_write.sum")]]
+                iss = float(r[h.index("smsp__issue_active.avg.pct_of_peak_sustained_active")]) / 100.0
                 res[stage] = dict(kernel=re.sub(r"\(.*", "", name), dram_bytes_read=rd, dram_bytes_write=wr,
-                                  dram_bytes_per_launch=rd + wr)
+                                  dram_bytes_per_launch=rd + wr, issue_active=round(iss, 4))
     json.dump(dict(source=rep.split("/")[-1], note="one ncu --set full capture of tools/profile_bench_step.py "
                    "(bicycle: batched projection of 8 views, view 0's raster passes); per launch", kernels=res), open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))

@@ -293,3 +293,44 @@ def loss_grad(render, target, lam=0.2):
     ss = C.c_double(0)
     loss = L.vko_loss_grad(W, H, lam, _p(r), _p(t), _p(g), C.byref(ss))
     return float(loss), g, float(ss.value)
+
+
+# ---- MCMC densification (DESIGN.md §4.7 readings R1-R5) ------------------
+def _mcmc_lib():
+    L = lib()
+    L.vko_rng.restype = C.c_uint64
+    L.vko_rng.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64]
+    L.vko_mcmc_relocate.restype = C.c_int64
+    L.vko_mcmc_relocate.argtypes = [C.c_int64, C.c_int32, C.c_float, C.c_uint64] + [C.c_void_p] * 8
+    L.vko_mcmc_noise.argtypes = [C.c_int64, C.c_float, C.c_float, C.c_uint64, C.c_uint32] + [C.c_void_p] * 4
+    return L
+
+
+def rng(seed, stream, i):
+    return int(_mcmc_lib().vko_rng(seed, stream, i))
+
+
+def mcmc_relocate(scene, dead_opacity=0.005, seed=0, m=None, v=None):
+    """Relocation of the dead Gaussians (vko_mcmc_relocate) on copies of the scene arrays (and of
+    the flat Adam moments m, v if given).  Returns (new scene dict, targets, n_dead, m, v)."""
+    L = _mcmc_lib()
+    sc = {k: np.ascontiguousarray(scene[k], np.float32).copy() for k in ("means", "log_scales", "quats",
+                                                                          "opacity_logits", "sh")}
+    n, K = sc["means"].shape[0], sc["sh"].shape[1]
+    mm = None if m is None else np.ascontiguousarray(m, np.float32).copy()
+    vv = None if v is None else np.ascontiguousarray(v, np.float32).copy()
+    tg = np.zeros(n, np.int64)
+    dead = L.vko_mcmc_relocate(n, K, dead_opacity, seed, _p(sc["means"]), _p(sc["log_scales"]), _p(sc["quats"]),
+                               _p(sc["opacity_logits"]), _p(sc["sh"]), _p(mm), _p(vv), _p(tg))
+    return sc, tg, int(dead), mm, vv
+
+
+def mcmc_noise(scene, lr_pos, noise_scale, seed=0, step=0):
+    """Positional noise (vko_mcmc_noise) on a copy of the means; returns the new means."""
+    L = _mcmc_lib()
+    means = np.ascontiguousarray(scene["means"], np.float32).copy()
+    ls = np.ascontiguousarray(scene["log_scales"], np.float32)
+    q = np.ascontiguousarray(scene["quats"], np.float32)
+    o = np.ascontiguousarray(scene["opacity_logits"], np.float32)
+    L.vko_mcmc_noise(means.shape[0], lr_pos, noise_scale, seed, step, _p(means), _p(ls), _p(q), _p(o))
+    return means

@@ -1077,3 +1077,97 @@ double vko_loss_grad(int32_t W, int32_t H, double lambda, const float* render, c
     if (ssim_out) *ssim_out = ssim;
     return (1.0 - lambda) * l1 + lambda * (1.0 - ssim);
 }
+
+/* ---- MCMC densification: S:273, readings R1-R5 of DESIGN.md §4.7 ----------- */
+uint64_t vko_rng(uint64_t seed, uint32_t stream, uint64_t i) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * ((((uint64_t)stream) << 40) ^ i);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static double rng_uniform(uint64_t seed, uint32_t stream, uint64_t i) {
+    return ((double)(vko_rng(seed, stream, i) >> 40) + 0.5) / 16777216.0;
+}
+
+static double rng_normal(uint64_t seed, uint32_t stream, uint64_t k) {
+    const double u1 = rng_uniform(seed, stream, 2 * k), u2 = rng_uniform(seed, stream, 2 * k + 1);
+    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+}
+
+static float x64_sigmoid(float o) { return (float)(1.0 / (1.0 + exp(-(double)o))); }
+
+int64_t vko_mcmc_relocate(int64_t n, int32_t sh_coeffs, float dead_opacity, uint64_t seed, float* means,
+                          float* log_scales, float* quats, float* opacity_logits, float* sh, float* m, float* v,
+                          int64_t* targets) {
+    float* rho = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+    uint64_t* W = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t* k = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+    uint64_t total = 0;
+    int64_t dead = 0;
+    for (int64_t i = 0; i < n; i++) {
+        rho[i] = x64_sigmoid(opacity_logits[i]);
+        const int is_dead = rho[i] < dead_opacity;
+        dead += is_dead;
+        total += is_dead ? 0 : (uint64_t)floor((double)rho[i] * 16777216.0);
+        W[i] = total;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        targets[i] = -1;
+        if (!(rho[i] < dead_opacity) || total == 0) continue;
+        const uint64_t t = (uint64_t)(((unsigned __int128)vko_rng(seed, 1, (uint64_t)i) * total) >> 64);
+        int64_t lo = 0, hi = n - 1;  /* first j with W[j] > t */
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if (W[mid] > t) hi = mid; else lo = mid + 1;
+        }
+        targets[i] = lo;
+        k[lo]++;
+    }
+    const int64_t S = 3 * (int64_t)sh_coeffs, F = 11 + S;
+    for (int64_t i = 0; i < n; i++) {  /* copies first (they read the targets' original rows) */
+        const int64_t j = targets[i];
+        if (j < 0) continue;
+        memcpy(means + 3 * i, means + 3 * j, 3 * sizeof(float));
+        memcpy(log_scales + 3 * i, log_scales + 3 * j, 3 * sizeof(float));
+        memcpy(quats + 4 * i, quats + 4 * j, 4 * sizeof(float));
+        memcpy(sh + S * i, sh + S * j, (size_t)S * sizeof(float));
+        const double rp = 1.0 - pow(1.0 - (double)rho[j], 1.0 / (double)(k[j] + 1));
+        opacity_logits[i] = (float)log(rp / (1.0 - rp));
+        if (m && v) {
+            const int64_t off[5] = {0, 3 * n, 6 * n, 10 * n, 11 * n}, w[5] = {3, 3, 4, 1, S};
+            for (int g = 0; g < 5; g++)
+                for (int64_t c = 0; c < w[g]; c++) {
+                    m[off[g] + w[g] * i + c] = 0.0f;
+                    v[off[g] + w[g] * i + c] = 0.0f;
+                }
+        }
+        (void)F;
+    }
+    for (int64_t j = 0; j < n; j++) {
+        if (k[j] == 0) continue;
+        const double rp = 1.0 - pow(1.0 - (double)rho[j], 1.0 / (double)(k[j] + 1));
+        opacity_logits[j] = (float)log(rp / (1.0 - rp));
+    }
+    free(rho); free(W); free(k);
+    return dead;
+}
+
+void vko_mcmc_noise(int64_t n, float lr_pos, float noise_scale, uint64_t seed, uint32_t step, float* means,
+                    const float* log_scales, const float* quats, const float* opacity_logits) {
+    for (int64_t i = 0; i < n; i++) {
+        const double rho = x64_sigmoid(opacity_logits[i]);
+        const double gate = 1.0 / (1.0 + exp(-100.0 * (0.005 - rho)));
+        const double a = quats[4 * i], b = quats[4 * i + 1], c = quats[4 * i + 2], d = quats[4 * i + 3];
+        const double qn = sqrt(a * a + b * b + c * c + d * d);
+        const double w = a / qn, x = b / qn, y = c / qn, z = d / qn;
+        const double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                             2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                             2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+        double e[3];
+        for (int q = 0; q < 3; q++) e[q] = exp((double)log_scales[3 * i + q]) * rng_normal(seed, 2 + 2 * step, 3 * (uint64_t)i + q);
+        const double kk = (double)lr_pos * (double)noise_scale * gate;
+        for (int r = 0; r < 3; r++)
+            means[3 * i + r] = (float)((double)means[3 * i + r] + kk * (R[3 * r] * e[0] + R[3 * r + 1] * e[1] + R[3 * r + 2] * e[2]));
+    }
+}

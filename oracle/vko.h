@@ -184,6 +184,31 @@ void vko_quat_renorm(int64_t n, float* q);
 double vko_loss_grad(int32_t W, int32_t H, double lambda, const float* render, const float* target,
                      double* dL_dr, double* ssim_out);
 
+/* ---- MCMC densification (fixed budget) ------------------------------- */
+
+/* Counter-based generator shared (as a definition, not as code) with the CUDA path (DESIGN.md
+ * §4.7 reading R1): h(seed, stream, i) = splitmix64(seed + 0x9E3779B97F4A7C15 * ((stream << 40) ^ i)),
+ * uniform u = ((h >> 40) + 0.5) / 2^24, normal = Box-Muller of the uniforms of counters 2i, 2i+1. */
+uint64_t vko_rng(uint64_t seed, uint32_t stream, uint64_t i);
+
+/* Relocation (SPEC S:273 densify_mcmc; "MCMC 1M densification"; readings R3-R4 of
+ * DESIGN.md §4.7): rho_i = X64 sigmoid(logit_i); dead_i = rho_i < dead_opacity; weights
+ * w_j = dead_j ? 0 : floor(rho_j 2^24); every dead i draws t = mulhi64(h(seed, 1, i), sum w) and
+ * takes the first j with inclusive prefix W_j > t (probability w_j / sum w); it copies j's means,
+ * log_scales, quats and sh, and j and its k_j copies all get rho' = 1 - (1 - rho_j)^(1/(k_j+1))
+ * (appearance-conserving: (1 - rho')^(k_j+1) = 1 - rho_j), logit' = log(rho'/(1 - rho')) (X64);
+ * the copies' Adam moments (m, v: flat [n * (11 + 3K)] group-major like the parameters, nullable)
+ * are zeroed.  targets[i] = j for dead i, -1 otherwise.  Returns the number of dead. */
+int64_t vko_mcmc_relocate(int64_t n, int32_t sh_coeffs, float dead_opacity, uint64_t seed, float* means,
+                          float* log_scales, float* quats, float* opacity_logits, float* sh, float* m, float* v,
+                          int64_t* targets);
+
+/* Positional noise after an optimizer step (reading R5): means_i += lr_pos * noise_scale *
+ * gate(rho_i) * Rq_i diag(exp(log_scales_i)) eps_i, gate(rho) = 1 / (1 + exp(-100 (0.005 - rho))),
+ * eps_i = the normals of counters 3i, 3i+1, 3i+2 of stream 2 + 2 step (fp64). */
+void vko_mcmc_noise(int64_t n, float lr_pos, float noise_scale, uint64_t seed, uint32_t step, float* means,
+                    const float* log_scales, const float* quats, const float* opacity_logits);
+
 #ifdef __cplusplus
 }
 #endif

@@ -315,6 +315,41 @@ size_t vks_loss_workspace_bytes(int32_t width, int32_t height);
 int vks_loss_grad(int32_t width, int32_t height, float lambda, const float* render, const float* target,
                   float* dL_dimage, float* loss, void* workspace, size_t workspace_bytes, vks_stream_t stream);
 
+/* ---- MCMC densification at a fixed budget ------------------------------
+ *
+ * Counter-based generator (DESIGN.md §4.7 R1): h(seed, stream, i) = splitmix64(seed +
+ * 0x9E3779B97F4A7C15 * ((stream << 40) ^ i)); uniform ((h >> 40) + 0.5) / 2^24; normal = Box-Muller
+ * of the uniforms of counters 2k, 2k+1.
+ *
+ * vks_mcmc_relocate — relocation of "dead" Gaussians (SPEC S:273 densify_mcmc):
+ * rho_i = sigmoid(opacity_logit_i) (evaluated in fp64, rounded to fp32); dead_i = rho_i <
+ * dead_opacity; integer weights w_j = dead_j ? 0 : floor(rho_j 2^24); each dead i draws
+ * t = mulhi64(h(seed, 1, i), sum w) and takes the first j with inclusive prefix W_j > t
+ * (probability w_j / sum w), copies j's means, log_scales, quats and sh, and j with its k_j copies
+ * all get rho' = 1 - (1 - rho_j)^(1/(k_j+1)) (appearance-conserving: (1 - rho')^(k_j+1) = 1 - rho_j),
+ * logit' = log(rho'/(1 - rho')).  The copies' Adam moments are zeroed.  Count unchanged (the
+ * budget).  Targets are exact integer decisions: identical to the CPU oracle's.
+ *   parameters: device fp32 rows as vks_project_fwd's inputs, updated in place
+ *   m, v: HOST arrays of 5 DEVICE pointers (the vks_adam_step groups) or both NULL
+ *   targets: device int64 [n] (nullable) <- j for dead i, -1 otherwise
+ *   n_dead: device int64 [1] (nullable) <- number of dead Gaussians
+ *   workspace: device, 256-byte aligned, >= vks_mcmc_workspace_bytes(n) (~28 B per Gaussian)
+ * Errors: VKS_ERR_INVALID_ARG (null pointer, n < 0, sh_coeffs outside [1, 64], dead_opacity
+ * outside [0, 1), exactly one of m / v NULL); VKS_ERR_WORKSPACE.  Asynchronous on `stream`.
+ *
+ * vks_mcmc_noise — positional noise after an optimizer step (R5): means_i += lr_pos *
+ * noise_scale * gate(rho_i) * Rq_i diag(exp(log_scales_i)) eps_i, gate(rho) = sigmoid(100 (0.005 -
+ * rho)), eps_i = the normals of counters 3i .. 3i+2 of stream 2 + 2 step (fp64 arithmetic).
+ * quats 16-byte aligned.  Asynchronous on `stream`.
+ */
+size_t vks_mcmc_workspace_bytes(int64_t n);
+int vks_mcmc_relocate(int64_t n, int32_t sh_coeffs, float dead_opacity, uint64_t seed, float* means,
+                      float* log_scales, float* quats, float* opacity_logits, float* sh, float* const* m,
+                      float* const* v, int64_t* targets, int64_t* n_dead, void* workspace, size_t workspace_bytes,
+                      vks_stream_t stream);
+int vks_mcmc_noise(int64_t n, float lr_pos, float noise_scale, uint64_t seed, uint32_t step, float* means,
+                   const float* log_scales, const float* quats, const float* opacity_logits, vks_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

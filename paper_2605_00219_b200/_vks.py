@@ -27,7 +27,8 @@ FLAG_GRAD_OVERWRITE = 1
 EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_project_fwd",
            "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats",
            "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch",
-           "vks_adam_step", "vks_loss_workspace_bytes", "vks_loss_grad")
+           "vks_adam_step", "vks_loss_workspace_bytes", "vks_loss_grad", "vks_mcmc_workspace_bytes",
+           "vks_mcmc_relocate", "vks_mcmc_noise")
 
 
 class VksCamera(C.Structure):
@@ -82,6 +83,12 @@ _lib.vks_loss_workspace_bytes.restype = C.c_size_t
 _lib.vks_loss_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
 _lib.vks_loss_grad.argtypes = [C.c_int32, C.c_int32, C.c_float, _P, _P, _P, _P, _P, C.c_size_t, _P]
 _lib.vks_loss_grad.restype = C.c_int
+_lib.vks_mcmc_workspace_bytes.restype = C.c_size_t
+_lib.vks_mcmc_workspace_bytes.argtypes = [C.c_int64]
+_lib.vks_mcmc_relocate.argtypes = [C.c_int64, C.c_int32, C.c_float, C.c_uint64] + [_P] * 10 + [C.c_size_t, _P]
+_lib.vks_mcmc_relocate.restype = C.c_int
+_lib.vks_mcmc_noise.argtypes = [C.c_int64, C.c_float, C.c_float, C.c_uint64, C.c_uint32] + [_P] * 5
+_lib.vks_mcmc_noise.restype = C.c_int
 for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats", "vks_raster_bwd",
            "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch", "vks_adam_step"):
     getattr(_lib, _f).restype = C.c_int
@@ -332,6 +339,37 @@ def vks_loss_grad(render, target, dL_dimage, loss, workspace, lam=0.2, stream=No
                             _ptr(dL_dimage, f32, "dL_dimage"), _ptr(loss, f32, "loss"),
                             _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
     _check("vks_loss_grad", st)
+
+
+def vks_mcmc_workspace_bytes(n: int) -> int:
+    return int(_lib.vks_mcmc_workspace_bytes(int(n)))
+
+
+def vks_mcmc_relocate(params, workspace, dead_opacity=0.005, seed=0, m=None, v=None, targets=None, n_dead=None,
+                      stream=None):
+    """MCMC relocation: params = GaussianParams-like (means, log_scales, quats,
+    opacity_logits, sh tensors, updated in place); m, v: 5-sequences of Adam moment tensors (or
+    None); targets: int64 [n] device tensor (or None); n_dead: int64 [1] device tensor (or None)."""
+    n, K = params.means.shape[0], params.sh.shape[1]
+    if (m is None) != (v is None):
+        raise ValueError("pass both m and v, or neither")
+    ma = None if m is None else (C.c_void_p * 5)(*[_ptr(t, f32, "m") for t in m])
+    va = None if v is None else (C.c_void_p * 5)(*[_ptr(t, f32, "v") for t in v])
+    st = _lib.vks_mcmc_relocate(n, K, float(dead_opacity), int(seed), _ptr(params.means, f32, "means"),
+                                _ptr(params.log_scales, f32, "log_scales"), _ptr(params.quats, f32, "quats"),
+                                _ptr(params.opacity_logits, f32, "opacity_logits"), _ptr(params.sh, f32, "sh"), ma, va,
+                                _ptr(targets, torch.int64, "targets"), _ptr(n_dead, torch.int64, "n_dead"),
+                                _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
+    _check("vks_mcmc_relocate", st)
+
+
+def vks_mcmc_noise(params, lr_pos, noise_scale, seed=0, step=0, stream=None):
+    """Positional noise after an optimizer step: params.means updated in place."""
+    st = _lib.vks_mcmc_noise(params.means.shape[0], float(lr_pos), float(noise_scale), int(seed), int(step),
+                             _ptr(params.means, f32, "means"), _ptr(params.log_scales, f32, "log_scales"),
+                             _ptr(params.quats, f32, "quats"), _ptr(params.opacity_logits, f32, "opacity_logits"),
+                             _stream(stream))
+    _check("vks_mcmc_noise", st)
 
 
 def vks_version() -> int:

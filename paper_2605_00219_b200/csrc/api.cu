@@ -261,4 +261,38 @@ int vks_loss_grad(int32_t width, int32_t height, float lambda, const float* rend
                                              (cudaStream_t)stream));
 }
 
+size_t vks_mcmc_workspace_bytes(int64_t n) {
+    if (n < 0) return 0;
+    return vks::mcmc_workspace_bytes(n);
+}
+
+int vks_mcmc_relocate(int64_t n, int32_t sh_coeffs, float dead_opacity, uint64_t seed, float* means,
+                      float* log_scales, float* quats, float* opacity_logits, float* sh, float* const* m,
+                      float* const* v, int64_t* targets, int64_t* n_dead, void* workspace, size_t workspace_bytes,
+                      vks_stream_t stream) {
+    if (n < 0 || n >= ((int64_t)1 << 40) || sh_coeffs < 1 || sh_coeffs > 64) return VKS_ERR_INVALID_ARG;
+    if (!(dead_opacity >= 0.0f && dead_opacity < 1.0f)) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !workspace)) return VKS_ERR_INVALID_ARG;
+    if ((m == nullptr) != (v == nullptr)) return VKS_ERR_INVALID_ARG;
+    if (m)
+        for (int g = 0; g < 5; g++)
+            if (n > 0 && (!m[g] || !v[g])) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (workspace_bytes < vks::mcmc_workspace_bytes(n) || (reinterpret_cast<uintptr_t>(workspace) & 255)))
+        return VKS_ERR_WORKSPACE;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_mcmc_relocate(n, sh_coeffs, dead_opacity, seed, means, log_scales, quats,
+                                                 opacity_logits, sh, m, v, targets, n_dead, workspace,
+                                                 (cudaStream_t)stream));
+}
+
+int vks_mcmc_noise(int64_t n, float lr_pos, float noise_scale, uint64_t seed, uint32_t step, float* means,
+                   const float* log_scales, const float* quats, const float* opacity_logits, vks_stream_t stream) {
+    if (n < 0) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits)) return VKS_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(quats) & 15) return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_mcmc_noise(n, lr_pos, noise_scale, seed, step, means, log_scales, quats,
+                                              opacity_logits, (cudaStream_t)stream));
+}
+
 }  // extern "C"

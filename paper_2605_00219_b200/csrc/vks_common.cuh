@@ -128,6 +128,12 @@ int launch_project_bwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
                              float* dlog_scales, float* dquats, float* dopacity_logits, float* dsh, cudaStream_t s);
 int launch_adam_step(const vks_adam_config& acfg, int64_t n, int32_t sh_coeffs, float* const* params,
                      const float* const* grads, float* const* m, float* const* v, cudaStream_t s);
+size_t mcmc_workspace_bytes(int64_t n);
+int launch_mcmc_relocate(int64_t n, int32_t sh_coeffs, float dead_opacity, unsigned long long seed, float* means,
+                         float* log_scales, float* quats, float* opacity_logits, float* sh, float* const* m,
+                         float* const* v, int64_t* targets, int64_t* n_dead, void* workspace, cudaStream_t s);
+int launch_mcmc_noise(int64_t n, float lr_pos, float noise_scale, unsigned long long seed, uint32_t step, float* means,
+                      const float* log_scales, const float* quats, const float* opacity_logits, cudaStream_t s);
 size_t loss_workspace_bytes(int W, int H);
 int launch_loss_grad(int W, int H, float lambda, const float* render, const float* target, float* dL, float* loss,
                      void* workspace, cudaStream_t s);

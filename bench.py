@@ -407,6 +407,30 @@ def run_ours(args):
     torch.cuda.synchronize()
     loss_ms = statistics.median([a.elapsed_time(b) for a, b in loss_ev[1:]])
     del tgt, dl_tmp, lws
+    # MCMC densification on a copy of the parameters: one relocation (every
+    # 100 iterations in training) and one noise step (every iteration), timed on their own
+    import copy as _copy
+    pc = _copy.copy(params)
+    pc.means, pc.log_scales, pc.quats = params.means.clone(), params.log_scales.clone(), params.quats.clone()
+    pc.opacity_logits, pc.sh = params.opacity_logits.clone(), params.sh.clone()
+    mws = torch.empty(P.vks_mcmc_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    ndead = torch.zeros(1, dtype=torch.int64, device="cuda")
+    rel_ev, noi_ev = [], []
+    for t in range(4):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(main)
+        P.vks_mcmc_relocate(pc, mws, dead_opacity=0.005, seed=100 + t, n_dead=ndead)
+        e1.record(main)
+        P.vks_mcmc_noise(pc, 1.6e-4, 5e5, seed=100 + t, step=t)
+        e2.record(main)
+        rel_ev.append((e0, e1))
+        noi_ev.append((e1, e2))
+    torch.cuda.synchronize()
+    mcmc = dict(row="f3 (SURVEY 8f): vks_mcmc_relocate + vks_mcmc_noise on the bench scene; not in value",
+                relocate_ms=round(statistics.median([a.elapsed_time(b) for a, b in rel_ev[1:]]), 4),
+                noise_ms=round(statistics.median([a.elapsed_time(b) for a, b in noi_ev[1:]]), 4),
+                dead_last=int(ndead.item()))
+    del pc, mws
     st_ms["project_bwd"] = statistics.median([a.elapsed_time(b) for a, b in pb_ms]) / B
     st_ms = {k: st_ms[k] for k in stages}
     rend = rends[0]
@@ -485,7 +509,7 @@ def run_ours(args):
                                 replayed_pairs=replayed, warp_entries=warp_entries,
                                 warp_entries_composited=warp_entries_comp),
                roofline=roofline, gpu_launches=gpu_launches, clocks=clk, optimizer=optimizer,
-               loss_grad=loss_grad)
+               loss_grad=loss_grad, mcmc=mcmc)
 
     if not args.no_e2e:
         # (1) the path end to end: each view's dL/dimage copied in from pinned host memory and its

@@ -334,3 +334,54 @@ def mcmc_noise(scene, lr_pos, noise_scale, seed=0, step=0):
     o = np.ascontiguousarray(scene["opacity_logits"], np.float32)
     L.vko_mcmc_noise(means.shape[0], lr_pos, noise_scale, seed, step, _p(means), _p(ls), _p(q), _p(o))
     return means
+
+
+# ---- default densification (DESIGN.md §4.7 readings R6-R9) -----------
+def _densify_lib():
+    L = _mcmc_lib()
+    L.vko_densify_stats.argtypes = [C.c_int64] + [C.c_void_p] * 4
+    L.vko_densify.restype = C.c_int64
+    L.vko_densify.argtypes = ([C.c_int64, C.c_int32] + [C.c_void_p] * 9 + [C.c_float, C.c_float, C.c_float, C.c_uint64,
+                              C.c_int64] + [C.c_void_p] * 7)
+    return L
+
+
+def densify_stats(dmeans2d, radii, accum, denom):
+    """Returns updated copies of (accum, denom) after one view (vko_densify_stats)."""
+    L = _densify_lib()
+    a = np.ascontiguousarray(accum, np.float32).copy()
+    d = np.ascontiguousarray(denom, np.float32).copy()
+    g = np.ascontiguousarray(dmeans2d, np.float32)
+    r = np.ascontiguousarray(radii, np.int32)
+    L.vko_densify_stats(a.shape[0], _p(g), _p(r), _p(a), _p(d))
+    return a, d
+
+
+def densify(scene, accum, denom, grad_threshold, size_threshold, prune_opacity=0.005, seed=0, m=None, v=None,
+            cap=None):
+    """One densification event (vko_densify).  Returns (new scene dict, n', m', v') — n' only (and
+    None for the rest) when n' > cap."""
+    L = _densify_lib()
+    sc = {k: np.ascontiguousarray(scene[k], np.float32) for k in ("means", "log_scales", "quats", "opacity_logits", "sh")}
+    n, K = sc["means"].shape[0], sc["sh"].shape[1]
+    F = 11 + 3 * K
+    cap = 2 * n if cap is None else cap
+    out = dict(means=np.zeros((cap, 3), np.float32), log_scales=np.zeros((cap, 3), np.float32),
+               quats=np.zeros((cap, 4), np.float32), opacity_logits=np.zeros(cap, np.float32),
+               sh=np.zeros((cap, K, 3), np.float32))
+    om = np.zeros(max(cap, 1) * F, np.float32) if m is not None else None
+    ov = np.zeros(max(cap, 1) * F, np.float32) if v is not None else None
+    mm = None if m is None else np.ascontiguousarray(m, np.float32)
+    vv = None if v is None else np.ascontiguousarray(v, np.float32)
+    a = np.ascontiguousarray(accum, np.float32)
+    d = np.ascontiguousarray(denom, np.float32)
+    np_ = L.vko_densify(n, K, _p(sc["means"]), _p(sc["log_scales"]), _p(sc["quats"]), _p(sc["opacity_logits"]),
+                        _p(sc["sh"]), _p(mm), _p(vv), _p(a), _p(d), grad_threshold, size_threshold, prune_opacity,
+                        seed, cap, _p(out["means"]), _p(out["log_scales"]), _p(out["quats"]),
+                        _p(out["opacity_logits"]), _p(out["sh"]), _p(om), _p(ov))
+    if np_ > cap:
+        return None, int(np_), None, None
+    out = {k: a_[:np_] for k, a_ in out.items()}
+    if om is not None:  # the flat group-major moments of n' rows are the first n' F entries
+        om, ov = om[:np_ * F], ov[:np_ * F]
+    return out, int(np_), om, ov

@@ -1171,3 +1171,82 @@ void vko_mcmc_noise(int64_t n, float lr_pos, float noise_scale, uint64_t seed, u
             means[3 * i + r] = (float)((double)means[3 * i + r] + kk * (R[3 * r] * e[0] + R[3 * r + 1] * e[1] + R[3 * r + 2] * e[2]));
     }
 }
+
+/* ---- default densification: S:261-269, readings R6-R9 ----------------------- */
+void vko_densify_stats(int64_t n, const float* dmeans2d, const int32_t* radii, float* accum, float* denom) {
+    for (int64_t i = 0; i < n; i++) {
+        if (radii[2 * i] <= 0 && radii[2 * i + 1] <= 0) continue;
+        const double gx = dmeans2d[2 * i], gy = dmeans2d[2 * i + 1];
+        accum[i] = (float)((double)accum[i] + sqrt(gx * gx + gy * gy));
+        denom[i] = denom[i] + 1.0f;
+    }
+}
+
+static int densify_kind(int64_t i, const float* log_scales, const float* opacity_logits, const float* accum,
+                        const float* denom, float gthr, float sthr, float pop) {
+    const float rho = x64_sigmoid(opacity_logits[i]);
+    if (rho < pop) return 0;                                     /* prune */
+    const float g = denom[i] > 0.0f ? accum[i] / denom[i] : 0.0f;
+    if (!(g > gthr)) return 1;                                   /* keep */
+    float smax = expf(log_scales[3 * i]);
+    for (int c = 1; c < 3; c++) smax = fmaxf(smax, expf(log_scales[3 * i + c]));
+    return smax < sthr ? 2 : 3;                                  /* clone : split */
+}
+
+int64_t vko_densify(int64_t n, int32_t sh_coeffs, const float* means, const float* log_scales, const float* quats,
+                    const float* opacity_logits, const float* sh, const float* m, const float* v,
+                    const float* accum, const float* denom, float grad_threshold, float size_threshold,
+                    float prune_opacity, uint64_t seed, int64_t cap, float* o_means, float* o_log_scales,
+                    float* o_quats, float* o_opacity_logits, float* o_sh, float* o_m, float* o_v) {
+    const int64_t S = 3 * (int64_t)sh_coeffs;
+    int64_t np = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const int k = densify_kind(i, log_scales, opacity_logits, accum, denom, grad_threshold, size_threshold,
+                                   prune_opacity);
+        np += k == 0 ? 0 : (k == 1 ? 1 : 2);
+    }
+    if (np > cap) return np;
+    const int64_t wid[5] = {3, 3, 4, 1, S};
+    int64_t o = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const int k = densify_kind(i, log_scales, opacity_logits, accum, denom, grad_threshold, size_threshold,
+                                   prune_opacity);
+        const int rows = k == 0 ? 0 : (k == 1 ? 1 : 2);
+        for (int r = 0; r < rows; r++, o++) {
+            memcpy(o_means + 3 * o, means + 3 * i, 3 * sizeof(float));
+            memcpy(o_log_scales + 3 * o, log_scales + 3 * i, 3 * sizeof(float));
+            memcpy(o_quats + 4 * o, quats + 4 * i, 4 * sizeof(float));
+            o_opacity_logits[o] = opacity_logits[i];
+            memcpy(o_sh + S * o, sh + S * i, (size_t)S * sizeof(float));
+            if (k == 3) {  /* split child r */
+                const double a = quats[4 * i], b = quats[4 * i + 1], c = quats[4 * i + 2], d = quats[4 * i + 3];
+                const double qn = sqrt(a * a + b * b + c * c + d * d);
+                const double w = a / qn, x = b / qn, y = c / qn, z = d / qn;
+                const double R[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                                     2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                                     2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+                double e[3];
+                for (int q = 0; q < 3; q++)
+                    e[q] = exp((double)log_scales[3 * i + q]) * rng_normal(seed, 3, 6 * (uint64_t)i + 3 * r + q);
+                for (int q = 0; q < 3; q++) {
+                    o_means[3 * o + q] = (float)((double)means[3 * i + q] + R[3 * q] * e[0] + R[3 * q + 1] * e[1] +
+                                                 R[3 * q + 2] * e[2]);
+                    o_log_scales[3 * o + q] = (float)((double)log_scales[3 * i + q] - log(1.6));
+                }
+            }
+            if (o_m && o_v) {
+                const int fresh = (k == 2 && r == 1) || k == 3;
+                int64_t off = 0, offo = 0;
+                for (int g = 0; g < 5; g++) {
+                    for (int64_t c = 0; c < wid[g]; c++) {
+                        o_m[offo + wid[g] * o + c] = (fresh || !m) ? 0.0f : m[off + wid[g] * i + c];
+                        o_v[offo + wid[g] * o + c] = (fresh || !v) ? 0.0f : v[off + wid[g] * i + c];
+                    }
+                    off += wid[g] * n;
+                    offo += wid[g] * np;
+                }
+            }
+        }
+    }
+    return np;
+}

@@ -209,6 +209,28 @@ int64_t vko_mcmc_relocate(int64_t n, int32_t sh_coeffs, float dead_opacity, uint
 void vko_mcmc_noise(int64_t n, float lr_pos, float noise_scale, uint64_t seed, uint32_t step, float* means,
                     const float* log_scales, const float* quats, const float* opacity_logits);
 
+/* ---- default densification ---------------------------------------------- */
+
+/* Screen-gradient statistics ("mean accumulated screen-gradient norm"; reading R6):
+ * for every Gaussian the view rasterised (radii > 0): accum += |dL/dmean2d| (Euclidean, pixels),
+ * denom += 1. */
+void vko_densify_stats(int64_t n, const float* dmeans2d, const int32_t* radii, float* accum, float* denom);
+
+/* One densification event (readings R7-R9 of DESIGN.md §4.7).  Per Gaussian i
+ * (rho = X64 sigmoid): prune if rho < prune_opacity; else with g = accum / denom (0 if denom = 0)
+ * and smax = max exp(log_scales): g > grad_threshold and smax < size_threshold -> clone (the row,
+ * then an identical copy), g > grad_threshold and smax >= size_threshold -> split (two children:
+ * log_scales - ln 1.6, means + Rq diag(s) eps with eps the normals of counters 6i + 3c .. of stream
+ * 3 (child c = 0, 1), other parameters copied), else keep.  Rows are emitted in i order (a clone's
+ * copy and a split's second child right after); new rows (copies, children) get zero moments, kept
+ * rows keep theirs.  m, v: flat group-major [n (11 + 3K)] (nullable; outputs likewise with n').
+ * Returns n'; writes the outputs only if n' <= cap. */
+int64_t vko_densify(int64_t n, int32_t sh_coeffs, const float* means, const float* log_scales, const float* quats,
+                    const float* opacity_logits, const float* sh, const float* m, const float* v,
+                    const float* accum, const float* denom, float grad_threshold, float size_threshold,
+                    float prune_opacity, uint64_t seed, int64_t cap, float* o_means, float* o_log_scales,
+                    float* o_quats, float* o_opacity_logits, float* o_sh, float* o_m, float* o_v);
+
 #ifdef __cplusplus
 }
 #endif

@@ -350,6 +350,39 @@ int vks_mcmc_relocate(int64_t n, int32_t sh_coeffs, float dead_opacity, uint64_t
 int vks_mcmc_noise(int64_t n, float lr_pos, float noise_scale, uint64_t seed, uint32_t step, float* means,
                    const float* log_scales, const float* quats, const float* opacity_logits, vks_stream_t stream);
 
+/* ---- default densification --------------------------------------------
+ *
+ * vks_densify_stats — screen-gradient statistics ("mean accumulated screen-gradient
+ * norm"; DESIGN.md §4.7 R6), after a view's vks_raster_bwd: for every Gaussian the view rasterised
+ * (radii != 0): accum += |dmeans2d| (Euclidean, pixels), denom += 1.
+ *   dmeans2d [n,2] fp32, radii [n,2] i32 (8-byte aligned), accum / denom [n] fp32 (in place).
+ *
+ * vks_densify — one densification event (R7-R9).  Per Gaussian (rho = sigmoid(logit)
+ * in fp64, rounded to fp32): rho < prune_opacity -> removed; else with g = accum / denom (0 when
+ * denom = 0) and smax = the largest exp(log_scale): g > grad_threshold and smax < size_threshold
+ * -> cloned (the row, then an identical copy); g > grad_threshold and smax >= size_threshold ->
+ * split (two children: log_scales - ln 1.6, means + Rq diag(s) eps with eps the normals of
+ * counters 6i + 3c .. 6i + 3c + 2 of stream 3 of the vks_mcmc generator, everything else copied);
+ * otherwise kept.  Rows are written in input order (a copy or second child right after its
+ * source); new rows get zero Adam moments, kept rows keep theirs.
+ *   params: HOST array of 5 DEVICE pointers (means, log_scales, quats, opacity_logits, sh as
+ *     vks_project_fwd's inputs); m, v: HOST arrays of 5 DEVICE pointers (vks_adam_step groups) or
+ *     both NULL; out_params / out_m / out_v likewise, each with room for `capacity` rows
+ *     (outputs never alias inputs)
+ *   *n_out (HOST) <- n', the new count.  If n' > capacity: VKS_ERR_CAPACITY, nothing else
+ *     written (grow the outputs, e.g. x1.5 as S:312, and call again).  Synchronises `stream`
+ *     once (to read n').
+ *   workspace: device, 256-byte aligned, >= vks_densify_workspace_bytes(n).
+ * Opacity reset (every 3000 iterations) is a clamp of the logits the caller applies.
+ */
+int vks_densify_stats(int64_t n, const float* dmeans2d, const int32_t* radii, float* accum, float* denom,
+                      vks_stream_t stream);
+size_t vks_densify_workspace_bytes(int64_t n);
+int vks_densify(int64_t n, int32_t sh_coeffs, const float* const* params, const float* const* m, const float* const* v,
+                const float* accum, const float* denom, float grad_threshold, float size_threshold, float prune_opacity,
+                uint64_t seed, int64_t capacity, float* const* out_params, float* const* out_m, float* const* out_v,
+                int64_t* n_out, void* workspace, size_t workspace_bytes, vks_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

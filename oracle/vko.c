@@ -1188,8 +1188,8 @@ static int densify_kind(int64_t i, const float* log_scales, const float* opacity
     if (rho < pop) return 0;                                     /* prune */
     const float g = denom[i] > 0.0f ? accum[i] / denom[i] : 0.0f;
     if (!(g > gthr)) return 1;                                   /* keep */
-    float smax = expf(log_scales[3 * i]);
-    for (int c = 1; c < 3; c++) smax = fmaxf(smax, expf(log_scales[3 * i + c]));
+    float smax = (float)exp((double)log_scales[3 * i]);
+    for (int c = 1; c < 3; c++) smax = fmaxf(smax, (float)exp((double)log_scales[3 * i + c]));
     return smax < sthr ? 2 : 3;                                  /* clone : split */
 }
 

@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 PINNED = {"project.cu", "binning.cu"}
-SOURCES = ["project.cu", "project_bwd.cu", "binning.cu", "raster.cu", "adam.cu", "loss.cu", "mcmc.cu", "api.cu"]
+SOURCES = ["project.cu", "project_bwd.cu", "binning.cu", "raster.cu", "adam.cu", "loss.cu", "mcmc.cu", "densify.cu", "api.cu"]
 HEADERS = ["vks_common.cuh"]
 
 

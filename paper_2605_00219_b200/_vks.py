@@ -28,7 +28,8 @@ EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_proje
            "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats",
            "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch",
            "vks_adam_step", "vks_loss_workspace_bytes", "vks_loss_grad", "vks_mcmc_workspace_bytes",
-           "vks_mcmc_relocate", "vks_mcmc_noise")
+           "vks_mcmc_relocate", "vks_mcmc_noise", "vks_densify_stats", "vks_densify_workspace_bytes",
+           "vks_densify")
 
 
 class VksCamera(C.Structure):
@@ -89,6 +90,13 @@ _lib.vks_mcmc_relocate.argtypes = [C.c_int64, C.c_int32, C.c_float, C.c_uint64] 
 _lib.vks_mcmc_relocate.restype = C.c_int
 _lib.vks_mcmc_noise.argtypes = [C.c_int64, C.c_float, C.c_float, C.c_uint64, C.c_uint32] + [_P] * 5
 _lib.vks_mcmc_noise.restype = C.c_int
+_lib.vks_densify_stats.argtypes = [C.c_int64] + [_P] * 5
+_lib.vks_densify_stats.restype = C.c_int
+_lib.vks_densify_workspace_bytes.restype = C.c_size_t
+_lib.vks_densify_workspace_bytes.argtypes = [C.c_int64]
+_lib.vks_densify.argtypes = ([C.c_int64, C.c_int32] + [_P] * 5 + [C.c_float, C.c_float, C.c_float, C.c_uint64,
+                             C.c_int64] + [_P] * 5 + [C.c_size_t, _P])
+_lib.vks_densify.restype = C.c_int
 for _f in ("vks_project_fwd", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats", "vks_raster_bwd",
            "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch", "vks_adam_step"):
     getattr(_lib, _f).restype = C.c_int
@@ -370,6 +378,38 @@ def vks_mcmc_noise(params, lr_pos, noise_scale, seed=0, step=0, stream=None):
                              _ptr(params.quats, f32, "quats"), _ptr(params.opacity_logits, f32, "opacity_logits"),
                              _stream(stream))
     _check("vks_mcmc_noise", st)
+
+
+def vks_densify_stats(dmeans2d, radii, accum, denom, stream=None):
+    """Screen-gradient statistics of one view: accum / denom updated in place."""
+    st = _lib.vks_densify_stats(accum.shape[0], _ptr(dmeans2d, f32, "dmeans2d"), _ptr(radii, i32, "radii"),
+                                _ptr(accum, f32, "accum"), _ptr(denom, f32, "denom"), _stream(stream))
+    _check("vks_densify_stats", st)
+
+
+def vks_densify_workspace_bytes(n: int) -> int:
+    return int(_lib.vks_densify_workspace_bytes(int(n)))
+
+
+def vks_densify(params, accum, denom, out_params, workspace, grad_threshold, size_threshold, prune_opacity=0.005,
+                seed=0, m=None, v=None, out_m=None, out_v=None, stream=None) -> int:
+    """One densification event.  params / out_params (/ m, v, out_m, out_v):
+    5-sequences of fp32 tensors in ADAM_GROUPS order; the outputs' first dimension is the capacity.
+    Returns n'; raises VksError(VKS_ERR_CAPACITY) when n' exceeds it (VksError.n_out holds n')."""
+    n, K = params[0].shape[0], params[4].shape[1]
+    cap = out_params[0].shape[0]
+    arr = lambda seq, nm: None if seq is None else (C.c_void_p * 5)(*[_ptr(t, f32, nm) for t in seq])  # noqa: E731
+    n_out = C.c_int64(0)
+    st = _lib.vks_densify(n, K, arr(params, "params"), arr(m, "m"), arr(v, "v"), _ptr(accum, f32, "accum"),
+                          _ptr(denom, f32, "denom"), float(grad_threshold), float(size_threshold),
+                          float(prune_opacity), int(seed), cap, arr(out_params, "out_params"), arr(out_m, "out_m"),
+                          arr(out_v, "out_v"), C.byref(n_out), _ptr(workspace, torch.uint8, "workspace"),
+                          workspace.numel(), _stream(stream))
+    if st != VKS_OK:
+        err = VksError("vks_densify", st)
+        err.n_out = int(n_out.value)
+        raise err
+    return int(n_out.value)
 
 
 def vks_version() -> int:

@@ -295,4 +295,40 @@ int vks_mcmc_noise(int64_t n, float lr_pos, float noise_scale, uint64_t seed, ui
                                               opacity_logits, (cudaStream_t)stream));
 }
 
+int vks_densify_stats(int64_t n, const float* dmeans2d, const int32_t* radii, float* accum, float* denom,
+                      vks_stream_t stream) {
+    if (n < 0) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!dmeans2d || !radii || !accum || !denom)) return VKS_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(dmeans2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7)) return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_densify_stats(n, dmeans2d, radii, accum, denom, (cudaStream_t)stream));
+}
+
+size_t vks_densify_workspace_bytes(int64_t n) {
+    if (n < 0) return 0;
+    return vks::densify_workspace_bytes(n);
+}
+
+int vks_densify(int64_t n, int32_t sh_coeffs, const float* const* params, const float* const* m, const float* const* v,
+                const float* accum, const float* denom, float grad_threshold, float size_threshold, float prune_opacity,
+                uint64_t seed, int64_t capacity, float* const* out_params, float* const* out_m, float* const* out_v,
+                int64_t* n_out, void* workspace, size_t workspace_bytes, vks_stream_t stream) {
+    if (n < 0 || n >= ((int64_t)1 << 31) || sh_coeffs < 1 || sh_coeffs > 64 || capacity < 0 || !n_out)
+        return VKS_ERR_INVALID_ARG;
+    if (!params || !out_params) return VKS_ERR_INVALID_ARG;
+    if ((m == nullptr) != (v == nullptr) || (out_m == nullptr) != (out_v == nullptr)) return VKS_ERR_INVALID_ARG;
+    for (int g = 0; g < 5; g++) {
+        if (n > 0 && (!params[g] || !out_params[g])) return VKS_ERR_INVALID_ARG;
+        if (n > 0 && m && (!m[g] || !v[g])) return VKS_ERR_INVALID_ARG;
+        if (n > 0 && out_m && (!out_m[g] || !out_v[g])) return VKS_ERR_INVALID_ARG;
+    }
+    if (n > 0 && (!accum || !denom || !workspace)) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (workspace_bytes < vks::densify_workspace_bytes(n) || (reinterpret_cast<uintptr_t>(workspace) & 255)))
+        return VKS_ERR_WORKSPACE;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::launch_densify(n, sh_coeffs, params, m, v, accum, denom, grad_threshold, size_threshold,
+                                           prune_opacity, seed, capacity, out_params, out_m, out_v, n_out, workspace,
+                                           (cudaStream_t)stream));
+}
+
 }  // extern "C"

@@ -128,6 +128,14 @@ int launch_project_bwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
                              float* dlog_scales, float* dquats, float* dopacity_logits, float* dsh, cudaStream_t s);
 int launch_adam_step(const vks_adam_config& acfg, int64_t n, int32_t sh_coeffs, float* const* params,
                      const float* const* grads, float* const* m, float* const* v, cudaStream_t s);
+size_t densify_workspace_bytes(int64_t n);
+int launch_densify_stats(int64_t n, const float* dmeans2d, const int32_t* radii, float* accum, float* denom,
+                         cudaStream_t s);
+int launch_densify(int64_t n, int32_t sh_coeffs, const float* const* params, const float* const* m,
+                   const float* const* v, const float* accum, const float* denom, float grad_threshold,
+                   float size_threshold, float prune_opacity, unsigned long long seed, int64_t capacity,
+                   float* const* out_params, float* const* out_m, float* const* out_v, int64_t* n_out, void* workspace,
+                   cudaStream_t s);
 size_t mcmc_workspace_bytes(int64_t n);
 int launch_mcmc_relocate(int64_t n, int32_t sh_coeffs, float dead_opacity, unsigned long long seed, float* means,
                          float* log_scales, float* quats, float* opacity_logits, float* sh, float* const* m,

@@ -430,7 +430,35 @@ def run_ours(args):
                 relocate_ms=round(statistics.median([a.elapsed_time(b) for a, b in rel_ev[1:]]), 4),
                 noise_ms=round(statistics.median([a.elapsed_time(b) for a, b in noi_ev[1:]]), 4),
                 dead_last=int(ndead.item()))
-    del pc, mws
+    # default densification (row f4): the statistics of the batch's 8 views, then one event (out of
+    # place into buffers with room for 2n), thresholds chosen so that ~5% of the Gaussians grow
+    acc, den = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for j in range(B):
+        P.vks_densify_stats(vbuf[j]["dm2"], vbuf[j]["radii"], acc, den)
+    e1.record(main)
+    torch.cuda.synchronize()
+    stats_ms = e0.elapsed_time(e1) / B
+    mg = (acc / den.clamp(min=1)).float()
+    gthr = float(torch.quantile(mg[den > 0][:1 << 24].float(), 0.95).item()) if bool((den > 0).any()) else 1.0
+    sthr = float(torch.quantile(params.log_scales.max(1).values.exp()[:1 << 24], 0.5).item())
+    src = [params.means, params.log_scales, params.quats, params.opacity_logits, params.sh]
+    dst = [torch.empty((2 * n,) + tuple(t.shape[1:]), device="cuda") for t in src]
+    dws = torch.empty(P.vks_densify_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    dens_ev, n_new = [], 0
+    for t in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        n_new = P.vks_densify(src, acc, den, dst, dws, gthr, sthr, 0.005, seed=t)
+        e1.record(main)
+        dens_ev.append((e0, e1))
+    torch.cuda.synchronize()
+    densify = dict(row="f4 (SURVEY 8f): vks_densify_stats per view + one vks_densify event; not in value",
+                   stats_ms_per_view=round(stats_ms, 4),
+                   densify_ms=round(statistics.median([a.elapsed_time(b) for a, b in dens_ev[1:]]), 4),
+                   n_before=n, n_after=n_new)
+    del pc, mws, dst, dws, acc, den
     st_ms["project_bwd"] = statistics.median([a.elapsed_time(b) for a, b in pb_ms]) / B
     st_ms = {k: st_ms[k] for k in stages}
     rend = rends[0]
@@ -509,7 +537,7 @@ def run_ours(args):
                                 replayed_pairs=replayed, warp_entries=warp_entries,
                                 warp_entries_composited=warp_entries_comp),
                roofline=roofline, gpu_launches=gpu_launches, clocks=clk, optimizer=optimizer,
-               loss_grad=loss_grad, mcmc=mcmc)
+               loss_grad=loss_grad, mcmc=mcmc, densify=densify)
 
     if not args.no_e2e:
         # (1) the path end to end: each view's dL/dimage copied in from pinned host memory and its

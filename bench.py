@@ -110,7 +110,8 @@ def algorithmic_bytes(n, vis, m, dpasses=4, batch=1, K=16):
         # and the opacity (4 B) written once per batch of `batch` views (SH for all n: upper bound
         # of the Gaussians some view shows); radii + tiles written for all (12 B), the other 36 B
         # of outputs for the visible
-        project_fwd=(44 + sh) * n / batch + 4 * n / batch + 12 * n + 36 * vis,
+        # ... plus the 36 B of 2D-gradient accumulators zeroed per Gaussian and view (g2d_zero)
+        project_fwd=(44 + sh) * n / batch + 4 * n / batch + 12 * n + 36 * vis + 36 * n,
         # id-order scan (read tiles twice, write offsets) + compaction of the visible (read depth,
         # means2d, radii; write depth key, id, rect code) + `dpasses` depth passes over V (count
         # 4 B, scatter 8 B in / 8 B out) + depth-order scan (ids + gathered rect codes in, rect
@@ -188,9 +189,9 @@ def run_ours(args):
     # soon as blocks of another view's raster kernels retire
     bstreams = [torch.cuda.Stream(priority=-1) for _ in range(S)] if args.prio else streams
     cfg_ow = dict(cfg, flags=P.FLAG_GRAD_OVERWRITE)
-    # stage boundaries (CUDA events on the launching stream); zero_2d is the caller's clear of
-    # the 2D-gradient accumulators that raster_bwd adds into (a torch fill, not one of ours)
-    stages = ["project_fwd", "bin_sort", "raster_fwd", "zero_2d", "raster_bwd", "project_bwd"]
+    # stage boundaries (CUDA events on the launching stream); the 2D-gradient accumulators that
+    # raster_bwd adds into are zeroed by the batched projection forward (g2d_zero)
+    stages = ["project_fwd", "bin_sort", "raster_fwd", "raster_bwd", "project_bwd"]
 
     copy_stream = torch.cuda.Stream()
 
@@ -215,7 +216,8 @@ def run_ours(args):
                                     params.sh, [vbuf[j]["means2d"] for j in range(nb)],
                                     [vbuf[j]["conics"] for j in range(nb)], [vbuf[j]["depths"] for j in range(nb)],
                                     [vbuf[j]["radii"] for j in range(nb)], [vbuf[j]["tiles"] for j in range(nb)],
-                                    [vbuf[j]["colors"] for j in range(nb)], opac)
+                                    [vbuf[j]["colors"] for j in range(nb)], opac,
+                                    g2d_zero=[vbuf[j]["g2d"] for j in range(nb)])
 
     def view_path(rend, vb, cam, dL, st, ev=None, copies=None):
         """One view's forward and raster backward on stream `st` (S views in flight, one stream
@@ -260,12 +262,10 @@ def run_ours(args):
                 slot["in_free"].record(st)
                 dL = slot["dL"]
             if ev is not None: ev[3].record(st)
-            vb["g2d"].zero_()
-            if ev is not None: ev[4].record(st)
             P.vks_raster_bwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],
                              rend.vals, rend.tile_offsets, rend.T_final, rend.n_contrib, dL, vb["dm2"], vb["dcon"],
                              vb["dcol"], vb["dop"], tile_order=rend.tile_order)
-            if ev is not None: ev[5].record(st)
+            if ev is not None: ev[4].record(st)
             if copies is not None and loss_out is None:
                 slot["in_free"].record(st)
             done = torch.cuda.Event()

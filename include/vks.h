@@ -235,13 +235,17 @@ int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
  *     pointers, each laid out as the matching vks_project_fwd output
  *   opacities [n]: one array for the batch (the opacity is view-independent); rows the
  *     footprint test culls are unspecified
+ *   g2d_zero (nullable): HOST array of n_views DEVICE pointers, each a view's [9n] fp32 block of
+ *     2D-gradient accumulators (dmeans2d [n,2] | dconics [n,3] | dcolors [n,3] | dopacities [n],
+ *     8-byte aligned) that vks_raster_bwd will add into: zeroed here, in the same pass, instead
+ *     of by a separate memset
  */
 int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,
                           const float* means, const float* log_scales, const float* quats,
                           const float* opacity_logits, const float* sh, float* const* means2d,
                           float* const* conics, float* const* depths, int32_t* const* radii,
                           int32_t* const* tiles_touched, float* const* colors, float* opacities,
-                          vks_stream_t stream);
+                          float* const* g2d_zero, vks_stream_t stream);
 
 /*
  * vks_project_bwd_batch — the projection backward of a batch of views in one pass: the sum over

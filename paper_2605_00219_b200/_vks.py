@@ -78,7 +78,7 @@ _lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 16
 _lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 10
 _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
 _lib.vks_project_bwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 17
-_lib.vks_project_fwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 13
+_lib.vks_project_fwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 14
 _lib.vks_adam_step.argtypes = [_P, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]
 _lib.vks_loss_workspace_bytes.restype = C.c_size_t
 _lib.vks_loss_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
@@ -268,9 +268,10 @@ def vks_project_bwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, colo
 
 
 def vks_project_fwd_batch(cfg, cams, means, log_scales, quats, opacity_logits, sh, means2d, conics, depths, radii,
-                          tiles_touched, colors, opacities, stream=None):
+                          tiles_touched, colors, opacities, g2d_zero=None, stream=None):
     """Batched projection forward: `cams` and the per-view outputs (means2d, conics, depths, radii,
-    tiles_touched, colors) are equal-length sequences; `opacities` is one tensor for the batch."""
+    tiles_touched, colors) are equal-length sequences; `opacities` is one tensor for the batch;
+    g2d_zero (optional): per view a [9n] fp32 tensor of 2D-gradient accumulators to zero."""
     nv = len(cams)
     per_view = (means2d, conics, depths, radii, tiles_touched, colors)
     if any(len(x) != nv for x in per_view):
@@ -283,7 +284,10 @@ def vks_project_fwd_batch(cfg, cams, means, log_scales, quats, opacity_logits, s
     st = _lib.vks_project_fwd_batch(C.byref(c), nv, karr, means.shape[0], _ptr(means, f32, "means"),
                                     _ptr(log_scales, f32, "log_scales"), _ptr(quats, f32, "quats"),
                                     _ptr(opacity_logits, f32, "opacity_logits"), _ptr(sh, f32, "sh"), *arrs,
-                                    _ptr(opacities, f32, "opacities"), _stream(stream))
+                                    _ptr(opacities, f32, "opacities"),
+                                    None if g2d_zero is None else (C.c_void_p * max(nv, 1))(
+                                        *[_ptr(t, f32, "g2d_zero") for t in g2d_zero]),
+                                    _stream(stream))
     _check("vks_project_fwd_batch", st)
 
 

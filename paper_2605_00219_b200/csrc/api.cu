@@ -177,11 +177,14 @@ int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
                           const float* opacity_logits, const float* sh, float* const* means2d,
                           float* const* conics, float* const* depths, int32_t* const* radii,
                           int32_t* const* tiles_touched, float* const* colors, float* opacities,
-                          vks_stream_t stream) {
+                          float* const* g2d_zero, vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (n_views < 1 || n_views > 16 || !cams || n < 0) return VKS_ERR_INVALID_ARG;
     if (!means2d || !conics || !depths || !radii || !tiles_touched || !colors) return VKS_ERR_INVALID_ARG;
+    if (g2d_zero)
+        for (int v = 0; v < n_views; v++)
+            if (n > 0 && (!g2d_zero[v] || (reinterpret_cast<uintptr_t>(g2d_zero[v]) & 7))) return VKS_ERR_INVALID_ARG;
     for (int v = 0; v < n_views; v++) {
         if (!camera_ok(cams + v) || cams[v].width != cams[0].width || cams[v].height != cams[0].height)
             return VKS_ERR_INVALID_ARG;
@@ -195,7 +198,7 @@ int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
     if (!device_present()) return VKS_ERR_CUDA;
     return cuda_status(vks::launch_project_fwd_batch(*cfg, n_views, cams, n, means, log_scales, quats, opacity_logits,
                                                      sh, means2d, conics, depths, radii, tiles_touched, colors,
-                                                     opacities, (cudaStream_t)stream));
+                                                     opacities, g2d_zero, (cudaStream_t)stream));
 }
 
 int vks_project_bwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,

@@ -419,6 +419,7 @@ struct FwdViewOut {
     int2* radii;
     int* tiles;
     float* colors;
+    float* g2d;  // nullable: the view's 2D-gradient accumulators [9n] (dmeans2d | dconics | dcolors | dopacities), zeroed
 };
 
 struct BatchFwdParams {
@@ -622,6 +623,14 @@ __global__ void __launch_bounds__(kThreads) project_fwd_batch_kernel(const Batch
             vis = ok;
         }
         if (!valid) continue;
+        if (V.g2d) {  // the raster backward's accumulators, cleared here instead of by a separate pass
+            reinterpret_cast<float2*>(V.g2d)[i] = make_float2(0.0f, 0.0f);
+            float* dcon = V.g2d + 2 * p.n + 3 * i;
+            float* dcol = V.g2d + 5 * p.n + 3 * i;
+            dcon[0] = 0.0f; dcon[1] = 0.0f; dcon[2] = 0.0f;
+            dcol[0] = 0.0f; dcol[1] = 0.0f; dcol[2] = 0.0f;
+            V.g2d[8 * p.n + i] = 0.0f;
+        }
         if (vis) {
             V.means2d[i] = make_float2(k.u, k.v);
             V.conics[3 * i + 0] = k.a;
@@ -711,7 +720,8 @@ int launch_project_fwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
                              const float* means, const float* log_scales, const float* quats,
                              const float* opacity_logits, const float* sh, float* const* means2d,
                              float* const* conics, float* const* depths, int32_t* const* radii,
-                             int32_t* const* tiles_touched, float* const* colors, float* opacities, cudaStream_t s) {
+                             int32_t* const* tiles_touched, float* const* colors, float* opacities,
+                             float* const* g2d_zero, cudaStream_t s) {
     if (n == 0) return VKS_OK;
     if (n_views < 1 || n_views > kMaxFwdViews) return VKS_ERR_INVALID_ARG;
     BatchFwdParams p{};
@@ -728,6 +738,7 @@ int launch_project_fwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
         V.radii = reinterpret_cast<int2*>(radii[v]);
         V.tiles = tiles_touched[v];
         V.colors = colors[v];
+        V.g2d = g2d_zero ? g2d_zero[v] : nullptr;
     }
     const bool al = aligned16(sh);
     switch (cfg.sh_coeffs) {

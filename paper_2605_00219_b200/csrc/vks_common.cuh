@@ -119,7 +119,8 @@ int launch_project_fwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
                              const float* means, const float* log_scales, const float* quats,
                              const float* opacity_logits, const float* sh, float* const* means2d,
                              float* const* conics, float* const* depths, int32_t* const* radii,
-                             int32_t* const* tiles_touched, float* const* colors, float* opacities, cudaStream_t s);
+                             int32_t* const* tiles_touched, float* const* colors, float* opacities,
+                             float* const* g2d_zero, cudaStream_t s);
 int launch_project_bwd_batch(const vks_config& cfg, int32_t n_views, const vks_camera* cams, int64_t n,
                              const float* means, const float* log_scales, const float* quats,
                              const float* opacity_logits, const float* sh, const float* const* colors,

@@ -447,7 +447,8 @@ def test_project_bwd_batch_equals_sum_of_views(oracle_lib, coeffs, deg, nv):
 @pytest.mark.parametrize("coeffs,deg,nv,fp", [(16, 3, 5, 0), (9, 2, 3, 0), (4, 1, 2, 1), (1, 0, 1, 0)])
 def test_project_fwd_batch_bit_exact(oracle_lib, coeffs, deg, nv, fp):
     """vks_project_fwd_batch: every view's outputs bit-identical to vks_project_fwd for that view
-    and to the oracle's O1 (P1), the opacities equal for every visible row."""
+    and to the oracle's O1 (P1), the opacities equal for every visible row; the optional
+    2D-gradient blocks (g2d_zero) come back zeroed (every row, culled or not)."""
     import torch
     import paper_2605_00219_b200 as P
     s = synth.make_scene(30001, "outdoor", 90 + nv)
@@ -460,10 +461,13 @@ def test_project_fwd_batch_bit_exact(oracle_lib, coeffs, deg, nv, fp):
     outs = [dict(means2d=e(n, 2), conics=e(n, 3), depths=e(n), radii=e(n, 2, dt=torch.int32),
                  tiles=e(n, dt=torch.int32), colors=e(n, 3)) for _ in range(nv)]
     opac = e(n)
+    g2d = [torch.full((9 * n,), float("nan"), device="cuda") for _ in range(nv)]
     P.vks_project_fwd_batch(cfg, cams, params.means, params.log_scales, params.quats, params.opacity_logits, params.sh,
                             [o["means2d"] for o in outs], [o["conics"] for o in outs], [o["depths"] for o in outs],
-                            [o["radii"] for o in outs], [o["tiles"] for o in outs], [o["colors"] for o in outs], opac)
+                            [o["radii"] for o in outs], [o["tiles"] for o in outs], [o["colors"] for o in outs], opac,
+                            g2d_zero=g2d)
     torch.cuda.synchronize()
+    assert all(bool((t == 0).all()) for t in g2d)
     for v, (cam, o) in enumerate(zip(cams, outs)):
         g = {k: to_np(t) for k, t in o.items()}
         g["tiles_touched"] = g.pop("tiles")

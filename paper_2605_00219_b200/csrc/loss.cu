@@ -75,32 +75,43 @@ __global__ void __launch_bounds__(kLossThreads) ssim_fwd_kernel(int W, int H, co
     }
     __syncthreads();
     double ssum = 0.0;
-    for (int k = tid; k < kTH * kTW; k += kLossThreads) {  // vertical sums -> S and partials
-        const int i0 = k / kTW, j = k % kTW;
-        const int px = cx0 + j, py = cy0 + i0;
-        if (px >= Wv || py >= Hv) continue;
-        double mx = 0, my = 0, exx = 0, eyy = 0, exy = 0;
+    // vertical sums -> S and partials; two vertically adjacent centres per thread share 10 of the
+    // 12 rows they read (halves the 64-bit shared-memory traffic)
+    for (int k = tid; k < (kTH / 2) * kTW; k += kLossThreads) {
+        const int i0 = 2 * (k / kTW), j = k % kTW;
+        double st[2][5] = {};
 #pragma unroll
-        for (int i = 0; i < kWin; i++) {
-            const double g = w.g[i];
-            mx += g * hs[0][i0 + i][j];
-            my += g * hs[1][i0 + i][j];
-            exx += g * hs[2][i0 + i][j];
-            eyy += g * hs[3][i0 + i][j];
-            exy += g * hs[4][i0 + i][j];
+        for (int t = 0; t < kWin + 1; t++) {
+            double hv[5];
+#pragma unroll
+            for (int q = 0; q < 5; q++) hv[q] = hs[q][i0 + t][j];
+            if (t < kWin) {
+#pragma unroll
+                for (int q = 0; q < 5; q++) st[0][q] += w.g[t] * hv[q];
+            }
+            if (t > 0) {
+#pragma unroll
+                for (int q = 0; q < 5; q++) st[1][q] += w.g[t - 1] * hv[q];
+            }
         }
-        const double sx2 = exx - mx * mx, sy2 = eyy - my * my, sxy = exy - mx * my;
-        const double l1 = 2 * mx * my + kC1, l2 = mx * mx + my * my + kC1;
-        const double c1 = 2 * sxy + kC2, c2 = sx2 + sy2 + kC2;
-        const double inv = 1.0 / (l2 * c2);  // the one fp64 division: 1/l2 = c2 inv, 1/c2 = l2 inv
-        const double S = l1 * c1 * inv;
-        const double dB = -S * (l2 * inv), dC = 2.0 * l1 * inv;
-        const double dA = 2.0 * my * c1 * inv - 2.0 * mx * S * (c2 * inv) - 2.0 * mx * dB - my * dC;
-        const size_t o = ((size_t)c * Hv + py) * Wv + px;
-        A[o] = dA;
-        B[o] = dB;
-        Cm[o] = dC;
-        ssum += S;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int px = cx0 + j, py = cy0 + i0 + h;
+            if (px >= Wv || py >= Hv) continue;
+            const double mx = st[h][0], my = st[h][1], exx = st[h][2], eyy = st[h][3], exy = st[h][4];
+            const double sx2 = exx - mx * mx, sy2 = eyy - my * my, sxy = exy - mx * my;
+            const double l1 = 2 * mx * my + kC1, l2 = mx * mx + my * my + kC1;
+            const double c1 = 2 * sxy + kC2, c2 = sx2 + sy2 + kC2;
+            const double inv = 1.0 / (l2 * c2);  // the one fp64 division: 1/l2 = c2 inv, 1/c2 = l2 inv
+            const double S = l1 * c1 * inv;
+            const double dB = -S * (l2 * inv), dC = 2.0 * l1 * inv;
+            const double dA = 2.0 * my * c1 * inv - 2.0 * mx * S * (c2 * inv) - 2.0 * mx * dB - my * dC;
+            const size_t o = ((size_t)c * Hv + py) * Wv + px;
+            A[o] = dA;
+            B[o] = dB;
+            Cm[o] = dC;
+            ssum += S;
+        }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) ssum += __shfl_xor_sync(VKS_FULL_MASK, ssum, o);
@@ -144,41 +155,58 @@ __global__ void __launch_bounds__(kLossThreads) ssim_bwd_kernel(int W, int H, fl
                 sm[2][r][s] = in ? Cm[o] : 0.0;
             }
             __syncthreads();
-            for (int k = tid; k < kIH * kTW; k += kLossThreads) {  // horizontal transposed sums
-                const int r = k / kTW, j = k % kTW;
-                double a = 0, b = 0, cc = 0;
+            for (int k = tid; k < kIH * (kTW / 2); k += kLossThreads) {  // horizontal transposed sums
+                const int r = k / (kTW / 2), j0 = 2 * (k % (kTW / 2));   // two adjacent columns
+                double o0[3] = {}, o1[3] = {};
 #pragma unroll
-                for (int i = 0; i < kWin; i++) {  // centre column (j + 10 - i) in tile coordinates
-                    const double g = w.g[i];
-                    a += g * sm[0][r][j + 2 * kR - i];
-                    b += g * sm[1][r][j + 2 * kR - i];
-                    cc += g * sm[2][r][j + 2 * kR - i];
+                for (int t = 0; t < kWin + 1; t++) {  // centre columns j0 .. j0 + 11 in tile coordinates
+                    const double v0 = sm[0][r][j0 + t], v1 = sm[1][r][j0 + t], v2 = sm[2][r][j0 + t];
+                    if (t < kWin) {
+                        const double g = w.g[2 * kR - t];
+                        o0[0] += g * v0; o0[1] += g * v1; o0[2] += g * v2;
+                    }
+                    if (t > 0) {
+                        const double g = w.g[2 * kR + 1 - t];
+                        o1[0] += g * v0; o1[1] += g * v1; o1[2] += g * v2;
+                    }
                 }
-                hs[0][r][j] = a; hs[1][r][j] = b; hs[2][r][j] = cc;
+#pragma unroll
+                for (int q = 0; q < 3; q++) {
+                    hs[q][r][j0] = o0[q];
+                    hs[q][r][j0 + 1] = o1[q];
+                }
             }
             __syncthreads();
         }
-        for (int k = tid; k < kTH * kTW; k += kLossThreads) {
-            const int i0 = k / kTW, j = k % kTW;
-            const int qx = qx0 + j, qy = qy0 + i0;
-            if (qx >= W || qy >= H) continue;
-            const size_t o = ((size_t)qy * W + qx) * 3 + c;
-            const double x = __ldg(render + o), y = __ldg(target + o);
-            const double d = x - y;
-            l1 += fabs(d);
-            double g = (1.0 - (double)lambda) * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_n;
+        for (int k = tid; k < (kTH / 2) * kTW; k += kLossThreads) {  // two vertically adjacent pixels
+            const int i0 = 2 * (k / kTW), j = k % kTW;
+            double acc[2][3] = {};
             if (ssim) {
-                double a = 0, b = 0, cc = 0;
 #pragma unroll
-                for (int i = 0; i < kWin; i++) {
-                    const double gw = w.g[i];
-                    a += gw * hs[0][i0 + 2 * kR - i][j];
-                    b += gw * hs[1][i0 + 2 * kR - i][j];
-                    cc += gw * hs[2][i0 + 2 * kR - i][j];
+                for (int t = 0; t < kWin + 1; t++) {  // centre rows i0 .. i0 + 11 in tile coordinates
+                    const double v0 = hs[0][i0 + t][j], v1 = hs[1][i0 + t][j], v2 = hs[2][i0 + t][j];
+                    if (t < kWin) {
+                        const double g = w.g[2 * kR - t];
+                        acc[0][0] += g * v0; acc[0][1] += g * v1; acc[0][2] += g * v2;
+                    }
+                    if (t > 0) {
+                        const double g = w.g[2 * kR + 1 - t];
+                        acc[1][0] += g * v0; acc[1][1] += g * v1; acc[1][2] += g * v2;
+                    }
                 }
-                g += k_ssim * (a + 2.0 * b * x + cc * y);
             }
-            dL[o] = (float)g;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int qx = qx0 + j, qy = qy0 + i0 + h;
+                if (qx >= W || qy >= H) continue;
+                const size_t o = ((size_t)qy * W + qx) * 3 + c;
+                const double x = __ldg(render + o), y = __ldg(target + o);
+                const double d = x - y;
+                l1 += fabs(d);
+                double g = (1.0 - (double)lambda) * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_n;
+                if (ssim) g += k_ssim * (acc[h][0] + 2.0 * acc[h][1] * x + acc[h][2] * y);
+                dL[o] = (float)g;
+            }
         }
     }
 #pragma unroll

@@ -40,8 +40,6 @@ def parse():
     ap.add_argument("--config", default="bicycle")
     ap.add_argument("--views-per-rank", type=int, default=8, help="views per rank per step (the batch)")
     ap.add_argument("--streams", type=int, default=3, help="views in flight per rank")
-    ap.add_argument("--prio", type=int, default=0,
-                    help="binning on high-priority streams (measured 620 vs 636 views/s without: off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows-every", type=int, default=8, help="oracle raster sample: every k-th tile row")
@@ -185,9 +183,6 @@ def run_ours(args):
         r._alloc_capacity(int(r.capacity * 1.1))
     main = torch.cuda.current_stream()
     streams = [torch.cuda.Stream() for _ in range(S)]
-    # binning on higher-priority streams: its chain of short, latency-bound kernels gets SMs as
-    # soon as blocks of another view's raster kernels retire
-    bstreams = [torch.cuda.Stream(priority=-1) for _ in range(S)] if args.prio else streams
     cfg_ow = dict(cfg, flags=P.FLAG_GRAD_OVERWRITE)
     # stage boundaries (CUDA events on the launching stream); the 2D-gradient accumulators that
     # raster_bwd adds into are zeroed by the batched projection forward (g2d_zero)
@@ -235,14 +230,8 @@ def run_ours(args):
             if copies is not None and loss_out is None:
                 st.wait_event(slot["img_free"])              # the previous image has left rend.image
             if ev is not None: ev[1].record(st)
-            bst = bstreams[streams.index(st)] if st in streams else st
-            if bst is not st:
-                bst.wait_stream(st)
-            with torch.cuda.stream(bst):
-                m = P.vks_bin_sort(cam, vb["means2d"], vb["radii"], vb["depths"], vb["tiles"], rend.offsets, None,
-                                   rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
-            if bst is not st:
-                st.wait_stream(bst)
+            m = P.vks_bin_sort(cam, vb["means2d"], vb["radii"], vb["depths"], vb["tiles"], rend.offsets, None,
+                               rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
             rend.num_isects = m
             if ev is not None: ev[2].record(st)
             P.vks_raster_fwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],

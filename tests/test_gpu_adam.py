@@ -103,3 +103,18 @@ def test_adam_zero_gradients_and_spec_example():
     # the same (1 - beta) back out, so the update is exactly the worked example's
     assert np.all(Mg["means"] == np.float32(1) - np.float32(0.9))
     assert np.all(Vg["means"] == np.float32(1) - np.float32(0.999))
+
+
+def test_adam_late_step():
+    """t = 10^4: the bias corrections are ~1 (1 - b1^t underflows to 1); same bounds."""
+    n, K, step = 3001, 16, 10000
+    p, g, m, v = _state(n, K, seed=99)
+    Pg, Mg, Vg = _gpu_step(p, g, m, v, LR, step)
+    Po, Mo, Vo = oracle.adam_step(p, g, m, v, LR32, beta1=B1, beta2=B2, eps=EPS, step=step)
+    for k in oracle.ADAM_GROUPS:
+        if k == "quats":
+            assert np.all(np.abs(Pg[k].astype(np.float64) - Po[k]) <= 1e-6)
+            continue
+        d = np.abs(Pg[k].astype(np.float64) - Po[k])
+        upd = np.abs(p[k].astype(np.float64) - Po[k])
+        assert np.all(d <= 2.0 ** -23 * np.abs(Po[k]) + 4e-6 * np.maximum(upd, 1e-3 * LR32["means"])), k

@@ -89,3 +89,24 @@ def test_densify_capacity_protocol():
     cap = int(1.5 * (n + 10)) + n
     big = [torch.empty((cap,) + tuple(t.shape[1:]), device="cuda") for t in prm]
     assert P.vks_densify(prm, accum, denom, big, ws, 0.5, 1e9) == 2 * n
+
+
+def test_densify_prunes_everything_and_keeps_everything():
+    """Every Gaussian below the prune opacity -> n' = 0; none above the gradient threshold and none
+    prunable -> the rows come back unchanged."""
+    import torch
+    import paper_2605_00219_b200 as P
+    n = 3001
+    s = synth.make_scene(n, "outdoor", 6)
+    G = oracle.ADAM_GROUPS
+    ws = torch.empty(P.vks_densify_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    out = None
+    for logit, expect in ((-8.0, 0), (2.0, n)):
+        s["opacity_logits"][:] = logit
+        prm = [torch.from_numpy(np.ascontiguousarray(s[k])).cuda() for k in G]
+        out = [torch.empty((2 * n,) + tuple(t.shape[1:]), device="cuda") for t in prm]
+        acc, den = torch.zeros(n, device="cuda"), torch.ones(n, device="cuda")
+        assert P.vks_densify(prm, acc, den, out, ws, 1e-3, 0.01) == expect
+        if expect:
+            for a, b in zip(prm, out):
+                assert torch.equal(a, b[:n])

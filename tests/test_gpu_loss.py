@@ -62,3 +62,14 @@ def test_identical_images_zero_gradient():
     _, t = _pair(40, 30, 2)
     loss, g = _gpu(t, t, 0.2)
     assert abs(loss) <= 1e-7 and np.abs(g).max() * 3 * 40 * 30 <= 1e-9
+
+
+@pytest.mark.parametrize("H,W,lam", [(11, 40, 1.0), (40, 11, 0.5), (33, 70, 1.0)])
+def test_loss_grad_pure_ssim_and_thin_images(H, W, lam):
+    """lambda = 1 (pure D-SSIM) and images one window thick in one dimension."""
+    r, t = _pair(H, W, seed=7 * H + W)
+    loss, g = _gpu(r, t, lam)
+    lo, go, _ = oracle.loss_grad(r, t, lam)
+    assert loss == pytest.approx(lo, rel=1e-6, abs=1e-9)
+    G, Go = g.astype(np.float64) * 3 * H * W, go * 3 * H * W
+    assert np.all(np.abs(G - Go) <= 1e-6 * np.abs(Go) + 1e-9)

@@ -71,3 +71,24 @@ def test_noise_matches_oracle():
     tol = 2 * np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64) + 1e-6 * disp
     assert np.all(np.abs(got - ref) <= tol), int((np.abs(got - ref) > tol).sum())
     assert (disp > 0).sum() > n // 4  # the dead half moved
+
+
+def test_relocate_degenerate_budgets():
+    """Every Gaussian dead (no alive weight): nothing moves and every target is -1; nobody dead:
+    the parameters are untouched."""
+    import torch
+    import paper_2605_00219_b200 as P
+    for logit in (-9.0, 3.0):
+        s = _scene(4097, 5, dead_frac=0.0)
+        s["opacity_logits"][:] = logit
+        prm = P.GaussianParams.from_host(s)
+        before = [t.clone() for t in (prm.means, prm.log_scales, prm.quats, prm.opacity_logits, prm.sh)]
+        tg = torch.empty(4097, dtype=torch.int64, device="cuda")
+        nd = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ws = torch.empty(P.vks_mcmc_workspace_bytes(4097), dtype=torch.uint8, device="cuda")
+        P.vks_mcmc_relocate(prm, ws, dead_opacity=0.005, seed=1, targets=tg, n_dead=nd)
+        torch.cuda.synchronize()
+        assert int(nd.item()) == (4097 if logit < 0 else 0)
+        assert bool((tg == -1).all())
+        for a, b in zip(before, (prm.means, prm.log_scales, prm.quats, prm.opacity_logits, prm.sh)):
+            assert torch.equal(a, b)

@@ -748,11 +748,14 @@ static void proj_bwd_one(const vko_config* cfg, const vko_camera* cam, int32_t f
     for (int k = 0; k < 3; k++) dmu[k] += R[k] * dt[0] + R[3 + k] * dt[1] + R[6 + k] * dt[2];
 }
 
-/* Running-error "mass" of the projection backward: the same chain as proj_bwd_one, evaluated
- * with every coefficient replaced by its absolute value and every sum by a sum of absolute terms,
- * in the evaluation structure of the fp32 CUDA kernel (DESIGN.md §7 P5).  Inputs are non-negative
- * masses of the 2D gradients; outputs bound sum|terms| of each parameter gradient, so an fp32
- * evaluation of the chain is accurate to a few hundred ulps of this mass. */
+/* "Mass" of the projection backward (sum |terms| per gradient entry): the
+ * chain of SURVEY §8c.6 (proj_bwd_one above), stage by stage, with every local coefficient replaced
+ * by its absolute value, i.e. |J_stage|^T applied to non-negative input masses; the two
+ * normalisations are written as two terms each (dq = (dq^ - q^<q^,dq^>)/|q|, the same for the SH
+ * direction), so they contribute (|I| + |q^||q^|^T)/|q|.  Inputs: masses of the 2D gradients.
+ * Outputs bound |gradient| (triangle inequality) and scale the rounding error of any fp32
+ * evaluation of the chain.  Pinned in tests/test_oracle_mass.py against an independent rebuild of
+ * the chain from autograd stage Jacobians (equal to 1e-9) and the bound property. */
 static void proj_bwd_mass_one(const vko_config* cfg, const vko_camera* cam, int32_t flags,
                               const double mu[3], const double ls[3], const double q[4], double o,
                               const double* sh, const double mdm2[2], const double mdcon[3],

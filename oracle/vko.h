@@ -132,9 +132,9 @@ void vko_project_bwd(const vko_config* cfg, const vko_camera* cam, int64_t n,
                      double* dmeans, double* dlog_scales, double* dquats,
                      double* dopacity_logits, double* dsh, int nthreads);
 
-/* Running-error mass of the projection backward (non-negative inputs = masses of the 2D
- * gradients; outputs = sum of |terms| of each parameter gradient in the CUDA kernel's evaluation
- * structure).  Used to classify condition-limited elements (DESIGN.md §7 P5). */
+/* Mass of the projection backward (non-negative inputs = masses of the 2D gradients; outputs =
+ * sum of |terms| of each parameter gradient along the SURVEY §8c.6 chain, stage by stage).  Used
+ * to classify condition-limited elements (DESIGN.md §7 P5); pinned by tests/test_oracle_mass.py. */
 void vko_project_bwd_mass(const vko_config* cfg, const vko_camera* cam, int64_t n,
                           const float* means, const float* log_scales, const float* quats,
                           const float* opacity_logits, const float* sh,

@@ -18,3 +18,16 @@ def oracle_lib():
     import oracle
     oracle.build()
     return oracle
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Per-field gradient parity counts (fail / condition-limited / worst ratio to the 1e-3 rule)
+    of the -m gpu parity tests that ran."""
+    try:
+        from gpu_helpers import PARITY_LOG
+    except ImportError:
+        return
+    if PARITY_LOG:
+        terminalreporter.write_sep("-", "gradient parity (SURVEY 8c.9 P4/P5): per field")
+        for line in PARITY_LOG:
+            terminalreporter.write_line(line)

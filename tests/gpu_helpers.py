@@ -65,6 +65,16 @@ def last_id_from_ncontrib(g, cam):
     return out
 
 
+# per-field gradient parity counts of this session, printed by tests/conftest.py at the end of the
+# run (so the driver's log shows fail / condition-limited / worst for every checked field)
+PARITY_LOG: list[str] = []
+
+# at most this fraction of a field's elements may pass through the condition-limited clause
+# (reported separately, never silently passed); the mass it uses is pinned in
+# tests/test_oracle_mass.py
+CL_FRACTION = 1e-5
+
+
 def grad_rule(g, ref, mass=None, rel=1e-3, abs_floor=1e-6, cond=1e-5):
     """Per-element rule: |g - ref| <= max(rel |ref|, abs_floor).  Elements that fail
     only because of cancellation (|g - ref| <= cond * mass) are counted as condition-limited."""
@@ -80,6 +90,16 @@ def grad_rule(g, ref, mass=None, rel=1e-3, abs_floor=1e-6, cond=1e-5):
     return dict(n=int(g.size), fail=int(bad.sum()), condition_limited=int(cl.sum()),
                 worst=float((err / np.maximum(rel * np.abs(ref), abs_floor)).max()) if g.size else 0.0,
                 bad_idx=np.nonzero(bad)[0][:10])
+
+
+def check_rule(tag, field, rule, cl_fraction=CL_FRACTION):
+    """Gate of one field: no failing element, and at most floor(cl_fraction * n) condition-limited
+    ones.  Logs the counts for the session summary either way."""
+    limit = int(cl_fraction * rule["n"])
+    PARITY_LOG.append(f"{tag:>24s} {field:<26s} n={rule['n']:>10d} fail={rule['fail']:>3d} "
+                      f"cond_limited={rule['condition_limited']:>3d} (limit {limit}) worst={rule['worst']:.3g}")
+    assert rule["fail"] == 0, (tag, field, {k: v for k, v in rule.items()})
+    assert rule["condition_limited"] <= limit, (tag, field, "too many condition-limited elements", rule)
 
 
 def sampled_rows(cam, every=8):

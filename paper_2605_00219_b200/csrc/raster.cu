@@ -319,7 +319,89 @@ __device__ __forceinline__ float warp_reduce_8plus1(const float v[8], float& e, 
     return c;
 }
 
-template <int PPT, int CULL>
+// Chunked cross-lane reduction of the backward (RED = 1): a warp writes each contributing entry's
+// nine per-lane partial sums (two pixels already summed in registers) to its own shared-memory
+// slot as three 16-byte words, and every kChunk entries (or at the end of a staged batch) reduces
+// the chunk at once: lane (j, s) = (lane / 8, lane % 8) sums entry j's partials of lanes s, s + 8,
+// s + 16, s + 24 (conflict-free 128-bit loads: 12-word lane slots), then an 8-lane transposed
+// butterfly (7 shuffles) leaves term s of entry j in lane s, which forms that term's output with
+// the entry's conic and issues one atomic (lane s = 0 also the opacity term).  The per-entry cost
+// is 3 shared stores plus a quarter of the chunk reduction, instead of a 32-lane butterfly of the
+// nine sums (19 shuffles, their selects and adds) and a per-entry epilogue.
+constexpr int kChunk = 4;
+struct WarpRed {
+    float4 p[kChunk][32][3];  // [slot][lane][m_x m_y m_xx m_xy | m_yy c0 c1 c2 | e - - -]
+};
+
+// the chunk's outputs: slot j < cnt holds stage entry (slots >> 5j) & 31
+__device__ __forceinline__ void flush_chunk(const WarpRed& red, const WarpStage& s, int cnt, uint32_t slots,
+                                            unsigned lane, float* __restrict__ dmeans2d, float* __restrict__ dconics,
+                                            float* __restrict__ dcolors, float* __restrict__ dopac) {
+    __syncwarp();
+    const int j = (int)(lane >> 3), sl = (int)(lane & 7);
+    float4 a0 = red.p[j][sl][0], a1 = red.p[j][sl][1];
+    float e = red.p[j][sl][2].x;
+#pragma unroll
+    for (int r = 1; r < 4; r++) {
+        const float4 b0 = red.p[j][sl + 8 * r][0], b1 = red.p[j][sl + 8 * r][1];
+        a0.x += b0.x; a0.y += b0.y; a0.z += b0.z; a0.w += b0.w;
+        a1.x += b1.x; a1.y += b1.y; a1.z += b1.z; a1.w += b1.w;
+        e += red.p[j][sl + 8 * r][2].x;
+    }
+    // 8-lane transposed butterfly: lane s ends with term s (bits of s select the kept halves)
+    float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    float h4[4], h2[2];
+    bool hi = sl & 4;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const float send = hi ? v[i] : v[i + 4];
+        const float keep = hi ? v[i + 4] : v[i];
+        h4[i] = keep + __shfl_xor_sync(VKS_FULL_MASK, send, 4);
+    }
+    hi = sl & 2;
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const float send = hi ? h4[i] : h4[i + 2];
+        const float keep = hi ? h4[i + 2] : h4[i];
+        h2[i] = keep + __shfl_xor_sync(VKS_FULL_MASK, send, 2);
+    }
+    hi = sl & 1;
+    float r;
+    {
+        const float send = hi ? h2[0] : h2[1];
+        const float keep = hi ? h2[1] : h2[0];
+        r = keep + __shfl_xor_sync(VKS_FULL_MASK, send, 1);
+    }
+    e += __shfl_xor_sync(VKS_FULL_MASK, e, 4);
+    e += __shfl_xor_sync(VKS_FULL_MASK, e, 2);
+    e += __shfl_xor_sync(VKS_FULL_MASK, e, 1);
+    const float other = __shfl_xor_sync(VKS_FULL_MASK, r, 1);  // lanes s = 0 <-> 1: the two first moments
+    if (j < cnt) {
+        const int jj = (int)((slots >> (5 * j)) & 31u);
+        const float4 A = s.a[jj], B = s.b[jj];
+        const uint32_t id = __float_as_uint(s.c[jj].y);
+        // dmean = -rho (a m_x + b m_y, b m_x + c m_y), dconic = -rho (m_xx / 2, m_xy, m_yy / 2)
+        const float nrho = -B.y;
+        float out;
+        float* dst;
+        if (sl < 2) {
+            const float diag = sl == 0 ? 2.0f * A.z : 2.0f * B.x;
+            out = nrho * fmaf(diag, r, A.w * other);
+            dst = dmeans2d + 2 * (size_t)id + sl;
+        } else if (sl < 5) {
+            out = nrho * (sl == 3 ? r : 0.5f * r);
+            dst = dconics + 3 * (size_t)id + (sl - 2);
+        } else {
+            out = r;
+            dst = dcolors + 3 * (size_t)id + (sl - 5);
+        }
+        atomicAdd(dst, out);
+        if (sl == 0) atomicAdd(dopac + id, e);
+    }
+    __syncwarp();
+}
+
+template <int PPT, int CULL, int RED>
 __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
@@ -335,10 +417,12 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                                                                  float* __restrict__ dmeans2d, float* __restrict__ dconics,
                                                                  float* __restrict__ dcolors, float* __restrict__ dopac) {
     __shared__ WarpStage stage[8 / PPT];
+    __shared__ WarpRed redbuf[RED ? 8 / PPT : 1];
     const int TX = tiles_x(cam);
     const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
     const unsigned lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
+    WarpRed& red = redbuf[RED ? threadIdx.x >> 5 : 0];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
@@ -365,8 +449,8 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
         lmax = max(lmax, last[k]);
     }
     const int wmax = __reduce_max_sync(VKS_FULL_MASK, lmax);  // positions >= wmax: nobody composited
-    // per-lane destination of gradient term k after the butterfly: lane 4k (k < 8) owns term k,
-    // lane 1 the opacity term; dst(g) = base + g * stride
+    // RED = 0: per-lane destination of gradient term k after the 32-lane butterfly: lane 4k (k < 8)
+    // owns term k, lane 1 the opacity term; dst(g) = base + g * stride
     const int myterm = (lane & 3) == 0 ? (int)(lane >> 2) : (lane == 1 ? 8 : -1);
     float* tbase = nullptr;
     int tstride = 0;
@@ -403,6 +487,8 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             if (p >= 0) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
             if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
         }
+        int cnt = 0;          // RED = 1: entries in the open chunk
+        uint32_t slots = 0;   // and their stage indices (5 bits each)
         while (live) {  // back to front over the entries whose support box meets the patch
             const int j = 31 - __clz(live);
             live &= ~(1u << j);
@@ -410,18 +496,26 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             const float4 A = s.a[j], B = s.b[j];
             const float4 Cc = s.c[j];
             const float c0 = B.z, c1 = B.w, c2 = Cc.x;
+            // evaluate first: an entry no pixel of the warp composited leaves every T, P and
+            // accumulator unchanged, so the warp skips it
+            float dx[PPT], dy[PPT], G[PPT], rG[PPT], alpha[PPT];
+            bool okk[PPT];
+            bool contrib = false;
+#pragma unroll
+            for (int k = 0; k < PPT; k++) {
+                okk[k] = eval_alpha(A, B, px, py[k], dx[k], dy[k], G[k], rG[k], alpha[k]) && pos < last[k];
+                contrib = contrib || okk[k];
+            }
+            if (RED && !__any_sync(VKS_FULL_MASK, contrib)) continue;
             // v[0..4]: moments sum(g dx), sum(g dy), sum(g dx^2), sum(g dx dy), sum(g dy^2) with
             // g = G dalpha (dL/dsigma = -rho g); v[5..7]: colour; e = sum(g) (dL/drho)
             float v[8], e = 0.0f;
-            bool contrib = false;
 #pragma unroll
             for (int k = 0; k < PPT; k++) {
                 // branch-free: an entry the pixel did not composite replays with alpha = 0, which
                 // leaves T, P and every accumulator bit-identical (T * 1, 0 * x + P, + 0)
-                float dx, dy, G, rG, alpha;
-                const bool ok = eval_alpha(A, B, px, py[k], dx, dy, G, rG, alpha) && pos < last[k];
-                contrib = contrib || ok;
-                const float a = ok ? alpha : 0.0f;
+                const bool ok = okk[k];
+                const float a = ok ? alpha[k] : 0.0f;
                 const float om = 1.0f - a;
                 T[k] = T[k] * rcp_ftz(om);  // om in [0.01, 1]
                 const float aT = a * T[k];
@@ -429,14 +523,24 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 const float dalpha = T[k] * (cw - P[k]);
                 P[k] = a * cw + om * P[k];
                 // no gradient where the pixel skipped the entry or alpha was clamped
-                const float g = (!ok || rG > 0.99f) ? 0.0f : G * dalpha;
-                const float gx = g * dx, gy = g * dy;
-                const float t[8] = {gx, gy, gx * dx, gx * dy, gy * dy, aT * w0[k], aT * w1[k], aT * w2[k]};
+                const float g = (!ok || rG[k] > 0.99f) ? 0.0f : G[k] * dalpha;
+                const float gx = g * dx[k], gy = g * dy[k];
+                const float t[8] = {gx, gy, gx * dx[k], gx * dy[k], gy * dy[k], aT * w0[k], aT * w1[k], aT * w2[k]};
 #pragma unroll
                 for (int q = 0; q < 8; q++) v[q] = k == 0 ? t[q] : v[q] + t[q];
                 e = k == 0 ? g : e + g;
             }
-            if (__any_sync(VKS_FULL_MASK, contrib)) {
+            if constexpr (RED) {
+                red.p[cnt][lane][0] = make_float4(v[0], v[1], v[2], v[3]);
+                red.p[cnt][lane][1] = make_float4(v[4], v[5], v[6], v[7]);
+                red.p[cnt][lane][2].x = e;
+                slots |= (uint32_t)j << (5 * cnt);
+                if (++cnt == kChunk) {
+                    flush_chunk(red, s, cnt, slots, lane, dmeans2d, dconics, dcolors, dopac);
+                    cnt = 0;
+                    slots = 0;
+                }
+            } else if (__any_sync(VKS_FULL_MASK, contrib)) {
                 const float r = warp_reduce_8plus1(v, e, lane);
                 const float other = __shfl_xor_sync(VKS_FULL_MASK, r, 4);  // lanes 0 <-> 4: the two first moments
                 // dmean = -rho (a m_x + b m_y, b m_x + c m_y), dconic = -rho (m_xx / 2, m_xy, m_yy / 2),
@@ -447,6 +551,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 if (myterm >= 0) atomicAdd(tbase + (size_t)__float_as_uint(Cc.y) * tstride, out);
             }
         }
+        if (RED && cnt > 0) flush_chunk(red, s, cnt, slots, lane, dmeans2d, dconics, dcolors, dopac);
     }
 }
 
@@ -462,14 +567,14 @@ int launch_fwd(const vks_config& cfg, const vks_camera& cam, const float* means2
     return LaunchCheck::check();
 }
 
-template <int PPT, int CULL>
+template <int PPT, int CULL, int RED>
 int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
                const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                float* dopacities, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_bwd_kernel<PPT, CULL><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
+    raster_bwd_kernel<PPT, CULL, RED><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
         reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage,
         dmeans2d, dconics, dcolors, dopacities);
@@ -514,11 +619,23 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
                  const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
                  const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                  float* dopacities, cudaStream_t st) {
-    switch (cull) {
-        case kCullNone: return launch_bwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-        case kCullBox: return launch_bwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-        default: return launch_bwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    // cross-lane reduction: chunked through shared memory (1, default) or a 32-lane butterfly per entry (0)
+    const int red = env_choice("VKS_RASTER_BWD_RED", 1, 0, 1);
+#define VKS_BWD_ARGS cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, \
+                     n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st
+    if (red) {
+        switch (cull) {
+            case kCullNone: return launch_bwd<PPT, kCullNone, 1>(VKS_BWD_ARGS);
+            case kCullBox: return launch_bwd<PPT, kCullBox, 1>(VKS_BWD_ARGS);
+            default: return launch_bwd<PPT, kCullEllipse, 1>(VKS_BWD_ARGS);
+        }
     }
+    switch (cull) {
+        case kCullNone: return launch_bwd<PPT, kCullNone, 0>(VKS_BWD_ARGS);
+        case kCullBox: return launch_bwd<PPT, kCullBox, 0>(VKS_BWD_ARGS);
+        default: return launch_bwd<PPT, kCullEllipse, 0>(VKS_BWD_ARGS);
+    }
+#undef VKS_BWD_ARGS
 }
 
 }  // namespace

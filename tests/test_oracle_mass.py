@@ -25,7 +25,7 @@ import torch
 
 import synth
 
-torch.set_default_dtype(torch.float64)
+F64 = torch.float64  # every tensor here is fp64 (explicitly: the default dtype is left alone)
 
 GRADS = ("dmeans", "dlog_scales", "dquats", "dopacity_logits", "dsh")
 IN2D = ("dmeans2d", "dconics", "dcolors", "dopacities")
@@ -42,7 +42,7 @@ def sh_basis(d):
     x, y, z = d[0], d[1], d[2]
     xx, yy, zz = x * x, y * y, z * z
     return torch.stack([
-        torch.as_tensor(C0) + 0 * x,
+        0 * x + C0,
         -C1 * y, C1 * z, -C1 * x,
         C2[0] * x * y, C2[1] * y * z, C2[2] * (2 * zz - xx - yy), C2[3] * x * z, C2[4] * (xx - yy),
         C3[0] * y * (3 * xx - yy), C3[1] * x * y * z, C3[2] * y * (4 * zz - xx - yy),
@@ -77,7 +77,7 @@ def chain_mass(cfg, cam, mu, ls, q, o, sh, flags, m2d):
     cly = bool(flags & (oracle.F_FOVY_HI | oracle.F_FOVY_LO))
     Lx = ((W - cx) / fx + 0.3 * (0.5 * W / fx)) if flags & oracle.F_FOVX_HI else -(cx / fx + 0.3 * (0.5 * W / fx))
     Ly = ((H - cy) / fy + 0.3 * (0.5 * H / fy)) if flags & oracle.F_FOVY_HI else -(cy / fy + 0.3 * (0.5 * H / fy))
-    col_on = torch.tensor([0.0 if flags & (oracle.F_CLAMP_R << ch) else 1.0 for ch in range(3)])
+    col_on = torch.tensor([0.0 if flags & (oracle.F_CLAMP_R << ch) else 1.0 for ch in range(3)], dtype=F64)
 
     # ---- the forward stages, each a function of the previous stage's outputs
     st_t = lambda mu_: R @ mu_ + tc                                                     # step 1
@@ -129,7 +129,7 @@ def chain_mass(cfg, cam, mu, ls, q, o, sh, flags, m2d):
     dn = torch.linalg.norm(d)
     dh = d / dn
     Y = sh_basis(dh)
-    rho = 1.0 / (1.0 + torch.exp(-torch.as_tensor(float(o))))
+    rho = 1.0 / (1.0 + torch.exp(-torch.as_tensor(float(o), dtype=F64)))
 
     # ---- reverse accumulation with |local Jacobian|^T
     (Jc,) = jac(st_conic, abc)

@@ -417,12 +417,12 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                                                                  float* __restrict__ dmeans2d, float* __restrict__ dconics,
                                                                  float* __restrict__ dcolors, float* __restrict__ dopac) {
     __shared__ WarpStage stage[8 / PPT];
-    __shared__ WarpRed redbuf[RED ? 8 / PPT : 1];
+    extern __shared__ float4 dyn_smem[];  // RED = 1: one WarpRed per warp (dynamic: 8 warps need 48 KB)
     const int TX = tiles_x(cam);
     const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
     const unsigned lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
-    WarpRed& red = redbuf[RED ? threadIdx.x >> 5 : 0];
+    WarpRed& red = reinterpret_cast<WarpRed*>(dyn_smem)[RED ? threadIdx.x >> 5 : 0];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
@@ -574,7 +574,13 @@ int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2
                const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                float* dopacities, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_bwd_kernel<PPT, CULL, RED><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
+    const size_t dyn = RED ? sizeof(WarpRed) * (8 / PPT) : 0;
+    if (dyn > 48 * 1024) {  // per call: the attribute belongs to the current device
+        cudaError_t e = cudaFuncSetAttribute(raster_bwd_kernel<PPT, CULL, RED>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return cuda_fail(e, "raster_bwd smem attribute");
+    }
+    raster_bwd_kernel<PPT, CULL, RED><<<n_tiles, 32 * 8 / PPT, dyn, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
         reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage,
         dmeans2d, dconics, dcolors, dopacities);

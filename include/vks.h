@@ -80,10 +80,11 @@ typedef struct {
 enum {
     VKS_OK = 0,
     VKS_ERR_INVALID_ARG = 1,
-    VKS_ERR_CAPACITY = 2,   /* vks_bin_sort: M > capacity (or M >= 2^30); *num_isects holds M */
+    VKS_ERR_CAPACITY = 2,   /* vks_bin_sort: M > capacity; *num_isects holds M (regrow and re-call) */
     VKS_ERR_WORKSPACE = 3,  /* workspace too small */
     VKS_ERR_CUDA = 4,       /* launch / runtime failure (incl. no CUDA device) */
-    VKS_ERR_UNSUPPORTED = 5
+    VKS_ERR_UNSUPPORTED = 5, /* configuration outside the library's limits (e.g. M >= 2^30 keys) */
+    VKS_ERR_NONFINITE = 6    /* VKS_FLAG_VALIDATE: a non-finite input (S:119 NonFiniteParameter) */
 };
 
 const char* vks_status_string(int status);
@@ -137,10 +138,12 @@ size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles
  *                           the rasterizer (heaviest tiles first); results never depend on it
  *   keys_unsorted / vals_unsorted (nullable, debug; [capacity] like keys/vals): the pre-sort pairs.
  * Tile grids of >= 2^20 tiles return VKS_ERR_INVALID_ARG.
- * If M > capacity (or M >= 2^30) returns VKS_ERR_CAPACITY after writing
- * offsets and *num_isects, touching no other output; the call is idempotent, so the caller
- * regrows and calls again.  Synchronises `stream` once (to read M).
- * workspace: device memory of >= vks_bin_sort_workspace_bytes(n, capacity, n_tiles).
+ * If M > capacity returns VKS_ERR_CAPACITY after writing offsets and *num_isects, touching no
+ * other output; the call is idempotent, so the caller regrows and calls again.  M >= 2^30 is a
+ * hard limit of the sort (30-bit look-back counts): VKS_ERR_UNSUPPORTED, *num_isects = M, no
+ * capacity helps.  Synchronises `stream` once (to read M).
+ * workspace: device memory of >= vks_bin_sort_workspace_bytes(n, capacity, n_tiles), 256-byte
+ * aligned (else VKS_ERR_WORKSPACE).
  */
 int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
                  const float* depths, const int32_t* tiles_touched, uint32_t* offsets,

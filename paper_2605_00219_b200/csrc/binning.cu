@@ -35,6 +35,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "vks_common.cuh"
 
@@ -1131,13 +1132,10 @@ template <int DBITS, int MODE>
 int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift, u32 kbias, const PassBufs& pb,
                 const float* depths, u64* keys64, cudaStream_t s) {
     constexpr size_t sm = sizeof(SortSmem<1 << DBITS>);
-    static bool attr = false;
-    if (!attr) {
-        if (cudaError_t e = cudaFuncSetAttribute(scatter_kernel<DBITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)sm))
-            return cuda_fail(e, "scatter smem attribute");
-        attr = true;
-    }
+    // set on every call: the attribute belongs to the current device (a process may drive several)
+    if (cudaError_t e = cudaFuncSetAttribute(scatter_kernel<DBITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sm))
+        return cuda_fail(e, "scatter smem attribute");
     const u32 T = (u32)((n + kSortTile - 1) / kSortTile);
     if (!T) return VKS_OK;
     digit_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(kin, n, shift, kbias, T, pb.counts);
@@ -1167,13 +1165,21 @@ int launch_pass_bits(int dbits, const u32* kin, const u32* vin, u32* kout, u32* 
 #undef VKS_PASS
 }
 
+constexpr int kMaxDevices = 64;
+
+// SM count of the CURRENT device, cached per device id (relaxed atomics: every writer stores the
+// same value, so concurrent first calls are benign)
 int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+    static std::atomic<int> cache[kMaxDevices];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = (dev >= 0 && dev < kMaxDevices) ? cache[dev].load(std::memory_order_relaxed) : 0;
+    if (sms <= 0) {
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+            cudaGetLastError();
+            sms = 148;
+        }
+        if (dev >= 0 && dev < kMaxDevices) cache[dev].store(sms, std::memory_order_relaxed);
     }
     return sms;
 }
@@ -1183,13 +1189,9 @@ template <int DBITS, int MODE>
 int launch_keys_pass(const ExpandSrc& src, u32* kout, u32* vout, const PassBufs& pb, const float* depths, u64* keys64,
                      cudaStream_t s) {
     constexpr size_t sm = sizeof(SortSmem<1 << DBITS>);
-    static bool attr = false;
-    if (!attr) {
-        if (cudaError_t e = cudaFuncSetAttribute(keys_scatter_kernel<DBITS, MODE>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))
-            return cuda_fail(e, "keys_scatter smem attribute");
-        attr = true;
-    }
+    if (cudaError_t e = cudaFuncSetAttribute(keys_scatter_kernel<DBITS, MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))
+        return cuda_fail(e, "keys_scatter smem attribute");
     const u32 T = (src.M + kSortTile - 1) / kSortTile;
     if (!T) return VKS_OK;
     keys_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(src, 0, T, pb.counts);
@@ -1222,13 +1224,9 @@ int launch_rect_diff(int TX, int TY, u32 count, const u64* rc, int* diff, cudaSt
     if (cells <= kDiffSmemMax) {
         const size_t sm = sizeof(int) * (size_t)cells;
         if (sm > 48 * 1024) {
-            static bool attr = false;
-            if (!attr) {
-                if (cudaError_t e = cudaFuncSetAttribute(rect_diff_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)(sizeof(int) * kDiffSmemMax)))
-                    return cuda_fail(e, "rect_diff smem attribute");
-                attr = true;
-            }
+            if (cudaError_t e = cudaFuncSetAttribute(rect_diff_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)(sizeof(int) * kDiffSmemMax)))
+                return cuda_fail(e, "rect_diff smem attribute");
         }
         const unsigned blocks = std::min<u32>(want, (u32)sm_count() * 2);
         rect_diff_kernel<true><<<blocks, kDiffThreads, sm, s>>>(TX, TY, count, rc, diff);
@@ -1243,13 +1241,9 @@ int launch_tile_count(int TX, int TY, int* diff, u32* tile_offsets, u32* order, 
     const size_t cells_bytes = sizeof(int) * (size_t)(TX + 1) * (TY + 1);
     if (cells_bytes <= kTileCountSmemMax) {
         if (cells_bytes > 48 * 1024) {
-            static bool attr = false;
-            if (!attr) {
-                if (cudaError_t e = cudaFuncSetAttribute(tile_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)kTileCountSmemMax))
-                    return cuda_fail(e, "tile_count smem attribute");
-                attr = true;
-            }
+            if (cudaError_t e = cudaFuncSetAttribute(tile_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)kTileCountSmemMax))
+                return cuda_fail(e, "tile_count smem attribute");
         }
         tile_count_kernel<true><<<1, 1024, cells_bytes, s>>>(TX, TY, diff, tile_offsets, order);
     } else {
@@ -1302,6 +1296,8 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     // rect areas < 2^20 tiles
     if (TX > 65535 || TY > 65535 || (int64_t)TX * TY >= (1 << 20)) return VKS_ERR_INVALID_ARG;
     if (workspace_bytes < bin_sort_workspace_bytes(n, capacity, n_tiles)) return VKS_ERR_WORKSPACE;
+    // the scatters bulk-copy (cp.async.bulk) from workspace arrays: 256-byte aligned base required
+    if (reinterpret_cast<uintptr_t>(workspace) & 255) return VKS_ERR_WORKSPACE;
     Workspace w = carve(workspace, n, capacity, TX, TY);
     if (cudaError_t e_ = cudaMemsetAsync(w.zeroA, 0, w.zeroA_bytes, s)) return cuda_fail(e_, "memset workspace");
     auto pass_bufs = [&](int p) { return PassBufs{w.counts, w.offs, w.cnt_lb[p], w.ctr + kCtrPass + p}; };
@@ -1318,7 +1314,10 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     }
     const u64 M = tot[0], V = tot[1];
     *num_isects = (int64_t)M;
-    if ((int64_t)M > capacity || M >= (1ull << 30)) return VKS_ERR_CAPACITY;
+    // the look-back counters hold 30-bit counts: no capacity makes M >= 2^30 sortable, so that is
+    // a hard limit (not a regrow request)
+    if (M >= (1ull << 30)) return VKS_ERR_UNSUPPORTED;
+    if ((int64_t)M > capacity) return VKS_ERR_CAPACITY;
     if (M == 0) {
         if (cudaMemsetAsync(tile_offsets, 0, sizeof(u32) * (n_tiles + 1), s) != cudaSuccess) return VKS_ERR_CUDA;
         if (tile_order) {  // every list is empty: identity schedule

@@ -329,6 +329,7 @@ __device__ __forceinline__ float warp_reduce_8plus1(const float v[8], float& e, 
 // is 3 shared stores plus a quarter of the chunk reduction, instead of a 32-lane butterfly of the
 // nine sums (19 shuffles, their selects and adds) and a per-entry epilogue.
 constexpr int kChunk = 4;
+int kCarveout = 100;  // percent of the unified L1 / shared memory given to shared memory (VKS_RASTER_CARVEOUT)
 struct WarpRed {
     float4 p[kChunk][32][3];  // [slot][lane][m_x m_y m_xx m_xy | m_yy c0 c1 c2 | e - - -]
 };
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
     const unsigned lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
-    WarpRed& red = reinterpret_cast<WarpRed*>(dyn_smem)[RED ? threadIdx.x >> 5 : 0];
+    WarpRed& red = reinterpret_cast<WarpRed*>(dyn_smem)[RED == 1 ? threadIdx.x >> 5 : 0];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
@@ -506,6 +507,8 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 okk[k] = eval_alpha(A, B, px, py[k], dx[k], dy[k], G[k], rG[k], alpha[k]) && pos < last[k];
                 contrib = contrib || okk[k];
             }
+            // RED >= 1: an entry no pixel of the warp composited leaves every T, P and accumulator
+            // unchanged, so the warp skips it
             if (RED && !__any_sync(VKS_FULL_MASK, contrib)) continue;
             // v[0..4]: moments sum(g dx), sum(g dy), sum(g dx^2), sum(g dx dy), sum(g dy^2) with
             // g = G dalpha (dL/dsigma = -rho g); v[5..7]: colour; e = sum(g) (dL/drho)
@@ -520,8 +523,9 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 T[k] = T[k] * rcp_ftz(om);  // om in [0.01, 1]
                 const float aT = a * T[k];
                 const float cw = c0 * w0[k] + c1 * w1[k] + c2 * w2[k];
-                const float dalpha = T[k] * (cw - P[k]);
-                P[k] = a * cw + om * P[k];
+                const float d = cw - P[k];
+                const float dalpha = T[k] * d;
+                P[k] = RED ? fmaf(a, d, P[k]) : a * cw + om * P[k];
                 // no gradient where the pixel skipped the entry or alpha was clamped
                 const float g = (!ok || rG[k] > 0.99f) ? 0.0f : G[k] * dalpha;
                 const float gx = g * dx[k], gy = g * dy[k];
@@ -530,7 +534,33 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 for (int q = 0; q < 8; q++) v[q] = k == 0 ? t[q] : v[q] + t[q];
                 e = k == 0 ? g : e + g;
             }
-            if constexpr (RED) {
+            if constexpr (RED == 3) {
+                // sparse entries (<= 2 pixels-lanes of the warp composite): those lanes add their own
+                // terms (the outputs are linear in the sums), skipping the butterfly
+                const unsigned cl = __ballot_sync(VKS_FULL_MASK, contrib);
+                if (__popc(cl) <= 2) {
+                    if (contrib) {
+                        const uint32_t id = __float_as_uint(Cc.y);
+                        const float nrho = -B.y;
+                        atomicAdd(dmeans2d + 2 * (size_t)id, nrho * fmaf(2.0f * A.z, v[0], A.w * v[1]));
+                        atomicAdd(dmeans2d + 2 * (size_t)id + 1, nrho * fmaf(2.0f * B.x, v[1], A.w * v[0]));
+                        atomicAdd(dconics + 3 * (size_t)id, nrho * 0.5f * v[2]);
+                        atomicAdd(dconics + 3 * (size_t)id + 1, nrho * v[3]);
+                        atomicAdd(dconics + 3 * (size_t)id + 2, nrho * 0.5f * v[4]);
+                        atomicAdd(dcolors + 3 * (size_t)id, v[5]);
+                        atomicAdd(dcolors + 3 * (size_t)id + 1, v[6]);
+                        atomicAdd(dcolors + 3 * (size_t)id + 2, v[7]);
+                        atomicAdd(dopac + id, e);
+                    }
+                } else {
+                    const float r = warp_reduce_8plus1(v, e, lane);
+                    const float other = __shfl_xor_sync(VKS_FULL_MASK, r, 4);
+                    const float nrho = -B.y;
+                    const float cr = fmaf(nrho, fmaf(kA, 2.0f * A.z, fmaf(kC, 2.0f * B.x, kH)), kOne);
+                    const float out = myterm == 8 ? e : fmaf(cr, r, (nrho * kB * A.w) * other);
+                    if (myterm >= 0) atomicAdd(tbase + (size_t)__float_as_uint(Cc.y) * tstride, out);
+                }
+            } else if constexpr (RED == 1) {
                 red.p[cnt][lane][0] = make_float4(v[0], v[1], v[2], v[3]);
                 red.p[cnt][lane][1] = make_float4(v[4], v[5], v[6], v[7]);
                 red.p[cnt][lane][2].x = e;
@@ -551,7 +581,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 if (myterm >= 0) atomicAdd(tbase + (size_t)__float_as_uint(Cc.y) * tstride, out);
             }
         }
-        if (RED && cnt > 0) flush_chunk(red, s, cnt, slots, lane, dmeans2d, dconics, dcolors, dopac);
+        if (RED == 1 && cnt > 0) flush_chunk(red, s, cnt, slots, lane, dmeans2d, dconics, dcolors, dopac);
     }
 }
 
@@ -574,10 +604,13 @@ int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2
                const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                float* dopacities, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    const size_t dyn = RED ? sizeof(WarpRed) * (8 / PPT) : 0;
-    if (dyn > 48 * 1024) {  // per call: the attribute belongs to the current device
+    const size_t dyn = RED == 1 ? sizeof(WarpRed) * (8 / PPT) : 0;
+    if (RED == 1) {  // per call: the attributes belong to the current device
         cudaError_t e = cudaFuncSetAttribute(raster_bwd_kernel<PPT, CULL, RED>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e == cudaSuccess)  // shared memory for 7 resident blocks (not the default L1-heavy split)
+            e = cudaFuncSetAttribute(raster_bwd_kernel<PPT, CULL, RED>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, kCarveout);
         if (e != cudaSuccess) return cuda_fail(e, "raster_bwd smem attribute");
     }
     raster_bwd_kernel<PPT, CULL, RED><<<n_tiles, 32 * 8 / PPT, dyn, st>>>(
@@ -626,21 +659,21 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
                  const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                  float* dopacities, cudaStream_t st) {
     // cross-lane reduction: chunked through shared memory (1, default) or a 32-lane butterfly per entry (0)
-    const int red = env_choice("VKS_RASTER_BWD_RED", 1, 0, 1);
+    const int red = env_choice("VKS_RASTER_BWD_RED", 2, 0, 3);
+    kCarveout = env_choice("VKS_RASTER_CARVEOUT", 50, 0, 100);
 #define VKS_BWD_ARGS cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, \
                      n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st
-    if (red) {
-        switch (cull) {
-            case kCullNone: return launch_bwd<PPT, kCullNone, 1>(VKS_BWD_ARGS);
-            case kCullBox: return launch_bwd<PPT, kCullBox, 1>(VKS_BWD_ARGS);
-            default: return launch_bwd<PPT, kCullEllipse, 1>(VKS_BWD_ARGS);
-        }
+#define VKS_BWD_CULL(R)                                                                  \
+    switch (cull) {                                                                      \
+        case kCullNone: return launch_bwd<PPT, kCullNone, R>(VKS_BWD_ARGS);              \
+        case kCullBox: return launch_bwd<PPT, kCullBox, R>(VKS_BWD_ARGS);                \
+        default: return launch_bwd<PPT, kCullEllipse, R>(VKS_BWD_ARGS);                  \
     }
-    switch (cull) {
-        case kCullNone: return launch_bwd<PPT, kCullNone, 0>(VKS_BWD_ARGS);
-        case kCullBox: return launch_bwd<PPT, kCullBox, 0>(VKS_BWD_ARGS);
-        default: return launch_bwd<PPT, kCullEllipse, 0>(VKS_BWD_ARGS);
-    }
+    if (red == 1) VKS_BWD_CULL(1)
+    if (red == 2) VKS_BWD_CULL(2)
+    if (red == 3) VKS_BWD_CULL(3)
+    VKS_BWD_CULL(0)
+#undef VKS_BWD_CULL
 #undef VKS_BWD_ARGS
 }
 

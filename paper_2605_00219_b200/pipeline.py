@@ -15,6 +15,9 @@ import torch
 from . import _vks as V
 
 
+GRAD_NAMES = ("dmeans", "dlog_scales", "dquats", "dopacity_logits", "dsh")
+
+
 @dataclass
 class GaussianParams:
     means: torch.Tensor
@@ -23,14 +26,24 @@ class GaussianParams:
     opacity_logits: torch.Tensor
     sh: torch.Tensor
     grad_flat: torch.Tensor
+    # storage rows (>= n): every parameter tensor is the first n rows of a zero-padded [rows, ...]
+    # tensor and every gradient group spans `rows` rows, so that the groups split into equal
+    # per-rank shards for the sharded optimizer (shard.ShardedAdam).  0 = n (no padding).
+    rows: int = 0
+    storage: tuple | None = None  # the padded parameter tensors (None when rows == n)
 
     @property
     def n(self) -> int:
         return self.means.shape[0]
 
+    @property
+    def n_rows(self) -> int:
+        return self.rows or self.n
+
     @staticmethod
     def layout(n: int, K: int):
-        """(offset, numel) of each gradient group inside grad_flat; groups start 256-byte aligned."""
+        """(offset, numel) of each gradient group inside grad_flat for n (storage) rows; groups
+        start 256-byte aligned."""
         sizes = [3 * n, 3 * n, 4 * n, n, 3 * K * n]
         offs, o = [], 0
         for s in sizes:
@@ -39,20 +52,47 @@ class GaussianParams:
         return offs, o
 
     @staticmethod
-    def from_host(scene: dict, device="cuda") -> "GaussianParams":
+    def from_host(scene: dict, device="cuda", pad_to: int = 1) -> "GaussianParams":
+        """pad_to: storage rows rounded up to a multiple of this (the world size of a sharded
+        optimizer); the padding rows are zero and never rendered."""
         t = {k: torch.as_tensor(v).to(device=device, dtype=torch.float32).contiguous() for k, v in scene.items()}
         n, K = t["means"].shape[0], t["sh"].shape[1]
-        _, total = GaussianParams.layout(n, K)
+        rows = -(-n // pad_to) * pad_to if pad_to > 1 else n
+        names = ("means", "log_scales", "quats", "opacity_logits", "sh")
+        storage = None
+        if rows != n:
+            storage = tuple(torch.zeros((rows,) + tuple(t[k].shape[1:]), dtype=torch.float32, device=device)
+                            for k in names)
+            for st, k in zip(storage, names):
+                st[:n].copy_(t[k])
+            t = {k: st[:n] for st, k in zip(storage, names)}
+        _, total = GaussianParams.layout(rows, K)
         g = torch.zeros(total, dtype=torch.float32, device=device)
-        return GaussianParams(t["means"], t["log_scales"], t["quats"], t["opacity_logits"], t["sh"], g)
+        return GaussianParams(t["means"], t["log_scales"], t["quats"], t["opacity_logits"], t["sh"], g,
+                              rows=rows if rows != n else 0, storage=storage)
+
+    def _group_shapes(self, rows):
+        K = self.sh.shape[1]
+        return [(rows, 3), (rows, 3), (rows, 4), (rows,), (rows, K, 3)]
 
     def grads(self) -> dict:
-        """Views into grad_flat: [dmeans | dlog_scales | dquats | dlogit | dsh] (group-major)."""
-        n, K = self.n, self.sh.shape[1]
-        offs, _ = GaussianParams.layout(n, K)
-        shapes = [(n, 3), (n, 3), (n, 4), (n,), (n, K, 3)]
-        names = ["dmeans", "dlog_scales", "dquats", "dopacity_logits", "dsh"]
-        return {nm: self.grad_flat[o:o + s].view(*sh) for nm, (o, s), sh in zip(names, offs, shapes)}
+        """Views into grad_flat: [dmeans | dlog_scales | dquats | dlogit | dsh] (group-major), n rows."""
+        return {nm: g.view(*sh) for nm, g, sh in zip(GRAD_NAMES, self.grad_groups(0, self.n),
+                                                      self._group_shapes(self.n))}
+
+    def grad_groups(self, r0: int = 0, r1: int | None = None) -> list:
+        """The five gradient groups restricted to storage rows [r0, r1) (flat views into grad_flat)."""
+        r1 = self.n_rows if r1 is None else r1
+        offs, _ = GaussianParams.layout(self.n_rows, self.sh.shape[1])
+        cols = [3, 3, 4, 1, 3 * self.sh.shape[1]]
+        return [self.grad_flat[o + r0 * c:o + r1 * c] for (o, _), c in zip(offs, cols)]
+
+    def param_groups(self, r0: int = 0, r1: int | None = None) -> list:
+        """The five parameter tensors restricted to storage rows [r0, r1) (padding rows included)."""
+        full = self.storage if self.storage is not None else (self.means, self.log_scales, self.quats,
+                                                              self.opacity_logits, self.sh)
+        r1 = self.n_rows if r1 is None else r1
+        return [t[r0:r1] for t in full]
 
 
 class ViewRenderer:
@@ -93,13 +133,15 @@ class ViewRenderer:
         rasterizer needs the sorted ids and the tile ranges)."""
         V.vks_project_fwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.means2d,
                           self.conics, self.depths, self.radii, self.tiles, self.colors, self.opacities)
-        while True:
+        for attempt in range(2):
             m = V.vks_bin_sort(cam, self.means2d, self.radii, self.depths, self.tiles, self.offsets,
                                self.keys if want_keys else None,
                                self.vals, self.tile_offsets, self.workspace, keys_unsorted, vals_unsorted,
                                raise_capacity=False, tile_order=self.tile_order)
             if m >= 0:
                 break
+            if attempt == 1:  # the call is idempotent: a regrown capacity always fits the same M
+                raise RuntimeError(f"vks_bin_sort: {-m} intersections exceed the regrown capacity {self.capacity}")
             self._alloc_capacity(int(-m * 1.25) + 1024)
         self.num_isects = m
         V.vks_raster_fwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.radii, self.vals,

@@ -2,14 +2,21 @@
 """Benchmark of the VkSplat hot path on B200 (BASELINE.json metric:
 "fwd+bwd rasterize iters/sec @5.8M Gaussians 1237x822; sort Gkeys/s; HBM GB/s").
 
-A step = one full pass of the hot path per rank: projection forward, index offsets + keys + radix
-sort + tile ranges, raster forward, raster backward, projection backward (SURVEY §8(a) rows
-a1-a8) for one view of the synthetic bicycle-shaped scene, plus (N > 1) the allreduce of the
-per-Gaussian gradient buffer (row a9).  Views are sharded across ranks (rank r renders ring views
-r, r+N, ...), so per-GPU work is fixed as N grows ("weak" scaling).
+A step = one training step's hot path per rank: a batch of ring views
+of the synthetic bicycle-shaped scene — one batched projection forward, then index offsets + keys
++ radix sort + tile ranges, raster forward and raster backward per view, one batched projection
+backward — plus (N > 1) the all-reduce of the per-Gaussian gradient buffer, chunked by Gaussian rows
+and overlapped with the projection backward (row a9).  Views are sharded across ranks:
+`--scaling strong` (default) splits one global batch of `--views` views (BASELINE config 4: "a
+batch of 8 views sharded across 1/2/4/8"); `--scaling weak` gives every rank `--views` distinct
+views of a ring of views x N cameras.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config bicycle]
+                    [--scaling strong|weak] [--views 8]
 
+Beside the step (not in `value`): `batch1` (the paper's iteration: one view at a time through the
+single-view entry points), `train_step` (the step plus the optimizer, row f1: sharded
+reduce-scatter / Adam / all-gather), the loss gradient, MCMC and densification rows.
 Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the reference arm of
 this tier) on the host cores.
 """
@@ -38,7 +45,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="bicycle")
-    ap.add_argument("--views-per-rank", type=int, default=8, help="views per rank per step (the batch)")
+    ap.add_argument("--views", type=int, default=8,
+                    help="views per step: the global batch (strong scaling) or per rank (weak scaling)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--ar-chunks", type=int, default=4,
+                    help="N > 1: gradient all-reduce chunks, each overlapped with the next projection-bwd chunk")
+    ap.add_argument("--no-batch1", action="store_true")
     ap.add_argument("--streams", type=int, default=3, help="views in flight per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -145,6 +157,18 @@ def measured_traffic(stage, key="dram_bytes_per_launch"):
         return None
 
 
+# The paper's RTX 3090 stage times, bicycle, default densification (seconds per
+# training run; the iteration count is not stated, 30k assumed (A28)): context only —
+# another GPU, and N grows over training there while it is fixed at 5.8M here.
+PAPER_CONTEXT = dict(
+    source="PAPER.md P:61-76, RTX 3090, bicycle, default densification, seconds per training run",
+    seconds=dict(project_fwd=32.6, index_offset=5.6, generate_keys=8.5, sorting=14.6, tile_ranges=0.5,
+                 raster_fwd=31.9, raster_bwd=163.0, proj_bwd_plus_optimizer=236.2),
+    ms_per_iter_at_30k_iters=dict(project_fwd=1.087, bin_sort=0.973, raster_fwd=1.063, raster_bwd=5.433,
+                                  proj_bwd_plus_optimizer=7.873),
+    note="iteration count not stated in the paper (30k assumed); N grows during training there")
+
+
 # ----------------------------------------------------------------------------------- ours
 def run_ours(args):
     import torch
@@ -152,7 +176,7 @@ def run_ours(args):
 
     import paper_2605_00219_b200 as P
     import synth
-    from paper_2605_00219_b200.shard import allreduce_grads
+    from paper_2605_00219_b200.shard import GradientSync, ShardedAdam, partition_views
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -168,12 +192,16 @@ def run_ours(args):
     c = synth.CONFIGS[args.config]
     cfg = synth.default_render_config(3)
     scene = synth.make_scene(c.n, c.kind, c.seed)
-    cams = synth.ring_cameras(c.width, c.height, c.kind, 8)
-    params = P.GaussianParams.from_host(scene)
+    # the views this rank renders every step (strong: its share of one global batch; weak: its own
+    # batch of distinct views) and the ring they come from
+    my_views, ring = partition_views(rank, world, args.views, args.scaling)
+    views_per_step = args.views if args.scaling == "strong" else args.views * world  # all ranks
+    cams = synth.ring_cameras(c.width, c.height, c.kind, ring)
+    params = P.GaussianParams.from_host(scene, pad_to=world)  # equal row shards for the sharded optimizer
     del scene
     n = params.n
-    B, S = args.views_per_rank, max(1, args.streams)
-    my_views = [(rank + world * j) % 8 for j in range(8)]  # rank r renders ring views r, r + N, ...
+    B, S = len(my_views), max(1, args.streams)
+    gsync = GradientSync(params, n_chunks=args.ar_chunks if world > 1 else 1)
     host_dL = {v: torch.from_numpy(synth.upstream_grad(c.height, c.width, c.seed + 1000 + v)) for v in set(my_views)}
     dLs = {v: t.cuda() for v, t in host_dL.items()}
     rends = [P.ViewRenderer(n, c.width, c.height) for _ in range(S)]
@@ -261,18 +289,29 @@ def run_ours(args):
             done.record(st)
         return m, done
 
-    def project_bwd_batch(vcams, st):
+    def project_bwd_batch(vcams, st, sync=None):
         """The batch's projection backward: one pass over the parameters for all its views,
-        overwriting the gradient buffer (row a8)."""
+        overwriting the gradient buffer (row a8).  With `sync` (N > 1), in Gaussian-row chunks,
+        each chunk's gradient all-reduce (row a9) started as soon as its rows are written."""
         g = params.grads()
         nb = len(vcams)
+        chunks = sync.chunks() if sync is not None else [(0, n)]
         with torch.cuda.stream(st):
-            P.vks_project_bwd_batch(cfg_ow, vcams, params.means, params.log_scales, params.quats,
-                                    params.opacity_logits, params.sh, [vbuf[j]["colors"] for j in range(nb)],
-                                    [vbuf[j]["radii"] for j in range(nb)], [vbuf[j]["dm2"] for j in range(nb)],
-                                    [vbuf[j]["dcon"] for j in range(nb)], [vbuf[j]["dcol"] for j in range(nb)],
-                                    [vbuf[j]["dop"] for j in range(nb)], g["dmeans"], g["dlog_scales"], g["dquats"],
-                                    g["dopacity_logits"], g["dsh"])
+            for r0, r1 in chunks:
+                P.vks_project_bwd_batch(cfg_ow, vcams, params.means[r0:r1], params.log_scales[r0:r1],
+                                        params.quats[r0:r1], params.opacity_logits[r0:r1], params.sh[r0:r1],
+                                        [vbuf[j]["colors"][r0:r1] for j in range(nb)],
+                                        [vbuf[j]["radii"][r0:r1] for j in range(nb)],
+                                        [vbuf[j]["dm2"][r0:r1] for j in range(nb)],
+                                        [vbuf[j]["dcon"][r0:r1] for j in range(nb)],
+                                        [vbuf[j]["dcol"][r0:r1] for j in range(nb)],
+                                        [vbuf[j]["dop"][r0:r1] for j in range(nb)], g["dmeans"][r0:r1],
+                                        g["dlog_scales"][r0:r1], g["dquats"][r0:r1], g["dopacity_logits"][r0:r1],
+                                        g["dsh"][r0:r1])
+                if sync is not None:
+                    sync.launch(r0, r1)
+            if sync is not None:
+                sync.finish()
 
     def step(s, copies=None):
         """One training step's hot path: a batch of B views per rank — one batched projection
@@ -280,7 +319,7 @@ def run_ours(args):
         over S streams, one batched projection backward (row a8) and the allreduce (row a9; no-op
         at N = 1).  The batch starts after the previous step's allreduce (an optimizer would run
         there)."""
-        vviews = [my_views[(s * B + j) % len(my_views)] for j in range(B)]
+        vviews = my_views
         vcams = [cams[v] for v in vviews]
         project_fwd_batch(vcams, main)  # after the previous step's allreduce (main stream order)
         start = torch.cuda.Event()
@@ -295,12 +334,11 @@ def run_ours(args):
                 cp = (copies[0][v], copies[1][k], None if copies[2] is None else copies[2][j:j + 1])
             m, done = view_path(rends[k], vbuf[j], cams[v], dLs[v], streams[k], copies=cp)
             main.wait_event(done)
-        project_bwd_batch(vcams, main)
+        project_bwd_batch(vcams, main, gsync if world > 1 else None)  # + the chunked all-reduce (row a9)
         if copies is not None and copies[2] is not None:
             copies[3].copy_(copies[2], non_blocking=True)  # the batch's losses to pinned host memory
         elif copies is not None:
             main.wait_stream(copy_stream)  # every image of the batch has reached the host
-        allreduce_grads(params.grad_flat)
         return m
 
     def timed(fn, nsteps):
@@ -335,8 +373,55 @@ def run_ours(args):
     if ncu_range:
         torch.cuda.cudart().cudaProfilerStop()
     clk = clocks.stop()
-    views_total = world * B * args.steps
+    views_total = views_per_step * args.steps
     value = views_total / (elapsed_ms / 1e3)
+
+    # --- batch 1: the paper's iteration — one view at a time through
+    # the single-view entry points (vks_project_fwd, vks_bin_sort, vks_raster_fwd, vks_raster_bwd,
+    # vks_project_bwd) on one stream, CUDA events between them; views cycle over the rank's views
+    batch1 = None
+    if not args.no_batch1:
+        rb = rends[0]
+        gb = params.grads()
+        nb1 = max(24, args.steps)
+        b1ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(nb1 + 3)]
+        for i in range(nb1 + 3):
+            cam = cams[my_views[i % B]]
+            dLv = dLs[my_views[i % B]]
+            e = b1ev[i]
+            e[0].record(main)
+            P.vks_project_fwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
+                              params.sh, rb.means2d, rb.conics, rb.depths, rb.radii, rb.tiles, rb.colors,
+                              rb.opacities)
+            e[1].record(main)
+            P.vks_bin_sort(cam, rb.means2d, rb.radii, rb.depths, rb.tiles, rb.offsets, None, rb.vals,
+                           rb.tile_offsets, rb.workspace, tile_order=rb.tile_order)
+            e[2].record(main)
+            P.vks_raster_fwd(cfg, cam, rb.means2d, rb.conics, rb.colors, rb.opacities, rb.radii, rb.vals,
+                             rb.tile_offsets, rb.image, rb.T_final, rb.n_contrib, tile_order=rb.tile_order)
+            e[3].record(main)
+            rb.g2d.zero_()  # the raster backward accumulates the view's 2D gradients
+            P.vks_raster_bwd(cfg, cam, rb.means2d, rb.conics, rb.colors, rb.opacities, rb.radii, rb.vals,
+                             rb.tile_offsets, rb.T_final, rb.n_contrib, dLv, rb.dmeans2d, rb.dconics, rb.dcolors,
+                             rb.dopacities, tile_order=rb.tile_order)
+            e[4].record(main)
+            P.vks_project_bwd(cfg_ow, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
+                              params.sh, rb.colors, rb.radii, rb.dmeans2d, rb.dconics, rb.dcolors, rb.dopacities,
+                              gb["dmeans"], gb["dlog_scales"], gb["dquats"], gb["dopacity_logits"], gb["dsh"])
+            e[5].record(main)
+        torch.cuda.synchronize()
+        b1 = b1ev[3:]
+        b1_total = b1[0][0].elapsed_time(b1[-1][5])
+        b1_stage = {name: statistics.median([e[q].elapsed_time(e[q + 1]) for e in b1])
+                    for q, name in enumerate(stages)}
+        b1_vis = int((rb.tiles > 0).sum().item())
+        batch1 = dict(value=round(len(b1) / (b1_total / 1e3), 3), unit="iters/s",
+                      ms_per_iter=round(b1_total / len(b1), 4),
+                      stages_ms={k: round(v, 4) for k, v in b1_stage.items()}, _vis=b1_vis, _m=rb.num_isects,
+                      note=("the paper's iteration: one view at a time through the single-view entry points "
+                            "on one stream (P:59, P:67-76; S:614-616), projection backward writing the "
+                            "gradients (overwrite), the 2D-gradient memset inside raster_bwd; "
+                            f"{len(b1)} timed views after 3 warm-up views"))
 
     # --- per-stage breakdown (its own timed region): views one at a time on one stream, CUDA
     # events between the entry points; medians over the views
@@ -491,6 +576,11 @@ def run_ours(args):
         tf = fl[k] / (st_ms[k] * 1e-3) / 1e12
         per_stage[k] = dict(ms=st_ms[k], bound="alu", achieved=tf, peak=fp32_peak_tflops, unit="TFLOP/s",
                             frac=tf / fp32_peak_tflops, algorithmic_flops=fl[k])
+    # the batched projection forward's fraction without the 2D-gradient zeroing it performs for the
+    # raster backward (36 B per Gaussian and view: a memset moved into the kernel, not projection work)
+    pf_bytes_proj = ab["project_fwd"] - 36 * n
+    per_stage["project_fwd"]["frac_without_g2d_zero"] = (pf_bytes_proj / (st_ms["project_fwd"] * 1e-3) / 1e9
+                                                         / pk["hbm_gbs"])
     # the dominant KERNEL: the longest of the single-kernel stages (bin_sort is a chain of ~25 short
     # kernels; its stage roofline is reported in stage_roofline)
     dom = max(("project_fwd", "raster_fwd", "raster_bwd", "project_bwd"), key=lambda k: per_stage[k]["ms"])
@@ -498,25 +588,52 @@ def run_ours(args):
     roofline = dict(kernel=dom, bound=d["bound"], achieved=round(d["achieved"], 3), peak=round(d["peak"], 3),
                     unit=d["unit"], frac=round(d["frac"], 4), traffic=measured_traffic(dom),
                     issue_active_ncu=measured_traffic(dom, "issue_active"),
-                    peak_source=(pk["src"] + (" HBM copy (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
-                                              f" FP32 FMA: 148 SM x 128 lanes x 2 flop x {clock_mhz:.0f} MHz")))
+                    peak_source=(pk["src"] + " HBM copy (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
+                                 f"derived (no measured FP32 figure in MEASURED_PEAKS.json): 148 SM x 128 FP32 "
+                                 f"lanes x 2 flop x {clock_mhz:.0f} MHz (median SM clock sampled in the timed "
+                                 f"region)"))
     # our kernels per view: bin_sort = id scan (3) + dpasses x (count, scan, scatter) + depth-order
     # scan (3) + rect diff + tile count + tile passes x 3; raster fwd; raster bwd; plus one batched
-    # project fwd and one batched project bwd per step
+    # project fwd and one chunked batched project bwd per step
     tp = max(1, ((rend.n_tiles - 1).bit_length() + 7) // 8)
-    gpu_launches = (((3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1) * B + 2) * args.steps
+    gpu_launches = (((3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1) * B + 1 + len(gsync.chunks() if world > 1
+                                                                                  else [0])) * args.steps
+    if batch1 is not None:
+        # stage rooflines of the single-view kernels (DESIGN.md §6.3 per-unit bytes): projection
+        # forward 60 B per Gaussian (geometry + opacity read, radii + tiles written) + 232 B per
+        # visible one (SH row read, outputs written); projection backward with overwrite 244 B per
+        # Gaussian (radii read, gradient row written) + 280 B per visible one (parameters, 2D
+        # gradients and colour read); binning as in the step
+        v1, m1 = batch1.pop("_vis"), batch1.pop("_m")
+        b1_bytes = dict(project_fwd=60 * n + 232 * v1, bin_sort=algorithmic_bytes(n, v1, m1, dpasses)["bin_sort"],
+                        project_bwd=244 * n + 280 * v1)
+        b1_roof = {}
+        for k, b in b1_bytes.items():
+            gbs = b / (batch1["stages_ms"][k] * 1e-3) / 1e9
+            b1_roof[k] = dict(bound="hbm", achieved=round(gbs, 1), peak=pk["hbm_gbs"], unit="GB/s",
+                              frac=round(gbs / pk["hbm_gbs"], 4), algorithmic_bytes=int(b))
+        for k in ("raster_fwd", "raster_bwd"):
+            tf = fl[k] / (batch1["stages_ms"][k] * 1e-3) / 1e12
+            b1_roof[k] = dict(bound="alu", achieved=round(tf, 3), peak=round(fp32_peak_tflops, 3), unit="TFLOP/s",
+                              frac=round(tf / fp32_peak_tflops, 4))
+        b1_roof["bin_sort"]["gkeys_per_s"] = round(m1 / (batch1["stages_ms"]["bin_sort"] * 1e-3) / 1e9, 3)
+        batch1["stage_roofline"] = b1_roof
+        batch1["gpu_launches_per_iter"] = (3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 4
 
     out = dict(metric=METRIC, value=round(value, 3), unit="iters/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(elapsed_ms / args.steps, 4), higher_is_better=True,
-               scaling="weak", vs_baseline=None, dtype="f32", data="synthetic",
+               scaling=args.scaling, vs_baseline=None, dtype="f32", data="synthetic",
                config=dict(workload=c.description + ", fwd+bwd", n_gaussians=n, width=c.width,
-                           height=c.height, sh_degree=3, footprint="support", views_per_rank_per_step=B,
-                           streams=S, visible=vis, num_isects=m_last,
+                           height=c.height, sh_degree=3, footprint="support", views_per_step=views_per_step,
+                           views_per_rank_per_step=B, streams=S, visible=vis, num_isects=m_last,
                            l2="inputs larger than L2 (params 1.37 GB, keys+vals 0.22 GB per view), no flush",
-                           parallelism=f"view-sharded dp{world}",
-                           step=(f"{B} ring views per rank: one batched projection forward, binning and both "
-                                 f"raster passes per view ({S} views in flight, one stream each), one batched projection "
-                                 f"backward, then one allreduce; unit = views")),
+                           parallelism=f"view-sharded dp{world} ({args.scaling} scaling)",
+                           step=(f"{B} ring views per rank ({views_per_step} per step in all): one batched projection "
+                                 f"forward, binning and both raster passes per view ({S} views in flight, one "
+                                 f"stream each), one batched projection backward"
+                                 + (f" in {len(gsync.chunks())} Gaussian-row chunks, each chunk's gradient "
+                                    f"all-reduce (NCCL) overlapping the next chunk" if world > 1 else "")
+                                 + "; unit = views")),
                stages_ms={k: round(v, 4) for k, v in st_ms.items()},
                stage_roofline={k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                                for k, v in per_stage.items()},
@@ -525,8 +642,8 @@ def run_ours(args):
                raster_work=dict(visited_pairs=visited, composited_pairs=composited, evaluated_pairs=evaluated,
                                 replayed_pairs=replayed, warp_entries=warp_entries,
                                 warp_entries_composited=warp_entries_comp),
-               roofline=roofline, gpu_launches=gpu_launches, clocks=clk, optimizer=optimizer,
-               loss_grad=loss_grad, mcmc=mcmc, densify=densify)
+               roofline=roofline, gpu_launches=gpu_launches, clocks=clk, batch1=batch1, optimizer=optimizer,
+               loss_grad=loss_grad, mcmc=mcmc, densify=densify, paper_context=PAPER_CONTEXT)
 
     if not args.no_e2e:
         # (1) the path end to end: each view's dL/dimage copied in from pinned host memory and its
@@ -576,6 +693,27 @@ def run_ours(args):
                                     note=("per view: the target image in from pinned host memory, loss + dL/dimage "
                                           "computed on the device (row f2), the batch's losses out; inside the "
                                           "timed region"))
+    # --- the training step (beside `value`): the step plus the optimizer (row f1) in its sharded
+    # form — reduce-scatter of the gradients, Adam on this rank's 1/N of the rows, all-gather of the
+    # parameters (at N = 1: Adam on every row).  Last, because it moves the parameters.
+    opt = ShardedAdam(params, lrs, rank, world)
+    tcount = [0]
+
+    def train(s):
+        step(s)
+        tcount[0] += 1
+        opt.step(tcount[0])
+
+    for s in range(2):
+        train(s)
+    tr_ms = timed(train, args.steps)
+    out["train_step"] = dict(
+        row="a1-a9 + f1: the step plus the sharded optimizer; not in value", value=round(
+            views_per_step * args.steps / (tr_ms / 1e3), 3), unit="iters/s", ms_per_step=round(tr_ms / args.steps, 4),
+        optimizer=("reduce-scatter + vks_adam_step on 1/%d of the rows + all-gather" % world if world > 1 else
+                   "vks_adam_step on every row"),
+        moments_bytes_per_rank=int(sum(t.numel() for t in opt.m) * 8))
+    del opt
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, c, cfg)
     if distributed:

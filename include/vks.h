@@ -76,6 +76,18 @@ typedef struct {
 /* vks_project_bwd WRITES its parameter gradients instead of accumulating them, and writes zeros
  * to the rows of Gaussians with radii == 0 (first view of a batch: no memset of the buffer). */
 #define VKS_FLAG_GRAD_OVERWRITE 1u
+/* Debug mode (SURVEY §8(b) "Errors"): before computing, the entry point checks its inputs on the
+ * device and synchronises `stream` once to read the result —
+ *   vks_project_fwd(_batch), vks_project_bwd(_batch): every parameter finite and every quaternion
+ *     of norm > 1e-12, else VKS_ERR_NONFINITE (S:119 NonFiniteParameter, S:52 ZeroQuaternion);
+ *     the backward also checks its 2D gradients;
+ *   vks_raster_fwd / vks_raster_bwd: tile_offsets a CSR (starts at 0, non-decreasing) whose entries
+ *     index [0, n), else VKS_ERR_UNSORTED (S:155 UnsortedInput); the backward also checks that
+ *     dL_dimage is finite (VKS_ERR_NONFINITE).
+ * Nothing is written when a check fails.  Without the flag, non-finite Gaussians are culled by the
+ * projection and nothing is checked.  Uses a module-scope device status word:
+ * not for concurrent streams. */
+#define VKS_FLAG_VALIDATE 2u
 
 enum {
     VKS_OK = 0,
@@ -84,7 +96,8 @@ enum {
     VKS_ERR_WORKSPACE = 3,  /* workspace too small */
     VKS_ERR_CUDA = 4,       /* launch / runtime failure (incl. no CUDA device) */
     VKS_ERR_UNSUPPORTED = 5, /* configuration outside the library's limits (e.g. M >= 2^30 keys) */
-    VKS_ERR_NONFINITE = 6    /* VKS_FLAG_VALIDATE: a non-finite input (S:119 NonFiniteParameter) */
+    VKS_ERR_NONFINITE = 6,   /* VKS_FLAG_VALIDATE: a non-finite input (S:119 NonFiniteParameter) */
+    VKS_ERR_UNSORTED = 7     /* VKS_FLAG_VALIDATE / vks_bin_sort_check: not a sorted binning */
 };
 
 const char* vks_status_string(int status);
@@ -151,6 +164,19 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
                  uint32_t* vals_unsorted, uint32_t* tile_offsets, uint32_t* tile_order,
                  int64_t* num_isects,
                  void* workspace, size_t workspace_bytes, vks_stream_t stream);
+
+/*
+ * vks_bin_sort_check — debug verification of a binning ("Tile Ranges" errors, S:155 UnsortedInput):
+ * checks that tile_offsets [n_tiles+1] is a CSR of [0, num_isects) (starts at 0, non-decreasing,
+ * ends at num_isects), that every id vals[k] < n, that the tile rect of Gaussian vals[k] (projection
+ * step 11 from means2d / radii) contains the tile k belongs to, and that the entries of every tile
+ * are strictly ascending in (f32 bits of depths[id], id) — i.e. the sort of the (tile | depth) keys
+ * with ties by id.  Returns VKS_OK or VKS_ERR_UNSORTED; synchronises `stream` once; writes nothing.
+ * Inputs as produced by vks_project_fwd / vks_bin_sort (device pointers).
+ */
+int vks_bin_sort_check(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
+                       const float* depths, const uint32_t* vals, const uint32_t* tile_offsets,
+                       int64_t num_isects, vks_stream_t stream);
 
 /*
  * vks_raster_fwd — "Rasterization Forward".

@@ -1,7 +1,7 @@
 """Build libvks.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
 Every translation unit is compiled with `-gencode arch=compute_100a,code=sm_100a -lineinfo -O3`.
-project.cu and binning.cu additionally use `-fmad=false`: their fp32 operation order is pinned
+project.cu, binning.cu and validate.cu additionally use `-fmad=false`: their fp32 operation order is pinned
  so projection outputs, tile rects and keys are bit-exact with the oracle.
 """
 from __future__ import annotations
@@ -19,8 +19,8 @@ BUILD_DIR = os.path.join(ROOT, "build", "vks")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-PINNED = {"project.cu", "binning.cu"}
-SOURCES = ["project.cu", "project_bwd.cu", "binning.cu", "raster.cu", "adam.cu", "loss.cu", "mcmc.cu", "densify.cu", "api.cu"]
+PINNED = {"project.cu", "binning.cu", "validate.cu"}
+SOURCES = ["project.cu", "project_bwd.cu", "binning.cu", "raster.cu", "adam.cu", "loss.cu", "mcmc.cu", "densify.cu", "validate.cu", "api.cu"]
 HEADERS = ["vks_common.cuh"]
 
 

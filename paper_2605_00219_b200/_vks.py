@@ -20,16 +20,18 @@ if not os.path.exists(LIB_PATH):
                       "(or __graft_entry__.build()); the CUDA path has no fallback")
 _lib = C.CDLL(LIB_PATH)
 
-VKS_OK, VKS_ERR_INVALID_ARG, VKS_ERR_CAPACITY, VKS_ERR_WORKSPACE, VKS_ERR_CUDA, VKS_ERR_UNSUPPORTED = range(6)
+(VKS_OK, VKS_ERR_INVALID_ARG, VKS_ERR_CAPACITY, VKS_ERR_WORKSPACE, VKS_ERR_CUDA, VKS_ERR_UNSUPPORTED,
+ VKS_ERR_NONFINITE, VKS_ERR_UNSORTED) = range(8)
 FOOTPRINT_SUPPORT, FOOTPRINT_3SIGMA = 0, 1
 FLAG_GRAD_OVERWRITE = 1
+FLAG_VALIDATE = 2
 
 EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_project_fwd",
            "vks_bin_sort_workspace_bytes", "vks_bin_sort", "vks_raster_fwd", "vks_raster_fwd_stats",
            "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch",
            "vks_adam_step", "vks_loss_workspace_bytes", "vks_loss_grad", "vks_mcmc_workspace_bytes",
            "vks_mcmc_relocate", "vks_mcmc_noise", "vks_densify_stats", "vks_densify_workspace_bytes",
-           "vks_densify")
+           "vks_densify", "vks_bin_sort_check")
 
 
 class VksCamera(C.Structure):
@@ -74,6 +76,7 @@ _lib.vks_bin_sort_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int32]
 _lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
 _lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 8 + [C.c_size_t, _P]
 _lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 12
+_lib.vks_bin_sort_check.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64, _P]
 _lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 16
 _lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 10
 _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
@@ -206,6 +209,18 @@ def vks_bin_sort(cam, means2d, radii, depths, tiles_touched, offsets, keys, vals
         return -int(m.value)
     _check("vks_bin_sort", st)
     return int(m.value)
+
+
+def vks_bin_sort_check(cam, means2d, radii, depths, vals, tile_offsets, num_isects, stream=None) -> int:
+    """Debug verification of a binning (include/vks.h): returns the status (VKS_OK or
+    VKS_ERR_UNSORTED) instead of raising on it; other failures raise."""
+    k = cam if isinstance(cam, VksCamera) else make_camera(cam)
+    st = _lib.vks_bin_sort_check(C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"), _ptr(radii, i32, "radii"),
+                                 _ptr(depths, f32, "depths"), _ptr(vals, u32, "vals"),
+                                 _ptr(tile_offsets, u32, "tile_offsets"), int(num_isects), _stream(stream))
+    if st not in (VKS_OK, VKS_ERR_UNSORTED):
+        _check("vks_bin_sort_check", st)
+    return st
 
 
 def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final,

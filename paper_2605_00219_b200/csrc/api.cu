@@ -21,7 +21,7 @@ int config_ok(const vks_config* c) {
     if (c->sh_degree < 0 || c->sh_degree > 3) return VKS_ERR_UNSUPPORTED;
     if (c->sh_coeffs < (c->sh_degree + 1) * (c->sh_degree + 1) || c->sh_coeffs > 64) return VKS_ERR_INVALID_ARG;
     if (c->footprint != VKS_FOOTPRINT_SUPPORT && c->footprint != VKS_FOOTPRINT_3SIGMA) return VKS_ERR_UNSUPPORTED;
-    if (c->flags & ~VKS_FLAG_GRAD_OVERWRITE) return VKS_ERR_UNSUPPORTED;
+    if (c->flags & ~(VKS_FLAG_GRAD_OVERWRITE | VKS_FLAG_VALIDATE)) return VKS_ERR_UNSUPPORTED;
     return VKS_OK;
 }
 
@@ -33,6 +33,31 @@ bool device_present() {
         return false;
     }
     return true;
+}
+
+bool validating(const vks_config* c) { return (c->flags & VKS_FLAG_VALIDATE) != 0; }
+
+// VKS_FLAG_VALIDATE: the Gaussian parameters are finite and the quaternions non-zero
+int check_params(int64_t n, int32_t sh_coeffs, const float* means, const float* log_scales, const float* quats,
+                 const float* opacity_logits, const float* sh, cudaStream_t s) {
+    int st = vks::validate_begin(s);
+    if (!st) st = vks::validate_finite(means, 3 * n, s);
+    if (!st) st = vks::validate_finite(log_scales, 3 * n, s);
+    if (!st) st = vks::validate_quats(quats, n, s);
+    if (!st) st = vks::validate_finite(opacity_logits, n, s);
+    if (!st) st = vks::validate_finite(sh, 3 * (int64_t)sh_coeffs * n, s);
+    return st ? st : vks::validate_end(s);
+}
+
+// the 2D gradients a projection backward consumes are finite
+int check_grads2d(int64_t n, const float* dmeans2d, const float* dconics, const float* dcolors,
+                  const float* dopacities, cudaStream_t s) {
+    int st = vks::validate_begin(s);
+    if (!st) st = vks::validate_finite(dmeans2d, 2 * n, s);
+    if (!st) st = vks::validate_finite(dconics, 3 * n, s);
+    if (!st) st = vks::validate_finite(dcolors, 3 * n, s);
+    if (!st) st = vks::validate_finite(dopacities, n, s);
+    return st ? st : vks::validate_end(s);
 }
 
 }  // namespace
@@ -47,6 +72,8 @@ const char* vks_status_string(int status) {
         case VKS_ERR_WORKSPACE: return "workspace too small";
         case VKS_ERR_CUDA: return "CUDA error";
         case VKS_ERR_UNSUPPORTED: return "unsupported configuration";
+        case VKS_ERR_NONFINITE: return "non-finite input (VKS_FLAG_VALIDATE)";
+        case VKS_ERR_UNSORTED: return "tile lists are not a sorted binning (VKS_FLAG_VALIDATE / vks_bin_sort_check)";
         default: return "unknown status";
     }
 }
@@ -69,6 +96,9 @@ int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, con
         (reinterpret_cast<uintptr_t>(radii) & 7))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
+    if (validating(cfg) && (st = check_params(n, cfg->sh_coeffs, means, log_scales, quats, opacity_logits, sh,
+                                              (cudaStream_t)stream)))
+        return st;
     return cuda_status(vks::launch_project_fwd(*cfg, *cam, n, means, log_scales, quats, opacity_logits, sh,
                                                means2d, conics, depths, radii, tiles_touched, colors,
                                                opacities, (cudaStream_t)stream));
@@ -98,6 +128,20 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
                                          workspace_bytes, (cudaStream_t)stream));
 }
 
+int vks_bin_sort_check(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
+                       const float* depths, const uint32_t* vals, const uint32_t* tile_offsets, int64_t num_isects,
+                       vks_stream_t stream) {
+    if (!camera_ok(cam) || n < 0 || num_isects < 0 || !tile_offsets) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means2d || !radii || !depths)) return VKS_ERR_INVALID_ARG;
+    if (num_isects > 0 && !vals) return VKS_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
+        return VKS_ERR_INVALID_ARG;
+    if (!device_present()) return VKS_ERR_CUDA;
+    int st = vks::validate_begin((cudaStream_t)stream);
+    if (!st) st = vks::validate_bins(*cam, n, means2d, radii, depths, vals, tile_offsets, num_isects, (cudaStream_t)stream);
+    return st ? st : vks::validate_end((cudaStream_t)stream);
+}
+
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
                    const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                    const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
@@ -110,6 +154,13 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
     if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
+    if (validating(cfg)) {  // the tile lists index [0, n) through a CSR (S:155 UnsortedInput)
+        st = vks::validate_begin((cudaStream_t)stream);
+        if (!st) st = vks::validate_csr(tile_offsets, vks::tiles_x(*cam) * vks::tiles_y(*cam), -1, vals, n,
+                                        (cudaStream_t)stream);
+        if (!st) st = vks::validate_end((cudaStream_t)stream);
+        if (st) return st;
+    }
     return cuda_status(vks::launch_raster_fwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
                                               tile_offsets, tile_order, image, T_final, n_contrib,
                                               (cudaStream_t)stream));
@@ -145,6 +196,14 @@ int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
     if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
+    if (validating(cfg)) {  // finite upstream gradient, tile lists a CSR over [0, n)
+        st = vks::validate_begin((cudaStream_t)stream);
+        if (!st) st = vks::validate_finite(dL_dimage, 3 * (int64_t)cam->width * cam->height, (cudaStream_t)stream);
+        if (!st) st = vks::validate_csr(tile_offsets, vks::tiles_x(*cam) * vks::tiles_y(*cam), -1, vals, n,
+                                        (cudaStream_t)stream);
+        if (!st) st = vks::validate_end((cudaStream_t)stream);
+        if (st) return st;
+    }
     return cuda_status(vks::launch_raster_bwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
                                               tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d,
                                               dconics,
@@ -167,6 +226,10 @@ int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, con
         (reinterpret_cast<uintptr_t>(dmeans2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
+    if (validating(cfg) &&
+        ((st = check_params(n, cfg->sh_coeffs, means, log_scales, quats, opacity_logits, sh, (cudaStream_t)stream)) ||
+         (st = check_grads2d(n, dmeans2d, dconics, dcolors, dopacities, (cudaStream_t)stream))))
+        return st;
     return cuda_status(vks::launch_project_bwd(*cfg, *cam, n, means, log_scales, quats, opacity_logits, sh, colors, radii,
                                                dmeans2d, dconics, dcolors, dopacities, dmeans, dlog_scales,
                                                dquats, dopacity_logits, dsh, (cudaStream_t)stream));
@@ -196,6 +259,9 @@ int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
     if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !opacities)) return VKS_ERR_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(quats) & 15) return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
+    if (validating(cfg) && (st = check_params(n, cfg->sh_coeffs, means, log_scales, quats, opacity_logits, sh,
+                                              (cudaStream_t)stream)))
+        return st;
     return cuda_status(vks::launch_project_fwd_batch(*cfg, n_views, cams, n, means, log_scales, quats, opacity_logits,
                                                      sh, means2d, conics, depths, radii, tiles_touched, colors,
                                                      opacities, g2d_zero, (cudaStream_t)stream));
@@ -225,6 +291,13 @@ int vks_project_bwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
     if ((reinterpret_cast<uintptr_t>(quats) & 15) || (reinterpret_cast<uintptr_t>(dquats) & 15))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
+    if (validating(cfg)) {
+        if ((st = check_params(n, cfg->sh_coeffs, means, log_scales, quats, opacity_logits, sh, (cudaStream_t)stream)))
+            return st;
+        for (int v = 0; v < n_views; v++)
+            if ((st = check_grads2d(n, dmeans2d[v], dconics[v], dcolors[v], dopacities[v], (cudaStream_t)stream)))
+                return st;
+    }
     return cuda_status(vks::launch_project_bwd_batch(*cfg, n_views, cams, n, means, log_scales, quats, opacity_logits,
                                                      sh, colors, radii, dmeans2d, dconics, dcolors, dopacities,
                                                      dmeans, dlog_scales, dquats, dopacity_logits, dsh,

@@ -25,6 +25,12 @@ namespace vks {
 namespace {
 
 
+int env_choice(const char* var, int dflt, int lo, int hi) {
+    const char* e = getenv(var);
+    const int v = e ? atoi(e) : dflt;
+    return (v >= lo && v <= hi) ? v : dflt;
+}
+
 // One warp's staged batch of 32 list entries (each warp walks the tile list on its own: no block
 // barriers, so a warp never waits for a slower one and stops as soon as its own pixels are done).
 struct WarpStage {  // all three arrays at a 16-byte stride: one address for the three loads
@@ -416,7 +422,8 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                                                                  const int* __restrict__ n_contrib,
                                                                  const float* __restrict__ dL_dimage,
                                                                  float* __restrict__ dmeans2d, float* __restrict__ dconics,
-                                                                 float* __restrict__ dcolors, float* __restrict__ dopac) {
+                                                                 float* __restrict__ dcolors, float* __restrict__ dopac,
+                                                                 int sparse_lanes) {
     __shared__ WarpStage stage[8 / PPT];
     extern __shared__ float4 dyn_smem[];  // RED = 1: one WarpRed per warp (dynamic: 8 warps need 48 KB)
     const int TX = tiles_x(cam);
@@ -538,7 +545,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 // sparse entries (<= 2 pixels-lanes of the warp composite): those lanes add their own
                 // terms (the outputs are linear in the sums), skipping the butterfly
                 const unsigned cl = __ballot_sync(VKS_FULL_MASK, contrib);
-                if (__popc(cl) <= 2) {
+                if (__popc(cl) <= sparse_lanes) {
                     if (contrib) {
                         const uint32_t id = __float_as_uint(Cc.y);
                         const float nrho = -B.y;
@@ -616,14 +623,8 @@ int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2
     raster_bwd_kernel<PPT, CULL, RED><<<n_tiles, 32 * 8 / PPT, dyn, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
         reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage,
-        dmeans2d, dconics, dcolors, dopacities);
+        dmeans2d, dconics, dcolors, dopacities, env_choice("VKS_RASTER_SPARSE", 2, 0, 32));
     return LaunchCheck::check();
-}
-
-int env_choice(const char* var, int dflt, int lo, int hi) {
-    const char* e = getenv(var);
-    const int v = e ? atoi(e) : dflt;
-    return (v >= lo && v <= hi) ? v : dflt;
 }
 
 // patch culling: ellipse by default (valid for both footprints); the box test needs the support

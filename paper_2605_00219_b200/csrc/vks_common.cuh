@@ -160,6 +160,16 @@ int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const 
                             const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                             const uint32_t* tile_offsets, const uint32_t* tile_order, unsigned long long* stats,
                             cudaStream_t s);
+// VKS_FLAG_VALIDATE checks (validate.cu): begin resets the status word, the checks enqueue,
+// end synchronises once and returns VKS_OK / VKS_ERR_NONFINITE / VKS_ERR_UNSORTED
+int validate_begin(cudaStream_t s);
+int validate_finite(const float* p, int64_t count, cudaStream_t s);
+int validate_quats(const float* q, int64_t n, cudaStream_t s);
+int validate_csr(const uint32_t* tile_offsets, int n_tiles, int64_t M, const uint32_t* vals, int64_t n,
+                 cudaStream_t s);
+int validate_bins(const vks_camera& cam, int64_t n, const float* means2d, const int32_t* radii, const float* depths,
+                  const uint32_t* vals, const uint32_t* tile_offsets, int64_t M, cudaStream_t s);
+int validate_end(cudaStream_t s);
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,

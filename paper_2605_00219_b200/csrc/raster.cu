@@ -1,5 +1,5 @@
 // raster.cu — "Rasterization Forward" and "Rasterization Backward";
-// DESIGN.md §4.3-4.4 and §6.
+// DESIGN.md §4.3-4.4 and §6.2.
 //
 // One block per 16x16 tile; each warp owns an 8 x 4*PPT pixel patch (PPT = 2 by default: 8x8,
 // two pixels per thread) and walks the tile's sorted list on its own in batches of 32 staged
@@ -9,14 +9,15 @@
 // patch with an exact test (the minimum of sigma over the patch rectangle against ln(255 rho));
 // the warp visits only entries that can composite somewhere in the patch (a finer per-8x4-band
 // test removed 20% of the evaluations but cost more instructions than it saved).  Forward and
-// backward evaluate
-// sigma / alpha through the SAME inline function, so skip / clamp / stop decisions replay
-// identically; sigma, alpha and the colour accumulation follow the pinned fp32 order of
-// DESIGN.md §4.3 (only exp differs from the oracle: ex2.approx here, expf there).  The backward
-// accumulates per (warp, Gaussian) the colour terms, sum(g) and the moments sum(g dx), sum(g dy),
-// sum(g dx^2), sum(g dx dy), sum(g dy^2) (g = G dalpha), reduces the 9 sums across the warp with
-// a transposed butterfly (14 shuffles instead of 45), turns the moments into the mean / conic
-// gradients with the Gaussian's conic, and issues one atomic per term from 9 lanes.
+// backward evaluate sigma / alpha through the SAME inline function, so skip / clamp / stop
+// decisions replay identically; sigma, alpha and the colour accumulation follow the pinned fp32
+// order of DESIGN.md §4.3 (only exp differs from the oracle: ex2.approx here, expf there).  The
+// backward accumulates per (warp, Gaussian) the colour terms, sum(g) and the moments sum(g dx),
+// sum(g dy), sum(g dx^2), sum(g dx dy), sum(g dy^2) (g = G dalpha).  An entry no lane composited
+// is skipped; an entry composited by at most 4 lanes (VKS_RASTER_SPARSE) is finished by those
+// lanes' own atomics (the outputs are linear in the sums); any other reduces its 9 sums across the
+// warp with a transposed butterfly (14 shuffles instead of 45), turns the moments into the mean /
+// conic gradients with the Gaussian's conic, and issues one atomic per term from 9 lanes.
 #include <stdlib.h>
 
 #include "vks_common.cuh"
@@ -325,90 +326,7 @@ __device__ __forceinline__ float warp_reduce_8plus1(const float v[8], float& e, 
     return c;
 }
 
-// Chunked cross-lane reduction of the backward (RED = 1): a warp writes each contributing entry's
-// nine per-lane partial sums (two pixels already summed in registers) to its own shared-memory
-// slot as three 16-byte words, and every kChunk entries (or at the end of a staged batch) reduces
-// the chunk at once: lane (j, s) = (lane / 8, lane % 8) sums entry j's partials of lanes s, s + 8,
-// s + 16, s + 24 (conflict-free 128-bit loads: 12-word lane slots), then an 8-lane transposed
-// butterfly (7 shuffles) leaves term s of entry j in lane s, which forms that term's output with
-// the entry's conic and issues one atomic (lane s = 0 also the opacity term).  The per-entry cost
-// is 3 shared stores plus a quarter of the chunk reduction, instead of a 32-lane butterfly of the
-// nine sums (19 shuffles, their selects and adds) and a per-entry epilogue.
-constexpr int kChunk = 4;
-int kCarveout = 100;  // percent of the unified L1 / shared memory given to shared memory (VKS_RASTER_CARVEOUT)
-struct WarpRed {
-    float4 p[kChunk][32][3];  // [slot][lane][m_x m_y m_xx m_xy | m_yy c0 c1 c2 | e - - -]
-};
-
-// the chunk's outputs: slot j < cnt holds stage entry (slots >> 5j) & 31
-__device__ __forceinline__ void flush_chunk(const WarpRed& red, const WarpStage& s, int cnt, uint32_t slots,
-                                            unsigned lane, float* __restrict__ dmeans2d, float* __restrict__ dconics,
-                                            float* __restrict__ dcolors, float* __restrict__ dopac) {
-    __syncwarp();
-    const int j = (int)(lane >> 3), sl = (int)(lane & 7);
-    float4 a0 = red.p[j][sl][0], a1 = red.p[j][sl][1];
-    float e = red.p[j][sl][2].x;
-#pragma unroll
-    for (int r = 1; r < 4; r++) {
-        const float4 b0 = red.p[j][sl + 8 * r][0], b1 = red.p[j][sl + 8 * r][1];
-        a0.x += b0.x; a0.y += b0.y; a0.z += b0.z; a0.w += b0.w;
-        a1.x += b1.x; a1.y += b1.y; a1.z += b1.z; a1.w += b1.w;
-        e += red.p[j][sl + 8 * r][2].x;
-    }
-    // 8-lane transposed butterfly: lane s ends with term s (bits of s select the kept halves)
-    float v[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-    float h4[4], h2[2];
-    bool hi = sl & 4;
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        const float send = hi ? v[i] : v[i + 4];
-        const float keep = hi ? v[i + 4] : v[i];
-        h4[i] = keep + __shfl_xor_sync(VKS_FULL_MASK, send, 4);
-    }
-    hi = sl & 2;
-#pragma unroll
-    for (int i = 0; i < 2; i++) {
-        const float send = hi ? h4[i] : h4[i + 2];
-        const float keep = hi ? h4[i + 2] : h4[i];
-        h2[i] = keep + __shfl_xor_sync(VKS_FULL_MASK, send, 2);
-    }
-    hi = sl & 1;
-    float r;
-    {
-        const float send = hi ? h2[0] : h2[1];
-        const float keep = hi ? h2[1] : h2[0];
-        r = keep + __shfl_xor_sync(VKS_FULL_MASK, send, 1);
-    }
-    e += __shfl_xor_sync(VKS_FULL_MASK, e, 4);
-    e += __shfl_xor_sync(VKS_FULL_MASK, e, 2);
-    e += __shfl_xor_sync(VKS_FULL_MASK, e, 1);
-    const float other = __shfl_xor_sync(VKS_FULL_MASK, r, 1);  // lanes s = 0 <-> 1: the two first moments
-    if (j < cnt) {
-        const int jj = (int)((slots >> (5 * j)) & 31u);
-        const float4 A = s.a[jj], B = s.b[jj];
-        const uint32_t id = __float_as_uint(s.c[jj].y);
-        // dmean = -rho (a m_x + b m_y, b m_x + c m_y), dconic = -rho (m_xx / 2, m_xy, m_yy / 2)
-        const float nrho = -B.y;
-        float out;
-        float* dst;
-        if (sl < 2) {
-            const float diag = sl == 0 ? 2.0f * A.z : 2.0f * B.x;
-            out = nrho * fmaf(diag, r, A.w * other);
-            dst = dmeans2d + 2 * (size_t)id + sl;
-        } else if (sl < 5) {
-            out = nrho * (sl == 3 ? r : 0.5f * r);
-            dst = dconics + 3 * (size_t)id + (sl - 2);
-        } else {
-            out = r;
-            dst = dcolors + 3 * (size_t)id + (sl - 5);
-        }
-        atomicAdd(dst, out);
-        if (sl == 0) atomicAdd(dopac + id, e);
-    }
-    __syncwarp();
-}
-
-template <int PPT, int CULL, int RED>
+template <int PPT, int CULL, int SPARSE>
 __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
@@ -425,12 +343,10 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                                                                  float* __restrict__ dcolors, float* __restrict__ dopac,
                                                                  int sparse_lanes) {
     __shared__ WarpStage stage[8 / PPT];
-    extern __shared__ float4 dyn_smem[];  // RED = 1: one WarpRed per warp (dynamic: 8 warps need 48 KB)
     const int TX = tiles_x(cam);
     const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
     const unsigned lane = threadIdx.x & 31;
     WarpStage& s = stage[threadIdx.x >> 5];
-    WarpRed& red = reinterpret_cast<WarpRed*>(dyn_smem)[RED == 1 ? threadIdx.x >> 5 : 0];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
@@ -457,7 +373,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
         lmax = max(lmax, last[k]);
     }
     const int wmax = __reduce_max_sync(VKS_FULL_MASK, lmax);  // positions >= wmax: nobody composited
-    // RED = 0: per-lane destination of gradient term k after the 32-lane butterfly: lane 4k (k < 8)
+    // per-lane destination of gradient term k after the 32-lane butterfly: lane 4k (k < 8)
     // owns term k, lane 1 the opacity term; dst(g) = base + g * stride
     const int myterm = (lane & 3) == 0 ? (int)(lane >> 2) : (lane == 1 ? 8 : -1);
     float* tbase = nullptr;
@@ -495,8 +411,6 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             if (p >= 0) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
             if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
         }
-        int cnt = 0;          // RED = 1: entries in the open chunk
-        uint32_t slots = 0;   // and their stage indices (5 bits each)
         while (live) {  // back to front over the entries whose support box meets the patch
             const int j = 31 - __clz(live);
             live &= ~(1u << j);
@@ -514,9 +428,9 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 okk[k] = eval_alpha(A, B, px, py[k], dx[k], dy[k], G[k], rG[k], alpha[k]) && pos < last[k];
                 contrib = contrib || okk[k];
             }
-            // RED >= 1: an entry no pixel of the warp composited leaves every T, P and accumulator
+            // SPARSE: an entry no pixel of the warp composited leaves every T, P and accumulator
             // unchanged, so the warp skips it
-            if (RED && !__any_sync(VKS_FULL_MASK, contrib)) continue;
+            if (SPARSE && !__any_sync(VKS_FULL_MASK, contrib)) continue;
             // v[0..4]: moments sum(g dx), sum(g dy), sum(g dx^2), sum(g dx dy), sum(g dy^2) with
             // g = G dalpha (dL/dsigma = -rho g); v[5..7]: colour; e = sum(g) (dL/drho)
             float v[8], e = 0.0f;
@@ -532,7 +446,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 const float cw = c0 * w0[k] + c1 * w1[k] + c2 * w2[k];
                 const float d = cw - P[k];
                 const float dalpha = T[k] * d;
-                P[k] = RED ? fmaf(a, d, P[k]) : a * cw + om * P[k];
+                P[k] = SPARSE ? fmaf(a, d, P[k]) : a * cw + om * P[k];
                 // no gradient where the pixel skipped the entry or alpha was clamped
                 const float g = (!ok || rG[k] > 0.99f) ? 0.0f : G[k] * dalpha;
                 const float gx = g * dx[k], gy = g * dy[k];
@@ -541,43 +455,24 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 for (int q = 0; q < 8; q++) v[q] = k == 0 ? t[q] : v[q] + t[q];
                 e = k == 0 ? g : e + g;
             }
-            if constexpr (RED == 3) {
-                // sparse entries (<= 2 pixels-lanes of the warp composite): those lanes add their own
-                // terms (the outputs are linear in the sums), skipping the butterfly
-                const unsigned cl = __ballot_sync(VKS_FULL_MASK, contrib);
-                if (__popc(cl) <= sparse_lanes) {
-                    if (contrib) {
-                        const uint32_t id = __float_as_uint(Cc.y);
-                        const float nrho = -B.y;
-                        atomicAdd(dmeans2d + 2 * (size_t)id, nrho * fmaf(2.0f * A.z, v[0], A.w * v[1]));
-                        atomicAdd(dmeans2d + 2 * (size_t)id + 1, nrho * fmaf(2.0f * B.x, v[1], A.w * v[0]));
-                        atomicAdd(dconics + 3 * (size_t)id, nrho * 0.5f * v[2]);
-                        atomicAdd(dconics + 3 * (size_t)id + 1, nrho * v[3]);
-                        atomicAdd(dconics + 3 * (size_t)id + 2, nrho * 0.5f * v[4]);
-                        atomicAdd(dcolors + 3 * (size_t)id, v[5]);
-                        atomicAdd(dcolors + 3 * (size_t)id + 1, v[6]);
-                        atomicAdd(dcolors + 3 * (size_t)id + 2, v[7]);
-                        atomicAdd(dopac + id, e);
-                    }
-                } else {
-                    const float r = warp_reduce_8plus1(v, e, lane);
-                    const float other = __shfl_xor_sync(VKS_FULL_MASK, r, 4);
+            // SPARSE: an entry composited by at most `sparse_lanes` lanes is reduced by those lanes'
+            // own atomics (the outputs are linear in the sums) instead of the 32-lane butterfly
+            const unsigned cl = __ballot_sync(VKS_FULL_MASK, contrib);
+            if (SPARSE && __popc(cl) <= sparse_lanes) {
+                if (contrib) {
+                    const uint32_t id = __float_as_uint(Cc.y);
                     const float nrho = -B.y;
-                    const float cr = fmaf(nrho, fmaf(kA, 2.0f * A.z, fmaf(kC, 2.0f * B.x, kH)), kOne);
-                    const float out = myterm == 8 ? e : fmaf(cr, r, (nrho * kB * A.w) * other);
-                    if (myterm >= 0) atomicAdd(tbase + (size_t)__float_as_uint(Cc.y) * tstride, out);
+                    atomicAdd(dmeans2d + 2 * (size_t)id, nrho * fmaf(2.0f * A.z, v[0], A.w * v[1]));
+                    atomicAdd(dmeans2d + 2 * (size_t)id + 1, nrho * fmaf(2.0f * B.x, v[1], A.w * v[0]));
+                    atomicAdd(dconics + 3 * (size_t)id, nrho * 0.5f * v[2]);
+                    atomicAdd(dconics + 3 * (size_t)id + 1, nrho * v[3]);
+                    atomicAdd(dconics + 3 * (size_t)id + 2, nrho * 0.5f * v[4]);
+                    atomicAdd(dcolors + 3 * (size_t)id, v[5]);
+                    atomicAdd(dcolors + 3 * (size_t)id + 1, v[6]);
+                    atomicAdd(dcolors + 3 * (size_t)id + 2, v[7]);
+                    atomicAdd(dopac + id, e);
                 }
-            } else if constexpr (RED == 1) {
-                red.p[cnt][lane][0] = make_float4(v[0], v[1], v[2], v[3]);
-                red.p[cnt][lane][1] = make_float4(v[4], v[5], v[6], v[7]);
-                red.p[cnt][lane][2].x = e;
-                slots |= (uint32_t)j << (5 * cnt);
-                if (++cnt == kChunk) {
-                    flush_chunk(red, s, cnt, slots, lane, dmeans2d, dconics, dcolors, dopac);
-                    cnt = 0;
-                    slots = 0;
-                }
-            } else if (__any_sync(VKS_FULL_MASK, contrib)) {
+            } else if (cl) {
                 const float r = warp_reduce_8plus1(v, e, lane);
                 const float other = __shfl_xor_sync(VKS_FULL_MASK, r, 4);  // lanes 0 <-> 4: the two first moments
                 // dmean = -rho (a m_x + b m_y, b m_x + c m_y), dconic = -rho (m_xx / 2, m_xy, m_yy / 2),
@@ -588,7 +483,6 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                 if (myterm >= 0) atomicAdd(tbase + (size_t)__float_as_uint(Cc.y) * tstride, out);
             }
         }
-        if (RED == 1 && cnt > 0) flush_chunk(red, s, cnt, slots, lane, dmeans2d, dconics, dcolors, dopac);
     }
 }
 
@@ -604,26 +498,17 @@ int launch_fwd(const vks_config& cfg, const vks_camera& cam, const float* means2
     return LaunchCheck::check();
 }
 
-template <int PPT, int CULL, int RED>
+template <int PPT, int CULL, int SPARSE>
 int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
                const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
-               float* dopacities, cudaStream_t st) {
+               float* dopacities, int sparse_lanes, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    const size_t dyn = RED == 1 ? sizeof(WarpRed) * (8 / PPT) : 0;
-    if (RED == 1) {  // per call: the attributes belong to the current device
-        cudaError_t e = cudaFuncSetAttribute(raster_bwd_kernel<PPT, CULL, RED>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        if (e == cudaSuccess)  // shared memory for 7 resident blocks (not the default L1-heavy split)
-            e = cudaFuncSetAttribute(raster_bwd_kernel<PPT, CULL, RED>,
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, kCarveout);
-        if (e != cudaSuccess) return cuda_fail(e, "raster_bwd smem attribute");
-    }
-    raster_bwd_kernel<PPT, CULL, RED><<<n_tiles, 32 * 8 / PPT, dyn, st>>>(
+    raster_bwd_kernel<PPT, CULL, SPARSE><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
         reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage,
-        dmeans2d, dconics, dcolors, dopacities, env_choice("VKS_RASTER_SPARSE", 2, 0, 32));
+        dmeans2d, dconics, dcolors, dopacities, sparse_lanes);
     return LaunchCheck::check();
 }
 
@@ -659,20 +544,20 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
                  const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
                  const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                  float* dopacities, cudaStream_t st) {
-    // cross-lane reduction: chunked through shared memory (1, default) or a 32-lane butterfly per entry (0)
-    const int red = env_choice("VKS_RASTER_BWD_RED", 2, 0, 3);
-    kCarveout = env_choice("VKS_RASTER_CARVEOUT", 50, 0, 100);
+    // SPARSE (default): skip entries no pixel of the warp composited, and reduce entries composited
+    // by <= VKS_RASTER_SPARSE lanes (default 4) with per-lane atomics; VKS_RASTER_BWD_SPARSE=0: the
+    // 32-lane butterfly for every entry (round-1 kernel, kept for A/B measurements)
+    const int sparse = env_choice("VKS_RASTER_BWD_SPARSE", 1, 0, 1);
+    const int lanes = env_choice("VKS_RASTER_SPARSE", 4, 0, 32);
 #define VKS_BWD_ARGS cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, \
-                     n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st
-#define VKS_BWD_CULL(R)                                                                  \
+                     n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, lanes, st
+#define VKS_BWD_CULL(SP)                                                                 \
     switch (cull) {                                                                      \
-        case kCullNone: return launch_bwd<PPT, kCullNone, R>(VKS_BWD_ARGS);              \
-        case kCullBox: return launch_bwd<PPT, kCullBox, R>(VKS_BWD_ARGS);                \
-        default: return launch_bwd<PPT, kCullEllipse, R>(VKS_BWD_ARGS);                  \
+        case kCullNone: return launch_bwd<PPT, kCullNone, SP>(VKS_BWD_ARGS);             \
+        case kCullBox: return launch_bwd<PPT, kCullBox, SP>(VKS_BWD_ARGS);               \
+        default: return launch_bwd<PPT, kCullEllipse, SP>(VKS_BWD_ARGS);                 \
     }
-    if (red == 1) VKS_BWD_CULL(1)
-    if (red == 2) VKS_BWD_CULL(2)
-    if (red == 3) VKS_BWD_CULL(3)
+    if (sparse) VKS_BWD_CULL(1)
     VKS_BWD_CULL(0)
 #undef VKS_BWD_CULL
 #undef VKS_BWD_ARGS

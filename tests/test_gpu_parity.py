@@ -321,6 +321,29 @@ def test_patch_culling_and_ppt_variants_agree(fp, monkeypatch):
     report(f"cull_fp{fp}", dict(stats={"/".join(k): v for k, v in stats.items()}))
 
 
+@pytest.mark.parametrize("lanes", ["0", "4", "32"])
+def test_raster_bwd_sparse_path_agrees(lanes, monkeypatch, oracle_lib):
+    """The raster backward's sparse-entry path (per-lane atomics for entries composited by few
+    lanes of a warp, skip of entries no lane composited) regroups the same sums: the 2D gradients
+    equal the butterfly-only kernel's up to summation order, and pass the P4 rule against the
+    oracle, with the threshold at 0 (never), 4 (default) and 32 (always)."""
+    s = synth.make_scene(200000, "indoor", 71)
+    cam = synth.ring_cameras(400, 300, "indoor", 8)[5]
+    cfg = synth.default_render_config()
+    _, ref, dL, _ = oracle_reference(oracle_lib, s, cam, cfg, synth.upstream_grad(300, 400, 6))
+    monkeypatch.setenv("VKS_RASTER_BWD_SPARSE", "0")
+    base = run_gpu(s, cam, cfg, dL=dL)
+    monkeypatch.setenv("VKS_RASTER_BWD_SPARSE", "1")
+    monkeypatch.setenv("VKS_RASTER_SPARSE", lanes)
+    g = run_gpu(s, cam, cfg, dL=dL)
+    for k in ("dmeans2d", "dconics", "dcolors", "dopacities"):
+        scale = np.abs(base[k]).max()
+        assert np.allclose(g[k], base[k], rtol=1e-4, atol=1e-6 * scale), (lanes, k)
+    cols = {"dmeans2d": [0, 1], "dconics": [2, 3, 4], "dcolors": [5, 6, 7], "dopacities": [8]}
+    for k, c in cols.items():
+        check_rule(f"sparse{lanes}", k, grad_rule(g[k], ref[k], ref["mass"][:, c].reshape(ref[k].shape)))
+
+
 @pytest.mark.parametrize("W,H", [(16, 16), (200, 150), (1600, 1000), (2000, 1600), (4200, 4000)])
 def test_binning_tile_pass_counts(oracle_lib, W, H):
     """Binning bit-exact for 1 tile (trivial pass), 130 tiles (one 8-bit pass), 6,300 and 12,500

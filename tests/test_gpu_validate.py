@@ -47,8 +47,9 @@ def test_validate_clean_inputs_pass_and_match(P):
     r0.backward(cfg, cam, p0, dLt)
     r1.backward(cfg_v, cam, p1, dLt)
     torch.cuda.synchronize()
-    assert torch.equal(r0.g2d, r1.g2d)
-    assert torch.equal(p0.grad_flat, p1.grad_flat)
+    # gradients: same computation, fp32 atomics sum in a run-dependent order
+    for a, b in ((r0.g2d, r1.g2d), (p0.grad_flat, p1.grad_flat)):
+        assert torch.allclose(a, b, rtol=1e-4, atol=1e-6 * float(a.abs().max()))
     assert P.vks_bin_sort_check(cam, r1.means2d, r1.radii, r1.depths, r1.vals, r1.tile_offsets,
                                 r1.num_isects) == P.VKS_OK
 

@@ -592,11 +592,11 @@ def run_ours(args):
                                  f"derived (no measured FP32 figure in MEASURED_PEAKS.json): 148 SM x 128 FP32 "
                                  f"lanes x 2 flop x {clock_mhz:.0f} MHz (median SM clock sampled in the timed "
                                  f"region)"))
-    # our kernels per view: bin_sort = id scan (3) + dpasses x (count, scan, scatter) + depth-order
-    # scan (3) + rect diff + tile count + tile passes x 3; raster fwd; raster bwd; plus one batched
+    # our kernels per view: bin_sort = id scan (2) + dpasses x (count, scan, scatter) + depth-order
+    # scan (2) + rect diff + tile count + tile passes x 3; raster fwd; raster bwd; plus one batched
     # project fwd and one chunked batched project bwd per step
     tp = max(1, ((rend.n_tiles - 1).bit_length() + 7) // 8)
-    gpu_launches = (((3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 1 + 1) * B + 1 + len(gsync.chunks() if world > 1
+    gpu_launches = (((2 + 3 * dpasses + 2 + 1 + 1 + 3 * tp) + 1 + 1) * B + 1 + len(gsync.chunks() if world > 1
                                                                                   else [0])) * args.steps
     if batch1 is not None:
         # stage rooflines of the single-view kernels (DESIGN.md §6.3 per-unit bytes): projection
@@ -618,7 +618,7 @@ def run_ours(args):
                               frac=round(tf / fp32_peak_tflops, 4))
         b1_roof["bin_sort"]["gkeys_per_s"] = round(m1 / (batch1["stages_ms"]["bin_sort"] * 1e-3) / 1e9, 3)
         batch1["stage_roofline"] = b1_roof
-        batch1["gpu_launches_per_iter"] = (3 + 3 * dpasses + 3 + 1 + 1 + 3 * tp) + 4
+        batch1["gpu_launches_per_iter"] = (2 + 3 * dpasses + 2 + 1 + 1 + 3 * tp) + 4
 
     out = dict(metric=METRIC, value=round(value, 3), unit="iters/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(elapsed_ms / args.steps, 4), higher_is_better=True,

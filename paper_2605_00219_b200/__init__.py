@@ -3,7 +3,8 @@ compositing and their backward as hand-written sm_100a CUDA kernels behind the C
 include/vks.h.  This package is the thin Python binding (`_vks`, same names as the C entry
 points) plus buffer orchestration (`pipeline`).  There is no CPU fallback: importing fails
 loudly when libvks.so is missing."""
-from ._vks import (ADAM_GROUPS, EXPORTS, FLAG_GRAD_OVERWRITE, FLAG_VALIDATE, VKS_ERR_NONFINITE, VKS_ERR_UNSORTED,
+from ._vks import (ADAM_GROUPS, EXPORTS, FLAG_GRAD_OVERWRITE, FLAG_VALIDATE, VKS_OK, VKS_ERR_NONFINITE, VKS_ERR_UNSORTED,
+                   VKS_ERR_CAPACITY, VKS_ERR_UNSUPPORTED,
                    vks_bin_sort_check, FOOTPRINT_3SIGMA, FOOTPRINT_SUPPORT,  # noqa: F401
                    VksError, exported_symbols, make_adam_config, make_camera, make_config, vks_adam_step, vks_bin_sort, vks_loss_grad,
                    vks_loss_workspace_bytes, vks_mcmc_noise, vks_mcmc_relocate, vks_mcmc_workspace_bytes,

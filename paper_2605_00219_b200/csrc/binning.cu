@@ -173,8 +173,8 @@ __device__ __forceinline__ int rect_tiles(u64 c) {
 // ------------------------------------------------------------------------------------------
 // 1./3. exclusive scans of tiles_touched, reduce-then-scan (no block waits on another):
 //   scan_reduce_kernel   per 4096-element block: sum (and number of visible Gaussians)
-//   scan_partials_kernel one block: exclusive scan of the block sums, totals
-//   scan_down_kernel     per block: rescan + block prefix -> output
+//   scan_down_kernel     per block: the block prefix (sum of the predecessors' block sums, read
+//                        by every block itself), rescan -> output; the last block writes totals
 // MODE 0: element i = tiles_touched[i];  MODE 1: element r = tiles of the depth-sorted rect code r.
 // Warp-striped layout: warp w of a block owns the 512 consecutive elements starting at
 // blockIdx.x * kScanTile + 512 w; lane l holds elements 32 j + l (j < 16), so every load and store
@@ -198,7 +198,7 @@ __device__ __forceinline__ void load_scan_items(const int* __restrict__ tiles, c
 // in id order, into (depth bits, id) pairs at their visible index (the input of the depth sort)
 // and reduces the depth-bit range.
 struct CompactOut {
-    const u32* vis_prefix;   // [blocks] exclusive block prefix of the visible counts
+    const u32* vis_prefix;   // [blocks] the reduce step's block visible counts
     const u32* depth_bits;   // [n]
     const float2* means2d;   // [n]
     const int2* radii;       // [n]
@@ -292,49 +292,6 @@ __global__ void __launch_bounds__(kDownThreads) scan_reduce_kernel(const int* __
     }
 }
 
-// exclusive scans of the P block sums (and block visible counts) in place; totals[0] = sum,
-// totals[1] = number of visible Gaussians
-__global__ void __launch_bounds__(1024) scan_partials_kernel(u32* __restrict__ part_sum, u32* __restrict__ part_vis,
-                                                            u32 P, u64* __restrict__ totals) {
-    __shared__ u32 s_w[32], s_v[32];
-    __shared__ u64 s_carry, s_vcarry;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) { s_carry = 0; s_vcarry = 0; }
-    __syncthreads();
-    for (u32 base = 0; base < P; base += 1024) {
-        const u32 i = base + tid;
-        const u32 c = i < P ? part_sum[i] : 0u;
-        const u32 cv = (i < P && part_vis) ? part_vis[i] : 0u;
-        u32 incl = c, vincl = cv;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const u32 t = __shfl_up_sync(VKS_FULL_MASK, incl, d);
-            const u32 tv = __shfl_up_sync(VKS_FULL_MASK, vincl, d);
-            if (lane >= d) { incl += t; vincl += tv; }
-        }
-        if (lane == 31) { s_w[warp] = incl; s_v[warp] = vincl; }
-        __syncthreads();
-        u32 wpre = 0, btot = 0, vpre = 0, vtot = 0;
-        for (int w = 0; w < 32; w++) {
-            if (w < warp) { wpre += s_w[w]; vpre += s_v[w]; }
-            btot += s_w[w];
-            vtot += s_v[w];
-        }
-        const u64 carry = s_carry, vcarry = s_vcarry;
-        if (i < P) {
-            part_sum[i] = (u32)(carry + wpre + incl - c);
-            if (part_vis) part_vis[i] = (u32)(vcarry + vpre + vincl - cv);
-        }
-        __syncthreads();
-        if (tid == 0) { s_carry = carry + btot; s_vcarry = vcarry + vtot; }
-        __syncthreads();
-    }
-    if (tid == 0) {
-        totals[0] = s_carry;
-        if (part_vis) totals[1] = s_vcarry;
-    }
-}
-
 // inclusive scan across the warp
 __device__ __forceinline__ u32 warp_incl_scan(u32 x, int lane) {
 #pragma unroll
@@ -358,13 +315,29 @@ __device__ __forceinline__ u32 warp_striped_excl(const int v[ITEMS], u32 out[ITE
     return carry;  // warp total
 }
 
+// The block's prefix is the sum of the block sums before it (part_sum / part_vis hold the reduce
+// step's raw block sums): every block sums its predecessors' sums itself (<= a few thousand u32
+// from L2), which replaces a single-block scan kernel and its launch between the two passes; the
+// last block writes the totals (M and the visible count) for the host.
 template <int MODE>
 __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __restrict__ tiles, const u64* __restrict__ rc,
-                                                                u64 count, const u32* __restrict__ part_prefix,
-                                                                u32* __restrict__ out, const CompactOut co) {
+                                                                u64 count, const u32* __restrict__ part_sum,
+                                                                u32* __restrict__ out, const CompactOut co,
+                                                                u64* __restrict__ totals) {
     constexpr int ITEMS = kDownItems;
     __shared__ u32 s_w[kDownThreads / 32], s_v[kDownThreads / 32];
+    __shared__ u32 s_pre[kDownThreads / 32], s_vpre[kDownThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {
+        u32 ps = 0, pv = 0;
+        for (u32 i = tid; i < blockIdx.x; i += kDownThreads) {
+            ps += __ldg(part_sum + i);
+            if (MODE == 0) pv += __ldg(co.vis_prefix + i);
+        }
+        ps = __reduce_add_sync(VKS_FULL_MASK, ps);
+        pv = __reduce_add_sync(VKS_FULL_MASK, pv);
+        if (lane == 0) { s_pre[warp] = ps; s_vpre[warp] = pv; }
+    }
     const u64 wbase = warp_base<ITEMS>(warp);
     int v[ITEMS];
     u32 ex[ITEMS];
@@ -383,10 +356,23 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
     }
     if (lane == 0) { s_w[warp] = wtot; s_v[warp] = wvis; }
     __syncthreads();
-    u32 pre = part_prefix[blockIdx.x], vpre = MODE == 0 ? co.vis_prefix[blockIdx.x] : 0u;
+    u32 pre = 0, vpre = 0, btot = 0, bvis = 0;
 #pragma unroll
-    for (int w = 0; w < kDownThreads / 32; w++)
+    for (int w = 0; w < kDownThreads / 32; w++) {
+        pre += s_pre[w];
+        vpre += s_vpre[w];
+    }
+    const u32 pre_blk = pre, vpre_blk = vpre;
+#pragma unroll
+    for (int w = 0; w < kDownThreads / 32; w++) {
         if (w < warp) { pre += s_w[w]; vpre += s_v[w]; }
+        btot += s_w[w];
+        bvis += s_v[w];
+    }
+    if (blockIdx.x == gridDim.x - 1 && tid == 0) {
+        totals[0] = (u64)pre_blk + btot;
+        if (MODE == 0) totals[1] = (u64)vpre_blk + bvis;
+    }
 #pragma unroll
     for (int j = 0; j < ITEMS; j++) {
         const u64 i = wbase + 32 * j + lane;
@@ -1271,9 +1257,8 @@ int run_scan(const int* tiles, const u64* rc_in, u64 count, u32* part_sum, u32* 
     if (!P) return VKS_OK;
     scan_reduce_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, MODE == 0 ? part_vis : nullptr,
                                                        co);
-    scan_partials_kernel<<<1, 1024, 0, s>>>(part_sum, MODE == 0 ? part_vis : nullptr, P, totals);
-    co.vis_prefix = part_vis;
-    scan_down_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co);
+    co.vis_prefix = part_vis;  // raw block visible counts; the down-sweep sums its predecessors'
+    scan_down_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co, totals);
     return check_launch(__func__);
 }
 

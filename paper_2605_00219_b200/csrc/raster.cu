@@ -37,7 +37,7 @@ int env_choice(const char* var, int dflt, int lo, int hi) {
 struct WarpStage {  // all three arrays at a 16-byte stride: one address for the three loads
     float4 a[32];    // u, v, 0.5*a, b
     float4 b[32];    // 0.5*c, rho, c0, c1
-    float4 c[32];    // c2, id (bits), -, -
+    float4 c[32];    // c2, id (bits), position in the batch (bits), -
 };
 
 struct Entry {  // one lane's gathered entry, in registers until it is stored to the stage
@@ -72,10 +72,12 @@ __device__ __forceinline__ Entry gather_entry(uint32_t g, const float2* __restri
     return e;
 }
 
-__device__ __forceinline__ void store_entry(WarpStage& s, int lane, const Entry& e) {
-    s.a[lane] = e.a;
-    s.b[lane] = e.b;
-    s.c[lane] = make_float4(e.c2, __uint_as_float(e.id), 0.0f, 0.0f);
+// the live entries of a batch are stored compacted (slot = rank among the live lanes), with
+// their position in the batch, so the visit loop is a plain counter over the slots
+__device__ __forceinline__ void store_entry(WarpStage& s, int slot, int lane, const Entry& e) {
+    s.a[slot] = e.a;
+    s.b[slot] = e.b;
+    s.c[slot] = make_float4(e.c2, __uint_as_float(e.id), __int_as_float(lane), 0.0f);
 }
 
 // sigma at one candidate point of the patch minus the bound on its fp32 evaluation error
@@ -217,17 +219,18 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
         __syncwarp();
         // each lane tests its own entry against the warp patch; the warp then visits, in list
         // order, only the entries that can composite somewhere in the patch
-        unsigned live = __ballot_sync(VKS_FULL_MASK, b + lane < end &&
-                                                         !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
-        if (b + lane < end) store_entry(s, lane, e_next);
+        const bool lv = b + lane < end && !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1);
+        const unsigned live = __ballot_sync(VKS_FULL_MASK, lv);
+        if (lv) store_entry(s, __popc(live & lanemask_lt()), lane, e_next);
         __syncwarp();
         if (b + 32 + lane < end) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
         if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
-        while (live) {
-            const int j = __ffs(live) - 1;
-            live &= live - 1;
-            const float4 A = s.a[j], B = s.b[j];
-            const float c2 = s.c[j].x;
+        const int nlive = __popc(live);
+        for (int q = 0; q < nlive; q++) {  // in list order
+            const float4 A = s.a[q], B = s.b[q];
+            const float4 Cq = s.c[q];
+            const float c2 = Cq.x;
+            const int j = __float_as_int(Cq.z);
             if constexpr (STATS) {
                 bool any = false;
 #pragma unroll
@@ -402,8 +405,9 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
         {
             const int p = bs + (int)lane;
             const bool ok = p >= 0 && p < wmax;
-            live = __ballot_sync(VKS_FULL_MASK, ok && !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1));
-            if (ok) store_entry(s, lane, e_next);
+            const bool lv = ok && !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1);
+            live = __ballot_sync(VKS_FULL_MASK, lv);
+            if (lv) store_entry(s, __popc(live & lanemask_lt()), lane, e_next);
         }
         __syncwarp();
         {
@@ -411,12 +415,10 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             if (p >= 0) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
             if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
         }
-        while (live) {  // back to front over the entries whose support box meets the patch
-            const int j = 31 - __clz(live);
-            live &= ~(1u << j);
-            const int pos = bs + j;
-            const float4 A = s.a[j], B = s.b[j];
-            const float4 Cc = s.c[j];
+        for (int q = __popc(live) - 1; q >= 0; q--) {  // back to front over the live entries
+            const float4 A = s.a[q], B = s.b[q];
+            const float4 Cc = s.c[q];
+            const int pos = bs + __float_as_int(Cc.z);
             const float c0 = B.z, c1 = B.w, c2 = Cc.x;
             // evaluate first: an entry no pixel of the warp composited leaves every T, P and
             // accumulator unchanged, so the warp skips it

@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvks.so")
+# VKS_DEBUG_CHECKS=1: the debug build with device-side bounds / invariant checks (_build.py)
+LIB_PATH = os.path.join(_HERE, "libvks_debug.so" if os.environ.get("VKS_DEBUG_CHECKS") == "1" else "libvks.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python paper_2605_00219_b200/_build.py` "

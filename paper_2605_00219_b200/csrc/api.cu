@@ -176,7 +176,7 @@ int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n
     if (n > 0 && (!means2d || !conics || !colors || !opacities || !radii)) return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
     return vks::launch_raster_fwd_stats(*cfg, *cam, means2d, conics, colors, opacities, radii, vals, tile_offsets,
-                                        tile_order, reinterpret_cast<unsigned long long*>(stats),
+                                        tile_order, reinterpret_cast<unsigned long long*>(stats), n,
                                         (cudaStream_t)stream);
 }
 

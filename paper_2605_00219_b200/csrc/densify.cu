@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(kDThreads) emit_kernel(int64_t n, int64_t n_ou
         }
         for (unsigned r = 0; r < rows; r++) {
             const int64_t oo = o0 + r;
+            VKS_DCHECK(oo >= 0 && oo < n_out);
             for (int c = 0; c < 4; c++) o.quats[4 * oo + c] = a.quats[4 * i + c];
             o.logits[oo] = a.logits[i];
             for (int c = 0; c < a.S; c++) o.sh[(int64_t)a.S * oo + c] = a.sh[(int64_t)a.S * i + c];

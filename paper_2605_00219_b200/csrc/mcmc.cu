@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kMThreads) sample_kernel(int64_t n, const floa
         const int64_t mid = lo + (hi - lo) / 2;
         if (__ldg(W + mid) > t) hi = mid; else lo = mid + 1;
     }
+    VKS_DCHECK(lo >= 0 && lo < n);
     target[i] = lo;
     atomicAdd(kcount + lo, 1u);
 }

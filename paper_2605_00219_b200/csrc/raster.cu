@@ -55,10 +55,12 @@ struct Entry {  // one lane's gathered entry, in registers until it is stored to
 enum { kCullNone = 0, kCullBox = 1, kCullEllipse = 2 };
 
 template <int CULL>
-__device__ __forceinline__ Entry gather_entry(uint32_t g, const float2* __restrict__ means2d,
+__device__ __forceinline__ Entry gather_entry(uint32_t g, uint32_t n, const float2* __restrict__ means2d,
                                               const float* __restrict__ conics, const float* __restrict__ colors,
                                               const float* __restrict__ opac, const int2* __restrict__ radii) {
     Entry e;
+    VKS_DCHECK(g < n);
+    (void)n;
     const float2 uv = __ldg(means2d + g);
     const float ca = __ldg(conics + 3 * (size_t)g), cb = __ldg(conics + 3 * (size_t)g + 1),
                 cc = __ldg(conics + 3 * (size_t)g + 2);
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                                                                  const uint32_t* __restrict__ tile_order,
                                                                  float* __restrict__ image, float* __restrict__ T_final,
                                                                  int* __restrict__ n_contrib,
-                                                                 unsigned long long* __restrict__ stats = nullptr) {
+                                                                 uint32_t n, unsigned long long* __restrict__ stats = nullptr) {
     __shared__ WarpStage stage[8 / PPT];
     unsigned long long n_eval = 0, n_comp = 0, n_went = 0, n_wcomp = 0;
     const int TX = tiles_x(cam);
@@ -206,10 +208,11 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
         last[k] = 0;
     }
     const uint32_t start = tile_offsets[tile], end = tile_offsets[tile + 1];
+    VKS_DCHECK(start <= end);
     // software pipeline: ids two batches ahead, gathered entries one batch ahead
     uint32_t id_next = (start + lane < end) ? __ldg(vals + start + lane) : 0u;
     Entry e_next;
-    if (start + lane < end) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
+    if (start + lane < end) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
     id_next = (start + 32 + lane < end) ? __ldg(vals + start + 32 + lane) : 0u;
     for (uint32_t b = start; b < end; b += 32) {
         bool all_done = true;
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
         const unsigned live = __ballot_sync(VKS_FULL_MASK, lv);
         if (lv) store_entry(s, __popc(live & lanemask_lt()), lane, e_next);
         __syncwarp();
-        if (b + 32 + lane < end) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
+        if (b + 32 + lane < end) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
         if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
         const int nlive = __popc(live);
         for (int q = 0; q < nlive; q++) {  // in list order
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                                                                  const float* __restrict__ dL_dimage,
                                                                  float* __restrict__ dmeans2d, float* __restrict__ dconics,
                                                                  float* __restrict__ dcolors, float* __restrict__ dopac,
-                                                                 int sparse_lanes) {
+                                                                 int sparse_lanes, uint32_t n) {
     __shared__ WarpStage stage[8 / PPT];
     const int TX = tiles_x(cam);
     const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
@@ -353,6 +356,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
+    VKS_DCHECK(start <= tile_offsets[tile + 1]);
     // per pixel: P = <S, w> where S is the colour composited behind the current entry (bg first):
     // dalpha only needs <c - S, w>, and <S, w> updates as P <- alpha <c, w> + (1 - alpha) P
     float py[PPT], T[PPT], w0[PPT], w1[PPT], w2[PPT], P[PPT];
@@ -396,7 +400,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     int p0 = bs + (int)lane;
     uint32_t id_next = (p0 >= 0 && p0 < wmax) ? __ldg(vals + start + p0) : 0u;
     Entry e_next;
-    if (p0 >= 0 && p0 < wmax) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
+    if (p0 >= 0 && p0 < wmax) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
     p0 -= 32;
     id_next = (p0 >= 0) ? __ldg(vals + start + p0) : 0u;
     for (; bs > -32; bs -= 32) {
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
         __syncwarp();
         {
             const int p = bs - 32 + (int)lane;
-            if (p >= 0) e_next = gather_entry<CULL>(id_next, means2d, conics, colors, opac, radii);
+            if (p >= 0) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
             if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
         }
         for (int q = __popc(live) - 1; q >= 0; q--) {  // back to front over the live entries
@@ -492,11 +496,11 @@ template <int PPT, int CULL>
 int launch_fwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                const uint32_t* tile_offsets, const uint32_t* tile_order, float* image, float* T_final,
-               int32_t* n_contrib, cudaStream_t st) {
+               int32_t* n_contrib, uint32_t n, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     raster_fwd_kernel<PPT, CULL><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
-        reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, image, T_final, n_contrib);
+        reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, image, T_final, n_contrib, n);
     return LaunchCheck::check();
 }
 
@@ -505,12 +509,12 @@ int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2
                const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
                const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
-               float* dopacities, int sparse_lanes, cudaStream_t st) {
+               float* dopacities, int sparse_lanes, uint32_t n, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     raster_bwd_kernel<PPT, CULL, SPARSE><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
         reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage,
-        dmeans2d, dconics, dcolors, dopacities, sparse_lanes);
+        dmeans2d, dconics, dcolors, dopacities, sparse_lanes, n);
     return LaunchCheck::check();
 }
 
@@ -532,11 +536,11 @@ template <int PPT>
 int dispatch_fwd(int cull, const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                  const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                  const uint32_t* tile_offsets, const uint32_t* tile_order, float* image, float* T_final,
-                 int32_t* n_contrib, cudaStream_t st) {
+                 int32_t* n_contrib, uint32_t n, cudaStream_t st) {
     switch (cull) {
-        case kCullNone: return launch_fwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
-        case kCullBox: return launch_fwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
-        default: return launch_fwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
+        case kCullNone: return launch_fwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
+        case kCullBox: return launch_fwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
+        default: return launch_fwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
     }
 }
 
@@ -545,14 +549,14 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
                  const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                  const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
                  const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
-                 float* dopacities, cudaStream_t st) {
+                 float* dopacities, uint32_t n, cudaStream_t st) {
     // SPARSE (default): skip entries no pixel of the warp composited, and reduce entries composited
     // by <= VKS_RASTER_SPARSE lanes (default 4) with per-lane atomics; VKS_RASTER_BWD_SPARSE=0: the
     // 32-lane butterfly for every entry (round-1 kernel, kept for A/B measurements)
     const int sparse = env_choice("VKS_RASTER_BWD_SPARSE", 1, 0, 1);
     const int lanes = env_choice("VKS_RASTER_SPARSE", 4, 0, 32);
 #define VKS_BWD_ARGS cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, \
-                     n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, lanes, st
+                     n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, lanes, n, st
 #define VKS_BWD_CULL(SP)                                                                 \
     switch (cull) {                                                                      \
         case kCullNone: return launch_bwd<PPT, kCullNone, SP>(VKS_BWD_ARGS);             \
@@ -570,22 +574,22 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
 int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                             const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                             const uint32_t* tile_offsets, const uint32_t* tile_order, unsigned long long* stats,
-                            cudaStream_t st) {
+                            int64_t n, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     const auto m2 = reinterpret_cast<const float2*>(means2d);
     const auto r2 = reinterpret_cast<const int2*>(radii);
     switch (cull_choice(cfg)) {
         case kCullNone:
             raster_fwd_kernel<2, kCullNone, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                           vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, stats);
+                                                                           vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, (uint32_t)n, stats);
             break;
         case kCullBox:
             raster_fwd_kernel<2, kCullBox, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                          vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, stats);
+                                                                          vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, (uint32_t)n, stats);
             break;
         default:
             raster_fwd_kernel<2, kCullEllipse, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                              vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, stats);
+                                                                              vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, (uint32_t)n, stats);
     }
     return LaunchCheck::check();
 }
@@ -594,12 +598,11 @@ int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
                       float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
-    (void)n;
     const int ppt = ppt_choice("VKS_RASTER_FWD_PPT");
     const int cull = cull_choice(cfg);
-    if (ppt == 4) return dispatch_fwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
-    if (ppt == 1) return dispatch_fwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
-    return dispatch_fwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, st);
+    if (ppt == 4) return dispatch_fwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
+    if (ppt == 1) return dispatch_fwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
+    return dispatch_fwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
 }
 
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
@@ -607,12 +610,11 @@ int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
                       const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
                       const float* T_final, const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
                       float* dconics, float* dcolors, float* dopacities, cudaStream_t st) {
-    (void)n;
     const int ppt = ppt_choice("VKS_RASTER_BWD_PPT");
     const int cull = cull_choice(cfg);
-    if (ppt == 4) return dispatch_bwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-    if (ppt == 1) return dispatch_bwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
-    return dispatch_bwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, st);
+    if (ppt == 4) return dispatch_bwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, (uint32_t)n, st);
+    if (ppt == 1) return dispatch_bwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, (uint32_t)n, st);
+    return dispatch_bwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, (uint32_t)n, st);
 }
 
 }  // namespace vks

@@ -8,6 +8,22 @@
 
 #define VKS_FULL_MASK 0xffffffffu
 
+// Debug build (libvks_debug.so, -DVKS_DEBUG_CHECKS; the stand-in for compute-sanitizer, which this
+// pool does not run): device-side bounds / invariant checks at the indexed memory accesses of the
+// kernels; a failed check prints its location and traps (the launch's stream reports an error).
+#ifdef VKS_DEBUG_CHECKS
+#define VKS_DCHECK(cond)                                                                          \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("VKS_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,        \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                  \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define VKS_DCHECK(cond) ((void)0)
+#endif
+
 namespace vks {
 
 constexpr int kTile = 16;
@@ -159,7 +175,7 @@ int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
 int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                             const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                             const uint32_t* tile_offsets, const uint32_t* tile_order, unsigned long long* stats,
-                            cudaStream_t s);
+                            int64_t n, cudaStream_t s);
 // VKS_FLAG_VALIDATE checks (validate.cu): begin resets the status word, the checks enqueue,
 // end synchronises once and returns VKS_OK / VKS_ERR_NONFINITE / VKS_ERR_UNSORTED
 int validate_begin(cudaStream_t s);

@@ -1,5 +1,6 @@
-"""Every kernel of libvks once, for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
-usage: python tools/sanitize_driver.py [config] [n_override]
+"""Every kernel of libvks once: for compute-sanitizer where it runs, and with VKS_DEBUG_CHECKS=1
+(libvks_debug.so: device-side bounds / invariant checks that trap) where it does not
+(tests/test_gpu_debug_checks.py).  usage: python tools/sanitize_driver.py [config] [n_override]
 
 Runs on one view of the config: the single-view and batched projection forward, bin sort (with the
 debug unsorted keys), vks_bin_sort_check, raster forward (+ stats), raster backward (sparse-entry and
@@ -76,4 +77,5 @@ dst = [torch.empty((2 * params.n,) + tuple(t.shape[1:]), device="cuda") for t in
 dws = torch.empty(P.vks_densify_workspace_bytes(params.n), dtype=torch.uint8, device="cuda")
 n_new = P.vks_densify(groups, acc, den, dst, dws, 1e-4, 0.05, 0.005, seed=1)
 torch.cuda.synchronize()
-print(f"sanitize driver ok: {name} n={params.n} M={r.num_isects} densified to {n_new}")
+print(f"sanitize driver ok: {name} n={params.n} M={r.num_isects} densified to {n_new} "
+      f"lib={os.path.basename(P._vks.LIB_PATH)}")

@@ -13,8 +13,11 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# VKS_DEBUG_CHECKS=1: the debug build with device-side bounds / invariant checks (_build.py)
-LIB_PATH = os.path.join(_HERE, "libvks_debug.so" if os.environ.get("VKS_DEBUG_CHECKS") == "1" else "libvks.so")
+# VKS_DEBUG_CHECKS=1: the debug build with device-side bounds / invariant checks (_build.py);
+# VKS_LIB_VARIANT=<name>: libvks_<name>.so, an in-tree build variant (measurement experiments)
+_variant = os.environ.get("VKS_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, "libvks_debug.so" if os.environ.get("VKS_DEBUG_CHECKS") == "1" else
+                        (f"libvks_{_variant}.so" if _variant else "libvks.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python paper_2605_00219_b200/_build.py` "

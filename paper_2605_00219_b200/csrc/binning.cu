@@ -854,7 +854,7 @@ __device__ __forceinline__ void rank_and_store(SortSmem<1 << DBITS>& S, u32 n, i
     for (int j = tid; j < kSortTile; j += kSortThreads) {
         const u32 key = S.keys[j];
         const u32 dest = S.gbase[((key - kbias) >> shift) & DMASK] + (u32)j;
-        VKS_DCHECK(dest < n || key == 0xFFFFFFFFu);  // only the last block's pads fall past n
+        VKS_DCHECK(dest < n || key - kbias == 0xFFFFFFFFu);  // only the last block's pads (key kbias - 1) fall past n
         if (dest < n) {
             const u32 val = S.vals[j];
             if (MODE != kPassTileLast) kout[dest] = key;
@@ -1102,7 +1102,7 @@ __global__ void __launch_bounds__(kSortThreads, 5) keys_scatter_kernel(const Exp
     const u32 c1 = min(c0 + 32u * kSortItems, src.M);
     if (c0 < c1)
         expand_chunk(src, b, c0, c1, [&](u32 slot, u32 tile, u32 id) {
-            VKS_DCHECK(slot >= S0 && slot - S0 < (u32)kSortTile && id < src.V + 0xFFFFFFFFu && tile < (u32)(1 << 24));
+            VKS_DCHECK(slot >= S0 && slot - S0 < (u32)kSortTile && tile < (u32)(1 << 24));
             S.keys[slot - S0] = tile;
             S.vals[slot - S0] = id;
         });

@@ -38,7 +38,7 @@ for sparse in ("1", "0"):
     os.environ["VKS_RASTER_BWD_SPARSE"] = sparse
     r.backward(dict(cfg, flags=P.FLAG_VALIDATE), cam, params, dL, accumulate=False)
 # batched projection (2 views) + backward
-views = [P.ViewRenderer(params.n, c.width, c.height) for _ in range(2)]
+views = [P.ViewRenderer(params.n, c.width, c.height, capacity=2 * r.capacity) for _ in range(2)]
 vc = cams[:2]
 P.vks_project_fwd_batch(cfg, vc, params.means, params.log_scales, params.quats, params.opacity_logits, params.sh,
                         [v.means2d for v in views], [v.conics for v in views], [v.depths for v in views],

@@ -1233,7 +1233,7 @@ __device__ __forceinline__ void tsort_pass(const u32* kin, const u32* iin, u32* 
     }
     const u32 ltmask = lanemask_lt();
     for (u32 base = 0; base < L; base += kTSortSub) {
-        for (int j = tid; j < kTSortWarps * RADIX; j += kTSortThreads) (&s_whist[0][0])[j] = 0;
+        for (int j = tid; j < kTSortWarps * RADIX; j += kTSortThreads) s_whist[j / RADIX][j % RADIX] = 0;
         __syncthreads();
         u32 kk[8], ii[8], rank[8];
         const u32 wb = base + (u32)warp * 256;

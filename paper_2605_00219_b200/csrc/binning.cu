@@ -88,10 +88,7 @@ constexpr int kPasses = kDepthPasses + kMaxTilePasses;
 struct Workspace {
     u32 *dk[2], *dv[2];  // depth sort ping-pong [n]
     u32* doff;           // depth-order slot offsets [n]
-    u32 *tk[2], *tv[2];  // tile sort ping-pong [capacity] (depth-major path)
-    u64* list;           // [capacity] (depth bits << 32 | id) in tile buckets (tile-major path; aliases tk/tv)
-    u32* tscratch;       // [4 * capacity] per-tile sort buffers of lists longer than shared memory holds
-    u32* order_ws;       // [n_tiles] tile schedule when the caller passes none
+    u32 *tk[2], *tv[2];  // tile sort ping-pong [capacity]
     u32* counts;         // [256 * sort tiles] digit counts of the current pass (digit-major)
     u32* offs;           // its exclusive scan
     u64* rcs;            // [n] tile-rect codes in depth order
@@ -104,7 +101,6 @@ struct Workspace {
     u32* ctr;            // [16] scan tile counters
     u64* totals;         // [3]: M, V, depth-bit range of the visible (2 x u32)
     int* diff;           // [(TY+1)*(TX+1)]
-    u32* gcursor;        // [n_tiles] tile-major fill: keys reserved per tile so far
     size_t zeroA_bytes;
     char* zeroA;
     size_t bytes;
@@ -124,18 +120,10 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
         w.dv[i] = reinterpret_cast<u32*>(take(4 * nn));
     }
     w.doff = reinterpret_cast<u32*>(take(4 * nn));
-    {   // one region for both paths: the depth-major tile passes' ping-pong buffers, or the
-        // tile-major path's bucketed list (8 B per key) followed by its big-tile sort buffers
-        char* region = take(24 * cap);
-        const size_t q = align_up(4 * cap);
-        for (int i = 0; i < 2; i++) {
-            w.tk[i] = reinterpret_cast<u32*>(region ? region + (2 * i) * q : nullptr);
-            w.tv[i] = reinterpret_cast<u32*>(region ? region + (2 * i + 1) * q : nullptr);
-        }
-        w.list = reinterpret_cast<u64*>(region);
-        w.tscratch = reinterpret_cast<u32*>(region ? region + align_up(8 * cap) : nullptr);
+    for (int i = 0; i < 2; i++) {
+        w.tk[i] = reinterpret_cast<u32*>(take(4 * cap));
+        w.tv[i] = reinterpret_cast<u32*>(take(4 * cap));
     }
-    w.order_ws = reinterpret_cast<u32*>(take(4 * (size_t)TX * TY));
     w.counts = reinterpret_cast<u32*>(take(4 * kMaxRadix * sort_tiles));
     w.offs = reinterpret_cast<u32*>(take(4 * kMaxRadix * sort_tiles));
     w.rcs = reinterpret_cast<u64*>(take(8 * nn));
@@ -149,7 +137,6 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
     w.ctr = reinterpret_cast<u32*>(take(4 * 16));
     w.totals = reinterpret_cast<u64*>(take(8 * 3));  // M, V, (u32 max ~depth bits, u32 max depth bits)
     w.diff = reinterpret_cast<int*>(take(4 * (size_t)(TX + 1) * (TY + 1)));
-    w.gcursor = reinterpret_cast<u32*>(take(4 * (size_t)TX * TY));
     w.zeroA_bytes = off - a0;
     w.bytes = off;
     return w;
@@ -465,7 +452,6 @@ __global__ void __launch_bounds__(kDiffThreads) rect_diff_kernel(int TX, int TY,
 #pragma unroll
         for (int q = 0; q < U; q++) {
             if (r0 + q * stride >= count) break;
-            if (!c[q]) continue;  // culled (rect codes by id): an empty rect
             int x0, x1, y0, y1;
             unpack_rect(c[q], x0, x1, y0, y1);
             VKS_DCHECK(x0 <= x1 && x1 <= TX && y0 <= y1 && y1 <= TY);
@@ -1124,311 +1110,6 @@ __global__ void __launch_bounds__(kSortThreads, 5) keys_scatter_kernel(const Exp
     rank_and_store<DBITS, MODE>(S, src.M, shift, 0u, kout, vout, depths, keys64);
 }
 
-// ------------------------------------------------------------------------------------------
-// 7. Tile-major binning (default when the tile grid fits the fill kernel's shared-memory cursors):
-// the depth sort over V and the tile passes over M are replaced by
-//   tile_fill_kernel   per chunk of 2048 visible Gaussians (id order): per-tile key counts in
-//                      shared memory, one global atomic per (chunk, tile) reserving a range of the
-//                      tile's list (tile_offsets from the difference array), then every key
-//                      (depth bits << 32 | id) written into its tile's range — in no particular order;
-//   tile_sort_kernel   per tile (heaviest first): a stable LSD radix sort of the list by the depth
-//                      bits, digits of <= 8 bits over the bits the tile's depth range needs, in
-//                      shared memory (lists <= 16384 keys) or L2-resident global scratch (longer),
-//                      then equal-depth runs ordered by id, and the ids (and keys) written out.
-// The result is the same unique order, ascending (tile, depth bits, id) = the stable sort of the
-// (tile | depth) keys in id-order slots; P2 checks it bit-exactly.
-constexpr int kFillThreads = 512;
-constexpr int kFillPer = 4;
-constexpr int kFillChunk = kFillThreads * kFillPer;
-constexpr int kFillMaxTiles = 16384;  // shared-memory cursors: 64 KB
-constexpr int kTSortThreads = 512;
-constexpr int kTSortWarps = kTSortThreads / 32;
-constexpr int kTSortSub = kTSortThreads * 8;  // keys ranked per sub-block (8 per thread)
-constexpr int kTSortSmall = 4096;             // list lengths of the shared-memory variants
-constexpr int kTSortMid = 12288;               // 4 u32 per key + 17 KB: <= 227 KB
-
-__global__ void __launch_bounds__(kFillThreads) tile_fill_kernel(u32 V, const u32* __restrict__ vids,
-                                                                const u32* __restrict__ vkeys,
-                                                                const u64* __restrict__ rc_by_id, int TX, int n_tiles,
-                                                                const u32* __restrict__ tile_offsets,
-                                                                u32* __restrict__ gcursor, u64* __restrict__ list) {
-    extern __shared__ u32 s_cur[];
-    const int tid = threadIdx.x;
-    for (int t = tid; t < n_tiles; t += kFillThreads) s_cur[t] = 0;
-    u64 rc[kFillPer];
-    u64 key[kFillPer];
-#pragma unroll
-    for (int q = 0; q < kFillPer; q++) {
-        const u32 i = blockIdx.x * (u32)kFillChunk + (u32)(q * kFillThreads + tid);
-        rc[q] = 0;
-        key[q] = 0;
-        if (i < V) {
-            const u32 g = __ldg(vids + i);
-            rc[q] = __ldg(rc_by_id + g);
-            key[q] = ((u64)__ldg(vkeys + i) << 32) | g;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kFillPer; q++) {
-        int x0, x1, y0, y1;
-        unpack_rect(rc[q], x0, x1, y0, y1);
-        for (int y = y0; y < y1; y++)
-            for (int x = x0; x < x1; x++) atomicAdd(&s_cur[y * TX + x], 1u);
-    }
-    __syncthreads();
-    for (int t = tid; t < n_tiles; t += kFillThreads) {
-        const u32 c = s_cur[t];
-        if (c) s_cur[t] = __ldg(tile_offsets + t) + atomicAdd(gcursor + t, c);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kFillPer; q++) {
-        int x0, x1, y0, y1;
-        unpack_rect(rc[q], x0, x1, y0, y1);
-        for (int y = y0; y < y1; y++)
-            for (int x = x0; x < x1; x++) {
-                const u32 slot = atomicAdd(&s_cur[y * TX + x], 1u);
-                VKS_DCHECK(slot < __ldg(tile_offsets + y * TX + x + 1));
-                list[slot] = key[q];
-            }
-    }
-}
-
-// one stable counting pass of L (key, index) pairs by digit (key - kbias) >> shift & (2^DB - 1):
-// histogram, exclusive scan, then sub-blocks of 4096 in order, each warp ranking its 256
-// consecutive pairs (warp-striped: pair base + 32 r + lane) with ballot multi-split, a block
-// prefix over the warps per digit, and a running base per digit across the sub-blocks
-template <int DB>
-__device__ __forceinline__ void tsort_pass(const u32* kin, const u32* iin, u32* kout, u32* iout, u32 L, int shift,
-                                           u32 kbias, u32* s_run, u32 (*s_whist)[256]) {
-    constexpr int RADIX = 1 << DB;
-    constexpr u32 DMASK = RADIX - 1;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int d = tid; d < RADIX; d += kTSortThreads) s_run[d] = 0;
-    __syncthreads();
-    for (u32 j = tid; j < L; j += kTSortThreads) atomicAdd(&s_run[((kin[j] - kbias) >> shift) & DMASK], 1u);
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of the RADIX counts (RADIX <= 256: 8 per lane)
-        u32 v[8], tot = 0;
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const int d = lane * 8 + q;
-            v[q] = d < RADIX ? s_run[d] : 0u;
-            tot += v[q];
-        }
-        u32 incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const u32 t = __shfl_up_sync(VKS_FULL_MASK, incl, o);
-            if (lane >= o) incl += t;
-        }
-        u32 run = incl - tot;
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const int d = lane * 8 + q;
-            if (d < RADIX) s_run[d] = run;
-            run += v[q];
-        }
-    }
-    const u32 ltmask = lanemask_lt();
-    for (u32 base = 0; base < L; base += kTSortSub) {
-        for (int j = tid; j < kTSortWarps * RADIX; j += kTSortThreads) s_whist[j / RADIX][j % RADIX] = 0;
-        __syncthreads();
-        u32 kk[8], ii[8], rank[8];
-        const u32 wb = base + (u32)warp * 256;
-#pragma unroll
-        for (int r = 0; r < 8; r++) {
-            const u32 e = wb + 32 * r + lane;
-            const bool ok = e < L;
-            kk[r] = ok ? kin[e] : 0u;
-            ii[r] = ok ? iin[e] : 0u;
-            const u32 d = ((kk[r] - kbias) >> shift) & DMASK;
-            const u32 peers = digit_peers<DB>(d, ok);
-            const u32 below = __popc(peers & ltmask);
-            const u32 before = s_whist[warp][d];
-            rank[r] = before + below;
-            __syncwarp();
-            if (ok && below == 0) s_whist[warp][d] = before + __popc(peers);
-            __syncwarp();
-        }
-        __syncthreads();
-        // per digit: exclusive prefix over the warps, added to the running base; advance the base
-        for (int d = tid; d < RADIX; d += kTSortThreads) {
-            u32 run = s_run[d];
-#pragma unroll
-            for (int w = 0; w < kTSortWarps; w++) {
-                const u32 c = s_whist[w][d];
-                s_whist[w][d] = run;
-                run += c;
-            }
-            s_run[d] = run;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < 8; r++) {
-            const u32 e = wb + 32 * r + lane;
-            if (e < L) {
-                const u32 d = ((kk[r] - kbias) >> shift) & DMASK;
-                const u32 dst = s_whist[warp][d] + rank[r];
-                kout[dst] = kk[r];
-                iout[dst] = ii[r];
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// stable LSD sort of the L (key, index) pairs in (k0, i0) over the significant bits of the key
-// range, digits of <= 8 bits; on return (k0, i0) hold the result (the buffers are swapped per pass)
-__device__ __forceinline__ void tsort_passes(u32*& k0, u32*& i0, u32*& k1, u32*& i1, u32 L, u32* s_run,
-                                             u32 (*s_whist)[256], u32* s_mm) {
-    const int tid = threadIdx.x;
-    if (tid == 0) { s_mm[0] = 0xFFFFFFFFu; s_mm[1] = 0u; }
-    __syncthreads();
-    u32 mn = 0xFFFFFFFFu, mx = 0u;
-    for (u32 j = tid; j < L; j += kTSortThreads) {
-        mn = min(mn, k0[j]);
-        mx = max(mx, k0[j]);
-    }
-    mn = __reduce_min_sync(VKS_FULL_MASK, mn);
-    mx = __reduce_max_sync(VKS_FULL_MASK, mx);
-    if ((tid & 31) == 0) { atomicMin(&s_mm[0], mn); atomicMax(&s_mm[1], mx); }
-    __syncthreads();
-    const u32 kbias = s_mm[0], range = s_mm[1] - s_mm[0];
-    const int sig = range ? 32 - __clz(range) : 0;
-    const int passes = (sig + 7) / 8;
-    const int db = passes ? (sig + passes - 1) / passes : 0;
-    for (int p = 0; p < passes; p++) {
-        const int shift = db * p;
-        switch (db) {  // block-uniform
-            case 1: tsort_pass<1>(k0, i0, k1, i1, L, shift, kbias, s_run, s_whist); break;
-            case 2: tsort_pass<2>(k0, i0, k1, i1, L, shift, kbias, s_run, s_whist); break;
-            case 3: tsort_pass<3>(k0, i0, k1, i1, L, shift, kbias, s_run, s_whist); break;
-            case 4: tsort_pass<4>(k0, i0, k1, i1, L, shift, kbias, s_run, s_whist); break;
-            case 5: tsort_pass<5>(k0, i0, k1, i1, L, shift, kbias, s_run, s_whist); break;
-            case 6: tsort_pass<6>(k0, i0, k1, i1, L, shift, kbias, s_run, s_whist); break;
-            case 7: tsort_pass<7>(k0, i0, k1, i1, L, shift, kbias, s_run, s_whist); break;
-            default: tsort_pass<8>(k0, i0, k1, i1, L, shift, kbias, s_run, s_whist); break;
-        }
-        u32* tk = k0; k0 = k1; k1 = tk;
-        u32* ti = i0; i0 = i1; i1 = ti;
-    }
-    __syncthreads();
-}
-
-// LCAP > 0: lists of length in (LMIN, LCAP] sorted in shared memory; LCAP == 0: lists longer than
-// LMIN, sorted in global scratch (4 u32 per key, at the list's own offset).  Other lengths exit.
-template <int LMIN, int LCAP>
-__global__ void __launch_bounds__(kTSortThreads) tile_sort_kernel(const u32* __restrict__ order,
-                                                                 const u32* __restrict__ tile_offsets,
-                                                                 const u64* __restrict__ list, u32 cap,
-                                                                 u32* __restrict__ scratch, u32* __restrict__ vals,
-                                                                 u64* __restrict__ keys64) {
-    extern __shared__ __align__(16) u32 s_buf[];
-    __shared__ u32 s_run[256];
-    __shared__ u32 s_whist[kTSortWarps][256];
-    __shared__ u32 s_mm[3];
-    const int tid = threadIdx.x;
-    const u32 t = __ldg(order + blockIdx.x);
-    const u32 b = __ldg(tile_offsets + t), L = __ldg(tile_offsets + t + 1) - b;
-    if (L <= (u32)LMIN || (LCAP > 0 && L > (u32)LCAP)) return;
-    u32 *k0, *k1, *i0, *i1;
-    if (LCAP > 0) {
-        k0 = s_buf;
-        k1 = s_buf + LCAP;
-        i0 = s_buf + 2 * LCAP;
-        i1 = s_buf + 3 * LCAP;
-    } else {
-        k0 = scratch + b;
-        k1 = scratch + cap + b;
-        i0 = scratch + 2 * (size_t)cap + b;
-        i1 = scratch + 3 * (size_t)cap + b;
-    }
-    // 1. stable LSD sort by the depth bits (the list holds the keys in fill order)
-    for (u32 j = tid; j < L; j += kTSortThreads) {
-        k0[j] = (u32)(__ldg(list + b + j) >> 32);
-        i0[j] = j;
-    }
-    tsort_passes(k0, i0, k1, i1, L, s_run, s_whist, s_mm);
-    // 2. runs of equal depth bits must be ordered by id: short runs by one thread each (runs are
-    // rare); if any run is longer than 32, the list is re-sorted by (depth bits, id) instead — LSD
-    // passes over the ids, then over the depth bits (stable)
-    if (tid == 0) s_mm[2] = 0;
-    __syncthreads();
-    for (u32 j = tid; j < L; j += kTSortThreads) {
-        const bool start = (j == 0 || k0[j - 1] != k0[j]) && j + 1 < L && k0[j + 1] == k0[j];
-        if (!start) continue;
-        u32 e = j + 1;
-        while (e < L && k0[e] == k0[j] && e - j <= 32) e++;
-        if (e - j > 32) { s_mm[2] = 1; continue; }
-        for (u32 a = j + 1; a < e; a++) {  // insertion sort of [j, e) by id
-            const u32 ia = i0[a];
-            const u32 ida = (u32)__ldg(list + b + ia);
-            u32 c = a;
-            while (c > j && (u32)__ldg(list + b + i0[c - 1]) > ida) {
-                i0[c] = i0[c - 1];
-                c--;
-            }
-            i0[c] = ia;
-        }
-    }
-    __syncthreads();
-    if (s_mm[2]) {
-        for (u32 j = tid; j < L; j += kTSortThreads) {
-            k0[j] = (u32)__ldg(list + b + j);
-            i0[j] = j;
-        }
-        tsort_passes(k0, i0, k1, i1, L, s_run, s_whist, s_mm);
-        for (u32 j = tid; j < L; j += kTSortThreads) k0[j] = (u32)(__ldg(list + b + i0[j]) >> 32);
-        tsort_passes(k0, i0, k1, i1, L, s_run, s_whist, s_mm);
-    }
-    __syncthreads();
-    for (u32 j = tid; j < L; j += kTSortThreads) {
-        const u64 x = __ldg(list + b + i0[j]);
-        vals[b + j] = (u32)x;
-        if (keys64) keys64[b + j] = ((u64)t << 32) | (x >> 32);
-    }
-}
-
-// VKS_BINNING=depth selects the depth-major path for A/B measurements
-bool binning_depth_major() {
-    const char* e = getenv("VKS_BINNING");
-    return e && e[0] == 'd';
-}
-
-int run_tile_major(const Workspace& w, int TX, int TY, u32 V, u32 M, int64_t capacity, const u32* tile_offsets,
-                   const u32* order, u32* vals, u64* keys64, cudaStream_t s) {
-    const int n_tiles = TX * TY;
-    if (V) {
-        const size_t sm = sizeof(u32) * (size_t)n_tiles;
-        if (cudaError_t e = cudaFuncSetAttribute(tile_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))
-            return cuda_fail(e, "tile_fill smem attribute");
-        tile_fill_kernel<<<(V + kFillChunk - 1) / kFillChunk, kFillThreads, sm, s>>>(
-            V, w.dv[1], w.dk[1], w.rc_by_id, TX, n_tiles, tile_offsets, w.gcursor, w.list);
-        if (int st = check_launch("tile_fill")) return st;
-    }
-    const size_t sm_small = 4 * sizeof(u32) * (size_t)kTSortSmall, sm_mid = 4 * sizeof(u32) * (size_t)kTSortMid;
-    if (cudaError_t e = cudaFuncSetAttribute(tile_sort_kernel<kTSortSmall, kTSortMid>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_mid))
-        return cuda_fail(e, "tile_sort smem attribute");
-    if (cudaError_t e = cudaFuncSetAttribute(tile_sort_kernel<0, kTSortSmall>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_small))
-        return cuda_fail(e, "tile_sort smem attribute");
-    // heaviest lists first (order = length classes, descending): the global-scratch and the
-    // 16K-key variants, then the 4K-key one (several blocks per SM)
-    tile_sort_kernel<kTSortMid, 0><<<n_tiles, kTSortThreads, 0, s>>>(order, tile_offsets, w.list, (u32)capacity,
-                                                                    w.tscratch, vals, keys64);
-    tile_sort_kernel<kTSortSmall, kTSortMid><<<n_tiles, kTSortThreads, sm_mid, s>>>(order, tile_offsets, w.list,
-                                                                                   (u32)capacity, w.tscratch, vals,
-                                                                                   keys64);
-    tile_sort_kernel<0, kTSortSmall><<<n_tiles, kTSortThreads, sm_small, s>>>(order, tile_offsets, w.list,
-                                                                             (u32)capacity, w.tscratch, vals, keys64);
-    (void)M;
-    (void)TY;
-    return check_launch("tile_sort");
-}
-
 struct PassBufs {
     u32* counts;  // [radix * T]
     u32* offs;    // [radix * T]
@@ -1639,16 +1320,6 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
         int st = launch_keys_debug(cam, n, tiles_touched, means2d, radii, depths, offsets, vals_unsorted,
                                    reinterpret_cast<u64*>(keys_unsorted), s);
         if (st) return st;
-    }
-    // tile-major path (default): rect difference array over the id-order rect codes, tile ranges,
-    // then the bucket fill and the per-tile sorts (section 7)
-    if (n_tiles <= kFillMaxTiles && !binning_depth_major()) {
-        u32* order = tile_order ? tile_order : w.order_ws;
-        int st = launch_rect_diff(TX, TY, (u32)n, w.rc_by_id, w.diff, s);
-        if (!st) st = launch_tile_count(TX, TY, w.diff, tile_offsets, order, s);
-        if (!st) st = run_tile_major(w, TX, TY, (u32)V, (u32)M, capacity, tile_offsets, order, vals,
-                                     reinterpret_cast<u64*>(keys), s);
-        return st;
     }
     // 2. depth sort of the V visible Gaussians (compacted in id order into dk[1]/dv[1] by the scan)
     //    over the significant bits of (depth bits - min depth bits): digits of <= 8 bits, as few

@@ -146,9 +146,11 @@ def raster_flops(visited, composited, replayed):
 
 def measured_traffic(stage, key="dram_bytes_per_launch"):
     """DRAM bytes (read + write) per launch of the stage's dominant kernel (or, key="issue_active",
-    its issue-slot utilisation) from the committed `ncu --set full` capture (profiles/
-    r1_traffic.json, written by tools/traffic_from_ncu.py), or None when no capture is committed."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+    its issue-slot utilisation) from the newest committed `ncu --set full` capture (profiles/
+    rNN_traffic.json, written by tools/traffic_from_ncu.py), or None when no capture is committed."""
+    import glob
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))  # the newest round's capture
+    path = cands[-1] if cands else ""
     try:
         with open(path) as f:
             t = json.load(f)

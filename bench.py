@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--ar-chunks", type=int, default=4,
                     help="N > 1: gradient all-reduce chunks, each overlapped with the next projection-bwd chunk")
     ap.add_argument("--no-batch1", action="store_true")
+    ap.add_argument("--no-records", action="store_true",
+                    help="raster passes gather the separate projection arrays instead of staging packed records")
     ap.add_argument("--streams", type=int, default=3, help="views in flight per rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -111,7 +113,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------- algorithmic work
-def algorithmic_bytes(n, vis, m, dpasses=4, batch=1, K=16):
+def algorithmic_bytes(n, vis, m, dpasses=4, batch=1, K=16, records=True):
     """Per-view algorithmic HBM bytes of the HBM-bound stages, for the algorithms as built
     (DESIGN.md §6).  Parameters are fp32; sh has K coefficients per channel."""
     sh = 12 * K
@@ -121,7 +123,8 @@ def algorithmic_bytes(n, vis, m, dpasses=4, batch=1, K=16):
         # of the Gaussians some view shows); radii + tiles written for all (12 B), the other 36 B
         # of outputs for the visible
         # ... plus the 36 B of 2D-gradient accumulators zeroed per Gaussian and view (g2d_zero)
-        project_fwd=(44 + sh) * n / batch + 4 * n / batch + 12 * n + 36 * vis + 36 * n,
+        # ... plus, with records, the 48-B packed raster record of every visible Gaussian
+        project_fwd=(44 + sh) * n / batch + 4 * n / batch + 12 * n + 36 * vis + 36 * n + (48 * vis if records else 0),
         # id-order scan (read tiles twice, write offsets) + compaction of the visible (read depth,
         # means2d, radii; write depth key, id, rect code) + `dpasses` depth passes over V (count
         # 4 B, scatter 8 B in / 8 B out) + depth-order scan (ids + gathered rect codes in, rect
@@ -206,7 +209,8 @@ def run_ours(args):
     gsync = GradientSync(params, n_chunks=args.ar_chunks if world > 1 else 1)
     host_dL = {v: torch.from_numpy(synth.upstream_grad(c.height, c.width, c.seed + 1000 + v)) for v in set(my_views)}
     dLs = {v: t.cuda() for v, t in host_dL.items()}
-    rends = [P.ViewRenderer(n, c.width, c.height) for _ in range(S)]
+    use_rec = not args.no_records
+    rends = [P.ViewRenderer(n, c.width, c.height, records=use_rec) for _ in range(S)]
     for r in rends:  # size the key capacity once (untimed)
         for v in set(my_views):
             r.forward(cfg, cams[v], params)
@@ -225,12 +229,14 @@ def run_ours(args):
     vbuf = []
     for _ in range(B):
         g2d = torch.zeros(9 * n, dtype=torch.float32, device="cuda")
-        vbuf.append(dict(means2d=torch.empty(n, 2, device="cuda"), conics=torch.empty(n, 3, device="cuda"),
+        vbuf.append(dict(means2d=torch.empty(n, 2, device="cuda"),
+                         conics=None if use_rec else torch.empty(n, 3, device="cuda"),  # the records carry them
                          depths=torch.empty(n, device="cuda"), tiles=torch.empty(n, dtype=torch.int32, device="cuda"),
                          colors=torch.empty(n, 3, device="cuda"),
                          radii=torch.empty(n, 2, dtype=torch.int32, device="cuda"), g2d=g2d,
                          dm2=g2d[: 2 * n].view(n, 2), dcon=g2d[2 * n: 5 * n].view(n, 3),
-                         dcol=g2d[5 * n: 8 * n].view(n, 3), dop=g2d[8 * n:]))
+                         dcol=g2d[5 * n: 8 * n].view(n, 3), dop=g2d[8 * n:],
+                         rec=torch.empty(n, 12, device="cuda") if use_rec else None))
     opac = torch.empty(n, device="cuda")  # view-independent
 
     def project_fwd_batch(vcams, st):
@@ -242,7 +248,8 @@ def run_ours(args):
                                     [vbuf[j]["conics"] for j in range(nb)], [vbuf[j]["depths"] for j in range(nb)],
                                     [vbuf[j]["radii"] for j in range(nb)], [vbuf[j]["tiles"] for j in range(nb)],
                                     [vbuf[j]["colors"] for j in range(nb)], opac,
-                                    g2d_zero=[vbuf[j]["g2d"] for j in range(nb)])
+                                    g2d_zero=[vbuf[j]["g2d"] for j in range(nb)],
+                                    records=[vbuf[j]["rec"] for j in range(nb)] if use_rec else None)
 
     def view_path(rend, vb, cam, dL, st, ev=None, copies=None):
         """One view's forward and raster backward on stream `st` (S views in flight, one stream
@@ -266,7 +273,7 @@ def run_ours(args):
             if ev is not None: ev[2].record(st)
             P.vks_raster_fwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],
                              rend.vals, rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib,
-                             tile_order=rend.tile_order)
+                             tile_order=rend.tile_order, records=vb["rec"])
             if copies is not None and loss_out is None:  # dL/dimage from the host, the image out
                 slot["img_done"].record(st)
                 with torch.cuda.stream(copy_stream):
@@ -283,7 +290,7 @@ def run_ours(args):
             if ev is not None: ev[3].record(st)
             P.vks_raster_bwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],
                              rend.vals, rend.tile_offsets, rend.T_final, rend.n_contrib, dL, vb["dm2"], vb["dcon"],
-                             vb["dcol"], vb["dop"], tile_order=rend.tile_order)
+                             vb["dcol"], vb["dop"], tile_order=rend.tile_order, records=vb["rec"])
             if ev is not None: ev[4].record(st)
             if copies is not None and loss_out is None:
                 slot["in_free"].record(st)
@@ -394,18 +401,19 @@ def run_ours(args):
             e[0].record(main)
             P.vks_project_fwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
                               params.sh, rb.means2d, rb.conics, rb.depths, rb.radii, rb.tiles, rb.colors,
-                              rb.opacities)
+                              rb.opacities, records=rb.records)
             e[1].record(main)
             P.vks_bin_sort(cam, rb.means2d, rb.radii, rb.depths, rb.tiles, rb.offsets, None, rb.vals,
                            rb.tile_offsets, rb.workspace, tile_order=rb.tile_order)
             e[2].record(main)
             P.vks_raster_fwd(cfg, cam, rb.means2d, rb.conics, rb.colors, rb.opacities, rb.radii, rb.vals,
-                             rb.tile_offsets, rb.image, rb.T_final, rb.n_contrib, tile_order=rb.tile_order)
+                             rb.tile_offsets, rb.image, rb.T_final, rb.n_contrib, tile_order=rb.tile_order,
+                             records=rb.records)
             e[3].record(main)
             rb.g2d.zero_()  # the raster backward accumulates the view's 2D gradients
             P.vks_raster_bwd(cfg, cam, rb.means2d, rb.conics, rb.colors, rb.opacities, rb.radii, rb.vals,
                              rb.tile_offsets, rb.T_final, rb.n_contrib, dLv, rb.dmeans2d, rb.dconics, rb.dcolors,
-                             rb.dopacities, tile_order=rb.tile_order)
+                             rb.dopacities, tile_order=rb.tile_order, records=rb.records)
             e[4].record(main)
             P.vks_project_bwd(cfg_ow, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
                               params.sh, rb.colors, rb.radii, rb.dmeans2d, rb.dconics, rb.dcolors, rb.dopacities,
@@ -546,13 +554,13 @@ def run_ours(args):
     stats = torch.zeros(6, dtype=torch.int64, device="cuda")
     P.vks_raster_fwd_stats(cfg, cams[my_views[(nv - 1) % len(my_views)]], vl["means2d"],
                            vl["conics"], vl["colors"], opac, vl["radii"], rend.vals, rend.tile_offsets, stats,
-                           tile_order=rend.tile_order)
+                           tile_order=rend.tile_order, records=vl["rec"])
     visited, composited, evaluated, replayed, warp_entries, warp_entries_comp = (int(x) for x in stats.tolist())
     # depth passes the sort ran: <= 8-bit digits over the visible depth-bit range
     dvis = vl["depths"][vl["tiles"] > 0].view(torch.int32).to(torch.int64)
     drange = int(dvis.max().item() - dvis.min().item()) if dvis.numel() else 0
     dpasses = max(1, (drange.bit_length() + 7) // 8)
-    ab = algorithmic_bytes(n, vis, m_last, dpasses, batch=B)
+    ab = algorithmic_bytes(n, vis, m_last, dpasses, batch=B, records=use_rec)
     fl = raster_flops(visited, composited, replayed)
     pk = peaks()
     clock_mhz = clk["sm_mhz"] or pk["sm_max_mhz"]
@@ -607,7 +615,8 @@ def run_ours(args):
         # Gaussian (radii read, gradient row written) + 280 B per visible one (parameters, 2D
         # gradients and colour read); binning as in the step
         v1, m1 = batch1.pop("_vis"), batch1.pop("_m")
-        b1_bytes = dict(project_fwd=60 * n + 232 * v1, bin_sort=algorithmic_bytes(n, v1, m1, dpasses)["bin_sort"],
+        b1_bytes = dict(project_fwd=60 * n + (232 + (48 if use_rec else 0)) * v1,
+                        bin_sort=algorithmic_bytes(n, v1, m1, dpasses)["bin_sort"],
                         project_bwd=244 * n + 280 * v1)
         b1_roof = {}
         for k, b in b1_bytes.items():
@@ -627,6 +636,8 @@ def run_ours(args):
                scaling=args.scaling, vs_baseline=None, dtype="f32", data="synthetic",
                config=dict(workload=c.description + ", fwd+bwd", n_gaussians=n, width=c.width,
                            height=c.height, sh_degree=3, footprint="support", views_per_step=views_per_step,
+                           raster_staging=("packed 48-B records, cp.async double-buffered per warp" if use_rec
+                                           else "gather of the separate arrays"),
                            views_per_rank_per_step=B, streams=S, visible=vis, num_isects=m_last,
                            l2="inputs larger than L2 (params 1.37 GB, keys+vals 0.22 GB per view), no flush",
                            parallelism=f"view-sharded dp{world} ({args.scaling} scaling)",

@@ -121,12 +121,21 @@ const char* vks_last_cuda_error(void);
  * other outputs are unspecified (currently written as zeros: whole-row stores keep
  * every DRAM sector fully written, which avoids read-modify-write fills).  fp32,
  * operation order pinned (bit-exact with the oracle's O1).
+ *   records [n,12] fp32 (nullable, 16-byte aligned): the packed raster record of every row with
+ *      tiles_touched > 0 — the values the rasterizer stages per list entry, copied from the
+ *      outputs above: (u, v, a/2, b), (c/2, opacity, c0, c1), (c2, bits of the row index i, 0, 0),
+ *      one 48-byte row per Gaussian.  Passed to
+ *      vks_raster_fwd / vks_raster_bwd, the rasterizer copies each tile's batches of entries into
+ *      shared memory with cp.async (three 16-byte copies per entry) instead of gathering eight
+ *      scalars from the separate arrays; results are identical.  Rows with tiles_touched == 0 are
+ *      written as zeros (each warp stores its 32 rows as three coalesced 512-byte runs).  With
+ *      records given, conics may be NULL (not written; the records carry a/2, b, c/2).
  */
 int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                     const float* means, const float* log_scales, const float* quats,
                     const float* opacity_logits, const float* sh,
                     float* means2d, float* conics, float* depths, int32_t* radii,
-                    int32_t* tiles_touched, float* colors, float* opacities,
+                    int32_t* tiles_touched, float* colors, float* opacities, float* records,
                     vks_stream_t stream);
 
 /*
@@ -192,12 +201,18 @@ int vks_bin_sort_check(const vks_camera* cam, int64_t n, const float* means2d, c
  * of its 8x8 patch can reach alpha >= 1/255 (exact minimum of sigma over the patch against
  * ln(255 rho), with an fp32 error margin) and skips the entry warp-uniformly if none can; radii
  * (the support box) are read only by the diagnostic box-culling mode (VKS_RASTER_CULL=1).
+ * records (nullable, 16-byte aligned): vks_project_fwd's packed raster records of the same view;
+ * when given, each warp's batches of 32 entries are copied into shared memory with cp.async
+ * (double-buffered, the next batch in flight while one is composited) instead of gathered from
+ * means2d / conics / colors / opacities; identical results.  With records, conics may be NULL
+ * (VKS_ERR_INVALID_ARG if a diagnostic gather mode — VKS_RASTER_CULL=1, 1 or 4 pixels per thread —
+ * is selected then).
  */
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    const float* means2d, const float* conics, const float* colors,
-                   const float* opacities, const int32_t* radii, const uint32_t* vals,
-                   const uint32_t* tile_offsets, const uint32_t* tile_order, float* image,
-                   float* T_final, int32_t* n_contrib,
+                   const float* opacities, const int32_t* radii, const float* records,
+                   const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                   float* image, float* T_final, int32_t* n_contrib,
                    vks_stream_t stream);
 
 /*
@@ -209,13 +224,13 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
  *   stats[3] += sum of n_contrib (entries the backward replays)
  *   stats[4] += (warp, entry) pairs processed after patch culling
  *   stats[5] += of those, pairs with at least one composited pixel
- * stats must hold 6 uint64 counters.
+ * stats must hold 6 uint64 counters.  records (nullable) as for vks_raster_fwd (same counts).
  */
 int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n,
                          const float* means2d, const float* conics, const float* colors,
-                         const float* opacities, const int32_t* radii, const uint32_t* vals,
-                         const uint32_t* tile_offsets, const uint32_t* tile_order, uint64_t* stats,
-                         vks_stream_t stream);
+                         const float* opacities, const int32_t* radii, const float* records,
+                         const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                         uint64_t* stats, vks_stream_t stream);
 
 /*
  * vks_raster_bwd — "Rasterization Backward".
@@ -223,12 +238,12 @@ int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n
  * and ACCUMULATES exact gradients of the forward w.r.t. mean2d, conic (a,b,c
  * as independent scalars), colour and opacity (0 where alpha was clamped).
  *   dL_dimage [H,W,3] -> dmeans2d [n,2], dconics [n,3], dcolors [n,3], dopacities [n] (+=)
- * tile_order as for vks_raster_fwd (nullable).
+ * tile_order and records as for vks_raster_fwd (nullable).
  */
 int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    const float* means2d, const float* conics, const float* colors,
-                   const float* opacities, const int32_t* radii, const uint32_t* vals,
-                   const uint32_t* tile_offsets, const uint32_t* tile_order,
+                   const float* opacities, const int32_t* radii, const float* records,
+                   const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
                    const float* T_final, const int32_t* n_contrib, const float* dL_dimage,
                    float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
                    vks_stream_t stream);
@@ -268,13 +283,15 @@ int vks_project_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
  *     2D-gradient accumulators (dmeans2d [n,2] | dconics [n,3] | dcolors [n,3] | dopacities [n],
  *     8-byte aligned) that vks_raster_bwd will add into: zeroed here, in the same pass, instead
  *     of by a separate memset
+ *   records (nullable): HOST array of n_views DEVICE pointers, each a view's [n,12] packed raster
+ *     records as for vks_project_fwd (16-byte aligned); with records, conics[v] may be NULL
  */
 int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,
                           const float* means, const float* log_scales, const float* quats,
                           const float* opacity_logits, const float* sh, float* const* means2d,
                           float* const* conics, float* const* depths, int32_t* const* radii,
                           int32_t* const* tiles_touched, float* const* colors, float* opacities,
-                          float* const* g2d_zero, vks_stream_t stream);
+                          float* const* g2d_zero, float* const* records, vks_stream_t stream);
 
 /*
  * vks_project_bwd_batch — the projection backward of a batch of views in one pass: the sum over

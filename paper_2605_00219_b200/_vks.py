@@ -77,15 +77,15 @@ _lib.vks_last_cuda_error.restype = C.c_char_p
 _lib.vks_version.restype = C.c_int
 _lib.vks_bin_sort_workspace_bytes.restype = C.c_size_t
 _lib.vks_bin_sort_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int32]
-_lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
+_lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 14
 _lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 8 + [C.c_size_t, _P]
-_lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 12
+_lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
 _lib.vks_bin_sort_check.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64, _P]
-_lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 16
-_lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 10
+_lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
+_lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 11
 _lib.vks_project_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
 _lib.vks_project_bwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 17
-_lib.vks_project_fwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 14
+_lib.vks_project_fwd_batch.argtypes = [_P, C.c_int32, _P, C.c_int64] + [_P] * 15
 _lib.vks_adam_step.argtypes = [_P, C.c_int64, C.c_int32, _P, _P, _P, _P, _P]
 _lib.vks_loss_workspace_bytes.restype = C.c_size_t
 _lib.vks_loss_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
@@ -176,7 +176,9 @@ f32, i32, u32, u64 = torch.float32, torch.int32, torch.uint32, torch.uint64
 
 
 def vks_project_fwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, means2d, conics, depths,
-                    radii, tiles_touched, colors, opacities, stream=None):
+                    radii, tiles_touched, colors, opacities, stream=None, records=None):
+    """records (optional, fp32 [n, 12], 16-byte aligned): the packed raster records of the visible
+    Gaussians, for vks_raster_fwd / vks_raster_bwd (include/vks.h)."""
     c, k = _cfgcam(cfg, cam)
     n = means.shape[0]
     st = _lib.vks_project_fwd(C.byref(c), C.byref(k), n, _ptr(means, f32, "means"),
@@ -185,7 +187,7 @@ def vks_project_fwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, mean
                               _ptr(means2d, f32, "means2d"), _ptr(conics, f32, "conics"),
                               _ptr(depths, f32, "depths"), _ptr(radii, i32, "radii"),
                               _ptr(tiles_touched, i32, "tiles_touched"), _ptr(colors, f32, "colors"),
-                              _ptr(opacities, f32, "opacities"), _stream(stream))
+                              _ptr(opacities, f32, "opacities"), _ptr(records, f32, "records"), _stream(stream))
     _check("vks_project_fwd", st)
 
 
@@ -228,11 +230,14 @@ def vks_bin_sort_check(cam, means2d, radii, depths, vals, tile_offsets, num_isec
 
 
 def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, image, T_final,
-                   n_contrib, stream=None, tile_order=None):
+                   n_contrib, stream=None, tile_order=None, records=None):
+    """records (optional): vks_project_fwd's packed raster records; when given, the kernel stages
+    them with cp.async instead of gathering the separate arrays (same results)."""
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_raster_fwd(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                              _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
-                             _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
+                             _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"),
+                             _ptr(records, f32, "records"), _ptr(vals, u32, "vals"),
                              _ptr(tile_offsets, u32, "tile_offsets"), _ptr(tile_order, u32, "tile_order"),
                              _ptr(image, f32, "image"),
                              _ptr(T_final, f32, "T_final"), _ptr(n_contrib, i32, "n_contrib"),
@@ -241,7 +246,7 @@ def vks_raster_fwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, ti
 
 
 def vks_raster_fwd_stats(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, stats, stream=None,
-                         tile_order=None):
+                         tile_order=None, records=None):
     """Diagnostic: accumulate [visited, composited, evaluated, replayed, warp_entries,
     warp_entries_composited] counts into the int64 CUDA tensor `stats` (6 entries)."""
     if stats.numel() < 6:
@@ -249,7 +254,8 @@ def vks_raster_fwd_stats(cfg, cam, means2d, conics, colors, opacities, radii, va
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_raster_fwd_stats(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                                    _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
-                                   _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
+                                   _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"),
+                                   _ptr(records, f32, "records"), _ptr(vals, u32, "vals"),
                                    _ptr(tile_offsets, u32, "tile_offsets"), _ptr(tile_order, u32, "tile_order"),
                                    _ptr(stats, torch.int64, "stats"),
                                    _stream(stream))
@@ -257,11 +263,12 @@ def vks_raster_fwd_stats(cfg, cam, means2d, conics, colors, opacities, radii, va
 
 
 def vks_raster_bwd(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, T_final, n_contrib,
-                   dL_dimage, dmeans2d, dconics, dcolors, dopacities, stream=None, tile_order=None):
+                   dL_dimage, dmeans2d, dconics, dcolors, dopacities, stream=None, tile_order=None, records=None):
     c, k = _cfgcam(cfg, cam)
     st = _lib.vks_raster_bwd(C.byref(c), C.byref(k), means2d.shape[0], _ptr(means2d, f32, "means2d"),
                              _ptr(conics, f32, "conics"), _ptr(colors, f32, "colors"),
-                             _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"), _ptr(vals, u32, "vals"),
+                             _ptr(opacities, f32, "opacities"), _ptr(radii, i32, "radii"),
+                             _ptr(records, f32, "records"), _ptr(vals, u32, "vals"),
                              _ptr(tile_offsets, u32, "tile_offsets"), _ptr(tile_order, u32, "tile_order"),
                              _ptr(T_final, f32, "T_final"),
                              _ptr(n_contrib, i32, "n_contrib"), _ptr(dL_dimage, f32, "dL_dimage"),
@@ -287,10 +294,11 @@ def vks_project_bwd(cfg, cam, means, log_scales, quats, opacity_logits, sh, colo
 
 
 def vks_project_fwd_batch(cfg, cams, means, log_scales, quats, opacity_logits, sh, means2d, conics, depths, radii,
-                          tiles_touched, colors, opacities, g2d_zero=None, stream=None):
+                          tiles_touched, colors, opacities, g2d_zero=None, stream=None, records=None):
     """Batched projection forward: `cams` and the per-view outputs (means2d, conics, depths, radii,
     tiles_touched, colors) are equal-length sequences; `opacities` is one tensor for the batch;
-    g2d_zero (optional): per view a [9n] fp32 tensor of 2D-gradient accumulators to zero."""
+    g2d_zero (optional): per view a [9n] fp32 tensor of 2D-gradient accumulators to zero;
+    records (optional): per view an fp32 [n, 12] tensor receiving the packed raster records."""
     nv = len(cams)
     per_view = (means2d, conics, depths, radii, tiles_touched, colors)
     if any(len(x) != nv for x in per_view):
@@ -300,12 +308,15 @@ def vks_project_fwd_batch(cfg, cams, means, log_scales, quats, opacity_logits, s
     dts = (f32, f32, f32, i32, i32, f32)
     names = ("means2d", "conics", "depths", "radii", "tiles_touched", "colors")
     arrs = [(C.c_void_p * max(nv, 1))(*[_ptr(t, dt, nm) for t in seq]) for seq, dt, nm in zip(per_view, dts, names)]
+    # (conics may be a sequence of None when records are written)
     st = _lib.vks_project_fwd_batch(C.byref(c), nv, karr, means.shape[0], _ptr(means, f32, "means"),
                                     _ptr(log_scales, f32, "log_scales"), _ptr(quats, f32, "quats"),
                                     _ptr(opacity_logits, f32, "opacity_logits"), _ptr(sh, f32, "sh"), *arrs,
                                     _ptr(opacities, f32, "opacities"),
                                     None if g2d_zero is None else (C.c_void_p * max(nv, 1))(
                                         *[_ptr(t, f32, "g2d_zero") for t in g2d_zero]),
+                                    None if records is None else (C.c_void_p * max(nv, 1))(
+                                        *[_ptr(t, f32, "records") for t in records]),
                                     _stream(stream))
     _check("vks_project_fwd_batch", st)
 

@@ -85,15 +85,17 @@ const char* vks_last_cuda_error(void) { return vks::last_error_buf(); }
 int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means,
                     const float* log_scales, const float* quats, const float* opacity_logits,
                     const float* sh, float* means2d, float* conics, float* depths, int32_t* radii,
-                    int32_t* tiles_touched, float* colors, float* opacities, vks_stream_t stream) {
+                    int32_t* tiles_touched, float* colors, float* opacities, float* records,
+                    vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
-    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !means2d || !conics ||
+    // conics may be NULL when the records (which carry them) are written
+    if (n > 0 && (!means || !log_scales || !quats || !opacity_logits || !sh || !means2d || (!conics && !records) ||
                   !depths || !radii || !tiles_touched || !colors || !opacities))
         return VKS_ERR_INVALID_ARG;
     if ((reinterpret_cast<uintptr_t>(quats) & 15) || (reinterpret_cast<uintptr_t>(means2d) & 7) ||
-        (reinterpret_cast<uintptr_t>(radii) & 7))
+        (reinterpret_cast<uintptr_t>(radii) & 7) || (reinterpret_cast<uintptr_t>(records) & 15))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
     if (validating(cfg) && (st = check_params(n, cfg->sh_coeffs, means, log_scales, quats, opacity_logits, sh,
@@ -101,7 +103,7 @@ int vks_project_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, con
         return st;
     return cuda_status(vks::launch_project_fwd(*cfg, *cam, n, means, log_scales, quats, opacity_logits, sh,
                                                means2d, conics, depths, radii, tiles_touched, colors,
-                                               opacities, (cudaStream_t)stream));
+                                               opacities, records, (cudaStream_t)stream));
 }
 
 size_t vks_bin_sort_workspace_bytes(int64_t n, int64_t capacity, int32_t n_tiles) {
@@ -144,14 +146,16 @@ int vks_bin_sort_check(const vks_camera* cam, int64_t n, const float* means2d, c
 
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
                    const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                   const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
-                   float* image, float* T_final, int32_t* n_contrib, vks_stream_t stream) {
+                   const float* records, const uint32_t* vals, const uint32_t* tile_offsets,
+                   const uint32_t* tile_order, float* image, float* T_final, int32_t* n_contrib,
+                   vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
     if (!tile_offsets || !image || !T_final || !n_contrib) return VKS_ERR_INVALID_ARG;
-    if (n > 0 && (!means2d || !conics || !colors || !opacities || !radii)) return VKS_ERR_INVALID_ARG;
-    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
+    if (n > 0 && (!means2d || (!conics && !records) || !colors || !opacities || !radii)) return VKS_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7) ||
+        (reinterpret_cast<uintptr_t>(records) & 15))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
     if (validating(cfg)) {  // the tile lists index [0, n) through a CSR (S:155 UnsortedInput)
@@ -161,39 +165,41 @@ int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
         if (!st) st = vks::validate_end((cudaStream_t)stream);
         if (st) return st;
     }
-    return cuda_status(vks::launch_raster_fwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
+    return cuda_status(vks::launch_raster_fwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, records, vals,
                                               tile_offsets, tile_order, image, T_final, n_contrib,
                                               (cudaStream_t)stream));
 }
 
 int vks_raster_fwd_stats(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
                          const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                         const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
-                         uint64_t* stats, vks_stream_t stream) {
+                         const float* records, const uint32_t* vals, const uint32_t* tile_offsets,
+                         const uint32_t* tile_order, uint64_t* stats, vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (!camera_ok(cam) || n < 0 || !tile_offsets || !stats) return VKS_ERR_INVALID_ARG;
-    if (n > 0 && (!means2d || !conics || !colors || !opacities || !radii)) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means2d || (!conics && !records) || !colors || !opacities || !radii)) return VKS_ERR_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(records) & 15) return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
-    return vks::launch_raster_fwd_stats(*cfg, *cam, means2d, conics, colors, opacities, radii, vals, tile_offsets,
+    return vks::launch_raster_fwd_stats(*cfg, *cam, means2d, conics, colors, opacities, radii, records, vals, tile_offsets,
                                         tile_order, reinterpret_cast<unsigned long long*>(stats), n,
                                         (cudaStream_t)stream);
 }
 
 int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, const float* means2d,
                    const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                   const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
-                   const float* T_final, const int32_t* n_contrib,
+                   const float* records, const uint32_t* vals, const uint32_t* tile_offsets,
+                   const uint32_t* tile_order, const float* T_final, const int32_t* n_contrib,
                    const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                    float* dopacities, vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (!camera_ok(cam) || n < 0) return VKS_ERR_INVALID_ARG;
     if (!tile_offsets || !T_final || !n_contrib || !dL_dimage) return VKS_ERR_INVALID_ARG;
-    if (n > 0 && (!means2d || !conics || !colors || !opacities || !radii || !dmeans2d || !dconics ||
+    if (n > 0 && (!means2d || (!conics && !records) || !colors || !opacities || !radii || !dmeans2d || !dconics ||
                   !dcolors || !dopacities))
         return VKS_ERR_INVALID_ARG;
-    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7))
+    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7) ||
+        (reinterpret_cast<uintptr_t>(records) & 15))
         return VKS_ERR_INVALID_ARG;
     if (!device_present()) return VKS_ERR_CUDA;
     if (validating(cfg)) {  // finite upstream gradient, tile lists a CSR over [0, n)
@@ -204,7 +210,7 @@ int vks_raster_bwd(const vks_config* cfg, const vks_camera* cam, int64_t n, cons
         if (!st) st = vks::validate_end((cudaStream_t)stream);
         if (st) return st;
     }
-    return cuda_status(vks::launch_raster_bwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, vals,
+    return cuda_status(vks::launch_raster_bwd(*cfg, *cam, n, means2d, conics, colors, opacities, radii, records, vals,
                                               tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d,
                                               dconics,
                                               dcolors, dopacities, (cudaStream_t)stream));
@@ -240,10 +246,13 @@ int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
                           const float* opacity_logits, const float* sh, float* const* means2d,
                           float* const* conics, float* const* depths, int32_t* const* radii,
                           int32_t* const* tiles_touched, float* const* colors, float* opacities,
-                          float* const* g2d_zero, vks_stream_t stream) {
+                          float* const* g2d_zero, float* const* records, vks_stream_t stream) {
     int st = config_ok(cfg);
     if (st) return st;
     if (n_views < 1 || n_views > 16 || !cams || n < 0) return VKS_ERR_INVALID_ARG;
+    if (records)
+        for (int v = 0; v < n_views; v++)
+            if (n > 0 && (!records[v] || (reinterpret_cast<uintptr_t>(records[v]) & 15))) return VKS_ERR_INVALID_ARG;
     if (!means2d || !conics || !depths || !radii || !tiles_touched || !colors) return VKS_ERR_INVALID_ARG;
     if (g2d_zero)
         for (int v = 0; v < n_views; v++)
@@ -251,7 +260,8 @@ int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
     for (int v = 0; v < n_views; v++) {
         if (!camera_ok(cams + v) || cams[v].width != cams[0].width || cams[v].height != cams[0].height)
             return VKS_ERR_INVALID_ARG;
-        if (n > 0 && (!means2d[v] || !conics[v] || !depths[v] || !radii[v] || !tiles_touched[v] || !colors[v]))
+        if (n > 0 && (!means2d[v] || (!conics[v] && !records) || !depths[v] || !radii[v] || !tiles_touched[v] ||
+                      !colors[v]))
             return VKS_ERR_INVALID_ARG;
         if ((reinterpret_cast<uintptr_t>(means2d[v]) & 7) || (reinterpret_cast<uintptr_t>(radii[v]) & 7))
             return VKS_ERR_INVALID_ARG;
@@ -264,7 +274,7 @@ int vks_project_fwd_batch(const vks_config* cfg, int32_t n_views, const vks_came
         return st;
     return cuda_status(vks::launch_project_fwd_batch(*cfg, n_views, cams, n, means, log_scales, quats, opacity_logits,
                                                      sh, means2d, conics, depths, radii, tiles_touched, colors,
-                                                     opacities, g2d_zero, (cudaStream_t)stream));
+                                                     opacities, g2d_zero, records, (cudaStream_t)stream));
 }
 
 int vks_project_bwd_batch(const vks_config* cfg, int32_t n_views, const vks_camera* cams, int64_t n,

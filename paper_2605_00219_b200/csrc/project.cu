@@ -49,6 +49,7 @@ struct Params {
     int* __restrict__ tiles;
     float* __restrict__ colors;
     float* __restrict__ opac;
+    float4* __restrict__ rec;  // nullable: packed raster records [n][3] (write_record)
     // backward
     const int2* __restrict__ radii_in;
     const float2* __restrict__ dm2;
@@ -61,6 +62,30 @@ struct Params {
     float* __restrict__ dologit;
     float* __restrict__ dsh;
 };
+
+// The packed raster records (include/vks.h, vks_project_fwd `records`): per visible Gaussian the
+// values the rasterizer stages per list entry, in its order — (u, v, a/2, b), (c/2, rho, c0, c1),
+// (c2, id bits, 0, 0).  A warp writes its 32 rows (1.5 KB) through a shared-memory buffer as three
+// fully coalesced 512-byte stores (48-byte rows stored lane by lane leave every 32-byte sector
+// half-written per instruction); culled rows get zeros, rows >= n nothing.  Every lane of the warp
+// calls it.
+constexpr int kRecWarpF4 = 96;  // float4 per warp buffer
+__device__ __forceinline__ void store_records_warp(float4* __restrict__ rec, int64_t g0, int64_t n, float4* sb, bool vis,
+                                                   float u, float v, float a, float b, float c, float rho,
+                                                   const float col[3]) {
+    const int lane = (int)lane_id();
+    const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    sb[3 * lane + 0] = vis ? make_float4(u, v, 0.5f * a, b) : z;
+    sb[3 * lane + 1] = vis ? make_float4(0.5f * c, rho, col[0], col[1]) : z;
+    sb[3 * lane + 2] = vis ? make_float4(col[2], __uint_as_float((uint32_t)(g0 + lane)), 0.0f, 0.0f) : z;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const int j = lane + 32 * k;
+        if (g0 + j / 3 < n) rec[3 * g0 + j] = sb[j];
+    }
+    __syncwarp();
+}
 
 __device__ __forceinline__ float dot3(const float* a, const float* b) {
     return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
@@ -231,6 +256,14 @@ struct ShLayout {
     static constexpr int kWarpFloats = 32 * SP;
 };
 
+// the single-view kernel reuses the warp's SH staging buffer for its 96-float4 record buffer
+template <int KS>
+constexpr bool rec_in_sh() {
+    if constexpr (KS > 0) return ShLayout<KS>::kWarpFloats * sizeof(float) >= 96 * sizeof(float4) &&
+                                 (ShLayout<KS>::kWarpFloats % 4) == 0;
+    return false;
+}
+
 // staged rows readable as float4 (16-byte aligned, whole float4 per row)
 template <int KS>
 constexpr bool vec_rows() {
@@ -374,12 +407,26 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
         }
         vis = ok;
     }
+    if (p.rec) {
+        // the warp's SH staging buffer is free once the colours are formed (rows of >= 12 floats
+        // hold the 96 float4); smaller layouts get a buffer of their own after the SH region
+        float4* sb;
+        if constexpr (rec_in_sh<KS>()) {
+            __syncwarp();  // every lane has read its SH row
+            sb = reinterpret_cast<float4*>(buf);
+        } else {
+            sb = reinterpret_cast<float4*>(smem + (KS > 0 ? kWarps * ShLayout<KS>::kWarpFloats : 0)) + warp * kRecWarpF4;
+        }
+        store_records_warp(p.rec, g0, p.n, sb, vis, k.u, k.v, k.a, k.b, k.c, k.rho, col);
+    }
     if (!valid) return;
     if (vis) {
         p.means2d[i] = make_float2(k.u, k.v);
-        p.conics[3 * i + 0] = k.a;
-        p.conics[3 * i + 1] = k.b;
-        p.conics[3 * i + 2] = k.c;
+        if (p.conics) {
+            p.conics[3 * i + 0] = k.a;
+            p.conics[3 * i + 1] = k.b;
+            p.conics[3 * i + 2] = k.c;
+        }
         p.depths[i] = k.t[2];
         p.radii[i] = make_int2((int)rxf, (int)ryf);
         p.tiles[i] = (x1 - x0) * (y1 - y0);
@@ -389,9 +436,11 @@ __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
         p.opac[i] = k.rho;
     } else {  // full rows: partial-sector writes would make L2 fetch the sector from DRAM first
         p.means2d[i] = make_float2(0.0f, 0.0f);
-        p.conics[3 * i + 0] = 0.0f;
-        p.conics[3 * i + 1] = 0.0f;
-        p.conics[3 * i + 2] = 0.0f;
+        if (p.conics) {
+            p.conics[3 * i + 0] = 0.0f;
+            p.conics[3 * i + 1] = 0.0f;
+            p.conics[3 * i + 2] = 0.0f;
+        }
         p.depths[i] = 0.0f;
         p.radii[i] = make_int2(0, 0);
         p.tiles[i] = 0;
@@ -419,6 +468,7 @@ struct FwdViewOut {
     int2* radii;
     int* tiles;
     float* colors;
+    float4* rec;  // nullable: packed raster records [n][3]
     float* g2d;  // nullable: the view's 2D-gradient accumulators [9n] (dmeans2d | dconics | dcolors | dopacities), zeroed
 };
 
@@ -622,6 +672,11 @@ __global__ void __launch_bounds__(kThreads) project_fwd_batch_kernel(const Batch
             }
             vis = ok;
         }
+        if (V.rec) {
+            float4* sb = reinterpret_cast<float4*>(smem + (KS > 0 ? kWarps * ShLayout<KS>::kWarpFloats : 0)) +
+                         warp * kRecWarpF4;
+            store_records_warp(V.rec, g0, p.n, sb, vis, k.u, k.v, k.a, k.b, k.c, G.rho, col);
+        }
         if (!valid) continue;
         if (V.g2d) {  // the raster backward's accumulators, cleared here instead of by a separate pass
             reinterpret_cast<float2*>(V.g2d)[i] = make_float2(0.0f, 0.0f);
@@ -633,9 +688,11 @@ __global__ void __launch_bounds__(kThreads) project_fwd_batch_kernel(const Batch
         }
         if (vis) {
             V.means2d[i] = make_float2(k.u, k.v);
-            V.conics[3 * i + 0] = k.a;
-            V.conics[3 * i + 1] = k.b;
-            V.conics[3 * i + 2] = k.c;
+            if (V.conics) {
+                V.conics[3 * i + 0] = k.a;
+                V.conics[3 * i + 1] = k.b;
+                V.conics[3 * i + 2] = k.c;
+            }
             V.depths[i] = k.t[2];
             V.radii[i] = make_int2((int)rxf, (int)ryf);
             V.tiles[i] = (x1 - x0) * (y1 - y0);
@@ -644,9 +701,11 @@ __global__ void __launch_bounds__(kThreads) project_fwd_batch_kernel(const Batch
             V.colors[3 * i + 2] = col[2];
         } else {  // whole rows (no read-for-merge of partial DRAM sectors)
             V.means2d[i] = make_float2(0.0f, 0.0f);
-            V.conics[3 * i + 0] = 0.0f;
-            V.conics[3 * i + 1] = 0.0f;
-            V.conics[3 * i + 2] = 0.0f;
+            if (V.conics) {
+                V.conics[3 * i + 0] = 0.0f;
+                V.conics[3 * i + 1] = 0.0f;
+                V.conics[3 * i + 2] = 0.0f;
+            }
             V.depths[i] = 0.0f;
             V.radii[i] = make_int2(0, 0);
             V.tiles[i] = 0;
@@ -661,6 +720,11 @@ template <int KS>
 int launch_fwd_batch_t(const BatchFwdParams& p, cudaStream_t s) {
     size_t sm = 0;
     if constexpr (KS > 0) sm = sizeof(float) * kWarps * ShLayout<KS>::kWarpFloats;
+    if (p.nv > 0) {
+        bool rec = false;
+        for (int v = 0; v < p.nv; v++) rec = rec || p.v[v].rec != nullptr;
+        if (rec) sm += sizeof(float4) * kWarps * kRecWarpF4;  // the records' staging buffers
+    }
     if (sm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(project_fwd_batch_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sm);
@@ -679,7 +743,7 @@ size_t smem_bytes() {
 
 template <int KS>
 int launch_fwd_t(const Params& p, cudaStream_t s) {
-    const size_t sm = smem_bytes<KS>();
+    const size_t sm = smem_bytes<KS>() + (p.rec && !rec_in_sh<KS>() ? sizeof(float4) * kWarps * kRecWarpF4 : 0);
     if (sm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(project_fwd_kernel<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return VKS_ERR_CUDA;
@@ -696,7 +760,7 @@ bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u
 int launch_project_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means,
                        const float* log_scales, const float* quats, const float* opacity_logits,
                        const float* sh, float* means2d, float* conics, float* depths, int32_t* radii,
-                       int32_t* tiles_touched, float* colors, float* opacities, cudaStream_t s) {
+                       int32_t* tiles_touched, float* colors, float* opacities, float* records, cudaStream_t s) {
     if (n == 0) return VKS_OK;
     Params p{};
     p.cam = cam; p.cfg = cfg; p.n = n;
@@ -706,6 +770,7 @@ int launch_project_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
     p.means2d = reinterpret_cast<float2*>(means2d); p.conics = conics; p.depths = depths;
     p.radii = reinterpret_cast<int2*>(radii); p.tiles = tiles_touched; p.colors = colors;
     p.opac = opacities;
+    p.rec = reinterpret_cast<float4*>(records);
     const bool al = aligned16(sh);
     switch (cfg.sh_coeffs) {
         case 16: return al ? launch_fwd_t<16>(p, s) : launch_fwd_t<0>(p, s);
@@ -721,7 +786,7 @@ int launch_project_fwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
                              const float* opacity_logits, const float* sh, float* const* means2d,
                              float* const* conics, float* const* depths, int32_t* const* radii,
                              int32_t* const* tiles_touched, float* const* colors, float* opacities,
-                             float* const* g2d_zero, cudaStream_t s) {
+                             float* const* g2d_zero, float* const* records, cudaStream_t s) {
     if (n == 0) return VKS_OK;
     if (n_views < 1 || n_views > kMaxFwdViews) return VKS_ERR_INVALID_ARG;
     BatchFwdParams p{};
@@ -739,6 +804,7 @@ int launch_project_fwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
         V.tiles = tiles_touched[v];
         V.colors = colors[v];
         V.g2d = g2d_zero ? g2d_zero[v] : nullptr;
+        V.rec = records ? reinterpret_cast<float4*>(records[v]) : nullptr;
     }
     const bool al = aligned16(sh);
     switch (cfg.sh_coeffs) {

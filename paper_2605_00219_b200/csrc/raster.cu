@@ -20,6 +20,8 @@
 // conic gradients with the Gaussian's conic, and issues one atomic per term from 9 lanes.
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "vks_common.cuh"
 
 namespace vks {
@@ -39,6 +41,28 @@ struct WarpStage {  // all three arrays at a 16-byte stride: one address for the
     float4 b[32];    // 0.5*c, rho, c0, c1
     float4 c[32];    // c2, id (bits), position in the batch (bits), -
 };
+
+// Records path (the projection's packed raster records, include/vks.h): each warp stages two
+// batches of 32 records with cp.async (three 16-byte copies per entry straight into shared
+// memory, slot = lane, the next batch in flight while the current one is visited); the live
+// entries are then visited in place (set bits of the warp's live mask).
+struct RecStage {
+    float4 a[2][32];  // u, v, 0.5*a, b
+    float4 b[2][32];  // 0.5*c, rho, c0, c1
+    float4 c[2][32];  // c2, id (bits), -, -
+};
+
+template <bool REC>
+using StageT = typename std::conditional<REC, RecStage, WarpStage>::type;
+
+// one lane's record -> slot `lane` of buffer `buf` (three cp.async.cg 16-byte copies)
+__device__ __forceinline__ void stage_record(RecStage& s, int buf, int lane, const float4* __restrict__ rec,
+                                             uint32_t id) {
+    const float4* g = rec + 3 * (size_t)id;
+    cp_async16(&s.a[buf][lane], g);
+    cp_async16(&s.b[buf][lane], g + 1);
+    cp_async16(&s.c[buf][lane], g + 2);
+}
 
 struct Entry {  // one lane's gathered entry, in registers until it is stored to the stage
     float4 a, b;
@@ -175,25 +199,26 @@ __device__ __forceinline__ PixelMap<PPT> pixel_map(int tile, int TX) {
 // stats[1] = composited pairs, stats[2] = pairs actually evaluated here (after patch culling),
 // stats[3] = sum of n_contrib (entries the backward replays), stats[4] = (warp, entry) pairs a
 // warp processed after patch culling, stats[5] = those with at least one composited pixel.
-template <int PPT, int CULL, bool STATS = false>
+template <int PPT, int CULL, bool STATS = false, bool REC = false>
 __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
                                                                  const float* __restrict__ colors,
                                                                  const float* __restrict__ opac,
                                                                  const int2* __restrict__ radii,
+                                                                 const float4* __restrict__ rec,
                                                                  const uint32_t* __restrict__ vals,
                                                                  const uint32_t* __restrict__ tile_offsets,
                                                                  const uint32_t* __restrict__ tile_order,
                                                                  float* __restrict__ image, float* __restrict__ T_final,
                                                                  int* __restrict__ n_contrib,
                                                                  uint32_t n, unsigned long long* __restrict__ stats = nullptr) {
-    __shared__ WarpStage stage[8 / PPT];
+    __shared__ StageT<REC> stage[8 / PPT];
     unsigned long long n_eval = 0, n_comp = 0, n_went = 0, n_wcomp = 0;
     const int TX = tiles_x(cam);
     const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
     const int lane = threadIdx.x & 31;
-    WarpStage& s = stage[threadIdx.x >> 5];
+    StageT<REC>& s = stage[threadIdx.x >> 5];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
     // a pixel is done once T < 1e-4 (T only changes when it composites, so the test is exact);
@@ -209,31 +234,71 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
     }
     const uint32_t start = tile_offsets[tile], end = tile_offsets[tile + 1];
     VKS_DCHECK(start <= end);
-    // software pipeline: ids two batches ahead, gathered entries one batch ahead
+    // software pipeline: ids two batches ahead, the next batch's entries one batch ahead (gathered
+    // into registers, or, REC, copied by cp.async into the other stage buffer)
     uint32_t id_next = (start + lane < end) ? __ldg(vals + start + lane) : 0u;
     Entry e_next;
-    if (start + lane < end) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
+    if constexpr (REC) {
+        VKS_DCHECK(start + lane >= end || id_next < n);
+        if (start + lane < end) stage_record(s, 0, lane, rec, id_next);
+        cp_async_commit();
+    } else {
+        if (start + lane < end) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
+    }
     id_next = (start + 32 + lane < end) ? __ldg(vals + start + 32 + lane) : 0u;
-    for (uint32_t b = start; b < end; b += 32) {
+    int buf = 0;
+    for (uint32_t b = start; b < end; b += 32, buf ^= 1) {
         bool all_done = true;
 #pragma unroll
         for (int k = 0; k < PPT; k++) all_done = all_done && T[k] < 1e-4f;
         if (__all_sync(VKS_FULL_MASK, all_done)) break;
-        __syncwarp();
+        __syncwarp();  // every lane is done with the buffer the next stores / copies overwrite
         // each lane tests its own entry against the warp patch; the warp then visits, in list
         // order, only the entries that can composite somewhere in the patch
-        const bool lv = b + lane < end && !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1);
-        const unsigned live = __ballot_sync(VKS_FULL_MASK, lv);
-        if (lv) store_entry(s, __popc(live & lanemask_lt()), lane, e_next);
-        __syncwarp();
-        if (b + 32 + lane < end) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
-        if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
+        unsigned live;
+        if constexpr (REC) {
+            VKS_DCHECK(b + 32 + lane >= end || id_next < n);
+            if (b + 32 + lane < end) stage_record(s, buf ^ 1, lane, rec, id_next);
+            cp_async_commit();
+            if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
+            cp_async_wait_group<1>();  // this lane's copies of batch b have landed
+            __syncwarp();              // ... and every other lane's
+            bool lv = false;
+            if (b + lane < end) {
+                Entry e;
+                e.a = s.a[buf][lane];
+                e.b = s.b[buf][lane];
+                lv = !culled<CULL>(e, pm.wx0, pm.wx1, pm.wy0, pm.wy1);
+            }
+            live = __ballot_sync(VKS_FULL_MASK, lv);
+        } else {
+            const bool lv = b + lane < end && !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1);
+            live = __ballot_sync(VKS_FULL_MASK, lv);
+            if (lv) store_entry(s, __popc(live & lanemask_lt()), lane, e_next);
+            __syncwarp();
+            if (b + 32 + lane < end) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
+            if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
+        }
         const int nlive = __popc(live);
+        const int base = (int)(b - start) + 1;
         for (int q = 0; q < nlive; q++) {  // in list order
-            const float4 A = s.a[q], B = s.b[q];
-            const float4 Cq = s.c[q];
-            const float c2 = Cq.x;
-            const int j = __float_as_int(Cq.z);
+            float4 A, B;
+            float c2;
+            int pos1;
+            if constexpr (REC) {  // the live slots in place: lowest set bit first
+                const int j = __ffs(live) - 1;
+                live &= live - 1;
+                A = s.a[buf][j];
+                B = s.b[buf][j];
+                c2 = s.c[buf][j].x;
+                pos1 = base + j;
+            } else {
+                A = s.a[q];
+                B = s.b[q];
+                const float4 Cq = s.c[q];
+                c2 = Cq.x;
+                pos1 = base + __float_as_int(Cq.z);
+            }
             if constexpr (STATS) {
                 bool any = false;
 #pragma unroll
@@ -245,14 +310,13 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                     n_comp++;
                     any = true;
                     T[k] = T[k] * (1.0f - alpha);
-                    last[k] = (int)(b - start) + j + 1;
+                    last[k] = pos1;
                 }
                 const bool wany = __any_sync(VKS_FULL_MASK, any);
                 if (lane == 0) { n_went++; n_wcomp += wany; }
             } else {
                 // branch-free: a skipped entry composites alpha = 0, which leaves C and T
                 // bit-identical (C + c * 0 = C, T * (1 - 0) = T)
-                const int pos1 = (int)(b - start) + j + 1;
 #pragma unroll
                 for (int k = 0; k < PPT; k++) {
                     float dx, dy, G, rG, alpha;
@@ -268,6 +332,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
             }
         }
     }
+    if constexpr (REC) cp_async_wait_all();  // no copy outlives the warp
     if constexpr (STATS) {
         unsigned long long visited = 0, replay = 0;
 #pragma unroll
@@ -332,13 +397,14 @@ __device__ __forceinline__ float warp_reduce_8plus1(const float v[8], float& e, 
     return c;
 }
 
-template <int PPT, int CULL, int SPARSE>
+template <int PPT, int CULL, int SPARSE, bool REC = false>
 __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
                                                                  const float* __restrict__ colors,
                                                                  const float* __restrict__ opac,
                                                                  const int2* __restrict__ radii,
+                                                                 const float4* __restrict__ rec,
                                                                  const uint32_t* __restrict__ vals,
                                                                  const uint32_t* __restrict__ tile_offsets,
                                                                  const uint32_t* __restrict__ tile_order,
@@ -348,11 +414,11 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
                                                                  float* __restrict__ dmeans2d, float* __restrict__ dconics,
                                                                  float* __restrict__ dcolors, float* __restrict__ dopac,
                                                                  int sparse_lanes, uint32_t n) {
-    __shared__ WarpStage stage[8 / PPT];
+    __shared__ StageT<REC> stage[8 / PPT];
     const int TX = tiles_x(cam);
     const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
     const unsigned lane = threadIdx.x & 31;
-    WarpStage& s = stage[threadIdx.x >> 5];
+    StageT<REC>& s = stage[threadIdx.x >> 5];
     const PixelMap<PPT> pm = pixel_map<PPT>(tile, TX);
     const float px = (float)pm.x + 0.5f;
     const uint32_t start = tile_offsets[tile];
@@ -400,28 +466,65 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
     int p0 = bs + (int)lane;
     uint32_t id_next = (p0 >= 0 && p0 < wmax) ? __ldg(vals + start + p0) : 0u;
     Entry e_next;
-    if (p0 >= 0 && p0 < wmax) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
+    if constexpr (REC) {
+        VKS_DCHECK(!(p0 >= 0 && p0 < wmax) || id_next < n);
+        if (p0 >= 0 && p0 < wmax) stage_record(s, 0, (int)lane, rec, id_next);
+        cp_async_commit();
+    } else {
+        if (p0 >= 0 && p0 < wmax) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
+    }
     p0 -= 32;
     id_next = (p0 >= 0) ? __ldg(vals + start + p0) : 0u;
-    for (; bs > -32; bs -= 32) {
+    int buf = 0;
+    for (; bs > -32; bs -= 32, buf ^= 1) {
         __syncwarp();
         unsigned live;
-        {
-            const int p = bs + (int)lane;
-            const bool ok = p >= 0 && p < wmax;
-            const bool lv = ok && !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1);
-            live = __ballot_sync(VKS_FULL_MASK, lv);
-            if (lv) store_entry(s, __popc(live & lanemask_lt()), lane, e_next);
-        }
-        __syncwarp();
-        {
-            const int p = bs - 32 + (int)lane;
-            if (p >= 0) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
+        if constexpr (REC) {
+            const int p = bs - 32 + (int)lane;  // the next batch's position of this lane
+            VKS_DCHECK(p < 0 || id_next < n);
+            if (p >= 0) stage_record(s, buf ^ 1, (int)lane, rec, id_next);
+            cp_async_commit();
             if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
+            cp_async_wait_group<1>();
+            __syncwarp();
+            const int pc = bs + (int)lane;
+            bool lv = false;
+            if (pc >= 0 && pc < wmax) {
+                Entry e;
+                e.a = s.a[buf][lane];
+                e.b = s.b[buf][lane];
+                lv = !culled<CULL>(e, pm.wx0, pm.wx1, pm.wy0, pm.wy1);
+            }
+            live = __ballot_sync(VKS_FULL_MASK, lv);
+        } else {
+            {
+                const int p = bs + (int)lane;
+                const bool ok = p >= 0 && p < wmax;
+                const bool lv = ok && !culled<CULL>(e_next, pm.wx0, pm.wx1, pm.wy0, pm.wy1);
+                live = __ballot_sync(VKS_FULL_MASK, lv);
+                if (lv) store_entry(s, __popc(live & lanemask_lt()), lane, e_next);
+            }
+            __syncwarp();
+            {
+                const int p = bs - 32 + (int)lane;
+                if (p >= 0) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
+                if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
+            }
         }
         for (int q = __popc(live) - 1; q >= 0; q--) {  // back to front over the live entries
-            const float4 A = s.a[q], B = s.b[q];
-            const float4 Cc = s.c[q];
+            float4 A, B, Cc;
+            if constexpr (REC) {  // the live slots in place: highest set bit first
+                const int j = 31 - __clz(live);
+                live &= ~(1u << j);
+                A = s.a[buf][j];
+                B = s.b[buf][j];
+                Cc = s.c[buf][j];
+                Cc.z = __int_as_float(j);
+            } else {
+                A = s.a[q];
+                B = s.b[q];
+                Cc = s.c[q];
+            }
             const int pos = bs + __float_as_int(Cc.z);
             const float c0 = B.z, c1 = B.w, c2 = Cc.x;
             // evaluate first: an entry no pixel of the warp composited leaves every T, P and
@@ -490,31 +593,33 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             }
         }
     }
+    if constexpr (REC) cp_async_wait_all();  // no copy outlives the warp
 }
 
-template <int PPT, int CULL>
+template <int PPT, int CULL, bool REC = false>
 int launch_fwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
-               const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-               const uint32_t* tile_offsets, const uint32_t* tile_order, float* image, float* T_final,
-               int32_t* n_contrib, uint32_t n, cudaStream_t st) {
+               const float* colors, const float* opacities, const int32_t* radii, const float* records,
+               const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order, float* image,
+               float* T_final, int32_t* n_contrib, uint32_t n, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_fwd_kernel<PPT, CULL><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
+    raster_fwd_kernel<PPT, CULL, false, REC><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
-        reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, image, T_final, n_contrib, n);
+        reinterpret_cast<const int2*>(radii), reinterpret_cast<const float4*>(records), vals, tile_offsets, tile_order,
+        image, T_final, n_contrib, n);
     return LaunchCheck::check();
 }
 
-template <int PPT, int CULL, int SPARSE>
+template <int PPT, int CULL, int SPARSE, bool REC = false>
 int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
-               const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-               const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
+               const float* colors, const float* opacities, const int32_t* radii, const float* records,
+               const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
                const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                float* dopacities, int sparse_lanes, uint32_t n, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_bwd_kernel<PPT, CULL, SPARSE><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
+    raster_bwd_kernel<PPT, CULL, SPARSE, REC><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
-        reinterpret_cast<const int2*>(radii), vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage,
-        dmeans2d, dconics, dcolors, dopacities, sparse_lanes, n);
+        reinterpret_cast<const int2*>(radii), reinterpret_cast<const float4*>(records), vals, tile_offsets, tile_order,
+        T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, sparse_lanes, n);
     return LaunchCheck::check();
 }
 
@@ -532,22 +637,32 @@ int ppt_choice(const char* var) {
     return v == 3 ? 2 : v;
 }
 
+// the records path (cp.async staging of the packed records) serves the default configuration:
+// 2 pixels per thread with the exact ellipse test or no culling; the diagnostic modes (1 / 4
+// pixels per thread, box culling) gather from the separate arrays
+bool use_records(const float* records, int ppt, int cull) {
+    return records != nullptr && ppt == 2 && cull != kCullBox;
+}
+
 template <int PPT>
 int dispatch_fwd(int cull, const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
                  const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
                  const uint32_t* tile_offsets, const uint32_t* tile_order, float* image, float* T_final,
                  int32_t* n_contrib, uint32_t n, cudaStream_t st) {
+#define VKS_FWD_ARGS cfg, cam, means2d, conics, colors, opacities, radii, nullptr, vals, tile_offsets, tile_order, \
+                     image, T_final, n_contrib, n, st
     switch (cull) {
-        case kCullNone: return launch_fwd<PPT, kCullNone>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
-        case kCullBox: return launch_fwd<PPT, kCullBox>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
-        default: return launch_fwd<PPT, kCullEllipse>(cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
+        case kCullNone: return launch_fwd<PPT, kCullNone>(VKS_FWD_ARGS);
+        case kCullBox: return launch_fwd<PPT, kCullBox>(VKS_FWD_ARGS);
+        default: return launch_fwd<PPT, kCullEllipse>(VKS_FWD_ARGS);
     }
+#undef VKS_FWD_ARGS
 }
 
 template <int PPT>
 int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
-                 const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-                 const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
+                 const float* colors, const float* opacities, const int32_t* radii, const float* records,
+                 const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order, const float* T_final,
                  const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                  float* dopacities, uint32_t n, cudaStream_t st) {
     // SPARSE (default): skip entries no pixel of the warp composited, and reduce entries composited
@@ -555,8 +670,17 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
     // 32-lane butterfly for every entry (round-1 kernel, kept for A/B measurements)
     const int sparse = env_choice("VKS_RASTER_BWD_SPARSE", 1, 0, 1);
     const int lanes = env_choice("VKS_RASTER_SPARSE", 4, 0, 32);
-#define VKS_BWD_ARGS cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, \
-                     n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, lanes, n, st
+#define VKS_BWD_ARGS cfg, cam, means2d, conics, colors, opacities, radii, records, vals, tile_offsets, tile_order, \
+                     T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, lanes, n, st
+    if constexpr (PPT == 2) {
+        if (use_records(records, PPT, cull)) {
+            if (sparse)
+                return cull == kCullNone ? launch_bwd<PPT, kCullNone, 1, true>(VKS_BWD_ARGS)
+                                         : launch_bwd<PPT, kCullEllipse, 1, true>(VKS_BWD_ARGS);
+            return cull == kCullNone ? launch_bwd<PPT, kCullNone, 0, true>(VKS_BWD_ARGS)
+                                     : launch_bwd<PPT, kCullEllipse, 0, true>(VKS_BWD_ARGS);
+        }
+    }
 #define VKS_BWD_CULL(SP)                                                                 \
     switch (cull) {                                                                      \
         case kCullNone: return launch_bwd<PPT, kCullNone, SP>(VKS_BWD_ARGS);             \
@@ -572,34 +696,46 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
 }  // namespace
 
 int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
-                            const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-                            const uint32_t* tile_offsets, const uint32_t* tile_order, unsigned long long* stats,
-                            int64_t n, cudaStream_t st) {
+                            const float* colors, const float* opacities, const int32_t* radii, const float* records,
+                            const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                            unsigned long long* stats, int64_t n, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
     const auto m2 = reinterpret_cast<const float2*>(means2d);
     const auto r2 = reinterpret_cast<const int2*>(radii);
-    switch (cull_choice(cfg)) {
-        case kCullNone:
-            raster_fwd_kernel<2, kCullNone, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                           vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, (uint32_t)n, stats);
-            break;
-        case kCullBox:
-            raster_fwd_kernel<2, kCullBox, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                          vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, (uint32_t)n, stats);
-            break;
-        default:
-            raster_fwd_kernel<2, kCullEllipse, true><<<n_tiles, 128, 0, st>>>(cfg, cam, m2, conics, colors, opacities, r2,
-                                                                              vals, tile_offsets, tile_order, nullptr, nullptr, nullptr, (uint32_t)n, stats);
+    const auto rc = reinterpret_cast<const float4*>(records);
+    const int cull = cull_choice(cfg);
+    if (!use_records(records, 2, cull) && n > 0 && !conics) return VKS_ERR_INVALID_ARG;
+#define VKS_STATS_ARGS cfg, cam, m2, conics, colors, opacities, r2, rc, vals, tile_offsets, tile_order, nullptr, nullptr, \
+                       nullptr, (uint32_t)n, stats
+    if (use_records(records, 2, cull)) {
+        if (cull == kCullNone) raster_fwd_kernel<2, kCullNone, true, true><<<n_tiles, 128, 0, st>>>(VKS_STATS_ARGS);
+        else raster_fwd_kernel<2, kCullEllipse, true, true><<<n_tiles, 128, 0, st>>>(VKS_STATS_ARGS);
+        return LaunchCheck::check();
     }
+    switch (cull) {
+        case kCullNone: raster_fwd_kernel<2, kCullNone, true><<<n_tiles, 128, 0, st>>>(VKS_STATS_ARGS); break;
+        case kCullBox: raster_fwd_kernel<2, kCullBox, true><<<n_tiles, 128, 0, st>>>(VKS_STATS_ARGS); break;
+        default: raster_fwd_kernel<2, kCullEllipse, true><<<n_tiles, 128, 0, st>>>(VKS_STATS_ARGS);
+    }
+#undef VKS_STATS_ARGS
     return LaunchCheck::check();
 }
 
 int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                      const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
-                      float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
+                      const float* records, const uint32_t* vals, const uint32_t* tile_offsets,
+                      const uint32_t* tile_order, float* image, float* T_final, int32_t* n_contrib, cudaStream_t st) {
     const int ppt = ppt_choice("VKS_RASTER_FWD_PPT");
     const int cull = cull_choice(cfg);
+    if (!use_records(records, ppt, cull) && n > 0 && !conics) return VKS_ERR_INVALID_ARG;  // a gather mode needs them
+    if (use_records(records, ppt, cull)) {
+        return cull == kCullNone
+                   ? launch_fwd<2, kCullNone, true>(cfg, cam, means2d, conics, colors, opacities, radii, records, vals,
+                                                   tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st)
+                   : launch_fwd<2, kCullEllipse, true>(cfg, cam, means2d, conics, colors, opacities, radii, records,
+                                                      vals, tile_offsets, tile_order, image, T_final, n_contrib,
+                                                      (uint32_t)n, st);
+    }
     if (ppt == 4) return dispatch_fwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
     if (ppt == 1) return dispatch_fwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
     return dispatch_fwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
@@ -607,14 +743,19 @@ int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
 
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                      const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
-                      const float* T_final, const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
-                      float* dconics, float* dcolors, float* dopacities, cudaStream_t st) {
+                      const float* records, const uint32_t* vals, const uint32_t* tile_offsets,
+                      const uint32_t* tile_order, const float* T_final, const int32_t* n_contrib,
+                      const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors, float* dopacities,
+                      cudaStream_t st) {
     const int ppt = ppt_choice("VKS_RASTER_BWD_PPT");
     const int cull = cull_choice(cfg);
-    if (ppt == 4) return dispatch_bwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, (uint32_t)n, st);
-    if (ppt == 1) return dispatch_bwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, (uint32_t)n, st);
-    return dispatch_bwd<2>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, (uint32_t)n, st);
+    if (!use_records(records, ppt, cull) && n > 0 && !conics) return VKS_ERR_INVALID_ARG;  // a gather mode needs them
+#define VKS_RB_ARGS cull, cfg, cam, means2d, conics, colors, opacities, radii, records, vals, tile_offsets, tile_order, \
+                    T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, (uint32_t)n, st
+    if (ppt == 4) return dispatch_bwd<4>(VKS_RB_ARGS);
+    if (ppt == 1) return dispatch_bwd<1>(VKS_RB_ARGS);
+    return dispatch_bwd<2>(VKS_RB_ARGS);
+#undef VKS_RB_ARGS
 }
 
 }  // namespace vks

@@ -88,6 +88,8 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Per-view constants of steps 6 and 12 (FOV limits, camera centre), computed once by the launcher
 // with the same IEEE fp32 operations in the same order (host code is compiled without FMA
@@ -124,7 +126,7 @@ namespace vks {
 int launch_project_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means,
                        const float* log_scales, const float* quats, const float* opacity_logits,
                        const float* sh, float* means2d, float* conics, float* depths, int32_t* radii,
-                       int32_t* tiles_touched, float* colors, float* opacities, cudaStream_t s);
+                       int32_t* tiles_touched, float* colors, float* opacities, float* records, cudaStream_t s);
 int launch_project_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means,
                        const float* log_scales, const float* quats, const float* opacity_logits,
                        const float* sh, const float* colors, const int32_t* radii, const float* dmeans2d,
@@ -136,7 +138,7 @@ int launch_project_fwd_batch(const vks_config& cfg, int32_t n_views, const vks_c
                              const float* opacity_logits, const float* sh, float* const* means2d,
                              float* const* conics, float* const* depths, int32_t* const* radii,
                              int32_t* const* tiles_touched, float* const* colors, float* opacities,
-                             float* const* g2d_zero, cudaStream_t s);
+                             float* const* g2d_zero, float* const* records, cudaStream_t s);
 int launch_project_bwd_batch(const vks_config& cfg, int32_t n_views, const vks_camera* cams, int64_t n,
                              const float* means, const float* log_scales, const float* quats,
                              const float* opacity_logits, const float* sh, const float* const* colors,
@@ -170,12 +172,12 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
                  void* workspace, size_t workspace_bytes, cudaStream_t s);
 int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                      const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                      const float* records, const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
                       float* image, float* T_final, int32_t* n_contrib, cudaStream_t s);
 int launch_raster_fwd_stats(const vks_config& cfg, const vks_camera& cam, const float* means2d, const float* conics,
-                            const float* colors, const float* opacities, const int32_t* radii, const uint32_t* vals,
-                            const uint32_t* tile_offsets, const uint32_t* tile_order, unsigned long long* stats,
-                            int64_t n, cudaStream_t s);
+                            const float* colors, const float* opacities, const int32_t* radii, const float* records,
+                            const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                            unsigned long long* stats, int64_t n, cudaStream_t s);
 // VKS_FLAG_VALIDATE checks (validate.cu): begin resets the status word, the checks enqueue,
 // end synchronises once and returns VKS_OK / VKS_ERR_NONFINITE / VKS_ERR_UNSORTED
 int validate_begin(cudaStream_t s);
@@ -188,7 +190,7 @@ int validate_bins(const vks_camera& cam, int64_t n, const float* means2d, const 
 int validate_end(cudaStream_t s);
 int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
-                      const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
+                      const float* records, const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
                       const float* T_final, const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
                       float* dconics, float* dcolors, float* dopacities, cudaStream_t s);
 }  // namespace vks

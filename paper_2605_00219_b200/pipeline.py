@@ -98,7 +98,11 @@ class GaussianParams:
 class ViewRenderer:
     """Scratch buffers for one resolution; `forward` then `backward` run one view's hot path."""
 
-    def __init__(self, n: int, width: int, height: int, device="cuda", capacity: int | None = None):
+    def __init__(self, n: int, width: int, height: int, device="cuda", capacity: int | None = None,
+                 records: bool = True):
+        """records: the projection also writes the packed raster records and both raster passes
+        stage them with cp.async (include/vks.h); False: the rasterizer gathers the separate
+        arrays (same results)."""
         self.device = device
         self.n, self.W, self.H = n, width, height
         self.TX, self.TY = (width + 15) // 16, (height + 15) // 16
@@ -107,6 +111,7 @@ class ViewRenderer:
         self.means2d, self.conics, self.depths = e(n, 2), e(n, 3), e(n)
         self.radii, self.tiles = e(n, 2, dt=torch.int32), e(n, dt=torch.int32)
         self.colors, self.opacities = e(n, 3), e(n)
+        self.records = e(n, 12) if records else None
         self.offsets = e(n, dt=torch.uint32)
         self.tile_offsets = e(self.n_tiles + 1, dt=torch.uint32)
         self.tile_order = e(self.n_tiles, dt=torch.uint32)  # raster schedule (heaviest tiles first)
@@ -132,7 +137,8 @@ class ViewRenderer:
         """want_keys: also write the sorted u64 (tile|depth) keys (verification only; the
         rasterizer needs the sorted ids and the tile ranges)."""
         V.vks_project_fwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.means2d,
-                          self.conics, self.depths, self.radii, self.tiles, self.colors, self.opacities)
+                          self.conics, self.depths, self.radii, self.tiles, self.colors, self.opacities,
+                          records=self.records)
         for attempt in range(2):
             m = V.vks_bin_sort(cam, self.means2d, self.radii, self.depths, self.tiles, self.offsets,
                                self.keys if want_keys else None,
@@ -145,7 +151,8 @@ class ViewRenderer:
             self._alloc_capacity(int(-m * 1.25) + 1024)
         self.num_isects = m
         V.vks_raster_fwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.radii, self.vals,
-                         self.tile_offsets, self.image, self.T_final, self.n_contrib, tile_order=self.tile_order)
+                         self.tile_offsets, self.image, self.T_final, self.n_contrib, tile_order=self.tile_order,
+                         records=self.records)
         return self.image
 
     def backward(self, cfg, cam, P: GaussianParams, dL_dimage: torch.Tensor, zero_2d: bool = True,
@@ -158,7 +165,7 @@ class ViewRenderer:
             cfg = dict(cfg, flags=int(cfg.get("flags", 0)) | V.FLAG_GRAD_OVERWRITE)
         V.vks_raster_bwd(cfg, cam, self.means2d, self.conics, self.colors, self.opacities, self.radii, self.vals,
                          self.tile_offsets, self.T_final, self.n_contrib, dL_dimage, self.dmeans2d, self.dconics,
-                         self.dcolors, self.dopacities, tile_order=self.tile_order)
+                         self.dcolors, self.dopacities, tile_order=self.tile_order, records=self.records)
         g = P.grads()
         V.vks_project_bwd(cfg, cam, P.means, P.log_scales, P.quats, P.opacity_logits, P.sh, self.colors, self.radii,
                           self.dmeans2d, self.dconics, self.dcolors, self.dopacities, g["dmeans"],

@@ -16,12 +16,14 @@ def to_np(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
 
 
-def run_gpu(scene, cam, cfg, dL=None, capacity=None, debug_unsorted=False):
-    """One view through the CUDA path.  Returns numpy copies of every stage output."""
+def run_gpu(scene, cam, cfg, dL=None, capacity=None, debug_unsorted=False, records=True):
+    """One view through the CUDA path.  Returns numpy copies of every stage output.
+    records: the raster passes stage the projection's packed records (default, as the bench) or
+    gather the separate arrays (False)."""
     import paper_2605_00219_b200 as P
     params = P.GaussianParams.from_host(scene)
     n = params.n
-    r = P.ViewRenderer(n, cam["width"], cam["height"], capacity=capacity)
+    r = P.ViewRenderer(n, cam["width"], cam["height"], capacity=capacity, records=records)
     ku = vu = None
     r.forward(cfg, cam, params, want_keys=True)  # may regrow the capacity
     if debug_unsorted:  # debug outputs must hold `capacity` entries (include/vks.h)
@@ -34,6 +36,8 @@ def run_gpu(scene, cam, cfg, dL=None, capacity=None, debug_unsorted=False):
     m = r.num_isects
     res = {k: to_np(v) for k, v in out.items()}
     res["num_isects"] = m
+    if r.records is not None:
+        res["records"] = to_np(r.records)
     res["keys"] = to_np(r.keys[:m])
     res["vals"] = to_np(r.vals[:m])
     if debug_unsorted:

@@ -71,17 +71,17 @@ def test_argument_validation_is_synchronous():
     cam = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
                              width=64, height=64))
     # null camera / negative n / bad degree / bad footprint -> errors before any CUDA call
-    assert lib.vks_project_fwd(C.byref(cfg), None, 0, *([None] * 13)) == V.VKS_ERR_INVALID_ARG
-    assert lib.vks_project_fwd(C.byref(cfg), C.byref(cam), -1, *([None] * 13)) == V.VKS_ERR_INVALID_ARG
+    assert lib.vks_project_fwd(C.byref(cfg), None, 0, *([None] * 14)) == V.VKS_ERR_INVALID_ARG
+    assert lib.vks_project_fwd(C.byref(cfg), C.byref(cam), -1, *([None] * 14)) == V.VKS_ERR_INVALID_ARG
     bad = V.make_config(dict(sh_degree=4, sh_coeffs=25))
-    assert lib.vks_project_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 13)) == V.VKS_ERR_UNSUPPORTED
+    assert lib.vks_project_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 14)) == V.VKS_ERR_UNSUPPORTED
     bad = V.make_config(dict(sh_degree=3, sh_coeffs=9))
-    assert lib.vks_project_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 13)) == V.VKS_ERR_INVALID_ARG
+    assert lib.vks_project_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 14)) == V.VKS_ERR_INVALID_ARG
     bad = V.make_config(dict(sh_degree=3, sh_coeffs=16, footprint=7))
-    assert lib.vks_raster_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 12)) == V.VKS_ERR_UNSUPPORTED
+    assert lib.vks_raster_fwd(C.byref(bad), C.byref(cam), 0, *([None] * 13)) == V.VKS_ERR_UNSUPPORTED
     wide = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
                               width=70000, height=64))
-    assert lib.vks_raster_bwd(C.byref(cfg), C.byref(wide), 0, *([None] * 16)) == V.VKS_ERR_INVALID_ARG
+    assert lib.vks_raster_bwd(C.byref(cfg), C.byref(wide), 0, *([None] * 17)) == V.VKS_ERR_INVALID_ARG
     arr = (C.c_void_p * 1)(None)
     cams = (V.VksCamera * 1)(cam)
     for nv in (0, 17):  # batch size outside [1, 16]
@@ -124,7 +124,7 @@ def test_no_cpu_fallback():
     cfg = V.make_config(dict(sh_degree=3, sh_coeffs=16))
     cam = V.make_camera(dict(R=[1, 0, 0, 0, 1, 0, 0, 0, 1], t=[0, 0, 0], fx=100, fy=100, cx=32, cy=32,
                              width=64, height=64))
-    st = lib.vks_raster_fwd(C.byref(cfg), C.byref(cam), 0, None, None, None, None, None, None, C.c_void_p(16),
+    st = lib.vks_raster_fwd(C.byref(cfg), C.byref(cam), 0, None, None, None, None, None, None, None, C.c_void_p(16),
                             None, C.c_void_p(16), C.c_void_p(16), C.c_void_p(16), None)
     assert st == V.VKS_ERR_CUDA
     assert b"no CUDA device" in lib.vks_last_cuda_error()

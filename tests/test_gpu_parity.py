@@ -321,6 +321,84 @@ def test_patch_culling_and_ppt_variants_agree(fp, monkeypatch):
     report(f"cull_fp{fp}", dict(stats={"/".join(k): v for k, v in stats.items()}))
 
 
+@pytest.mark.parametrize("kind,n,W,H,view", [("indoor", 200000, 400, 300, 3), ("outdoor", 60000, 333, 211, 5)])
+def test_records_path_agrees_with_gather(kind, n, W, H, view):
+    """The packed raster records (vks_project_fwd `records`) hold exactly the projection's outputs
+    of every visible row — (u, v, a/2, b), (c/2, rho, c0, c1), (c2, id, 0, 0), bit for bit — and
+    both raster passes staging them with cp.async give the identical image, T and n_contrib as the
+    gather path, and the same 2D gradients up to atomic summation order (ragged 333x211 image)."""
+    s = synth.make_scene(n, kind, 72)
+    cam = synth.ring_cameras(W, H, kind, 8)[view]
+    cfg = synth.default_render_config()
+    dL = synth.upstream_grad(H, W, 6)
+    rec = run_gpu(s, cam, cfg, dL=dL, records=True)
+    gat = run_gpu(s, cam, cfg, dL=dL, records=False)
+    vis = rec["tiles_touched"] > 0
+    assert vis.sum() > n // 10
+    R = rec["records"][vis].reshape(-1, 12)
+    ids = np.nonzero(vis)[0]
+    want = np.stack([rec["means2d"][vis, 0], rec["means2d"][vis, 1], 0.5 * rec["conics"][vis, 0],
+                     rec["conics"][vis, 1], 0.5 * rec["conics"][vis, 2], rec["opacities"][vis],
+                     rec["colors"][vis, 0], rec["colors"][vis, 1], rec["colors"][vis, 2]], 1).astype(np.float32)
+    assert np.array_equal(R[:, :9].view(np.uint32), want.view(np.uint32))
+    assert np.array_equal(R[:, 9].view(np.uint32), ids.astype(np.uint32))
+    culled = rec["records"][~vis]
+    assert not culled.any()  # culled rows: zeros
+    for k in ("image", "T_final", "n_contrib", "vals", "tile_offsets"):
+        assert np.array_equal(rec[k], gat[k]), k
+    for k in ("dmeans2d", "dconics", "dcolors", "dopacities"):
+        scale = np.abs(gat[k]).max()
+        assert np.allclose(rec[k], gat[k], rtol=1e-4, atol=1e-6 * scale), k
+    # the raster statistics (bench roofline counts) are the same through either staging
+    import torch
+    import paper_2605_00219_b200 as P
+    params = P.GaussianParams.from_host(s)
+    r = P.ViewRenderer(params.n, W, H)
+    r.forward(cfg, cam, params)
+    st = [torch.zeros(6, dtype=torch.int64, device="cuda") for _ in range(2)]
+    for t, recs in zip(st, (None, r.records)):
+        P.vks_raster_fwd_stats(cfg, cam, r.means2d, r.conics, r.colors, r.opacities, r.radii, r.vals, r.tile_offsets,
+                               t, tile_order=r.tile_order, records=recs)
+    assert st[0].tolist() == st[1].tolist()
+
+
+def test_batched_projection_records_match_single_view():
+    """vks_project_fwd_batch writes every view's records bit-identical to vks_project_fwd's."""
+    import torch
+    import paper_2605_00219_b200 as P
+    s = synth.make_scene(50001, "outdoor", 73)
+    cams = synth.ring_cameras(320, 240, "outdoor", 8)[:3]
+    cfg = synth.default_render_config()
+    params = P.GaussianParams.from_host(s)
+    n = params.n
+    e = lambda *sh, dt=torch.float32: torch.empty(*sh, dtype=dt, device="cuda")
+    outs = [dict(m=e(n, 2), c=e(n, 3), d=e(n), r=e(n, 2, dt=torch.int32), t=e(n, dt=torch.int32), col=e(n, 3),
+                 rec=torch.full((n, 12), float("nan"), device="cuda")) for _ in cams]
+    op = e(n)
+    P.vks_project_fwd_batch(cfg, cams, params.means, params.log_scales, params.quats, params.opacity_logits, params.sh,
+                            [o["m"] for o in outs], [o["c"] for o in outs], [o["d"] for o in outs],
+                            [o["r"] for o in outs], [o["t"] for o in outs], [o["col"] for o in outs], op,
+                            records=[o["rec"] for o in outs])
+    # the records carry the conics: conics may be omitted (the bench's configuration)
+    rec2 = [torch.full((n, 12), float("nan"), device="cuda") for _ in cams]
+    P.vks_project_fwd_batch(cfg, cams, params.means, params.log_scales, params.quats, params.opacity_logits, params.sh,
+                            [o["m"] for o in outs], [None] * len(cams), [o["d"] for o in outs],
+                            [o["r"] for o in outs], [o["t"] for o in outs], [o["col"] for o in outs], op,
+                            records=rec2)
+    for o, r2 in zip(outs, rec2):
+        assert torch.equal(o["rec"].view(torch.int32), r2.view(torch.int32))
+    for cam, o in zip(cams, outs):
+        r = P.ViewRenderer(n, cam["width"], cam["height"])
+        r.records.fill_(float("nan"))
+        P.vks_project_fwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits, params.sh,
+                          r.means2d, r.conics, r.depths, r.radii, r.tiles, r.colors, r.opacities, records=r.records)
+        torch.cuda.synchronize()
+        vis = (r.tiles > 0).cpu().numpy()
+        assert vis.sum() > 1000
+        a, b = to_np(o["rec"])[vis], to_np(r.records)[vis]
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
 @pytest.mark.parametrize("lanes", ["0", "4", "32"])
 def test_raster_bwd_sparse_path_agrees(lanes, monkeypatch, oracle_lib):
     """The raster backward's sparse-entry path (per-lane atomics for entries composited by few

@@ -28,7 +28,8 @@ def fwd_batch():
     P.vks_project_fwd_batch(cfg, cams[:B], params.means, params.log_scales, params.quats, params.opacity_logits,
                             params.sh, [r.means2d for r in views], [r.conics for r in views],
                             [r.depths for r in views], [r.radii for r in views], [r.tiles for r in views],
-                            [r.colors for r in views], views[0].opacities, g2d_zero=[r.g2d for r in views])
+                            [r.colors for r in views], views[0].opacities, g2d_zero=[r.g2d for r in views],
+                            records=[r.records for r in views])
 
 
 def view(v):
@@ -36,10 +37,10 @@ def view(v):
     r.num_isects = P.vks_bin_sort(cams[v], r.means2d, r.radii, r.depths, r.tiles, r.offsets, None, r.vals,
                                   r.tile_offsets, r.workspace, tile_order=r.tile_order)
     P.vks_raster_fwd(cfg, cams[v], r.means2d, r.conics, r.colors, views[0].opacities, r.radii, r.vals,
-                     r.tile_offsets, r.image, r.T_final, r.n_contrib, tile_order=r.tile_order)
+                     r.tile_offsets, r.image, r.T_final, r.n_contrib, tile_order=r.tile_order, records=r.records)
     P.vks_raster_bwd(cfg, cams[v], r.means2d, r.conics, r.colors, views[0].opacities, r.radii, r.vals,
                      r.tile_offsets, r.T_final, r.n_contrib, dLs[v], r.dmeans2d, r.dconics, r.dcolors,
-                     r.dopacities, tile_order=r.tile_order)
+                     r.dopacities, tile_order=r.tile_order, records=r.records)
 
 
 def bwd_batch():

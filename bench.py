@@ -595,9 +595,23 @@ def run_ours(args):
     # kernels; its stage roofline is reported in stage_roofline)
     dom = max(("project_fwd", "raster_fwd", "raster_bwd", "project_bwd"), key=lambda k: per_stage[k]["ms"])
     d = per_stage[dom]
+    # the raster kernels are issue-bound: beside the flop model, their warp-instruction
+    # rate against the issue peak (4 schedulers x 148 SMs x the sampled clock), from the ncu-counted
+    # instructions of one launch (committed capture, bicycle view 0) and this run's live launch time
+    issue = {}
+    for k, units in (("raster_fwd", ("evaluated_pairs", evaluated)), ("raster_bwd", ("replayed_pairs", replayed))):
+        wi = measured_traffic(k, "warp_instructions_per_launch")
+        if wi:
+            ipk = 4 * 148 * clock_mhz * 1e6
+            issue[k] = dict(warp_instructions_per_launch_ncu=int(wi),
+                            achieved=round(wi / (st_ms[k] * 1e-3) / 1e9, 1), peak=round(ipk / 1e9, 1),
+                            unit="G warp-instructions/s", frac=round(wi / (st_ms[k] * 1e-3) / ipk, 4),
+                            lane_instructions_per_pair=round(32 * wi / max(1, units[1]), 2), per=units[0],
+                            warp_instructions_per_warp_entry=round(wi / max(1, warp_entries), 1))
+            per_stage[k]["issue"] = issue[k]
     roofline = dict(kernel=dom, bound=d["bound"], achieved=round(d["achieved"], 3), peak=round(d["peak"], 3),
                     unit=d["unit"], frac=round(d["frac"], 4), traffic=measured_traffic(dom),
-                    issue_active_ncu=measured_traffic(dom, "issue_active"),
+                    issue_active_ncu=measured_traffic(dom, "issue_active"), issue=issue.get(dom),
                     peak_source=(pk["src"] + " HBM copy (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
                                  f"derived (no measured FP32 figure in MEASURED_PEAKS.json): 148 SM x 128 FP32 "
                                  f"lanes x 2 flop x {clock_mhz:.0f} MHz (median SM clock sampled in the timed "

@@ -205,8 +205,8 @@ int vks_bin_sort_check(const vks_camera* cam, int64_t n, const float* means2d, c
  * when given, each warp's batches of 32 entries are copied into shared memory with cp.async
  * (double-buffered, the next batch in flight while one is composited) instead of gathered from
  * means2d / conics / colors / opacities; identical results.  With records, conics may be NULL
- * (VKS_ERR_INVALID_ARG if a diagnostic gather mode — VKS_RASTER_CULL=1, 1 or 4 pixels per thread —
- * is selected then).
+ * (VKS_ERR_INVALID_ARG if the diagnostic box-culling mode VKS_RASTER_CULL=1, which gathers from
+ * the separate arrays, is selected then).
  */
 int vks_raster_fwd(const vks_config* cfg, const vks_camera* cam, int64_t n,
                    const float* means2d, const float* conics, const float* colors,

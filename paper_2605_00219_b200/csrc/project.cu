@@ -8,6 +8,7 @@
 // shared memory with coalesced 16-byte loads, and only for lanes that survived culling (the SH
 // bytes of culled Gaussians are never read).
 #include "vks_common.cuh"
+#include "vks_sh.cuh"
 
 namespace vks {
 namespace {
@@ -16,20 +17,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
 // 3DGS real spherical-harmonics constants (closed forms in DESIGN.md §4.1 step 12)
-#define C0 0.28209479177387814f
-#define C1 0.4886025119029199f
-#define C20 1.0925484305920792f
-#define C21 -1.0925484305920792f
-#define C22 0.31539156525252005f
-#define C23 -1.0925484305920792f
-#define C24 0.5462742152960396f
-#define C30 -0.5900435899266435f
-#define C31 2.890611442640554f
-#define C32 -0.4570457994644658f
-#define C33 0.3731763325901154f
-#define C34 -0.4570457994644658f
-#define C35 1.445305721320277f
-#define C36 -0.5900435899266435f
+using namespace sh;  // the SH basis constants (vks_sh.cuh)
 
 struct Params {
     vks_camera cam;
@@ -49,18 +37,7 @@ struct Params {
     int* __restrict__ tiles;
     float* __restrict__ colors;
     float* __restrict__ opac;
-    float4* __restrict__ rec;  // nullable: packed raster records [n][3] (write_record)
-    // backward
-    const int2* __restrict__ radii_in;
-    const float2* __restrict__ dm2;
-    const float* __restrict__ dcon;
-    const float* __restrict__ dcol;
-    const float* __restrict__ dop;
-    float* __restrict__ dmeans;
-    float* __restrict__ dls;
-    float4* __restrict__ dquats;
-    float* __restrict__ dologit;
-    float* __restrict__ dsh;
+    float4* __restrict__ rec;  // nullable: packed raster records [n][3] (store_records_warp)
 };
 
 // The packed raster records (include/vks.h, vks_project_fwd `records`): per visible Gaussian the

@@ -8,6 +8,7 @@
 // DESIGN.md §4.1 steps 1 and 6.  All parameter / 2D-gradient loads are issued up front; SH rows of
 // a warp are staged through shared memory with coalesced 16-byte loads (active lanes only).
 #include "vks_common.cuh"
+#include "vks_sh.cuh"
 
 namespace vks {
 namespace {
@@ -15,20 +16,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-#define C0 0.28209479177387814f
-#define C1 0.4886025119029199f
-#define C20 1.0925484305920792f
-#define C21 -1.0925484305920792f
-#define C22 0.31539156525252005f
-#define C23 -1.0925484305920792f
-#define C24 0.5462742152960396f
-#define C30 -0.5900435899266435f
-#define C31 2.890611442640554f
-#define C32 -0.4570457994644658f
-#define C33 0.3731763325901154f
-#define C34 -0.4570457994644658f
-#define C35 1.445305721320277f
-#define C36 -0.5900435899266435f
+using namespace sh;  // the SH basis constants (vks_sh.cuh)
 
 struct Params {
     vks_camera cam;

@@ -637,11 +637,12 @@ int ppt_choice(const char* var) {
     return v == 3 ? 2 : v;
 }
 
-// the records path (cp.async staging of the packed records) serves the default configuration:
-// 2 pixels per thread with the exact ellipse test or no culling; the diagnostic modes (1 / 4
-// pixels per thread, box culling) gather from the separate arrays
+// the records path (cp.async staging of the packed records) serves every layout with the exact
+// ellipse test or no culling; the diagnostic box-culling mode gathers from the separate arrays
+// (it needs the radii)
 bool use_records(const float* records, int ppt, int cull) {
-    return records != nullptr && ppt == 2 && cull != kCullBox;
+    (void)ppt;
+    return records != nullptr && cull != kCullBox;
 }
 
 template <int PPT>
@@ -672,14 +673,12 @@ int dispatch_bwd(int cull, const vks_config& cfg, const vks_camera& cam, const f
     const int lanes = env_choice("VKS_RASTER_SPARSE", 4, 0, 32);
 #define VKS_BWD_ARGS cfg, cam, means2d, conics, colors, opacities, radii, records, vals, tile_offsets, tile_order, \
                      T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, lanes, n, st
-    if constexpr (PPT == 2) {
-        if (use_records(records, PPT, cull)) {
-            if (sparse)
-                return cull == kCullNone ? launch_bwd<PPT, kCullNone, 1, true>(VKS_BWD_ARGS)
-                                         : launch_bwd<PPT, kCullEllipse, 1, true>(VKS_BWD_ARGS);
-            return cull == kCullNone ? launch_bwd<PPT, kCullNone, 0, true>(VKS_BWD_ARGS)
-                                     : launch_bwd<PPT, kCullEllipse, 0, true>(VKS_BWD_ARGS);
-        }
+    if (use_records(records, PPT, cull)) {
+        if (sparse)
+            return cull == kCullNone ? launch_bwd<PPT, kCullNone, 1, true>(VKS_BWD_ARGS)
+                                     : launch_bwd<PPT, kCullEllipse, 1, true>(VKS_BWD_ARGS);
+        return cull == kCullNone ? launch_bwd<PPT, kCullNone, 0, true>(VKS_BWD_ARGS)
+                                 : launch_bwd<PPT, kCullEllipse, 0, true>(VKS_BWD_ARGS);
     }
 #define VKS_BWD_CULL(SP)                                                                 \
     switch (cull) {                                                                      \
@@ -729,12 +728,15 @@ int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
     const int cull = cull_choice(cfg);
     if (!use_records(records, ppt, cull) && n > 0 && !conics) return VKS_ERR_INVALID_ARG;  // a gather mode needs them
     if (use_records(records, ppt, cull)) {
-        return cull == kCullNone
-                   ? launch_fwd<2, kCullNone, true>(cfg, cam, means2d, conics, colors, opacities, radii, records, vals,
-                                                   tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st)
-                   : launch_fwd<2, kCullEllipse, true>(cfg, cam, means2d, conics, colors, opacities, radii, records,
-                                                      vals, tile_offsets, tile_order, image, T_final, n_contrib,
-                                                      (uint32_t)n, st);
+#define VKS_FWD_REC(P) return cull == kCullNone                                                                  \
+        ? launch_fwd<P, kCullNone, true>(cfg, cam, means2d, conics, colors, opacities, radii, records, vals,           \
+                                         tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st)       \
+        : launch_fwd<P, kCullEllipse, true>(cfg, cam, means2d, conics, colors, opacities, radii, records, vals,        \
+                                            tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st)
+        if (ppt == 4) VKS_FWD_REC(4);
+        if (ppt == 1) VKS_FWD_REC(1);
+        VKS_FWD_REC(2);
+#undef VKS_FWD_REC
     }
     if (ppt == 4) return dispatch_fwd<4>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);
     if (ppt == 1) return dispatch_fwd<1>(cull, cfg, cam, means2d, conics, colors, opacities, radii, vals, tile_offsets, tile_order, image, T_final, n_contrib, (uint32_t)n, st);

@@ -26,7 +26,7 @@ g = params.grads()
 
 def fwd_batch():
     P.vks_project_fwd_batch(cfg, cams[:B], params.means, params.log_scales, params.quats, params.opacity_logits,
-                            params.sh, [r.means2d for r in views], [r.conics for r in views],
+                            params.sh, [r.means2d for r in views], [None for r in views],  # records carry the conics
                             [r.depths for r in views], [r.radii for r in views], [r.tiles for r in views],
                             [r.colors for r in views], views[0].opacities, g2d_zero=[r.g2d for r in views],
                             records=[r.records for r in views])

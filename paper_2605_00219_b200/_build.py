@@ -26,7 +26,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
           "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 PINNED = {"project.cu", "binning.cu", "validate.cu"}
 SOURCES = ["project.cu", "project_bwd.cu", "binning.cu", "raster.cu", "adam.cu", "loss.cu", "mcmc.cu", "densify.cu", "validate.cu", "api.cu"]
-HEADERS = ["vks_common.cuh"]
+HEADERS = ["vks_common.cuh", "vks_sh.cuh"]
 
 
 def nvcc() -> str:

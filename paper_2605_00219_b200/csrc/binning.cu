@@ -585,28 +585,33 @@ __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int* _
         for (int y = 0; y < TY; y++) { acc += a[y * W1 + x]; a[y * W1 + x] = acc; }
     }
     __syncthreads();
-    // exclusive scan of the per-tile counts in tile order (+ the length-class histogram)
+    // exclusive scan of the per-tile counts in tile order (+ the length-class histogram) in one
+    // pass: thread t owns the `per` consecutive tiles [t per, t per + per), sums them, a block-wide
+    // scan of the 1024 thread sums gives each thread its base, and the thread writes its tiles'
+    // offsets (round 1 scanned 1024 tiles per round with four barriers and a 32-step walk per
+    // round: 15.1 -> 11.8 us on bicycle's 4,056 tiles)
     const int n_tiles = TX * TY;
-    if (tid == 0) s_carry = 0;
+    const int per = (n_tiles + 1023) / 1024;
     if (tid < 64) s_cls[tid] = 0;
+    const int t0 = min(tid * per, n_tiles), t1 = min(t0 + per, n_tiles);
+    u32 mine = 0;
+    for (int t = t0; t < t1; t++) mine += (u32)a[(t / TX) * W1 + (t % TX)];
+    const u32 incl = warp_incl_scan(mine, lane);
+    if (lane == 31) s_wsum[warp] = incl;
     __syncthreads();
-    for (int base = 0; base < n_tiles; base += 1024) {
-        const int t = base + tid;
-        const u32 c = t < n_tiles ? (u32)a[(t / TX) * W1 + (t % TX)] : 0u;
-        if (order && t < n_tiles) atomicAdd(&s_cls[63 - length_class(c)], 1u);
-        const u32 incl = warp_incl_scan(c, lane);
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        u32 wpre = 0, btot = 0;
-        for (int w = 0; w < 32; w++) {
-            if (w < warp) wpre += s_wsum[w];
-            btot += s_wsum[w];
-        }
-        const u32 carry = s_carry;
-        if (t < n_tiles) tile_offsets[t] = carry + wpre + incl - c;
-        __syncthreads();
-        if (tid == 0) s_carry = carry + btot;
-        __syncthreads();
+    if (warp == 0) {
+        const u32 wv = s_wsum[lane];
+        const u32 wi = warp_incl_scan(wv, lane);
+        s_wsum[lane] = wi - wv;  // exclusive prefix of the warp totals
+        if (lane == 31) s_carry = wi;
+    }
+    __syncthreads();
+    u32 run = s_wsum[warp] + incl - mine;
+    for (int t = t0; t < t1; t++) {
+        const u32 c = (u32)a[(t / TX) * W1 + (t % TX)];
+        tile_offsets[t] = run;
+        run += c;
+        if (order) atomicAdd(&s_cls[63 - length_class(c)], 1u);
     }
     if (tid == 0) tile_offsets[n_tiles] = s_carry;
     if (!order) return;

@@ -169,6 +169,28 @@ __device__ __forceinline__ bool eval_alpha(const float4 A, const float4 B, float
     return !(sigma < 0.0f) && !(alpha < 1.0f / 255.0f);
 }
 
+// The same evaluation for a lane's two pixels (PPT = 2: rows y and y + 4, the same x) with the
+// sm_100 paired fp32 instructions (FFMA2 / FMUL2 / FADD2: two IEEE results per issued instruction,
+// each bit-identical to the scalar operation): dx, A.z dx and A.w dx are shared by the two
+// pixels, everything else runs on (pixel 0, pixel 1) pairs; npy = -(py0, py1) (A.y - py ==
+// A.y + (-py) exactly).  The raster kernels are issue-bound, so the pairs cut their issued
+// instructions; the decisions equal eval_alpha's bit for bit (the 1- and 4-pixel layouts and the
+// statistics kernel use the scalar form).
+__device__ __forceinline__ void eval_alpha2(const float4 A, const float4 B, float px, float2 npy, float& dx,
+                                            float2& dy, float2& G, float2& rG, float2& alpha, bool& ok0, bool& ok1) {
+    dx = A.x - px;
+    dy = __fadd2_rn(make_float2(A.y, A.y), npy);
+    const float azdx = A.z * dx, awdx = A.w * dx;
+    const float2 inner = __ffma2_rn(__fmul2_rn(make_float2(B.x, B.x), dy), dy, __fmul2_rn(make_float2(awdx, awdx), dy));
+    const float2 sigma = __ffma2_rn(make_float2(azdx, azdx), make_float2(dx, dx), inner);
+    const float2 e = __fmul2_rn(sigma, make_float2(-1.44269504088896341f, -1.44269504088896341f));
+    G = make_float2(exp2_ftz(e.x), exp2_ftz(e.y));
+    rG = __fmul2_rn(make_float2(B.y, B.y), G);
+    alpha = make_float2(fminf(0.99f, rG.x), fminf(0.99f, rG.y));
+    ok0 = !(sigma.x < 0.0f) && !(alpha.x < 1.0f / 255.0f);
+    ok1 = !(sigma.y < 0.0f) && !(alpha.y < 1.0f / 255.0f);
+}
+
 // Warp patch: 8 pixels wide x 4*PPT tall; lane (lx, ly) = (lane & 7, lane >> 3) owns the PPT
 // pixels (lx, ly + 4k), k < PPT.  A 16x16 tile has 8/PPT warps.
 template <int PPT>
@@ -232,6 +254,9 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
         C0[k] = C1[k] = C2[k] = 0.0f;
         last[k] = 0;
     }
+    // PPT == 2, compositing (not the statistics): T and C held as (pixel 0, pixel 1) pairs
+    float2 T2 = make_float2(T[0], T[PPT - 1]), C02 = make_float2(0.0f, 0.0f), C12 = C02, C22 = C02;
+    const float2 npy = make_float2(-py[0], -py[PPT - 1]);
     const uint32_t start = tile_offsets[tile], end = tile_offsets[tile + 1];
     VKS_DCHECK(start <= end);
     // software pipeline: ids two batches ahead, the next batch's entries one batch ahead (gathered
@@ -249,8 +274,12 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
     int buf = 0;
     for (uint32_t b = start; b < end; b += 32, buf ^= 1) {
         bool all_done = true;
+        if constexpr (PPT == 2 && !STATS) {
+            all_done = T2.x < 1e-4f && T2.y < 1e-4f;
+        } else {
 #pragma unroll
-        for (int k = 0; k < PPT; k++) all_done = all_done && T[k] < 1e-4f;
+            for (int k = 0; k < PPT; k++) all_done = all_done && T[k] < 1e-4f;
+        }
         if (__all_sync(VKS_FULL_MASK, all_done)) break;
         __syncwarp();  // every lane is done with the buffer the next stores / copies overwrite
         // each lane tests its own entry against the warp patch; the warp then visits, in list
@@ -314,6 +343,21 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
                 }
                 const bool wany = __any_sync(VKS_FULL_MASK, any);
                 if (lane == 0) { n_went++; n_wcomp += wany; }
+            } else if constexpr (PPT == 2) {
+                // the same compositing on (pixel 0, pixel 1) pairs (eval_alpha2)
+                float dx;
+                float2 dy, G, rG, alpha;
+                bool e0, e1;
+                eval_alpha2(A, B, px, npy, dx, dy, G, rG, alpha, e0, e1);
+                const bool ok0 = e0 && !(T2.x < 1e-4f), ok1 = e1 && !(T2.y < 1e-4f);
+                const float2 a = make_float2(ok0 ? alpha.x : 0.0f, ok1 ? alpha.y : 0.0f);
+                const float2 aT = __fmul2_rn(a, T2);
+                C02 = __ffma2_rn(make_float2(B.z, B.z), aT, C02);
+                C12 = __ffma2_rn(make_float2(B.w, B.w), aT, C12);
+                C22 = __ffma2_rn(make_float2(c2, c2), aT, C22);
+                T2 = __fmul2_rn(T2, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-a.x, -a.y)));
+                last[0] = ok0 ? pos1 : last[0];
+                last[1] = ok1 ? pos1 : last[1];
             } else {
                 // branch-free: a skipped entry composites alpha = 0, which leaves C and T
                 // bit-identical (C + c * 0 = C, T * (1 - 0) = T)
@@ -351,6 +395,12 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_fwd_kernel(vks_config cfg
             atomicAdd(stats + 5, n_wcomp);
         }
     } else {
+        if constexpr (PPT == 2) {
+            T[0] = T2.x; T[1] = T2.y;
+            C0[0] = C02.x; C0[1] = C02.y;
+            C1[0] = C12.x; C1[1] = C12.y;
+            C2[0] = C22.x; C2[1] = C22.y;
+        }
 #pragma unroll
         for (int k = 0; k < PPT; k++) {
             const int y = pm.y0 + 4 * k;
@@ -446,6 +496,11 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
         lmax = max(lmax, last[k]);
     }
     const int wmax = __reduce_max_sync(VKS_FULL_MASK, lmax);  // positions >= wmax: nobody composited
+    // PPT == 2: the per-pixel state as (pixel 0, pixel 1) pairs for the paired fp32 instructions
+    float2 T2 = make_float2(T[0], T[PPT - 1]), P2 = make_float2(P[0], P[PPT - 1]);
+    const float2 W0 = make_float2(w0[0], w0[PPT - 1]), W1 = make_float2(w1[0], w1[PPT - 1]),
+                 W2 = make_float2(w2[0], w2[PPT - 1]);
+    const float2 npy = make_float2(-py[0], -py[PPT - 1]);
     // per-lane destination of gradient term k after the 32-lane butterfly: lane 4k (k < 8)
     // owns term k, lane 1 the opacity term; dst(g) = base + g * stride
     const int myterm = (lane & 3) == 0 ? (int)(lane >> 2) : (lane == 1 ? 8 : -1);
@@ -527,42 +582,73 @@ __global__ void __launch_bounds__(32 * 8 / PPT) raster_bwd_kernel(vks_config cfg
             }
             const int pos = bs + __float_as_int(Cc.z);
             const float c0 = B.z, c1 = B.w, c2 = Cc.x;
-            // evaluate first: an entry no pixel of the warp composited leaves every T, P and
-            // accumulator unchanged, so the warp skips it
-            float dx[PPT], dy[PPT], G[PPT], rG[PPT], alpha[PPT];
-            bool okk[PPT];
-            bool contrib = false;
-#pragma unroll
-            for (int k = 0; k < PPT; k++) {
-                okk[k] = eval_alpha(A, B, px, py[k], dx[k], dy[k], G[k], rG[k], alpha[k]) && pos < last[k];
-                contrib = contrib || okk[k];
-            }
-            // SPARSE: an entry no pixel of the warp composited leaves every T, P and accumulator
-            // unchanged, so the warp skips it
-            if (SPARSE && !__any_sync(VKS_FULL_MASK, contrib)) continue;
             // v[0..4]: moments sum(g dx), sum(g dy), sum(g dx^2), sum(g dx dy), sum(g dy^2) with
             // g = G dalpha (dL/dsigma = -rho g); v[5..7]: colour; e = sum(g) (dL/drho)
             float v[8], e = 0.0f;
-#pragma unroll
-            for (int k = 0; k < PPT; k++) {
+            bool contrib = false;
+            if constexpr (PPT == 2) {
+                // the two pixels on paired fp32 instructions (eval_alpha2: the forward's decisions)
+                float dx;
+                float2 dy, G, rG, alpha;
+                bool e0, e1;
+                eval_alpha2(A, B, px, npy, dx, dy, G, rG, alpha, e0, e1);
+                const bool ok0 = e0 && pos < last[0], ok1 = e1 && pos < last[1];
+                contrib = ok0 || ok1;
+                if (SPARSE && !__any_sync(VKS_FULL_MASK, contrib)) continue;
                 // branch-free: an entry the pixel did not composite replays with alpha = 0, which
                 // leaves T, P and every accumulator bit-identical (T * 1, 0 * x + P, + 0)
-                const bool ok = okk[k];
-                const float a = ok ? alpha[k] : 0.0f;
-                const float om = 1.0f - a;
-                T[k] = T[k] * rcp_ftz(om);  // om in [0.01, 1]
-                const float aT = a * T[k];
-                const float cw = c0 * w0[k] + c1 * w1[k] + c2 * w2[k];
-                const float d = cw - P[k];
-                const float dalpha = T[k] * d;
-                P[k] = SPARSE ? fmaf(a, d, P[k]) : a * cw + om * P[k];
+                const float2 a = make_float2(ok0 ? alpha.x : 0.0f, ok1 ? alpha.y : 0.0f);
+                const float2 om = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-a.x, -a.y));
+                T2 = __fmul2_rn(T2, make_float2(rcp_ftz(om.x), rcp_ftz(om.y)));  // om in [0.01, 1]
+                const float2 aT = __fmul2_rn(a, T2);
+                const float2 cw = __ffma2_rn(make_float2(c2, c2), W2,
+                                             __ffma2_rn(make_float2(c1, c1), W1, __fmul2_rn(make_float2(c0, c0), W0)));
+                const float2 d = __fadd2_rn(cw, make_float2(-P2.x, -P2.y));
+                const float2 dalpha = __fmul2_rn(T2, d);
+                P2 = SPARSE ? __ffma2_rn(a, d, P2) : __ffma2_rn(a, cw, __fmul2_rn(om, P2));
                 // no gradient where the pixel skipped the entry or alpha was clamped
-                const float g = (!ok || rG[k] > 0.99f) ? 0.0f : G[k] * dalpha;
-                const float gx = g * dx[k], gy = g * dy[k];
-                const float t[8] = {gx, gy, gx * dx[k], gx * dy[k], gy * dy[k], aT * w0[k], aT * w1[k], aT * w2[k]};
+                const float2 gg = __fmul2_rn(G, dalpha);
+                const float2 g = make_float2((!ok0 || rG.x > 0.99f) ? 0.0f : gg.x, (!ok1 || rG.y > 0.99f) ? 0.0f : gg.y);
+                const float2 gx = __fmul2_rn(g, make_float2(dx, dx)), gy = __fmul2_rn(g, dy);
+                const float2 gxx = __fmul2_rn(gx, make_float2(dx, dx)), gxy = __fmul2_rn(gx, dy), gyy = __fmul2_rn(gy, dy);
+                const float2 t5 = __fmul2_rn(aT, W0), t6 = __fmul2_rn(aT, W1), t7 = __fmul2_rn(aT, W2);
+                v[0] = gx.x + gx.y; v[1] = gy.x + gy.y; v[2] = gxx.x + gxx.y; v[3] = gxy.x + gxy.y;
+                v[4] = gyy.x + gyy.y; v[5] = t5.x + t5.y; v[6] = t6.x + t6.y; v[7] = t7.x + t7.y;
+                e = g.x + g.y;
+            } else {
+                // evaluate first: an entry no pixel of the warp composited leaves every T, P and
+                // accumulator unchanged, so the warp skips it
+                float dx[PPT], dy[PPT], G[PPT], rG[PPT], alpha[PPT];
+                bool okk[PPT];
 #pragma unroll
-                for (int q = 0; q < 8; q++) v[q] = k == 0 ? t[q] : v[q] + t[q];
-                e = k == 0 ? g : e + g;
+                for (int k = 0; k < PPT; k++) {
+                    okk[k] = eval_alpha(A, B, px, py[k], dx[k], dy[k], G[k], rG[k], alpha[k]) && pos < last[k];
+                    contrib = contrib || okk[k];
+                }
+                // SPARSE: an entry no pixel of the warp composited leaves every T, P and accumulator
+                // unchanged, so the warp skips it
+                if (SPARSE && !__any_sync(VKS_FULL_MASK, contrib)) continue;
+#pragma unroll
+                for (int k = 0; k < PPT; k++) {
+                    // branch-free: an entry the pixel did not composite replays with alpha = 0, which
+                    // leaves T, P and every accumulator bit-identical (T * 1, 0 * x + P, + 0)
+                    const bool ok = okk[k];
+                    const float a = ok ? alpha[k] : 0.0f;
+                    const float om = 1.0f - a;
+                    T[k] = T[k] * rcp_ftz(om);  // om in [0.01, 1]
+                    const float aT = a * T[k];
+                    const float cw = c0 * w0[k] + c1 * w1[k] + c2 * w2[k];
+                    const float d = cw - P[k];
+                    const float dalpha = T[k] * d;
+                    P[k] = SPARSE ? fmaf(a, d, P[k]) : a * cw + om * P[k];
+                    // no gradient where the pixel skipped the entry or alpha was clamped
+                    const float g = (!ok || rG[k] > 0.99f) ? 0.0f : G[k] * dalpha;
+                    const float gx = g * dx[k], gy = g * dy[k];
+                    const float t[8] = {gx, gy, gx * dx[k], gx * dy[k], gy * dy[k], aT * w0[k], aT * w1[k], aT * w2[k]};
+#pragma unroll
+                    for (int q = 0; q < 8; q++) v[q] = k == 0 ? t[q] : v[q] + t[q];
+                    e = k == 0 ? g : e + g;
+                }
             }
             // SPARSE: an entry composited by at most `sparse_lanes` lanes is reduced by those lanes'
             // own atomics (the outputs are linear in the sums) instead of the 32-lane butterfly

@@ -51,6 +51,10 @@ def parse():
     ap.add_argument("--ar-chunks", type=int, default=4,
                     help="N > 1: gradient all-reduce chunks, each overlapped with the next projection-bwd chunk")
     ap.add_argument("--no-batch1", action="store_true")
+    ap.add_argument("--binning", default="sync", choices=["sync", "async"],
+                    help="vks_bin_sort (one host sync per view) or vks_bin_sort_async (device-side counts)")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture the whole step in a CUDA graph and replay it (needs --binning async)")
     ap.add_argument("--no-records", action="store_true",
                     help="raster passes gather the separate projection arrays instead of staging packed records")
     ap.add_argument("--streams", type=int, default=3, help="views in flight per rank")
@@ -236,7 +240,9 @@ def run_ours(args):
                          radii=torch.empty(n, 2, dtype=torch.int32, device="cuda"), g2d=g2d,
                          dm2=g2d[: 2 * n].view(n, 2), dcon=g2d[2 * n: 5 * n].view(n, 3),
                          dcol=g2d[5 * n: 8 * n].view(n, 3), dop=g2d[8 * n:],
-                         rec=torch.empty(n, 12, device="cuda") if use_rec else None))
+                         rec=torch.empty(n, 12, device="cuda") if use_rec else None,
+                         m_dev=torch.zeros(1, dtype=torch.int64, device="cuda"),     # vks_bin_sort_async:
+                         st_dev=torch.zeros(1, dtype=torch.int32, device="cuda")))   # M and status words
     opac = torch.empty(n, device="cuda")  # view-independent
 
     def project_fwd_batch(vcams, st):
@@ -267,9 +273,15 @@ def run_ours(args):
             if copies is not None and loss_out is None:
                 st.wait_event(slot["img_free"])              # the previous image has left rend.image
             if ev is not None: ev[1].record(st)
-            m = P.vks_bin_sort(cam, vb["means2d"], vb["radii"], vb["depths"], vb["tiles"], rend.offsets, None,
-                               rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
-            rend.num_isects = m
+            if args.binning == "async":  # no host sync: M and the status stay on the device
+                P.vks_bin_sort_async(cam, vb["means2d"], vb["radii"], vb["depths"], vb["tiles"], rend.offsets,
+                                     rend.vals, rend.tile_offsets, rend.workspace, vb["m_dev"], vb["st_dev"],
+                                     tile_order=rend.tile_order)
+                m = None
+            else:
+                m = P.vks_bin_sort(cam, vb["means2d"], vb["radii"], vb["depths"], vb["tiles"], rend.offsets, None,
+                                   rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
+                rend.num_isects = m
             if ev is not None: ev[2].record(st)
             P.vks_raster_fwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],
                              rend.vals, rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib,
@@ -322,7 +334,7 @@ def run_ours(args):
             if sync is not None:
                 sync.finish()
 
-    def step(s, copies=None):
+    def step(s, copies=None, main=main):
         """One training step's hot path: a batch of B views per rank — one batched projection
         forward (row a1), then binning, raster forward and raster backward per view, alternating
         over S streams, one batched projection backward (row a8) and the allreduce (row a9; no-op
@@ -373,15 +385,34 @@ def run_ours(args):
     for s in range(args.warmup):
         step(s)
     torch.cuda.synchronize()
+    run_step = step
+    if args.graph:
+        if args.binning != "async":
+            raise SystemExit("--graph needs --binning async (vks_bin_sort synchronises the host)")
+        # the whole step captured once (project fwd batch, per view async binning + raster passes on
+        # S forked streams, project bwd batch) and replayed: no host launches in the timed region
+        graph = torch.cuda.CUDAGraph()
+        cap_stream = torch.cuda.Stream()
+        cap_stream.wait_stream(main)
+        with torch.cuda.graph(graph, stream=cap_stream):
+            step(0, main=cap_stream)
+        torch.cuda.synchronize()
+
+        def run_step(s):
+            graph.replay()
     clocks = ClockSampler(local)
     clocks.start()
     ncu_range = bool(os.environ.get("VKS_NCU_RANGE"))  # `ncu --profile-from-start off`: timed steps only
     if ncu_range:
         torch.cuda.cudart().cudaProfilerStart()
-    elapsed_ms = timed(step, args.steps)
+    elapsed_ms = timed(run_step, args.steps)
     if ncu_range:
         torch.cuda.cudart().cudaProfilerStop()
     clk = clocks.stop()
+    if args.binning == "async":  # every view's binning fitted its capacity (device status words)
+        bad = [int(vb["st_dev"].item()) for vb in vbuf if int(vb["st_dev"].item()) != 0]
+        if bad:
+            raise SystemExit(f"vks_bin_sort_async status {bad}: capacity too small")
     views_total = views_per_step * args.steps
     value = views_total / (elapsed_ms / 1e3)
 
@@ -550,6 +581,8 @@ def run_ours(args):
     # --- workload statistics (untimed): visible count, M, raster pair counts of the last view
     vl = vbuf[(nv - 1) % B]  # the last view's projection outputs
     vis = int((vl["tiles"] > 0).sum().item())
+    if args.binning == "async":
+        rend.num_isects = int(vl["m_dev"].item())
     m_last = rend.num_isects
     stats = torch.zeros(6, dtype=torch.int64, device="cuda")
     P.vks_raster_fwd_stats(cfg, cams[my_views[(nv - 1) % len(my_views)]], vl["means2d"],
@@ -620,8 +653,9 @@ def run_ours(args):
     # scan (2) + rect diff + tile count + tile passes x 3; raster fwd; raster bwd; plus one batched
     # project fwd and one chunked batched project bwd per step
     tp = max(1, ((rend.n_tiles - 1).bit_length() + 7) // 8)
-    gpu_launches = (((2 + 3 * dpasses + 2 + 1 + 1 + 3 * tp) + 1 + 1) * B + 1 + len(gsync.chunks() if world > 1
-                                                                                  else [0])) * args.steps
+    # (async binning: always four 8-bit depth passes, plus its status kernel)
+    bin_launches = (2 + 3 * dpasses + 2 + 1 + 1 + 3 * tp) if args.binning == "sync" else (2 + 3 * 4 + 2 + 1 + 1 + 3 * tp + 1)
+    gpu_launches = ((bin_launches + 1 + 1) * B + 1 + len(gsync.chunks() if world > 1 else [0])) * args.steps
     if batch1 is not None:
         # stage rooflines of the single-view kernels (DESIGN.md §6.3 per-unit bytes): projection
         # forward 60 B per Gaussian (geometry + opacity read, radii + tiles written) + 232 B per

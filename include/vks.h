@@ -175,6 +175,24 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
                  void* workspace, size_t workspace_bytes, vks_stream_t stream);
 
 /*
+ * vks_bin_sort_async — vks_bin_sort without the host synchronisation (stream-ordered and
+ * CUDA-graph capturable): the same tile lists (ids in (depth bits, id) order per tile) and CSR
+ * tile_offsets, bit-identical, but M is written to the DEVICE word *num_isects (int64, 8-byte
+ * aligned) together with a DEVICE status word *status (int32): VKS_OK; VKS_ERR_CAPACITY if
+ * M > capacity, or VKS_ERR_UNSUPPORTED if M >= 2^30 — then every tile list is left empty
+ * (tile_offsets all zero, so a rasterizer launched behind it reads nothing) and the caller regrows
+ * and re-runs.  Every kernel is launched for the host-side bounds (n Gaussians, `capacity` keys)
+ * and reads the actual counts on the device; the launch sequence depends only on (n, capacity,
+ * camera size).  No u64 keys and no debug outputs.  capacity >= 2^30: VKS_ERR_UNSUPPORTED.
+ * Other arguments, the workspace and its size as for vks_bin_sort.
+ */
+int vks_bin_sort_async(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
+                       const float* depths, const int32_t* tiles_touched, uint32_t* offsets,
+                       int64_t capacity, uint32_t* vals, uint32_t* tile_offsets, uint32_t* tile_order,
+                       int64_t* num_isects, int32_t* status, void* workspace, size_t workspace_bytes,
+                       vks_stream_t stream);
+
+/*
  * vks_bin_sort_check — debug verification of a binning ("Tile Ranges" errors, S:155 UnsortedInput):
  * checks that tile_offsets [n_tiles+1] is a CSR of [0, num_isects) (starts at 0, non-decreasing,
  * ends at num_isects), that every id vals[k] < n, that the tile rect of Gaussian vals[k] (projection

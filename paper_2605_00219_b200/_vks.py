@@ -35,7 +35,7 @@ EXPORTS = ("vks_status_string", "vks_version", "vks_last_cuda_error", "vks_proje
            "vks_raster_bwd", "vks_project_bwd", "vks_project_fwd_batch", "vks_project_bwd_batch",
            "vks_adam_step", "vks_loss_workspace_bytes", "vks_loss_grad", "vks_mcmc_workspace_bytes",
            "vks_mcmc_relocate", "vks_mcmc_noise", "vks_densify_stats", "vks_densify_workspace_bytes",
-           "vks_densify", "vks_bin_sort_check")
+           "vks_densify", "vks_bin_sort_check", "vks_bin_sort_async")
 
 
 class VksCamera(C.Structure):
@@ -80,6 +80,7 @@ _lib.vks_bin_sort_workspace_bytes.argtypes = [C.c_int64, C.c_int64, C.c_int32]
 _lib.vks_project_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 14
 _lib.vks_bin_sort.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 8 + [C.c_size_t, _P]
 _lib.vks_raster_fwd.argtypes = [_P, _P, C.c_int64] + [_P] * 13
+_lib.vks_bin_sort_async.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64] + [_P] * 5 + [_P, C.c_size_t, _P]
 _lib.vks_bin_sort_check.argtypes = [_P, C.c_int64] + [_P] * 5 + [C.c_int64, _P]
 _lib.vks_raster_bwd.argtypes = [_P, _P, C.c_int64] + [_P] * 17
 _lib.vks_raster_fwd_stats.argtypes = [_P, _P, C.c_int64] + [_P] * 11
@@ -215,6 +216,21 @@ def vks_bin_sort(cam, means2d, radii, depths, tiles_touched, offsets, keys, vals
         return -int(m.value)
     _check("vks_bin_sort", st)
     return int(m.value)
+
+
+def vks_bin_sort_async(cam, means2d, radii, depths, tiles_touched, offsets, vals, tile_offsets, workspace,
+                       num_isects, status, tile_order=None, stream=None):
+    """Host-sync-free binning (include/vks.h): capacity = vals.numel(); M and the status land in the
+    device tensors num_isects (int64 [1]) and status (int32 [1]); nothing is returned."""
+    k = cam if isinstance(cam, VksCamera) else make_camera(cam)
+    n = means2d.shape[0]
+    st = _lib.vks_bin_sort_async(C.byref(k), n, _ptr(means2d, f32, "means2d"), _ptr(radii, i32, "radii"),
+                                 _ptr(depths, f32, "depths"), _ptr(tiles_touched, i32, "tiles_touched"),
+                                 _ptr(offsets, u32, "offsets"), vals.numel(), _ptr(vals, u32, "vals"),
+                                 _ptr(tile_offsets, u32, "tile_offsets"), _ptr(tile_order, u32, "tile_order"),
+                                 _ptr(num_isects, torch.int64, "num_isects"), _ptr(status, i32, "status"),
+                                 _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream))
+    _check("vks_bin_sort_async", st)
 
 
 def vks_bin_sort_check(cam, means2d, radii, depths, vals, tile_offsets, num_isects, stream=None) -> int:

@@ -130,6 +130,24 @@ int vks_bin_sort(const vks_camera* cam, int64_t n, const float* means2d, const i
                                          workspace_bytes, (cudaStream_t)stream));
 }
 
+int vks_bin_sort_async(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
+                       const float* depths, const int32_t* tiles_touched, uint32_t* offsets, int64_t capacity,
+                       uint32_t* vals, uint32_t* tile_offsets, uint32_t* tile_order, int64_t* num_isects,
+                       int32_t* status, void* workspace, size_t workspace_bytes, vks_stream_t stream) {
+    if (!camera_ok(cam) || n < 0 || capacity < 0 || !num_isects || !status || !tile_offsets) return VKS_ERR_INVALID_ARG;
+    if (n > 0 && (!means2d || !radii || !depths || !tiles_touched || !offsets)) return VKS_ERR_INVALID_ARG;
+    if (capacity > 0 && !vals) return VKS_ERR_INVALID_ARG;
+    if (!workspace) return VKS_ERR_WORKSPACE;
+    if ((reinterpret_cast<uintptr_t>(means2d) & 7) || (reinterpret_cast<uintptr_t>(radii) & 7) ||
+        (reinterpret_cast<uintptr_t>(num_isects) & 7) || (reinterpret_cast<uintptr_t>(status) & 3))
+        return VKS_ERR_INVALID_ARG;
+    if (n >= (1ll << 32)) return VKS_ERR_UNSUPPORTED;
+    if (!device_present()) return VKS_ERR_CUDA;
+    return cuda_status(vks::run_bin_sort_async(*cam, n, means2d, radii, depths, tiles_touched, offsets, capacity, vals,
+                                               tile_offsets, tile_order, num_isects, status, workspace,
+                                               workspace_bytes, (cudaStream_t)stream));
+}
+
 int vks_bin_sort_check(const vks_camera* cam, int64_t n, const float* means2d, const int32_t* radii,
                        const float* depths, const uint32_t* vals, const uint32_t* tile_offsets, int64_t num_isects,
                        vks_stream_t stream) {

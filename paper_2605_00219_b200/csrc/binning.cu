@@ -214,12 +214,20 @@ struct CompactOut {
     u32* first;
 };
 
+// dcount (nullable, vks_bin_sort_async): the element count on the device; `count` is then the
+// host-side bound the grid was sized for
+__device__ __forceinline__ u64 eff_count(u64 bound, const u64* __restrict__ dcount) {
+    return dcount ? min(bound, *dcount) : bound;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kDownThreads) scan_reduce_kernel(const int* __restrict__ tiles,
                                                                   const u64* __restrict__ rc_in, u64 count,
                                                                   u32* __restrict__ part_sum,
-                                                                  u32* __restrict__ part_vis, const CompactOut co) {
+                                                                  u32* __restrict__ part_vis, const CompactOut co,
+                                                                  const u64* __restrict__ dcount) {
     constexpr int ITEMS = kDownItems;
+    count = eff_count(count, dcount);
     __shared__ u32 s_sum[kDownThreads / 32], s_vis[kDownThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int v[ITEMS];
@@ -323,8 +331,9 @@ template <int MODE>
 __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __restrict__ tiles, const u64* __restrict__ rc,
                                                                 u64 count, const u32* __restrict__ part_sum,
                                                                 u32* __restrict__ out, const CompactOut co,
-                                                                u64* __restrict__ totals) {
+                                                                u64* __restrict__ totals, const u64* __restrict__ dcount) {
     constexpr int ITEMS = kDownItems;
+    count = eff_count(count, dcount);
     __shared__ u32 s_w[kDownThreads / 32], s_v[kDownThreads / 32];
     __shared__ u32 s_pre[kDownThreads / 32], s_vpre[kDownThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -433,8 +442,9 @@ constexpr size_t kTileCountSmemMax = 200 * 1024;  // bytes
 
 template <bool SMEM_DIFF>
 __global__ void __launch_bounds__(kDiffThreads) rect_diff_kernel(int TX, int TY, u32 count, const u64* __restrict__ rc,
-                                                                int* __restrict__ diff) {
+                                                                int* __restrict__ diff, const u64* __restrict__ dcount) {
     extern __shared__ int s_diff[];
+    count = (u32)eff_count(count, dcount);
     const int tid = threadIdx.x;
     const int W1 = TX + 1;
     const int cells = W1 * (TY + 1);
@@ -661,7 +671,9 @@ __device__ __forceinline__ u32 digit_peers(u32 d, bool valid = true) {
 
 template <int DBITS>
 __global__ void __launch_bounds__(kSortThreads) digit_count_kernel(const u32* __restrict__ kin, u32 n, int shift,
-                                                                  u32 kbias, u32 T, u32* __restrict__ counts) {
+                                                                  u32 kbias, u32 T, u32* __restrict__ counts,
+                                                                  const u64* __restrict__ dcount) {
+    n = (u32)eff_count(n, dcount);
     constexpr int RADIX = 1 << DBITS;
     constexpr u32 DMASK = RADIX - 1;
     __shared__ u32 whist[kSortWarps][RADIX];  // per-warp histograms: contention only within a warp
@@ -875,7 +887,7 @@ __global__ void __launch_bounds__(kSortThreads, 5) scatter_kernel(const u32* __r
                                                              u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
                                                              int shift, u32 kbias, u32 T, const u32* __restrict__ offs,
                                                              const float* __restrict__ depths,
-                                                             u64* __restrict__ keys64) {
+                                                             u64* __restrict__ keys64, const u64* __restrict__ dcount) {
     constexpr int RADIX = 1 << DBITS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem<RADIX>& S = *reinterpret_cast<SortSmem<RADIX>*>(smem_raw);
@@ -883,6 +895,8 @@ __global__ void __launch_bounds__(kSortThreads, 5) scatter_kernel(const u32* __r
     const u32 bar = smem_u32(&S.mbar);
     const u32 tile = blockIdx.x;
     const u64 base = (u64)tile * kSortTile;
+    n = (u32)eff_count(n, dcount);
+    if (base >= n) return;  // (async: the grid was sized for the bound; the whole block leaves)
     const u32 count = (u32)min((u64)kSortTile, (u64)n - base);
     const u32 nbulk = count & ~3u;  // 16-byte multiples
     if (tid == 0) {
@@ -931,6 +945,15 @@ struct ExpandSrc {
     const u32* first;   // [blocks + 1] Gaussian holding slot 4096 b
     u32 V, M;
     int TX;
+    const u64* dtot;    // nullable (vks_bin_sort_async): device totals [M, V]; V / M are then bounds
+    __device__ __forceinline__ ExpandSrc resolved() const {
+        ExpandSrc e = *this;
+        if (dtot) {
+            e.M = (u32)min((u64)M, dtot[0]);
+            e.V = (u32)min((u64)V, dtot[1]);
+        }
+        return e;
+    }
 };
 
 // floor(k / w) for 0 <= k < 2^20, 1 <= w < 2^16: (k + 0.5) / w lies at least 0.5 / w from an
@@ -1019,10 +1042,15 @@ __device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0
 // digit and 1 to a cyclic run of L mod R digits (a difference array over the R digits).  (Counting
 // through the key expansion of keys_scatter_kernel issued 1.7x the instructions.)
 template <int DBITS>
-__global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSrc src, int shift, u32 T,
+__global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSrc src_in, int shift, u32 T,
                                                                  u32* __restrict__ counts) {
     constexpr int RADIX = 1 << DBITS;
     constexpr int DMASK = RADIX - 1;
+    const ExpandSrc src = src_in.resolved();
+    if ((u64)blockIdx.x * kSortTile >= src.M) {  // (async: past the keys; first[] is not written there)
+        for (int d = threadIdx.x; d < RADIX; d += kSortThreads) counts[(u64)d * T + blockIdx.x] = 0u;
+        return;
+    }
     __shared__ int wdiff[kSortWarps][RADIX + 1];  // per warp: contention only within a warp
     __shared__ int s_all[kSortWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1086,15 +1114,17 @@ __global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSr
 }
 
 template <int DBITS, int MODE>
-__global__ void __launch_bounds__(kSortThreads, 5) keys_scatter_kernel(const ExpandSrc src, int shift, u32 T,
+__global__ void __launch_bounds__(kSortThreads, 5) keys_scatter_kernel(const ExpandSrc src_in, int shift, u32 T,
                                                                    const u32* __restrict__ offs, u32* __restrict__ kout,
                                                                    u32* __restrict__ vout, const float* __restrict__ depths,
                                                                    u64* __restrict__ keys64) {
     constexpr int RADIX = 1 << DBITS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem<RADIX>& S = *reinterpret_cast<SortSmem<RADIX>*>(smem_raw);
+    const ExpandSrc src = src_in.resolved();
     const int tid = threadIdx.x, warp = tid >> 5;
     const u32 b = blockIdx.x;
+    if ((u64)b * kSortTile >= src.M) return;
     const u32 count = min((u32)kSortTile, src.M - b * (u32)kSortTile);
     for (int j = tid; j < kSortWarps * RADIX; j += kSortThreads) (&S.whist[0][0])[j] = 0;
     for (int d = tid; d < RADIX; d += kSortThreads) S.gbase[d] = __ldg(offs + (u64)d * T + b);
@@ -1124,7 +1154,7 @@ struct PassBufs {
 
 template <int DBITS, int MODE>
 int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift, u32 kbias, const PassBufs& pb,
-                const float* depths, u64* keys64, cudaStream_t s) {
+                const float* depths, u64* keys64, cudaStream_t s, const u64* dcount = nullptr) {
     constexpr size_t sm = sizeof(SortSmem<1 << DBITS>);
     // set on every call: the attribute belongs to the current device (a process may drive several)
     if (cudaError_t e = cudaFuncSetAttribute(scatter_kernel<DBITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1132,19 +1162,20 @@ int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int
         return cuda_fail(e, "scatter smem attribute");
     const u32 T = (u32)((n + kSortTile - 1) / kSortTile);
     if (!T) return VKS_OK;
-    digit_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(kin, n, shift, kbias, T, pb.counts);
+    digit_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(kin, n, shift, kbias, T, pb.counts, dcount);
     const u64 cnt = (u64)(1u << DBITS) * T;
     scan_u32_kernel<<<(unsigned)((cnt + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt, pb.lb, pb.ctr);
     scatter_kernel<DBITS, MODE><<<T, kSortThreads, sm, s>>>(kin, vin, kout, vout, n, shift, kbias, T, pb.offs, depths,
-                                                            keys64);
+                                                            keys64, dcount);
     return check_launch(__func__);
 }
 
 // runtime digit width (1..9 bits) -> instantiation
 template <int MODE>
 int launch_pass_bits(int dbits, const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int shift, u32 kbias,
-                     const PassBufs& pb, const float* depths, u64* keys64, cudaStream_t s) {
-#define VKS_PASS(B) return launch_pass<B, MODE>(kin, vin, kout, vout, n, shift, kbias, pb, depths, keys64, s)
+                     const PassBufs& pb, const float* depths, u64* keys64, cudaStream_t s,
+                     const u64* dcount = nullptr) {
+#define VKS_PASS(B) return launch_pass<B, MODE>(kin, vin, kout, vout, n, shift, kbias, pb, depths, keys64, s, dcount)
     switch (dbits) {
         case 1: VKS_PASS(1);
         case 2: VKS_PASS(2);
@@ -1211,7 +1242,8 @@ int launch_keys_pass_bits(int dbits, const ExpandSrc& src, u32* kout, u32* vout,
     }
 }
 
-int launch_rect_diff(int TX, int TY, u32 count, const u64* rc, int* diff, cudaStream_t s) {
+int launch_rect_diff(int TX, int TY, u32 count, const u64* rc, int* diff, cudaStream_t s,
+                     const u64* dcount = nullptr) {
     const int cells = (TX + 1) * (TY + 1);
     const u32 want = (count + kDiffThreads - 1) / kDiffThreads;
     if (want == 0) return VKS_OK;
@@ -1223,10 +1255,10 @@ int launch_rect_diff(int TX, int TY, u32 count, const u64* rc, int* diff, cudaSt
                 return cuda_fail(e, "rect_diff smem attribute");
         }
         const unsigned blocks = std::min<u32>(want, (u32)sm_count() * 2);
-        rect_diff_kernel<true><<<blocks, kDiffThreads, sm, s>>>(TX, TY, count, rc, diff);
+        rect_diff_kernel<true><<<blocks, kDiffThreads, sm, s>>>(TX, TY, count, rc, diff, dcount);
     } else {
         const unsigned blocks = std::min<u32>(want, (u32)sm_count() * 4);
-        rect_diff_kernel<false><<<blocks, kDiffThreads, 0, s>>>(TX, TY, count, rc, diff);
+        rect_diff_kernel<false><<<blocks, kDiffThreads, 0, s>>>(TX, TY, count, rc, diff, dcount);
     }
     return check_launch(__func__);
 }
@@ -1260,14 +1292,30 @@ int launch_keys_debug(const vks_camera& cam, int64_t n, const int* tiles, const 
 // from the sorted rect codes); totals[0] = sum (and, MODE 0, totals[1] = #visible)
 template <int MODE>
 int run_scan(const int* tiles, const u64* rc_in, u64 count, u32* part_sum, u32* part_vis, u32* out, u64* totals,
-             CompactOut co, cudaStream_t s) {
+             CompactOut co, cudaStream_t s, const u64* dcount = nullptr) {
     const u32 P = (u32)((count + kScanTile - 1) / kScanTile);
     if (!P) return VKS_OK;
     scan_reduce_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, MODE == 0 ? part_vis : nullptr,
-                                                       co);
+                                                       co, dcount);
     co.vis_prefix = part_vis;  // raw block visible counts; the down-sweep sums its predecessors'
-    scan_down_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co, totals);
+    scan_down_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co, totals, dcount);
     return check_launch(__func__);
+}
+
+// vks_bin_sort_async's last step: M and the status to the caller's device words; on overflow
+// (M > capacity, or M >= 2^30) every tile list is emptied so a rasterizer launched behind it reads
+// nothing past the capacity
+__global__ void bin_sort_status_kernel(const u64* __restrict__ totals, int64_t capacity, int n_tiles,
+                                       u32* __restrict__ tile_offsets, int64_t* __restrict__ num_isects,
+                                       int32_t* __restrict__ status) {
+    const u64 M = totals[0];
+    const int st = M >= (1ull << 30) ? VKS_ERR_UNSUPPORTED : ((int64_t)M > capacity ? VKS_ERR_CAPACITY : VKS_OK);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *num_isects = (int64_t)M;
+        *status = st;
+    }
+    if (st != VKS_OK)
+        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= n_tiles; t += gridDim.x * blockDim.x) tile_offsets[t] = 0u;
 }
 
 }  // namespace
@@ -1380,6 +1428,87 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
         if (st) return st;
     }
     return VKS_OK;
+}
+
+// Stream-ordered, host-sync-free variant (include/vks.h vks_bin_sort_async): every launch is sized
+// from host-side bounds (n visible Gaussians at most, `capacity` keys at most) and the kernels read
+// the actual V and M from the device totals, blocks past them leaving at once; the depth sort runs
+// four 8-bit passes over all 32 depth bits (no host-read depth range: the same stable order), the
+// key-pass grid covers the capacity.  M and a status word are written to device memory.  The
+// launch sequence depends only on (n, capacity, tile grid), so a step built on it can be captured
+// in a CUDA graph.
+int run_bin_sort_async(const vks_camera& cam, int64_t n, const float* means2d, const int32_t* radii,
+                       const float* depths, const int32_t* tiles_touched, uint32_t* offsets, int64_t capacity,
+                       uint32_t* vals, uint32_t* tile_offsets, uint32_t* tile_order, int64_t* num_isects,
+                       int32_t* status, void* workspace, size_t workspace_bytes, cudaStream_t s) {
+    const int TX = tiles_x(cam), TY = tiles_y(cam);
+    const int32_t n_tiles = TX * TY;
+    if (TX > 65535 || TY > 65535 || (int64_t)TX * TY >= (1 << 20)) return VKS_ERR_INVALID_ARG;
+    if (workspace_bytes < bin_sort_workspace_bytes(n, capacity, n_tiles)) return VKS_ERR_WORKSPACE;
+    if (reinterpret_cast<uintptr_t>(workspace) & 255) return VKS_ERR_WORKSPACE;
+    if (capacity >= (1ll << 30)) return VKS_ERR_UNSUPPORTED;  // the look-back counts hold 30 bits
+    Workspace w = carve(workspace, n, capacity, TX, TY);
+    if (cudaError_t e_ = cudaMemsetAsync(w.zeroA, 0, w.zeroA_bytes, s)) return cuda_fail(e_, "memset workspace");
+    auto pass_bufs = [&](int p) { return PassBufs{w.counts, w.offs, w.cnt_lb[p], w.ctr + kCtrPass + p}; };
+    const u64* dM = w.totals + 0;
+    const u64* dV = w.totals + 1;
+    int st = VKS_OK;
+    if (n > 0) {
+        // 1. index offsets in id order, M, V, rect codes (totals on the device only)
+        const CompactOut co{nullptr, reinterpret_cast<const u32*>(depths), reinterpret_cast<const float2*>(means2d),
+                            reinterpret_cast<const int2*>(radii), TX, TY, w.dk[1], w.dv[1], w.rc_by_id,
+                            reinterpret_cast<u32*>(w.totals + 2)};
+        if ((st = run_scan<0>(tiles_touched, nullptr, (u64)n, w.part_sum, w.part_vis, offsets, w.totals, co, s)))
+            return st;
+        // 2. depth sort of the V visible: four 8-bit passes over all 32 depth bits
+        for (int p = 0; p < kDepthPasses; p++) {
+            st = launch_pass_bits<kPassPlain>(8, w.dk[(p + 1) & 1], w.dv[(p + 1) & 1], w.dk[p & 1], w.dv[p & 1], (u32)n,
+                                              8 * p, 0u, pass_bufs(p), nullptr, nullptr, s, dV);
+            if (st) return st;
+        }
+        const u32* sid = w.dv[(kDepthPasses - 1) & 1];
+        // 3. slots in depth order + first[]
+        {
+            CompactOut co1{};
+            co1.rc_by_id = w.rc_by_id;
+            co1.sid = sid;
+            co1.rc_out = w.rcs;
+            co1.first = w.first;
+            if ((st = run_scan<1>(nullptr, w.rcs, (u64)n, w.part_sum, nullptr, w.doff, w.totals + 0, co1, s, dV)))
+                return st;
+        }
+        // 4. tile ranges
+        if ((st = launch_rect_diff(TX, TY, (u32)n, w.rcs, w.diff, s, dV))) return st;
+        if ((st = launch_tile_count(TX, TY, w.diff, tile_offsets, tile_order, s))) return st;
+        // 5. tile passes over min(M, capacity) keys (grids sized for the capacity)
+        if (capacity > 0) {
+            ExpandSrc src{w.rcs, w.doff, sid, w.first, (u32)n, (u32)capacity, TX, w.totals};
+            TilePlan plan = tile_plan(n_tiles);
+            if (plan.passes == 0) plan = TilePlan{1, 1};
+            if (plan.passes == 1) {
+                st = launch_keys_pass_bits<kPassTileLast>(plan.dbits, src, nullptr, vals, pass_bufs(kDepthPasses),
+                                                          depths, nullptr, s);
+            } else {
+                st = launch_keys_pass_bits<kPassPlain>(plan.dbits, src, w.tk[0], w.tv[0], pass_bufs(kDepthPasses),
+                                                       nullptr, nullptr, s);
+                for (int p = 1; !st && p < plan.passes; p++) {
+                    const bool last = p == plan.passes - 1;
+                    st = last ? launch_pass_bits<kPassTileLast>(plan.dbits, w.tk[(p - 1) & 1], w.tv[(p - 1) & 1],
+                                                                w.tk[p & 1], vals, (u32)capacity, plan.dbits * p, 0u,
+                                                                pass_bufs(kDepthPasses + p), depths, nullptr, s, dM)
+                              : launch_pass_bits<kPassPlain>(plan.dbits, w.tk[(p - 1) & 1], w.tv[(p - 1) & 1],
+                                                             w.tk[p & 1], w.tv[p & 1], (u32)capacity, plan.dbits * p,
+                                                             0u, pass_bufs(kDepthPasses + p), nullptr, nullptr, s, dM);
+                }
+            }
+            if (st) return st;
+        }
+    } else {
+        if ((st = launch_tile_count(TX, TY, w.diff, tile_offsets, tile_order, s))) return st;  // empty lists
+    }
+    bin_sort_status_kernel<<<(n_tiles + 1 + 1023) / 1024, 1024, 0, s>>>(w.totals, capacity, n_tiles, tile_offsets,
+                                                                        num_isects, status);
+    return check_launch("bin_sort_status");
 }
 
 }  // namespace vks

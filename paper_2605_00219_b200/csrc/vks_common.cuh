@@ -170,6 +170,10 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
                  int64_t capacity, uint64_t* keys, uint32_t* vals, uint64_t* keys_unsorted,
                  uint32_t* vals_unsorted, uint32_t* tile_offsets, uint32_t* tile_order, int64_t* num_isects,
                  void* workspace, size_t workspace_bytes, cudaStream_t s);
+int run_bin_sort_async(const vks_camera& cam, int64_t n, const float* means2d, const int32_t* radii,
+                       const float* depths, const int32_t* tiles_touched, uint32_t* offsets, int64_t capacity,
+                       uint32_t* vals, uint32_t* tile_offsets, uint32_t* tile_order, int64_t* num_isects,
+                       int32_t* status, void* workspace, size_t workspace_bytes, cudaStream_t s);
 int launch_raster_fwd(const vks_config& cfg, const vks_camera& cam, int64_t n, const float* means2d,
                       const float* conics, const float* colors, const float* opacities, const int32_t* radii,
                       const float* records, const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,

@@ -113,6 +113,9 @@ def test_argument_validation_is_synchronous():
     m = C.c_int64(0)
     assert lib.vks_bin_sort(C.byref(cam), 5, *([None] * 5), 0, *([None] * 4), None, None, C.byref(m), None, 0,
                             None) == V.VKS_ERR_INVALID_ARG
+    # async binning: device M / status words required, capacity below 2^30
+    assert lib.vks_bin_sort_async(C.byref(cam), 0, *([None] * 5), 0, *([None] * 3), None, None, P, 1 << 20,
+                                  None) == V.VKS_ERR_INVALID_ARG
 
 
 def test_no_cpu_fallback():

@@ -28,6 +28,10 @@ constexpr int kIP = kI + 3;                       // float row pitch 45: the 4 r
 constexpr int kRun = 4;                           // outputs per thread and pass
 constexpr int kLossThreads = 256;
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
+#ifndef VKS_LOSS_MAP_T
+#define VKS_LOSS_MAP_T double  // storage type of the partial maps between the two kernels
+#endif
+typedef VKS_LOSS_MAP_T map_t;
 
 struct Gauss {
     double g[kWin];
@@ -63,8 +67,8 @@ struct BwdSmem {
 // block (x: centre tile, y: centre tile, z: channel).  Centre p's window covers pixels p .. p+10.
 __global__ void __launch_bounds__(kLossThreads, 3) ssim_fwd_kernel(int W, int H, const float* __restrict__ render,
                                                                const float* __restrict__ target, const Gauss w,
-                                                               double* __restrict__ A, double* __restrict__ B,
-                                                               double* __restrict__ Cm, double* __restrict__ s_part) {
+                                                               map_t* __restrict__ A, map_t* __restrict__ B,
+                                                               map_t* __restrict__ Cm, double* __restrict__ s_part) {
     extern __shared__ __align__(16) unsigned char loss_smem[];
     FwdSmem& S = *reinterpret_cast<FwdSmem*>(loss_smem);
     const int tid = threadIdx.x, c = blockIdx.z;
@@ -160,9 +164,9 @@ __global__ void __launch_bounds__(kLossThreads, 3) ssim_fwd_kernel(int W, int H,
             const double dB = -Sv * (l2 * inv), dC = 2.0 * l1 * inv;
             const double dA = 2.0 * my * c1 * inv - 2.0 * mx * Sv * (c2 * inv) - 2.0 * mx * dB - my * dC;
             const size_t off = ((size_t)c * Hv + py) * Wv + px;
-            A[off] = dA;
-            B[off] = dB;
-            Cm[off] = dC;
+            A[off] = (map_t)dA;
+            B[off] = (map_t)dB;
+            Cm[off] = (map_t)dC;
             ssum += Sv;
         }
     }
@@ -181,8 +185,8 @@ __global__ void __launch_bounds__(kLossThreads, 3) ssim_fwd_kernel(int W, int H,
 //   - lambda / (3 Nv) sum_{centres p: q in window(p)} w(q - p) (A_p + 2 B_p r_q + C_p t_q)
 __global__ void __launch_bounds__(kLossThreads, 3) ssim_bwd_kernel(int W, int H, float lambda, const float* __restrict__ render,
                                                                const float* __restrict__ target, const Gauss w,
-                                                               const double* __restrict__ A, const double* __restrict__ B,
-                                                               const double* __restrict__ Cm, float* __restrict__ dL,
+                                                               const map_t* __restrict__ A, const map_t* __restrict__ B,
+                                                               const map_t* __restrict__ Cm, float* __restrict__ dL,
                                                                double* __restrict__ l1_part) {
     extern __shared__ __align__(16) unsigned char loss_smem[];
     BwdSmem& S = *reinterpret_cast<BwdSmem*>(loss_smem);
@@ -209,9 +213,9 @@ __global__ void __launch_bounds__(kLossThreads, 3) ssim_bwd_kernel(int W, int H,
                 const int py = qy0 - 2 * kR + r, px = qx0 - 2 * kR + sc;
                 const bool in = k < kI * kI && px >= 0 && py >= 0 && px < Wv && py < Hv;
                 const size_t o = ((size_t)c * Hv + py) * Wv + px;
-                va[u] = in ? __ldg(A + o) : 0.0;
-                vb[u] = in ? __ldg(B + o) : 0.0;
-                vc[u] = in ? __ldg(Cm + o) : 0.0;
+                va[u] = in ? (double)__ldg(A + o) : 0.0;
+                vb[u] = in ? (double)__ldg(B + o) : 0.0;
+                vc[u] = in ? (double)__ldg(Cm + o) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < kHalf; u++) {
@@ -325,7 +329,8 @@ __global__ void __launch_bounds__(kLossThreads) loss_finalize_kernel(int W, int 
 }
 
 struct LossWs {
-    double *A, *B, *C, *s_part, *l1_part;
+    map_t *A, *B, *C;
+    double *s_part, *l1_part;
     size_t bytes;
 };
 
@@ -338,9 +343,9 @@ LossWs carve_loss(void* base, int W, int H) {
     size_t off = 0;
     char* b = static_cast<char*>(base);
     auto take = [&](size_t n) { double* p = b ? reinterpret_cast<double*>(b + off) : nullptr; off += (8 * n + 255) & ~(size_t)255; return p; };
-    w.A = take(maps);
-    w.B = take(maps);
-    w.C = take(maps);
+    w.A = reinterpret_cast<map_t*>(take(maps));  // (sized for doubles whatever map_t is)
+    w.B = reinterpret_cast<map_t*>(take(maps));
+    w.C = reinterpret_cast<map_t*>(take(maps));
     w.s_part = take(nfwd > 0 ? nfwd : 1);
     w.l1_part = take(nbwd);
     w.bytes = off;

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python bench.py --steps 20 --no-cpu-baseline --no-e2e --no-batch1 > gpurun_out/b_sync.json 2> gpurun_out/b_sync.err
-timeout 600 python bench.py --steps 20 --no-cpu-baseline --no-e2e --no-batch1 --binning async > gpurun_out/b_async.json 2> gpurun_out/b_async.err
-timeout 600 python bench.py --steps 20 --no-cpu-baseline --no-e2e --no-batch1 --binning async --graph > gpurun_out/b_graph.json 2> gpurun_out/b_graph.err
+timeout 300 python tools/time_raster_ab.py bicycle 0 VKS_RASTER_SPARSE 2 4 6 8 12 > gpurun_out/ab_sparse.log 2>&1
+timeout 300 python tools/time_raster_ab.py mcmc 0 VKS_RASTER_SPARSE 4 8 >> gpurun_out/ab_sparse.log 2>&1

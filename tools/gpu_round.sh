@@ -1,3 +1,4 @@
+# round-end evidence: GPU tests, smoke, bench line, launch list of two timed steps, full ncu capture
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt

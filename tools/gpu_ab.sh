@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 300 python tools/time_raster_ab.py bicycle 0 VKS_RASTER_SPARSE 2 4 6 8 12 > gpurun_out/ab_sparse.log 2>&1
-timeout 300 python tools/time_raster_ab.py mcmc 0 VKS_RASTER_SPARSE 4 8 >> gpurun_out/ab_sparse.log 2>&1
+VKS_LIB_VARIANT=lossf32 timeout 600 python -m pytest tests/test_gpu_loss.py -q -p no:cacheprovider > gpurun_out/t_lossf32.log 2>&1; echo "rc=$?" >> gpurun_out/t_lossf32.log
+VKS_LIB_VARIANT=lossf32 timeout 120 python tools/time_loss.py bicycle > gpurun_out/loss_time.log 2>&1
+timeout 120 python tools/time_loss.py bicycle >> gpurun_out/loss_time.log 2>&1

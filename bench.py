@@ -57,7 +57,9 @@ def parse():
                     help="capture the whole step in a CUDA graph and replay it (needs --binning async)")
     ap.add_argument("--no-records", action="store_true",
                     help="raster passes gather the separate projection arrays instead of staging packed records")
-    ap.add_argument("--streams", type=int, default=3, help="views in flight per rank")
+    ap.add_argument("--streams", type=int, default=4, help="views in flight per rank")
+    ap.add_argument("--split", default="bin-high", choices=["none", "bin-high", "raster-high", "same"],
+                    help="binning and raster passes of a view on separate streams (with these priorities)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows-every", type=int, default=8, help="oracle raster sample: every k-th tile row")
@@ -221,6 +223,13 @@ def run_ours(args):
         r._alloc_capacity(int(r.capacity * 1.1))
     main = torch.cuda.current_stream()
     streams = [torch.cuda.Stream() for _ in range(S)]
+    # --split: per slot a binning stream and a raster stream (the view's raster waits for its
+    # binning; the slot's next binning waits for the slot's previous raster: the buffers are shared)
+    hi, lo = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (-1, 0)
+    pb = {"bin-high": -1, "raster-high": 0, "same": 0}.get(args.split, 0)
+    pr = {"bin-high": 0, "raster-high": -1, "same": 0}.get(args.split, 0)
+    bin_streams = [torch.cuda.Stream(priority=pb) for _ in range(S)] if args.split != "none" else None
+    ras_streams = [torch.cuda.Stream(priority=pr) for _ in range(S)] if args.split != "none" else None
     cfg_ow = dict(cfg, flags=P.FLAG_GRAD_OVERWRITE)
     # stage boundaries (CUDA events on the launching stream); the 2D-gradient accumulators that
     # raster_bwd adds into are zeroed by the batched projection forward (g2d_zero)
@@ -257,7 +266,9 @@ def run_ours(args):
                                     g2d_zero=[vbuf[j]["g2d"] for j in range(nb)],
                                     records=[vbuf[j]["rec"] for j in range(nb)] if use_rec else None)
 
-    def view_path(rend, vb, cam, dL, st, ev=None, copies=None):
+    st_done_prev = [None] * S  # --split: the event after each slot's last raster pass
+
+    def view_path(rend, vb, cam, dL, st, ev=None, copies=None, split_k=None):
         """One view's forward and raster backward on stream `st` (S views in flight, one stream
         each).  copies = (host target image, slot, loss slot): the e2e variant — the view's target
         image comes in from pinned host memory on a copy stream ("Copy Image to Device"),
@@ -269,10 +280,14 @@ def run_ours(args):
                 copy_stream.wait_event(slot["in_free"])      # the slot's previous consumer is done
                 slot["in"].copy_(host_src, non_blocking=True)
                 slot["in_ready"].record(copy_stream)
-        with torch.cuda.stream(st):
+        bst = st
+        if split_k is not None:  # binning on the slot's binning stream, the raster passes on its raster stream
+            bst, st = bin_streams[split_k], ras_streams[split_k]
+            bst.wait_event(st_done_prev[split_k])
+        with torch.cuda.stream(bst):
             if copies is not None and loss_out is None:
-                st.wait_event(slot["img_free"])              # the previous image has left rend.image
-            if ev is not None: ev[1].record(st)
+                bst.wait_event(slot["img_free"])             # the previous image has left rend.image
+            if ev is not None: ev[1].record(bst)
             if args.binning == "async":  # no host sync: M and the status stay on the device
                 P.vks_bin_sort_async(cam, vb["means2d"], vb["radii"], vb["depths"], vb["tiles"], rend.offsets,
                                      rend.vals, rend.tile_offsets, rend.workspace, vb["m_dev"], vb["st_dev"],
@@ -282,7 +297,12 @@ def run_ours(args):
                 m = P.vks_bin_sort(cam, vb["means2d"], vb["radii"], vb["depths"], vb["tiles"], rend.offsets, None,
                                    rend.vals, rend.tile_offsets, rend.workspace, tile_order=rend.tile_order)
                 rend.num_isects = m
-            if ev is not None: ev[2].record(st)
+            if ev is not None: ev[2].record(bst)
+        if bst is not st:
+            bdone = torch.cuda.Event()
+            bdone.record(bst)
+            st.wait_event(bdone)
+        with torch.cuda.stream(st):
             P.vks_raster_fwd(cfg, cam, vb["means2d"], vb["conics"], vb["colors"], opac, vb["radii"],
                              rend.vals, rend.tile_offsets, rend.image, rend.T_final, rend.n_contrib,
                              tile_order=rend.tile_order, records=vb["rec"])
@@ -308,6 +328,8 @@ def run_ours(args):
                 slot["in_free"].record(st)
             done = torch.cuda.Event()
             done.record(st)
+        if split_k is not None:
+            st_done_prev[split_k] = done
         return m, done
 
     def project_bwd_batch(vcams, st, sync=None):
@@ -347,13 +369,17 @@ def run_ours(args):
         start.record(main)
         for st in streams:
             st.wait_event(start)
+        if bin_streams is not None:
+            for k in range(S):
+                st_done_prev[k] = start
         m = 0
         for j, v in enumerate(vviews):
             k = j % S
             cp = None
             if copies is not None:
                 cp = (copies[0][v], copies[1][k], None if copies[2] is None else copies[2][j:j + 1])
-            m, done = view_path(rends[k], vbuf[j], cams[v], dLs[v], streams[k], copies=cp)
+            m, done = view_path(rends[k], vbuf[j], cams[v], dLs[v], streams[k], copies=cp,
+                                split_k=k if bin_streams is not None else None)
             main.wait_event(done)
         project_bwd_batch(vcams, main, gsync if world > 1 else None)  # + the chunked all-reduce (row a9)
         if copies is not None and copies[2] is not None:
@@ -690,8 +716,9 @@ def run_ours(args):
                            l2="inputs larger than L2 (params 1.37 GB, keys+vals 0.22 GB per view), no flush",
                            parallelism=f"view-sharded dp{world} ({args.scaling} scaling)",
                            step=(f"{B} ring views per rank ({views_per_step} per step in all): one batched projection "
-                                 f"forward, binning and both raster passes per view ({S} views in flight, one "
-                                 f"stream each), one batched projection backward"
+                                 f"forward, binning and both raster passes per view ({S} views in flight"
+                                 + (f"; per slot a binning stream and a raster stream, {args.split}" if args.split != "none"
+                                    else ", one stream each") + "), one batched projection backward"
                                  + (f" in {len(gsync.chunks())} Gaussian-row chunks, each chunk's gradient "
                                     f"all-reduce (NCCL) overlapping the next chunk" if world > 1 else "")
                                  + "; unit = views")),

@@ -221,15 +221,19 @@ __device__ __forceinline__ PixelMap<PPT> pixel_map(int tile, int TX) {
 // stats[1] = composited pairs, stats[2] = pairs actually evaluated here (after patch culling),
 // stats[3] = sum of n_contrib (entries the backward replays), stats[4] = (warp, entry) pairs a
 // warp processed after patch culling, stats[5] = those with at least one composited pixel.
+// minimum resident blocks per SM of the records kernels at 2 pixels per thread (scaled with the
+// block size for the other layouts; a register budget; the gather kernels hold more registers and
+// stay unconstrained): the forward at 12 (<= 42 registers; measured
+// 0.216 vs 0.224 ms on bicycle), the backward unconstrained (56 registers; 10 blocks measured slower)
 #ifndef VKS_RASTER_FWD_MINB
-#define VKS_RASTER_FWD_MINB 1
+#define VKS_RASTER_FWD_MINB 12
 #endif
 #ifndef VKS_RASTER_BWD_MINB
 #define VKS_RASTER_BWD_MINB 1
 #endif
 
 template <int PPT, int CULL, bool STATS = false, bool REC = false>
-__global__ void __launch_bounds__(32 * 8 / PPT, VKS_RASTER_FWD_MINB) raster_fwd_kernel(vks_config cfg, vks_camera cam,
+__global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_FWD_MINB * PPT + 1) / 2 : 1) raster_fwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
                                                                  const float* __restrict__ colors,
@@ -455,7 +459,7 @@ __device__ __forceinline__ float warp_reduce_8plus1(const float v[8], float& e, 
 }
 
 template <int PPT, int CULL, int SPARSE, bool REC = false>
-__global__ void __launch_bounds__(32 * 8 / PPT, VKS_RASTER_BWD_MINB) raster_bwd_kernel(vks_config cfg, vks_camera cam,
+__global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_BWD_MINB * PPT + 1) / 2 : 1) raster_bwd_kernel(vks_config cfg, vks_camera cam,
                                                                  const float2* __restrict__ means2d,
                                                                  const float* __restrict__ conics,
                                                                  const float* __restrict__ colors,

@@ -25,8 +25,14 @@ constexpr int kR = 5, kWin = 11;                  // window radius / width
 constexpr int kI = kT + 2 * kR;                   // tile + halo (42)
 constexpr int kIP = kI + 3;                       // float row pitch 45: the 4 rows x 8 column groups of
                                                   // a warp's sliding-window loads hit 32 distinct banks
-constexpr int kRun = 4;                           // outputs per thread and pass
-constexpr int kLossThreads = 256;
+#ifndef VKS_LOSS_RUN
+#define VKS_LOSS_RUN 4
+#endif
+#ifndef VKS_LOSS_THREADS
+#define VKS_LOSS_THREADS 512  // 2 blocks x 16 warps per SM (70-75 KB of shared memory per block):
+#endif                        // 0.153 ms vs 0.159 with 256 threads, 0.167 with 2 outputs per thread
+constexpr int kRun = VKS_LOSS_RUN;                // outputs per thread and pass
+constexpr int kLossThreads = VKS_LOSS_THREADS;
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 #ifndef VKS_LOSS_MAP_T
 #define VKS_LOSS_MAP_T double  // storage type of the partial maps between the two kernels
@@ -65,7 +71,7 @@ struct BwdSmem {
 };
 
 // block (x: centre tile, y: centre tile, z: channel).  Centre p's window covers pixels p .. p+10.
-__global__ void __launch_bounds__(kLossThreads, 3) ssim_fwd_kernel(int W, int H, const float* __restrict__ render,
+__global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssim_fwd_kernel(int W, int H, const float* __restrict__ render,
                                                                const float* __restrict__ target, const Gauss w,
                                                                map_t* __restrict__ A, map_t* __restrict__ B,
                                                                map_t* __restrict__ Cm, double* __restrict__ s_part) {
@@ -183,7 +189,7 @@ __global__ void __launch_bounds__(kLossThreads, 3) ssim_fwd_kernel(int W, int H,
 
 // block (x, y: pixel tile, z: channel).  dL_q = (1 - lambda) sign(r - t) / (3 N)
 //   - lambda / (3 Nv) sum_{centres p: q in window(p)} w(q - p) (A_p + 2 B_p r_q + C_p t_q)
-__global__ void __launch_bounds__(kLossThreads, 3) ssim_bwd_kernel(int W, int H, float lambda, const float* __restrict__ render,
+__global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssim_bwd_kernel(int W, int H, float lambda, const float* __restrict__ render,
                                                                const float* __restrict__ target, const Gauss w,
                                                                const map_t* __restrict__ A, const map_t* __restrict__ B,
                                                                const map_t* __restrict__ Cm, float* __restrict__ dL,

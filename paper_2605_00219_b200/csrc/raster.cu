@@ -55,13 +55,22 @@ struct RecStage {
 template <bool REC>
 using StageT = typename std::conditional<REC, RecStage, WarpStage>::type;
 
-// one lane's record -> slot `lane` of buffer `buf` (three cp.async.cg 16-byte copies)
+// one lane's record -> slot `lane` of buffer `buf` (three cp.async 16-byte copies).  CA: through L1
+// (.ca), so the four warps of a tile, which stage the same entries, share L1 hits; otherwise L2
+// only (.cg)
+template <bool CA = true>
 __device__ __forceinline__ void stage_record(RecStage& s, int buf, int lane, const float4* __restrict__ rec,
                                              uint32_t id) {
     const float4* g = rec + 3 * (size_t)id;
-    cp_async16(&s.a[buf][lane], g);
-    cp_async16(&s.b[buf][lane], g + 1);
-    cp_async16(&s.c[buf][lane], g + 2);
+    if constexpr (CA) {
+        cp_async16_ca(&s.a[buf][lane], g);
+        cp_async16_ca(&s.b[buf][lane], g + 1);
+        cp_async16_ca(&s.c[buf][lane], g + 2);
+    } else {
+        cp_async16(&s.a[buf][lane], g);
+        cp_async16(&s.b[buf][lane], g + 1);
+        cp_async16(&s.c[buf][lane], g + 2);
+    }
 }
 
 struct Entry {  // one lane's gathered entry, in registers until it is stored to the stage
@@ -225,6 +234,9 @@ __device__ __forceinline__ PixelMap<PPT> pixel_map(int tile, int TX) {
 // block size for the other layouts; a register budget; the gather kernels hold more registers and
 // stay unconstrained): the forward at 12 (<= 42 registers; measured
 // 0.216 vs 0.224 ms on bicycle), the backward unconstrained (56 registers; 10 blocks measured slower)
+#ifndef VKS_RASTER_REC_CA
+#define VKS_RASTER_REC_CA true
+#endif
 #ifndef VKS_RASTER_FWD_MINB
 #define VKS_RASTER_FWD_MINB 12
 #endif
@@ -276,7 +288,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_FWD_MINB * PPT
     Entry e_next;
     if constexpr (REC) {
         VKS_DCHECK(start + lane >= end || id_next < n);
-        if (start + lane < end) stage_record(s, 0, lane, rec, id_next);
+        if (start + lane < end) stage_record<VKS_RASTER_REC_CA>(s, 0, lane, rec, id_next);
         cp_async_commit();
     } else {
         if (start + lane < end) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
@@ -298,7 +310,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_FWD_MINB * PPT
         unsigned live;
         if constexpr (REC) {
             VKS_DCHECK(b + 32 + lane >= end || id_next < n);
-            if (b + 32 + lane < end) stage_record(s, buf ^ 1, lane, rec, id_next);
+            if (b + 32 + lane < end) stage_record<VKS_RASTER_REC_CA>(s, buf ^ 1, lane, rec, id_next);
             cp_async_commit();
             if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
             cp_async_wait_group<1>();  // this lane's copies of batch b have landed
@@ -534,7 +546,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_BWD_MINB * PPT
     Entry e_next;
     if constexpr (REC) {
         VKS_DCHECK(!(p0 >= 0 && p0 < wmax) || id_next < n);
-        if (p0 >= 0 && p0 < wmax) stage_record(s, 0, (int)lane, rec, id_next);
+        if (p0 >= 0 && p0 < wmax) stage_record<VKS_RASTER_REC_CA>(s, 0, (int)lane, rec, id_next);
         cp_async_commit();
     } else {
         if (p0 >= 0 && p0 < wmax) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
@@ -548,7 +560,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_BWD_MINB * PPT
         if constexpr (REC) {
             const int p = bs - 32 + (int)lane;  // the next batch's position of this lane
             VKS_DCHECK(p < 0 || id_next < n);
-            if (p >= 0) stage_record(s, buf ^ 1, (int)lane, rec, id_next);
+            if (p >= 0) stage_record<VKS_RASTER_REC_CA>(s, buf ^ 1, (int)lane, rec, id_next);
             cp_async_commit();
             if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
             cp_async_wait_group<1>();

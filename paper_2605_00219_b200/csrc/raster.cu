@@ -46,11 +46,17 @@ struct WarpStage {  // all three arrays at a 16-byte stride: one address for the
 // batches of 32 records with cp.async (three 16-byte copies per entry straight into shared
 // memory, slot = lane, the next batch in flight while the current one is visited); the live
 // entries are then visited in place (set bits of the warp's live mask).
+#ifndef VKS_RASTER_NBUF
+#define VKS_RASTER_NBUF 2  // stage buffers per warp: NBUF - 1 batches in flight
+#endif
+constexpr int kNB = VKS_RASTER_NBUF;
 struct RecStage {
-    float4 a[2][32];  // u, v, 0.5*a, b
-    float4 b[2][32];  // 0.5*c, rho, c0, c1
-    float4 c[2][32];  // c2, id (bits), -, -
+    float4 a[kNB][32];  // u, v, 0.5*a, b
+    float4 b[kNB][32];  // 0.5*c, rho, c0, c1
+    float4 c[kNB][32];  // c2, id (bits), -, -
 };
+__device__ __forceinline__ int nb_next(int b) { return b + 1 == kNB ? 0 : b + 1; }
+__device__ __forceinline__ int nb_ahead(int b) { return b == 0 ? kNB - 1 : b - 1; }  // (b + kNB - 1) % kNB
 
 template <bool REC>
 using StageT = typename std::conditional<REC, RecStage, WarpStage>::type;
@@ -286,16 +292,22 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_FWD_MINB * PPT
     // into registers, or, REC, copied by cp.async into the other stage buffer)
     uint32_t id_next = (start + lane < end) ? __ldg(vals + start + lane) : 0u;
     Entry e_next;
+    constexpr int kAhead = REC ? kNB - 1 : 1;  // batches in flight
     if constexpr (REC) {
-        VKS_DCHECK(start + lane >= end || id_next < n);
-        if (start + lane < end) stage_record<VKS_RASTER_REC_CA>(s, 0, lane, rec, id_next);
-        cp_async_commit();
+#pragma unroll
+        for (int q = 0; q < kNB - 1; q++) {  // batches 0 .. kNB - 2
+            const uint32_t pq = start + 32 * q + lane;
+            if (q > 0) id_next = pq < end ? __ldg(vals + pq) : 0u;
+            VKS_DCHECK(pq >= end || id_next < n);
+            if (pq < end) stage_record<VKS_RASTER_REC_CA>(s, q, lane, rec, id_next);
+            cp_async_commit();
+        }
     } else {
         if (start + lane < end) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
     }
-    id_next = (start + 32 + lane < end) ? __ldg(vals + start + 32 + lane) : 0u;
+    id_next = (start + 32 * kAhead + lane < end) ? __ldg(vals + start + 32 * kAhead + lane) : 0u;
     int buf = 0;
-    for (uint32_t b = start; b < end; b += 32, buf ^= 1) {
+    for (uint32_t b = start; b < end; b += 32, buf = nb_next(buf)) {
         bool all_done = true;
         if constexpr (PPT == 2 && !STATS) {
             all_done = T2.x < 1e-4f && T2.y < 1e-4f;
@@ -309,11 +321,11 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_FWD_MINB * PPT
         // order, only the entries that can composite somewhere in the patch
         unsigned live;
         if constexpr (REC) {
-            VKS_DCHECK(b + 32 + lane >= end || id_next < n);
-            if (b + 32 + lane < end) stage_record<VKS_RASTER_REC_CA>(s, buf ^ 1, lane, rec, id_next);
+            VKS_DCHECK(b + 32 * kAhead + lane >= end || id_next < n);
+            if (b + 32 * kAhead + lane < end) stage_record<VKS_RASTER_REC_CA>(s, nb_ahead(buf), lane, rec, id_next);
             cp_async_commit();
-            if (b + 64 + lane < end) id_next = __ldg(vals + b + 64 + lane);
-            cp_async_wait_group<1>();  // this lane's copies of batch b have landed
+            if (b + 32 * (kAhead + 1) + lane < end) id_next = __ldg(vals + b + 32 * (kAhead + 1) + lane);
+            cp_async_wait_group<kNB - 1>();  // this lane's copies of batch b have landed
             __syncwarp();              // ... and every other lane's
             bool lv = false;
             if (b + lane < end) {
@@ -544,26 +556,32 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_BWD_MINB * PPT
     int p0 = bs + (int)lane;
     uint32_t id_next = (p0 >= 0 && p0 < wmax) ? __ldg(vals + start + p0) : 0u;
     Entry e_next;
+    constexpr int kAhead = REC ? kNB - 1 : 1;  // batches in flight
     if constexpr (REC) {
-        VKS_DCHECK(!(p0 >= 0 && p0 < wmax) || id_next < n);
-        if (p0 >= 0 && p0 < wmax) stage_record<VKS_RASTER_REC_CA>(s, 0, (int)lane, rec, id_next);
-        cp_async_commit();
+#pragma unroll
+        for (int q = 0; q < kNB - 1; q++) {  // batches bs, bs - 32, ... (kNB - 1 of them)
+            const int pq = p0 - 32 * q;
+            if (q > 0) id_next = pq >= 0 ? __ldg(vals + start + pq) : 0u;
+            VKS_DCHECK(!(pq >= 0 && pq < wmax) || id_next < n);
+            if (pq >= 0 && pq < wmax) stage_record<VKS_RASTER_REC_CA>(s, q, (int)lane, rec, id_next);
+            cp_async_commit();
+        }
     } else {
         if (p0 >= 0 && p0 < wmax) e_next = gather_entry<CULL>(id_next, n, means2d, conics, colors, opac, radii);
     }
-    p0 -= 32;
+    p0 -= 32 * kAhead;
     id_next = (p0 >= 0) ? __ldg(vals + start + p0) : 0u;
     int buf = 0;
-    for (; bs > -32; bs -= 32, buf ^= 1) {
+    for (; bs > -32; bs -= 32, buf = nb_next(buf)) {
         __syncwarp();
         unsigned live;
         if constexpr (REC) {
-            const int p = bs - 32 + (int)lane;  // the next batch's position of this lane
+            const int p = bs - 32 * kAhead + (int)lane;  // this lane's position kAhead batches on
             VKS_DCHECK(p < 0 || id_next < n);
-            if (p >= 0) stage_record<VKS_RASTER_REC_CA>(s, buf ^ 1, (int)lane, rec, id_next);
+            if (p >= 0) stage_record<VKS_RASTER_REC_CA>(s, nb_ahead(buf), (int)lane, rec, id_next);
             cp_async_commit();
             if (p - 32 >= 0) id_next = __ldg(vals + start + p - 32);
-            cp_async_wait_group<1>();
+            cp_async_wait_group<kNB - 1>();
             __syncwarp();
             const int pc = bs + (int)lane;
             bool lv = false;

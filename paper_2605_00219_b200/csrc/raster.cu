@@ -3,9 +3,12 @@
 //
 // One block per 16x16 tile; each warp owns an 8 x 4*PPT pixel patch (PPT = 2 by default: 8x8,
 // two pixels per thread) and walks the tile's sorted list on its own in batches of 32 staged
-// into its shared-memory slice as packed float4 records (software-pipelined: ids two batches
-// ahead, records one batch ahead), so there are no block barriers and a warp stops as soon as
-// its own pixels are saturated.  Before a batch is visited each lane tests its entry against the
+// into its shared-memory slice (software-pipelined: ids two batches ahead, entries one batch
+// ahead) — with the projection's packed records (the default) by cp.async.ca straight into a
+// double-buffered stage, else gathered from the separate arrays into registers and stored — so
+// there are no block barriers and a warp stops as soon as its own pixels are saturated.  With
+// two pixels per thread the per-pixel math runs on paired fp32 instructions (FFMA2 / FMUL2 /
+// FADD2, eval_alpha2).  Before a batch is visited each lane tests its entry against the
 // patch with an exact test (the minimum of sigma over the patch rectangle against ln(255 rho));
 // the warp visits only entries that can composite somewhere in the patch (a finer per-8x4-band
 // test removed 20% of the evaluations but cost more instructions than it saved).  Forward and

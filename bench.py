@@ -448,6 +448,7 @@ def run_ours(args):
     batch1 = None
     if not args.no_batch1:
         rb = rends[0]
+        rb_con = None if rb.records is not None else rb.conics  # the records carry the conics
         gb = params.grads()
         nb1 = max(24, args.steps)
         b1ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(nb1 + 3)]
@@ -457,18 +458,18 @@ def run_ours(args):
             e = b1ev[i]
             e[0].record(main)
             P.vks_project_fwd(cfg, cam, params.means, params.log_scales, params.quats, params.opacity_logits,
-                              params.sh, rb.means2d, rb.conics, rb.depths, rb.radii, rb.tiles, rb.colors,
+                              params.sh, rb.means2d, rb_con, rb.depths, rb.radii, rb.tiles, rb.colors,
                               rb.opacities, records=rb.records)
             e[1].record(main)
             P.vks_bin_sort(cam, rb.means2d, rb.radii, rb.depths, rb.tiles, rb.offsets, None, rb.vals,
                            rb.tile_offsets, rb.workspace, tile_order=rb.tile_order)
             e[2].record(main)
-            P.vks_raster_fwd(cfg, cam, rb.means2d, rb.conics, rb.colors, rb.opacities, rb.radii, rb.vals,
+            P.vks_raster_fwd(cfg, cam, rb.means2d, rb_con, rb.colors, rb.opacities, rb.radii, rb.vals,
                              rb.tile_offsets, rb.image, rb.T_final, rb.n_contrib, tile_order=rb.tile_order,
                              records=rb.records)
             e[3].record(main)
             rb.g2d.zero_()  # the raster backward accumulates the view's 2D gradients
-            P.vks_raster_bwd(cfg, cam, rb.means2d, rb.conics, rb.colors, rb.opacities, rb.radii, rb.vals,
+            P.vks_raster_bwd(cfg, cam, rb.means2d, rb_con, rb.colors, rb.opacities, rb.radii, rb.vals,
                              rb.tile_offsets, rb.T_final, rb.n_contrib, dLv, rb.dmeans2d, rb.dconics, rb.dcolors,
                              rb.dopacities, tile_order=rb.tile_order, records=rb.records)
             e[4].record(main)

@@ -225,8 +225,7 @@ def run_ours(args):
     streams = [torch.cuda.Stream() for _ in range(S)]
     # --split: per slot a binning stream and a raster stream (the view's raster waits for its
     # binning; the slot's next binning waits for the slot's previous raster: the buffers are shared)
-    hi, lo = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (-1, 0)
-    pb = {"bin-high": -1, "raster-high": 0, "same": 0}.get(args.split, 0)
+    pb = {"bin-high": -1, "raster-high": 0, "same": 0}.get(args.split, 0)  # priorities (lower = higher)
     pr = {"bin-high": 0, "raster-high": -1, "same": 0}.get(args.split, 0)
     bin_streams = [torch.cuda.Stream(priority=pb) for _ in range(S)] if args.split != "none" else None
     ras_streams = [torch.cuda.Stream(priority=pr) for _ in range(S)] if args.split != "none" else None

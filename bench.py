@@ -194,12 +194,20 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    # VKS_BENCH_BACKEND=gloo with more ranks than GPUs: a functional check of the N > 1 code path
+    # (partitions, chunked all-reduce, sharded optimizer) on a smaller box — not a measurement
+    backend = os.environ.get("VKS_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     # launched by torchrun (even with one rank): the NCCL process group, barriers, max-over-ranks
     # timing and the gradient allreduce all run
     distributed = "WORLD_SIZE" in os.environ
     if distributed:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     c = synth.CONFIGS[args.config]
     cfg = synth.default_render_config(3)
     scene = synth.make_scene(c.n, c.kind, c.seed)

@@ -543,17 +543,17 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_BWD_MINB * PPT
     // owns term k, lane 1 the opacity term; dst(g) = base + g * stride
     const int myterm = (lane & 3) == 0 ? (int)(lane >> 2) : (lane == 1 ? 8 : -1);
     float* tbase = nullptr;
-    int tstride = 0;
+    unsigned tstride = 0;  // bytes: dst(g) = base + g * stride is one 64-bit IMAD.WIDE.U32
     // term selectors for the epilogue: term 0 -> a, term 1 -> c, both -> b (other moment),
     // conic terms 2/3/4 -> 1/2, 1, 1/2, colour terms -> 1
     const float kA = myterm == 0 ? 1.0f : 0.0f, kC = myterm == 1 ? 1.0f : 0.0f;
     const float kB = myterm == 0 || myterm == 1 ? 1.0f : 0.0f;
     const float kH = myterm == 3 ? 1.0f : (myterm == 2 || myterm == 4 ? 0.5f : 0.0f);
     const float kOne = myterm >= 5 && myterm < 8 ? 1.0f : 0.0f;
-    if (myterm >= 0 && myterm < 2) { tbase = dmeans2d + myterm; tstride = 2; }
-    else if (myterm >= 2 && myterm < 5) { tbase = dconics + (myterm - 2); tstride = 3; }
-    else if (myterm >= 5 && myterm < 8) { tbase = dcolors + (myterm - 5); tstride = 3; }
-    else if (myterm == 8) { tbase = dopac; tstride = 1; }
+    if (myterm >= 0 && myterm < 2) { tbase = dmeans2d + myterm; tstride = 2 * sizeof(float); }
+    else if (myterm >= 2 && myterm < 5) { tbase = dconics + (myterm - 2); tstride = 3 * sizeof(float); }
+    else if (myterm >= 5 && myterm < 8) { tbase = dcolors + (myterm - 5); tstride = 3 * sizeof(float); }
+    else if (myterm == 8) { tbase = dopac; tstride = sizeof(float); }
     // batches of 32 positions, back to front: [bs, bs+32) with bs = wmax-32, wmax-64, ...
     int bs = wmax - 32;
     int p0 = bs + (int)lane;
@@ -719,7 +719,9 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_BWD_MINB * PPT
                 const float nrho = -B.y;
                 const float cr = fmaf(nrho, fmaf(kA, 2.0f * A.z, fmaf(kC, 2.0f * B.x, kH)), kOne);
                 const float out = myterm == 8 ? e : fmaf(cr, r, (nrho * kB * A.w) * other);
-                if (myterm >= 0) atomicAdd(tbase + (size_t)__float_as_uint(Cc.y) * tstride, out);
+                if (myterm >= 0)
+                    atomicAdd(reinterpret_cast<float*>(reinterpret_cast<char*>(tbase) +
+                                                       (unsigned long long)__float_as_uint(Cc.y) * tstride), out);
             }
         }
     }

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-VKS_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/tr2.json 2> gpurun_out/tr2.err; echo "rc=$?" >> gpurun_out/tr2.err
-VKS_BENCH_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline --scaling weak --no-e2e > gpurun_out/tr2w.json 2> gpurun_out/tr2w.err; echo "rc=$?" >> gpurun_out/tr2w.err
+timeout 600 python tools/time_raster_ab.py bicycle 0 > gpurun_out/ab_addr.log 2>&1
+timeout 600 python tools/time_raster_ab.py bicycle 0 >> gpurun_out/ab_addr.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "tiny or records or sparse" > gpurun_out/t_addr.log 2>&1; echo "rc=$?" >> gpurun_out/t_addr.log

@@ -12,7 +12,13 @@ batch of 8 views sharded across 1/2/4/8"); `--scaling weak` gives every rank `--
 views of a ring of views x N cameras.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config bicycle]
-                    [--scaling strong|weak] [--views 8]
+                    [--scaling strong|weak] [--views 8] [--streams 4] [--split bin-high]
+                    [--binning sync|async] [--graph] [--no-records]
+
+Four views are in flight per rank (`--streams`), each slot with a binning stream of high
+priority and a raster stream (`--split`); the raster passes stage the projection's packed records
+(`--no-records`: gather the separate arrays); `--binning async --graph` runs the host-sync-free
+binning and replays the whole step as one CUDA graph (measured no faster).
 
 Beside the step (not in `value`): `batch1` (the paper's iteration: one view at a time through the
 single-view entry points), `train_step` (the step plus the optimizer, row f1: sharded
@@ -277,7 +283,7 @@ def run_ours(args):
 
     def view_path(rend, vb, cam, dL, st, ev=None, copies=None, split_k=None):
         """One view's forward and raster backward on stream `st` (S views in flight, one stream
-        each).  copies = (host target image, slot, loss slot): the e2e variant — the view's target
+        each, or with split_k a binning and a raster stream per slot).  copies = (host target image, slot, loss slot): the e2e variant — the view's target
         image comes in from pinned host memory on a copy stream ("Copy Image to Device"),
         vks_loss_grad turns the rendered image and the target into the loss and dL/dimage on the
         device ("Loss Gradient"), and raster_bwd consumes that."""

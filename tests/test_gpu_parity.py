@@ -321,12 +321,14 @@ def test_patch_culling_and_ppt_variants_agree(fp, monkeypatch):
     report(f"cull_fp{fp}", dict(stats={"/".join(k): v for k, v in stats.items()}))
 
 
-@pytest.mark.parametrize("kind,n,W,H,view", [("indoor", 200000, 400, 300, 3), ("outdoor", 60000, 333, 211, 5)])
+@pytest.mark.parametrize("kind,n,W,H,view", [("indoor", 200000, 400, 300, 3), ("outdoor", 60001, 333, 211, 5),
+                                              ("outdoor", 777, 64, 48, 1)])
 def test_records_path_agrees_with_gather(kind, n, W, H, view):
     """The packed raster records (vks_project_fwd `records`) hold exactly the projection's outputs
     of every visible row — (u, v, a/2, b), (c/2, rho, c0, c1), (c2, id, 0, 0), bit for bit — and
     both raster passes staging them with cp.async give the identical image, T and n_contrib as the
-    gather path, and the same 2D gradients up to atomic summation order (ragged 333x211 image)."""
+    gather path, and the same 2D gradients up to atomic summation order (ragged 333x211 image, a
+    ragged last warp of rows, a scene smaller than one block)."""
     s = synth.make_scene(n, kind, 72)
     cam = synth.ring_cameras(W, H, kind, 8)[view]
     cfg = synth.default_render_config()
@@ -334,7 +336,7 @@ def test_records_path_agrees_with_gather(kind, n, W, H, view):
     rec = run_gpu(s, cam, cfg, dL=dL, records=True)
     gat = run_gpu(s, cam, cfg, dL=dL, records=False)
     vis = rec["tiles_touched"] > 0
-    assert vis.sum() > n // 10
+    assert vis.sum() > n // 20
     R = rec["records"][vis].reshape(-1, 12)
     ids = np.nonzero(vis)[0]
     want = np.stack([rec["means2d"][vis, 0], rec["means2d"][vis, 1], 0.5 * rec["conics"][vis, 0],

@@ -1,6 +1,2 @@
 mkdir -p gpurun_out
-for v in "" "VKS_LIB_VARIANT=items8" "VKS_LIB_VARIANT=items12"; do
-  echo "== $v" >> gpurun_out/items.log
-  env $v timeout 300 python tools/time_binsort.py bicycle 30 >> gpurun_out/items.log 2>&1
-  env $v timeout 300 python tools/time_binsort.py stress 10 >> gpurun_out/items.log 2>&1
-done
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -k "records" > gpurun_out/t_rec.log 2>&1; echo "rc=$?" >> gpurun_out/t_rec.log

@@ -15,7 +15,7 @@ views of a ring of views x N cameras.
                     [--scaling strong|weak] [--views 8] [--streams 4] [--split bin-high]
                     [--binning sync|async] [--graph] [--no-records]
 
-Four views are in flight per rank (`--streams`), each slot with a binning stream of high
+Every view of the batch is in flight (`--streams`, 8 slots), each slot with a binning stream of high
 priority and a raster stream (`--split`); the raster passes stage the projection's packed records
 (`--no-records`: gather the separate arrays); `--binning async --graph` runs the host-sync-free
 binning and replays the whole step as one CUDA graph (measured no faster).
@@ -63,7 +63,7 @@ def parse():
                     help="capture the whole step in a CUDA graph and replay it (needs --binning async)")
     ap.add_argument("--no-records", action="store_true",
                     help="raster passes gather the separate projection arrays instead of staging packed records")
-    ap.add_argument("--streams", type=int, default=4, help="views in flight per rank")
+    ap.add_argument("--streams", type=int, default=8, help="views in flight per rank")
     ap.add_argument("--split", default="bin-high", choices=["none", "bin-high", "raster-high", "same"],
                     help="binning and raster passes of a view on separate streams (with these priorities)")
     ap.add_argument("--no-e2e", action="store_true")

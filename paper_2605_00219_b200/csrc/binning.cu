@@ -48,6 +48,11 @@ typedef uint32_t u32;
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
+#ifndef VKS_CNT_SCAN_ITEMS
+#define VKS_CNT_SCAN_ITEMS 16
+#endif
+constexpr int kCntItems = VKS_CNT_SCAN_ITEMS;             // scan_u32 (the digit-count matrices):
+constexpr int kCntTile = kScanThreads * kCntItems;         // elements per block
 constexpr int kDownThreads = 512;  // the down-sweeps: same 4096-element tiles, 8 items per thread
 constexpr int kDownItems = kScanTile / kDownThreads;
 
@@ -114,7 +119,7 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
     const size_t nn = (size_t)(n > 0 ? n : 1), cap = (size_t)(capacity > 0 ? capacity : 1);
     const size_t scan_tiles = (nn + kScanTile - 1) / kScanTile;
     const size_t sort_tiles = (std::max(nn, cap) + kSortTile - 1) / kSortTile;
-    const size_t cnt_scan_tiles = (kMaxRadix * sort_tiles + kScanTile - 1) / kScanTile;
+    const size_t cnt_scan_tiles = (kMaxRadix * sort_tiles + kCntTile - 1) / kCntTile;
     for (int i = 0; i < 2; i++) {
         w.dk[i] = reinterpret_cast<u32*>(take(4 * nn));
         w.dv[i] = reinterpret_cast<u32*>(take(4 * nn));
@@ -714,15 +719,15 @@ __global__ void __launch_bounds__(kScanThreads) scan_u32_kernel(const u32* __res
     if (tid == 0) s_tile = atomicAdd(ctr, 1u);
     __syncthreads();
     const u64 tile = s_tile;
-    const u64 wbase = tile * kScanTile + (u64)warp * 32 * kScanItems;
-    int v[kScanItems];
-    u32 ex[kScanItems];
+    const u64 wbase = tile * kCntTile + (u64)warp * 32 * kCntItems;
+    int v[kCntItems];
+    u32 ex[kCntItems];
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
+    for (int j = 0; j < kCntItems; j++) {
         const u64 i = wbase + 32 * j + lane;
         v[j] = i < count ? (int)__ldg(in + i) : 0;
     }
-    const u32 wtot = warp_striped_excl(v, ex, lane);
+    const u32 wtot = warp_striped_excl<kCntItems>(v, ex, lane);
     if (lane == 0) s_warp[warp] = wtot;
     __syncthreads();
     u64 wpre = 0, btotal = 0;
@@ -762,7 +767,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_u32_kernel(const u32* __res
     __syncthreads();
     const u32 pre = (u32)(s_prefix + wpre);
 #pragma unroll
-    for (int j = 0; j < kScanItems; j++) {
+    for (int j = 0; j < kCntItems; j++) {
         const u64 i = wbase + 32 * j + lane;
         if (i < count) out[i] = pre + ex[j];
     }
@@ -1164,7 +1169,7 @@ int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int
     if (!T) return VKS_OK;
     digit_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(kin, n, shift, kbias, T, pb.counts, dcount);
     const u64 cnt = (u64)(1u << DBITS) * T;
-    scan_u32_kernel<<<(unsigned)((cnt + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt, pb.lb, pb.ctr);
+    scan_u32_kernel<<<(unsigned)((cnt + kCntTile - 1) / kCntTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt, pb.lb, pb.ctr);
     scatter_kernel<DBITS, MODE><<<T, kSortThreads, sm, s>>>(kin, vin, kout, vout, n, shift, kbias, T, pb.offs, depths,
                                                             keys64, dcount);
     return check_launch(__func__);
@@ -1221,7 +1226,7 @@ int launch_keys_pass(const ExpandSrc& src, u32* kout, u32* vout, const PassBufs&
     if (!T) return VKS_OK;
     keys_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(src, 0, T, pb.counts);
     const u64 cnt = (u64)(1u << DBITS) * T;
-    scan_u32_kernel<<<(unsigned)((cnt + kScanTile - 1) / kScanTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt,
+    scan_u32_kernel<<<(unsigned)((cnt + kCntTile - 1) / kCntTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt,
                                                                                      pb.lb, pb.ctr);
     keys_scatter_kernel<DBITS, MODE><<<T, kSortThreads, sm, s>>>(src, 0, T, pb.offs, kout, vout, depths, keys64);
     return check_launch(__func__);

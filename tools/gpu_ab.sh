@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
-for a in "--streams 4" "--streams 5" "--streams 6" "--streams 8" "--streams 4"; do
-  echo "== $a" >> gpurun_out/streams.log
-  timeout 300 python bench.py --steps 20 --no-cpu-baseline --no-e2e --no-batch1 $a 2>>gpurun_out/streams.err | python -c "import json,sys; p=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(p['value'], p['ms_per_step'])" >> gpurun_out/streams.log
+for v in "" "VKS_LIB_VARIANT=cs4" "VKS_LIB_VARIANT=cs8" ""; do
+  echo "== $v" >> gpurun_out/cs.log
+  env $v timeout 300 python tools/time_binsort.py bicycle 30 >> gpurun_out/cs.log 2>&1
+  env $v timeout 300 python tools/time_binsort.py stress 10 >> gpurun_out/cs.log 2>&1
 done
+VKS_LIB_VARIANT=cs4 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "binning or tiny or bicycle" > gpurun_out/t_cs4.log 2>&1; echo "rc=$?" >> gpurun_out/t_cs4.log

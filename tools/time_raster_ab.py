@@ -35,15 +35,18 @@ def med(fn, reps=21):
     return statistics.median(ts[2:])
 
 
+ORDER = None if os.environ.get("VKS_TOOL_NO_ORDER") == "1" else r.tile_order  # LPT schedule or tile id order
+
+
 def run(rec):
     fwd = med(lambda: P.vks_raster_fwd(cfg, cam, r.means2d, r.conics, r.colors, r.opacities, r.radii, r.vals,
-                                       r.tile_offsets, r.image, r.T_final, r.n_contrib, tile_order=r.tile_order,
+                                       r.tile_offsets, r.image, r.T_final, r.n_contrib, tile_order=ORDER,
                                        records=rec))
 
     def bwd():
         P.vks_raster_bwd(cfg, cam, r.means2d, r.conics, r.colors, r.opacities, r.radii, r.vals, r.tile_offsets,
                          r.T_final, r.n_contrib, dL, r.dmeans2d, r.dconics, r.dcolors, r.dopacities,
-                         tile_order=r.tile_order, records=rec)
+                         tile_order=ORDER, records=rec)
     bwd_ms = med(bwd)
     return fwd, bwd_ms
 
@@ -55,3 +58,20 @@ for val in (sys.argv[4:] if var else ["-"]):
     for name, rec in (("gather", None), ("records", r.records)):
         f, b = run(rec)
         print(f"{c.name} view {view} {var or ''}={val} {name:8s} raster_fwd {f:.4f} ms  raster_bwd {b:.4f} ms", flush=True)
+
+if os.environ.get("VKS_TOOL_WORK_ORDER") == "1":
+    # the backward scheduled by its own work estimate from the forward: per tile the sum over its
+    # four 8x8 warp patches of the patch's largest n_contrib (the replay range), heaviest first
+    H, W = c.height, c.width
+    TX, TY = (W + 15) // 16, (H + 15) // 16
+    nc = torch.zeros(TY * 16, TX * 16, dtype=torch.int32, device="cuda")
+    nc[:H, :W] = r.n_contrib
+    patch = nc.view(TY * 2, 8, TX * 2, 8).amax(dim=(1, 3)).to(torch.int64)  # [2TY, 2TX]
+    work = patch.view(TY, 2, TX, 2).sum(dim=(1, 3)).reshape(-1)
+    order_w = torch.argsort(work, descending=True).to(torch.int32).view(torch.uint32).contiguous()
+
+    def bwd_w():
+        P.vks_raster_bwd(cfg, cam, r.means2d, r.conics, r.colors, r.opacities, r.radii, r.vals, r.tile_offsets,
+                         r.T_final, r.n_contrib, dL, r.dmeans2d, r.dconics, r.dcolors, r.dopacities,
+                         tile_order=order_w, records=r.records)
+    print(f"{c.name} view {view} backward with the work order: {med(bwd_w):.4f} ms", flush=True)

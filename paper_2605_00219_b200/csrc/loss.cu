@@ -4,23 +4,25 @@
 //   loss = (1 - lambda) mean|r - t| + lambda (1 - SSIM),   SSIM = mean over channels and valid
 //   11x11 windows (Gaussian, sigma 1.5) of S = (2 mx my + C1)(2 sxy + C2) / ((mx^2 + my^2 + C1)
 //   (sx2 + sy2 + C2)).
-// Three kernels: ssim_fwd_kernel (per 32x32 tile of window centres and channel: the separable
-// window sums of x, y, x^2, y^2, xy — horizontal into shared memory, then vertical — and S with
-// its partials dS/dmx, dS/dE[x^2], dS/dE[xy] per centre), ssim_bwd_kernel (per 32x32 pixel tile
-// and channel: the transposed separable window sums of the three partial maps, the L1
-// subgradient, dL/dr), loss_finalize_kernel (one block: the block partial sums -> loss,
-// deterministic).  The window sums, S, the partials and the transposed pass are fp64: the
-// variances E[x^2] - mx^2 cancel down to ~C2 = 9e-4, and fp32 statistics would put up to ~1e-3
-// relative error into the gradient.  Each thread produces four adjacent outputs of a pass from a
-// sliding register window (14 inputs for 4 outputs of an 11-tap pass: 3.5 shared-memory loads and
-// products per output instead of 11), so the kernels are bound by the fp64 FMAs, not by 64-bit
-// shared-memory traffic (round 1: one output per thread, 0.17 ms for 1237x822, mio-throttled).
+// Three kernels: ssim_fused_kernel (per 32x32 tile of window centres and channel: the separable
+// window sums of x, y, x^2, y^2, xy — horizontal into shared memory, then vertical — S with its
+// partials A = dS/dmx, B = dS/dE[x^2], C = dS/dE[xy] per centre, then the transposed separable
+// sums of A, B, C over the 42x42 pixel region the tile's windows reach and each pixel's partial
+// A + 2 B x + C y, into a per-tile slot), loss_combine_kernel (per pixel: the L1 subgradient plus
+// the <= 2x2 tile partials in a fixed order, dL/dr) and loss_finalize_kernel (one block: the block
+// partial sums -> loss, deterministic).  The window sums, S, the partials and the transposed sums
+// are fp64: the variances E[x^2] - mx^2 cancel down to ~C2 = 9e-4, and fp32 statistics would put
+// up to ~1e-3 relative error into the gradient.  Each thread produces four adjacent outputs of a
+// pass from a sliding register window (14 inputs for 4 outputs of an 11-tap pass: 3.5 shared-
+// memory loads and products per output instead of 11).  Round 1/2 ran the transposed sums in a
+// second kernel over 32x32 pixel tiles, reading fp64 maps of A, B, C (72 B per pixel) with a
+// 10-pixel halo back from HBM: 0.154 ms for 1237x822, the second kernel at 25% of the fp64 pipe.
 #include "vks_common.cuh"
 
 namespace vks {
 namespace {
 
-constexpr int kT = 32;                        // tile of centres (fwd) / pixels (bwd), square
+constexpr int kT = 32;                             // tile of window centres, square
 constexpr int kR = 5, kWin = 11;                  // window radius / width
 constexpr int kI = kT + 2 * kR;                   // tile + halo (42)
 constexpr int kIP = kI + 3;                       // float row pitch 45: the 4 rows x 8 column groups of
@@ -28,16 +30,10 @@ constexpr int kIP = kI + 3;                       // float row pitch 45: the 4 r
 #ifndef VKS_LOSS_RUN
 #define VKS_LOSS_RUN 4
 #endif
-#ifndef VKS_LOSS_THREADS
-#define VKS_LOSS_THREADS 512  // 2 blocks x 16 warps per SM (70-75 KB of shared memory per block):
-#endif                        // 0.153 ms vs 0.159 with 256 threads, 0.167 with 2 outputs per thread
 constexpr int kRun = VKS_LOSS_RUN;                // outputs per thread and pass
-constexpr int kLossThreads = VKS_LOSS_THREADS;
+constexpr int kVRun = 2;                          // ... in the vertical forward pass (32 x 16 items)
+constexpr int kLossThreads = 512;             // 2 blocks x 16 warps per SM (75 KB of shared memory each)
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
-#ifndef VKS_LOSS_MAP_T
-#define VKS_LOSS_MAP_T double  // storage type of the partial maps between the two kernels
-#endif
-typedef VKS_LOSS_MAP_T map_t;
 
 struct Gauss {
     double g[kWin];
@@ -55,28 +51,40 @@ Gauss window() {
     return w;
 }
 
-// dynamic shared memory of the two kernels.  64-bit rows are padded to an odd pitch: a warp
-// stores four rows x eight runs (elements 4g + o of each row), and with pitch 33 / 43 doubles
-// those 32 stores / loads spread over all 16 bank pairs (two wavefronts, the minimum for 256 B)
-constexpr int kHP = kT + 1, kMP = kI + 1;
-struct FwdSmem {
-    float sx[kI][kIP], sy[kI][kIP];   // input tile + halo
-    double hs[5][kI][kHP];            // horizontal window sums of x, y, x^2, y^2, xy
+// dynamic shared memory of the fused kernel.  64-bit rows are padded to an odd pitch: a warp
+// stores four rows x eight runs (elements 4g + o of each row), and with pitch 33 doubles those 32
+// stores / loads spread over all 16 bank pairs (two wavefronts, the minimum for 256 B)
+constexpr int kHP = kT + 1;
+constexpr int kHtRun = 3, kHtRuns = kI / kHtRun;  // horizontal transposed pass: 14 runs of 3 columns
+constexpr int kURuns = (kI + kRun - 1) / kRun;    // vertical transposed pass: 11 runs of 4 rows
+constexpr int kUP = kI + 3;                       // pitch of the transposed rows (45)
+struct FusedSmem {
+    float sx[kI][kIP], sy[kI][kIP];   // input tile + halo = the pixel region the centres reach
+    union {
+        double hs[5][kI][kHP];        // horizontal window sums of x, y, x^2, y^2, xy
+        struct {
+            double abc[3][kT][kHP];   // the centres' partials A, B, C
+            double ht[3][kT][kUP];    // their horizontal transposed sums over the pixel columns
+        } t;
+    } u;
     double red[kLossThreads / 32];
 };
-struct BwdSmem {
-    double sm[3][kI][kMP];            // partial maps of the centres that reach the tile
-    double hs[3][kI][kHP];            // their horizontal transposed sums
-    double red[kLossThreads / 32];
-};
+static_assert(kI % kHtRun == 0 && kLossThreads >= kI * kURuns && kLossThreads >= kT * kHtRuns && kLossThreads >= kT * (kT / kVRun),
+              "the single-item phases need one thread per item");
 
-// block (x: centre tile, y: centre tile, z: channel).  Centre p's window covers pixels p .. p+10.
-__global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssim_fwd_kernel(int W, int H, const float* __restrict__ render,
-                                                               const float* __restrict__ target, const Gauss w,
-                                                               map_t* __restrict__ A, map_t* __restrict__ B,
-                                                               map_t* __restrict__ Cm, double* __restrict__ s_part) {
+// block (x: centre tile, y: centre tile, z: channel).  Centre p's window covers pixels p .. p+10,
+// so the block's 32x32 centres reach the 42x42 pixel region starting at the tile origin.  The
+// block computes the window statistics, S and its partials A, B, C for its centres, then the
+// transposed window sums of A, B, C over the region and, per pixel q,
+//   part_b(q) = sum_{centres p of the block} w(q - p) (A_p + 2 B_p x_q + C_p y_q)
+// into its own 42x42 slot of `part` (fp64).  A pixel is reached by at most 2x2 blocks;
+// loss_combine_kernel adds their slots in a fixed order (deterministic).
+__global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int H, const float* __restrict__ render,
+                                                                    const float* __restrict__ target, const Gauss w,
+                                                                    double* __restrict__ part,
+                                                                    double* __restrict__ s_part) {
     extern __shared__ __align__(16) unsigned char loss_smem[];
-    FwdSmem& S = *reinterpret_cast<FwdSmem*>(loss_smem);
+    FusedSmem& S = *reinterpret_cast<FusedSmem*>(loss_smem);
     const int tid = threadIdx.x, c = blockIdx.z;
     const int Wv = W - 2 * kR, Hv = H - 2 * kR;
     const int cx0 = blockIdx.x * kT, cy0 = blockIdx.y * kT;
@@ -104,8 +112,8 @@ __global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssi
     }
     __syncthreads();
     // horizontal sums: item = (row, run of 4 centre columns); inputs j0 .. j0 + 13 of the row
-    for (int k = tid; k < kI * (kT / kRun); k += kLossThreads) {
-        const int r = k / (kT / kRun), j0 = kRun * (k % (kT / kRun));
+    if (tid < kI * (kT / kRun)) {
+        const int r = tid / (kT / kRun), j0 = kRun * (tid % (kT / kRun));
         double acc[kRun][5];
 #pragma unroll
         for (int o = 0; o < kRun; o++)
@@ -131,25 +139,28 @@ __global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssi
 #pragma unroll
         for (int o = 0; o < kRun; o++)
 #pragma unroll
-            for (int q = 0; q < 5; q++) S.hs[q][r][j0 + o] = acc[o][q];
+            for (int q = 0; q < 5; q++) S.u.hs[q][r][j0 + o] = acc[o][q];
     }
     __syncthreads();
-    // vertical sums -> S and partials: item = (column, run of 4 centre rows); rows i0 .. i0 + 13
+    // vertical sums -> S and the partials: item = (column, run of 2 centre rows: all
+    // 512 threads busy); rows i0 .. i0 + 11
     double ssum = 0.0;
-    for (int k = tid; k < kT * (kT / kRun); k += kLossThreads) {
-        const int j = k % kT, i0 = kRun * (k / kT);
-        double st[kRun][5];
+    const bool vitem = tid < kT * (kT / kVRun);
+    const int vj = tid % kT, vi0 = kVRun * (tid / kT);
+    double pa[kVRun], pb[kVRun], pc[kVRun];
+    if (vitem) {
+        double st[kVRun][5];
 #pragma unroll
-        for (int o = 0; o < kRun; o++)
+        for (int o = 0; o < kVRun; o++)
 #pragma unroll
             for (int q = 0; q < 5; q++) st[o][q] = 0.0;
 #pragma unroll
-        for (int i = 0; i < kWin + kRun - 1; i++) {
+        for (int i = 0; i < kWin + kVRun - 1; i++) {
             double hv[5];
 #pragma unroll
-            for (int q = 0; q < 5; q++) hv[q] = S.hs[q][i0 + i][j];
+            for (int q = 0; q < 5; q++) hv[q] = S.u.hs[q][vi0 + i][vj];
 #pragma unroll
-            for (int o = 0; o < kRun; o++) {
+            for (int o = 0; o < kVRun; o++) {
                 const int t = i - o;
                 if (t >= 0 && t < kWin) {
 #pragma unroll
@@ -158,8 +169,9 @@ __global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssi
             }
         }
 #pragma unroll
-        for (int o = 0; o < kRun; o++) {
-            const int px = cx0 + j, py = cy0 + i0 + o;
+        for (int o = 0; o < kVRun; o++) {
+            pa[o] = pb[o] = pc[o] = 0.0;  // centres outside the valid range contribute nothing
+            const int px = cx0 + vj, py = cy0 + vi0 + o;
             if (px >= Wv || py >= Hv) continue;
             const double mx = st[o][0], my = st[o][1], exx = st[o][2], eyy = st[o][3], exy = st[o][4];
             const double sx2 = exx - mx * mx, sy2 = eyy - my * my, sxy = exy - mx * my;
@@ -168,12 +180,19 @@ __global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssi
             const double inv = 1.0 / (l2 * c2);  // the one fp64 division: 1/l2 = c2 inv, 1/c2 = l2 inv
             const double Sv = l1 * c1 * inv;
             const double dB = -Sv * (l2 * inv), dC = 2.0 * l1 * inv;
-            const double dA = 2.0 * my * c1 * inv - 2.0 * mx * Sv * (c2 * inv) - 2.0 * mx * dB - my * dC;
-            const size_t off = ((size_t)c * Hv + py) * Wv + px;
-            A[off] = (map_t)dA;
-            B[off] = (map_t)dB;
-            Cm[off] = (map_t)dC;
+            pa[o] = 2.0 * my * c1 * inv - 2.0 * mx * Sv * (c2 * inv) - 2.0 * mx * dB - my * dC;
+            pb[o] = dB;
+            pc[o] = dC;
             ssum += Sv;
+        }
+    }
+    __syncthreads();  // every read of hs done: abc / ht alias it
+    if (vitem) {
+#pragma unroll
+        for (int o = 0; o < kVRun; o++) {
+            S.u.t.abc[0][vi0 + o][vj] = pa[o];
+            S.u.t.abc[1][vi0 + o][vj] = pb[o];
+            S.u.t.abc[2][vi0 + o][vj] = pc[o];
         }
     }
 #pragma unroll
@@ -185,126 +204,123 @@ __global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssi
         for (int q = 0; q < kLossThreads / 32; q++) t += S.red[q];
         s_part[((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
     }
-}
-
-// block (x, y: pixel tile, z: channel).  dL_q = (1 - lambda) sign(r - t) / (3 N)
-//   - lambda / (3 Nv) sum_{centres p: q in window(p)} w(q - p) (A_p + 2 B_p r_q + C_p t_q)
-__global__ void __launch_bounds__(kLossThreads, kLossThreads >= 512 ? 2 : 3) ssim_bwd_kernel(int W, int H, float lambda, const float* __restrict__ render,
-                                                               const float* __restrict__ target, const Gauss w,
-                                                               const map_t* __restrict__ A, const map_t* __restrict__ B,
-                                                               const map_t* __restrict__ Cm, float* __restrict__ dL,
-                                                               double* __restrict__ l1_part) {
-    extern __shared__ __align__(16) unsigned char loss_smem[];
-    BwdSmem& S = *reinterpret_cast<BwdSmem*>(loss_smem);
-    const int tid = threadIdx.x, c = blockIdx.z;
-    const int Wv = W - 2 * kR, Hv = H - 2 * kR;
-    const bool ssim = lambda != 0.0f && Wv > 0 && Hv > 0;
-    const int qx0 = blockIdx.x * kT, qy0 = blockIdx.y * kT;
-    const double inv_n = 1.0 / (3.0 * (double)W * (double)H);
-    const double k_ssim = ssim ? -(double)lambda / (3.0 * (double)Wv * (double)Hv) : 0.0;
-    double l1 = 0.0;
-    if (ssim) {
-        // centres p = q - i (i in [0, 10]) for q in the tile: rows qy0-10 .. qy0+31, same columns
-        // every load of the region in flight before the first shared-memory store (in halves:
-        // 3 x 4 doubles in registers per thread)
-        constexpr int kIt = (kI * kI + kLossThreads - 1) / kLossThreads;  // 7
-        constexpr int kHalf = (kIt + 1) / 2;
+    // horizontal transposed sums: item = (centre row, run of 3 pixel columns u0 .. u0 + 2:
+    // 448 items); pixel
+    // column u takes centre columns u - 10 .. u (those inside the tile), centre u0 - 10 + jj with
+    // weight g[10 + o - jj] for output o
+    if (tid < kT * kHtRuns) {
+        const int r = tid / kHtRuns, u0 = kHtRun * (tid % kHtRuns);
+        double acc[kHtRun][3];
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            double va[kHalf], vb[kHalf], vc[kHalf];
+        for (int o = 0; o < kHtRun; o++) acc[o][0] = acc[o][1] = acc[o][2] = 0.0;
 #pragma unroll
-            for (int u = 0; u < kHalf; u++) {
-                const int k = tid + (h * kHalf + u) * kLossThreads;
-                const int r = k / kI, sc = k % kI;
-                const int py = qy0 - 2 * kR + r, px = qx0 - 2 * kR + sc;
-                const bool in = k < kI * kI && px >= 0 && py >= 0 && px < Wv && py < Hv;
-                const size_t o = ((size_t)c * Hv + py) * Wv + px;
-                va[u] = in ? (double)__ldg(A + o) : 0.0;
-                vb[u] = in ? (double)__ldg(B + o) : 0.0;
-                vc[u] = in ? (double)__ldg(Cm + o) : 0.0;
-            }
+        for (int jj = 0; jj < kWin + kHtRun - 1; jj++) {
+            const int j = u0 - 2 * kR + jj;
+            if (j < 0 || j >= kT) continue;
+            const double v0 = S.u.t.abc[0][r][j], v1 = S.u.t.abc[1][r][j], v2 = S.u.t.abc[2][r][j];
 #pragma unroll
-            for (int u = 0; u < kHalf; u++) {
-                const int k = tid + (h * kHalf + u) * kLossThreads;
-                if (k < kI * kI) {
-                    S.sm[0][k / kI][k % kI] = va[u];
-                    S.sm[1][k / kI][k % kI] = vb[u];
-                    S.sm[2][k / kI][k % kI] = vc[u];
+            for (int o = 0; o < kHtRun; o++) {
+                const int t = 2 * kR + o - jj;
+                if (t >= 0 && t < kWin) {
+                    const double g = w.g[t];
+                    acc[o][0] += g * v0;
+                    acc[o][1] += g * v1;
+                    acc[o][2] += g * v2;
                 }
             }
         }
-        __syncthreads();
-        // horizontal transposed sums: item = (row, run of 4 pixel columns); centre columns
-        // j0 .. j0 + 13 of the row, pixel j0 + o takes centre column j0 + o + t with weight g[10 - t]
-        for (int k = tid; k < kI * (kT / kRun); k += kLossThreads) {
-            const int r = k / (kT / kRun), j0 = kRun * (k % (kT / kRun));
-            double acc[kRun][3];
 #pragma unroll
-            for (int o = 0; o < kRun; o++) acc[o][0] = acc[o][1] = acc[o][2] = 0.0;
+        for (int o = 0; o < kHtRun; o++)
 #pragma unroll
-            for (int i = 0; i < kWin + kRun - 1; i++) {
-                const double v0 = S.sm[0][r][j0 + i], v1 = S.sm[1][r][j0 + i], v2 = S.sm[2][r][j0 + i];
-#pragma unroll
-                for (int o = 0; o < kRun; o++) {
-                    const int t = i - o;
-                    if (t >= 0 && t < kWin) {
-                        const double g = w.g[2 * kR - t];
-                        acc[o][0] += g * v0;
-                        acc[o][1] += g * v1;
-                        acc[o][2] += g * v2;
-                    }
-                }
-            }
-#pragma unroll
-            for (int o = 0; o < kRun; o++)
-#pragma unroll
-                for (int q = 0; q < 3; q++) S.hs[q][r][j0 + o] = acc[o][q];
-        }
-        __syncthreads();
+            for (int q = 0; q < 3; q++) S.u.t.ht[q][r][u0 + o] = acc[o][q];
     }
-    // vertical transposed sums + the pixel gradient: item = (column, run of 4 pixel rows)
-    for (int k = tid; k < kT * (kT / kRun); k += kLossThreads) {
-        const int j = k % kT, i0 = kRun * (k / kT);
+    __syncthreads();
+    // vertical transposed sums + the block's pixel partial: item = (pixel column u, run of 4 pixel
+    // rows v0 .. v0 + 3); pixel row v takes centre rows v - 10 .. v
+    if (tid < kI * kURuns) {
+        const int u = tid % kI, v0 = kRun * (tid / kI);
         double acc[kRun][3];
 #pragma unroll
         for (int o = 0; o < kRun; o++) acc[o][0] = acc[o][1] = acc[o][2] = 0.0;
-        if (ssim) {
 #pragma unroll
-            for (int i = 0; i < kWin + kRun - 1; i++) {
-                const double v0 = S.hs[0][i0 + i][j], v1 = S.hs[1][i0 + i][j], v2 = S.hs[2][i0 + i][j];
+        for (int ii = 0; ii < kWin + kRun - 1; ii++) {
+            const int i = v0 - 2 * kR + ii;
+            if (i < 0 || i >= kT) continue;
+            const double v0_ = S.u.t.ht[0][i][u], v1_ = S.u.t.ht[1][i][u], v2_ = S.u.t.ht[2][i][u];
 #pragma unroll
-                for (int o = 0; o < kRun; o++) {
-                    const int t = i - o;
-                    if (t >= 0 && t < kWin) {
-                        const double g = w.g[2 * kR - t];
-                        acc[o][0] += g * v0;
-                        acc[o][1] += g * v1;
-                        acc[o][2] += g * v2;
-                    }
+            for (int o = 0; o < kRun; o++) {
+                const int t = 2 * kR + o - ii;
+                if (t >= 0 && t < kWin) {
+                    const double g = w.g[t];
+                    acc[o][0] += g * v0_;
+                    acc[o][1] += g * v1_;
+                    acc[o][2] += g * v2_;
                 }
             }
         }
+        double* slot = part + (((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * (kI * kI);
 #pragma unroll
         for (int o = 0; o < kRun; o++) {
-            const int qx = qx0 + j, qy = qy0 + i0 + o;
-            if (qx >= W || qy >= H) continue;
-            const size_t off = ((size_t)qy * W + qx) * 3 + c;
-            const double x = __ldg(render + off), y = __ldg(target + off);
-            const double d = x - y;
+            const int v = v0 + o;
+            if (v >= kI || cx0 + u >= W || cy0 + v >= H) continue;
+            const double x = S.sx[v][u], y = S.sy[v][u];
+            slot[v * kI + u] = acc[o][0] + 2.0 * acc[o][1] * x + acc[o][2] * y;
+        }
+    }
+}
+
+// one thread per pixel (all three channels).  dL_q = (1 - lambda) sign(r - t) / (3 N)
+//   - lambda / (3 Nv) (sum over the <= 2x2 centre tiles whose region holds q of their partial)
+__global__ void __launch_bounds__(256) loss_combine_kernel(int W, int H, float lambda, const float* __restrict__ render,
+                                                          const float* __restrict__ target,
+                                                          const double* __restrict__ part, int gx, int gy,
+                                                          float* __restrict__ dL, double* __restrict__ l1_part) {
+    __shared__ double red[8];
+    const int tid = threadIdx.x;
+    const int Wv = W - 2 * kR, Hv = H - 2 * kR;
+    const bool ssim = lambda != 0.0f && Wv > 0 && Hv > 0;
+    const double inv_n = 1.0 / (3.0 * (double)W * (double)H);
+    const double k_ssim = ssim ? -(double)lambda / (3.0 * (double)Wv * (double)Hv) : 0.0;
+    const size_t q = (size_t)blockIdx.x * 256 + tid;
+    double l1 = 0.0;
+    if (q < (size_t)W * H) {
+        const int qy = (int)(q / W), qx = (int)(q % W);
+        // tiles b with 0 <= q - 32 b < 42, ascending: (x1 - 1 when it reaches q,) x1; -1 = none
+        const int x1 = min(qx / kT, gx - 1), y1 = min(qy / kT, gy - 1);
+        const int bx[2] = {x1 >= 1 && qx - kT * (x1 - 1) < kI ? x1 - 1 : -1, x1};
+        const int by[2] = {y1 >= 1 && qy - kT * (y1 - 1) < kI ? y1 - 1 : -1, y1};
+        // every load in flight before the arithmetic: 3 + 3 pixel values, up to 3 x 4 partials
+        float xs[3], ys[3];
+        double pv[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            xs[c] = __ldg(render + q * 3 + c);
+            ys[c] = __ldg(target + q * 3 + c);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int ty = by[k >> 1], tx = bx[k & 1];
+                const bool ok = ssim && ty >= 0 && tx >= 0;
+                const size_t blk = ((size_t)c * gy + (ok ? ty : 0)) * gx + (ok ? tx : 0);
+                pv[c][k] = ok ? __ldg(part + blk * (kI * kI) + (qy - kT * ty) * kI + (qx - kT * tx)) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            const double d = (double)xs[c] - (double)ys[c];
             l1 += fabs(d);
             double g = (1.0 - (double)lambda) * (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) * inv_n;
-            if (ssim) g += k_ssim * (acc[o][0] + 2.0 * acc[o][1] * x + acc[o][2] * y);
-            dL[off] = (float)g;
+            if (ssim) g += k_ssim * (((pv[c][0] + pv[c][1]) + pv[c][2]) + pv[c][3]);  // tiles in fixed order
+            dL[q * 3 + c] = (float)g;
         }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) l1 += __shfl_xor_sync(VKS_FULL_MASK, l1, o);
-    if ((tid & 31) == 0) S.red[tid >> 5] = l1;
+    if ((tid & 31) == 0) red[tid >> 5] = l1;
     __syncthreads();
     if (tid == 0) {
         double t = 0.0;
-        for (int q = 0; q < kLossThreads / 32; q++) t += S.red[q];
-        l1_part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+        for (int i = 0; i < 8; i++) t += red[i];
+        l1_part[blockIdx.x] = t;
     }
 }
 
@@ -335,25 +351,24 @@ __global__ void __launch_bounds__(kLossThreads) loss_finalize_kernel(int W, int 
 }
 
 struct LossWs {
-    map_t *A, *B, *C;
-    double *s_part, *l1_part;
+    double *part, *s_part, *l1_part;
+    int gx, gy, nl;
     size_t bytes;
 };
 
 LossWs carve_loss(void* base, int W, int H) {
     LossWs w{};
     const int Wv = W - 2 * kR > 0 ? W - 2 * kR : 0, Hv = H - 2 * kR > 0 ? H - 2 * kR : 0;
-    const size_t maps = (size_t)3 * Wv * Hv;
-    const size_t nfwd = (size_t)3 * ((Wv + kT - 1) / kT) * ((Hv + kT - 1) / kT);
-    const size_t nbwd = (size_t)3 * ((W + kT - 1) / kT) * ((H + kT - 1) / kT);
+    w.gx = (Wv + kT - 1) / kT;
+    w.gy = (Hv + kT - 1) / kT;
+    const size_t nfwd = (size_t)3 * w.gx * w.gy;
+    w.nl = (int)(((size_t)W * H + 255) / 256);
     size_t off = 0;
     char* b = static_cast<char*>(base);
     auto take = [&](size_t n) { double* p = b ? reinterpret_cast<double*>(b + off) : nullptr; off += (8 * n + 255) & ~(size_t)255; return p; };
-    w.A = reinterpret_cast<map_t*>(take(maps));  // (sized for doubles whatever map_t is)
-    w.B = reinterpret_cast<map_t*>(take(maps));
-    w.C = reinterpret_cast<map_t*>(take(maps));
+    w.part = take(nfwd * kI * kI > 0 ? nfwd * kI * kI : 1);
     w.s_part = take(nfwd > 0 ? nfwd : 1);
-    w.l1_part = take(nbwd);
+    w.l1_part = take(w.nl > 0 ? (size_t)w.nl : 1);
     w.bytes = off;
     return w;
 }
@@ -369,23 +384,22 @@ int launch_loss_grad(int W, int H, float lambda, const float* render, const floa
     const int Wv = W - 2 * kR, Hv = H - 2 * kR;
     const bool ssim = lambda != 0.0f && Wv > 0 && Hv > 0;
     int ns = 0;
-    // shared memory beyond 48 KB: the attributes are set on every call (per-device state)
-    if (cudaFuncSetAttribute(ssim_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwdSmem)) ||
-        cudaFuncSetAttribute(ssim_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BwdSmem)))
+    // shared memory beyond 48 KB: the attribute is set on every call (per-device state)
+    if (cudaFuncSetAttribute(ssim_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FusedSmem)))
         return cuda_fail(cudaGetLastError(), "loss smem attribute");
     if (ssim) {
-        const dim3 g((Wv + kT - 1) / kT, (Hv + kT - 1) / kT, 3);
-        ssim_fwd_kernel<<<g, kLossThreads, sizeof(FwdSmem), s>>>(W, H, render, target, w, ws.A, ws.B, ws.C, ws.s_part);
+        const dim3 g(ws.gx, ws.gy, 3);
+        ssim_fused_kernel<<<g, kLossThreads, sizeof(FusedSmem), s>>>(W, H, render, target, w, ws.part, ws.s_part);
         ns = (int)(g.x * g.y * g.z);
         if (int e = LaunchCheck::check()) return e;
     }
-    const dim3 gb((W + kT - 1) / kT, (H + kT - 1) / kT, 3);
-    ssim_bwd_kernel<<<gb, kLossThreads, sizeof(BwdSmem), s>>>(W, H, lambda, render, target, w, ws.A, ws.B, ws.C, dL,
-                                                              ws.l1_part);
-    if (int e = LaunchCheck::check()) return e;
+    if (ws.nl > 0) {
+        loss_combine_kernel<<<ws.nl, 256, 0, s>>>(W, H, lambda, render, target, ws.part, ws.gx, ws.gy, dL,
+                                                  ws.l1_part);
+        if (int e = LaunchCheck::check()) return e;
+    }
     if (loss) {
-        loss_finalize_kernel<<<1, kLossThreads, 0, s>>>(W, H, lambda, ws.s_part, ns, ws.l1_part,
-                                                        (int)(gb.x * gb.y * gb.z), loss);
+        loss_finalize_kernel<<<1, kLossThreads, 0, s>>>(W, H, lambda, ws.s_part, ns, ws.l1_part, ws.nl, loss);
         return LaunchCheck::check();
     }
     return VKS_OK;

@@ -31,7 +31,6 @@ constexpr int kIP = kI + 3;                       // float row pitch 45: the 4 r
 #define VKS_LOSS_RUN 4
 #endif
 constexpr int kRun = VKS_LOSS_RUN;                // outputs per thread and pass
-constexpr int kVRun = 2;                          // ... in the vertical forward pass (32 x 16 items)
 constexpr int kLossThreads = 512;             // 2 blocks x 16 warps per SM (75 KB of shared memory each)
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
@@ -51,26 +50,31 @@ Gauss window() {
     return w;
 }
 
-// dynamic shared memory of the fused kernel.  64-bit rows are padded to an odd pitch: a warp
-// stores four rows x eight runs (elements 4g + o of each row), and with pitch 33 doubles those 32
-// stores / loads spread over all 16 bank pairs (two wavefronts, the minimum for 256 B)
-constexpr int kHP = kT + 1;
-constexpr int kHtRun = 3, kHtRuns = kI / kHtRun;  // horizontal transposed pass: 14 runs of 3 columns
-constexpr int kURuns = (kI + kRun - 1) / kRun;    // vertical transposed pass: 11 runs of 4 rows
-constexpr int kUP = kI + 3;                       // pitch of the transposed rows (45)
+// dynamic shared memory of the fused kernel: two regions reused phase by phase.  64-bit rows
+// have an odd pitch, so a warp reading one element of 32 consecutive rows (stride 33 or 45
+// doubles) spreads over all 16 bank pairs; 32 consecutive columns of a row are contiguous.
+constexpr int kHP = kT + 1;       // 33
+constexpr int kXP = kI + 1;       // 43
+constexpr int kUP = kI + 3;       // 45
+constexpr int kLen = 16, kVLen = 14;  // rolling-window run lengths: 2 x 16 centre rows, 3 x 14 pixel cols / rows
 struct FusedSmem {
-    float sx[kI][kIP], sy[kI][kIP];   // input tile + halo = the pixel region the centres reach
-    union {
-        double hs[5][kI][kHP];        // horizontal window sums of x, y, x^2, y^2, xy
+    union {                                 // region A
+        double hs[5][kI][kHP];              // horizontal window sums of x, y, x^2, y^2, xy  (P1 -> P2)
+        double abc[3][kT][kHP];             // the centres' partials A, B, C                 (P3 -> P4)
+        double vt[3][kI][kXP];              // transposed window sums of A, B, C per pixel   (P5 -> P6)
+    } a;
+    union {                                 // region B
         struct {
-            double abc[3][kT][kHP];   // the centres' partials A, B, C
-            double ht[3][kT][kUP];    // their horizontal transposed sums over the pixel columns
-        } t;
-    } u;
+            float sx[kI][kIP], sy[kI][kIP];  // input tile + halo                             (P0 -> P1)
+        } in;
+        double st[5][kT][kHP];              // window statistics per centre                  (P2 -> P3)
+        double ht[3][kT][kUP];              // horizontal transposed sums of A, B, C         (P4 -> P5)
+    } b;
     double red[kLossThreads / 32];
 };
-static_assert(kI % kHtRun == 0 && kLossThreads >= kI * kURuns && kLossThreads >= kT * kHtRuns && kLossThreads >= kT * (kT / kVRun),
-              "the single-item phases need one thread per item");
+static_assert(kLossThreads >= kI * (kT / kRun) && kLossThreads >= kT * 5 * 2 && kLossThreads >= kT * 3 * 3 &&
+              kLossThreads >= kI * 3 * 3 && 2 * kLen == kT && 3 * kVLen == kI,
+              "one item per thread in every phase");
 
 // block (x: centre tile, y: centre tile, z: channel).  Centre p's window covers pixels p .. p+10,
 // so the block's 32x32 centres reach the 42x42 pixel region starting at the tile origin.  The
@@ -78,7 +82,9 @@ static_assert(kI % kHtRun == 0 && kLossThreads >= kI * kURuns && kLossThreads >=
 // transposed window sums of A, B, C over the region and, per pixel q,
 //   part_b(q) = sum_{centres p of the block} w(q - p) (A_p + 2 B_p x_q + C_p y_q)
 // into its own 42x42 slot of `part` (fp64).  A pixel is reached by at most 2x2 blocks;
-// loss_combine_kernel adds their slots in a fixed order (deterministic).
+// loss_combine_kernel adds their slots in a fixed order (deterministic).  The vertical and the
+// transposed passes run one (column or row, quantity, run) per thread with the 11-tap window
+// rolling in registers: 26 (24) shared-memory loads for 16 (14) outputs.
 __global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int H, const float* __restrict__ render,
                                                                     const float* __restrict__ target, const Gauss w,
                                                                     double* __restrict__ part,
@@ -88,7 +94,7 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int 
     const int tid = threadIdx.x, c = blockIdx.z;
     const int Wv = W - 2 * kR, Hv = H - 2 * kR;
     const int cx0 = blockIdx.x * kT, cy0 = blockIdx.y * kT;
-    {   // every load of the tile in flight before the first shared-memory store
+    {   // P0: every load of the tile in flight before the first shared-memory store
         constexpr int kIt = (kI * kI + kLossThreads - 1) / kLossThreads;
         float vx[kIt], vy[kIt];
 #pragma unroll
@@ -105,13 +111,13 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int 
         for (int it = 0; it < kIt; it++) {
             const int k = tid + it * kLossThreads;
             if (k < kI * kI) {
-                S.sx[k / kI][k % kI] = vx[it];
-                S.sy[k / kI][k % kI] = vy[it];
+                S.b.in.sx[k / kI][k % kI] = vx[it];
+                S.b.in.sy[k / kI][k % kI] = vy[it];
             }
         }
     }
     __syncthreads();
-    // horizontal sums: item = (row, run of 4 centre columns); inputs j0 .. j0 + 13 of the row
+    // P1 horizontal sums: item = (row, run of 4 centre columns); inputs j0 .. j0 + 13 of the row
     if (tid < kI * (kT / kRun)) {
         const int r = tid / (kT / kRun), j0 = kRun * (tid % (kT / kRun));
         double acc[kRun][5];
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int 
             for (int q = 0; q < 5; q++) acc[o][q] = 0.0;
 #pragma unroll
         for (int i = 0; i < kWin + kRun - 1; i++) {
-            const double x = S.sx[r][j0 + i], y = S.sy[r][j0 + i];
+            const double x = S.b.in.sx[r][j0 + i], y = S.b.in.sy[r][j0 + i];
             const double xx = x * x, yy = y * y, xy = x * y;
 #pragma unroll
             for (int o = 0; o < kRun; o++) {
@@ -139,61 +145,53 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int 
 #pragma unroll
         for (int o = 0; o < kRun; o++)
 #pragma unroll
-            for (int q = 0; q < 5; q++) S.u.hs[q][r][j0 + o] = acc[o][q];
+            for (int q = 0; q < 5; q++) S.a.hs[q][r][j0 + o] = acc[o][q];
     }
     __syncthreads();
-    // vertical sums -> S and the partials: item = (column, run of 2 centre rows: all
-    // 512 threads busy); rows i0 .. i0 + 11
-    double ssum = 0.0;
-    const bool vitem = tid < kT * (kT / kVRun);
-    const int vj = tid % kT, vi0 = kVRun * (tid / kT);
-    double pa[kVRun], pb[kVRun], pc[kVRun];
-    if (vitem) {
-        double st[kVRun][5];
+    // P2 vertical sums: item = (centre column j, statistic q, half h): centre rows 16h .. 16h + 15
+    // from hs rows 16h .. 16h + 25
+    if (tid < kT * 5 * 2) {
+        const int j = tid % kT, q = (tid / kT) % 5, i0 = kLen * (tid / (kT * 5));
+        double acc[kLen];
 #pragma unroll
-        for (int o = 0; o < kVRun; o++)
+        for (int o = 0; o < kLen; o++) acc[o] = 0.0;
 #pragma unroll
-            for (int q = 0; q < 5; q++) st[o][q] = 0.0;
+        for (int i = 0; i < kLen + kWin - 1; i++) {
+            const double v = S.a.hs[q][i0 + i][j];
 #pragma unroll
-        for (int i = 0; i < kWin + kVRun - 1; i++) {
-            double hv[5];
-#pragma unroll
-            for (int q = 0; q < 5; q++) hv[q] = S.u.hs[q][vi0 + i][vj];
-#pragma unroll
-            for (int o = 0; o < kVRun; o++) {
+            for (int o = 0; o < kLen; o++) {
                 const int t = i - o;
-                if (t >= 0 && t < kWin) {
-#pragma unroll
-                    for (int q = 0; q < 5; q++) st[o][q] += w.g[t] * hv[q];
-                }
+                if (t >= 0 && t < kWin) acc[o] += w.g[t] * v;
             }
         }
 #pragma unroll
-        for (int o = 0; o < kVRun; o++) {
-            pa[o] = pb[o] = pc[o] = 0.0;  // centres outside the valid range contribute nothing
-            const int px = cx0 + vj, py = cy0 + vi0 + o;
-            if (px >= Wv || py >= Hv) continue;
-            const double mx = st[o][0], my = st[o][1], exx = st[o][2], eyy = st[o][3], exy = st[o][4];
+        for (int o = 0; o < kLen; o++) S.b.st[q][i0 + o][j] = acc[o];
+    }
+    __syncthreads();
+    // P3 S and its partials per centre (two centres per thread); centres outside the valid range
+    // contribute nothing
+    double ssum = 0.0;
+#pragma unroll
+    for (int m = 0; m < kT * kT / kLossThreads; m++) {
+        const int k = tid + m * kLossThreads, i = k / kT, j = k % kT;
+        double pa = 0.0, pb = 0.0, pc = 0.0;
+        if (cx0 + j < Wv && cy0 + i < Hv) {
+            const double mx = S.b.st[0][i][j], my = S.b.st[1][i][j];
+            const double exx = S.b.st[2][i][j], eyy = S.b.st[3][i][j], exy = S.b.st[4][i][j];
             const double sx2 = exx - mx * mx, sy2 = eyy - my * my, sxy = exy - mx * my;
             const double l1 = 2 * mx * my + kC1, l2 = mx * mx + my * my + kC1;
             const double c1 = 2 * sxy + kC2, c2 = sx2 + sy2 + kC2;
             const double inv = 1.0 / (l2 * c2);  // the one fp64 division: 1/l2 = c2 inv, 1/c2 = l2 inv
             const double Sv = l1 * c1 * inv;
             const double dB = -Sv * (l2 * inv), dC = 2.0 * l1 * inv;
-            pa[o] = 2.0 * my * c1 * inv - 2.0 * mx * Sv * (c2 * inv) - 2.0 * mx * dB - my * dC;
-            pb[o] = dB;
-            pc[o] = dC;
+            pa = 2.0 * my * c1 * inv - 2.0 * mx * Sv * (c2 * inv) - 2.0 * mx * dB - my * dC;
+            pb = dB;
+            pc = dC;
             ssum += Sv;
         }
-    }
-    __syncthreads();  // every read of hs done: abc / ht alias it
-    if (vitem) {
-#pragma unroll
-        for (int o = 0; o < kVRun; o++) {
-            S.u.t.abc[0][vi0 + o][vj] = pa[o];
-            S.u.t.abc[1][vi0 + o][vj] = pb[o];
-            S.u.t.abc[2][vi0 + o][vj] = pc[o];
-        }
+        S.a.abc[0][i][j] = pa;
+        S.a.abc[1][i][j] = pb;
+        S.a.abc[2][i][j] = pc;
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) ssum += __shfl_xor_sync(VKS_FULL_MASK, ssum, o);
@@ -204,68 +202,57 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int 
         for (int q = 0; q < kLossThreads / 32; q++) t += S.red[q];
         s_part[((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
     }
-    // horizontal transposed sums: item = (centre row, run of 3 pixel columns u0 .. u0 + 2:
-    // 448 items); pixel
-    // column u takes centre columns u - 10 .. u (those inside the tile), centre u0 - 10 + jj with
-    // weight g[10 + o - jj] for output o
-    if (tid < kT * kHtRuns) {
-        const int r = tid / kHtRuns, u0 = kHtRun * (tid % kHtRuns);
-        double acc[kHtRun][3];
+    // P4 horizontal transposed sums: item = (centre row r, partial m, third): pixel columns
+    // u0 .. u0 + 13 (u0 = 14 third) take centre columns u - 10 .. u inside the tile: centre
+    // u0 - 10 + jj feeds output o with weight g[10 + o - jj]
+    if (tid < kT * 3 * 3) {
+        const int r = tid % kT, m = (tid / kT) % 3, u0 = kVLen * (tid / (kT * 3));
+        double acc[kVLen];
 #pragma unroll
-        for (int o = 0; o < kHtRun; o++) acc[o][0] = acc[o][1] = acc[o][2] = 0.0;
+        for (int o = 0; o < kVLen; o++) acc[o] = 0.0;
 #pragma unroll
-        for (int jj = 0; jj < kWin + kHtRun - 1; jj++) {
+        for (int jj = 0; jj < kVLen + kWin - 1; jj++) {
             const int j = u0 - 2 * kR + jj;
-            if (j < 0 || j >= kT) continue;
-            const double v0 = S.u.t.abc[0][r][j], v1 = S.u.t.abc[1][r][j], v2 = S.u.t.abc[2][r][j];
+            const double v = (j >= 0 && j < kT) ? S.a.abc[m][r][j] : 0.0;
 #pragma unroll
-            for (int o = 0; o < kHtRun; o++) {
+            for (int o = 0; o < kVLen; o++) {
                 const int t = 2 * kR + o - jj;
-                if (t >= 0 && t < kWin) {
-                    const double g = w.g[t];
-                    acc[o][0] += g * v0;
-                    acc[o][1] += g * v1;
-                    acc[o][2] += g * v2;
-                }
+                if (t >= 0 && t < kWin) acc[o] += w.g[t] * v;
             }
         }
 #pragma unroll
-        for (int o = 0; o < kHtRun; o++)
-#pragma unroll
-            for (int q = 0; q < 3; q++) S.u.t.ht[q][r][u0 + o] = acc[o][q];
+        for (int o = 0; o < kVLen; o++) S.b.ht[m][r][u0 + o] = acc[o];
     }
     __syncthreads();
-    // vertical transposed sums + the block's pixel partial: item = (pixel column u, run of 4 pixel
-    // rows v0 .. v0 + 3); pixel row v takes centre rows v - 10 .. v
-    if (tid < kI * kURuns) {
-        const int u = tid % kI, v0 = kRun * (tid / kI);
-        double acc[kRun][3];
+    // P5 vertical transposed sums: item = (pixel column u, partial m, third): pixel rows v0 .. v0 + 13
+    // take centre rows v - 10 .. v inside the tile
+    if (tid < kI * 3 * 3) {
+        const int u = tid % kI, m = (tid / kI) % 3, v0 = kVLen * (tid / (kI * 3));
+        double acc[kVLen];
 #pragma unroll
-        for (int o = 0; o < kRun; o++) acc[o][0] = acc[o][1] = acc[o][2] = 0.0;
+        for (int o = 0; o < kVLen; o++) acc[o] = 0.0;
 #pragma unroll
-        for (int ii = 0; ii < kWin + kRun - 1; ii++) {
+        for (int ii = 0; ii < kVLen + kWin - 1; ii++) {
             const int i = v0 - 2 * kR + ii;
-            if (i < 0 || i >= kT) continue;
-            const double v0_ = S.u.t.ht[0][i][u], v1_ = S.u.t.ht[1][i][u], v2_ = S.u.t.ht[2][i][u];
+            const double v = (i >= 0 && i < kT) ? S.b.ht[m][i][u] : 0.0;
 #pragma unroll
-            for (int o = 0; o < kRun; o++) {
+            for (int o = 0; o < kVLen; o++) {
                 const int t = 2 * kR + o - ii;
-                if (t >= 0 && t < kWin) {
-                    const double g = w.g[t];
-                    acc[o][0] += g * v0_;
-                    acc[o][1] += g * v1_;
-                    acc[o][2] += g * v2_;
-                }
+                if (t >= 0 && t < kWin) acc[o] += w.g[t] * v;
             }
         }
-        double* slot = part + (((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * (kI * kI);
 #pragma unroll
-        for (int o = 0; o < kRun; o++) {
-            const int v = v0 + o;
-            if (v >= kI || cx0 + u >= W || cy0 + v >= H) continue;
-            const double x = S.sx[v][u], y = S.sy[v][u];
-            slot[v * kI + u] = acc[o][0] + 2.0 * acc[o][1] * x + acc[o][2] * y;
-        }
+        for (int o = 0; o < kVLen; o++) S.a.vt[m][v0 + o][u] = acc[o];
+    }
+    __syncthreads();
+    // P6 the block's pixel partial A + 2 B x + C y over the region (pixel values re-read: L2)
+    double* slot = part + (((size_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * (kI * kI);
+    for (int k = tid; k < kI * kI; k += kLossThreads) {
+        const int v = k / kI, u = k % kI;
+        if (cx0 + u >= W || cy0 + v >= H) continue;
+        const size_t off = ((size_t)(cy0 + v) * W + (cx0 + u)) * 3 + c;
+        const double x = __ldg(render + off), y = __ldg(target + off);
+        slot[k] = S.a.vt[0][v][u] + 2.0 * S.a.vt[1][v][u] * x + S.a.vt[2][v][u] * y;
     }
 }
 

@@ -73,3 +73,19 @@ def test_loss_grad_pure_ssim_and_thin_images(H, W, lam):
     assert loss == pytest.approx(lo, rel=1e-6, abs=1e-9)
     G, Go = g.astype(np.float64) * 3 * H * W, go * 3 * H * W
     assert np.all(np.abs(G - Go) <= 1e-6 * np.abs(Go) + 1e-9)
+
+
+@pytest.mark.parametrize("H,W", [(42, 42), (43, 75), (74, 74), (75, 106), (12, 300)])
+def test_loss_grad_tile_seams(H, W):
+    """Centre-tile seams of the fused kernel (32x32 centre tiles, each reaching a 42x42 pixel
+    region; a pixel gets the partials of 1, 2 or 4 tiles): one tile exactly (42x42), a ragged
+    second tile (43x75), 2x2 tiles whose regions overlap by 10 pixels (74x74: Wv = 64) and one past
+    it (75x106), and a strip two centres high (12x300)."""
+    r, t = _pair(H, W, seed=11 * H + W)
+    loss, g = _gpu(r, t, 0.2)
+    lo, go, _ = oracle.loss_grad(r, t, 0.2)
+    assert loss == pytest.approx(lo, rel=1e-6, abs=1e-9)
+    G, Go = g.astype(np.float64) * 3 * H * W, go * 3 * H * W
+    err = np.abs(G - Go)
+    bad = err > 1e-6 * np.abs(Go) + 1e-9
+    assert not bad.any(), (int(bad.sum()), np.argwhere(bad)[:4].tolist(), float(err.max()))

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_loss.py -x -q 2>&1 | tail -1
+python -m pytest tests/test_gpu_loss.py -x -q 2>&1 | tail -3
 python bench.py > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err; tail -c 300 gpurun_out/bench_quick.err
 python - <<'PY'
 import json

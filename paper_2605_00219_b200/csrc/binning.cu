@@ -661,15 +661,24 @@ enum { kPassPlain = 0, kPassTileLast = 2 };
 
 // lanes of the warp holding the same DBITS-bit digit (and the same `valid`): DBITS ballots
 // instead of __match_any_sync, whose cost grows with the number of distinct values
+// Each bit: the predicate straight from d & (1 << b) (one LOP3), the ballot, and the lanes with
+// the same bit as this lane — the ballot, inverted under the predicate's complement — ANDed in:
+// 4 instructions per bit (the C++ form compiled to 6: shift, and, compare, select, vote, merge).
 template <int DBITS>
 __device__ __forceinline__ u32 digit_peers(u32 d, bool valid = true) {
     u32 peers = __ballot_sync(VKS_FULL_MASK, valid);
     if (!valid) peers = ~peers;
 #pragma unroll
     for (int b = 0; b < DBITS; b++) {
-        const bool bit = (d >> b) & 1u;
-        const u32 bal = __ballot_sync(VKS_FULL_MASK, bit);
-        peers &= bit ? bal : ~bal;
+        u32 same;
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %1, %2;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+            "@!p not.b32 %0, %0;\n\t}"
+            : "=r"(same)
+            : "r"(d), "r"(1u << b));
+        peers &= same;
     }
     return peers;
 }

@@ -972,11 +972,13 @@ struct ExpandSrc {
 
 // floor(k / w) for 0 <= k < 2^20, 1 <= w < 2^16: (k + 0.5) / w lies at least 0.5 / w from an
 // integer, while x * rcp.approx(w) errs by < 2^-21 (k + 0.5) / w < 0.5 / w
-__device__ __forceinline__ int div_floor(int k, int w) {
+__device__ __forceinline__ float rcp_width(int w) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)w));  // w >= 1: no range special cases
-    return (int)(((float)k + 0.5f) * r);
+    return r;
 }
+__device__ __forceinline__ int div_floor_r(int k, float r) { return (int)(((float)k + 0.5f) * r); }
+__device__ __forceinline__ int div_floor(int k, int w) { return div_floor_r(k, rcp_width(w)); }
 
 // f(slot, tile, id) for every key slot in [c0, c1) (c1 - c0 <= 512, all inside block b), one
 // slot per lane per round of 32.  The Gaussian owning slot s is the last one with slot0 <= s.  A
@@ -1013,6 +1015,14 @@ __device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0
     while (W < c1) {
         const u32 a = a_n, id = id_n;  // lane j: Gaussian g + j (a = its first slot; ~0: none)
         const u64 rc = rc_n;
+        // per Gaussian, once per group: slot k of the rect (rows outer) is tile
+        // base + k + floor(k / w) (TX - w), base = y0 TX + x0; floor via 1 / w
+        int gx0, gx1, gy0, gy1;
+        unpack_rect(rc, gx0, gx1, gy0, gy1);
+        const int gw = max(gx1 - gx0, 1);
+        const u32 gbase = (u32)(gy0 * src.TX + gx0);
+        const int gstep = src.TX - gw;
+        const float grw = rcp_width(gw);
         const u32 gn = g + 32;
         a_n = 0xFFFFFFFFu;  // the next group's records, in flight while this group expands
         if (gn + lane < src.V) {
@@ -1033,16 +1043,15 @@ __device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0
             const int own = base + __popc(starts & ltle);
             const int srcl = own < 0 ? 0 : own;
             const u32 a_o = __shfl_sync(VKS_FULL_MASK, a, srcl);
-            const u64 rc_o = __shfl_sync(VKS_FULL_MASK, rc, srcl);
+            const u32 base_o = __shfl_sync(VKS_FULL_MASK, gbase, srcl);
+            const int step_o = __shfl_sync(VKS_FULL_MASK, gstep, srcl);
+            const float rw_o = __shfl_sync(VKS_FULL_MASK, grw, srcl);
             const u32 id_o = __shfl_sync(VKS_FULL_MASK, id, srcl);
             const u32 slot = W + (u32)lane;
             if (slot < gend) {
-                int x0, x1, y0, y1;
-                unpack_rect(rc_o, x0, x1, y0, y1);
-                const int w = x1 - x0;
                 const int k = (int)(slot - a_o);  // index within the rect, rows outer
-                const int ry = div_floor(k, w);
-                f(slot, (u32)((y0 + ry) * src.TX + x0 + (k - ry * w)), id_o);
+                const int ry = div_floor_r(k, rw_o);
+                f(slot, base_o + (u32)k + (u32)(ry * step_o), id_o);
             }
             base += __popc(starts);
         }

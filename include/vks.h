@@ -374,7 +374,7 @@ int vks_adam_step(const vks_adam_config* acfg, int64_t n, int32_t sh_coeffs, flo
  *   render, target: device [height, width, 3] fp32 (HWC, as vks_raster_fwd's image)
  *   dL_dimage: device [height, width, 3] fp32, written; loss: device fp32 [1], written (nullable)
  *   workspace: device, 256-byte aligned, >= vks_loss_workspace_bytes(width, height) bytes
- *     (fp64 partial maps of the window centres: ~72 B per pixel)
+ *     (one fp64 42x42 partial slot per 32x32 tile of window centres and channel: ~41 B per pixel)
  * Errors (before any launch): VKS_ERR_INVALID_ARG for a null pointer, a size outside [1, 65536],
  * lambda outside [0, 1], or lambda > 0 with width or height < 11; VKS_ERR_WORKSPACE.
  * Asynchronous on `stream`; deterministic.

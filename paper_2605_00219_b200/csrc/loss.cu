@@ -256,27 +256,38 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int 
     }
 }
 
-// one thread per pixel (all three channels).  dL_q = (1 - lambda) sign(r - t) / (3 N)
+// one thread per pixel (all three channels), image rows over the grid's rows.  dL_q = (1 - lambda) sign(r - t) / (3 N)
 //   - lambda / (3 Nv) (sum over the <= 2x2 centre tiles whose region holds q of their partial)
-__global__ void __launch_bounds__(256) loss_combine_kernel(int W, int H, float lambda, const float* __restrict__ render,
+constexpr int kCombThreads = 128;  // pixels per combine block (1237 columns: 10 blocks, 3% idle)
+__global__ void __launch_bounds__(kCombThreads) loss_combine_kernel(int W, int H, float lambda, const float* __restrict__ render,
                                                           const float* __restrict__ target,
                                                           const double* __restrict__ part, int gx, int gy,
                                                           float* __restrict__ dL, double* __restrict__ l1_part) {
-    __shared__ double red[8];
+    __shared__ double red[kCombThreads / 32];
     const int tid = threadIdx.x;
     const int Wv = W - 2 * kR, Hv = H - 2 * kR;
     const bool ssim = lambda != 0.0f && Wv > 0 && Hv > 0;
     const double inv_n = 1.0 / (3.0 * (double)W * (double)H);
     const double k_ssim = ssim ? -(double)lambda / (3.0 * (double)Wv * (double)Hv) : 0.0;
-    const size_t q = (size_t)blockIdx.x * 256 + tid;
+    const int qx = blockIdx.x * kCombThreads + tid;
     double l1 = 0.0;
-    if (q < (size_t)W * H) {
-        const int qy = (int)(q / W), qx = (int)(q % W);
+    for (int qy = blockIdx.y; qx < W && qy < H; qy += gridDim.y) {  // rows blockIdx.y + k gridDim.y
+        const size_t q = (size_t)qy * W + qx;
         // tiles b with 0 <= q - 32 b < 42, ascending: (x1 - 1 when it reaches q,) x1; -1 = none
         const int x1 = min(qx / kT, gx - 1), y1 = min(qy / kT, gy - 1);
         const int bx[2] = {x1 >= 1 && qx - kT * (x1 - 1) < kI ? x1 - 1 : -1, x1};
         const int by[2] = {y1 >= 1 && qy - kT * (y1 - 1) < kI ? y1 - 1 : -1, y1};
         // every load in flight before the arithmetic: 3 + 3 pixel values, up to 3 x 4 partials
+        // (tile k's slot offset for this pixel once; the channels are gx gy 42^2 apart)
+        const size_t cstride = (size_t)gx * gy * (kI * kI);
+        size_t toff[4];
+        bool tok[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int ty = by[k >> 1], tx = bx[k & 1];
+            tok[k] = ssim && ty >= 0 && tx >= 0;
+            toff[k] = tok[k] ? (size_t)(ty * gx + tx) * (kI * kI) + (size_t)((qy - kT * ty) * kI + (qx - kT * tx)) : 0;
+        }
         float xs[3], ys[3];
         double pv[3][4];
 #pragma unroll
@@ -284,12 +295,7 @@ __global__ void __launch_bounds__(256) loss_combine_kernel(int W, int H, float l
             xs[c] = __ldg(render + q * 3 + c);
             ys[c] = __ldg(target + q * 3 + c);
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int ty = by[k >> 1], tx = bx[k & 1];
-                const bool ok = ssim && ty >= 0 && tx >= 0;
-                const size_t blk = ((size_t)c * gy + (ok ? ty : 0)) * gx + (ok ? tx : 0);
-                pv[c][k] = ok ? __ldg(part + blk * (kI * kI) + (qy - kT * ty) * kI + (qx - kT * tx)) : 0.0;
-            }
+            for (int k = 0; k < 4; k++) pv[c][k] = tok[k] ? __ldg(part + toff[k] + c * cstride) : 0.0;
         }
 #pragma unroll
         for (int c = 0; c < 3; c++) {
@@ -306,8 +312,8 @@ __global__ void __launch_bounds__(256) loss_combine_kernel(int W, int H, float l
     __syncthreads();
     if (tid == 0) {
         double t = 0.0;
-        for (int i = 0; i < 8; i++) t += red[i];
-        l1_part[blockIdx.x] = t;
+        for (int i = 0; i < kCombThreads / 32; i++) t += red[i];
+        l1_part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
 }
 
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(kLossThreads) loss_finalize_kernel(int W, int 
 
 struct LossWs {
     double *part, *s_part, *l1_part;
-    int gx, gy, nl;
+    int gx, gy, ncx, ncy, nl;
     size_t bytes;
 };
 
@@ -349,7 +355,9 @@ LossWs carve_loss(void* base, int W, int H) {
     w.gx = (Wv + kT - 1) / kT;
     w.gy = (Hv + kT - 1) / kT;
     const size_t nfwd = (size_t)3 * w.gx * w.gy;
-    w.nl = (int)(((size_t)W * H + 255) / 256);
+    w.ncx = (W + kCombThreads - 1) / kCombThreads;
+    w.ncy = H < 65535 ? H : 65535;  // grid rows (the kernel strides over the image rows)
+    w.nl = w.ncx * w.ncy;
     size_t off = 0;
     char* b = static_cast<char*>(base);
     auto take = [&](size_t n) { double* p = b ? reinterpret_cast<double*>(b + off) : nullptr; off += (8 * n + 255) & ~(size_t)255; return p; };
@@ -381,7 +389,7 @@ int launch_loss_grad(int W, int H, float lambda, const float* render, const floa
         if (int e = LaunchCheck::check()) return e;
     }
     if (ws.nl > 0) {
-        loss_combine_kernel<<<ws.nl, 256, 0, s>>>(W, H, lambda, render, target, ws.part, ws.gx, ws.gy, dL,
+        loss_combine_kernel<<<dim3(ws.ncx, ws.ncy), kCombThreads, 0, s>>>(W, H, lambda, render, target, ws.part, ws.gx, ws.gy, dL,
                                                   ws.l1_part);
         if (int e = LaunchCheck::check()) return e;
     }

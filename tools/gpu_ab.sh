@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:"project_" -o gpurun_out/proj_src python tools/profile_batch.py bicycle 8 > gpurun_out/proj_ncu.log 2>&1
-tail -1 gpurun_out/proj_ncu.log
+timeout 600 python tools/time_binsort_async.py bicycle
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none --csv --log-file gpurun_out/binasync_launches.csv python tools/time_binsort_async.py bicycle 1 > /dev/null 2>&1

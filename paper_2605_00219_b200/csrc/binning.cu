@@ -787,7 +787,6 @@ struct SortSmem {
     alignas(128) u32 keys[kSortTile];  // input staging (bulk copy), then the reordered tile
     alignas(128) u32 vals[kSortTile];
     u32 whist[kSortWarps][RADIX];
-    u32 binstart[RADIX];
     u32 gbase[RADIX];
     u32 wsum[kSortWarps];
     alignas(8) unsigned long long mbar;
@@ -851,14 +850,15 @@ __device__ __forceinline__ void rank_and_store(SortSmem<1 << DBITS>& S, u32 n, i
     }
     if (lane == 31) S.wsum[warp] = incl;
     __syncthreads();
-    {
+    {   // the digit's block start folded into its per-warp offsets: one shared-memory read per key
         u32 start = incl - total;
         for (int w = 0; w < warp; w++) start += S.wsum[w];
 #pragma unroll
         for (int q = 0; q < DPT; q++) {
             const int d = tid * DPT + q;
             if (d < RADIX) {
-                S.binstart[d] = start;
+#pragma unroll
+                for (int w = 0; w < kSortWarps; w++) S.whist[w][d] += start;
                 S.gbase[d] -= start;
             }
             start += dtot[q];
@@ -871,8 +871,7 @@ __device__ __forceinline__ void rank_and_store(SortSmem<1 << DBITS>& S, u32 n, i
         const int slot = seg + i * 32 + lane;
         kk[i] = S.keys[slot];
         vv[i] = S.vals[slot];
-        const u32 d = ((kk[i] - kbias) >> shift) & DMASK;
-        rank[i] += S.binstart[d] + S.whist[warp][d];
+        rank[i] += S.whist[warp][((kk[i] - kbias) >> shift) & DMASK];
     }
     __syncthreads();
 #pragma unroll

@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python tools/time_binsort_async.py bicycle
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none --csv --log-file gpurun_out/binasync_launches.csv python tools/time_binsort_async.py bicycle 1 > /dev/null 2>&1
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_bin_async.py -x -q -k "bin or sort or async or P2 or bicycle" 2>&1 | tail -2
+for i in 1 2; do timeout 300 python tools/time_binsort.py bicycle; done
+run() { timeout 300 python bench.py --steps 20 --no-e2e --no-cpu-baseline --no-batch1 "$@" 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['stages_ms']['bin_sort'], d['clocks']['sm_mhz'])"; }
+echo "bench $(run)"; echo "bench $(run)"

@@ -342,16 +342,8 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
     __shared__ u32 s_w[kDownThreads / 32], s_v[kDownThreads / 32];
     __shared__ u32 s_pre[kDownThreads / 32], s_vpre[kDownThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    {
-        u32 ps = 0, pv = 0;
-        for (u32 i = tid; i < blockIdx.x; i += kDownThreads) {
-            ps += __ldg(part_sum + i);
-            if (MODE == 0) pv += __ldg(co.vis_prefix + i);
-        }
-        ps = __reduce_add_sync(VKS_FULL_MASK, ps);
-        pv = __reduce_add_sync(VKS_FULL_MASK, pv);
-        if (lane == 0) { s_pre[warp] = ps; s_vpre[warp] = pv; }
-    }
+    // the tile's items first (the DRAM round trip), the predecessors' block sums (L2) while they
+    // are in flight
     const u64 wbase = warp_base<ITEMS>(warp);
     int v[ITEMS];
     u32 ex[ITEMS];
@@ -362,6 +354,16 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
         dbits_pre[q] = (MODE == 0 && i < count) ? __ldg(co.depth_bits + i) : 0u;
     }
     load_scan_items<MODE, ITEMS>(tiles, rc, count, wbase, lane, v);
+    {
+        u32 ps = 0, pv = 0;
+        for (u32 i = tid; i < blockIdx.x; i += kDownThreads) {
+            ps += __ldg(part_sum + i);
+            if (MODE == 0) pv += __ldg(co.vis_prefix + i);
+        }
+        ps = __reduce_add_sync(VKS_FULL_MASK, ps);
+        pv = __reduce_add_sync(VKS_FULL_MASK, pv);
+        if (lane == 0) { s_pre[warp] = ps; s_vpre[warp] = pv; }
+    }
     const u32 wtot = warp_striped_excl<ITEMS>(v, ex, lane);
     u32 wvis = 0;
     if (MODE == 0) {

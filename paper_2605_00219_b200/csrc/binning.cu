@@ -257,7 +257,9 @@ __global__ void __launch_bounds__(kDownThreads) scan_reduce_kernel(const int* __
     } else {
         load_scan_items<MODE, ITEMS>(tiles, rc_in, count, wbase, lane, v);
         // tile rect code of every visible Gaussian at its id (0 for the others: whole sectors are
-        // written), computed exactly as projection step 11 (this TU is compiled -fmad=false)
+        // written), computed exactly as projection step 11 (this TU is compiled -fmad=false).
+        // means2d / radii are loaded for every row in range (the projection writes culled rows as
+        // zeros), not only where tiles > 0: one DRAM round trip instead of two dependent ones
         const float2* __restrict__ means2d = co.means2d;
         const int2* __restrict__ radii = co.radii;
 #pragma unroll
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kDownThreads) scan_reduce_kernel(const int* __
 #pragma unroll
             for (int q = 0; q < 8; q++) {
                 const u64 i = wbase + 32 * (h + q) + lane;
-                if (v[h + q] > 0) {
+                if (i < count) {
                     m[q] = __ldg(means2d + i);
                     r[q] = __ldg(radii + i);
                 }

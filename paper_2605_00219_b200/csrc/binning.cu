@@ -16,7 +16,7 @@
 //                         many as the visible depth-bit range needs (bicycle: 27 bits, 4 x 7).
 //  3. scan (depth order) reduce-then-scan of the rect tile counts; the reduce gathers the rect
 //                         codes into depth order -> first key slot of each Gaussian, and
-//                         first[b] = the Gaussian holding key slot 4096 b.
+//                         first[c] = the Gaussian holding key slot 512 c (one per warp chunk).
 //  4. rect_diff_kernel    2-D difference array of the rects (4 shared-memory updates per Gaussian)
 //     tile_count_kernel   2-D prefix -> per-tile list lengths -> CSR tile_offsets.
 //  5. key pass            the first tile-bit pass straight from the rect codes, never storing the
@@ -63,6 +63,8 @@ constexpr int kSortWarps = kSortThreads / 32;
 #endif
 constexpr int kSortItems = VKS_SORT_ITEMS;  // keys per thread of a radix block
 constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys per block
+constexpr int kKeyChunk = 32 * kSortItems;             // key slots one warp expands (512)
+constexpr int kChunksPerTile = kSortTile / kKeyChunk;  // 8
 constexpr int kDepthPasses = 4;  // at most (32 significant depth bits in digits of <= 9 bits)
 constexpr int kMaxRadix = 512;    // digits of <= 9 bits
 constexpr int kMaxTilePasses = 3;
@@ -98,7 +100,7 @@ struct Workspace {
     u32* offs;           // its exclusive scan
     u64* rcs;            // [n] tile-rect codes in depth order
     u64* rc_by_id;       // [n] tile-rect codes at the Gaussian id (visible rows)
-    u32* first;          // [key blocks + 2] depth-order Gaussian holding slot 4096 b
+    u32* first;          // [key chunks + 2] depth-order Gaussian holding slot 512 c
     u32* part_sum;       // [scan blocks] block sums of the 1-D scans
     u32* part_vis;       // [scan blocks] visible counts
     // region A (zeroed before the scan)
@@ -133,7 +135,7 @@ Workspace carve(void* base, int64_t n, int64_t capacity, int TX, int TY) {
     w.offs = reinterpret_cast<u32*>(take(4 * kMaxRadix * sort_tiles));
     w.rcs = reinterpret_cast<u64*>(take(8 * nn));
     w.rc_by_id = reinterpret_cast<u64*>(take(8 * nn));
-    w.first = reinterpret_cast<u32*>(take(4 * ((cap + kSortTile - 1) / kSortTile + 2)));
+    w.first = reinterpret_cast<u32*>(take(4 * ((cap + kKeyChunk - 1) / kKeyChunk + 2)));
     w.part_sum = reinterpret_cast<u32*>(take(4 * scan_tiles));
     w.part_vis = reinterpret_cast<u32*>(take(4 * scan_tiles));
     const size_t a0 = off;
@@ -213,7 +215,7 @@ struct CompactOut {
     u64* rc_by_id;           // [n] rect codes (visible rows only)
     u32* dminmax;            // [2] max(~depth bits), max(depth bits) over the visible (zeroed)
     // MODE 1 (depth order): the reduce step gathers the rect codes of the depth-sorted ids into
-    // rc_out (coalesced), the down-sweep writes first[b] = the Gaussian holding key slot 4096 b
+    // rc_out (coalesced), the down-sweep writes first[c] = the Gaussian holding key slot 512 c
     const u32* sid;
     u64* rc_out;
     u32* first;
@@ -398,8 +400,8 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
             out[i] = pre + ex[j];
             if (MODE == 1) {  // key blocks whose first slot lies in this Gaussian's range
                 const u32 a = pre + ex[j], e = a + (u32)v[j];
-                for (u32 b = (a + kSortTile - 1) / kSortTile; b * (u32)kSortTile < e; b++) co.first[b] = (u32)i;
-                if (i == count - 1) co.first[(e + kSortTile - 1) / kSortTile] = (u32)i;  // sentinel: last one
+                for (u32 b = (a + kKeyChunk - 1) / kKeyChunk; b * (u32)kKeyChunk < e; b++) co.first[b] = (u32)i;
+                if (i == count - 1) co.first[(e + kKeyChunk - 1) / kKeyChunk] = (u32)i;  // sentinel: last one
             }
         }
     }
@@ -950,16 +952,17 @@ __global__ void __launch_bounds__(kSortThreads, 5) scatter_kernel(const u32* __r
 // ------------------------------------------------------------------------------------------
 // 4. key generation fused with the first tile pass.  Block b owns the key slots
 // [4096 b, 4096 b + 4096) of the depth-ordered key sequence (slot0[r] + k, rows outer) and expands
-// exactly those keys from the rect codes: the Gaussians covering the range are r0 = first[b] ..
-// first[b+1] (first[] is written by the depth-order scan); each warp expands the 512 slots it
-// later ranks (expand_chunk).  keys_count_kernel only histograms the first tile digit;
+// exactly those keys from the rect codes: the Gaussians covering the range are r0 = first[8 b] ..
+// the one holding slot 4096 (b + 1) (first[c] = the Gaussian holding slot 512 c, written by the
+// depth-order scan); each warp expands the 512 slots it later ranks, starting at first[c0 / 512]
+// (expand_chunk).  keys_count_kernel only histograms the first tile digit;
 // keys_scatter_kernel re-expands the block (cheaper than writing and re-reading M keys) and ranks
 // and stores it like any radix pass.
 struct ExpandSrc {
     const u64* rc;      // [V] rect codes, depth order
     const u32* slot0;   // [V] first slot of each Gaussian's keys
     const u32* sid;     // [V] Gaussian ids, depth order
-    const u32* first;   // [blocks + 1] Gaussian holding slot 4096 b
+    const u32* first;   // [chunks + 1] Gaussian holding slot 512 c (chunks = ceil(M / 512))
     u32 V, M;
     int TX;
     const u64* dtot;    // nullable (vks_bin_sort_async): device totals [M, V]; V / M are then bounds
@@ -993,18 +996,9 @@ __device__ __forceinline__ int div_floor(int k, int w) { return div_floor_r(k, r
 template <class F>
 __device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0, u32 c1, F&& f) {
     const int lane = threadIdx.x & 31;
-    // owner of c0 within [first[b], first[b + 1]]
-    u32 lo = __ldg(src.first + b), hi = __ldg(src.first + b + 1);
-    while (lo < hi) {
-        const u32 step = (hi - lo + 32) / 32;  // probes lo, lo + step, ... cover [lo, hi]
-        const u32 p = lo + (u32)lane * step;
-        const bool le = p <= hi && __ldg(src.slot0 + p) <= c0;
-        const int L = 31 - __clz(__ballot_sync(VKS_FULL_MASK, le));  // lane 0 always true
-        const u32 nlo = lo + (u32)L * step;
-        hi = min(hi, nlo + step - 1);
-        lo = nlo;
-        if (step == 1) break;
-    }
+    // owner of c0 (a multiple of 512): written by the depth-order scan, no search
+    (void)b;
+    const u32 lo = __ldg(src.first + c0 / kKeyChunk);
     const u32 ltle = 0xFFFFFFFFu >> (31 - lane);  // bits 0..lane
     u32 g = lo;  // first Gaussian of the current group
     u32 a_n = 0xFFFFFFFFu, id_n = 0;
@@ -1087,7 +1081,9 @@ __global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSr
     const u32 b = blockIdx.x;
     const u32 S = b * (u32)kSortTile;
     const u32 E = min(S + (u32)kSortTile, src.M);
-    const u32 r0 = __ldg(src.first + b), r1 = __ldg(src.first + b + 1);
+    // the Gaussians holding the block's first slot and slot E (its chunk, or the sentinel)
+    const u32 r0 = __ldg(src.first + b * kChunksPerTile);
+    const u32 r1 = __ldg(src.first + (E - 1) / kKeyChunk + 1);
     int all = 0;
     for (u32 r = r0 + tid; r <= r1; r += kSortThreads) {
         int x0, x1, y0, y1;

@@ -585,20 +585,22 @@ __global__ void __launch_bounds__(kThreads) project_fwd_batch_kernel(const Batch
         q = __ldg(p.quats + i);
         o = __ldg(p.ologit + i);
     }
+    // SH rows of the warp's Gaussians staged once for all views, issued with the parameter loads
+    // (every row in range, not only those gauss_core keeps: one DRAM round trip instead of two
+    // dependent ones; a dropped Gaussian's row is never read)
+    const unsigned gmask = __ballot_sync(VKS_FULL_MASK, valid);
+    float* buf = nullptr;
+    if constexpr (KS > 0) {
+        buf = smem + warp * ShLayout<KS>::kWarpFloats;
+        if (gmask) sh_stage_async<KS>(p.sh, g0, gmask, buf);
+        cp_async_commit();
+    }
     GCore G;
     gauss_core(p.cfg, ls, q, o, G);
     G.ok = G.ok && valid;
     if (valid) p.opac[i] = G.ok ? G.rho : 0.0f;
-    // SH rows of every Gaussian that some view may show, staged once
-    const unsigned gmask = __ballot_sync(VKS_FULL_MASK, G.ok);
-    float* buf = nullptr;
     if constexpr (KS > 0) {
-        buf = smem + warp * ShLayout<KS>::kWarpFloats;
-        if (gmask) {
-            sh_stage_async<KS>(p.sh, g0, gmask, buf);
-            cp_async_commit();
-            cp_async_wait_all();
-        }
+        cp_async_wait_all();
         __syncwarp();
     }
     const int TX = tiles_x(p.v[0].cam), TY = tiles_y(p.v[0].cam);

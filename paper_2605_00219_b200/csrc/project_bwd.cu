@@ -527,6 +527,26 @@ __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const Batch
     const int warp = threadIdx.x >> 5;
     const int64_t g0 = i - lane;
     const bool valid = i < p.n;
+    // the SH rows (staged once) and the parameters are requested with the radii, for every row in
+    // range (nearly every Gaussian is seen by some view of a batch): one DRAM round trip instead
+    // of radii -> visibility -> parameters
+    const unsigned vmask = __ballot_sync(VKS_FULL_MASK, valid);
+    float* shv = nullptr;
+    if constexpr (KS > 0) {
+        shv = smem + warp * 2 * ShLayout<KS>::kWarpFloats;
+        if (vmask) stage_in_async<KS>(p.sh, g0, vmask, shv);
+    }
+    float mu[3] = {0, 0, 0}, ls[3] = {0, 0, 0}, o = 0.0f;
+    float4 q = make_float4(1, 0, 0, 0);
+    if (valid) {
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            mu[c] = __ldg(p.means + 3 * i + c);
+            ls[c] = __ldg(p.ls + 3 * i + c);
+        }
+        q = __ldg(p.quats + i);
+        o = __ldg(p.ologit + i);
+    }
     // visibility in each view (radii != 0)
     unsigned vis = 0;
     if (valid) {
@@ -539,13 +559,10 @@ __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const Batch
     const unsigned amask = __ballot_sync(VKS_FULL_MASK, act);
     const int K = KFULL ? KS : (p.cfg.sh_degree + 1) * (p.cfg.sh_degree + 1);  // KFULL: compile-time
     const int S = 3 * p.cfg.sh_coeffs;
-    // shared memory per warp: the SH rows (staged once) and the dSH accumulator rows
-    float* shv = nullptr;
+    // shared memory per warp: the SH rows and the dSH accumulator rows
     float* acc = nullptr;
     if constexpr (KS > 0) {
-        shv = smem + warp * 2 * ShLayout<KS>::kWarpFloats;
         float* accw = shv + ShLayout<KS>::kWarpFloats;
-        if (amask) stage_in_async<KS>(p.sh, g0, amask, shv);
         acc = accw + lane * ShLayout<KS>::SP;
 #pragma unroll
         for (int j = 0; j < 3 * KS; j++) acc[j] = 0.0f;
@@ -554,17 +571,6 @@ __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const Batch
     }
     float dmu[3] = {0, 0, 0}, dsv[3] = {0, 0, 0}, dqr[4] = {0, 0, 0, 0}, drho = 0.0f;
     if (amask) {
-        float mu[3] = {0, 0, 0}, ls[3] = {0, 0, 0}, o = 0.0f;
-        float4 q = make_float4(1, 0, 0, 0);
-        if (act) {
-#pragma unroll
-            for (int c = 0; c < 3; c++) {
-                mu[c] = __ldg(p.means + 3 * i + c);
-                ls[c] = __ldg(p.ls + 3 * i + c);
-            }
-            q = __ldg(p.quats + i);
-            o = __ldg(p.ologit + i);
-        }
         // view-independent part of the chain
         const float qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
         const float iqn = 1.0f / qn;

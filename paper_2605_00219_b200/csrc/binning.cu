@@ -987,8 +987,8 @@ __device__ __forceinline__ int div_floor_r(int k, float r) { return (int)(((floa
 __device__ __forceinline__ int div_floor(int k, int w) { return div_floor_r(k, rcp_width(w)); }
 
 // f(slot, tile, id) for every key slot in [c0, c1) (c1 - c0 <= 512, all inside block b), one
-// slot per lane per round of 32.  The Gaussian owning slot s is the last one with slot0 <= s.  A
-// 32-ary search finds the owner of c0; from there the warp takes the chunk's Gaussians in groups
+// slot per lane per round of 32.  The Gaussian owning slot s is the last one with slot0 <= s; the
+// owner of c0 (a multiple of 512) is first[c0 / 512]; from there the warp takes the chunk's Gaussians in groups
 // of 32 (lane j = one Gaussian, its record loaded one group ahead).  Within a group the keys are
 // contiguous slots; per round the lanes whose first key falls in the 32-slot window set one bit
 // each of an OR-reduced word, and a lane's owner is the last owner before the window plus the

@@ -788,6 +788,9 @@ __global__ void __launch_bounds__(kScanThreads) scan_u32_kernel(const u32* __res
     }
 }
 
+#ifndef VKS_SCATTER_MINB
+#define VKS_SCATTER_MINB 5  // resident blocks per SM of the scatter kernels (48 registers; 4: 64 registers,
+#endif                      // 756 vs 757.5 views/s; 6: 40 registers with spills, 713)
 template <int RADIX>
 struct SortSmem {
     alignas(128) u32 keys[kSortTile];  // input staging (bulk copy), then the reordered tile
@@ -902,7 +905,7 @@ __device__ __forceinline__ void rank_and_store(SortSmem<1 << DBITS>& S, u32 n, i
 }
 
 template <int DBITS, int MODE>
-__global__ void __launch_bounds__(kSortThreads, 5) scatter_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
+__global__ void __launch_bounds__(kSortThreads, VKS_SCATTER_MINB) scatter_kernel(const u32* __restrict__ kin, const u32* __restrict__ vin,
                                                              u32* __restrict__ kout, u32* __restrict__ vout, u32 n,
                                                              int shift, u32 kbias, u32 T, const u32* __restrict__ offs,
                                                              const float* __restrict__ depths,
@@ -1136,7 +1139,7 @@ __global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSr
 }
 
 template <int DBITS, int MODE>
-__global__ void __launch_bounds__(kSortThreads, 5) keys_scatter_kernel(const ExpandSrc src_in, int shift, u32 T,
+__global__ void __launch_bounds__(kSortThreads, VKS_SCATTER_MINB) keys_scatter_kernel(const ExpandSrc src_in, int shift, u32 T,
                                                                    const u32* __restrict__ offs, u32* __restrict__ kout,
                                                                    u32* __restrict__ vout, const float* __restrict__ depths,
                                                                    u64* __restrict__ keys64) {

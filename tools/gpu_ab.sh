@@ -1,11 +1,10 @@
-python -m pytest tests/test_gpu_parity.py -x -q -k "records or tiny or mcmc or bicycle or culling or ragged" 2>&1 | tail -1
-for v in default nopairs pairsb10; do
+for v in default sm4 sm6; do
   if [ $v = default ]; then unset VKS_LIB_VARIANT; else export VKS_LIB_VARIANT=$v; fi
-  for c in bicycle mcmc stress; do echo "$v $(timeout 600 python tools/time_raster_ab.py $c 0 2>&1 | grep records)"; done
+  echo "$v $(timeout 300 python tools/time_binsort.py bicycle)"
 done
 unset VKS_LIB_VARIANT
-run() { timeout 300 python bench.py --steps 20 --no-e2e --no-cpu-baseline --no-batch1 "$@" 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['stages_ms']['raster_fwd'], d['clocks']['sm_mhz'])"; }
-for v in default nopairs pairsb10 default nopairs; do
+run() { timeout 300 python bench.py --steps 20 --no-e2e --no-cpu-baseline --no-batch1 "$@" 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['stages_ms']['bin_sort'], d['clocks']['sm_mhz'])"; }
+for v in default sm4 sm6 default sm4 sm6; do
   if [ $v = default ]; then unset VKS_LIB_VARIANT; else export VKS_LIB_VARIANT=$v; fi
   echo "bench $v $(run)"
 done

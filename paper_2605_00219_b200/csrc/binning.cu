@@ -73,6 +73,37 @@ constexpr u64 kScanFlagAgg = 1ull << 62;
 constexpr u64 kScanFlagInc = 2ull << 62;
 constexpr u64 kScanMask = (1ull << 62) - 1;
 
+#ifndef VKS_PDL
+#define VKS_PDL 1
+#endif
+// Programmatic dependent launch: every kernel of the binning chain is launched with programmatic
+// stream serialization and waits for its predecessor grid (griddepcontrol.wait; a no-op after a
+// plain launch) before its first global-memory access, so its launch and block scheduling
+// overlap the predecessor's tail instead of following it.
+__device__ __forceinline__ void pdl_wait() {
+#if VKS_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+#if VKS_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);  // errors: the callers' check_launch
+#else
+    kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+#endif
+}
+
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct TilePlan {
@@ -233,6 +264,7 @@ __global__ void __launch_bounds__(kDownThreads) scan_reduce_kernel(const int* __
                                                                   u32* __restrict__ part_sum,
                                                                   u32* __restrict__ part_vis, const CompactOut co,
                                                                   const u64* __restrict__ dcount) {
+    pdl_wait();
     constexpr int ITEMS = kDownItems;
     count = eff_count(count, dcount);
     __shared__ u32 s_sum[kDownThreads / 32], s_vis[kDownThreads / 32];
@@ -341,6 +373,7 @@ __global__ void __launch_bounds__(kDownThreads) scan_down_kernel(const int* __re
                                                                 u64 count, const u32* __restrict__ part_sum,
                                                                 u32* __restrict__ out, const CompactOut co,
                                                                 u64* __restrict__ totals, const u64* __restrict__ dcount) {
+    pdl_wait();
     constexpr int ITEMS = kDownItems;
     count = eff_count(count, dcount);
     __shared__ u32 s_w[kDownThreads / 32], s_v[kDownThreads / 32];
@@ -454,6 +487,7 @@ constexpr size_t kTileCountSmemMax = 200 * 1024;  // bytes
 template <bool SMEM_DIFF>
 __global__ void __launch_bounds__(kDiffThreads) rect_diff_kernel(int TX, int TY, u32 count, const u64* __restrict__ rc,
                                                                 int* __restrict__ diff, const u64* __restrict__ dcount) {
+    pdl_wait();
     extern __shared__ int s_diff[];
     count = (u32)eff_count(count, dcount);
     const int tid = threadIdx.x;
@@ -558,6 +592,7 @@ __global__ void __launch_bounds__(kKeysThreads) keys_debug_kernel(vks_camera cam
 // ------------------------------------------------------------------------------------------
 // 5. per-tile counts -> CSR tile_offsets
 __global__ void iota_kernel(u32* __restrict__ out, u32 n) {
+    pdl_wait();
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = i;
 }
@@ -576,6 +611,7 @@ __device__ __forceinline__ int length_class(u32 len) {
 template <bool SMEM>
 __global__ void __launch_bounds__(1024) tile_count_kernel(int TX, int TY, int* __restrict__ diff,
                                                          u32* __restrict__ tile_offsets, u32* __restrict__ order) {
+    pdl_wait();
     extern __shared__ int s_cells[];
     __shared__ u32 s_wsum[32];
     __shared__ u32 s_carry;
@@ -693,6 +729,7 @@ template <int DBITS>
 __global__ void __launch_bounds__(kSortThreads) digit_count_kernel(const u32* __restrict__ kin, u32 n, int shift,
                                                                   u32 kbias, u32 T, u32* __restrict__ counts,
                                                                   const u64* __restrict__ dcount) {
+    pdl_wait();
     n = (u32)eff_count(n, dcount);
     constexpr int RADIX = 1 << DBITS;
     constexpr u32 DMASK = RADIX - 1;
@@ -727,6 +764,7 @@ __global__ void __launch_bounds__(kSortThreads) digit_count_kernel(const u32* __
 // the tile counts use reduce-then-scan instead, measured: 39 us vs 30 us on 4.15M elements.)
 __global__ void __launch_bounds__(kScanThreads) scan_u32_kernel(const u32* __restrict__ in, u32* __restrict__ out,
                                                                u64 count, u64* __restrict__ lb, u32* __restrict__ ctr) {
+    pdl_wait();
     __shared__ u32 s_tile;
     __shared__ u32 s_warp[kScanThreads / 32];
     __shared__ u64 s_prefix;
@@ -910,6 +948,7 @@ __global__ void __launch_bounds__(kSortThreads, VKS_SCATTER_MINB) scatter_kernel
                                                              int shift, u32 kbias, u32 T, const u32* __restrict__ offs,
                                                              const float* __restrict__ depths,
                                                              u64* __restrict__ keys64, const u64* __restrict__ dcount) {
+    pdl_wait();
     constexpr int RADIX = 1 << DBITS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem<RADIX>& S = *reinterpret_cast<SortSmem<RADIX>*>(smem_raw);
@@ -1067,6 +1106,7 @@ __device__ __forceinline__ void expand_chunk(const ExpandSrc& src, u32 b, u32 c0
 template <int DBITS>
 __global__ void __launch_bounds__(kSortThreads) keys_count_kernel(const ExpandSrc src_in, int shift, u32 T,
                                                                  u32* __restrict__ counts) {
+    pdl_wait();
     constexpr int RADIX = 1 << DBITS;
     constexpr int DMASK = RADIX - 1;
     const ExpandSrc src = src_in.resolved();
@@ -1143,6 +1183,7 @@ __global__ void __launch_bounds__(kSortThreads, VKS_SCATTER_MINB) keys_scatter_k
                                                                    const u32* __restrict__ offs, u32* __restrict__ kout,
                                                                    u32* __restrict__ vout, const float* __restrict__ depths,
                                                                    u64* __restrict__ keys64) {
+    pdl_wait();
     constexpr int RADIX = 1 << DBITS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SortSmem<RADIX>& S = *reinterpret_cast<SortSmem<RADIX>*>(smem_raw);
@@ -1187,10 +1228,10 @@ int launch_pass(const u32* kin, const u32* vin, u32* kout, u32* vout, u32 n, int
         return cuda_fail(e, "scatter smem attribute");
     const u32 T = (u32)((n + kSortTile - 1) / kSortTile);
     if (!T) return VKS_OK;
-    digit_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(kin, n, shift, kbias, T, pb.counts, dcount);
+    launch_k(digit_count_kernel<DBITS>, T, kSortThreads, 0, s, kin, n, shift, kbias, T, pb.counts, dcount);
     const u64 cnt = (u64)(1u << DBITS) * T;
-    scan_u32_kernel<<<(unsigned)((cnt + kCntTile - 1) / kCntTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt, pb.lb, pb.ctr);
-    scatter_kernel<DBITS, MODE><<<T, kSortThreads, sm, s>>>(kin, vin, kout, vout, n, shift, kbias, T, pb.offs, depths,
+    launch_k(scan_u32_kernel, (unsigned)((cnt + kCntTile - 1) / kCntTile), kScanThreads, 0, s, pb.counts, pb.offs, cnt, pb.lb, pb.ctr);
+    launch_k(scatter_kernel<DBITS, MODE>, T, kSortThreads, sm, s, kin, vin, kout, vout, n, shift, kbias, T, pb.offs, depths,
                                                             keys64, dcount);
     return check_launch(__func__);
 }
@@ -1244,11 +1285,11 @@ int launch_keys_pass(const ExpandSrc& src, u32* kout, u32* vout, const PassBufs&
         return cuda_fail(e, "keys_scatter smem attribute");
     const u32 T = (src.M + kSortTile - 1) / kSortTile;
     if (!T) return VKS_OK;
-    keys_count_kernel<DBITS><<<T, kSortThreads, 0, s>>>(src, 0, T, pb.counts);
+    launch_k(keys_count_kernel<DBITS>, T, kSortThreads, 0, s, src, 0, T, pb.counts);
     const u64 cnt = (u64)(1u << DBITS) * T;
-    scan_u32_kernel<<<(unsigned)((cnt + kCntTile - 1) / kCntTile), kScanThreads, 0, s>>>(pb.counts, pb.offs, cnt,
+    launch_k(scan_u32_kernel, (unsigned)((cnt + kCntTile - 1) / kCntTile), kScanThreads, 0, s, pb.counts, pb.offs, cnt,
                                                                                      pb.lb, pb.ctr);
-    keys_scatter_kernel<DBITS, MODE><<<T, kSortThreads, sm, s>>>(src, 0, T, pb.offs, kout, vout, depths, keys64);
+    launch_k(keys_scatter_kernel<DBITS, MODE>, T, kSortThreads, sm, s, src, 0, T, pb.offs, kout, vout, depths, keys64);
     return check_launch(__func__);
 }
 
@@ -1280,10 +1321,10 @@ int launch_rect_diff(int TX, int TY, u32 count, const u64* rc, int* diff, cudaSt
                 return cuda_fail(e, "rect_diff smem attribute");
         }
         const unsigned blocks = std::min<u32>(want, (u32)sm_count() * 2);
-        rect_diff_kernel<true><<<blocks, kDiffThreads, sm, s>>>(TX, TY, count, rc, diff, dcount);
+        launch_k(rect_diff_kernel<true>, blocks, kDiffThreads, sm, s, TX, TY, count, rc, diff, dcount);
     } else {
         const unsigned blocks = std::min<u32>(want, (u32)sm_count() * 4);
-        rect_diff_kernel<false><<<blocks, kDiffThreads, 0, s>>>(TX, TY, count, rc, diff, dcount);
+        launch_k(rect_diff_kernel<false>, blocks, kDiffThreads, 0, s, TX, TY, count, rc, diff, dcount);
     }
     return check_launch(__func__);
 }
@@ -1296,9 +1337,9 @@ int launch_tile_count(int TX, int TY, int* diff, u32* tile_offsets, u32* order, 
                                                      (int)kTileCountSmemMax))
                 return cuda_fail(e, "tile_count smem attribute");
         }
-        tile_count_kernel<true><<<1, 1024, cells_bytes, s>>>(TX, TY, diff, tile_offsets, order);
+        launch_k(tile_count_kernel<true>, 1, 1024, cells_bytes, s, TX, TY, diff, tile_offsets, order);
     } else {
-        tile_count_kernel<false><<<1, 1024, 0, s>>>(TX, TY, diff, tile_offsets, order);
+        launch_k(tile_count_kernel<false>, 1, 1024, 0, s, TX, TY, diff, tile_offsets, order);
     }
     return check_launch(__func__);
 }
@@ -1320,10 +1361,10 @@ int run_scan(const int* tiles, const u64* rc_in, u64 count, u32* part_sum, u32* 
              CompactOut co, cudaStream_t s, const u64* dcount = nullptr) {
     const u32 P = (u32)((count + kScanTile - 1) / kScanTile);
     if (!P) return VKS_OK;
-    scan_reduce_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, MODE == 0 ? part_vis : nullptr,
+    launch_k(scan_reduce_kernel<MODE>, P, kDownThreads, 0, s, tiles, rc_in, count, part_sum, MODE == 0 ? part_vis : nullptr,
                                                        co, dcount);
     co.vis_prefix = part_vis;  // raw block visible counts; the down-sweep sums its predecessors'
-    scan_down_kernel<MODE><<<P, kDownThreads, 0, s>>>(tiles, rc_in, count, part_sum, out, co, totals, dcount);
+    launch_k(scan_down_kernel<MODE>, P, kDownThreads, 0, s, tiles, rc_in, count, part_sum, out, co, totals, dcount);
     return check_launch(__func__);
 }
 
@@ -1333,6 +1374,7 @@ int run_scan(const int* tiles, const u64* rc_in, u64 count, u32* part_sum, u32* 
 __global__ void bin_sort_status_kernel(const u64* __restrict__ totals, int64_t capacity, int n_tiles,
                                        u32* __restrict__ tile_offsets, int64_t* __restrict__ num_isects,
                                        int32_t* __restrict__ status) {
+    pdl_wait();
     const u64 M = totals[0];
     const int st = M >= (1ull << 30) ? VKS_ERR_UNSUPPORTED : ((int64_t)M > capacity ? VKS_ERR_CAPACITY : VKS_OK);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1387,7 +1429,7 @@ int run_bin_sort(const vks_camera& cam, int64_t n, const float* means2d, const i
     if (M == 0) {
         if (cudaMemsetAsync(tile_offsets, 0, sizeof(u32) * (n_tiles + 1), s) != cudaSuccess) return VKS_ERR_CUDA;
         if (tile_order) {  // every list is empty: identity schedule
-            iota_kernel<<<(n_tiles + 255) / 256, 256, 0, s>>>(tile_order, (u32)n_tiles);
+            launch_k(iota_kernel, (n_tiles + 255) / 256, 256, 0, s, tile_order, (u32)n_tiles);
             if (int e_ = check_launch("tile_order")) return e_;
         }
         return VKS_OK;
@@ -1531,7 +1573,7 @@ int run_bin_sort_async(const vks_camera& cam, int64_t n, const float* means2d, c
     } else {
         if ((st = launch_tile_count(TX, TY, w.diff, tile_offsets, tile_order, s))) return st;  // empty lists
     }
-    bin_sort_status_kernel<<<(n_tiles + 1 + 1023) / 1024, 1024, 0, s>>>(w.totals, capacity, n_tiles, tile_offsets,
+    launch_k(bin_sort_status_kernel, (n_tiles + 1 + 1023) / 1024, 1024, 0, s, w.totals, capacity, n_tiles, tile_offsets,
                                                                         num_isects, status);
     return check_launch("bin_sort_status");
 }

@@ -73,37 +73,6 @@ constexpr u64 kScanFlagAgg = 1ull << 62;
 constexpr u64 kScanFlagInc = 2ull << 62;
 constexpr u64 kScanMask = (1ull << 62) - 1;
 
-#ifndef VKS_PDL
-#define VKS_PDL 1
-#endif
-// Programmatic dependent launch: every kernel of the binning chain is launched with programmatic
-// stream serialization and waits for its predecessor grid (griddepcontrol.wait; a no-op after a
-// plain launch) before its first global-memory access, so its launch and block scheduling
-// overlap the predecessor's tail instead of following it.
-__device__ __forceinline__ void pdl_wait() {
-#if VKS_PDL
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-}
-template <typename... KArgs, typename... Args>
-void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
-#if VKS_PDL
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);  // errors: the callers' check_launch
-#else
-    kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
-#endif
-}
-
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct TilePlan {

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kLossThreads, 2) ssim_fused_kernel(int W, int 
                                                                     const float* __restrict__ target, const Gauss w,
                                                                     double* __restrict__ part,
                                                                     double* __restrict__ s_part) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char loss_smem[];
     FusedSmem& S = *reinterpret_cast<FusedSmem*>(loss_smem);
     const int tid = threadIdx.x, c = blockIdx.z;
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(kCombThreads) loss_combine_kernel(int W, int H
                                                           const float* __restrict__ target,
                                                           const double* __restrict__ part, int gx, int gy,
                                                           float* __restrict__ dL, double* __restrict__ l1_part) {
+    pdl_wait();
     __shared__ double red[kCombThreads / 32];
     const int tid = threadIdx.x;
     const int Wv = W - 2 * kR, Hv = H - 2 * kR;
@@ -320,6 +322,7 @@ __global__ void __launch_bounds__(kCombThreads) loss_combine_kernel(int W, int H
 __global__ void __launch_bounds__(kLossThreads) loss_finalize_kernel(int W, int H, float lambda, const double* __restrict__ s_part,
                                                                     int ns, const double* __restrict__ l1_part, int nl,
                                                                     float* __restrict__ loss) {
+    pdl_wait();
     __shared__ double red[2][kLossThreads / 32];
     const int tid = threadIdx.x;
     double s = 0.0, l = 0.0;
@@ -384,17 +387,17 @@ int launch_loss_grad(int W, int H, float lambda, const float* render, const floa
         return cuda_fail(cudaGetLastError(), "loss smem attribute");
     if (ssim) {
         const dim3 g(ws.gx, ws.gy, 3);
-        ssim_fused_kernel<<<g, kLossThreads, sizeof(FusedSmem), s>>>(W, H, render, target, w, ws.part, ws.s_part);
+        launch_k(ssim_fused_kernel, g, kLossThreads, sizeof(FusedSmem), s, W, H, render, target, w, ws.part, ws.s_part);
         ns = (int)(g.x * g.y * g.z);
         if (int e = LaunchCheck::check()) return e;
     }
     if (ws.nl > 0) {
-        loss_combine_kernel<<<dim3(ws.ncx, ws.ncy), kCombThreads, 0, s>>>(W, H, lambda, render, target, ws.part, ws.gx, ws.gy, dL,
+        launch_k(loss_combine_kernel, dim3(ws.ncx, ws.ncy), kCombThreads, 0, s, W, H, lambda, render, target, ws.part, ws.gx, ws.gy, dL,
                                                   ws.l1_part);
         if (int e = LaunchCheck::check()) return e;
     }
     if (loss) {
-        loss_finalize_kernel<<<1, kLossThreads, 0, s>>>(W, H, lambda, ws.s_part, ns, ws.l1_part, ws.nl, loss);
+        launch_k(loss_finalize_kernel, 1, kLossThreads, 0, s, W, H, lambda, ws.s_part, ns, ws.l1_part, ws.nl, loss);
         return LaunchCheck::check();
     }
     return VKS_OK;

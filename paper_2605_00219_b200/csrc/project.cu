@@ -296,6 +296,7 @@ __device__ __forceinline__ void sh_stage_async(const float* __restrict__ src, in
 // forward: KS = compile-time stored SH coefficients (1,4,9,16) or 0 = generic (runtime stride)
 template <int KS>
 __global__ void __launch_bounds__(kThreads) project_fwd_kernel(const Params p) {
+    pdl_wait();
     extern __shared__ float smem[];
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const unsigned lane = lane_id();
@@ -567,6 +568,7 @@ __device__ __forceinline__ bool footprint_rect_g(const Core& k, float kk, const 
 
 template <int KS>
 __global__ void __launch_bounds__(kThreads) project_fwd_batch_kernel(const BatchFwdParams p) {
+    pdl_wait();
     extern __shared__ float smem[];
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const unsigned lane = lane_id();
@@ -710,7 +712,7 @@ int launch_fwd_batch_t(const BatchFwdParams& p, cudaStream_t s) {
         if (e != cudaSuccess) return VKS_ERR_CUDA;
     }
     const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
-    project_fwd_batch_kernel<KS><<<blocks, kThreads, sm, s>>>(p);
+    launch_k(project_fwd_batch_kernel<KS>, blocks, kThreads, sm, s, p);
     return LaunchCheck::check();
 }
 
@@ -728,7 +730,7 @@ int launch_fwd_t(const Params& p, cudaStream_t s) {
         if (e != cudaSuccess) return VKS_ERR_CUDA;
     }
     const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
-    project_fwd_kernel<KS><<<blocks, kThreads, sm, s>>>(p);
+    launch_k(project_fwd_kernel<KS>, blocks, kThreads, sm, s, p);
     return LaunchCheck::check();
 }
 

@@ -215,6 +215,7 @@ __device__ __forceinline__ void sh_basis_and_grad(float x, float y, float z, int
 
 template <int KS, bool OVERWRITE>
 __global__ void __launch_bounds__(kThreads) project_bwd_kernel(const Params p) {
+    pdl_wait();
     extern __shared__ float smem[];
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const unsigned lane = lane_id();
@@ -521,6 +522,7 @@ __device__ __forceinline__ void load_view(const ViewIn& V, int64_t i, bool on, V
 
 template <int KS, bool OVERWRITE, bool KFULL>
 __global__ void __launch_bounds__(kThreads) project_bwd_batch_kernel(const BatchParams p) {
+    pdl_wait();
     extern __shared__ float smem[];
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     const unsigned lane = lane_id();
@@ -809,7 +811,7 @@ int launch_batch_t(const BatchParams& p, cudaStream_t s) {
             cudaSuccess)
         return VKS_ERR_CUDA;
     const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
-    project_bwd_batch_kernel<KS, OW, KF><<<blocks, kThreads, sm, s>>>(p);
+    launch_k(project_bwd_batch_kernel<KS, OW, KF>, blocks, kThreads, sm, s, p);
     return LaunchCheck::check();
 }
 
@@ -829,12 +831,12 @@ int launch_t(const Params& p, cudaStream_t s) {
         cudaFuncSetAttribute(project_bwd_kernel<KS, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
         return VKS_ERR_CUDA;
     const unsigned blocks = (unsigned)((p.n + kThreads - 1) / kThreads);
-    project_bwd_kernel<KS, OW><<<blocks, kThreads, sm, s>>>(p);
+    launch_k(project_bwd_kernel<KS, OW>, blocks, kThreads, sm, s, p);
     return LaunchCheck::check();
 }
 
 template <int KS>
-int launch_k(const Params& p, cudaStream_t s) {
+int launch_bwd_k(const Params& p, cudaStream_t s) {
     return (p.cfg.flags & VKS_FLAG_GRAD_OVERWRITE) ? launch_t<KS, true>(p, s) : launch_t<KS, false>(p, s);
 }
 
@@ -858,11 +860,11 @@ int launch_project_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, 
     p.dquats = reinterpret_cast<float4*>(dquats); p.dologit = dopacity_logits; p.dsh = dsh;
     const bool al = aligned16(sh) && aligned16(dsh);
     switch (cfg.sh_coeffs) {
-        case 16: return al ? launch_k<16>(p, s) : launch_k<0>(p, s);
-        case 9: return launch_k<9>(p, s);
-        case 4: return al ? launch_k<4>(p, s) : launch_k<0>(p, s);
-        case 1: return launch_k<1>(p, s);
-        default: return launch_k<0>(p, s);
+        case 16: return al ? launch_bwd_k<16>(p, s) : launch_bwd_k<0>(p, s);
+        case 9: return launch_bwd_k<9>(p, s);
+        case 4: return al ? launch_bwd_k<4>(p, s) : launch_bwd_k<0>(p, s);
+        case 1: return launch_bwd_k<1>(p, s);
+        default: return launch_bwd_k<0>(p, s);
     }
 }
 

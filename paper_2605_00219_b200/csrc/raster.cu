@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_FWD_MINB * PPT
                                                                  float* __restrict__ image, float* __restrict__ T_final,
                                                                  int* __restrict__ n_contrib,
                                                                  uint32_t n, unsigned long long* __restrict__ stats = nullptr) {
+    pdl_wait();
     __shared__ StageT<REC> stage[8 / PPT];
     unsigned long long n_eval = 0, n_comp = 0, n_went = 0, n_wcomp = 0;
     const int TX = tiles_x(cam);
@@ -502,6 +503,7 @@ __global__ void __launch_bounds__(32 * 8 / PPT, REC ? (VKS_RASTER_BWD_MINB * PPT
                                                                  float* __restrict__ dmeans2d, float* __restrict__ dconics,
                                                                  float* __restrict__ dcolors, float* __restrict__ dopac,
                                                                  int sparse_lanes, uint32_t n) {
+    pdl_wait();
     __shared__ StageT<REC> stage[8 / PPT];
     const int TX = tiles_x(cam);
     const int tile = tile_order ? (int)__ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
@@ -734,10 +736,10 @@ int launch_fwd(const vks_config& cfg, const vks_camera& cam, const float* means2
                const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order, float* image,
                float* T_final, int32_t* n_contrib, uint32_t n, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_fwd_kernel<PPT, CULL, false, REC><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
+    launch_k(raster_fwd_kernel<PPT, CULL, false, REC>, n_tiles, 32 * 8 / PPT, 0, st,
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
         reinterpret_cast<const int2*>(radii), reinterpret_cast<const float4*>(records), vals, tile_offsets, tile_order,
-        image, T_final, n_contrib, n);
+        image, T_final, n_contrib, n, nullptr);
     return LaunchCheck::check();
 }
 
@@ -748,7 +750,7 @@ int launch_bwd(const vks_config& cfg, const vks_camera& cam, const float* means2
                const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d, float* dconics, float* dcolors,
                float* dopacities, int sparse_lanes, uint32_t n, cudaStream_t st) {
     const int n_tiles = tiles_x(cam) * tiles_y(cam);
-    raster_bwd_kernel<PPT, CULL, SPARSE, REC><<<n_tiles, 32 * 8 / PPT, 0, st>>>(
+    launch_k(raster_bwd_kernel<PPT, CULL, SPARSE, REC>, n_tiles, 32 * 8 / PPT, 0, st,
         cfg, cam, reinterpret_cast<const float2*>(means2d), conics, colors, opacities,
         reinterpret_cast<const int2*>(radii), reinterpret_cast<const float4*>(records), vals, tile_offsets, tile_order,
         T_final, n_contrib, dL_dimage, dmeans2d, dconics, dcolors, dopacities, sparse_lanes, n);

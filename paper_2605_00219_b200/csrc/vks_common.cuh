@@ -1,6 +1,7 @@
 // vks_common.cuh — shared device helpers of the CUDA path (never shared with oracle/).
 #pragma once
 #include <cuda_runtime.h>
+#include <utility>
 #include <stdint.h>
 #include <stdio.h>
 
@@ -201,4 +202,35 @@ int launch_raster_bwd(const vks_config& cfg, const vks_camera& cam, int64_t n, c
                       const float* records, const uint32_t* vals, const uint32_t* tile_offsets, const uint32_t* tile_order,
                       const float* T_final, const int32_t* n_contrib, const float* dL_dimage, float* dmeans2d,
                       float* dconics, float* dcolors, float* dopacities, cudaStream_t s);
+#ifndef VKS_PDL
+#define VKS_PDL 1
+#endif
+// Programmatic dependent launch: the kernels of the path are launched with programmatic stream
+// serialization and waits for its predecessor grid (griddepcontrol.wait; a no-op after a
+// plain launch) before its first global-memory access, so its launch and block scheduling
+// overlap the predecessor's tail instead of following it.
+__device__ __forceinline__ void pdl_wait() {
+#if VKS_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+#if VKS_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);  // errors: the callers' check_launch
+#else
+    kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+#endif
+}
+
 }  // namespace vks

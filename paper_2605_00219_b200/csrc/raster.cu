@@ -242,7 +242,9 @@ __device__ __forceinline__ PixelMap<PPT> pixel_map(int tile, int TX) {
 // minimum resident blocks per SM of the records kernels at 2 pixels per thread (scaled with the
 // block size for the other layouts; a register budget; the gather kernels hold more registers and
 // stay unconstrained): the forward at 12 (<= 42 registers; measured
-// 0.216 vs 0.224 ms on bicycle), the backward unconstrained (56 registers; 10 blocks measured slower)
+// 0.216 vs 0.224 ms on bicycle), the backward at 7 (63 registers: 0.443 vs 0.461 ms unconstrained at
+// 77 registers / 6 blocks on bicycle, 1.346 vs 1.416 on stress, step 773 vs 761 views/s; 8 blocks at
+// 59 registers 0.477, 10 slower still)
 #ifndef VKS_RASTER_REC_CA
 #define VKS_RASTER_REC_CA true
 #endif
@@ -250,7 +252,7 @@ __device__ __forceinline__ PixelMap<PPT> pixel_map(int tile, int TX) {
 #define VKS_RASTER_FWD_MINB 12
 #endif
 #ifndef VKS_RASTER_BWD_MINB
-#define VKS_RASTER_BWD_MINB 1
+#define VKS_RASTER_BWD_MINB 7
 #endif
 
 template <int PPT, int CULL, bool STATS = false, bool REC = false>

@@ -567,7 +567,12 @@ __device__ __forceinline__ bool footprint_rect_g(const Core& k, float kk, const 
 }
 
 template <int KS>
-__global__ void __launch_bounds__(kThreads) project_fwd_batch_kernel(const BatchFwdParams p) {
+#ifdef VKS_PFWD_MINB  // measurement builds only: a residency target for the batched forward
+#define VKS_PFWD_LB kThreads, VKS_PFWD_MINB
+#else
+#define VKS_PFWD_LB kThreads
+#endif
+__global__ void __launch_bounds__(VKS_PFWD_LB) project_fwd_batch_kernel(const BatchFwdParams p) {
     pdl_wait();
     extern __shared__ float smem[];
     const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
